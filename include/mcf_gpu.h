@@ -1,0 +1,167 @@
+/*
+ * mcf_gpu.h -- C-ABI of the B200 MCF operator library (libmcf_b200.so).
+ *
+ * This is the drop-in boundary for the MCTensor operator layer of the
+ * reference (/root/reference/proj/include/mcfloat).  The reference exposes a
+ * header-only C++20 template API (namespace mcf) over host value types
+ * MCTensor<P> / NdArray; each function below replaces one of those entry
+ * points and is cited as  [replaces <file>:<line>].  include/mcf_gpu.hpp
+ * re-exposes the reference's own signatures on top of this ABI.
+ *
+ * Conventions (all entry points):
+ *  - MC tensors are (numel, nc) arrays with the component index fastest
+ *    (mctensor.hpp:8-9); component storage is IEEE binary16 (uint16 bits),
+ *    binary32 or binary64 according to `prec` (precision.hpp:84-162).  The
+ *    reference stores the same values as exactly representable doubles.
+ *  - Working-precision ("Tensor") operands are plain arrays of the same
+ *    storage type.  `vn` is the operand's element count: 1 (scalar) or any
+ *    count dividing numel for a trailing-suffix broadcast, read as
+ *    v[e % vn] (mc_ops.hpp:14-15, 317-329, 391).
+ *  - Pointers without the mcf_h_ prefix are DEVICE pointers; the call is
+ *    asynchronous on `stream` (NULL = legacy default stream), allocates
+ *    nothing, and is safe from several host threads on distinct streams.
+ *    mcf_h_* entry points take HOST pointers, stage through the library's
+ *    device workspace and return when the result is in host memory.
+ *  - Results are bit-identical to the reference for every elementwise
+ *    operator, every precision and 1 <= nc <= 8, including unordered or
+ *    overlapping components, zeros and non-finite values.  The one
+ *    documented difference: exp uses a correctly rounded binary64 exp where
+ *    the reference calls the host libm ("Exp-MCN").
+ *  - Contractions (dot/mv/mm) are within the reference's own error bound,
+ *    not bitwise (the summation order is the GPU's); nc == 1 is bitwise the
+ *    reference's plain left-to-right fl-MAC chain (linalg.hpp:47-53).
+ *  - Return value: MCF_OK or an error code; mcf_last_error() returns the
+ *    calling thread's last message, worded like the reference's exceptions
+ *    (e.g. "MCTensor ops support 1 <= nc <= 8", mc_ops.hpp:35).
+ */
+#ifndef MCF_GPU_H
+#define MCF_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mcf_stream; /* == cudaStream_t */
+
+typedef enum mcf_status {
+  MCF_OK = 0,
+  MCF_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  MCF_ERR_UNSUPPORTED = 2,      /* mcf::unsupported_operation (linalg.hpp:30-32) */
+  MCF_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
+  MCF_ERR_NO_DEVICE = 4         /* library loaded without a usable B200 */
+} mcf_status;
+
+typedef enum mcf_prec { MCF_B16 = 0, MCF_B32 = 1, MCF_B64 = 2 } mcf_prec; /* precision.hpp:209 */
+
+typedef enum mcf_reduce { /* linalg.hpp:23 */
+  MCF_SEQUENTIAL = 0,
+  MCF_PAIRWISE_TREE = 1
+} mcf_reduce;
+
+/* ---- library ------------------------------------------------------------- */
+int mcf_abi_version(void);
+const char* mcf_last_error(void);
+/* kernels launched by this thread since the last reset (instrumentation) */
+int64_t mcf_launch_count(void);
+void mcf_reset_launch_count(void);
+
+/* ---- error-free transforms, array forms  [replaces eft.hpp:89-111] -------- */
+mcf_status mcf_two_sum(mcf_prec p, const void* a, const void* b, void* s, void* e, int64_t n,
+                       mcf_stream stream);
+mcf_status mcf_two_prod(mcf_prec p, const void* a, const void* b, void* prod, void* e,
+                        int64_t n, mcf_stream stream);
+
+/* ---- renormalization ------------------------------------------------------ */
+/* [replaces mc_ops.hpp:339-348 renormalize] */
+mcf_status mcf_renormalize(mcf_prec p, const void* h, int nc, void* out, int r_nc, int64_t numel,
+                           mcf_stream stream);
+/* [replaces mc_ops.hpp:350-359 simple_renorm] */
+mcf_status mcf_simple_renorm(mcf_prec p, const void* h, int nc, void* out, int r_nc,
+                             int64_t numel, mcf_stream stream);
+/* [replaces mctensor.hpp:56-65 MCTensor::approx]  out: numel values */
+mcf_status mcf_approx(mcf_prec p, const void* x, int nc, void* out, int64_t numel,
+                      mcf_stream stream);
+/* [replaces mc_ops.hpp:376-381 negate] */
+mcf_status mcf_negate(mcf_prec p, const void* x, int nc, void* out, int64_t numel,
+                      mcf_stream stream);
+
+/* ---- elementwise MCF operators ------------------------------------------- */
+/* [replaces mc_ops.hpp:384-394 grow_expn(MCTensor, NdArray)] */
+mcf_status mcf_grow_expn(mcf_prec p, const void* x, int nc, const void* v, int64_t vn,
+                         void* out, int64_t numel, mcf_stream stream);
+/* [replaces mc_ops.hpp:398-410 scaling_n(MCTensor, NdArray, expanded)]
+ * out has nc+1 components when expanded != 0 */
+mcf_status mcf_scaling_n(mcf_prec p, const void* x, int nc, const void* v, int64_t vn,
+                         int expanded, void* out, int64_t numel, mcf_stream stream);
+/* [replaces mc_ops.hpp:494-507 div_n(NdArray, MCTensor)] */
+mcf_status mcf_div_n(mcf_prec p, const void* v, int64_t vn, const void* y, int nc, void* out,
+                     int64_t numel, mcf_stream stream);
+/* binary ops pad mixed nc to max(ncx, ncy) [mc_ops.hpp:414-436]; out has that nc */
+/* [replaces mc_ops.hpp:440-446 add_mcn] */
+mcf_status mcf_add_mcn(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                       int64_t numel, mcf_stream stream);
+/* [replaces mc_ops.hpp:448-454 div_mcn] */
+mcf_status mcf_div_mcn(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                       int64_t numel, mcf_stream stream);
+/* [replaces mc_ops.hpp:456-462 mul_mcn (fast: x / (1/y))] */
+mcf_status mcf_mul_mcn(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                       int64_t numel, mcf_stream stream);
+/* [replaces mc_ops.hpp:464-470 mul_mcn_slow] */
+mcf_status mcf_mul_mcn_slow(mcf_prec p, const void* x, int ncx, const void* y, int ncy,
+                            void* out, int64_t numel, mcf_stream stream);
+/* [replaces mc_ops.hpp:472-480 square_mcn] */
+mcf_status mcf_square_mcn(mcf_prec p, const void* x, int nc, void* out, int64_t numel,
+                          mcf_stream stream);
+/* [replaces mc_ops.hpp:482-490 exp_mcn] */
+mcf_status mcf_exp_mcn(mcf_prec p, const void* x, int nc, void* out, int64_t numel,
+                       mcf_stream stream);
+
+/* ---- contractions, MC x Tensor  [replaces linalg.hpp:38-253] -------------- */
+/* out[b,i,j,:] = sum_k x[b,i,k,:] * w[b',k,j], b' = b if w_batched else 0.
+ * dot_mcn = (batch=1, m=1, n=1), mv_mcn = (n=1), mm_mcn = (batch=1),
+ * bmm_mcn / mm4d_mcn = (w_batched=1), matmul_mcn 3/2 and 4/2 = (w_batched=0).
+ * nc + 1 <= 8 (linalg.hpp:112,128,147,187).  strategy/leaf_arity mirror
+ * ReductionPlan (linalg.hpp:25-28); nc == 1 with MCF_SEQUENTIAL is the plain
+ * working-precision chain, bitwise.  For nc >= 2 the GPU carries an
+ * extended accumulator in registers; results are within the reference's own
+ * relative error (tests/test_gpu_linalg.py states the bound). */
+mcf_status mcf_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t batch,
+                       int64_t m, int64_t k, int64_t n, int w_batched, void* out,
+                       int strategy, int leaf_arity, mcf_stream stream);
+/* [replaces linalg.hpp:159-166 mm_mcn(MCTensor, MCTensor)]: always returns
+ * MCF_ERR_UNSUPPORTED with the reference's message, like the reference. */
+mcf_status mcf_mm_mcn_mcmc_refusal(void);
+/* NEW capability (the reference refuses it): MC x MC products.
+ * out[i,j,:] = sum_k x[i,k,:] * y[k,j,:]; checked against SURVEY 8c recipe B. */
+mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
+                       int64_t n, void* out, mcf_stream stream);
+/* out[b,:] = sum_k x[b,k,:] * y[b,k,:]  (batched MC x MC dots) */
+mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch,
+                        int64_t k, void* out, mcf_stream stream);
+
+/* ---- host-buffer entry points (blocking; the reference's calling model) --- */
+/* op: "grow_expn" "scaling_n" "div_n" "add_mcn" "div_mcn" "mul_mcn"
+ *     "mul_mcn_slow" "square_mcn" "exp_mcn" "negate" "approx".
+ * x/y: MC operands (host), v: working-precision operand (host) or NULL.
+ * Staged through pinned buffers in chunks so H2D, compute and D2H overlap. */
+mcf_status mcf_h_elementwise(const char* op, mcf_prec p, const void* x, int ncx, const void* y,
+                             int ncy, const void* v, int64_t vn, void* out, int64_t numel);
+mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t batch,
+                         int64_t m, int64_t k, int64_t n, int w_batched, void* out);
+mcf_status mcf_h_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
+                         int64_t n, void* out);
+
+/* ---- host input generation (mcf::Rng, rng.hpp:13-65) ----------------------- */
+/* n draws of Rng(seed).uniform() (53-bit, [0,1)), bitwise the reference's */
+void mcf_rng_uniform(uint64_t seed, int64_t n, double* out);
+/* n draws of Rng(seed).normal() (Box-Muller with spare) */
+void mcf_rng_normal(uint64_t seed, int64_t n, double* out);
+/* n draws of Rng(seed).below(bound) */
+void mcf_rng_below(uint64_t seed, uint64_t bound, int64_t n, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCF_GPU_H */

@@ -1,0 +1,650 @@
+// elementwise.cu -- the elementwise MCF operators (mc_ops.hpp) on sm_100a.
+//
+// One thread owns EPT consecutive elements; with binary32 components the
+// (…, nc) layout makes an EPT-element slice a multiple of 16 bytes, so every
+// operand moves with 128-bit streaming loads/stores (ld.global.cs /
+// st.global.cs: each byte is touched once, keep L2 for the next operand).
+// All nc components live in registers; the operator bodies are the
+// register fast paths of mcf_fast.cuh, and any element whose fast-path
+// preconditions fail re-runs the literal restatement (mcf_lit.cuh).
+// Precisions / nc without an instantiated fast path run the literal kernel.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+
+#include "mcf_exp.cuh"
+#include "mcf_fast.cuh"
+#include "mcf_lit.cuh"
+#include "mcf_prec.cuh"
+#include "mcf_runtime.h"
+
+namespace mcfg {
+namespace {
+
+template <class P>
+using RT = typename P::rt;
+template <class P>
+using ST = typename P::st;
+
+constexpr int kThreads = 256;
+
+// ---- vector IO ---------------------------------------------------------------
+
+template <int B>
+struct VecOf;
+template <>
+struct VecOf<16> { using T = uint4; };
+template <>
+struct VecOf<8> { using T = uint2; };
+template <>
+struct VecOf<4> { using T = unsigned int; };
+template <>
+struct VecOf<2> { using T = unsigned short; };
+
+template <class T, int N>
+__device__ __forceinline__ void load_stream(const T* __restrict__ p, T (&d)[N]) {
+  constexpr int B = N * (int)sizeof(T);
+  constexpr int V = (B % 16 == 0) ? 16 : (B % 8 == 0) ? 8 : (B % 4 == 0) ? 4 : 2;
+  using VT = typename VecOf<V>::T;
+  VT tmp[B / V];
+#pragma unroll
+  for (int i = 0; i < B / V; ++i) tmp[i] = __ldcs(reinterpret_cast<const VT*>(p) + i);
+  memcpy(&d[0], &tmp[0], B);
+}
+
+template <class T, int N>
+__device__ __forceinline__ void store_stream(T* __restrict__ p, const T (&d)[N]) {
+  constexpr int B = N * (int)sizeof(T);
+  constexpr int V = (B % 16 == 0) ? 16 : (B % 8 == 0) ? 8 : (B % 4 == 0) ? 4 : 2;
+  using VT = typename VecOf<V>::T;
+  VT tmp[B / V];
+  memcpy(&tmp[0], &d[0], B);
+#pragma unroll
+  for (int i = 0; i < B / V; ++i) __stcs(reinterpret_cast<VT*>(p) + i, tmp[i]);
+}
+
+// elements per thread so that one thread's slice of an nc-component operand
+// is a whole number of 16-byte vectors when possible
+template <class P, int NC>
+constexpr int ept_for() {
+  constexpr int b = (int)sizeof(ST<P>) * NC;
+  return b % 16 == 0 ? 1 : (2 * b) % 16 == 0 ? 2 : (4 * b) % 16 == 0 ? 4 : 8;
+}
+
+// ---- operator table -------------------------------------------------------------
+// Each op supplies the register fast path (compile-time nc) and the literal
+// restatement (runtime nc).  Flags say which operands it reads.
+enum OpId {
+  kGrow, kScale, kScaleX, kDivN, kAdd, kDiv, kMul, kMulSlow, kSquare, kExp, kNeg, kApprox,
+  kRenorm, kSimple
+};
+
+template <int OP>
+struct OpTraits {
+  static constexpr bool kY = OP == kAdd || OP == kDiv || OP == kMul || OP == kMulSlow;
+  static constexpr bool kV = OP == kGrow || OP == kScale || OP == kScaleX || OP == kDivN;
+};
+
+template <int OP, class P, int NC, int ONC>
+__device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[NC], RT<P> v,
+                                         RT<P> (&o)[ONC]) {
+  if constexpr (OP == kGrow) return fast::grow<P, NC>(x, v, o);
+  else if constexpr (OP == kScale || OP == kScaleX) return fast::scale<P, NC, ONC>(x, v, o);
+  else if constexpr (OP == kDivN) {
+    RT<P> num[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) num[i] = i == 0 ? v : RT<P>(0);
+    return fast::div<P, NC>(num, x, o);  // x holds the MC divisor y
+  } else if constexpr (OP == kAdd) return fast::add<P, NC>(x, y, o);
+  else if constexpr (OP == kDiv) return fast::div<P, NC>(x, y, o);
+  else if constexpr (OP == kMul) return fast::mul_fast<P, NC>(x, y, o);
+  else if constexpr (OP == kMulSlow) return fast::mul_slow<P, NC>(x, y, o);
+  else if constexpr (OP == kSquare) return fast::square<P, NC>(x, o);
+  else if constexpr (OP == kExp) return fast::exp<P, NC>(x, o);
+  else if constexpr (OP == kNeg) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) o[i] = -x[i];
+    return true;
+  } else if constexpr (OP == kRenorm) {
+    RT<P> h[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) h[i] = x[i];
+    return fast::renorm<P, NC, ONC>(h, o);
+  } else {
+    return false;
+  }
+}
+
+// literal restatement with runtime component counts (padded operands)
+template <int OP, class P>
+__device__ __noinline__ void run_lit(const RT<P>* x, const RT<P>* y, RT<P> v, RT<P>* o, int nc,
+                                     int onc) {
+  if constexpr (OP == kGrow) lit::grow<P>(x, nc, v, o);
+  else if constexpr (OP == kScale || OP == kScaleX) lit::scale<P>(x, nc, v, o, onc);
+  else if constexpr (OP == kDivN) {
+    RT<P> num[lit::kMaxNc];
+    for (int i = 0; i < nc; ++i) num[i] = i == 0 ? v : RT<P>(0);
+    lit::div<P>(num, x, nc, o);
+  } else if constexpr (OP == kAdd) lit::add<P>(x, nc, y, nc, o, nc);
+  else if constexpr (OP == kDiv) lit::div<P>(x, y, nc, o);
+  else if constexpr (OP == kMul) lit::mul_fast<P>(x, y, nc, o);
+  else if constexpr (OP == kMulSlow) lit::mul_slow<P>(x, y, nc, o);
+  else if constexpr (OP == kSquare) lit::square<P>(x, nc, o);
+  else if constexpr (OP == kExp) lit::exp<P>(x, nc, o);
+  else if constexpr (OP == kNeg) {
+    for (int i = 0; i < nc; ++i) o[i] = -x[i];
+  } else if constexpr (OP == kApprox) {
+    o[0] = lit::approx<P>(x, nc);
+  } else if constexpr (OP == kRenorm) lit::renorm<P>(x, nc, o, onc);
+  else if constexpr (OP == kSimple) lit::simple_renorm<P>(x, nc, o, onc);
+}
+
+// v[e % vn]: vmode 0 = per-element (vn == numel), 1 = scalar, 2 = general suffix
+template <class P>
+__device__ __forceinline__ RT<P> v_at(const ST<P>* v, int64_t vn, int vmode, int64_t e) {
+  if (vmode == 0) return P::ld(v[e]);
+  if (vmode == 1) return P::ld(v[0]);
+  return P::ld(v[e % vn]);
+}
+
+// ---- fast kernel ----------------------------------------------------------------
+
+template <int OP, class P, int NC, int ONC>
+__global__ void __launch_bounds__(kThreads) k_fast(const ST<P>* __restrict__ x,
+                                                   const ST<P>* __restrict__ y,
+                                                   const ST<P>* __restrict__ v, int64_t vn,
+                                                   int vmode, ST<P>* __restrict__ out,
+                                                   int64_t numel) {
+  constexpr int EPT = ept_for<P, NC>();
+  constexpr bool kY = OpTraits<OP>::kY, kV = OpTraits<OP>::kV;
+  struct Frag {
+    ST<P> xs[EPT * NC];
+    ST<P> ys[kY ? EPT * NC : 1];
+    RT<P> vs[kV ? EPT : 1];
+  };
+  // full EPT-element groups, vector IO
+  auto load = [&](Frag& f, int64_t e0) {
+    load_stream<ST<P>, EPT * NC>(x + e0 * NC, f.xs);
+    if constexpr (kY) load_stream<ST<P>, EPT * NC>(y + e0 * NC, f.ys);
+    if constexpr (kV) {
+      if (vmode == 0 && (EPT * sizeof(ST<P>)) % 4 == 0) {
+        ST<P> vv[EPT];
+        load_stream<ST<P>, EPT>(v + e0, vv);
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) f.vs[i] = P::ld(vv[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) f.vs[i] = v_at<P>(v, vn, vmode, e0 + i);
+      }
+    }
+  };
+  auto compute = [&](const Frag& f, ST<P> (&os)[EPT * ONC], int count) {
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      if (i >= count) break;
+      RT<P> xa[NC], ya[NC], oa[ONC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        xa[c] = P::ld(f.xs[i * NC + c]);
+        ya[c] = kY ? P::ld(f.ys[i * NC + c]) : RT<P>(0);
+      }
+      const RT<P> vv = kV ? f.vs[i] : RT<P>(0);
+      if (!run_fast<OP, P, NC, ONC>(xa, ya, vv, oa)) run_lit<OP, P>(xa, ya, vv, oa, NC, ONC);
+#pragma unroll
+      for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
+    }
+  };
+  const int64_t groups = numel / EPT;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // software pipeline: the next group's loads are in flight while this one computes
+  Frag cur;
+  if (g < groups) load(cur, g * EPT);
+  for (; g < groups; g += stride) {
+    Frag nxt;
+    const bool more = g + stride < groups;
+    if (more) load(nxt, (g + stride) * EPT);
+    ST<P> os[EPT * ONC];
+    compute(cur, os, EPT);
+    store_stream<ST<P>, EPT * ONC>(out + g * EPT * ONC, os);
+    if (more) cur = nxt;
+  }
+  // ragged tail (< EPT elements): one thread, scalar IO
+  if (blockIdx.x == 0 && threadIdx.x == 0 && groups * EPT < numel) {
+    const int64_t e0 = groups * EPT;
+    const int cnt = (int)(numel - e0);
+    Frag f;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const bool in = i < cnt;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        f.xs[i * NC + c] = in ? x[(e0 + i) * NC + c] : P::sv(RT<P>(0));
+        if constexpr (kY) f.ys[i * NC + c] = in ? y[(e0 + i) * NC + c] : P::sv(RT<P>(0));
+      }
+      if constexpr (kV) f.vs[i] = in ? v_at<P>(v, vn, vmode, e0 + i) : RT<P>(0);
+    }
+    ST<P> os[EPT * ONC];
+    compute(f, os, cnt);
+    for (int i = 0; i < cnt; ++i)
+#pragma unroll
+      for (int c = 0; c < ONC; ++c) out[(e0 + i) * ONC + c] = os[i * ONC + c];
+  }
+}
+
+// ---- literal kernel (any precision, any nc, mixed-nc padding) ----------------
+
+template <int OP, class P>
+__global__ void __launch_bounds__(kThreads) k_lit(const ST<P>* __restrict__ x, int ncx,
+                                                  const ST<P>* __restrict__ y, int ncy,
+                                                  const ST<P>* __restrict__ v, int64_t vn,
+                                                  int vmode, ST<P>* __restrict__ out, int onc,
+                                                  int64_t numel) {
+  constexpr bool kY = OpTraits<OP>::kY, kV = OpTraits<OP>::kV;
+  const int nc = kY ? (ncx > ncy ? ncx : ncy) : ncx;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < numel; e += stride) {
+    RT<P> xa[lit::kMaxNc], ya[lit::kMaxNc], oa[lit::kMaxNc + 1];
+    for (int c = 0; c < nc; ++c) {
+      xa[c] = c < ncx ? P::ld(x[e * ncx + c]) : RT<P>(0);
+      ya[c] = (kY && c < ncy) ? P::ld(y[e * ncy + c]) : RT<P>(0);
+    }
+    const RT<P> vv = kV ? v_at<P>(v, vn, vmode, e) : RT<P>(0);
+    run_lit<OP, P>(xa, ya, vv, oa, nc, onc);
+    for (int c = 0; c < onc; ++c) out[e * onc + c] = P::sv(oa[c]);
+  }
+}
+
+// ---- EFT array kernels (eft.hpp:89-111) -------------------------------------------
+
+template <class P, bool PROD>
+__global__ void __launch_bounds__(kThreads) k_eft(const ST<P>* __restrict__ a,
+                                                  const ST<P>* __restrict__ b,
+                                                  ST<P>* __restrict__ s, ST<P>* __restrict__ e,
+                                                  int64_t n) {
+  constexpr int EPT = ept_for<P, 1>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g * EPT < n; g += stride) {
+    const int64_t i0 = g * EPT;
+    ST<P> as[EPT], bs[EPT], ss[EPT], es[EPT];
+    const bool full = i0 + EPT <= n;
+    if (full) {
+      load_stream<ST<P>, EPT>(a + i0, as);
+      load_stream<ST<P>, EPT>(b + i0, bs);
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        as[i] = i0 + i < n ? a[i0 + i] : P::sv(RT<P>(0));
+        bs[i] = i0 + i < n ? b[i0 + i] : P::sv(RT<P>(0));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      RT<P> hi, lo;
+      if constexpr (PROD) two_prod<P>(P::ld(as[i]), P::ld(bs[i]), hi, lo);
+      else two_sum<P>(P::ld(as[i]), P::ld(bs[i]), hi, lo);
+      ss[i] = P::sv(hi);
+      es[i] = P::sv(lo);
+    }
+    if (full) {
+      store_stream<ST<P>, EPT>(s + i0, ss);
+      store_stream<ST<P>, EPT>(e + i0, es);
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPT; ++i)
+        if (i0 + i < n) {
+          s[i0 + i] = ss[i];
+          e[i0 + i] = es[i];
+        }
+    }
+  }
+}
+
+// approx: MC -> one working-precision value per element (smallest first)
+template <class P, int NC>
+__global__ void __launch_bounds__(kThreads) k_approx(const ST<P>* __restrict__ x,
+                                                     ST<P>* __restrict__ out, int64_t numel) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < numel; e += stride) {
+    RT<P> acc = P::ld(x[e * NC + NC - 1]);
+#pragma unroll
+    for (int i = NC - 2; i >= 0; --i) acc = P::add(acc, P::ld(x[e * NC + i]));
+    out[e] = P::sv(acc);
+  }
+}
+
+// ---- host launch helpers -----------------------------------------------------
+
+template <class K>
+int per_sm(K kernel) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, 0) != cudaSuccess || n < 1) n = 1;
+  return n;
+}
+
+struct Args {
+  const void* x;
+  int ncx;
+  const void* y;
+  int ncy;
+  const void* v;
+  int64_t vn;
+  void* out;
+  int onc;
+  int64_t numel;
+  cudaStream_t stream;
+};
+
+int vmode_of(int64_t vn, int64_t numel) { return vn == numel ? 0 : (vn == 1 ? 1 : 2); }
+
+template <int OP, class P, int NC, int ONC>
+mcf_status launch_fast(const Args& a) {
+  auto k = k_fast<OP, P, NC, ONC>;
+  static const int occ = per_sm(k);
+  constexpr int EPT = ept_for<P, NC>();
+  const int grid = mcfr::grid_for((a.numel + EPT - 1) / EPT, kThreads, occ);
+  k<<<grid, kThreads, 0, a.stream>>>(static_cast<const ST<P>*>(a.x), static_cast<const ST<P>*>(a.y),
+                                      static_cast<const ST<P>*>(a.v), a.vn, vmode_of(a.vn, a.numel),
+                                      static_cast<ST<P>*>(a.out), a.numel);
+  mcfr::note_launch();
+  return mcfr::check_launch("mcf elementwise kernel");
+}
+
+template <int OP, class P>
+mcf_status launch_lit(const Args& a) {
+  auto k = k_lit<OP, P>;
+  static const int occ = per_sm(k);
+  const int grid = mcfr::grid_for(a.numel, kThreads, occ);
+  k<<<grid, kThreads, 0, a.stream>>>(static_cast<const ST<P>*>(a.x), a.ncx,
+                                      static_cast<const ST<P>*>(a.y), a.ncy,
+                                      static_cast<const ST<P>*>(a.v), a.vn, vmode_of(a.vn, a.numel),
+                                      static_cast<ST<P>*>(a.out), a.onc, a.numel);
+  mcfr::note_launch();
+  return mcfr::check_launch("mcf elementwise kernel (literal)");
+}
+
+// fast paths exist for binary32 with nc 1..4 and equal operand nc
+template <int OP, class P>
+mcf_status dispatch(const Args& a) {
+  if (a.numel == 0) return MCF_OK;
+  if constexpr (std::is_same<P, PB32>::value) {
+    if constexpr (OP == kRenorm) {
+      if (a.ncx == a.onc) {
+        switch (a.ncx) {
+          case 2: return launch_fast<kRenorm, P, 2, 2>(a);
+          case 3: return launch_fast<kRenorm, P, 3, 3>(a);
+          case 4: return launch_fast<kRenorm, P, 4, 4>(a);
+          default: break;
+        }
+      } else if (a.ncx == a.onc + 1) {
+        switch (a.onc) {
+          case 2: return launch_fast<kRenorm, P, 3, 2>(a);
+          case 3: return launch_fast<kRenorm, P, 4, 3>(a);
+          default: break;
+        }
+      }
+    } else if constexpr (OP == kScaleX) {
+      switch (a.ncx) {
+        case 1: return launch_fast<OP, P, 1, 2>(a);
+        case 2: return launch_fast<OP, P, 2, 3>(a);
+        case 3: return launch_fast<OP, P, 3, 4>(a);
+        default: break;
+      }
+    } else if constexpr (OP != kApprox && OP != kSimple) {
+      const bool same_nc = !OpTraits<OP>::kY || a.ncx == a.ncy;
+      if (same_nc) {
+        switch (a.ncx) {
+          case 1: return launch_fast<OP, P, 1, 1>(a);
+          case 2: return launch_fast<OP, P, 2, 2>(a);
+          case 3: return launch_fast<OP, P, 3, 3>(a);
+          case 4:
+            if constexpr (OP != kMulSlow && OP != kSquare) return launch_fast<OP, P, 4, 4>(a);
+            break;
+          default: break;
+        }
+      }
+    }
+  }
+  return launch_lit<OP, P>(a);
+}
+
+template <int OP>
+mcf_status dispatch_prec(mcf_prec p, const Args& a) {
+  const mcf_status ready = mcfr::ensure_device_tables();
+  if (ready != MCF_OK) return ready;
+  switch (p) {
+    case MCF_B16: return dispatch<OP, PB16>(a);
+    case MCF_B32: return dispatch<OP, PB32>(a);
+    case MCF_B64: return dispatch<OP, PB64>(a);
+  }
+  return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "unknown precision");
+}
+
+mcf_status approx_dispatch(mcf_prec p, const void* x, int nc, void* out, int64_t numel,
+                           cudaStream_t s) {
+  if (numel == 0) return MCF_OK;
+  auto go = [&](auto tag, auto nct) -> mcf_status {
+    using P = decltype(tag);
+    constexpr int NC = decltype(nct)::value;
+    auto k = k_approx<P, NC>;
+    static const int occ = per_sm(k);
+    k<<<mcfr::grid_for(numel, kThreads, occ), kThreads, 0, s>>>(static_cast<const ST<P>*>(x),
+                                                                static_cast<ST<P>*>(out), numel);
+    mcfr::note_launch();
+    return mcfr::check_launch("mcf approx kernel");
+  };
+  if (p == MCF_B32) {
+    switch (nc) {
+      case 1: return go(PB32{}, std::integral_constant<int, 1>{});
+      case 2: return go(PB32{}, std::integral_constant<int, 2>{});
+      case 3: return go(PB32{}, std::integral_constant<int, 3>{});
+      case 4: return go(PB32{}, std::integral_constant<int, 4>{});
+    }
+  }
+  Args a{x, nc, nullptr, nc, nullptr, 1, out, 1, numel, s};
+  return dispatch_prec<kApprox>(p, a);
+}
+
+std::mutex g_tab_mu;
+bool g_tab_done[64];
+
+}  // namespace
+}  // namespace mcfg
+
+namespace mcfr {
+mcf_status ensure_device_tables() {
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) d = 0;
+  std::lock_guard<std::mutex> lk(mcfg::g_tab_mu);
+  if (mcfg::g_tab_done[d]) return MCF_OK;
+  // The literal fallback path keeps reference-sized staging arrays in local
+  // memory (binary64 renorm stages are 640 B per frame and the deepest chain,
+  // mul_mcn -> div -> add -> renorm, exceeds the 1 KiB default stack).
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitStackSize);
+  if (cur < 4096 && cudaDeviceSetLimit(cudaLimitStackSize, 4096) != cudaSuccess)
+    return fail(MCF_ERR_CUDA, "mcf: cannot raise the device stack limit");
+  double tab[4096];
+  exp2_table(tab);
+  if (cudaMemcpyToSymbol(mcfg::g_exp_tab, tab, sizeof(tab)) != cudaSuccess)
+    return fail(MCF_ERR_CUDA, "mcf: cannot upload the exp table to the device");
+  mcfg::g_tab_done[d] = true;
+  return MCF_OK;
+}
+}  // namespace mcfr
+
+// ---- C-ABI ---------------------------------------------------------------------
+
+using mcfg::Args;
+
+namespace {
+
+mcf_status check_common(mcf_prec p, int64_t numel, const char* op) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, std::string(op) + ": unknown precision");
+  if (numel < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, std::string(op) + ": negative element count");
+  return MCF_OK;
+}
+
+mcf_status check_nc(int nc) {
+  if (mcfr::bad_nc(nc)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
+  return MCF_OK;
+}
+
+mcf_status check_vn(int64_t vn, int64_t numel, const char* op) {
+  if (vn < 1 || (numel > 0 && numel % vn != 0))
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT,
+                      std::string(op) + ": operand of " + std::to_string(vn) +
+                          " elements does not broadcast over " + std::to_string(numel));
+  return MCF_OK;
+}
+
+#define MCF_TRY(expr)                  \
+  do {                                 \
+    const mcf_status _s = (expr);      \
+    if (_s != MCF_OK) return _s;       \
+  } while (0)
+
+template <int OP>
+mcf_status binary(const char* name, mcf_prec p, const void* x, int ncx, const void* y, int ncy,
+                  void* out, int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, name));
+  MCF_TRY(check_nc(ncx));
+  MCF_TRY(check_nc(ncy));
+  const int nc = ncx > ncy ? ncx : ncy;
+  Args a{x, ncx, y, ncy, nullptr, 1, out, nc, numel, s};
+  return mcfg::dispatch_prec<OP>(p, a);
+}
+
+}  // namespace
+
+extern "C" {
+
+mcf_status mcf_two_sum(mcf_prec p, const void* a, const void* b, void* s, void* e, int64_t n,
+                       mcf_stream stream) {
+  MCF_TRY(check_common(p, n, "two_sum"));
+  if (n == 0) return MCF_OK;
+  auto go = [&](auto tag) -> mcf_status {
+    using P = decltype(tag);
+    using S = typename P::st;
+    auto k = mcfg::k_eft<P, false>;
+    static const int occ = mcfg::per_sm(k);
+    constexpr int EPT = mcfg::ept_for<P, 1>();
+    k<<<mcfr::grid_for((n + EPT - 1) / EPT, mcfg::kThreads, occ), mcfg::kThreads, 0, stream>>>(
+        static_cast<const S*>(a), static_cast<const S*>(b), static_cast<S*>(s), static_cast<S*>(e), n);
+    mcfr::note_launch();
+    return mcfr::check_launch("two_sum kernel");
+  };
+  return p == MCF_B16 ? go(mcfg::PB16{}) : p == MCF_B32 ? go(mcfg::PB32{}) : go(mcfg::PB64{});
+}
+
+mcf_status mcf_two_prod(mcf_prec p, const void* a, const void* b, void* prod, void* e, int64_t n,
+                        mcf_stream stream) {
+  MCF_TRY(check_common(p, n, "two_prod"));
+  if (n == 0) return MCF_OK;
+  auto go = [&](auto tag) -> mcf_status {
+    using P = decltype(tag);
+    using S = typename P::st;
+    auto k = mcfg::k_eft<P, true>;
+    static const int occ = mcfg::per_sm(k);
+    constexpr int EPT = mcfg::ept_for<P, 1>();
+    k<<<mcfr::grid_for((n + EPT - 1) / EPT, mcfg::kThreads, occ), mcfg::kThreads, 0, stream>>>(
+        static_cast<const S*>(a), static_cast<const S*>(b), static_cast<S*>(prod), static_cast<S*>(e), n);
+    mcfr::note_launch();
+    return mcfr::check_launch("two_prod kernel");
+  };
+  return p == MCF_B16 ? go(mcfg::PB16{}) : p == MCF_B32 ? go(mcfg::PB32{}) : go(mcfg::PB64{});
+}
+
+mcf_status mcf_renormalize(mcf_prec p, const void* h, int nc, void* out, int r_nc, int64_t numel,
+                           mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "renormalize"));
+  MCF_TRY(check_nc(nc));
+  MCF_TRY(check_nc(r_nc));
+  return mcfg::dispatch_prec<mcfg::kRenorm>(p, Args{h, nc, nullptr, nc, nullptr, 1, out, r_nc, numel, s});
+}
+
+mcf_status mcf_simple_renorm(mcf_prec p, const void* h, int nc, void* out, int r_nc,
+                             int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "simple_renorm"));
+  MCF_TRY(check_nc(nc));
+  MCF_TRY(check_nc(r_nc));
+  return mcfg::dispatch_prec<mcfg::kSimple>(p, Args{h, nc, nullptr, nc, nullptr, 1, out, r_nc, numel, s});
+}
+
+mcf_status mcf_approx(mcf_prec p, const void* x, int nc, void* out, int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "approx"));
+  MCF_TRY(check_nc(nc));
+  return mcfg::approx_dispatch(p, x, nc, out, numel, s);
+}
+
+mcf_status mcf_negate(mcf_prec p, const void* x, int nc, void* out, int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "negate"));
+  MCF_TRY(check_nc(nc));
+  return mcfg::dispatch_prec<mcfg::kNeg>(p, Args{x, nc, nullptr, nc, nullptr, 1, out, nc, numel, s});
+}
+
+mcf_status mcf_grow_expn(mcf_prec p, const void* x, int nc, const void* v, int64_t vn, void* out,
+                         int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "grow_expn"));
+  MCF_TRY(check_nc(nc));
+  MCF_TRY(check_vn(vn, numel, "grow_expn"));
+  return mcfg::dispatch_prec<mcfg::kGrow>(p, Args{x, nc, nullptr, nc, v, vn, out, nc, numel, s});
+}
+
+mcf_status mcf_scaling_n(mcf_prec p, const void* x, int nc, const void* v, int64_t vn, int expanded,
+                         void* out, int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "scaling_n"));
+  MCF_TRY(check_nc(nc));
+  MCF_TRY(check_vn(vn, numel, "scaling_n"));
+  if (expanded) {
+    MCF_TRY(check_nc(nc + 1));
+    return mcfg::dispatch_prec<mcfg::kScaleX>(p, Args{x, nc, nullptr, nc, v, vn, out, nc + 1, numel, s});
+  }
+  return mcfg::dispatch_prec<mcfg::kScale>(p, Args{x, nc, nullptr, nc, v, vn, out, nc, numel, s});
+}
+
+mcf_status mcf_div_n(mcf_prec p, const void* v, int64_t vn, const void* y, int nc, void* out,
+                     int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "div_n"));
+  MCF_TRY(check_nc(nc));
+  MCF_TRY(check_vn(vn, numel, "div_n"));
+  return mcfg::dispatch_prec<mcfg::kDivN>(p, Args{y, nc, nullptr, nc, v, vn, out, nc, numel, s});
+}
+
+mcf_status mcf_add_mcn(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                       int64_t numel, mcf_stream s) {
+  return binary<mcfg::kAdd>("add_mcn", p, x, ncx, y, ncy, out, numel, s);
+}
+mcf_status mcf_div_mcn(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                       int64_t numel, mcf_stream s) {
+  return binary<mcfg::kDiv>("div_mcn", p, x, ncx, y, ncy, out, numel, s);
+}
+mcf_status mcf_mul_mcn(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                       int64_t numel, mcf_stream s) {
+  return binary<mcfg::kMul>("mul_mcn", p, x, ncx, y, ncy, out, numel, s);
+}
+mcf_status mcf_mul_mcn_slow(mcf_prec p, const void* x, int ncx, const void* y, int ncy, void* out,
+                            int64_t numel, mcf_stream s) {
+  return binary<mcfg::kMulSlow>("mul_mcn_slow", p, x, ncx, y, ncy, out, numel, s);
+}
+
+mcf_status mcf_square_mcn(mcf_prec p, const void* x, int nc, void* out, int64_t numel,
+                          mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "square_mcn"));
+  MCF_TRY(check_nc(nc));
+  return mcfg::dispatch_prec<mcfg::kSquare>(p, Args{x, nc, nullptr, nc, nullptr, 1, out, nc, numel, s});
+}
+
+mcf_status mcf_exp_mcn(mcf_prec p, const void* x, int nc, void* out, int64_t numel, mcf_stream s) {
+  MCF_TRY(check_common(p, numel, "exp_mcn"));
+  MCF_TRY(check_nc(nc));
+  MCF_TRY(mcfr::ensure_device_tables());
+  return mcfg::dispatch_prec<mcfg::kExp>(p, Args{x, nc, nullptr, nc, nullptr, 1, out, nc, numel, s});
+}
+
+}  // extern "C"

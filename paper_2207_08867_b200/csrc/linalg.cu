@@ -1,0 +1,385 @@
+// linalg.cu -- MC contractions (linalg.hpp) on sm_100a.
+//
+// Reference-order kernels (this file, "exact"): every output element runs the
+// reference's DotCore (linalg.hpp:38-91) with the register fast paths --
+// term(k) = ScalingN expanded to nc+1 (:55-57), sequential add_kernel at
+// nc+1 (:63-69) or the pairwise tree (:71-75), final renorm to nc (:89) --
+// so results are bit-identical to the reference.  nc == 1 is the plain
+// fl-MAC chain (:47-53).  An output whose fast-path preconditions fail is
+// recomputed by the literal restatement (mcf_lit.cuh).
+//
+// MC x MC (the reference refuses it, linalg.hpp:159-166) uses the same
+// DotCore with SURVEY 8c "recipe B" terms: the mul_mcn_slow term set
+// (mc_ops.hpp:240-250) renormalized to nc+1.
+//
+// The throughput kernels (compensated register accumulators on tiled
+// operands) live in mm_fast.cu.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <type_traits>
+
+#include "mcf_fast.cuh"
+#include "mcf_lit.cuh"
+#include "mcf_prec.cuh"
+#include "mcf_runtime.h"
+
+namespace mcfg {
+namespace {
+
+template <class P>
+using RT = typename P::rt;
+template <class P>
+using ST = typename P::st;
+
+constexpr int kThreads = 128;
+
+// ---- literal DotCore (runtime nc; fallback and non-instantiated shapes) ----
+
+template <class P>
+__device__ void lit_term(const ST<P>* x, int64_t xi, const ST<P>* w, int64_t wi, int nc,
+                         RT<P>* out) {
+  RT<P> xc[lit::kMaxNc];
+  for (int c = 0; c < nc; ++c) xc[c] = P::ld(x[xi * nc + c]);
+  lit::scale<P>(xc, nc, P::ld(w[wi]), out, nc + 1);
+}
+
+template <class P>
+__device__ void lit_reduce(const ST<P>* x, int64_t xa, const ST<P>* w, int64_t wa, int64_t ws,
+                           int nc, int64_t lo, int64_t hi, int strategy, int leaf, RT<P>* acc) {
+  const int64_t leafn = leaf > 1 ? leaf : 1;
+  if (strategy == MCF_SEQUENTIAL || hi - lo <= leafn) {
+    lit_term<P>(x, xa + lo, w, wa + lo * ws, nc, acc);
+    RT<P> t[lit::kMaxNc + 1];
+    for (int64_t k = lo + 1; k < hi; ++k) {
+      lit_term<P>(x, xa + k, w, wa + k * ws, nc, t);
+      lit::add<P>(acc, nc + 1, t, nc + 1, acc, nc + 1);
+    }
+    return;
+  }
+  const int64_t mid = lo + (hi - lo) / 2;
+  RT<P> rhs[lit::kMaxNc + 1];
+  lit_reduce<P>(x, xa, w, wa, ws, nc, lo, mid, strategy, leaf, acc);
+  lit_reduce<P>(x, xa, w, wa, ws, nc, mid, hi, strategy, leaf, rhs);
+  lit::add<P>(acc, nc + 1, rhs, nc + 1, acc, nc + 1);
+}
+
+template <class P>
+__device__ __noinline__ void lit_dot(const ST<P>* x, int64_t xa, const ST<P>* w, int64_t wa,
+                                     int64_t ws, int nc, int64_t len, int strategy, int leaf,
+                                     RT<P>* out) {
+  if (len == 0) {
+    for (int c = 0; c < nc; ++c) out[c] = RT<P>(0);
+    return;
+  }
+  if (nc == 1 && strategy == MCF_SEQUENTIAL) {
+    RT<P> acc = RT<P>(0);
+    for (int64_t k = 0; k < len; ++k)
+      acc = P::add(acc, P::mul(P::ld(x[xa + k]), P::ld(w[wa + k * ws])));
+    out[0] = acc;
+    return;
+  }
+  RT<P> acc[lit::kMaxNc + 1];
+  lit_reduce<P>(x, xa, w, wa, ws, nc, 0, len, strategy, leaf, acc);
+  lit::renorm<P>(acc, nc + 1, out, nc);
+}
+
+// recipe B, literal
+template <class P>
+__device__ void lit_mcmc_term(const ST<P>* x, int64_t xi, const ST<P>* y, int64_t yi, int nc,
+                              RT<P>* out) {
+  RT<P> a[lit::kMaxNc], b[lit::kMaxNc], h[lit::kStage];
+  for (int c = 0; c < nc; ++c) {
+    a[c] = P::ld(x[xi * nc + c]);
+    b[c] = P::ld(y[yi * nc + c]);
+  }
+  int m = 0;
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; i + j < nc; ++j) {
+      two_prod<P>(a[i], b[j], h[m], h[m + 1]);
+      m += 2;
+    }
+  for (int i = 1; i < nc; ++i) h[m++] = P::mul(a[i], b[nc - i]);
+  lit::renorm<P>(h, m, out, nc + 1);
+}
+
+template <class P>
+__device__ __noinline__ void lit_mcmc(const ST<P>* x, int64_t xa, int64_t xs, const ST<P>* y,
+                                      int64_t ya, int64_t ys, int nc, int64_t len, RT<P>* out) {
+  if (len == 0) {
+    for (int c = 0; c < nc; ++c) out[c] = RT<P>(0);
+    return;
+  }
+  if (nc == 1) {
+    RT<P> acc = RT<P>(0);
+    for (int64_t k = 0; k < len; ++k)
+      acc = P::add(acc, P::mul(P::ld(x[xa + k * xs]), P::ld(y[ya + k * ys])));
+    out[0] = acc;
+    return;
+  }
+  RT<P> acc[lit::kMaxNc + 1], t[lit::kMaxNc + 1];
+  lit_mcmc_term<P>(x, xa, y, ya, nc, acc);
+  for (int64_t k = 1; k < len; ++k) {
+    lit_mcmc_term<P>(x, xa + k * xs, y, ya + k * ys, nc, t);
+    lit::add<P>(acc, nc + 1, t, nc + 1, acc, nc + 1);
+  }
+  lit::renorm<P>(acc, nc + 1, out, nc);
+}
+
+// ---- register DotCore (compile-time nc) ---------------------------------------
+
+template <class P, int NC>
+__device__ __forceinline__ bool fast_term(const ST<P>* x, int64_t xi, RT<P> v,
+                                          RT<P> (&t)[NC + 1]) {
+  RT<P> xc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) xc[c] = P::ld(x[xi * NC + c]);
+  return fast::scale<P, NC, NC + 1>(xc, v, t);
+}
+
+// sequential DotCore over k in [0, len); false -> recompute with lit_dot
+template <class P, int NC>
+__device__ __forceinline__ bool fast_dot_seq(const ST<P>* x, int64_t xa, const ST<P>* w,
+                                             int64_t wa, int64_t ws, int64_t len,
+                                             RT<P> (&out)[NC]) {
+  RT<P> acc[NC + 1], t[NC + 1];
+  bool ok = fast_term<P, NC>(x, xa, P::ld(w[wa]), acc);
+  for (int64_t k = 1; k < len; ++k) {
+    ok &= fast_term<P, NC>(x, xa + k, P::ld(w[wa + k * ws]), t);
+    ok &= fast::add_ordered<P, NC + 1, NC + 1>(acc, t, acc);
+  }
+  ok &= fast::renorm<P, NC + 1, NC>(acc, out);
+  return ok;
+}
+
+template <class P, int NC>
+__device__ __forceinline__ bool fast_mcmc_term(const ST<P>* x, int64_t xi, const ST<P>* y,
+                                               int64_t yi, RT<P> (&t)[NC + 1]) {
+  RT<P> a[NC], b[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    a[c] = P::ld(x[xi * NC + c]);
+    b[c] = P::ld(y[yi * NC + c]);
+  }
+  RT<P> h[fast::mul_slow_terms(NC)];
+  int m = 0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i)
+#pragma unroll
+    for (int j = 0; i + j < NC; ++j) {
+      two_prod<P>(a[i], b[j], h[m], h[m + 1]);
+      m += 2;
+    }
+#pragma unroll
+  for (int i = 1; i < NC; ++i) h[m++] = P::mul(a[i], b[NC - i]);
+  return fast::renorm<P, fast::mul_slow_terms(NC), NC + 1>(h, t);
+}
+
+// ---- kernels -----------------------------------------------------------------------
+
+// out[b, i, j] for a batch of MC x Tensor products; one thread per output,
+// consecutive threads on consecutive j (coalesced w reads, broadcast x reads)
+template <class P, int NC>
+__global__ void __launch_bounds__(kThreads) k_bmm_exact(const ST<P>* __restrict__ x, int nc,
+                                                        const ST<P>* __restrict__ w,
+                                                        int64_t batch, int64_t m, int64_t k,
+                                                        int64_t n, int w_batched,
+                                                        ST<P>* __restrict__ out, int strategy,
+                                                        int leaf) {
+  const int64_t total = batch * m * n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += stride) {
+    const int64_t b = o / (m * n), r = o % (m * n), i = r / n, j = r % n;
+    const int64_t xa = (b * m + i) * k;              // element index of x[b, i, 0]
+    const int64_t wa = (w_batched ? b * k * n : 0) + j;
+    RT<P> res[lit::kMaxNc];
+    bool done = false;
+    if constexpr (NC > 0) {
+      if (strategy == MCF_SEQUENTIAL && k > 0) {
+        if constexpr (NC == 1) {
+          RT<P> acc = RT<P>(0);
+          for (int64_t t = 0; t < k; ++t)
+            acc = P::add(acc, P::mul(P::ld(x[xa + t]), P::ld(w[wa + t * n])));
+          res[0] = acc;
+          done = true;
+        } else {
+          RT<P> o2[NC];
+          done = fast_dot_seq<P, NC>(x, xa, w, wa, n, k, o2);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) res[c] = o2[c];
+        }
+      }
+    }
+    const int ncr = NC > 0 ? NC : nc;
+    if (!done) lit_dot<P>(x, xa, w, wa, n, ncr, k, strategy, leaf, res);
+    for (int c = 0; c < ncr; ++c) out[o * ncr + c] = P::sv(res[c]);
+  }
+}
+
+// MC x MC, recipe B: out[i, j] = sum_k x[xa_i + k*xs] * y[ya_j + k*ys]
+// dot: (x, y both (batch, k, nc)); mm: x (m, k, nc), y (k, n, nc)
+template <class P, int NC>
+__global__ void __launch_bounds__(kThreads) k_mcmc_exact(const ST<P>* __restrict__ x,
+                                                         const ST<P>* __restrict__ y, int nc,
+                                                         int64_t rows, int64_t cols, int64_t k,
+                                                         int mm_layout, ST<P>* __restrict__ out) {
+  const int64_t total = rows * cols;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += stride) {
+    const int64_t i = o / cols, j = o % cols;
+    // mm: x row i (xa=i*k, xs=1), y column j (ya=j, ys=cols); dot: both row o
+    const int64_t xa = mm_layout ? i * k : o * k, xs = 1;
+    const int64_t ya = mm_layout ? j : o * k, ys = mm_layout ? cols : 1;
+    RT<P> res[lit::kMaxNc];
+    bool done = false;
+    if constexpr (NC > 1) {
+      if (k > 0) {
+        RT<P> acc[NC + 1], t[NC + 1];
+        done = fast_mcmc_term<P, NC>(x, xa, y, ya, acc);
+        for (int64_t kk = 1; kk < k; ++kk) {
+          done &= fast_mcmc_term<P, NC>(x, xa + kk * xs, y, ya + kk * ys, t);
+          done &= fast::add_ordered<P, NC + 1, NC + 1>(acc, t, acc);
+        }
+        RT<P> o2[NC];
+        done &= fast::renorm<P, NC + 1, NC>(acc, o2);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) res[c] = o2[c];
+      }
+    }
+    const int ncr = NC > 0 ? NC : nc;
+    if (!done) lit_mcmc<P>(x, xa, xs, y, ya, ys, ncr, k, res);
+    for (int c = 0; c < ncr; ++c) out[o * ncr + c] = P::sv(res[c]);
+  }
+}
+
+template <class K>
+int per_sm(K kernel) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, 0) != cudaSuccess || n < 1) n = 1;
+  return n;
+}
+
+template <class P, int NC>
+mcf_status launch_bmm(const void* x, int nc, const void* w, int64_t batch, int64_t m, int64_t k,
+                      int64_t n, int w_batched, void* out, int strategy, int leaf, cudaStream_t s) {
+  auto kern = k_bmm_exact<P, NC>;
+  static const int occ = per_sm(kern);
+  const int grid = mcfr::grid_for(batch * m * n, kThreads, occ);
+  kern<<<grid, kThreads, 0, s>>>(static_cast<const ST<P>*>(x), nc, static_cast<const ST<P>*>(w), batch,
+                                 m, k, n, w_batched, static_cast<ST<P>*>(out), strategy, leaf);
+  mcfr::note_launch();
+  return mcfr::check_launch("mcf bmm kernel");
+}
+
+template <class P, int NC>
+mcf_status launch_mcmc(const void* x, const void* y, int nc, int64_t rows, int64_t cols, int64_t k,
+                       int mm_layout, void* out, cudaStream_t s) {
+  auto kern = k_mcmc_exact<P, NC>;
+  static const int occ = per_sm(kern);
+  const int grid = mcfr::grid_for(rows * cols, kThreads, occ);
+  kern<<<grid, kThreads, 0, s>>>(static_cast<const ST<P>*>(x), static_cast<const ST<P>*>(y), nc, rows,
+                                 cols, k, mm_layout, static_cast<ST<P>*>(out));
+  mcfr::note_launch();
+  return mcfr::check_launch("mcf mc x mc kernel");
+}
+
+template <class P>
+mcf_status bmm_prec(const void* x, int nc, const void* w, int64_t batch, int64_t m, int64_t k,
+                    int64_t n, int w_batched, void* out, int strategy, int leaf, cudaStream_t s) {
+  if constexpr (std::is_same<P, PB32>::value) {
+    switch (nc) {
+      case 1: return launch_bmm<P, 1>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf, s);
+      case 2: return launch_bmm<P, 2>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf, s);
+      case 3: return launch_bmm<P, 3>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf, s);
+      default: break;
+    }
+  }
+  if (nc == 1) return launch_bmm<P, 1>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf, s);
+  return launch_bmm<P, 0>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf, s);
+}
+
+template <class P>
+mcf_status mcmc_prec(const void* x, const void* y, int nc, int64_t rows, int64_t cols, int64_t k,
+                     int mm_layout, void* out, cudaStream_t s) {
+  if constexpr (std::is_same<P, PB32>::value || std::is_same<P, PB16>::value) {
+    switch (nc) {
+      case 2: return launch_mcmc<P, 2>(x, y, nc, rows, cols, k, mm_layout, out, s);
+      case 3: return launch_mcmc<P, 3>(x, y, nc, rows, cols, k, mm_layout, out, s);
+      default: break;
+    }
+  }
+  return launch_mcmc<P, 0>(x, y, nc, rows, cols, k, mm_layout, out, s);
+}
+
+}  // namespace
+}  // namespace mcfg
+
+// ---- C-ABI ---------------------------------------------------------------------
+
+namespace {
+mcf_status check_lin(mcf_prec p, int nc, const char* op) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, std::string(op) + ": unknown precision");
+  if (mcfr::bad_nc(nc) || mcfr::bad_nc(nc + 1))
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
+  return MCF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+mcf_status mcf_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
+                       int64_t k, int64_t n, int w_batched, void* out, int strategy, int leaf_arity,
+                       mcf_stream stream) {
+  const mcf_status st = check_lin(p, nc, "mm_mcn");
+  if (st != MCF_OK) return st;
+  if (batch < 0 || m < 0 || k < 0 || n < 0)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: negative dimension");
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_PAIRWISE_TREE)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: unknown reduction strategy");
+  if (batch * m * n == 0) return MCF_OK;
+  if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  // the literal pairwise tree recurses ceil(log2 k) deep (linalg.hpp:59-76)
+  if (strategy == MCF_PAIRWISE_TREE && mcfr::ensure_stack(16384) != MCF_OK) return MCF_ERR_CUDA;
+  switch (p) {
+    case MCF_B16: return mcfg::bmm_prec<mcfg::PB16>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf_arity, stream);
+    case MCF_B32: return mcfg::bmm_prec<mcfg::PB32>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf_arity, stream);
+    default: return mcfg::bmm_prec<mcfg::PB64>(x, nc, w, batch, m, k, n, w_batched, out, strategy, leaf_arity, stream);
+  }
+}
+
+mcf_status mcf_mm_mcn_mcmc_refusal(void) {
+  return mcfr::fail(MCF_ERR_UNSUPPORTED,
+                    "mm_mcn: matrix products of two MCTensors are not supported; convert one "
+                    "operand to a working-precision tensor first");
+}
+
+mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
+                       int64_t n, void* out, mcf_stream stream) {
+  const mcf_status st = check_lin(p, nc, "mm_mcmc");
+  if (st != MCF_OK) return st;
+  if (m < 0 || k < 0 || n < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcmc: negative dimension");
+  if (m * n == 0) return MCF_OK;
+  if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  switch (p) {
+    case MCF_B16: return mcfg::mcmc_prec<mcfg::PB16>(x, y, nc, m, n, k, 1, out, stream);
+    case MCF_B32: return mcfg::mcmc_prec<mcfg::PB32>(x, y, nc, m, n, k, 1, out, stream);
+    default: return mcfg::mcmc_prec<mcfg::PB64>(x, y, nc, m, n, k, 1, out, stream);
+  }
+}
+
+mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch, int64_t k,
+                        void* out, mcf_stream stream) {
+  const mcf_status st = check_lin(p, nc, "dot_mcmc");
+  if (st != MCF_OK) return st;
+  if (batch < 0 || k < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "dot_mcmc: negative dimension");
+  if (batch == 0) return MCF_OK;
+  if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  switch (p) {
+    case MCF_B16: return mcfg::mcmc_prec<mcfg::PB16>(x, y, nc, batch, 1, k, 0, out, stream);
+    case MCF_B32: return mcfg::mcmc_prec<mcfg::PB32>(x, y, nc, batch, 1, k, 0, out, stream);
+    default: return mcfg::mcmc_prec<mcfg::PB64>(x, y, nc, batch, 1, k, 0, out, stream);
+  }
+}
+
+}  // extern "C"

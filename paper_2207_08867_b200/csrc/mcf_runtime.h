@@ -1,0 +1,52 @@
+// mcf_runtime.h -- host-side runtime shared by the library's translation units:
+// error reporting (thread-local, reference-worded messages), launch
+// accounting, grid sizing and the device workspace used by the mcf_h_* entry
+// points.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/mcf_gpu.h"
+
+namespace mcfr {
+
+mcf_status fail(mcf_status code, const std::string& msg);
+inline mcf_status ok() { return MCF_OK; }
+void note_launch();
+// CUDA error after a launch -> MCF_ERR_CUDA with the runtime's message
+mcf_status check_launch(const char* what);
+
+int sm_count();
+// grid for a grid-stride kernel: enough CTAs to fill every SM `per_sm` deep,
+// never more than needed to cover `work_items` with `threads` each.
+inline int grid_for(int64_t work_items, int threads, int per_sm) {
+  const int64_t need = (work_items + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+  const int64_t g = need < cap ? need : cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+inline bool bad_nc(int nc) { return nc < 1 || nc > 8; }
+inline std::size_t elem_bytes(mcf_prec p) {
+  return p == MCF_B16 ? 2 : (p == MCF_B32 ? 4 : 8);
+}
+bool valid_prec(int p);
+
+// binary128-computed 2^(j/2048), j < 2048, as (hi, lo) pairs (4096 doubles)
+void exp2_table(double* out);
+
+// per-device init of constant tables used by the elementwise kernels (and the
+// stack limit the literal fallback path needs)
+mcf_status ensure_device_tables();
+// raise the per-thread device stack to at least `bytes` (recursive tree plan)
+mcf_status ensure_stack(std::size_t bytes);
+
+// device workspace for the host-buffer entry points (grows, per device)
+void* workspace(std::size_t bytes, int slot);
+cudaStream_t side_stream(int slot);
+void* pinned(std::size_t bytes, int slot);
+
+}  // namespace mcfr
