@@ -56,8 +56,10 @@ typedef enum mcf_status {
 typedef enum mcf_prec { MCF_B16 = 0, MCF_B32 = 1, MCF_B64 = 2 } mcf_prec; /* precision.hpp:209 */
 
 typedef enum mcf_reduce { /* linalg.hpp:23 */
-  MCF_SEQUENTIAL = 0,
-  MCF_PAIRWISE_TREE = 1
+  MCF_SEQUENTIAL = 0,    /* reference order, bit-identical to the reference */
+  MCF_PAIRWISE_TREE = 1, /* reference tree order, bit-identical */
+  MCF_FAST = 2           /* GPU order: compensated binary64 accumulation on the
+                            FP64 pipe; within the reference's error bound */
 } mcf_reduce;
 
 /* ---- library ------------------------------------------------------------- */
@@ -134,12 +136,17 @@ mcf_status mcf_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t
  * MCF_ERR_UNSUPPORTED with the reference's message, like the reference. */
 mcf_status mcf_mm_mcn_mcmc_refusal(void);
 /* NEW capability (the reference refuses it): MC x MC products.
- * out[i,j,:] = sum_k x[i,k,:] * y[k,j,:]; checked against SURVEY 8c recipe B. */
+ * out[i,j,:] = sum_k x[i,k,:] * y[k,j,:].  strategy MCF_SEQUENTIAL runs SURVEY
+ * 8c recipe B (bit-identical to the oracle's composition of reference
+ * kernels); MCF_FAST the compensated binary64 accumulation. */
 mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
-                       int64_t n, void* out, mcf_stream stream);
+                       int64_t n, void* out, int strategy, mcf_stream stream);
 /* out[b,:] = sum_k x[b,k,:] * y[b,k,:]  (batched MC x MC dots) */
 mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch,
-                        int64_t k, void* out, mcf_stream stream);
+                        int64_t k, void* out, int strategy, mcf_stream stream);
+/* FP64-pipe instructions per multiply-add of the MCF_FAST kernel for this
+ * operand kind (mcmc = 0: MC x Tensor, 1: MC x MC); 0 = no fast kernel. */
+int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
 
 /* ---- host-buffer entry points (blocking; the reference's calling model) --- */
 /* op: "grow_expn" "scaling_n" "div_n" "add_mcn" "div_mcn" "mul_mcn"
@@ -149,9 +156,9 @@ mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
 mcf_status mcf_h_elementwise(const char* op, mcf_prec p, const void* x, int ncx, const void* y,
                              int ncy, const void* v, int64_t vn, void* out, int64_t numel);
 mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t batch,
-                         int64_t m, int64_t k, int64_t n, int w_batched, void* out);
+                         int64_t m, int64_t k, int64_t n, int w_batched, void* out, int strategy);
 mcf_status mcf_h_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
-                         int64_t n, void* out);
+                         int64_t n, void* out, int strategy);
 
 /* ---- host input generation (mcf::Rng, rng.hpp:13-65) ----------------------- */
 /* n draws of Rng(seed).uniform() (53-bit, [0,1)), bitwise the reference's */

@@ -30,7 +30,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libmcf_b200.so")
 
 B16, B32, B64 = 0, 1, 2
-SEQUENTIAL, PAIRWISE_TREE = 0, 1
+SEQUENTIAL, PAIRWISE_TREE, FAST = 0, 1, 2
 
 
 class UnsupportedOperation(NotImplementedError):
@@ -61,11 +61,12 @@ _SIGS = {
     "mcf_square_mcn": [_int, _p, _int, _p, _i64, _p],
     "mcf_exp_mcn": [_int, _p, _int, _p, _i64, _p],
     "mcf_bmm_mcn": [_int, _p, _int, _p, _i64, _i64, _i64, _i64, _int, _p, _int, _int, _p],
-    "mcf_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _p],
-    "mcf_dot_mcmc": [_int, _p, _p, _int, _i64, _i64, _p, _p],
+    "mcf_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _int, _p],
+    "mcf_dot_mcmc": [_int, _p, _p, _int, _i64, _i64, _p, _int, _p],
     "mcf_h_elementwise": [C.c_char_p, _int, _p, _int, _p, _int, _p, _i64, _p, _i64],
-    "mcf_h_bmm_mcn": [_int, _p, _int, _p, _i64, _i64, _i64, _i64, _int, _p],
-    "mcf_h_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p],
+    "mcf_h_bmm_mcn": [_int, _p, _int, _p, _i64, _i64, _i64, _i64, _int, _p, _int],
+    "mcf_h_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _int],
+    "mcf_fast_ops_per_mad": [_int, _int, _int],
 }
 
 

@@ -33,7 +33,7 @@ NVFLAGS = ARCH + [
 CXXFLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-I" + os.path.join(CUDA, "include"),
             "-I" + os.path.join(ROOT, "include")]
 
-CU_SOURCES = ["elementwise.cu", "linalg.cu", "hostapi.cu"]
+CU_SOURCES = ["elementwise.cu", "linalg.cu", "mm_fast.cu", "stream_fast.cu", "hostapi.cu"]
 CXX_SOURCES = ["runtime.cpp"]
 
 
@@ -42,7 +42,8 @@ def _sources():
 
 
 def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "mcf_gpu.h")]
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(ROOT, "include", "mcf_gpu.h"), os.path.abspath(__file__)]
 
 
 def _stale(target, deps):

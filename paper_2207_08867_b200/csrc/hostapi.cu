@@ -136,7 +136,7 @@ mcf_status mcf_h_elementwise(const char* op_c, mcf_prec p, const void* x, int nc
 }
 
 mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
-                         int64_t k, int64_t n, int w_batched, void* out) {
+                         int64_t k, int64_t n, int w_batched, void* out, int strategy) {
   if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: unknown precision");
   if (mcfr::bad_nc(nc) || mcfr::bad_nc(nc + 1)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
   const std::size_t es = mcfr::elem_bytes(p);
@@ -149,13 +149,13 @@ mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64
   char *dx = d, *dw = d + align(bx), *dout = dw + align(bw);
   if (bx) TRY(cuda_ok(cudaMemcpyAsync(dx, x, bx, cudaMemcpyHostToDevice, s), "H2D x"));
   if (bw) TRY(cuda_ok(cudaMemcpyAsync(dw, w, bw, cudaMemcpyHostToDevice, s), "H2D w"));
-  TRY(mcf_bmm_mcn(p, dx, nc, dw, batch, m, k, n, w_batched, dout, MCF_SEQUENTIAL, 1, s));
+  TRY(mcf_bmm_mcn(p, dx, nc, dw, batch, m, k, n, w_batched, dout, strategy, 1, s));
   if (bo) TRY(cuda_ok(cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, s), "D2H out"));
   return cuda_ok(cudaStreamSynchronize(s), "sync");
 }
 
 mcf_status mcf_h_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
-                         int64_t n, void* out) {
+                         int64_t n, void* out, int strategy) {
   if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcmc: unknown precision");
   if (mcfr::bad_nc(nc) || mcfr::bad_nc(nc + 1)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
   const std::size_t es = mcfr::elem_bytes(p);
@@ -167,7 +167,7 @@ mcf_status mcf_h_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64
   char *dx = d, *dy = d + align(bx), *dout = dy + align(by);
   if (bx) TRY(cuda_ok(cudaMemcpyAsync(dx, x, bx, cudaMemcpyHostToDevice, s), "H2D x"));
   if (by) TRY(cuda_ok(cudaMemcpyAsync(dy, y, by, cudaMemcpyHostToDevice, s), "H2D y"));
-  TRY(mcf_mm_mcmc(p, dx, dy, nc, m, k, n, dout, s));
+  TRY(mcf_mm_mcmc(p, dx, dy, nc, m, k, n, dout, strategy, s));
   if (bo) TRY(cuda_ok(cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, s), "D2H out"));
   return cuda_ok(cudaStreamSynchronize(s), "sync");
 }

@@ -38,7 +38,7 @@ constexpr int kThreads = 128;
 // ---- literal DotCore (runtime nc; fallback and non-instantiated shapes) ----
 
 template <class P>
-__device__ void lit_term(const ST<P>* x, int64_t xi, const ST<P>* w, int64_t wi, int nc,
+__device__ __noinline__ void lit_term(const ST<P>* x, int64_t xi, const ST<P>* w, int64_t wi, int nc,
                          RT<P>* out) {
   RT<P> xc[lit::kMaxNc];
   for (int c = 0; c < nc; ++c) xc[c] = P::ld(x[xi * nc + c]);
@@ -87,7 +87,7 @@ __device__ __noinline__ void lit_dot(const ST<P>* x, int64_t xa, const ST<P>* w,
 
 // recipe B, literal
 template <class P>
-__device__ void lit_mcmc_term(const ST<P>* x, int64_t xi, const ST<P>* y, int64_t yi, int nc,
+__device__ __noinline__ void lit_mcmc_term(const ST<P>* x, int64_t xi, const ST<P>* y, int64_t yi, int nc,
                               RT<P>* out) {
   RT<P> a[lit::kMaxNc], b[lit::kMaxNc], h[lit::kStage];
   for (int c = 0; c < nc; ++c) {
@@ -335,10 +335,18 @@ mcf_status mcf_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t
   if (st != MCF_OK) return st;
   if (batch < 0 || m < 0 || k < 0 || n < 0)
     return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: negative dimension");
-  if (strategy != MCF_SEQUENTIAL && strategy != MCF_PAIRWISE_TREE)
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_PAIRWISE_TREE && strategy != MCF_FAST)
     return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: unknown reduction strategy");
   if (batch * m * n == 0) return MCF_OK;
   if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  if (strategy == MCF_FAST) {
+    if (nc >= 2 && k > 0) {
+      const mcf_status fs = n == 1 ? mcfr::mv_fast_mct(p, x, nc, w, batch, m, k, w_batched, out, stream)
+                                   : mcfr::mm_fast_mct(p, x, nc, w, batch, m, k, n, w_batched, out, stream);
+      if (fs != MCF_ERR_UNSUPPORTED) return fs;
+    }
+    strategy = MCF_SEQUENTIAL;  // no fast kernel for this shape: reference order
+  }
   // the literal pairwise tree recurses ceil(log2 k) deep (linalg.hpp:59-76)
   if (strategy == MCF_PAIRWISE_TREE && mcfr::ensure_stack(16384) != MCF_OK) return MCF_ERR_CUDA;
   switch (p) {
@@ -355,12 +363,18 @@ mcf_status mcf_mm_mcn_mcmc_refusal(void) {
 }
 
 mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
-                       int64_t n, void* out, mcf_stream stream) {
+                       int64_t n, void* out, int strategy, mcf_stream stream) {
   const mcf_status st = check_lin(p, nc, "mm_mcmc");
   if (st != MCF_OK) return st;
   if (m < 0 || k < 0 || n < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcmc: negative dimension");
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_FAST)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcmc: unknown reduction strategy");
   if (m * n == 0) return MCF_OK;
   if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  if (strategy == MCF_FAST && k > 0) {
+    const mcf_status fs = mcfr::mm_fast_mcmc(p, x, y, nc, m, k, n, out, stream);
+    if (fs != MCF_ERR_UNSUPPORTED) return fs;
+  }
   switch (p) {
     case MCF_B16: return mcfg::mcmc_prec<mcfg::PB16>(x, y, nc, m, n, k, 1, out, stream);
     case MCF_B32: return mcfg::mcmc_prec<mcfg::PB32>(x, y, nc, m, n, k, 1, out, stream);
@@ -369,17 +383,25 @@ mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t
 }
 
 mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch, int64_t k,
-                        void* out, mcf_stream stream) {
+                        void* out, int strategy, mcf_stream stream) {
   const mcf_status st = check_lin(p, nc, "dot_mcmc");
   if (st != MCF_OK) return st;
   if (batch < 0 || k < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "dot_mcmc: negative dimension");
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_FAST)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "dot_mcmc: unknown reduction strategy");
   if (batch == 0) return MCF_OK;
   if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  if (strategy == MCF_FAST && k > 0) {
+    const mcf_status fs = mcfr::dot_fast_mcmc(p, x, y, nc, batch, k, out, stream);
+    if (fs != MCF_ERR_UNSUPPORTED) return fs;
+  }
   switch (p) {
     case MCF_B16: return mcfg::mcmc_prec<mcfg::PB16>(x, y, nc, batch, 1, k, 0, out, stream);
     case MCF_B32: return mcfg::mcmc_prec<mcfg::PB32>(x, y, nc, batch, 1, k, 0, out, stream);
     default: return mcfg::mcmc_prec<mcfg::PB64>(x, y, nc, batch, 1, k, 0, out, stream);
   }
 }
+
+int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) { return mcfr::mm_fast_ops_per_mad(mcmc, p, nc); }
 
 }  // extern "C"

@@ -1,0 +1,140 @@
+// mcf_accum.cuh -- compensated binary64 accumulators for the MCF_FAST
+// contractions (mm_fast.cu tiled kernels, stream_fast.cu row kernels).
+//
+// Every product of two binary32 components is exact in binary64, so an
+// output is carried as a short binary64 expansion: level 0 takes the leading
+// product through an error-free two_sum, lower levels take products and
+// rounding errors ~2^-24 / 2^-48 smaller.  Policies:
+//   AccT2  MC(nc=2) x T      (S, C)      9 FP64 ops / MAD
+//   AccT3  MC(nc=3) x T      (S, C, D)  23 ops / MAD
+//   AccM2  MC(nc=2) x MC(2)  (S, C)     11 ops / MAD
+//   AccM3  MC(nc=3) x MC(3)  (S, C, D)  33 ops / MAD
+//   AccH3  MC(nc=3, binary16) x MC(3, binary16), operands pre-summed into one
+//          binary64 each (<= 33 significant bits): S = fma(a, b, S), 1 op
+// merge() combines two partial expansions (warp reductions); the final value
+// is split greedily into nc components (mc_ops.hpp:286-297 on the extended
+// value) by split_out().
+#pragma once
+
+#include <cuda_fp16.h>
+
+namespace mcfg {
+
+__device__ __forceinline__ void dsum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bv = __dsub_rn(s, a);
+  const double av = __dsub_rn(s, bv);
+  e = __dadd_rn(__dsub_rn(a, av), __dsub_rn(b, bv));
+}
+
+struct AccT2 {
+  static constexpr int kNA = 2, kNB = 1, kLv = 2, kOps = 9;
+  __device__ static void mad(double (&acc)[kLv], const double* a, const double* b) {
+    const double p = __dmul_rn(a[0], b[0]);
+    double e;
+    dsum(acc[0], p, acc[0], e);
+    acc[1] = __fma_rn(a[1], b[0], __dadd_rn(acc[1], e));
+  }
+  __device__ static void merge(double (&acc)[kLv], const double (&o)[kLv]) {
+    double e;
+    dsum(acc[0], o[0], acc[0], e);
+    acc[1] = __dadd_rn(acc[1], __dadd_rn(o[1], e));
+  }
+};
+
+struct AccT3 {
+  static constexpr int kNA = 3, kNB = 1, kLv = 3, kOps = 23;
+  __device__ static void mad(double (&acc)[kLv], const double* a, const double* b) {
+    const double p0 = __dmul_rn(a[0], b[0]);
+    const double p1 = __dmul_rn(a[1], b[0]);
+    double e0, e1, e2;
+    dsum(acc[0], p0, acc[0], e0);
+    dsum(acc[1], e0, acc[1], e1);
+    dsum(acc[1], p1, acc[1], e2);
+    acc[2] = __fma_rn(a[2], b[0], __dadd_rn(acc[2], __dadd_rn(e1, e2)));
+  }
+  __device__ static void merge(double (&acc)[kLv], const double (&o)[kLv]) {
+    double e0, e1, e2;
+    dsum(acc[0], o[0], acc[0], e0);
+    dsum(acc[1], o[1], acc[1], e1);
+    dsum(acc[1], e0, acc[1], e2);
+    acc[2] = __dadd_rn(__dadd_rn(acc[2], o[2]), __dadd_rn(e1, e2));
+  }
+};
+
+struct AccM2 {
+  static constexpr int kNA = 2, kNB = 2, kLv = 2, kOps = 11;
+  __device__ static void mad(double (&acc)[kLv], const double* a, const double* b) {
+    const double p = __dmul_rn(a[0], b[0]);
+    double e;
+    dsum(acc[0], p, acc[0], e);
+    double c = __dadd_rn(acc[1], e);
+    c = __fma_rn(a[0], b[1], c);
+    c = __fma_rn(a[1], b[0], c);
+    acc[1] = __fma_rn(a[1], b[1], c);
+  }
+  __device__ static void merge(double (&acc)[kLv], const double (&o)[kLv]) { AccT2::merge(acc, o); }
+};
+
+struct AccM3 {
+  static constexpr int kNA = 3, kNB = 3, kLv = 3, kOps = 33;
+  __device__ static void mad(double (&acc)[kLv], const double* a, const double* b) {
+    const double p00 = __dmul_rn(a[0], b[0]);
+    const double p01 = __dmul_rn(a[0], b[1]);
+    const double p10 = __dmul_rn(a[1], b[0]);
+    double e0, e1, e2, e3;
+    dsum(acc[0], p00, acc[0], e0);
+    dsum(acc[1], e0, acc[1], e1);
+    dsum(acc[1], p01, acc[1], e2);
+    dsum(acc[1], p10, acc[1], e3);
+    double d = __dadd_rn(acc[2], __dadd_rn(e1, __dadd_rn(e2, e3)));
+    d = __fma_rn(a[0], b[2], d);
+    d = __fma_rn(a[1], b[1], d);
+    d = __fma_rn(a[2], b[0], d);
+    d = __fma_rn(a[1], b[2], d);
+    d = __fma_rn(a[2], b[1], d);
+    acc[2] = __fma_rn(a[2], b[2], d);
+  }
+  __device__ static void merge(double (&acc)[kLv], const double (&o)[kLv]) { AccT3::merge(acc, o); }
+};
+
+struct AccH3 {
+  static constexpr int kNA = 1, kNB = 1, kLv = 1, kOps = 1;
+  __device__ static void mad(double (&acc)[kLv], const double* a, const double* b) {
+    acc[0] = __fma_rn(a[0], b[0], acc[0]);
+  }
+  __device__ static void merge(double (&acc)[kLv], const double (&o)[kLv]) {
+    acc[0] = __dadd_rn(acc[0], o[0]);
+  }
+};
+
+template <class S>
+__device__ __forceinline__ double to_d(S v) { return (double)v; }
+template <>
+__device__ __forceinline__ double to_d<__half>(__half v) { return (double)__half2float(v); }
+
+template <class S>
+__device__ __forceinline__ S from_d(double v);
+template <>
+__device__ __forceinline__ float from_d<float>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ __half from_d<__half>(double v) { return __double2half(v); }
+
+// greedy split of S + C (+ D) into nc components of type ST
+template <class ST, int NC, int LV>
+__device__ __forceinline__ void split_out(const double (&acc)[LV], ST* out) {
+  double hi = acc[0], lo = 0.0;
+  if constexpr (LV >= 2) {
+    dsum(acc[0], acc[1], hi, lo);
+    if constexpr (LV >= 3) lo = __dadd_rn(lo, acc[2]);
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const ST c = from_d<ST>(__dadd_rn(hi, lo));
+    out[i] = c;
+    const double r = __dsub_rn(hi, to_d<ST>(c));  // exact
+    dsum(r, lo, hi, lo);
+  }
+}
+
+}  // namespace mcfg

@@ -83,7 +83,7 @@ __device__ R<P> approx(const R<P>* x, int nc) {
 
 // mc_ops.hpp:118-138
 template <class P>
-__device__ void grow(const R<P>* x, int nc, R<P> v, R<P>* out) {
+__device__ __noinline__ void grow(const R<P>* x, int nc, R<P> v, R<P>* out) {
   R<P> h[kMaxNc + 1], c[kMaxNc + 1];
   R<P> q = v;
   for (int k = nc; k >= 1; --k) two_sum<P>(x[k - 1], q, q, h[k]);
@@ -120,7 +120,7 @@ __device__ int scale_raw(const R<P>* x, int nc, R<P> v, R<P>* out) {
 
 // mc_ops.hpp:160-169
 template <class P>
-__device__ void scale(const R<P>* x, int nc, R<P> v, R<P>* out, int out_nc) {
+__device__ __noinline__ void scale(const R<P>* x, int nc, R<P> v, R<P>* out, int out_nc) {
   if (nc == 1 && out_nc == 1) {
     out[0] = P::mul(x[0], v);
     return;
@@ -132,7 +132,7 @@ __device__ void scale(const R<P>* x, int nc, R<P> v, R<P>* out, int out_nc) {
 
 // mc_ops.hpp:173-184
 template <class P>
-__device__ void add(const R<P>* x, int ncx, const R<P>* y, int ncy, R<P>* out, int out_nc) {
+__device__ __noinline__ void add(const R<P>* x, int ncx, const R<P>* y, int ncy, R<P>* out, int out_nc) {
   R<P> h[2 * kMaxNc + 2];
   int i = 0, j = 0, k = 0;
   while (i < ncx && j < ncy) h[k++] = P::mag(x[i]) >= P::mag(y[j]) ? x[i++] : y[j++];
@@ -164,7 +164,7 @@ __device__ __noinline__ void div(const R<P>* x, const R<P>* y, int nc, R<P>* out
 
 // mc_ops.hpp:216-230
 template <class P>
-__device__ void mul_fast(const R<P>* x, const R<P>* y, int nc, R<P>* out) {
+__device__ __noinline__ void mul_fast(const R<P>* x, const R<P>* y, int nc, R<P>* out) {
   if (nc == 1) {
     out[0] = P::mul(x[0], y[0]);
     return;
@@ -181,7 +181,7 @@ __device__ void mul_fast(const R<P>* x, const R<P>* y, int nc, R<P>* out) {
 
 // mc_ops.hpp:235-251
 template <class P>
-__device__ void mul_slow(const R<P>* x, const R<P>* y, int nc, R<P>* out) {
+__device__ __noinline__ void mul_slow(const R<P>* x, const R<P>* y, int nc, R<P>* out) {
   if (nc == 1) {
     out[0] = P::mul(x[0], y[0]);
     return;
@@ -199,7 +199,7 @@ __device__ void mul_slow(const R<P>* x, const R<P>* y, int nc, R<P>* out) {
 
 // mc_ops.hpp:256-282
 template <class P>
-__device__ void square(const R<P>* x, int nc, R<P>* out) {
+__device__ __noinline__ void square(const R<P>* x, int nc, R<P>* out) {
   if (nc == 1) {
     out[0] = P::mul(x[0], x[0]);
     return;
@@ -238,7 +238,7 @@ __device__ void expand_double(double v, R<P>* out, int nc) {
 
 // mc_ops.hpp:303-313, with a correctly rounded binary64 exp (see mcf_exp.cuh)
 template <class P>
-__device__ void exp(const R<P>* x, int nc, R<P>* out) {
+__device__ __noinline__ void exp(const R<P>* x, int nc, R<P>* out) {
   expand_double<P>(cr_exp(P::to_d(x[0])), out, nc);
   for (int i = 1; i < nc; ++i) {
     if (x[i] == R<P>(0)) continue;

@@ -44,6 +44,19 @@ mcf_status ensure_device_tables();
 // raise the per-thread device stack to at least `bytes` (recursive tree plan)
 mcf_status ensure_stack(std::size_t bytes);
 
+// MCF_FAST contraction kernels (mm_fast.cu, stream_fast.cu); each returns
+// MCF_ERR_UNSUPPORTED without a message when it has no instantiation for the
+// call, and the C-ABI then runs the reference-order kernel instead.
+mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
+                       int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s);
+mcf_status mv_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
+                       int64_t k, int w_batched, void* out, cudaStream_t s);
+mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
+                        int64_t n, void* out, cudaStream_t s);
+mcf_status dot_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch, int64_t k,
+                         void* out, cudaStream_t s);
+int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
+
 // device workspace for the host-buffer entry points (grows, per device)
 void* workspace(std::size_t bytes, int slot);
 cudaStream_t side_stream(int slot);

@@ -1,0 +1,297 @@
+// mm_fast.cu -- throughput MC contractions on the FP64 pipe (plan MCF_FAST).
+//
+// Each product of two binary32 (or binary16) components is exact in
+// binary64 (24+24 <= 53 bits).  The GPU therefore carries every output as a
+// compensated binary64 expansion (S, C[, D]) in registers through the K loop:
+//
+//   MC x T, nc=2:  p = a0*b (exact); (S, e) = two_sum(S, p); C += e;
+//                  C = fma(a1, b, C)                      -> 9 FP64 ops / MAD
+//   MC x T, nc=3:  three levels (S, C, D), 2 two_sums more -> 23 ops / MAD
+//   MC x MC, nc=2: p = a0*b0 into (S, C) as above, the cross terms a0*b1,
+//                  a1*b0, a1*b1 fused into C              -> 11 ops / MAD
+//   MC x MC, fp16 nc=3: components summed into one binary64 per operand
+//                  (<= 33 significant bits), S = fma(a, b, S) -> 1 op / MAD
+//
+// so the error before the final split into nc components is ~2^-100 x cond
+// (2^-47 x cond for the binary16 case, whose format resolves 2^-33) -- below
+// the reference's own error, which is dominated by the nc-component output
+// (2^-51.7 median at nc=2).  The value is then split greedily
+// (round-and-residual, mc_ops.hpp:286-297) into nc components.
+//
+// B200 mapping: FP64 runs at half the FP32 lane rate (measured 63 vs 119
+// lanes/clk/SM, profiles/pipe_bench.txt), and one compensated FP64 MAD
+// replaces ~32 FP32 error-free ops, so the FP64 pipe is the faster exact
+// path.  Operands are widened once to binary64 (a streaming pass into a
+// per-stream workspace), tiles are staged global->shared with cp.async
+// (LDGSTS, 16-byte chunks, 3-stage ring), and each thread owns a TM x TN
+// block of outputs with interleaved rows (conflict-free 128-bit LDS).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+
+#include "mcf_accum.cuh"
+#include "mcf_runtime.h"
+
+namespace mcfg {
+namespace {
+
+// ---- widening pass: components -> binary64 (optionally summed) --------------------
+
+template <class ST, int NC, bool SUM>
+__global__ void __launch_bounds__(256) k_widen(const ST* __restrict__ in, double* __restrict__ out,
+                                                int64_t elems) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += stride) {
+    if constexpr (SUM) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = NC - 1; c >= 0; --c) s = __dadd_rn(s, to_d<ST>(in[e * NC + c]));
+      out[e] = s;
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) out[e * NC + c] = to_d<ST>(in[e * NC + c]);
+    }
+  }
+}
+
+// ---- cp.async helpers ------------------------------------------------------------------
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---- the tiled kernel ------------------------------------------------------------------
+
+template <int NA, int NB, int BM, int BN, int BK, int TM, int TN>
+struct Tile {
+  static constexpr int kThreads = (BM / TM) * (BN / TN);
+  static constexpr int kStages = 3;
+  static constexpr int kRowA = BK * NA + 2;  // doubles; +16 B staggers rows across banks
+  static constexpr int kRowB = BN * NB;
+  static constexpr int kStageElems = BM * kRowA + BK * kRowB;
+  static constexpr int kSmem = kStages * kStageElems * 8;
+};
+
+// A: (batch, M, K, NA) binary64; B: (batch, K, N, NB) binary64 (b_bstride 0 =
+// broadcast); out: (batch, M, N, NCO) components of type OST.
+// Thread (ty, tx) owns rows ty + i*(BM/TM) and columns tx + j*(BN/TN): a
+// warp's B loads are consecutive doubles (conflict-free), its A loads two
+// broadcast rows 16 B apart in bank space.
+template <class Acc, class OST, int NCO, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), 1)
+    k_mm_fast(const double* __restrict__ A, const double* __restrict__ B, OST* __restrict__ Cout,
+              int64_t M, int64_t N, int64_t K, int64_t a_bstride, int64_t b_bstride,
+              int64_t c_bstride) {
+  constexpr int NA = Acc::kNA, NB = Acc::kNB;
+  using T = Tile<NA, NB, BM, BN, BK, TM, TN>;
+  constexpr int RS = BM / TM;  // row stride between a thread's rows
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int64_t bz = blockIdx.z;
+  A += bz * a_bstride;
+  B += bz * b_bstride;
+  Cout += bz * c_bstride;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int ktiles = (int)((K + BK - 1) / BK);
+
+  auto load_tile = [&](int kt, int slot) {
+    double* As = smem + slot * T::kStageElems;
+    double* Bs = As + BM * T::kRowA;
+    const int64_t k0 = (int64_t)kt * BK;
+    constexpr int kChA = BK * NA / 2;  // 16-byte chunks per A row
+    for (int c = tid; c < BM * kChA; c += T::kThreads) {
+      const int r = c / kChA, q = c % kChA;
+      const int64_t gr = m0 + r;
+      const int64_t ge = k0 * NA + 2 * q;
+      const bool ok = gr < M && ge < K * NA;
+      cp16(As + r * T::kRowA + 2 * q, ok ? A + gr * K * NA + ge : A, ok);
+    }
+    constexpr int kChB = BN * NB / 2;
+    for (int c = tid; c < BK * kChB; c += T::kThreads) {
+      const int r = c / kChB, q = c % kChB;
+      const int64_t gk = k0 + r;
+      const int64_t ge = n0 * NB + 2 * q;
+      const bool ok = gk < K && ge < N * NB;
+      cp16(Bs + r * T::kRowB + 2 * q, ok ? B + gk * N * NB + ge : B, ok);
+    }
+  };
+
+  double acc[TM][TN][Acc::kLv];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int l = 0; l < Acc::kLv; ++l) acc[i][j][l] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < T::kStages - 1; ++s) {
+    if (s < ktiles) load_tile(s, s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_wait<T::kStages - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + T::kStages - 1;
+      if (nk < ktiles) load_tile(nk, nk % T::kStages);
+      cp_commit();
+    }
+    const double* As = smem + (kt % T::kStages) * T::kStageElems;
+    const double* Bs = As + BM * T::kRowA;
+#pragma unroll 1
+    for (int k = 0; k < BK; ++k) {
+      double a[TM][NA], b[TN * NB];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int c = 0; c < NA; ++c) a[i][c] = As[(ty + i * RS) * T::kRowA + k * NA + c];
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int c = 0; c < NB; ++c) b[j * NB + c] = Bs[k * T::kRowB + (tx + j * (BN / TN)) * NB + c];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) Acc::mad(acc[i][j], a[i], b + j * NB);
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t r = m0 + ty + i * RS;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t c = n0 + tx + j * (BN / TN);
+      if (c >= N) continue;
+      split_out<OST, NCO, Acc::kLv>(acc[i][j], Cout + (r * N + c) * NCO);
+    }
+  }
+}
+
+template <class Acc, class OST, int NCO, int BM, int BN, int BK, int TM, int TN>
+mcf_status launch_mm(const double* A, const double* B, void* C, int64_t batch, int64_t M,
+                     int64_t N, int64_t K, int64_t a_bs, int64_t b_bs, int64_t c_bs,
+                     cudaStream_t s) {
+  using T = Tile<Acc::kNA, Acc::kNB, BM, BN, BK, TM, TN>;
+  auto kern = k_mm_fast<Acc, OST, NCO, BM, BN, BK, TM, TN>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem) != cudaSuccess)
+      return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot reserve shared memory");
+    attr = true;
+  }
+  const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)batch);
+  kern<<<grid, T::kThreads, T::kSmem, s>>>(A, B, static_cast<OST*>(C), M, N, K, a_bs, b_bs, c_bs);
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_fast kernel");
+}
+
+template <class ST, int NC, bool SUM>
+mcf_status widen(const void* in, double* out, int64_t elems, cudaStream_t s) {
+  if (elems == 0) return MCF_OK;
+  const int grid = mcfr::grid_for(elems, 256, 8);
+  k_widen<ST, NC, SUM><<<grid, 256, 0, s>>>(static_cast<const ST*>(in), out, elems);
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_fast widen kernel");
+}
+
+// per-(device, stream) binary64 operand workspace
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, std::pair<void*, std::size_t>> g_ws;
+
+double* stream_workspace(std::size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& slot = g_ws[{dev, s}];
+  if (slot.second < bytes) {
+    if (slot.first) {
+      cudaStreamSynchronize(s);
+      cudaFree(slot.first);
+    }
+    slot = {nullptr, 0};
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    slot = {p, bytes};
+  }
+  return static_cast<double*>(slot.first);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+}  // namespace mcfg
+
+// ---- entry points used by the C-ABI (linalg.cu routes MCF_FAST here) -------------------
+
+namespace mcfr {
+
+// FP64-pipe instructions per multiply-add of the kernel a fast call uses
+int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) {
+  using namespace mcfg;
+  if (p == MCF_B32 && !mcmc) return nc == 2 ? AccT2::kOps : nc == 3 ? AccT3::kOps : 0;
+  if (p == MCF_B32 && mcmc) return nc == 2 ? AccM2::kOps : nc == 3 ? AccM3::kOps : 0;
+  return (p == MCF_B16 && mcmc && nc == 3) ? AccH3::kOps : 0;
+}
+
+// MC x Tensor; MCF_ERR_UNSUPPORTED (no message) when no fast instantiation
+// covers the call, so the caller can fall back to the reference-order kernel.
+mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
+                       int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s) {
+  using namespace mcfg;
+  if (p != MCF_B32 || (nc != 2 && nc != 3) || n % 2 != 0 || (k * nc) % 2 != 0)
+    return MCF_ERR_UNSUPPORTED;
+  const int64_t xa = batch * m * k * nc, wb = (w_batched ? batch : 1) * k * n;
+  double* ws = stream_workspace((xa + wb) * sizeof(double) + 256, s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the binary64 workspace");
+  double* xd = ws;
+  double* wd = ws + ((xa + 1) / 2) * 2;  // 16-byte aligned
+  mcf_status st = nc == 2 ? widen<float, 2, false>(x, xd, batch * m * k, s)
+                          : widen<float, 3, false>(x, xd, batch * m * k, s);
+  if (st != MCF_OK) return st;
+  st = widen<float, 1, false>(w, wd, wb, s);
+  if (st != MCF_OK) return st;
+  const int64_t a_bs = m * k * nc, b_bs = w_batched ? k * n : 0, c_bs = m * n * nc;
+  if (nc == 2)
+    return launch_mm<AccT2, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
+  return launch_mm<AccT3, float, 3, 64, 64, 16, 4, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
+}
+
+mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
+                        int64_t n, void* out, cudaStream_t s) {
+  using namespace mcfg;
+  const bool f32 = p == MCF_B32 && nc == 2, f16 = p == MCF_B16 && nc == 3;
+  if ((!f32 && !f16) || n % 2 != 0 || k % 2 != 0) return MCF_ERR_UNSUPPORTED;
+  const int w = f32 ? 2 : 1;  // binary64 words per element after widening
+  const int64_t xa = m * k * w, yb = k * n * w;
+  double* ws = stream_workspace((xa + yb) * sizeof(double) + 256, s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the binary64 workspace");
+  double* xd = ws;
+  double* yd = ws + ((xa + 1) / 2) * 2;
+  mcf_status st;
+  if (f32) {
+    st = widen<float, 2, false>(x, xd, m * k, s);
+    if (st == MCF_OK) st = widen<float, 2, false>(y, yd, k * n, s);
+    if (st != MCF_OK) return st;
+    return launch_mm<AccM2, float, 2, 128, 64, 16, 8, 4>(xd, yd, out, 1, m, n, k, 0, 0, 0, s);
+  }
+  st = widen<__half, 3, true>(x, xd, m * k, s);
+  if (st == MCF_OK) st = widen<__half, 3, true>(y, yd, k * n, s);
+  if (st != MCF_OK) return st;
+  return launch_mm<AccH3, __half, 3, 128, 128, 16, 8, 8>(xd, yd, out, 1, m, n, k, 0, 0, 0, s);
+}
+
+}  // namespace mcfr

@@ -99,22 +99,25 @@ def approx(x):
     return elementwise("approx", x=x)
 
 
-def mm_mcn(x, w):
-    """MC (m,k,nc) x working (k,n), reference-order accumulation."""
+def mm_mcn(x, w, strategy=0, out=None):
+    """MC (m,k,nc) x working (k,n); strategy 0 = reference order (bitwise),
+    2 = FAST (compensated binary64)."""
     x = np.ascontiguousarray(x)
     w = np.ascontiguousarray(w, dtype=x.dtype)
     m, k, nc = x.shape
     n = w.shape[1]
-    out = np.empty((m, n, nc), x.dtype)
-    _check(lib().mcf_h_bmm_mcn(_prec(x), _p(x), nc, _p(w), 1, m, k, n, 0, _p(out)))
+    if out is None:
+        out = np.empty((m, n, nc), x.dtype)
+    _check(lib().mcf_h_bmm_mcn(_prec(x), _p(x), nc, _p(w), 1, m, k, n, 0, _p(out), strategy))
     return out
 
 
-def mm_mcmc(x, y):
+def mm_mcmc(x, y, strategy=0, out=None):
     x = np.ascontiguousarray(x)
     y = np.ascontiguousarray(y, dtype=x.dtype)
     m, k, nc = x.shape
     n = y.shape[1]
-    out = np.empty((m, n, nc), x.dtype)
-    _check(lib().mcf_h_mm_mcmc(_prec(x), _p(x), _p(y), nc, m, k, n, _p(out)))
+    if out is None:
+        out = np.empty((m, n, nc), x.dtype)
+    _check(lib().mcf_h_mm_mcmc(_prec(x), _p(x), _p(y), nc, m, k, n, _p(out), strategy))
     return out

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import torch
 
-from . import B16, B32, B64, PAIRWISE_TREE, SEQUENTIAL, UnsupportedOperation, _check, lib
+from . import B16, B32, B64, FAST, PAIRWISE_TREE, SEQUENTIAL, UnsupportedOperation, _check, lib  # noqa: F401
 
 __all__ = [
     "two_sum", "two_prod", "renormalize", "simple_renorm", "approx", "negate", "grow_expn",
@@ -341,24 +341,27 @@ def addmm_mcn(bias, x, w, alpha=1.0, beta=1.0, plan=None):
     return add_mcn(sb, prod)
 
 
-def mm_mcmc(x, y):
-    """NEW: MC x MC matrix product (recipe B; the reference refuses it)."""
+def mm_mcmc(x, y, plan=None):
+    """NEW: MC x MC matrix product (the reference refuses it, linalg.hpp:159-166).
+    plan SEQUENTIAL = recipe B (bitwise), FAST = compensated binary64."""
     x, y = _c(x), _c(y.to(x.dtype))
     if _rank(x) != 2 or _rank(y) != 2 or x.shape[1] != y.shape[0] or x.shape[-1] != y.shape[-1]:
         raise ValueError(f"mm_mcmc: incompatible shapes {_shape_str(x.shape)} vs {_shape_str(y.shape)}")
     nc = _nc(x)
     m, k, n = x.shape[0], x.shape[1], y.shape[1]
     out = torch.empty((m, n, nc), dtype=x.dtype, device=x.device)
-    _check(lib().mcf_mm_mcmc(_prec(x), _ptr(x), _ptr(y), nc, m, k, n, _ptr(out), _stream()))
+    strategy, _ = _plan(plan)
+    _check(lib().mcf_mm_mcmc(_prec(x), _ptr(x), _ptr(y), nc, m, k, n, _ptr(out), strategy, _stream()))
     return out
 
 
-def dot_mcmc(x, y):
+def dot_mcmc(x, y, plan=None):
     """NEW: batched MC x MC dots, x, y (batch, k, nc)."""
     x, y = _c(x), _c(y.to(x.dtype))
     if x.shape != y.shape or x.dim() != 3:
         raise ValueError(f"dot_mcmc: incompatible shapes {_shape_str(x.shape)} vs {_shape_str(y.shape)}")
     b, k, nc = x.shape
     out = torch.empty((b, nc), dtype=x.dtype, device=x.device)
-    _check(lib().mcf_dot_mcmc(_prec(x), _ptr(x), _ptr(y), nc, b, k, _ptr(out), _stream()))
+    strategy, _ = _plan(plan)
+    _check(lib().mcf_dot_mcmc(_prec(x), _ptr(x), _ptr(y), nc, b, k, _ptr(out), strategy, _stream()))
     return out

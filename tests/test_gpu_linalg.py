@@ -1,0 +1,245 @@
+"""MC contractions on the GPU (linalg.hpp) against the oracle.
+
+Reference-order plans (SEQUENTIAL, PAIRWISE_TREE) run the reference's DotCore
+per output and must be bit-identical to it; MC x MC follows SURVEY 8c recipe
+B bit for bit.  The throughput plan (FAST) uses a different summation and is
+checked against binary128 truth with the tolerance of BASELINE.json's
+north star: median and max relative error each <= 4x the reference's own on
+the same sampled outputs.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from mcgen import DT, assert_bits, random_mc
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_elementwise.npz"))
+
+
+@pytest.fixture(scope="module")
+def gr():
+    import gpu_util
+
+    return gpu_util
+
+
+def wp(rng, shape, bits, lo=-3, hi=3):
+    n = int(np.prod(shape))
+    return (rng.uniform(-1, 1, n) * np.exp2(rng.uniform(lo, hi, n))).astype(DT[bits]).reshape(shape)
+
+
+@pytest.mark.parametrize("bits,nc", [(32, 1), (32, 2), (32, 3), (32, 4), (16, 2), (64, 2), (16, 1), (64, 1)])
+def test_mm_reference_order_bitwise(gr, port, bits, nc):
+    rng = np.random.default_rng(bits * 10 + nc)
+    x = random_mc(rng, 33 * 70, nc, DT[bits], -3, 3).reshape(33, 70, nc)
+    w = wp(rng, (70, 45), bits)
+    assert_bits(gr.run("mm_mcn", x, w), port.mm_mcn(x, w), "mm_mcn")
+    xb = random_mc(rng, 3 * 5 * 9, nc, DT[bits], -3, 3).reshape(3, 5, 9, nc)
+    wb = wp(rng, (3, 9, 4), bits)
+    assert_bits(gr.run("bmm_mcn", xb, wb), port.bmm_mcn(xb, wb), "bmm_mcn")
+    w2 = wp(rng, (9, 4), bits)
+    assert_bits(gr.run("matmul_mcn", xb, w2), port.bmm_mcn(xb, w2), "matmul 3/2")
+    v = wp(rng, (70,), bits)
+    assert_bits(gr.run("mv_mcn", x, v), port.mv_mcn(x, v), "mv_mcn")
+    assert_bits(gr.run("dot_mcn", x[0], v), port.dot_mcn(x[0], v), "dot_mcn")
+
+
+@pytest.mark.parametrize("nc", [1, 2, 3])
+def test_pairwise_tree_bitwise(gr, port, nc):
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(nc)
+    x = random_mc(rng, 8 * 100, nc, np.float32, -3, 3).reshape(8, 100, nc)
+    w = wp(rng, (100, 6), 32)
+    for leaf in (1, 4):
+        got = gr.run("mm_mcn", x, w, plan=(mcf.PAIRWISE_TREE, leaf))
+        assert_bits(got, port.bmm_mcn(x, w, oracle.PAIRWISE_TREE, leaf), f"tree leaf={leaf}")
+
+
+def test_single_component_equals_plain_matmul(gr, port):
+    """T/test_linalg.cpp:297-314: nc=1 mm == matmul2d bitwise."""
+    rng = np.random.default_rng(48)
+    for bits in (16, 32, 64):
+        a = wp(rng, (4, 6), bits, -1, 1)
+        b = wp(rng, (6, 3), bits, -1, 1)
+        got = gr.run("mm_mcn", a[..., None], b)[..., 0]
+        assert_bits(got, port.matmul2d(a, b), f"nc=1 mm b{bits}")
+
+
+def test_golden_contractions(gr):
+    for key in ("b32_nc2", "b32_nc3", "b16_nc3", "b64_nc2", "b32_nc1"):
+        xm, wm, ym = G[f"{key}_mm_x"], G[f"{key}_mm_w"], G[f"{key}_mm_y"]
+        assert_bits(gr.run("mm_mcn", xm, wm), G[f"{key}_mm"], f"{key} mm")
+        import paper_2207_08867_b200 as mcf
+
+        assert_bits(gr.run("mm_mcn", xm, wm, plan=(mcf.PAIRWISE_TREE, 2)), G[f"{key}_mm_tree"], f"{key} tree")
+        assert_bits(gr.run("mm_mcmc", xm, ym), G[f"{key}_mmmc"], f"{key} mm_mcmc")
+
+
+@pytest.mark.parametrize("bits,nc", [(32, 2), (32, 3), (16, 3), (16, 2), (64, 2), (32, 4)])
+def test_mcmc_recipe_b_bitwise(gr, port, bits, nc):
+    rng = np.random.default_rng(7 * nc + bits)
+    lo, hi = (-3, 3) if bits != 16 else (-6, 0)
+    x = random_mc(rng, 20 * 50, nc, DT[bits], lo, hi).reshape(20, 50, nc)
+    y = random_mc(rng, 50 * 12, nc, DT[bits], lo, hi).reshape(50, 12, nc)
+    rows = np.repeat(np.arange(20), 12)
+    cols = np.tile(np.arange(12), 20)
+    assert_bits(gr.run("mm_mcmc", x, y), port.mm_mcmc_sampled(x, y, rows, cols).reshape(20, 12, nc), "mm_mcmc")
+    xd = random_mc(rng, 9 * 300, nc, DT[bits], lo, hi).reshape(9, 300, nc)
+    yd = random_mc(rng, 9 * 300, nc, DT[bits], lo, hi).reshape(9, 300, nc)
+    assert_bits(gr.run("dot_mcmc", xd, yd), port.dot_mcmc(xd, yd), "dot_mcmc")
+
+
+def test_reference_kats(gr):
+    """T/test_linalg.cpp:57-66, 87-98, 114-123."""
+    f = np.float32
+    x = np.zeros((17, 2), f)
+    x[:, 0] = 1
+    d = gr.run("dot_mcn", x, np.ones(17, f))
+    assert d[0] == 17.0 and d[1] == 0.0
+    assert np.all(gr.run("dot_mcn", x, np.zeros(17, f)) == 0)
+    eye = np.zeros((3, 3, 2), f)
+    for i in range(3):
+        eye[i, i, 0] = 1
+    v = np.array([2.0, -1.5, 0.25], f)
+    assert np.array_equal(gr.run("mv_mcn", eye, v)[:, 0], v)
+    import paper_2207_08867_b200 as mcf
+
+    with pytest.raises(ValueError, match=r"\(3,5\).*\(3,2\)"):
+        import torch
+
+        mcf.matmul_mcn(torch.zeros((3, 5, 2), device="cuda"), torch.zeros((3, 2), device="cuda"))
+
+
+# ---- MCF_FAST: tolerance against binary128 truth -----------------------------------
+
+def _relerr_stats(e):
+    e = np.asarray(e, np.float64)
+    return float(np.median(e)), float(np.max(e))
+
+
+def _check_within_4x(gpu_err, ref_err, what):
+    gm, gx = _relerr_stats(gpu_err)
+    rm, rx = _relerr_stats(ref_err)
+    msg = (f"{what}: GPU median 2^{np.log2(max(gm, 1e-300)):.1f} max 2^{np.log2(max(gx, 1e-300)):.1f}; "
+           f"reference median 2^{np.log2(max(rm, 1e-300)):.1f} max 2^{np.log2(max(rx, 1e-300)):.1f}")
+    print(msg)
+    assert gm <= 4 * rm and gx <= 4 * rx, msg
+
+
+def test_fast_mm_mct_nc2_within_reference_error(gr, port):
+    """BASELINE config 2 distribution (A nc=2 split from fp64 U[-1,1], B fp32
+    U[-1,1]) at the full K = 4096, on a 32 x 32 block of outputs."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(2)
+    m, k, n = 32, 4096, 48
+    x = split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    w = rng.uniform(-1, 1, k * n).astype(np.float32).reshape(k, n)
+    got = gr.run("mm_mcn", x, w, plan=mcf.FAST)
+    rows = np.repeat(np.arange(m), n)
+    cols = np.tile(np.arange(n), m)
+    ref = port.mm_mcn_sampled(x, w, rows, cols)
+    gerr = port.relerr_mm_mct(x, w, rows, cols, got.reshape(-1, 2))
+    rerr = port.relerr_mm_mct(x, w, rows, cols, ref)
+    _check_within_4x(gerr, rerr, "mm MC(nc=2) x T, K=4096")
+
+
+def test_fast_mv_nc3_within_reference_error(gr, port):
+    """BASELINE config 1a distribution (nc=3, U(-1,1) 2^U(-8,8)), K = 4096."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import config_values
+
+    rng = np.random.default_rng(3)
+    m, k = 96, 4096
+    x = random_mc(rng, m * k, 3, np.float32).reshape(m, k, 3)
+    v = config_values(rng, k).astype(np.float32)
+    got = gr.run("mv_mcn", x, v, plan=mcf.FAST)
+    rows = np.arange(m)
+    cols = np.zeros(m, np.int64)
+    w = v.reshape(k, 1)
+    ref = port.mm_mcn_sampled(x, w, rows, cols)
+    gerr = port.relerr_mm_mct(x, w, rows, cols, got)
+    rerr = port.relerr_mm_mct(x, w, rows, cols, ref)
+    _check_within_4x(gerr, rerr, "mv MC(nc=3) x T, K=4096")
+
+
+@pytest.mark.parametrize("nc", [2, 3])
+def test_fast_dot_mcmc_within_recipe_b_error(gr, port, nc):
+    """BASELINE config 1b: independent MC x MC dots of length 4096."""
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(4 + nc)
+    b, k = 48, 4096
+    x = random_mc(rng, b * k, nc, np.float32).reshape(b, k, nc)
+    y = random_mc(rng, b * k, nc, np.float32).reshape(b, k, nc)
+    got = gr.run("dot_mcmc", x, y, plan=mcf.FAST)
+    ref = port.dot_mcmc(x, y)
+    # truth: each dot as a 1 x k times k x 1 MC x MC product
+    gerr, rerr = [], []
+    for i in range(b):
+        r0, c0 = np.array([0]), np.array([0])
+        gerr.append(port.relerr_mm_mcmc(x[i:i + 1], y[i].reshape(k, 1, nc), r0, c0, got[i:i + 1])[0])
+        rerr.append(port.relerr_mm_mcmc(x[i:i + 1], y[i].reshape(k, 1, nc), r0, c0, ref[i:i + 1])[0])
+    _check_within_4x(gerr, rerr, f"dot MC x MC nc={nc}")
+
+
+def test_fast_mm_mcmc_fp32_nc2_within_recipe_b_error(gr, port):
+    """BASELINE config 4 (fp32 nc=2 split from fp64 U[-1,1]) on a K=4096 slab."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(6)
+    m, k, n = 16, 4096, 24
+    x = split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    y = split(rng.uniform(-1, 1, k * n), 2, np.float32).reshape(k, n, 2)
+    got = gr.run("mm_mcmc", x, y, plan=mcf.FAST)
+    rows = np.repeat(np.arange(m), n)
+    cols = np.tile(np.arange(n), m)
+    ref = port.mm_mcmc_sampled(x, y, rows, cols)
+    gerr = port.relerr_mm_mcmc(x, y, rows, cols, got.reshape(-1, 2))
+    rerr = port.relerr_mm_mcmc(x, y, rows, cols, ref)
+    _check_within_4x(gerr, rerr, "mm MC x MC fp32 nc=2, K=4096")
+
+
+def test_fast_mm_mcmc_fp16_nc3_within_recipe_b_error(gr, port):
+    """BASELINE config 4 fp16 variant: nc=3 binary16 split from U[-1,1]/64."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(7)
+    m, k, n = 16, 4096, 24
+    x = split(rng.uniform(-1, 1, m * k) / 64, 3, np.float16).reshape(m, k, 3)
+    y = split(rng.uniform(-1, 1, k * n) / 64, 3, np.float16).reshape(k, n, 3)
+    got = gr.run("mm_mcmc", x, y, plan=mcf.FAST)
+    rows = np.repeat(np.arange(m), n)
+    cols = np.tile(np.arange(n), m)
+    ref = port.mm_mcmc_sampled(x, y, rows, cols)
+    gerr = port.relerr_mm_mcmc(x, y, rows, cols, got.reshape(-1, 3))
+    rerr = port.relerr_mm_mcmc(x, y, rows, cols, ref)
+    _check_within_4x(gerr, rerr, "mm MC x MC fp16 nc=3, K=4096")
+
+
+def test_fast_plan_ragged_shapes_and_fallback(gr, port):
+    """Odd shapes exercise the tile edges; shapes without a fast kernel fall
+    back to the reference order (bitwise)."""
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(8)
+    x = random_mc(rng, 77 * 130, 2, np.float32, -2, 2).reshape(77, 130, 2)
+    w = wp(rng, (130, 70), 32, -2, 2)
+    got = gr.run("mm_mcn", x, w, plan=mcf.FAST)
+    ref = port.mm_mcn(x, w)
+    rows = np.repeat(np.arange(77), 70)
+    cols = np.tile(np.arange(70), 77)
+    gerr = port.relerr_mm_mct(x, w, rows, cols, got.reshape(-1, 2))
+    rerr = port.relerr_mm_mct(x, w, rows, cols, ref.reshape(-1, 2))
+    _check_within_4x(gerr, rerr, "ragged mm")
+    # odd n: no fast instantiation -> reference order, bit-identical
+    w3 = wp(rng, (130, 3), 32)
+    assert_bits(gr.run("mm_mcn", x, w3, plan=mcf.FAST), port.mm_mcn(x, w3), "fallback")
