@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the MCF operator hot path on B200 (driver contract).
+
+Headline workload (BASELINE.json metric "MC mm effective GFLOP/s (2MNK/t)"):
+config 2 -- A = 4096 x 4096 MCTensor (nc=2, binary32 components split from
+binary64 U[-1,1]) times B = 4096 x 4096 binary32 U[-1,1], plan MCF_FAST.
+A "step" is one full 4096^3 MC x Tensor product; under torchrun the output
+rows are sharded across ranks (strong scaling, no data-path collective).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+The JSON line carries, besides the contract keys:
+  roofline      the mm kernel against the FP64 FMA pipe (the pipe it runs on),
+                counted in the kernel's own FP64 ops per multiply-add
+  cpu_baseline  the reference's own C++ (oracle/_ref, compiled here from
+                /root/reference) timed on this box's host cores on a bounded
+                sample of the same product
+  e2e           the same metric through the reference-facing host-buffer C-ABI
+                (mcf_h_bmm_mcn) from pinned host memory, copies included
+  elementwise   config 0 operator suite (2^24 elements, fp32 nc=2): GB/s and
+                fraction of measured HBM bandwidth per operator
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = K = N = 4096
+METRIC = "MC mm effective GFLOP/s (2MNK/t)"
+UNIT = "GFLOP/s"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---- clocks during the timed region -------------------------------------------------
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.summary = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if not self.proc:
+            return
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if sm:
+            busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+            self.summary = {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                            "samples": len(sm)}
+
+
+# ---- reference arm ---------------------------------------------------------------
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_sample(a, b, threads):
+    """Time the reference's mm_mcn (oracle/_ref) on `threads` full output rows
+    of the config-2 product, one row per thread; returns (GFLOP/s, seconds,
+    rows, kind)."""
+    import oracle
+
+    rows = max(threads, 1)
+    if oracle.ref_available():
+        ref = oracle.Oracle("ref")
+        t, _ = ref.time_mm_rows(a[:rows], b, rows, threads=threads)
+        kind = "reference"
+    else:  # the reference tree did not compile here: the C port, one thread per row
+        port = oracle.Oracle("port")
+        import concurrent.futures as cf
+
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda r: port.mm_mcn(a[r:r + 1], b), range(rows)))
+        t = time.perf_counter() - t0
+        kind = "port"
+    return 2.0 * rows * K * N / t / 1e9, t, rows, kind
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import paper_2207_08867_b200 as mcf  # noqa: F401  (rng + generators only)
+    from paper_2207_08867_b200 import data
+
+    a, b = data.config2(M, K, N)
+    threads = cpu_threads()
+    for _ in range(args.warmup):
+        reference_sample(a, b, threads)
+    vals, secs = [], []
+    kind = "reference"
+    rows = threads
+    for _ in range(args.steps):
+        v, t, rows, kind = reference_sample(a, b, threads)
+        vals.append(v)
+        secs.append(t)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(secs), 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (reference emulation of b32)",
+        "data": "synthetic",
+        "config": {"workload": "config2: MC(4096x4096, nc=2, fp32) x T(4096x4096, fp32)", "M": M, "K": K, "N": N,
+                   "nc": 2, "sample_rows_per_step": rows},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{rows} full output rows (x {K} x {N}) of the 4096^3 product per step, one row per thread"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm ---------------------------------------------------------------------
+
+def elementwise_suite(torch, mcf, hbm_gbs):
+    """Config 0 (2^24 elements, fp32 nc=2): device time per operator."""
+    from paper_2207_08867_b200 import data
+
+    n = 1 << 24
+    x, y, yd, v, xe = (torch.from_numpy(t).cuda() for t in data.config0(n))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ops = {
+        "grow_expn": (lambda: mcf.grow_expn(x, v), 20), "scaling_n": (lambda: mcf.scaling_n(x, v), 20),
+        "div_n": (lambda: mcf.div_n(v, yd), 20), "add_mcn": (lambda: mcf.add_mcn(x, y), 24),
+        "mul_mcn": (lambda: mcf.mul_mcn(x, yd), 24), "div_mcn": (lambda: mcf.div_mcn(x, yd), 24),
+        "exp_mcn": (lambda: mcf.exp_mcn(xe), 16), "square_mcn": (lambda: mcf.square_mcn(x), 16),
+    }
+    res = {}
+    for name, (f, bpe) in ops.items():
+        for _ in range(3):
+            f()
+        ts = []
+        for _ in range(5):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        gbs = bpe * n / ms / 1e6
+        res[name] = {"us": round(ms * 1e3, 1), "GB/s": round(gbs, 1), "frac_hbm": round(gbs / hbm_gbs, 3),
+                     "bytes_per_elem": bpe}
+    del x, y, yd, v, xe, flush
+    return res
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2207_08867_b200 as mcf
+    from paper_2207_08867_b200 import data
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6446.6))
+
+    # inputs: generated on the host from the reference's Rng, resident in HBM
+    a_h, b_h = data.config2(M, K, N)
+    r0, r1 = rank * M // world, (rank + 1) * M // world
+    rows = r1 - r0
+    a = torch.from_numpy(a_h[r0:r1]).cuda()
+    b = torch.from_numpy(b_h).cuda()
+    out = torch.empty((rows, N, 2), dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        rc = lib.mcf_bmm_mcn(mcf.B32, a.data_ptr(), 2, b.data_ptr(), 1, rows, K, N, 0, out.data_ptr(),
+                             mcf.FAST, 1, stream.cuda_stream)
+        if rc != 0:
+            raise RuntimeError(lib.mcf_last_error().decode())
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    mcf.reset_launch_count()
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for e0, e1 in ev:
+            flush.zero_()  # L2 flush between steps (outside the event pair)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = mcf.launch_count()
+    times = [e0.elapsed_time(e1) for e0, e1 in ev]
+    ms = sum(times) / len(times)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = 2.0 * M * N * K / (ms * 1e-3) / 1e9
+
+    # roofline: the mm kernel on the FP64 FMA pipe, counted in its own ops/MAD
+    ops_per_mad = lib.mcf_fast_ops_per_mad(0, mcf.B32, 2)
+    import ctypes as C
+
+    f64 = C.c_double(0.0)
+    f32 = C.c_double(0.0)
+    lib.mcf_probe_pipe_rates(C.byref(f64), C.byref(f32))
+    achieved = ops_per_mad * rows * N * K / (ms * 1e-3) / 1e12
+    peak64 = f64.value / 1e12
+
+    # e2e through the host-buffer C-ABI, pinned buffers, copies inside the timed region
+    a_pin = torch.from_numpy(a_h[r0:r1]).pin_memory()
+    b_pin = torch.from_numpy(b_h).pin_memory()
+    o_pin = torch.empty((rows, N, 2), dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, args.steps // 2)
+
+    def e2e_step():
+        rc = lib.mcf_h_bmm_mcn(mcf.B32, a_pin.data_ptr(), 2, b_pin.data_ptr(), 1, rows, K, N, 0,
+                               o_pin.data_ptr(), mcf.FAST)
+        if rc != 0:
+            raise RuntimeError(lib.mcf_last_error().decode())
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = 2.0 * M * N * K / e2e_s / 1e9
+
+    ew = None
+    cpu = None
+    if rank == 0 and world == 1:
+        ew = elementwise_suite(torch, mcf, hbm)
+        gf, t, nrows, kind = reference_sample(a_h, b_h, cpu_threads())
+        cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cpu_threads(), "kind": kind,
+               "sample": f"{nrows} full output rows of the 4096^3 product, one row per host thread ({t:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 (compensated, on fp32 nc=2 components)", "data": "synthetic",
+            "config": {"workload": "config2: MC(4096x4096, nc=2, fp32) x T(4096x4096, fp32)", "M": M, "K": K,
+                       "N": N, "nc": 2, "plan": "MCF_FAST", "parallelism": f"rows/{world}" if world > 1 else "1 GPU",
+                       "l2": "256 MiB buffer written between timed steps"},
+            "roofline": {"bound": "fp64_fma_pipe", "achieved": round(achieved, 3), "peak": round(peak64, 3),
+                         "unit": "TFLOP/s", "frac": round(achieved / peak64, 3) if peak64 else None,
+                         "traffic": None, "ops_per_mad": ops_per_mad,
+                         "peak_source": "measured in this run by mcf_probe_pipe_rates (DFMA chains, all SMs)"},
+            "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": int(a_pin.numel() * 4 + b_pin.numel() * 4),
+                    "d2h_bytes_per_step": int(o_pin.numel() * 4)},
+            "gpu_launches": launches,
+            "clocks": clk.summary,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        if ew:
+            line["elementwise"] = {"config": "config0: 2^24 elements, fp32 nc=2, bit-exact vs reference",
+                                   "hbm_peak_gbs": hbm, "ops": ew}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

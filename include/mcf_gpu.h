@@ -68,6 +68,9 @@ const char* mcf_last_error(void);
 /* kernels launched by this thread since the last reset (instrumentation) */
 int64_t mcf_launch_count(void);
 void mcf_reset_launch_count(void);
+/* measured FMA instruction rates (lane-ops/s, whole GPU) of the FP64 and FP32
+ * pipes on the current device: the roofline denominators of the contractions */
+int mcf_probe_pipe_rates(double* fp64_ops_per_s, double* fp32_ops_per_s);
 
 /* ---- error-free transforms, array forms  [replaces eft.hpp:89-111] -------- */
 mcf_status mcf_two_sum(mcf_prec p, const void* a, const void* b, void* s, void* e, int64_t n,

@@ -67,6 +67,7 @@ _SIGS = {
     "mcf_h_bmm_mcn": [_int, _p, _int, _p, _i64, _i64, _i64, _i64, _int, _p, _int],
     "mcf_h_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _int],
     "mcf_fast_ops_per_mad": [_int, _int, _int],
+    "mcf_probe_pipe_rates": [_p, _p],
 }
 
 

@@ -232,8 +232,61 @@ double* stream_workspace(std::size_t bytes, cudaStream_t s) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// pipe-rate probe: 8 independent FMA chains per thread, all SMs, 8 CTAs/SM
+template <bool F64>
+__global__ void __launch_bounds__(256) k_probe(double* out, int iters, double a) {
+  double d[8];
+  float f[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    d[i] = a + i + threadIdx.x;
+    f[i] = (float)d[i];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if constexpr (F64) d[i] = __fma_rn(d[i], a, d[(i + 1) & 7]);
+      else f[i] = __fmaf_rn(f[i], (float)a, f[(i + 1) & 7]);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += d[i] + f[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 }  // namespace
 }  // namespace mcfg
+
+extern "C" int mcf_probe_pipe_rates(double* fp64_ops_per_s, double* fp32_ops_per_s) {
+  using namespace mcfg;
+  const int sms = mcfr::sm_count(), blocks = sms * 8, threads = 256, iters = 2048;
+  double* buf = nullptr;
+  if (cudaMalloc(&buf, (size_t)blocks * threads * sizeof(double)) != cudaSuccess) return 1;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double rates[2] = {0, 0};
+  for (int kind = 0; kind < 2; ++kind) {
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      if (kind == 0) k_probe<true><<<blocks, threads>>>(buf, iters, 0.999999);
+      else k_probe<false><<<blocks, threads>>>(buf, iters, 0.999999);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double r = (double)blocks * threads * iters * 8 / (ms * 1e-3);
+      if (r > rates[kind]) rates[kind] = r;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  if (fp64_ops_per_s) *fp64_ops_per_s = rates[0];
+  if (fp32_ops_per_s) *fp32_ops_per_s = rates[1];
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
 
 // ---- entry points used by the C-ABI (linalg.cu routes MCF_FAST here) -------------------
 
