@@ -143,6 +143,21 @@ __device__ __noinline__ void run_lit(const RT<P>* x, const RT<P>* y, RT<P> v, RT
   else if constexpr (OP == kSimple) lit::simple_renorm<P>(x, nc, o, onc);
 }
 
+// one element through the literal path, operands read from memory (global or
+// shared) and the result written to memory: nothing of the caller's register
+// state escapes to the stack on the fast path
+template <int OP, class P>
+__device__ __noinline__ void lit_element(const ST<P>* xe, const ST<P>* ye, RT<P> v, ST<P>* oe, int nc,
+                                         int onc) {
+  RT<P> xa[lit::kMaxNc], ya[lit::kMaxNc], oa[lit::kMaxNc + 1];
+  for (int c = 0; c < nc; ++c) {
+    xa[c] = P::ld(xe[c]);
+    ya[c] = ye ? P::ld(ye[c]) : RT<P>(0);
+  }
+  run_lit<OP, P>(xa, ya, v, oa, nc, onc);
+  for (int c = 0; c < onc; ++c) oe[c] = P::sv(oa[c]);
+}
+
 // v[e % vn]: vmode 0 = per-element (vn == numel), 1 = scalar, 2 = general suffix
 template <class P>
 __device__ __forceinline__ RT<P> v_at(const ST<P>* v, int64_t vn, int vmode, int64_t e) {
@@ -182,7 +197,9 @@ __global__ void __launch_bounds__(kThreads) k_fast(const ST<P>* __restrict__ x,
       }
     }
   };
-  auto compute = [&](const Frag& f, ST<P> (&os)[EPT * ONC], int count) {
+  // returns a mask of elements whose fast path declined (re-run by redo())
+  auto compute = [&](const Frag& f, ST<P> (&os)[EPT * ONC], int count) -> unsigned {
+    unsigned bail = 0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       if (i >= count) break;
@@ -193,10 +210,20 @@ __global__ void __launch_bounds__(kThreads) k_fast(const ST<P>* __restrict__ x,
         ya[c] = kY ? P::ld(f.ys[i * NC + c]) : RT<P>(0);
       }
       const RT<P> vv = kV ? f.vs[i] : RT<P>(0);
-      if (!run_fast<OP, P, NC, ONC>(xa, ya, vv, oa)) run_lit<OP, P>(xa, ya, vv, oa, NC, ONC);
+      if (!run_fast<OP, P, NC, ONC>(xa, ya, vv, oa)) bail |= 1u << i;
 #pragma unroll
       for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
     }
+    return bail;
+  };
+  // literal re-run of declined elements straight from/to global memory, after
+  // the vector store (same thread, later store wins)
+  auto redo = [&](unsigned bail, int64_t e0, const Frag& f) {
+#pragma unroll 1
+    for (int i = 0; i < EPT; ++i)
+      if (bail >> i & 1u)
+        lit_element<OP, P>(x + (e0 + i) * NC, kY ? y + (e0 + i) * NC : nullptr, kV ? f.vs[i] : RT<P>(0),
+                           out + (e0 + i) * ONC, NC, ONC);
   };
   const int64_t groups = numel / EPT;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -209,8 +236,9 @@ __global__ void __launch_bounds__(kThreads) k_fast(const ST<P>* __restrict__ x,
     const bool more = g + stride < groups;
     if (more) load(nxt, (g + stride) * EPT);
     ST<P> os[EPT * ONC];
-    compute(cur, os, EPT);
+    const unsigned bail = compute(cur, os, EPT);
     store_stream<ST<P>, EPT * ONC>(out + g * EPT * ONC, os);
+    if (bail) redo(bail, g * EPT, cur);
     if (more) cur = nxt;
   }
   // ragged tail (< EPT elements): one thread, scalar IO
@@ -229,10 +257,175 @@ __global__ void __launch_bounds__(kThreads) k_fast(const ST<P>* __restrict__ x,
       if constexpr (kV) f.vs[i] = in ? v_at<P>(v, vn, vmode, e0 + i) : RT<P>(0);
     }
     ST<P> os[EPT * ONC];
-    compute(f, os, cnt);
+    const unsigned bail = compute(f, os, cnt);
     for (int i = 0; i < cnt; ++i)
 #pragma unroll
       for (int c = 0; c < ONC; ++c) out[(e0 + i) * ONC + c] = os[i * ONC + c];
+    if (bail) redo(bail, e0, f);
+  }
+}
+
+// ---- TMA-staged kernel (bulk copies into a shared-memory ring) ---------------
+//
+// One persistent CTA per SM.  A producer warp streams whole tiles of every
+// operand into a kStages-deep ring with cp.async.bulk (TMA, 1-D), completion
+// tracked by mbarrier transaction counts; 16 consumer warps read their
+// elements from shared memory (LDS.128), run the same register fast path and
+// store with 128-bit streaming stores.  Bytes in flight per SM are set by the
+// ring (kStages x ~40 KiB), not by registers, which keeps HBM busy while the
+// consumers spend their issue slots on the operator itself.
+
+namespace tma {
+
+constexpr int kConsumerWarps = 16;
+constexpr int kCtasPerSm = 2;  // two rings per SM: 32 consumer warps hide FP latency
+constexpr int kSmemBudget = 100 * 1024;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// the suspend-time hint parks the waiting warp instead of spinning on the
+// barrier (spinning costs issue slots the computing warps need)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class P, int NC, int OP>
+struct Geo {
+  static constexpr int EPT = ept_for<P, NC>();
+  static constexpr int kThreads = kConsumerWarps * 32;
+  static constexpr int kRound = kThreads * EPT;                 // elements per round
+  static constexpr int kRounds = 1;
+  static constexpr int kTile = kRound * kRounds;                // elements per tile
+  static constexpr bool kY = OpTraits<OP>::kY, kV = OpTraits<OP>::kV;
+  static constexpr int kXBytes = kTile * NC * (int)sizeof(typename P::st);
+  static constexpr int kYBytes = kY ? kXBytes : 0;
+  static constexpr int kVBytes = kV ? kTile * (int)sizeof(typename P::st) : 0;
+  static constexpr int kStageBytes = kXBytes + kYBytes + kVBytes;
+  static constexpr int kFit = kSmemBudget / kStageBytes;
+  static constexpr int kStages = kFit >= 8 ? 8 : (kFit >= 4 ? 4 : 2);  // power of two: cheap ring index
+  static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
+};
+
+}  // namespace tma
+
+// vmode here is 0 (v per element) or 1 (scalar v); `tiles` full tiles only
+template <int OP, class P, int NC, int ONC>
+__global__ void __launch_bounds__(tma::kConsumerWarps * 32 + 32, tma::kCtasPerSm)
+    k_tma(const ST<P>* __restrict__ x, const ST<P>* __restrict__ y, const ST<P>* __restrict__ v,
+          int vmode, ST<P>* __restrict__ out, int64_t tiles) {
+  using G = tma::Geo<P, NC, OP>;
+  constexpr int EPT = G::EPT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int S = G::kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * G::kStageBytes);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], tma::kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == tma::kConsumerWarps) {  // producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int s = it % S;
+        const unsigned ph = (unsigned)(it / S) & 1u;
+        tma::mbar_wait(&empty[s], ph ^ 1u);
+        unsigned char* st = smem + s * G::kStageBytes;
+        tma::mbar_expect_tx(&full[s], G::kStageBytes);
+        const int64_t e0 = t * G::kTile;
+        tma::bulk_g2s(st, x + e0 * NC, G::kXBytes, &full[s]);
+        if constexpr (G::kY) tma::bulk_g2s(st + G::kXBytes, y + e0 * NC, G::kYBytes, &full[s]);
+        if constexpr (G::kV) tma::bulk_g2s(st + G::kXBytes + G::kYBytes, v + e0, G::kVBytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  RT<P> vscalar = RT<P>(0);
+  if constexpr (G::kV) {
+    if (vmode == 1) vscalar = P::ld(v[0]);
+  }
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    const int s = it % S;
+    const unsigned ph = (unsigned)(it / S) & 1u;
+    tma::mbar_wait(&full[s], ph);
+    const unsigned char* st = smem + s * G::kStageBytes;
+    const ST<P>* xs_s = reinterpret_cast<const ST<P>*>(st);
+    const ST<P>* ys_s = reinterpret_cast<const ST<P>*>(st + G::kXBytes);
+    const ST<P>* vs_s = reinterpret_cast<const ST<P>*>(st + G::kXBytes + G::kYBytes);
+#pragma unroll
+    for (int r = 0; r < G::kRounds; ++r) {
+      const int l0 = r * G::kRound + threadIdx.x * EPT;  // element offset inside the tile
+      ST<P> xs[EPT * NC], ys[G::kY ? EPT * NC : 1], vv[G::kV ? EPT : 1];
+      memcpy(xs, xs_s + l0 * NC, sizeof(xs));
+      if constexpr (G::kY) memcpy(ys, ys_s + l0 * NC, sizeof(ys));
+      if constexpr (G::kV) {
+        if (vmode == 0) memcpy(vv, vs_s + l0, sizeof(vv));
+      }
+      ST<P> os[EPT * ONC];
+      unsigned bail = 0;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        RT<P> xa[NC], ya[NC], oa[ONC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          xa[c] = P::ld(xs[i * NC + c]);
+          ya[c] = G::kY ? P::ld(ys[i * NC + c]) : RT<P>(0);
+        }
+        RT<P> ve = RT<P>(0);
+        if constexpr (G::kV) ve = vmode == 0 ? P::ld(vv[i]) : vscalar;
+        if (!run_fast<OP, P, NC, ONC>(xa, ya, ve, oa)) bail |= 1u << i;
+#pragma unroll
+        for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
+      }
+      ST<P>* og = out + (t * G::kTile + l0) * ONC;
+      store_stream<ST<P>, EPT * ONC>(og, os);
+      if (bail) {  // literal re-run from the staged operands (stage not yet released)
+#pragma unroll 1
+        for (int i = 0; i < EPT; ++i)
+          if (bail >> i & 1u) {
+            RT<P> ve = RT<P>(0);
+            if constexpr (G::kV) ve = vmode == 0 ? P::ld(vs_s[l0 + i]) : vscalar;
+            lit_element<OP, P>(xs_s + (l0 + i) * NC, G::kY ? ys_s + (l0 + i) * NC : nullptr, ve,
+                               og + i * ONC, NC, ONC);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[s]);
   }
 }
 
@@ -343,13 +536,46 @@ int vmode_of(int64_t vn, int64_t numel) { return vn == numel ? 0 : (vn == 1 ? 1 
 
 template <int OP, class P, int NC, int ONC>
 mcf_status launch_fast(const Args& a) {
+  using G = tma::Geo<P, NC, OP>;
+  const int vmode = vmode_of(a.vn, a.numel);
+  const ST<P>* x = static_cast<const ST<P>*>(a.x);
+  const ST<P>* y = static_cast<const ST<P>*>(a.y);
+  const ST<P>* v = static_cast<const ST<P>*>(a.v);
+  ST<P>* out = static_cast<ST<P>*>(a.out);
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  static const bool tma_on = [] {
+    const char* e = getenv("MCF_EW_TMA");
+    return !(e && e[0] == '0');
+  }();
+  int64_t done = 0;
+  const int64_t tiles = a.numel / G::kTile;
+  if (tma_on && vmode != 2 && tiles > 0 && al16(x) && (!G::kY || al16(y)) && (!G::kV || vmode != 0 || al16(v)) &&
+      al16(out) && ((int64_t)G::kTile * ONC * sizeof(ST<P>)) % 16 == 0) {
+    auto kt = k_tma<OP, P, NC, ONC>;
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem) != cudaSuccess)
+        return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot reserve shared memory for the TMA ring");
+      attr = true;
+    }
+    const int64_t slots = (int64_t)mcfr::sm_count() * tma::kCtasPerSm;
+    const int grid = (int)(tiles < slots ? tiles : slots);
+    kt<<<grid, tma::kConsumerWarps * 32 + 32, G::kSmem, a.stream>>>(x, y, v, vmode, out, tiles);
+    mcfr::note_launch();
+    const mcf_status st = mcfr::check_launch("mcf elementwise kernel (TMA)");
+    if (st != MCF_OK) return st;
+    done = tiles * G::kTile;
+    if (done == a.numel) return MCF_OK;
+  }
+  // remaining elements (or everything): register-pipelined grid-stride kernel
+  const int64_t rest = a.numel - done;
   auto k = k_fast<OP, P, NC, ONC>;
   static const int occ = per_sm(k);
   constexpr int EPT = ept_for<P, NC>();
-  const int grid = mcfr::grid_for((a.numel + EPT - 1) / EPT, kThreads, occ);
-  k<<<grid, kThreads, 0, a.stream>>>(static_cast<const ST<P>*>(a.x), static_cast<const ST<P>*>(a.y),
-                                      static_cast<const ST<P>*>(a.v), a.vn, vmode_of(a.vn, a.numel),
-                                      static_cast<ST<P>*>(a.out), a.numel);
+  const int grid = mcfr::grid_for((rest + EPT - 1) / EPT, kThreads, occ);
+  k<<<grid, kThreads, 0, a.stream>>>(x + done * NC, G::kY ? y + done * NC : y,
+                                      (G::kV && vmode == 0) ? v + done : v, vmode == 0 ? rest : a.vn, vmode,
+                                      out + done * ONC, rest);
   mcfr::note_launch();
   return mcfr::check_launch("mcf elementwise kernel");
 }

@@ -68,15 +68,37 @@ __device__ __forceinline__ bool sweep_once(RT<P> (&h)[N]) {
   return changed;
 }
 
-// repeated sweeps until one leaves the sequence unchanged (fully unrolled:
-// no loop counter, one early exit per sweep)
+// the same sweep without the change test
 template <class P, int N>
+__device__ __forceinline__ void sweep_blind(RT<P> (&h)[N]) {
+  RT<P> q = h[N - 1];
+#pragma unroll
+  for (int i = N - 2; i >= 0; --i) {
+    RT<P> s, e;
+    two_sum<P>(h[i], q, s, e);
+    h[i + 1] = e;
+    q = s;
+  }
+  h[0] = q;
+}
+
+// repeated sweeps until one leaves the sequence unchanged (fully unrolled:
+// no loop counter, one early exit per sweep).  The first PU sweeps skip the
+// change test: a sweep over a compressed finite sequence is the identity on
+// its nonzero subsequence, and no pass before the 7th can hit the reference's
+// cap, so PU <= 6 blind sweeps followed by tested ones give the reference's
+// result.  PU is chosen per operator from the measured pass distribution
+// (the warp pays for its slowest lane).
+template <class P, int N, int PU = 0>
 __device__ __forceinline__ bool sweeps(RT<P> (&h)[N]) {
+  static_assert(PU < kSafeSweeps, "blind sweeps must stay below the pass cap");
   if constexpr (N < 2) {
     return true;
   } else {
 #pragma unroll
-    for (int pass = 0; pass < kSafeSweeps; ++pass)
+    for (int pass = 0; pass < PU; ++pass) sweep_blind<P, N>(h);
+#pragma unroll
+    for (int pass = PU; pass < kSafeSweeps; ++pass)
       if (!sweep_once<P, N>(h)) return true;
     return false;
   }
@@ -96,13 +118,48 @@ __device__ __forceinline__ void compact(const RT<P> (&h)[N], RT<P> (&out)[R]) {
   }
 }
 
-// renorm_kernel(h, N, out, R); PRE leading terms are known to be ordered
-template <class P, int N, int R, int PRE = 1>
+// One backward scan that both compacts (first R nonzeros, +0 padded) and
+// evaluates the reference's is_compressed over the nonzero subsequence:
+// out[0] always holds the nearest nonzero below position i, i.e. the
+// successor the reference compares h[i] with.
+template <class P, int N, int R>
+__device__ __forceinline__ bool scan(const RT<P> (&h)[N], RT<P> (&out)[R]) {
+  bool comp = true;
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = RT<P>(0);
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    const bool nz = h[i] != RT<P>(0);
+    if (i < N - 1) comp &= !nz | (P::add(h[i], out[0]) == h[i]);
+#pragma unroll
+    for (int r = R - 1; r > 0; --r) out[r] = nz ? out[r - 1] : out[r];
+    out[0] = nz ? h[i] : out[0];
+  }
+  return comp;
+}
+
+// renorm_kernel(h, N, out, R); PRE leading terms are known to be ordered.
+// PU blind sweeps (see sweeps()), then scan; while the scan finds the
+// sequence not compressed, one more sweep (a real reference pass: pass
+// index PU + extra < 6 keeps it below the cap) and scan again.
+template <class P, int N, int R, int PRE = 1, int PU = 0>
 __device__ __forceinline__ bool renorm(RT<P> (&h)[N], RT<P> (&out)[R]) {
+  static_assert(PU < kSafeSweeps - 1, "blind sweeps must stay below the pass cap");
   sort_net<P, N, PRE>(h);
-  const bool ok = sweeps<P, N>(h);
-  compact<P, N, R>(h, out);
-  return ok && P::finite(out[0]);
+  if constexpr (N >= 2) {
+#pragma unroll
+    for (int pass = 0; pass < PU; ++pass) sweep_blind<P, N>(h);
+  }
+  bool comp = scan<P, N, R>(h, out);
+  if constexpr (N >= 2) {
+#pragma unroll 1
+    for (int extra = PU; !comp; ++extra) {
+      if (extra >= kSafeSweeps - 1) return false;  // a 7th pass could hit the cap: literal path
+      sweep_blind<P, N>(h);
+      comp = scan<P, N, R>(h, out);
+    }
+  }
+  return P::finite(out[0]);
 }
 
 template <class P, int NC>
@@ -134,7 +191,8 @@ __device__ __forceinline__ bool grow(const RT<P> (&x)[NC], RT<P> v, RT<P> (&out)
   // renorm_kernel(h, nc+1, out, nc) otherwise.  The two agree whenever the
   // ladder is compressed (compressed => strictly magnitude-ordered => the
   // sort is the identity and the pass loop never runs), so renorm always.
-  return renorm<P, NC + 1, NC>(h, out);
+  // (config 0: <= 2 passes, warp maximum 1 or 2 -> one blind sweep)
+  return renorm<P, NC + 1, NC, 1, 1>(h, out);
 }
 
 // mc_ops.hpp:143-158
@@ -163,13 +221,13 @@ __device__ __forceinline__ bool scale(const RT<P> (&x)[NC], RT<P> v, RT<P> (&out
   } else {
     RT<P> st[2 * NC];
     scale_raw<P, NC>(x, v, st);
-    return renorm<P, 2 * NC, ONC>(st, out);
+    return renorm<P, 2 * NC, ONC, 1, 1>(st, out);  // config 0: <= 2 passes
   }
 }
 
 // mc_ops.hpp:173-184 for ordered operands: the magnitude merge with x winning
 // ties equals the stable sort of the concatenation x ++ y.
-template <class P, int NC, int ONC>
+template <class P, int NC, int ONC, int PU = 2>
 __device__ __forceinline__ bool add_ordered(const RT<P> (&x)[NC], const RT<P> (&y)[NC],
                                             RT<P> (&out)[ONC]) {
   RT<P> h[2 * NC];
@@ -178,14 +236,15 @@ __device__ __forceinline__ bool add_ordered(const RT<P> (&x)[NC], const RT<P> (&
     h[i] = x[i];
     h[NC + i] = y[i];
   }
-  return renorm<P, 2 * NC, ONC, NC>(h, out);
+  return renorm<P, 2 * NC, ONC, NC, PU>(h, out);
 }
 
 template <class P, int NC>
 __device__ __forceinline__ bool add(const RT<P> (&x)[NC], const RT<P> (&y)[NC],
                                     RT<P> (&out)[NC]) {
   const bool ord = ordered<P, NC>(x) & ordered<P, NC>(y);
-  return add_ordered<P, NC, NC>(x, y, out) && ord;
+  // config 0: 1-3 passes, the warp maximum is 3 for 99.7% of warps
+  return add_ordered<P, NC, NC, 3>(x, y, out) && ord;
 }
 
 // mc_ops.hpp:188-207  long division, nc digits + 1 guard digit
@@ -206,10 +265,10 @@ __device__ __forceinline__ bool div(const RT<P> (&x)[NC], const RT<P> (&y)[NC],
       if (d == NC) break;
       RT<P> st[2 * NC], sc[NC];
       scale_raw<P, NC>(y, -q[d], st);
-      ok &= renorm<P, 2 * NC, NC>(st, sc);
-      ok &= add_ordered<P, NC, NC>(r, sc, r);  // both are renorm outputs: ordered
+      ok &= renorm<P, 2 * NC, NC, 1, 1>(st, sc);
+      ok &= add_ordered<P, NC, NC, 2>(r, sc, r);  // both are renorm outputs: ordered
     }
-    ok &= renorm<P, NC + 1, NC>(q, out);
+    ok &= renorm<P, NC + 1, NC, 1, 1>(q, out);
     return ok;
   }
 }
@@ -267,7 +326,7 @@ __device__ __forceinline__ bool mul_slow(const RT<P> (&x)[NC], const RT<P> (&y)[
       }
 #pragma unroll
     for (int i = 1; i < NC; ++i) h[m++] = P::mul(x[i], y[NC - i]);
-    return renorm<P, mul_slow_terms(NC), NC>(h, out);
+    return renorm<P, mul_slow_terms(NC), NC, 1, 2>(h, out);
   }
 }
 
@@ -296,7 +355,7 @@ __device__ __forceinline__ bool square(const RT<P> (&x)[NC], RT<P> (&out)[NC]) {
       const RT<P> p = P::mul(x[i], x[j]);
       h[m++] = i == j ? p : P::twice(p);
     }
-    return renorm<P, square_terms(NC), NC>(h, out);
+    return renorm<P, square_terms(NC), NC, 1, 3>(h, out);  // config 0: warp max 3 passes
   }
 }
 
