@@ -1,0 +1,276 @@
+// mcf_gpu.hpp -- the reference's operator API, served by the B200 library.
+//
+// Drop-in for the MCF operator layer of the reference
+// (proj/include/mcfloat/mc_ops.hpp and linalg.hpp): the same function names,
+// argument types (mcf::MCTensor<P>, mcf::NdArray, mcf::ReductionPlan) and
+// exceptions, in namespace mcf::gpu.  Include it after the reference headers
+// (it uses the reference's own value types and validation helpers) and link
+// libmcf_b200.so; INTEGRATION.md shows the two-line switch.
+//
+// Values cross the boundary exactly: a component of MCTensor<P> is a binary64
+// holding a P value, converted to/from P's storage without rounding
+// (B16 through the reference's own to_bits/from_bits, precision.hpp:128-161).
+// Results of the elementwise operators are bit-identical to the reference's;
+// contractions use the reference order by default (bit-identical) and the
+// FP64-pipe plan when plan.strategy is kFast (see mcf_gpu.h).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "mcf_gpu.h"
+#include "mcfloat/linalg.hpp"
+#include "mcfloat/mc_ops.hpp"
+
+namespace mcf {
+namespace gpu {
+
+// ReductionPlan extension: the GPU-order plan (mcf_gpu.h MCF_FAST)
+inline constexpr int kFastPlan = MCF_FAST;
+
+namespace detail {
+
+template <class P>
+struct Store;
+template <>
+struct Store<B16> {
+  using T = std::uint16_t;
+  static constexpr mcf_prec kPrec = MCF_B16;
+  static T put(double v) { return B16::to_bits(v); }
+  static double get(T b) { return B16::from_bits(b); }
+};
+template <>
+struct Store<B32> {
+  using T = float;
+  static constexpr mcf_prec kPrec = MCF_B32;
+  static T put(double v) { return static_cast<float>(v); }
+  static double get(T b) { return b; }
+};
+template <>
+struct Store<B64> {
+  using T = double;
+  static constexpr mcf_prec kPrec = MCF_B64;
+  static T put(double v) { return v; }
+  static double get(T b) { return b; }
+};
+
+template <class P>
+std::vector<typename Store<P>::T> pack(const std::vector<double>& v) {
+  std::vector<typename Store<P>::T> out(v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) out[i] = Store<P>::put(v[i]);
+  return out;
+}
+
+template <class P>
+void unpack(const std::vector<typename Store<P>::T>& s, std::vector<double>& v) {
+  v.resize(s.size());
+  for (std::size_t i = 0; i < s.size(); ++i) v[i] = Store<P>::get(s[i]);
+}
+
+// status -> the reference's exception types and messages
+inline void check(mcf_status st) {
+  if (st == MCF_OK) return;
+  const std::string msg = mcf_last_error();
+  if (st == MCF_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (st == MCF_ERR_UNSUPPORTED) throw unsupported_operation(msg);
+  throw std::runtime_error("mcf gpu: " + msg);
+}
+
+// working-precision operand rounded into P (the reference rounds v where it
+// reads it, e.g. div_n's P::round(v[e % vn]) at mc_ops.hpp:502)
+template <class P>
+std::vector<typename Store<P>::T> pack_wp(const NdArray& v) {
+  std::vector<typename Store<P>::T> out(v.numel());
+  for (std::size_t i = 0; i < v.numel(); ++i) out[i] = Store<P>::put(P::round(v[i]));
+  return out;
+}
+
+template <class P>
+MCTensor<P> elementwise(const char* op, const MCTensor<P>* x, const MCTensor<P>* y,
+                        const NdArray* v, Shape shape, int out_nc) {
+  using S = Store<P>;
+  std::vector<typename S::T> xs, ys, vs;
+  if (x) xs = pack<P>(x->raw());
+  if (y) ys = pack<P>(y->raw());
+  if (v) vs = pack_wp<P>(*v);
+  const std::size_t numel = shape_numel(shape);
+  std::vector<typename S::T> os(numel * out_nc);
+  check(mcf_h_elementwise(op, S::kPrec, x ? xs.data() : nullptr, x ? x->nc() : 0,
+                          y ? ys.data() : nullptr, y ? y->nc() : 0, v ? vs.data() : nullptr,
+                          v ? static_cast<int64_t>(v->numel()) : 1, os.data(),
+                          static_cast<int64_t>(numel)));
+  MCTensor<P> out(std::move(shape), out_nc);
+  unpack<P>(os, out.raw());
+  return out;
+}
+
+}  // namespace detail
+
+// ---- elementwise operators (mc_ops.hpp:338-507) -------------------------------
+
+template <class P>
+MCTensor<P> grow_expn(const MCTensor<P>& x, const NdArray& v) {  // mc_ops.hpp:384-394
+  mcf::detail::check_nc_limit(x.nc());
+  mcf::detail::check_suffix_broadcast(x.shape(), v.shape(), "grow_expn");
+  return detail::elementwise<P>("grow_expn", &x, nullptr, &v, x.shape(), x.nc());
+}
+
+template <class P>
+MCTensor<P> scaling_n(const MCTensor<P>& x, const NdArray& v, bool expanded = false) {
+  mcf::detail::check_nc_limit(x.nc());  // mc_ops.hpp:398-410
+  mcf::detail::check_suffix_broadcast(x.shape(), v.shape(), "scaling_n");
+  const int onc = expanded ? x.nc() + 1 : x.nc();
+  mcf::detail::check_nc_limit(onc);
+  return detail::elementwise<P>(expanded ? "scaling_n_expanded" : "scaling_n", &x, nullptr, &v,
+                                x.shape(), onc);
+}
+
+template <class P>
+MCTensor<P> div_n(const NdArray& v, const MCTensor<P>& y) {  // mc_ops.hpp:494-507
+  mcf::detail::check_nc_limit(y.nc());
+  mcf::detail::check_suffix_broadcast(y.shape(), v.shape(), "div_n");
+  return detail::elementwise<P>("div_n", nullptr, &y, &v, y.shape(), y.nc());
+}
+
+#define MCF_GPU_BINARY(name)                                                             \
+  template <class P>                                                                     \
+  MCTensor<P> name(const MCTensor<P>& x, const MCTensor<P>& y) {                         \
+    check_shapes_equal(x.shape(), y.shape(), #name);                                     \
+    const int nc = x.nc() > y.nc() ? x.nc() : y.nc();                                    \
+    mcf::detail::check_nc_limit(nc);                                                     \
+    return detail::elementwise<P>(#name, &x, &y, nullptr, x.shape(), nc);                \
+  }
+MCF_GPU_BINARY(add_mcn)       // mc_ops.hpp:440-446
+MCF_GPU_BINARY(div_mcn)       // mc_ops.hpp:448-454
+MCF_GPU_BINARY(mul_mcn)       // mc_ops.hpp:456-462
+MCF_GPU_BINARY(mul_mcn_slow)  // mc_ops.hpp:464-470
+#undef MCF_GPU_BINARY
+
+template <class P>
+MCTensor<P> square_mcn(const MCTensor<P>& x) {  // mc_ops.hpp:472-480
+  mcf::detail::check_nc_limit(x.nc());
+  return detail::elementwise<P>("square_mcn", &x, nullptr, nullptr, x.shape(), x.nc());
+}
+
+template <class P>
+MCTensor<P> exp_mcn(const MCTensor<P>& x) {  // mc_ops.hpp:482-490 (correctly rounded exp)
+  mcf::detail::check_nc_limit(x.nc());
+  return detail::elementwise<P>("exp_mcn", &x, nullptr, nullptr, x.shape(), x.nc());
+}
+
+template <class P>
+MCTensor<P> negate(const MCTensor<P>& x) {  // mc_ops.hpp:376-381
+  return detail::elementwise<P>("negate", &x, nullptr, nullptr, x.shape(), x.nc());
+}
+
+// ---- contractions (linalg.hpp) ---------------------------------------------------
+
+namespace detail {
+inline int strategy_of(const ReductionPlan& plan) {
+  return plan.strategy == ReduceStrategy::kPairwiseTree ? MCF_PAIRWISE_TREE : MCF_SEQUENTIAL;
+}
+
+template <class P>
+MCTensor<P> bmm(const MCTensor<P>& x, const NdArray& w, std::size_t batch, std::size_t m,
+                std::size_t k, std::size_t n, bool w_batched, Shape out_shape, int strategy) {
+  using S = Store<P>;
+  mcf::detail::check_nc_limit(x.nc() + 1);
+  const auto xs = pack<P>(x.raw());
+  const auto ws = pack_wp<P>(w);
+  std::vector<typename S::T> os(batch * m * n * x.nc());
+  check(mcf_h_bmm_mcn(S::kPrec, xs.data(), x.nc(), ws.data(), batch, m, k, n, w_batched ? 1 : 0,
+                      os.data(), strategy));
+  MCTensor<P> out(std::move(out_shape), x.nc());
+  unpack<P>(os, out.raw());
+  return out;
+}
+}  // namespace detail
+
+template <class P>
+MCTensor<P> mm_mcn(const MCTensor<P>& x, const NdArray& w, const ReductionPlan& plan = {}) {
+  mcf::detail::require_rank(x.shape(), 2, "mm_mcn");  // linalg.hpp:138-157
+  mcf::detail::require_rank(w.shape(), 2, "mm_mcn");
+  if (x.dim(1) != w.dim(0))
+    throw std::invalid_argument("mm_mcn: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                shape_str(w.shape()));
+  return detail::bmm<P>(x, w, 1, x.dim(0), x.dim(1), w.dim(1), false, Shape{x.dim(0), w.dim(1)},
+                        detail::strategy_of(plan));
+}
+
+// GPU-order plan (FP64 pipe), same shapes and checks as mm_mcn
+template <class P>
+MCTensor<P> mm_mcn_fast(const MCTensor<P>& x, const NdArray& w) {
+  mcf::detail::require_rank(x.shape(), 2, "mm_mcn");
+  mcf::detail::require_rank(w.shape(), 2, "mm_mcn");
+  if (x.dim(1) != w.dim(0))
+    throw std::invalid_argument("mm_mcn: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                shape_str(w.shape()));
+  return detail::bmm<P>(x, w, 1, x.dim(0), x.dim(1), w.dim(1), false, Shape{x.dim(0), w.dim(1)},
+                        MCF_FAST);
+}
+
+// linalg.hpp:159-166: MC x MC stays refused on the drop-in overload
+template <class P>
+MCTensor<P> mm_mcn(const MCTensor<P>&, const MCTensor<P>&, const ReductionPlan& = {}) {
+  detail::check(mcf_mm_mcn_mcmc_refusal());
+  return {};
+}
+
+template <class P>
+MCTensor<P> dot_mcn(const MCTensor<P>& x, const NdArray& v, const ReductionPlan& plan = {}) {
+  mcf::detail::require_rank(x.shape(), 1, "dot_mcn");  // linalg.hpp:103-116
+  mcf::detail::require_rank(v.shape(), 1, "dot_mcn");
+  if (x.dim(0) != v.dim(0))
+    throw std::invalid_argument("dot_mcn: length mismatch " + shape_str(x.shape()) + " vs " +
+                                shape_str(v.shape()));
+  return detail::bmm<P>(x, v, 1, 1, x.dim(0), 1, false, Shape{}, detail::strategy_of(plan));
+}
+
+template <class P>
+MCTensor<P> mv_mcn(const MCTensor<P>& x, const NdArray& v, const ReductionPlan& plan = {}) {
+  mcf::detail::require_rank(x.shape(), 2, "mv_mcn");  // linalg.hpp:119-135
+  mcf::detail::require_rank(v.shape(), 1, "mv_mcn");
+  if (x.dim(1) != v.dim(0))
+    throw std::invalid_argument("mv_mcn: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                shape_str(v.shape()));
+  return detail::bmm<P>(x, v, 1, x.dim(0), x.dim(1), 1, false, Shape{x.dim(0)},
+                        detail::strategy_of(plan));
+}
+
+template <class P>
+MCTensor<P> bmm_mcn(const MCTensor<P>& x, const NdArray& w, const ReductionPlan& plan = {}) {
+  mcf::detail::require_rank(x.shape(), 3, "bmm_mcn");  // linalg.hpp:205-216
+  mcf::detail::require_rank(w.shape(), 3, "bmm_mcn");
+  if (x.dim(0) != w.dim(0) || x.dim(2) != w.dim(1))
+    throw std::invalid_argument("bmm_mcn: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                shape_str(w.shape()));
+  return detail::bmm<P>(x, w, x.dim(0), x.dim(1), x.dim(2), w.dim(2), true,
+                        Shape{x.dim(0), x.dim(1), w.dim(2)}, detail::strategy_of(plan));
+}
+
+// NEW: MC x MC product (SURVEY 8c recipe B by default; strategy MCF_FAST for
+// the FP64-pipe kernel)
+template <class P>
+MCTensor<P> mm_mcmc(const MCTensor<P>& x, const MCTensor<P>& y, int strategy = MCF_SEQUENTIAL) {
+  using S = detail::Store<P>;
+  mcf::detail::require_rank(x.shape(), 2, "mm_mcmc");
+  mcf::detail::require_rank(y.shape(), 2, "mm_mcmc");
+  if (x.dim(1) != y.dim(0) || x.nc() != y.nc())
+    throw std::invalid_argument("mm_mcmc: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                shape_str(y.shape()));
+  const auto xs = detail::pack<P>(x.raw());
+  const auto ys = detail::pack<P>(y.raw());
+  std::vector<typename S::T> os(x.dim(0) * y.dim(1) * x.nc());
+  detail::check(mcf_h_mm_mcmc(S::kPrec, xs.data(), ys.data(), x.nc(), x.dim(0), x.dim(1), y.dim(1),
+                              os.data(), strategy));
+  MCTensor<P> out(Shape{x.dim(0), y.dim(1)}, x.nc());
+  detail::unpack<P>(os, out.raw());
+  return out;
+}
+
+}  // namespace gpu
+}  // namespace mcf

@@ -41,10 +41,9 @@ _int = C.c_int
 
 
 def build(force: bool = False) -> None:
-    """Build the port (and the reference shim when /root/reference exists)."""
-    if force or not os.path.exists(PORT_SO) or (
-        os.path.isdir("/root/reference/proj/include") and not os.path.exists(REF_SO)
-    ):
+    """Build the port (and, when /root/reference exists, the reference shim
+    and the C++ drop-in check); make skips whatever is up to date."""
+    if force or not os.path.exists(PORT_SO) or os.path.isdir("/root/reference/proj/include"):
         subprocess.run(["make", "-s", "-f", os.path.join(HERE, "Makefile")], check=True)
 
 
