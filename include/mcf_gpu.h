@@ -151,6 +151,33 @@ mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
  * operand kind (mcmc = 0: MC x Tensor, 1: MC x MC); 0 = no fast kernel. */
 int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
 
+/* ---- MC-MLP step pieces (config 3; binary32 components) -------------------
+ * Activations are feature-major (features x n).  Forward of one MCLinear is
+ * mcf_bmm_mcn(W (out x in, MC), A_prev (in x n)) followed by
+ * mcf_mlp_bias_act: h = approx(add_mcn(z, bias)), act = relu(h) or h
+ * [replaces autodiff.hpp:255-276 mc_linear_op forward + :133-144 relu]. */
+mcf_status mcf_mlp_bias_act(const float* z, int nc, const float* bias, int64_t out_dim, int64_t n,
+                            int relu, float* h, float* act, mcf_stream stream);
+/* cross-entropy over logits (classes x n): per-sample terms, gradient
+ * (softmax - onehot) / n_global, and (optionally) the left-to-right sum of the
+ * terms [replaces autodiff.hpp:541-582]. */
+mcf_status mcf_mlp_cross_entropy(const float* logits, const int* labels, int64_t classes, int64_t n,
+                                 int64_t n_global, float* grad, float* terms, float* term_sum,
+                                 mcf_stream stream);
+/* C = op(A) op(B) in binary32 with the reduction index increasing, fl_mul then
+ * fl_add (matmul2d, ndarray.hpp:147-165); relu_mask (optional, C's shape)
+ * zeroes entries whose mask <= 0 (ReLU backward) [mc_linear_op backward,
+ * autodiff.hpp:279-297]. */
+mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_t lda, const float* b,
+                                int64_t ldb, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
+                                const float* relu_mask, mcf_stream stream);
+/* out[r] = sum_j g[r, j] in order (bias gradient, autodiff.hpp:287-292) */
+mcf_status mcf_rowsum_f32_ordered(const float* g, int64_t rows, int64_t n, float* out,
+                                  mcf_stream stream);
+/* MC-SGD, momentum 0: w <- grow_expn(w, -lr * g) in place
+ * [replaces optim.hpp:54-77 + mc_ops.hpp:509-513] */
+mcf_status mcf_sgd_grow(float* w, int nc, const float* g, int64_t numel, float lr, mcf_stream stream);
+
 /* ---- host-buffer entry points (blocking; the reference's calling model) --- */
 /* op: "grow_expn" "scaling_n" "div_n" "add_mcn" "div_mcn" "mul_mcn"
  *     "mul_mcn_slow" "square_mcn" "exp_mcn" "negate" "approx".

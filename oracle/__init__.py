@@ -122,6 +122,8 @@ class Oracle:
             L.mcfref_time_mm_rows.restype = C.c_double
             L.mcfref_time_dot_mcmc.argtypes = [_int, _p, _p, _int, _i64, _i64, _int, _p]
             L.mcfref_time_dot_mcmc.restype = C.c_double
+            L.mcfref_mlp_train.argtypes = [_p, _int, _int, _p, _p, _p, _i64, _int, C.c_double, _p, _p]
+            L.mcfref_mlp_train.restype = _int
 
     @staticmethod
     def _check(rc, what):
@@ -326,6 +328,31 @@ class Oracle:
         if t < 0:
             raise OracleError("time_dot_mcmc failed")
         return t, out
+
+
+def mlp_train_reference(dims, nc, params, X, labels, steps, lr):
+    """The reference's own MC-MLP training loop (oracle/_ref).  params: list of
+    (W (out, in, nc), b (out, nc)) float32 per layer; X (n, dims[0]) float32;
+    returns (losses[steps], list of final (W, b))."""
+    ref = Oracle("ref")
+    flat = np.concatenate([np.concatenate([w.ravel(), b.ravel()]) for w, b in params]).astype(np.float32)
+    dims_c = np.ascontiguousarray(dims, np.int32)
+    X = np.ascontiguousarray(X, np.float32)
+    lab = np.ascontiguousarray(labels, np.int32)
+    losses = np.empty(steps, np.float32)
+    out = np.empty_like(flat)
+    rc = ref.lib.mcfref_mlp_train(_ptr(dims_c), len(dims) - 1, nc, _ptr(flat), _ptr(X), _ptr(lab), X.shape[0],
+                                  steps, float(lr), _ptr(losses), _ptr(out))
+    if rc != 0:
+        raise OracleError("mcfref_mlp_train failed")
+    res, off = [], 0
+    for w, b in params:
+        W = out[off:off + w.size].reshape(w.shape)
+        off += w.size
+        B = out[off:off + b.size].reshape(b.shape)
+        off += b.size
+        res.append((W, B))
+    return losses, res
 
 
 def ref_available() -> bool:

@@ -121,6 +121,12 @@ double mcfref_time_mm_rows(int prec, const void* x, int nc, const void* w, int64
 /* Times the recipe-B MC x MC dot over `batch` dots of length k. */
 double mcfref_time_dot_mcmc(int prec, const void* x, const void* y, int nc,
                             int64_t batch, int64_t k, int threads, void* out);
+/* MC-MLP training with the reference's own MCSequential / MCLinear / ReLU /
+ * cross_entropy_loss / Tape / MCSGD (binary32, momentum 0).  params holds,
+ * per layer, W (dims[l+1] x dims[l] x nc) then b (dims[l+1] x nc). */
+int mcfref_mlp_train(const int* dims, int nlayers, int nc, const float* params, const float* X,
+                     const int* labels, int64_t n, int steps, double lr, float* losses,
+                     float* params_out);
 
 #ifdef __cplusplus
 }

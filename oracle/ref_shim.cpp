@@ -20,6 +20,8 @@
 #include "mcf_oracle.h"
 #include "mcfloat/linalg.hpp"
 #include "mcfloat/mc_ops.hpp"
+#include "mcfloat/nn.hpp"
+#include "mcfloat/optim.hpp"
 
 namespace {
 
@@ -447,6 +449,56 @@ double mcfref_time_dot_mcmc(int prec, const void* x, const void* y, int nc, std:
     if (out) from_vec<P>(o, out, 0);
   });
   return elapsed;
+}
+
+// MC-MLP training with the reference's own modules (config 3 oracle):
+// MCSequential of MCLinear(+bias) and ReLULayer (nn.hpp:49-92,132-136,162-201),
+// cross_entropy_loss (autodiff.hpp:541-582), Tape::backward (:209-228) and
+// MCSGD (optim.hpp:34-77, momentum 0).  params: for each layer l the weight
+// (dims[l+1] x dims[l] x nc) then the bias (dims[l+1] x nc), binary32
+// components; X (n x dims[0]) binary32; losses[s] = loss before update s.
+int mcfref_mlp_train(const int* dims, int nlayers, int nc, const float* params, const float* X,
+                     const int* labels, int64_t n, int steps, double lr, float* losses,
+                     float* params_out) {
+  using P = mcf::B32;
+  try {
+    mcf::Rng rng(1);
+    mcf::MCSequential<P> model;
+    std::vector<mcf::MCLinear<P>*> lins;
+    for (int l = 0; l < nlayers; ++l) {
+      auto lin = std::make_unique<mcf::MCLinear<P>>(dims[l], dims[l + 1], true, nc, rng);
+      lins.push_back(lin.get());
+      model.add(std::move(lin));
+      if (l + 1 < nlayers) model.add(std::make_unique<mcf::ReLULayer<P>>());
+    }
+    const float* p = params;
+    for (auto* lin : lins) {
+      for (auto& v : lin->weight().raw()) v = *p++;
+      for (auto& v : lin->bias()->raw()) v = *p++;
+    }
+    NdArray x(Shape{static_cast<std::size_t>(n), static_cast<std::size_t>(dims[0])});
+    for (std::size_t i = 0; i < x.numel(); ++i) x[i] = X[i];
+    const std::vector<int> lab(labels, labels + n);
+    mcf::MCSGD<P> opt(model.parameters(), {lr, 0.0, false});
+    for (int s = 0; s < steps; ++s) {
+      mcf::Tape<P> tape;
+      const mcf::Var in = tape.leaf(x);
+      const mcf::Var logits = model.forward(tape, in);
+      const mcf::Var loss = mcf::cross_entropy_loss(tape, logits, lab);
+      losses[s] = static_cast<float>(tape.value(loss)[0]);
+      tape.backward(loss);
+      opt.step();
+      model.zero_grad();
+    }
+    float* q = params_out;
+    for (auto* lin : lins) {
+      for (double v : lin->weight().raw()) *q++ = static_cast<float>(v);
+      for (double v : lin->bias()->raw()) *q++ = static_cast<float>(v);
+    }
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -68,6 +68,11 @@ _SIGS = {
     "mcf_h_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _int],
     "mcf_fast_ops_per_mad": [_int, _int, _int],
     "mcf_probe_pipe_rates": [_p, _p],
+    "mcf_mlp_bias_act": [_p, _int, _p, _i64, _i64, _int, _p, _p, _p],
+    "mcf_mlp_cross_entropy": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
+    "mcf_gemm_f32_ordered": [_int, _int, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _p],
+    "mcf_rowsum_f32_ordered": [_p, _i64, _i64, _p, _p],
+    "mcf_sgd_grow": [_p, _int, _p, _i64, C.c_float, _p],
 }
 
 

@@ -1,0 +1,266 @@
+// mlp.cu -- the MC-MLP training step around the MC contractions (config 3).
+//
+// The reference composes MCLinear / ReLU / cross-entropy / MC-SGD from its
+// library (nn.hpp:49-92, autodiff.hpp:133-144, 255-298, 541-582, optim.hpp:54-77,
+// mc_ops.hpp:509-513).  The GPU keeps activations feature-major, (features x
+// batch), so every layer's forward is the MC x Tensor product
+//   Z_l (out x N, MC) = W_l (out x in, MC) . A_{l-1} (in x N)
+// exactly as the reference computes matmul_mcn(W, transpose2d(X)) before its
+// transpose (autodiff.hpp:265).  This file adds the kernels around it, each
+// reproducing the reference's rounding sequence:
+//   k_bias_act  z + bias (add_mcn, x = product, y = bias), approx(), ReLU
+//   k_ce        max-shifted softmax, log-sum-exp, per-sample loss terms and
+//               the gradient (softmax - onehot) / N, all rounded in binary32
+//   k_seqsum    the loss's left-to-right binary32 sum (autodiff.hpp:572)
+//   k_gemm      matmul2d (ndarray.hpp:147-165): fl_mul then fl_add, reduction
+//               index in increasing order, no fma -- used for dW = G A^T and
+//               dA = approx(W)^T G (+ ReLU mask) of mc_linear_op's backward
+//   k_rowsum    the bias gradient, rows summed in order
+//   k_sgd_grow  MC-SGD (momentum 0): u = 0*u + g, delta = -lr*u, and the
+//               Grow-ExpN update of the MC parameter in place
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "mcf_fast.cuh"
+#include "mcf_lit.cuh"
+#include "mcf_prec.cuh"
+#include "mcf_runtime.h"
+
+namespace mcfg {
+namespace {
+
+using P = PB32;
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_bias_act(const float* __restrict__ z, const float* __restrict__ bias,
+                                                  int64_t out_dim, int64_t n, int relu,
+                                                  float* __restrict__ h, float* __restrict__ act) {
+  const int64_t total = out_dim * n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t o = e / n;
+    float zx[NC], by[NC], r[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      zx[c] = z[e * NC + c];
+      by[c] = bias[o * NC + c];
+    }
+    if (!fast::add<P, NC>(zx, by, r)) lit::add<P>(zx, NC, by, NC, r, NC);
+    const float v = fast::approx<P, NC>(r);
+    h[e] = v;
+    if (act) act[e] = relu ? (v > 0.0f ? v : 0.0f) : v;  // Tape::relu, autodiff.hpp:134
+  }
+}
+
+// one thread per sample (column n of the C x n logits)
+__global__ void __launch_bounds__(256) k_ce(const float* __restrict__ logits, const int* __restrict__ labels,
+                                            int64_t classes, int64_t n, float n_global,
+                                            float* __restrict__ grad, float* __restrict__ terms) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  float m = logits[s];
+  for (int64_t c = 1; c < classes; ++c) {
+    const float z = logits[c * n + s];
+    m = m < z ? z : m;  // std::max
+  }
+  float sum = 0.0f;
+  for (int64_t c = 0; c < classes; ++c) {
+    const float d = __fsub_rn(logits[c * n + s], m);
+    const float ex = __double2float_rn(cr_exp((double)d));  // P::round(std::exp(...))
+    grad[c * n + s] = ex;
+    sum = __fadd_rn(sum, ex);
+  }
+  const int lab = labels[s];
+  for (int64_t c = 0; c < classes; ++c) {
+    float sm = __fdiv_rn(grad[c * n + s], sum);
+    if (c == lab) sm = __fsub_rn(sm, 1.0f);
+    // fl_mul(1, fl_div(d, n)), accumulated into a zero gradient (fl_add(0, .))
+    grad[c * n + s] = __fadd_rn(0.0f, __fmul_rn(1.0f, __fdiv_rn(sm, n_global)));
+  }
+  const float lse = __fadd_rn(m, __double2float_rn(log((double)sum)));
+  terms[s] = __fsub_rn(lse, logits[(int64_t)lab * n + s]);
+}
+
+__global__ void k_seqsum(const float* __restrict__ terms, int64_t n, float* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  float acc = 0.0f;
+  for (int64_t i = 0; i < n; ++i) acc = __fadd_rn(acc, terms[i]);
+  out[0] = acc;
+}
+
+// C[i, j] = sum_k A(i, k) * B(k, j), k increasing, fl_mul then fl_add.
+// A(i, k) = TA ? a[k * lda + i] : a[i * lda + k];  B(k, j) = TB ? b[j * ldb + k] : b[k * ldb + j]
+// mask (optional): C[i, j] = mask[i * ldc + j] > 0 ? (0 + c) : 0  (ReLU backward)
+// zero_add: C = 0 + c (accumulation into a zero gradient)
+constexpr int GB = 64, GK = 16, GT = 256;  // 64x64 tile, 4x4 per thread
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
+                                             int64_t ldb, float* __restrict__ c, int64_t ldc, int64_t M, int64_t N,
+                                             int64_t K, const float* __restrict__ mask) {
+  __shared__ float As[GK][GB + 1];
+  __shared__ float Bs[GK][GB + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t i0 = (int64_t)blockIdx.y * GB, j0 = (int64_t)blockIdx.x * GB;
+  float acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0f;
+  for (int64_t k0 = 0; k0 < K; k0 += GK) {
+    for (int t = threadIdx.x; t < GK * GB; t += GT) {
+      // A tile: rows i0..i0+63, cols k0..k0+15 -> As[k][i]
+      int kk, ii;
+      if (TA) { ii = t % GB; kk = t / GB; } else { kk = t % GK; ii = t / GK; }
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      As[kk][ii] = (gi < M && gk < K) ? (TA ? a[gk * lda + gi] : a[gi * lda + gk]) : 0.0f;
+      int kb, jb;
+      if (TB) { kb = t % GK; jb = t / GK; } else { jb = t % GB; kb = t / GB; }
+      const int64_t gj = j0 + jb, gkb = k0 + kb;
+      Bs[kb][jb] = (gj < N && gkb < K) ? (TB ? b[gj * ldb + gkb] : b[gkb * ldb + gj]) : 0.0f;
+    }
+    __syncthreads();
+    const int kmax = (int)((K - k0) < GK ? (K - k0) : GK);
+    for (int kk = 0; kk < kmax; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = As[kk][ty + 16 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = Bs[kk][tx + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t gi = i0 + ty + 16 * u;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t gj = j0 + tx + 16 * v;
+      if (gj >= N) continue;
+      float r = __fadd_rn(0.0f, acc[u][v]);
+      if (mask) r = mask[gi * ldc + gj] > 0.0f ? __fadd_rn(0.0f, r) : 0.0f;
+      c[gi * ldc + gj] = r;
+    }
+  }
+}
+
+// g (rows x n): out[r] = sum_j g[r, j], j increasing, starting from 0
+__global__ void __launch_bounds__(256) k_rowsum(const float* __restrict__ g, int64_t rows, int64_t n,
+                                                float* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  float acc = 0.0f;
+  for (int64_t j = 0; j < n; ++j) acc = __fadd_rn(acc, g[r * n + j]);
+  out[r] = acc;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_sgd_grow(float* __restrict__ w, const float* __restrict__ g, int64_t numel,
+                                                  float lr) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < numel; e += stride) {
+    // optim.hpp:70-73 with momentum 0: u = fl_add(fl_mul(0, 0), g); update = -fl_mul(lr, u)
+    const float u = __fadd_rn(__fmul_rn(0.0f, 0.0f), g[e]);
+    const float delta = -__fmul_rn(lr, u);
+    float x[NC], o[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) x[c] = w[e * NC + c];
+    if (!fast::grow<P, NC>(x, delta, o)) lit::grow<P>(x, NC, delta, o);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) w[e * NC + c] = o[c];
+  }
+}
+
+}  // namespace
+}  // namespace mcfg
+
+// ---- C-ABI ---------------------------------------------------------------------
+
+namespace {
+mcf_status launched(const char* what) {
+  mcfr::note_launch();
+  return mcfr::check_launch(what);
+}
+int grid_of(int64_t n) { return mcfr::grid_for(n, 256, 8); }
+
+// this translation unit's copy of the device exp table (mcf_exp.cuh keeps the
+// table per translation unit; k_ce's cr_exp reads this one)
+std::mutex g_tab_mu;
+bool g_tab_done[64];
+mcf_status ensure_tables_here() {
+  const mcf_status st = mcfr::ensure_device_tables();  // stack limit + elementwise copy
+  if (st != MCF_OK) return st;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) d = 0;
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (g_tab_done[d]) return MCF_OK;
+  double tab[4096];
+  mcfr::exp2_table(tab);
+  if (cudaMemcpyToSymbol(mcfg::g_exp_tab, tab, sizeof(tab)) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot upload the exp table (mlp)");
+  g_tab_done[d] = true;
+  return MCF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+mcf_status mcf_mlp_bias_act(const float* z, int nc, const float* bias, int64_t out_dim, int64_t n, int relu,
+                            float* h, float* act, mcf_stream s) {
+  if (nc != 2 && nc != 3) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mlp_bias_act: nc must be 2 or 3");
+  if (out_dim * n == 0) return MCF_OK;
+  if (nc == 2) mcfg::k_bias_act<2><<<grid_of(out_dim * n), 256, 0, s>>>(z, bias, out_dim, n, relu, h, act);
+  else mcfg::k_bias_act<3><<<grid_of(out_dim * n), 256, 0, s>>>(z, bias, out_dim, n, relu, h, act);
+  return launched("mlp_bias_act kernel");
+}
+
+mcf_status mcf_mlp_cross_entropy(const float* logits, const int* labels, int64_t classes, int64_t n,
+                                 int64_t n_global, float* grad, float* terms, float* term_sum, mcf_stream s) {
+  if (n == 0) return MCF_OK;
+  const mcf_status ok = ensure_tables_here();
+  if (ok != MCF_OK) return ok;
+  mcfg::k_ce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(logits, labels, classes, n, (float)n_global, grad, terms);
+  mcf_status st = launched("mlp cross-entropy kernel");
+  if (st != MCF_OK || !term_sum) return st;
+  mcfg::k_seqsum<<<1, 32, 0, s>>>(terms, n, term_sum);
+  return launched("mlp loss sum kernel");
+}
+
+mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb,
+                                float* c, int64_t ldc, int64_t m, int64_t n, int64_t k, const float* relu_mask,
+                                mcf_stream s) {
+  if (m * n == 0) return MCF_OK;
+  const dim3 grid((unsigned)((n + mcfg::GB - 1) / mcfg::GB), (unsigned)((m + mcfg::GB - 1) / mcfg::GB));
+  if (trans_a && trans_b) mcfg::k_gemm<true, true><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
+  else if (trans_a) mcfg::k_gemm<true, false><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
+  else if (trans_b) mcfg::k_gemm<false, true><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
+  else mcfg::k_gemm<false, false><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
+  return launched("ordered fp32 gemm kernel");
+}
+
+mcf_status mcf_rowsum_f32_ordered(const float* g, int64_t rows, int64_t n, float* out, mcf_stream s) {
+  if (rows == 0) return MCF_OK;
+  mcfg::k_rowsum<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(g, rows, n, out);
+  return launched("row-sum kernel");
+}
+
+mcf_status mcf_sgd_grow(float* w, int nc, const float* g, int64_t numel, float lr, mcf_stream s) {
+  if (nc != 2 && nc != 3) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "sgd_grow: nc must be 2 or 3");
+  if (numel == 0) return MCF_OK;
+  const mcf_status ok = mcfr::ensure_device_tables();
+  if (ok != MCF_OK) return ok;
+  if (nc == 2) mcfg::k_sgd_grow<2><<<grid_of(numel), 256, 0, s>>>(w, g, numel, lr);
+  else mcfg::k_sgd_grow<3><<<grid_of(numel), 256, 0, s>>>(w, g, numel, lr);
+  return launched("sgd grow kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+"""MC-MLP training (BASELINE config 3) on the MCF operators.
+
+The reference composes this from its library: MCSequential of MCLinear layers
+(nn.hpp:49-92, 162-201) with ReLU (autodiff.hpp:133-144), cross-entropy
+(autodiff.hpp:541-582), reverse-mode tape (autodiff.hpp:209-228) and MC-SGD
+applied through Grow-ExpN (optim.hpp:54-77, mc_ops.hpp:509-513).  Here one
+training step is a fixed sequence of C-ABI calls on feature-major activations
+(features x batch):
+
+  forward   Z = W . A_prev (MC x Tensor, mcf_bmm_mcn, plan FAST or reference
+            order), h = approx(add_mcn(Z, b)), A = relu(h)   (mcf_mlp_bias_act)
+  loss      mcf_mlp_cross_entropy (terms, gradient / N_global, ordered sum)
+  backward  dW = G A_prev^T, dA = approx(W)^T G masked by h_prev > 0,
+            db = row sums of G  (ordered binary32: mcf_gemm_f32_ordered,
+            mcf_rowsum_f32_ordered -- matmul2d semantics)
+  exchange  data parallel: one flat binary32 gradient buffer, all_reduce(sum)
+            over the process group (NCCL over NVLink on GPUs)
+  update    mcf_sgd_grow: w <- grow_expn(w, -lr * g), identical on every rank
+
+Single process with the reference-order plan, every step is bit-identical to
+the reference's own training loop (tests/test_gpu_mlp.py); with plan FAST the
+forward products carry the compensated binary64 accumulation and the loss
+trajectory stays within the reference's rounding spread.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import B32, FAST, SEQUENTIAL, _check, lib
+from . import data as _data
+
+
+def init_params(dims, nc=2, seed=3000):
+    """Kaiming-uniform fan-in init (nn.hpp:41-47, 55-59): per layer the weight
+    draws U(-1/sqrt(in), 1/sqrt(in)) then the bias draws, one Rng stream; each
+    binary64 draw split into nc binary32 components (BASELINE config 3)."""
+    counts = [dims[l + 1] * dims[l] + dims[l + 1] for l in range(len(dims) - 1)]
+    u = _data.uniform(seed, sum(counts))
+    params, off = [], 0
+    for l in range(len(dims) - 1):
+        fan_in, out = dims[l], dims[l + 1]
+        bound = 1.0 / np.sqrt(float(fan_in))
+        w = -bound + 2.0 * bound * u[off:off + out * fan_in]
+        off += out * fan_in
+        b = -bound + 2.0 * bound * u[off:off + out]
+        off += out
+        params.append((_data.split(w, nc).reshape(out, fan_in, nc), _data.split(b, nc).reshape(out, nc)))
+    return params
+
+
+def make_batch(n, in_dim=784, classes=10, seed_x=3001, seed_y=3002):
+    """X ~ N(0,1) rounded to binary32 (Rng::normal), labels Rng::below(classes)."""
+    x = _data.normal(seed_x, n * in_dim).astype(np.float32).reshape(n, in_dim)
+    y = _data.below(seed_y, classes, n).astype(np.int32)
+    return x, y
+
+
+class GradExchange:
+    """Flat binary32 gradient buffer + sum all-reduce across a process group.
+    Works for any torch device/backend (NCCL on B200s, gloo on CPU tests)."""
+
+    def __init__(self, shapes, device, group=None):
+        self.shapes = shapes
+        sizes = [int(np.prod(s)) for s in shapes]
+        self.flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
+        self.views, off = [], 0
+        for s, n in zip(shapes, sizes):
+            self.views.append(self.flat[off:off + n].view(*s))
+            off += n
+        self.group = group
+
+    def world(self):
+        if self.group is None:
+            return 1
+        import torch.distributed as dist
+
+        return dist.get_world_size(self.group)
+
+    def all_reduce(self, loss_sum: torch.Tensor = None):
+        if self.world() > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+            if loss_sum is not None:
+                dist.all_reduce(loss_sum, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class MCMLP:
+    """Device-resident MC-MLP; `step()` runs forward, loss, backward, gradient
+    exchange and the MC-SGD update, and returns the step's loss."""
+
+    def __init__(self, dims, params, lr=0.01, nc=2, plan=FAST, group=None, device="cuda"):
+        self.dims, self.nc, self.lr, self.plan = list(dims), nc, float(lr), plan
+        self.L = len(dims) - 1
+        self.W = [torch.from_numpy(np.ascontiguousarray(w)).to(device) for w, _ in params]
+        self.b = [torch.from_numpy(np.ascontiguousarray(b)).to(device) for _, b in params]
+        shapes = []
+        for l in range(self.L):
+            shapes += [(dims[l + 1], dims[l]), (dims[l + 1],)]
+        self.grads = GradExchange(shapes, device, group)
+        self.lib = lib()
+        self._bufs = None
+
+    def _alloc(self, n):
+        if self._bufs is not None and self._bufs["n"] == n:
+            return self._bufs
+        dev = self.W[0].device
+        f = dict(dtype=torch.float32, device=dev)
+        bufs = {"n": n}
+        bufs["Z"] = [torch.empty((self.dims[l + 1], n, self.nc), **f) for l in range(self.L)]
+        bufs["H"] = [torch.empty((self.dims[l + 1], n), **f) for l in range(self.L)]
+        bufs["A"] = [torch.empty((self.dims[l + 1], n), **f) for l in range(self.L - 1)]
+        bufs["G"] = [torch.empty((self.dims[l + 1], n), **f) for l in range(self.L)]
+        bufs["Wa"] = [torch.empty((self.dims[l + 1], self.dims[l]), **f) for l in range(self.L)]
+        bufs["terms"] = torch.empty(n, **f)
+        bufs["loss"] = torch.zeros(1, **f)
+        self._bufs = bufs
+        return bufs
+
+    def step(self, xt: torch.Tensor, labels: torch.Tensor, n_global: int) -> torch.Tensor:
+        """xt: (in, n_local) binary32 (feature-major batch shard); labels (n_local,)
+        int32.  Returns the (globally summed) loss terms as a 1-element device
+        tensor, no host sync; loss_value() turns it into the loss."""
+        L, nc, lib_ = self.L, self.nc, self.lib
+        n = xt.shape[1]
+        B = self._alloc(n)
+        s = torch.cuda.current_stream().cuda_stream
+        acts = [xt]
+        for l in range(L):
+            out_dim, in_dim = self.dims[l + 1], self.dims[l]
+            _check(lib_.mcf_bmm_mcn(B32, self.W[l].data_ptr(), nc, acts[l].data_ptr(), 1, out_dim, in_dim, n, 0,
+                                    B["Z"][l].data_ptr(), self.plan, 1, s))
+            last = l == L - 1
+            _check(lib_.mcf_mlp_bias_act(B["Z"][l].data_ptr(), nc, self.b[l].data_ptr(), out_dim, n, 0 if last else 1,
+                                         B["H"][l].data_ptr(), None if last else B["A"][l].data_ptr(), s))
+            if not last:
+                acts.append(B["A"][l])
+        # loss + dL/dlogits
+        _check(lib_.mcf_mlp_cross_entropy(B["H"][L - 1].data_ptr(), labels.data_ptr(), self.dims[-1], n, n_global,
+                                          B["G"][L - 1].data_ptr(), B["terms"].data_ptr(), B["loss"].data_ptr(), s))
+        # backward
+        gv = self.grads.views
+        for l in range(L - 1, -1, -1):
+            out_dim, in_dim = self.dims[l + 1], self.dims[l]
+            G = B["G"][l]
+            # dW (out x in) = G (out x n) . A_prev^T  (A_prev is in x n)
+            _check(lib_.mcf_gemm_f32_ordered(0, 1, G.data_ptr(), n, acts[l].data_ptr(), n, gv[2 * l].data_ptr(),
+                                             in_dim, out_dim, in_dim, n, None, s))
+            _check(lib_.mcf_rowsum_f32_ordered(G.data_ptr(), out_dim, n, gv[2 * l + 1].data_ptr(), s))
+            if l > 0:
+                _check(lib_.mcf_approx(B32, self.W[l].data_ptr(), nc, B["Wa"][l].data_ptr(), out_dim * in_dim, s))
+                # dA_prev (in x n) = approx(W)^T (in x out) . G (out x n), ReLU mask = H_{l-1}
+                _check(lib_.mcf_gemm_f32_ordered(1, 0, B["Wa"][l].data_ptr(), in_dim, G.data_ptr(), n,
+                                                 B["G"][l - 1].data_ptr(), n, in_dim, n, out_dim,
+                                                 B["H"][l - 1].data_ptr(), s))
+        self.grads.all_reduce(B["loss"])
+        for l in range(L):
+            _check(lib_.mcf_sgd_grow(self.W[l].data_ptr(), nc, gv[2 * l].data_ptr(), self.W[l].numel() // nc,
+                                     C.c_float(self.lr), s))
+            _check(lib_.mcf_sgd_grow(self.b[l].data_ptr(), nc, gv[2 * l + 1].data_ptr(), self.b[l].numel() // nc,
+                                     C.c_float(self.lr), s))
+        return B["loss"]
+
+    @staticmethod
+    def loss_value(loss_sum: torch.Tensor, n_global: int) -> float:
+        """fl_div(sum of terms, N) in binary32 (autodiff.hpp:575) -- on the host,
+        where the step's result is read anyway (a device scalar division by a
+        Python number may be evaluated as a multiplication by its reciprocal)."""
+        return float(np.float32(loss_sum.item()) / np.float32(n_global))
+
+    def params_numpy(self):
+        torch.cuda.synchronize()
+        return [(w.cpu().numpy(), b.cpu().numpy()) for w, b in zip(self.W, self.b)]
+
+
+__all__ = ["init_params", "make_batch", "GradExchange", "MCMLP", "SEQUENTIAL", "FAST"]

@@ -1,0 +1,81 @@
+"""Data-parallel logic of the MC-MLP step on CPU (world_size 2, gloo).
+
+Each rank holds a different gradient shard in the flat buffer of
+paper_2207_08867_b200.mlp.GradExchange; after all_reduce both ranks hold the
+sum, and applying the MC-SGD update (grow_expn with -lr*g, through the oracle
+here: no GPU on CPU) leaves the MC parameters bitwise identical on every rank.
+Row-sharding helpers of the MC mm are checked to tile the output exactly.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    from paper_2207_08867_b200.mlp import GradExchange
+
+    shapes = [(6, 5), (6,), (3, 6), (3,)]
+    ex = GradExchange(shapes, "cpu", group=dist.group.WORLD)
+    g = torch.Generator().manual_seed(100 + rank)
+    for v in ex.views:
+        v.copy_(torch.randn(v.shape, generator=g))
+    mine = ex.flat.clone()
+    loss = torch.tensor([float(rank + 1)])
+    ex.all_reduce(loss)
+    # every rank's contribution, gathered for the check
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    want = parts[0].clone()
+    for p in parts[1:]:
+        want += p
+    assert torch.equal(ex.flat, want)
+    assert loss.item() == sum(range(1, world + 1))
+    # identical MC-SGD update on every rank (momentum 0): w <- grow_expn(w, -(lr * (0 + g)))
+    port = oracle.Oracle("port")
+    rng = np.random.default_rng(5)  # same seed on all ranks: replicated weights
+    w = np.stack([rng.uniform(-1, 1, 30).astype(np.float32), np.zeros(30, np.float32)], -1)
+    gflat = ex.views[0].numpy().ravel().astype(np.float32)
+    lr = np.float32(0.01)
+    delta = -(lr * (np.float32(0) + gflat)).astype(np.float32)
+    w_new = port.grow_expn(w, delta)
+    np.save(os.path.join(outdir, f"w{rank}.npy"), w_new)
+    dist.destroy_process_group()
+
+
+def test_gradient_allreduce_and_identical_updates(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    w0 = np.load(tmp_path / "w0.npy")
+    w1 = np.load(tmp_path / "w1.npy")
+    assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+
+
+@pytest.mark.parametrize("m,world", [(4096, 1), (4096, 2), (4096, 8), (10, 8), (1023, 4)])
+def test_row_shards_tile_the_output(m, world):
+    rows = []
+    for r in range(world):
+        r0, r1 = r * m // world, (r + 1) * m // world
+        rows.append((r0, r1))
+    assert rows[0][0] == 0 and rows[-1][1] == m
+    for (a0, a1), (b0, b1) in zip(rows, rows[1:]):
+        assert a1 == b0 and a0 <= a1
