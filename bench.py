@@ -202,6 +202,100 @@ def elementwise_suite(torch, mcf, hbm_gbs):
     return res
 
 
+def _dev_time(torch, fn, reps, flush=None):
+    for _ in range(2):
+        fn()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def other_configs(torch, mcf, hbm_gbs, f64_peak):
+    """BASELINE configs 1, 3 and 4 on this GPU (1-GPU shapes at full size).
+    Inputs are drawn on the device (torch CUDA generator, seeded) with each
+    config's distribution; parity for these paths is in tests/."""
+    import numpy as np
+
+    from paper_2207_08867_b200 import mlp
+
+    g = torch.Generator(device="cuda").manual_seed(2207)
+    res = {}
+
+    def cfg0_dist(shape, nc, dtype=torch.float32, scale=1.0):
+        v = (torch.rand(shape, generator=g, device="cuda", dtype=torch.float64) * 2 - 1)
+        v = v * torch.exp2(torch.rand(shape, generator=g, device="cuda", dtype=torch.float64) * 16 - 8) * scale
+        comps = []
+        for _ in range(nc):
+            c = v.to(dtype)
+            comps.append(c)
+            v = v - c.to(torch.float64)
+        return torch.stack(comps, -1).contiguous()
+
+    # config 1a: MC (65536 x 4096, nc=3) x T vector, FAST (HBM-bound)
+    M, K = 65536, 4096
+    x = cfg0_dist((M, K), 3)
+    v = cfg0_dist((K,), 1)[..., 0].contiguous()
+    ms = _dev_time(torch, lambda: mcf.mv_mcn(x, v, plan=mcf.FAST), 5)
+    byts = M * K * 12 + K * 4 + M * 12
+    res["config1a_mv_nc3"] = {"shape": [M, K, 3], "ms": round(ms, 4), "GB/s": round(byts / ms / 1e6, 1),
+                              "frac_hbm": round(byts / ms / 1e6 / hbm_gbs, 3),
+                              "GMAD/s": round(M * K / ms / 1e6, 1)}
+    # config 1b: 65536 independent MC x MC dots (length 4096, nc=3)
+    y = cfg0_dist((M, K), 3)
+    ms = _dev_time(torch, lambda: mcf.dot_mcmc(x, y, plan=mcf.FAST), 5)
+    byts = 2 * M * K * 12 + M * 12
+    res["config1b_dots_mcmc_nc3"] = {"shape": [M, K, 3], "ms": round(ms, 4), "GB/s": round(byts / ms / 1e6, 1),
+                                     "frac_hbm": round(byts / ms / 1e6 / hbm_gbs, 3)}
+    del x, y, v
+    torch.cuda.empty_cache()
+    # config 3: MC-MLP 784-1024-1024-10, nc=2, batch 8192 on one GPU, MC-SGD lr 0.01
+    dims = [784, 1024, 1024, 10]
+    params = mlp.init_params(dims, 2)
+    xb, yb = mlp.make_batch(8192)
+    model = mlp.MCMLP(dims, params, lr=0.01, plan=mcf.FAST)
+    xt = torch.from_numpy(np.ascontiguousarray(xb.T)).cuda()
+    yt = torch.from_numpy(yb).cuda()
+    first = model.loss_value(model.step(xt, yt, 8192), 8192)
+    ms = _dev_time(torch, lambda: model.step(xt, yt, 8192), 10)
+    last = model.loss_value(model.step(xt, yt, 8192), 8192)
+    res["config3_mlp"] = {"dims": dims, "batch": 8192, "ms_per_step": round(ms, 3),
+                          "steps_per_s": round(1e3 / ms, 2), "loss_first": first, "loss_after_14_steps": last}
+    del model, xt, yt
+    # config 4: MC x MC 16384^3, fp32 nc=2 and fp16 nc=3 (values U[-1,1]/64)
+    N4 = 16384
+    u = lambda:(torch.rand((N4, N4), generator=g, device="cuda", dtype=torch.float64) * 2 - 1)
+    for tag, dtype, nc, scale, reps in (("fp32_nc2", torch.float32, 2, 1.0, 1), ("fp16_nc3", torch.float16, 3, 1 / 64, 2)):
+        va, vb = u() * scale, u() * scale
+
+        def split(v):
+            comps = []
+            for _ in range(nc):
+                c = v.to(dtype)
+                comps.append(c)
+                v = v - c.to(torch.float64)
+            return torch.stack(comps, -1).contiguous()
+
+        a, b = split(va), split(vb)
+        del va, vb
+        ms = _dev_time(torch, lambda: mcf.mm_mcmc(a, b, plan=mcf.FAST), reps)
+        ops = mcf.lib().mcf_fast_ops_per_mad(1, mcf.B32 if nc == 2 else mcf.B16, nc)
+        res[f"config4_mcmc_{tag}"] = {"M=N=K": N4, "ms": round(ms, 2),
+                                       "GFLOP/s_eff": round(2 * N4 ** 3 / ms / 1e6, 1),
+                                       "fp64_ops_per_mad": ops,
+                                       "frac_fp64_peak": round(ops * N4 ** 3 / (ms * 1e-3) / 1e12 / f64_peak, 3)}
+        del a, b
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -295,11 +389,18 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_val = 2.0 * M * N * K / e2e_s / 1e9
+    h2d_bytes = int(a_pin.numel() * 4 + b_pin.numel() * 4)
+    d2h_bytes = int(o_pin.numel() * 4)
 
     ew = None
     cpu = None
+    others = None
     if rank == 0 and world == 1:
+        del a, b, out, a_pin, b_pin, o_pin
+        torch.cuda.empty_cache()
         ew = elementwise_suite(torch, mcf, hbm)
+        if not args.no_extras:
+            others = other_configs(torch, mcf, hbm, peak64)
         gf, t, nrows, kind = reference_sample(a_h, b_h, cpu_threads())
         cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cpu_threads(), "kind": kind,
                "sample": f"{nrows} full output rows of the 4096^3 product, one row per host thread ({t:.1f} s)"}
@@ -317,8 +418,7 @@ def run_ours(args):
                          "traffic": None, "ops_per_mad": ops_per_mad,
                          "peak_source": "measured in this run by mcf_probe_pipe_rates (DFMA chains, all SMs)"},
             "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
-                    "h2d_bytes_per_step": int(a_pin.numel() * 4 + b_pin.numel() * 4),
-                    "d2h_bytes_per_step": int(o_pin.numel() * 4)},
+                    "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes},
             "gpu_launches": launches,
             "clocks": clk.summary,
         }
@@ -327,6 +427,8 @@ def run_ours(args):
         if ew:
             line["elementwise"] = {"config": "config0: 2^24 elements, fp32 nc=2, bit-exact vs reference",
                                    "hbm_peak_gbs": hbm, "ops": ew}
+        if others:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -339,6 +441,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip configs 1, 3, 4 (headline + config 0 only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
