@@ -59,6 +59,63 @@ __global__ void __launch_bounds__(256) k_widen(const ST* __restrict__ in, double
   }
 }
 
+// ---- power-of-two operand scaling for the offset-accumulation policies ---------------
+// Row i of A is scaled by 2^-ea[i], column j of B by 2^-eb[j], with 2^e the
+// smallest power of two above the largest leading component, so every
+// leading product is below 1 in magnitude.  Scaling by powers of two is exact
+// in binary64 and undone on the output.
+
+__device__ __forceinline__ int exp_above(float m) { return m > 0.0f ? ilogbf(m) + 1 : 0; }
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+
+template <class ST, int NC>
+__global__ void __launch_bounds__(256) k_rowexp(const ST* __restrict__ a, int64_t rows, int64_t k,
+                                                 int* __restrict__ e) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float m = 0.0f;
+  for (int64_t t = lane; t < k; t += 32) m = fmaxf(m, fabsf((float)to_d<ST>(a[(r * k + t) * NC])));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) e[r] = exp_above(m);
+}
+
+template <class ST, int NC>
+__global__ void __launch_bounds__(256) k_colexp(const ST* __restrict__ b, int64_t k, int64_t n,
+                                                 int* __restrict__ e) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float m = 0.0f;
+  for (int64_t t = 0; t < k; ++t) m = fmaxf(m, fabsf((float)to_d<ST>(b[(t * n + j) * NC])));
+  e[j] = exp_above(m);
+}
+
+// out = in * 2^-e[row] (BY_ROW, rows of `cols` elements) or * 2^-e[col].
+// PAIR: each nc=2 element becomes (sum, err) = two_sum(c0, c1) in binary64
+// (sum + err == c0 + c1 exactly); any nonzero err raises *inexact.
+template <class ST, int NC, bool BY_ROW, bool PAIR>
+__global__ void __launch_bounds__(256) k_widen_scaled(const ST* __restrict__ in, double* __restrict__ out,
+                                                       int64_t rows, int64_t cols, const int* __restrict__ e,
+                                                       int* __restrict__ inexact) {
+  const int64_t elems = rows * cols;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < elems; x += stride) {
+    const double s = pow2(-(BY_ROW ? e[x / cols] : e[x % cols]));
+    if constexpr (PAIR) {
+      static_assert(NC == 2, "pairs are formed from two components");
+      double sum, err;
+      dsum(to_d<ST>(in[x * 2]), to_d<ST>(in[x * 2 + 1]), sum, err);
+      out[x * 2] = __dmul_rn(sum, s);
+      out[x * 2 + 1] = __dmul_rn(err, s);
+      if (err != 0.0) atomicOr(inexact, 1);
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) out[x * NC + c] = __dmul_rn(to_d<ST>(in[x * NC + c]), s);
+    }
+  }
+}
+
 // ---- cp.async helpers ------------------------------------------------------------------
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem, bool valid) {
@@ -87,11 +144,15 @@ struct Tile {
 // Thread (ty, tx) owns rows ty + i*(BM/TM) and columns tx + j*(BN/TN): a
 // warp's B loads are consecutive doubles (conflict-free), its A loads two
 // broadcast rows 16 B apart in bank space.
-template <class Acc, class OST, int NCO, int BM, int BN, int BK, int TM, int TN>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN), 1)
+template <class Acc, class OST, int NCO, int BM, int BN, int BK, int TM, int TN, int MINB = 1>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
     k_mm_fast(const double* __restrict__ A, const double* __restrict__ B, OST* __restrict__ Cout,
               int64_t M, int64_t N, int64_t K, int64_t a_bstride, int64_t b_bstride,
-              int64_t c_bstride) {
+              int64_t c_bstride, const int* __restrict__ row_e, const int* __restrict__ col_e,
+              double sigma, const int* __restrict__ inexact, int want_inexact) {
+  // the exact-sum and the err-carrying variants are both launched; the
+  // widening pass's flag decides which one runs (the other exits here)
+  if (inexact && ((*inexact != 0) != (want_inexact != 0))) return;
   constexpr int NA = Acc::kNA, NB = Acc::kNB;
   using T = Tile<NA, NB, BM, BN, BK, TM, TN>;
   constexpr int RS = BM / TM;  // row stride between a thread's rows
@@ -133,7 +194,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 1)
 #pragma unroll
     for (int j = 0; j < TN; ++j)
 #pragma unroll
-      for (int l = 0; l < Acc::kLv; ++l) acc[i][j][l] = 0.0;
+      for (int l = 0; l < Acc::kLv; ++l) acc[i][j][l] = l == 0 ? sigma : 0.0;
 
 #pragma unroll
   for (int s = 0; s < T::kStages - 1; ++s) {
@@ -176,17 +237,27 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 1)
     for (int j = 0; j < TN; ++j) {
       const int64_t c = n0 + tx + j * (BN / TN);
       if (c >= N) continue;
-      split_out<OST, NCO, Acc::kLv>(acc[i][j], Cout + (r * N + c) * NCO);
+      if (row_e) {
+        // offset policies: S = tau - sigma (exact), undo the operand scaling
+        const double sc = pow2(row_e[bz * M + r] + col_e[(b_bstride ? bz * N : 0) + c]);
+        double v[Acc::kLv];
+#pragma unroll
+        for (int l = 0; l < Acc::kLv; ++l) v[l] = __dmul_rn(l == 0 ? __dsub_rn(acc[i][j][0], sigma) : acc[i][j][l], sc);
+        split_out<OST, NCO, Acc::kLv>(v, Cout + (r * N + c) * NCO);
+      } else {
+        split_out<OST, NCO, Acc::kLv>(acc[i][j], Cout + (r * N + c) * NCO);
+      }
     }
   }
 }
 
-template <class Acc, class OST, int NCO, int BM, int BN, int BK, int TM, int TN>
+template <class Acc, class OST, int NCO, int BM, int BN, int BK, int TM, int TN, int MINB = 1>
 mcf_status launch_mm(const double* A, const double* B, void* C, int64_t batch, int64_t M,
                      int64_t N, int64_t K, int64_t a_bs, int64_t b_bs, int64_t c_bs,
-                     cudaStream_t s) {
+                     cudaStream_t s, const int* row_e = nullptr, const int* col_e = nullptr,
+                     double sigma = 0.0, const int* inexact = nullptr, int want_inexact = 0) {
   using T = Tile<Acc::kNA, Acc::kNB, BM, BN, BK, TM, TN>;
-  auto kern = k_mm_fast<Acc, OST, NCO, BM, BN, BK, TM, TN>;
+  auto kern = k_mm_fast<Acc, OST, NCO, BM, BN, BK, TM, TN, MINB>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem) != cudaSuccess)
@@ -194,9 +265,39 @@ mcf_status launch_mm(const double* A, const double* B, void* C, int64_t batch, i
     attr = true;
   }
   const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)batch);
-  kern<<<grid, T::kThreads, T::kSmem, s>>>(A, B, static_cast<OST*>(C), M, N, K, a_bs, b_bs, c_bs);
+  kern<<<grid, T::kThreads, T::kSmem, s>>>(A, B, static_cast<OST*>(C), M, N, K, a_bs, b_bs, c_bs, row_e,
+                                            col_e, sigma, inexact, want_inexact);
   mcfr::note_launch();
   return mcfr::check_launch("mm_fast kernel");
+}
+
+// sigma = 2^(ceil(log2 K) + 1): every partial sum of products below 1 in
+// magnitude stays below sigma / 2
+double offset_sigma(int64_t k) {
+  int e = 0;
+  while ((int64_t(1) << e) < k) ++e;
+  return ldexp(1.0, e + 1);
+}
+
+// exponents + scaled widening of A (rows of k elements, nca comps) and B
+// (k x n, ncb comps); nc=2 operands become (sum, err) pairs, *inexact is
+// cleared first and raised if any err is nonzero
+template <int NCA, int NCB>
+mcf_status widen_scaled(const float* x, const float* w, int64_t rows, int64_t k, int64_t brows, int64_t n,
+                        double* xd, double* wd, int* ea, int* eb, int* inexact, cudaStream_t s) {
+  if (cudaMemsetAsync(inexact, 0, sizeof(int), s) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the exactness flag");
+  k_rowexp<float, NCA><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(x, rows, k, ea);
+  mcfr::note_launch();
+  k_colexp<float, NCB><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w, brows, n, eb);
+  mcfr::note_launch();
+  k_widen_scaled<float, NCA, true, NCA == 2><<<mcfr::grid_for(rows * k, 256, 8), 256, 0, s>>>(x, xd, rows, k, ea,
+                                                                                              inexact);
+  mcfr::note_launch();
+  k_widen_scaled<float, NCB, false, NCB == 2><<<mcfr::grid_for(brows * n, 256, 8), 256, 0, s>>>(w, wd, brows, n, eb,
+                                                                                                inexact);
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_fast scaling kernels");
 }
 
 template <class ST, int NC, bool SUM>
@@ -295,8 +396,8 @@ namespace mcfr {
 // FP64-pipe instructions per multiply-add of the kernel a fast call uses
 int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) {
   using namespace mcfg;
-  if (p == MCF_B32 && !mcmc) return nc == 2 ? AccT2::kOps : nc == 3 ? AccT3::kOps : 0;
-  if (p == MCF_B32 && mcmc) return nc == 2 ? AccM2::kOps : nc == 3 ? AccM3::kOps : 0;
+  if (p == MCF_B32 && !mcmc) return nc == 2 ? AccP2<1>::kOps : nc == 3 ? AccT3::kOps : 0;
+  if (p == MCF_B32 && mcmc) return nc == 2 ? AccP2<2>::kOps : nc == 3 ? AccM3::kOps : 0;
   return (p == MCF_B16 && mcmc && nc == 3) ? AccH3::kOps : 0;
 }
 
@@ -308,18 +409,34 @@ mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t
   if (p != MCF_B32 || (nc != 2 && nc != 3) || n % 2 != 0 || (k * nc) % 2 != 0)
     return MCF_ERR_UNSUPPORTED;
   const int64_t xa = batch * m * k * nc, wb = (w_batched ? batch : 1) * k * n;
-  double* ws = stream_workspace((xa + wb) * sizeof(double) + 256, s);
+  const int64_t ne = batch * m + (w_batched ? batch : 1) * n;  // scale exponents
+  double* ws = stream_workspace((xa + wb) * sizeof(double) + ne * sizeof(int) + 512, s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the binary64 workspace");
   double* xd = ws;
   double* wd = ws + ((xa + 1) / 2) * 2;  // 16-byte aligned
+  const int64_t a_bs = m * k * nc, b_bs = w_batched ? k * n : 0, c_bs = m * n * nc;
+  if (nc == 2 && !w_batched) {
+    // offset accumulation on (sum, err) operands: rows of A and columns of B
+    // scaled by powers of two (AccP2 / AccP2X, see mcf_accum.cuh)
+    int* ea = reinterpret_cast<int*>(wd + ((wb + 1) / 2) * 2);
+    int* eb = ea + batch * m;
+    int* flag = eb + n;
+    mcf_status st = widen_scaled<2, 1>(static_cast<const float*>(x), static_cast<const float*>(w), batch * m, k, k,
+                                       n, xd, wd, ea, eb, flag, s);
+    if (st != MCF_OK) return st;
+    const double sg = offset_sigma(k);
+    st = launch_mm<AccP2<1>, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea, eb,
+                                                          sg, flag, 0);
+    if (st != MCF_OK) return st;
+    return launch_mm<AccP2X<1>, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea,
+                                                             eb, sg, flag, 1);
+  }
   mcf_status st = nc == 2 ? widen<float, 2, false>(x, xd, batch * m * k, s)
                           : widen<float, 3, false>(x, xd, batch * m * k, s);
   if (st != MCF_OK) return st;
   st = widen<float, 1, false>(w, wd, wb, s);
   if (st != MCF_OK) return st;
-  const int64_t a_bs = m * k * nc, b_bs = w_batched ? k * n : 0, c_bs = m * n * nc;
-  if (nc == 2)
-    return launch_mm<AccT2, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
+  if (nc == 2) return launch_mm<AccT2, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
   return launch_mm<AccT3, float, 3, 64, 64, 16, 4, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
 }
 
@@ -330,16 +447,23 @@ mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
   if ((!f32 && !f16) || n % 2 != 0 || k % 2 != 0) return MCF_ERR_UNSUPPORTED;
   const int w = f32 ? 2 : 1;  // binary64 words per element after widening
   const int64_t xa = m * k * w, yb = k * n * w;
-  double* ws = stream_workspace((xa + yb) * sizeof(double) + 256, s);
+  double* ws = stream_workspace((xa + yb) * sizeof(double) + (m + n) * sizeof(int) + 512, s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the binary64 workspace");
   double* xd = ws;
   double* yd = ws + ((xa + 1) / 2) * 2;
   mcf_status st;
   if (f32) {
-    st = widen<float, 2, false>(x, xd, m * k, s);
-    if (st == MCF_OK) st = widen<float, 2, false>(y, yd, k * n, s);
+    int* ea = reinterpret_cast<int*>(yd + ((yb + 1) / 2) * 2);
+    int* eb = ea + m;
+    int* flag = eb + n;
+    st = widen_scaled<2, 2>(static_cast<const float*>(x), static_cast<const float*>(y), m, k, k, n, xd, yd, ea, eb,
+                            flag, s);
     if (st != MCF_OK) return st;
-    return launch_mm<AccM2, float, 2, 128, 64, 16, 8, 4>(xd, yd, out, 1, m, n, k, 0, 0, 0, s);
+    const double sg = offset_sigma(k);
+    st = launch_mm<AccP2<2>, float, 2, 128, 64, 16, 8, 4>(xd, yd, out, 1, m, n, k, 0, 0, 0, s, ea, eb, sg, flag, 0);
+    if (st != MCF_OK) return st;
+    return launch_mm<AccP2X<2>, float, 2, 128, 64, 16, 8, 4>(xd, yd, out, 1, m, n, k, 0, 0, 0, s, ea, eb, sg, flag,
+                                                             1);
   }
   st = widen<__half, 3, true>(x, xd, m * k, s);
   if (st == MCF_OK) st = widen<__half, 3, true>(y, yd, k * n, s);
