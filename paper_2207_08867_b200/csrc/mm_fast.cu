@@ -211,7 +211,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
     }
     const double* As = smem + (kt % T::kStages) * T::kStageElems;
     const double* Bs = As + BM * T::kRowA;
-#pragma unroll 1
+    // unrolled by 2 so the running value's old and new registers alternate
+    // instead of being copied (IMAD.MOV pairs) every step
+#pragma unroll 2
     for (int k = 0; k < BK; ++k) {
       double a[TM][NA], b[TN * NB];
 #pragma unroll
