@@ -4,11 +4,13 @@
 // Every product of two binary32 components is exact in binary64, so an
 // output is carried as a short binary64 expansion: level 0 takes the leading
 // product through an error-free two_sum, lower levels take products and
-// rounding errors ~2^-24 / 2^-48 smaller.  Policies:
-//   AccT2  MC(nc=2) x T      (S, C)      9 FP64 ops / MAD
-//   AccT3  MC(nc=3) x T      (S, C, D)  23 ops / MAD
-//   AccM2  MC(nc=2) x MC(2)  (S, C)     11 ops / MAD
-//   AccM3  MC(nc=3) x MC(3)  (S, C, D)  33 ops / MAD
+// rounding errors ~2^-24 / 2^-48 smaller.  Policies (FP64 ops per MAD):
+//   AccP2<NB>  nc=2 x T / MC(2), offset accumulation on (sum, err) pairs   4
+//   AccP2X<NB> same, err terms folded in (used when the widening flag is set) 5/7
+//   AccT2  MC(nc=2) x T      (S, C)      6  (streaming kernels)
+//   AccT3  MC(nc=3) x T      (S, C, D)  14
+//   AccM2  MC(nc=2) x MC(2)  (S, C)      8
+//   AccM3  MC(nc=3) x MC(3)  (S, C, D)  23
 //   AccH3  MC(nc=3, binary16) x MC(3, binary16), operands pre-summed into one
 //          binary64 each (<= 33 significant bits): S = fma(a, b, S), 1 op
 // merge() combines two partial expansions (warp reductions); the final value

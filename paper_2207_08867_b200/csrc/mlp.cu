@@ -152,14 +152,27 @@ __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_
   }
 }
 
-// g (rows x n): out[r] = sum_j g[r, j], j increasing, starting from 0
-__global__ void __launch_bounds__(256) k_rowsum(const float* __restrict__ g, int64_t rows, int64_t n,
-                                                float* __restrict__ out) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
+// g (rows x n): out[r] = sum_j g[r, j], j increasing, starting from 0.
+// One warp per 32 rows: the warp loads 32 x 32 tiles coalesced (rows of g are
+// contiguous), transposes through shared memory, and lane l adds row l's 32
+// values in order -- the same left-to-right chain as the reference.
+__global__ void __launch_bounds__(32) k_rowsum(const float* __restrict__ g, int64_t rows, int64_t n,
+                                               float* __restrict__ out) {
+  __shared__ float tile[32][33];
+  const int lane = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
   float acc = 0.0f;
-  for (int64_t j = 0; j < n; ++j) acc = __fadd_rn(acc, g[r * n + j]);
-  out[r] = acc;
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t r = r0 + rr, j = j0 + lane;
+      tile[rr][lane] = (r < rows && j < n) ? g[r * n + j] : 0.0f;
+    }
+    __syncwarp();
+    const int cnt = (int)((n - j0) < 32 ? (n - j0) : 32);
+    for (int c = 0; c < cnt; ++c) acc = __fadd_rn(acc, tile[lane][c]);
+    __syncwarp();
+  }
+  if (r0 + lane < rows) out[r0 + lane] = acc;
 }
 
 template <int NC>
@@ -249,7 +262,7 @@ mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_
 
 mcf_status mcf_rowsum_f32_ordered(const float* g, int64_t rows, int64_t n, float* out, mcf_stream s) {
   if (rows == 0) return MCF_OK;
-  mcfg::k_rowsum<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(g, rows, n, out);
+  mcfg::k_rowsum<<<(unsigned)((rows + 31) / 32), 32, 0, s>>>(g, rows, n, out);
   return launched("row-sum kernel");
 }
 
