@@ -45,6 +45,18 @@ def peaks():
         return {}
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the mm kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic_*.json, newest round), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_traffic_r*.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    return d.get("traffic_bytes_per_launch"), os.path.relpath(files[-1], ROOT)
+
+
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -405,6 +417,7 @@ def run_ours(args):
         cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cpu_threads(), "kind": kind,
                "sample": f"{nrows} full output rows of the 4096^3 product, one row per host thread ({t:.1f} s)"}
 
+    traffic, traffic_src = ncu_traffic()
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -415,7 +428,8 @@ def run_ours(args):
                        "l2": "256 MiB buffer written between timed steps"},
             "roofline": {"bound": "fp64_fma_pipe", "achieved": round(achieved, 3), "peak": round(peak64, 3),
                          "unit": "TFLOP/s", "frac": round(achieved / peak64, 3) if peak64 else None,
-                         "traffic": None, "ops_per_mad": ops_per_mad,
+                         "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
+                         "traffic_source": traffic_src, "ops_per_mad": ops_per_mad,
                          "peak_source": "measured in this run by mcf_probe_pipe_rates (DFMA chains, all SMs)"},
             "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes},

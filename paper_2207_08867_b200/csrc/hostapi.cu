@@ -145,8 +145,18 @@ mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64
   auto align = [](std::size_t b) { return (b + 255) & ~std::size_t(255); };
   char* d = static_cast<char*>(mcfr::workspace(align(bx) + align(bw) + align(bo) + 256, 0));
   if (!d) return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot allocate device workspace");
-  cudaStream_t s = mcfr::side_stream(0);
   char *dx = d, *dw = d + align(bx), *dout = dw + align(bw);
+  if (strategy == MCF_FAST && p == MCF_B32 && nc == 2 && batch == 1 && m >= 1024 && k > 0 &&
+      mcfr::ensure_device_tables() == MCF_OK) {
+    // the headline shape: row-chunked so the copies overlap the FP64 mm
+    const cudaStream_t comp[2] = {mcfr::side_stream(4), mcfr::side_stream(5)};
+    const mcf_status st = mcfr::mm_fast_mct_host(
+        static_cast<const float*>(x), static_cast<const float*>(w), m, k, n, static_cast<float*>(out),
+        reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dw), reinterpret_cast<float*>(dout),
+        mcfr::side_stream(3), comp, mcfr::side_stream(6));
+    if (st != MCF_ERR_UNSUPPORTED) return st;
+  }
+  cudaStream_t s = mcfr::side_stream(0);
   if (bx) TRY(cuda_ok(cudaMemcpyAsync(dx, x, bx, cudaMemcpyHostToDevice, s), "H2D x"));
   if (bw) TRY(cuda_ok(cudaMemcpyAsync(dw, w, bw, cudaMemcpyHostToDevice, s), "H2D w"));
   TRY(mcf_bmm_mcn(p, dx, nc, dw, batch, m, k, n, w_batched, dout, strategy, 1, s));

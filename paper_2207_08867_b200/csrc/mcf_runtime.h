@@ -56,6 +56,10 @@ mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
 mcf_status dot_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch, int64_t k,
                          void* out, cudaStream_t s);
 int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
+// host-buffer MC(nc=2, binary32) x T, pipelined over row chunks (hostapi.cu)
+mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout,
+                            float* dx, float* dw, float* dout, cudaStream_t cin, const cudaStream_t comp[2],
+                            cudaStream_t cout);
 
 // device workspace for the host-buffer entry points (grows, per device)
 void* workspace(std::size_t bytes, int slot);

@@ -1,14 +1,15 @@
 // mm_fast.cu -- throughput MC contractions on the FP64 pipe (plan MCF_FAST).
 //
 // Each product of two binary32 (or binary16) components is exact in
-// binary64 (24+24 <= 53 bits).  The GPU therefore carries every output as a
-// compensated binary64 expansion (S, C[, D]) in registers through the K loop:
+// binary64 (24+24 <= 53 bits).  The GPU therefore carries every output as an
+// extended binary64 accumulator in registers through the K loop (policies in
+// mcf_accum.cuh):
 //
-//   MC x T, nc=2:  p = a0*b (exact); (S, e) = two_sum(S, p); C += e;
-//                  C = fma(a1, b, C)                      -> 9 FP64 ops / MAD
-//   MC x T, nc=3:  three levels (S, C, D), 2 two_sums more -> 23 ops / MAD
-//   MC x MC, nc=2: p = a0*b0 into (S, C) as above, the cross terms a0*b1,
-//                  a1*b0, a1*b1 fused into C              -> 11 ops / MAD
+//   nc=2 (MC x T and MC x MC): operands widened to (sum, err) pairs and scaled
+//     by powers of two per row of A / column of B; offset accumulation
+//     t = fma(a,b,tau), q = t - tau, C += fma(a,b,-q)   -> 4 FP64 ops / MAD
+//     (5-7 when some err is nonzero: AccP2X, chosen by a device flag)
+//   MC x T, nc=3:  three levels (S, C, D)                 -> 14 ops / MAD
 //   MC x MC, fp16 nc=3: components summed into one binary64 per operand
 //                  (<= 33 significant bits), S = fma(a, b, S) -> 1 op / MAD
 //
@@ -24,15 +25,17 @@
 // path.  Operands are widened once to binary64 (a streaming pass into a
 // per-stream workspace), tiles are staged global->shared with cp.async
 // (LDGSTS, 16-byte chunks, 3-stage ring), and each thread owns a TM x TN
-// block of outputs with interleaved rows (conflict-free 128-bit LDS).
+// block of outputs with interleaved rows and columns (conflict-free LDS).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <mutex>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "mcf_accum.cuh"
 #include "mcf_runtime.h"
@@ -65,7 +68,8 @@ __global__ void __launch_bounds__(256) k_widen(const ST* __restrict__ in, double
 // leading product is below 1 in magnitude.  Scaling by powers of two is exact
 // in binary64 and undone on the output.
 
-__device__ __forceinline__ int exp_above(float m) { return m > 0.0f ? ilogbf(m) + 1 : 0; }
+// (non-finite maxima leave the row / column unscaled: Inf and NaN propagate)
+__device__ __forceinline__ int exp_above(float m) { return m > 0.0f && isfinite(m) ? ilogbf(m) + 1 : 0; }
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
 template <class ST, int NC>
@@ -81,14 +85,27 @@ __global__ void __launch_bounds__(256) k_rowexp(const ST* __restrict__ a, int64_
   if (lane == 0) e[r] = exp_above(m);
 }
 
+// column maxima of B (k x n, row-major): CTA (x, y) covers 256 columns of a
+// kColRows-row slab, coalesced along n; slabs meet through atomicMax on the
+// bit pattern (monotone in the magnitude for non-negative binary32; e must
+// start at 0).  k_colexp_fin turns the maxima into exponents in place.
+constexpr int kColRows = 64;
+
 template <class ST, int NC>
-__global__ void __launch_bounds__(256) k_colexp(const ST* __restrict__ b, int64_t k, int64_t n,
+__global__ void __launch_bounds__(256) k_colmax(const ST* __restrict__ b, int64_t k, int64_t n,
                                                  int* __restrict__ e) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
+  const int64_t t0 = (int64_t)blockIdx.y * kColRows;
+  const int64_t t1 = t0 + kColRows < k ? t0 + kColRows : k;
   float m = 0.0f;
-  for (int64_t t = 0; t < k; ++t) m = fmaxf(m, fabsf((float)to_d<ST>(b[(t * n + j) * NC])));
-  e[j] = exp_above(m);
+  for (int64_t t = t0; t < t1; ++t) m = fmaxf(m, fabsf((float)to_d<ST>(b[(t * n + j) * NC])));
+  if (m > 0.0f) atomicMax(e + j, __float_as_int(m));
+}
+
+__global__ void __launch_bounds__(256) k_colexp_fin(int* __restrict__ e, int64_t n) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) e[j] = exp_above(__int_as_float(e[j]));
 }
 
 // out = in * 2^-e[row] (BY_ROW, rows of `cols` elements) or * 2^-e[col].
@@ -284,22 +301,46 @@ double offset_sigma(int64_t k) {
 // exponents + scaled widening of A (rows of k elements, nca comps) and B
 // (k x n, ncb comps); nc=2 operands become (sum, err) pairs, *inexact is
 // cleared first and raised if any err is nonzero
+// B side: column exponents and the scaled widening of B (raises *inexact,
+// which the caller has cleared)
+template <int NCB>
+mcf_status widen_scaled_b(const float* w, int64_t brows, int64_t n, double* wd, int* eb, int* inexact,
+                          cudaStream_t s) {
+  if (cudaMemsetAsync(eb, 0, n * sizeof(int), s) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the column maxima");
+  const dim3 g((unsigned)((n + 255) / 256), (unsigned)((brows + kColRows - 1) / kColRows));
+  if (brows > 0) {
+    k_colmax<float, NCB><<<g, 256, 0, s>>>(w, brows, n, eb);
+    mcfr::note_launch();
+  }
+  k_colexp_fin<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(eb, n);
+  mcfr::note_launch();
+  k_widen_scaled<float, NCB, false, NCB == 2><<<mcfr::grid_for(brows * n, 256, 8), 256, 0, s>>>(w, wd, brows, n, eb,
+                                                                                                inexact);
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_fast B scaling kernels");
+}
+
+// A side: row exponents and the scaled widening of A (rows x k)
+template <int NCA>
+mcf_status widen_scaled_a(const float* x, int64_t rows, int64_t k, double* xd, int* ea, int* inexact,
+                          cudaStream_t s) {
+  k_rowexp<float, NCA><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(x, rows, k, ea);
+  mcfr::note_launch();
+  k_widen_scaled<float, NCA, true, NCA == 2><<<mcfr::grid_for(rows * k, 256, 8), 256, 0, s>>>(x, xd, rows, k, ea,
+                                                                                              inexact);
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_fast A scaling kernels");
+}
+
 template <int NCA, int NCB>
 mcf_status widen_scaled(const float* x, const float* w, int64_t rows, int64_t k, int64_t brows, int64_t n,
                         double* xd, double* wd, int* ea, int* eb, int* inexact, cudaStream_t s) {
   if (cudaMemsetAsync(inexact, 0, sizeof(int), s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the exactness flag");
-  k_rowexp<float, NCA><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(x, rows, k, ea);
-  mcfr::note_launch();
-  k_colexp<float, NCB><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w, brows, n, eb);
-  mcfr::note_launch();
-  k_widen_scaled<float, NCA, true, NCA == 2><<<mcfr::grid_for(rows * k, 256, 8), 256, 0, s>>>(x, xd, rows, k, ea,
-                                                                                              inexact);
-  mcfr::note_launch();
-  k_widen_scaled<float, NCB, false, NCB == 2><<<mcfr::grid_for(brows * n, 256, 8), 256, 0, s>>>(w, wd, brows, n, eb,
-                                                                                                inexact);
-  mcfr::note_launch();
-  return mcfr::check_launch("mm_fast scaling kernels");
+  const mcf_status st = widen_scaled_a<NCA>(x, rows, k, xd, ea, inexact, s);
+  if (st != MCF_OK) return st;
+  return widen_scaled_b<NCB>(w, brows, n, wd, eb, inexact, s);
 }
 
 template <class ST, int NC, bool SUM>
@@ -440,6 +481,76 @@ mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t
   if (st != MCF_OK) return st;
   if (nc == 2) return launch_mm<AccT2, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
   return launch_mm<AccT3, float, 3, 64, 64, 16, 4, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s);
+}
+
+// Host-buffer MC(nc=2, binary32) x T product, pipelined over row chunks of A:
+// B is copied, scaled and widened once; then chunk c's H2D copy (stream cin),
+// its widening and mm (alternating comp[0] / comp[1], so one chunk's tail CTAs
+// overlap the next chunk's first ones) and its D2H copy (cout) overlap the
+// neighbouring chunks.  dx / dw / dout are device buffers of the full sizes.
+mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout,
+                            float* dx, float* dw, float* dout, cudaStream_t cin, const cudaStream_t comp[2],
+                            cudaStream_t cout) {
+  using namespace mcfg;
+  if (m <= 0 || k <= 0 || n <= 0 || n % 2 != 0) return MCF_ERR_UNSUPPORTED;
+  const int64_t rc = std::max<int64_t>(512, ((m + 7) / 8 + 127) / 128 * 128);
+  const int nch = (int)((m + rc - 1) / rc);
+  double* ws = stream_workspace((m * k * 2 + k * n) * sizeof(double) + (m + n + nch + 1) * sizeof(int) + 512,
+                                comp[0]);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the binary64 workspace");
+  double* xd = ws;
+  double* wd = ws + m * k * 2;
+  int* ea = reinterpret_cast<int*>(wd + ((k * n + 1) / 2) * 2);
+  int* eb = ea + m;
+  int* flag_b = eb + n;  // then one flag per chunk
+  std::vector<cudaEvent_t> ev(2 * nch + 2, nullptr);
+  for (auto& e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return fail(MCF_ERR_CUDA, "mm_fast: cannot create pipeline events");
+  auto done = [&](mcf_status st) {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    return st;
+  };
+  auto cu = [&](cudaError_t e, const char* what) {
+    return e == cudaSuccess ? MCF_OK : fail(MCF_ERR_CUDA, std::string("mm_mcn pipeline: ") + what + ": " +
+                                                              cudaGetErrorString(e));
+  };
+#define PIPE_TRY(expr)                    \
+  do {                                    \
+    const mcf_status _s = (expr);         \
+    if (_s != MCF_OK) return done(_s);    \
+  } while (0)
+  const double sg = offset_sigma(k);
+  PIPE_TRY(cu(cudaMemcpyAsync(dw, hw, k * n * sizeof(float), cudaMemcpyHostToDevice, cin), "H2D w"));
+  PIPE_TRY(cu(cudaEventRecord(ev[0], cin), "event"));
+  PIPE_TRY(cu(cudaStreamWaitEvent(comp[0], ev[0], 0), "wait"));
+  PIPE_TRY(cu(cudaMemsetAsync(flag_b, 0, sizeof(int), comp[0]), "flag"));
+  PIPE_TRY(widen_scaled_b<1>(dw, k, n, wd, eb, flag_b, comp[0]));
+  PIPE_TRY(cu(cudaEventRecord(ev[1], comp[0]), "event"));
+  PIPE_TRY(cu(cudaStreamWaitEvent(comp[1], ev[1], 0), "wait"));
+  for (int c = 0; c < nch; ++c) {
+    const int64_t r0 = c * rc, rows = std::min<int64_t>(rc, m - r0);
+    cudaStream_t cs = comp[c & 1];
+    cudaEvent_t ex = ev[2 + 2 * c], em = ev[3 + 2 * c];
+    int* fl = flag_b + 1 + c;
+    PIPE_TRY(cu(cudaMemcpyAsync(dx + r0 * k * 2, hx + r0 * k * 2, rows * k * 2 * sizeof(float),
+                                cudaMemcpyHostToDevice, cin), "H2D x"));
+    PIPE_TRY(cu(cudaEventRecord(ex, cin), "event"));
+    PIPE_TRY(cu(cudaStreamWaitEvent(cs, ex, 0), "wait"));
+    PIPE_TRY(cu(cudaMemcpyAsync(fl, flag_b, sizeof(int), cudaMemcpyDeviceToDevice, cs), "flag"));
+    PIPE_TRY(widen_scaled_a<2>(dx + r0 * k * 2, rows, k, xd + r0 * k * 2, ea + r0, fl, cs));
+    PIPE_TRY((launch_mm<AccP2<1>, float, 2, 128, 64, 16, 8, 4>(xd + r0 * k * 2, wd, dout + r0 * n * 2, 1, rows, n, k,
+                                                               0, 0, 0, cs, ea + r0, eb, sg, fl, 0)));
+    PIPE_TRY((launch_mm<AccP2X<1>, float, 2, 128, 64, 16, 8, 4>(xd + r0 * k * 2, wd, dout + r0 * n * 2, 1, rows, n,
+                                                                k, 0, 0, 0, cs, ea + r0, eb, sg, fl, 1)));
+    PIPE_TRY(cu(cudaEventRecord(em, cs), "event"));
+    PIPE_TRY(cu(cudaStreamWaitEvent(cout, em, 0), "wait"));
+    PIPE_TRY(cu(cudaMemcpyAsync(hout + r0 * n * 2, dout + r0 * n * 2, rows * n * 2 * sizeof(float),
+                                cudaMemcpyDeviceToHost, cout), "D2H out"));
+  }
+#undef PIPE_TRY
+  return done(cu(cudaStreamSynchronize(cout), "sync"));
 }
 
 mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,

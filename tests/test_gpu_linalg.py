@@ -243,3 +243,31 @@ def test_fast_plan_ragged_shapes_and_fallback(gr, port):
     # odd n: no fast instantiation -> reference order, bit-identical
     w3 = wp(rng, (130, 3), 32)
     assert_bits(gr.run("mm_mcn", x, w3, plan=mcf.FAST), port.mm_mcn(x, w3), "fallback")
+
+
+def test_host_pipelined_fast_mm_equals_device_path(gr, port):
+    """mcf_h_bmm_mcn's row-chunked pipeline (copies overlapping the mm, two
+    compute streams, per-chunk exactness flags) returns the device entry
+    point's bits; a chunk whose operands need the err-carrying kernel still
+    meets the tolerance."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(21)
+    m, k, n = 2000, 300, 96  # 4 chunks of 512 rows, the last one ragged
+    x = split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    w = rng.uniform(-1, 1, k * n).astype(np.float32).reshape(k, n)
+    dev = gr.run("mm_mcn", x, w, plan=mcf.FAST)
+    hst = mcf.host.mm_mcn(x, w, strategy=mcf.FAST)
+    assert_bits(hst, dev, "host pipeline vs device")
+    # components spanning > 53 bits in one chunk only: (sum, err) pairs there
+    x2 = x.copy()
+    x2[1500, :, 1] = (x2[1500, :, 0] * np.float32(2.0 ** -40)).astype(np.float32)
+    hst2 = mcf.host.mm_mcn(x2, w, strategy=mcf.FAST)
+    rows = np.repeat(np.array([0, 1499, 1500, 1999]), n)
+    cols = np.tile(np.arange(n), 4)
+    got = hst2[rows, cols]
+    ref = port.mm_mcn_sampled(x2, w, rows, cols)
+    gerr = port.relerr_mm_mct(x2, w, rows, cols, got.reshape(-1, 2))
+    rerr = port.relerr_mm_mct(x2, w, rows, cols, ref)
+    _check_within_4x(gerr, rerr, "host pipeline, inexact chunk")
