@@ -84,66 +84,119 @@ __global__ void __launch_bounds__(256) k_ce(const float* __restrict__ logits, co
   terms[s] = __fsub_rn(lse, logits[(int64_t)lab * n + s]);
 }
 
-__global__ void k_seqsum(const float* __restrict__ terms, int64_t n, float* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// the loss sum, left to right from 0; the block stages 2048-term slabs in
+// shared memory so thread 0's chain reads them at shared-memory latency
+__global__ void __launch_bounds__(256) k_seqsum(const float* __restrict__ terms, int64_t n, float* __restrict__ out) {
+  __shared__ float buf[2048];
   float acc = 0.0f;
-  for (int64_t i = 0; i < n; ++i) acc = __fadd_rn(acc, terms[i]);
-  out[0] = acc;
+  for (int64_t j0 = 0; j0 < n; j0 += 2048) {
+    const int cnt = (int)((n - j0) < 2048 ? (n - j0) : 2048);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) buf[t] = terms[j0 + t];
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int t = 0; t < cnt; ++t) acc = __fadd_rn(acc, buf[t]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = acc;
 }
 
 // C[i, j] = sum_k A(i, k) * B(k, j), k increasing, fl_mul then fl_add.
 // A(i, k) = TA ? a[k * lda + i] : a[i * lda + k];  B(k, j) = TB ? b[j * ldb + k] : b[k * ldb + j]
 // mask (optional): C[i, j] = mask[i * ldc + j] > 0 ? (0 + c) : 0  (ReLU backward)
-// zero_add: C = 0 + c (accumulation into a zero gradient)
-constexpr int GB = 64, GK = 16, GT = 256;  // 64x64 tile, 4x4 per thread
+// The chain per output is fixed by the reference (no split-K, no fma), so
+// the parallelism is the outputs: BM x BN tiles, 256 threads as 16 x 16,
+// each thread TM x TN outputs in two row halves and two column halves
+// (rows ty*TM/2 + u and BM/2 + ty*TM/2 + u; columns likewise), so a warp's
+// fragment loads are 128-bit and conflict-free.  K tiles of 16 staged
+// through shared memory (k-major, both operands), the next tile prefetched
+// into registers while the current one is consumed.
+constexpr int GK = 16, GT = 256;
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
                                              int64_t ldb, float* __restrict__ c, int64_t ldc, int64_t M, int64_t N,
                                              int64_t K, const float* __restrict__ mask) {
-  __shared__ float As[GK][GB + 1];
-  __shared__ float Bs[GK][GB + 1];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int64_t i0 = (int64_t)blockIdx.y * GB, j0 = (int64_t)blockIdx.x * GB;
-  float acc[4][4];
+  static_assert(BM == 16 * TM && BN == 16 * TN, "16 x 16 threads");
+  constexpr int PA = BM + 4, PB = BN + 4;       // rows stay 16-byte aligned
+  constexpr int LA = BM * GK / GT, LB = BN * GK / GT;  // elements per thread per tile
+  constexpr int HM = TM / 2, HN = TN / 2;
+  __shared__ __align__(16) float As[2][GK][PA];
+  __shared__ __align__(16) float Bs[2][GK][PB];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
+  float ra[LA], rb[LB];
+  auto fetch = [&](int64_t k0) {
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0f;
-  for (int64_t k0 = 0; k0 < K; k0 += GK) {
-    for (int t = threadIdx.x; t < GK * GB; t += GT) {
-      // A tile: rows i0..i0+63, cols k0..k0+15 -> As[k][i]
-      int kk, ii;
-      if (TA) { ii = t % GB; kk = t / GB; } else { kk = t % GK; ii = t / GK; }
+    for (int r = 0; r < LA; ++r) {
+      const int e = tid + r * GT;
+      const int kk = TA ? e / BM : e % GK, ii = TA ? e % BM : e / GK;
       const int64_t gi = i0 + ii, gk = k0 + kk;
-      As[kk][ii] = (gi < M && gk < K) ? (TA ? a[gk * lda + gi] : a[gi * lda + gk]) : 0.0f;
-      int kb, jb;
-      if (TB) { kb = t % GK; jb = t / GK; } else { jb = t % GB; kb = t / GB; }
-      const int64_t gj = j0 + jb, gkb = k0 + kb;
-      Bs[kb][jb] = (gj < N && gkb < K) ? (TB ? b[gj * ldb + gkb] : b[gkb * ldb + gj]) : 0.0f;
+      ra[r] = (gi < M && gk < K) ? (TA ? a[gk * lda + gi] : a[gi * lda + gk]) : 0.0f;
     }
-    __syncthreads();
-    const int kmax = (int)((K - k0) < GK ? (K - k0) : GK);
+#pragma unroll
+    for (int r = 0; r < LB; ++r) {
+      const int e = tid + r * GT;
+      const int kk = TB ? e % GK : e / BN, jj = TB ? e / GK : e % BN;
+      const int64_t gj = j0 + jj, gk = k0 + kk;
+      rb[r] = (gj < N && gk < K) ? (TB ? b[gj * ldb + gk] : b[gk * ldb + gj]) : 0.0f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < LA; ++r) {
+      const int e = tid + r * GT;
+      As[buf][TA ? e / BM : e % GK][TA ? e % BM : e / GK] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < LB; ++r) {
+      const int e = tid + r * GT;
+      Bs[buf][TB ? e % GK : e / BN][TB ? e / GK : e % BN] = rb[r];
+    }
+  };
+  float acc[TM][TN];
+#pragma unroll
+  for (int u = 0; u < TM; ++u)
+#pragma unroll
+    for (int v = 0; v < TN; ++v) acc[u][v] = 0.0f;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < K; k0 += GK) {
+    const bool more = k0 + GK < K;
+    if (more) fetch(k0 + GK);
+    const int kmax = (int)((K - k0) < GK ? (K - k0) : GK);  // exactly K terms per chain
     for (int kk = 0; kk < kmax; ++kk) {
-      float av[4], bv[4];
+      float av[TM], bv[TN];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) av[u] = As[kk][ty + 16 * u];
+      for (int u = 0; u < HM; ++u) {
+        av[u] = As[buf][kk][ty * HM + u];
+        av[HM + u] = As[buf][kk][BM / 2 + ty * HM + u];
+      }
 #pragma unroll
-      for (int v = 0; v < 4; ++v) bv[v] = Bs[kk][tx + 16 * v];
+      for (int v = 0; v < HN; ++v) {
+        bv[v] = Bs[buf][kk][tx * HN + v];
+        bv[HN + v] = Bs[buf][kk][BN / 2 + tx * HN + v];
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < TM; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+        for (int v = 0; v < TN; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
     }
-    __syncthreads();
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t gi = i0 + ty + 16 * u;
+  for (int u = 0; u < TM; ++u) {
+    const int64_t gi = i0 + (u < HM ? ty * HM + u : BM / 2 + ty * HM + (u - HM));
     if (gi >= M) continue;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int64_t gj = j0 + tx + 16 * v;
+    for (int v = 0; v < TN; ++v) {
+      const int64_t gj = j0 + (v < HN ? tx * HN + v : BN / 2 + tx * HN + (v - HN));
       if (gj >= N) continue;
       float r = __fadd_rn(0.0f, acc[u][v]);
       if (mask) r = mask[gi * ldc + gj] > 0.0f ? __fadd_rn(0.0f, r) : 0.0f;
@@ -153,26 +206,58 @@ __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_
 }
 
 // g (rows x n): out[r] = sum_j g[r, j], j increasing, starting from 0.
-// One warp per 32 rows: the warp loads 32 x 32 tiles coalesced (rows of g are
-// contiguous), transposes through shared memory, and lane l adds row l's 32
-// values in order -- the same left-to-right chain as the reference.
-__global__ void __launch_bounds__(32) k_rowsum(const float* __restrict__ g, int64_t rows, int64_t n,
-                                               float* __restrict__ out) {
-  __shared__ float tile[32][33];
-  const int lane = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  float acc = 0.0f;
-  for (int64_t j0 = 0; j0 < n; j0 += 32) {
-    for (int rr = 0; rr < 32; ++rr) {
-      const int64_t r = r0 + rr, j = j0 + lane;
-      tile[rr][lane] = (r < rows && j < n) ? g[r * n + j] : 0.0f;
+// 32 rows per CTA; the 8 warps stage 32 x 128 slabs (coalesced: rows of g are
+// contiguous) into a double-buffered shared tile, and lane l of warp 0 adds
+// row l's values in order -- the reference's left-to-right chain -- while the
+// other warps fetch the next slab.
+constexpr int RS_ROWS = 32, RS_COLS = 128;
+
+__global__ void __launch_bounds__(256) k_rowsum(const float* __restrict__ g, int64_t rows, int64_t n,
+                                                float* __restrict__ out) {
+  __shared__ float tile[2][RS_ROWS][RS_COLS + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * RS_ROWS;
+  auto load = [&](int64_t j0, int buf) {
+    // warp w loads rows w, w+8, w+16, w+24; lane covers 8 columns strided by 32
+#pragma unroll
+    for (int q = 0; q < RS_ROWS / 8; ++q) {
+      const int rr = warp + 8 * q;
+      const int64_t r = r0 + rr;
+#pragma unroll
+      for (int cc = 0; cc < RS_COLS / 32; ++cc) {
+        const int64_t j = j0 + cc * 32 + lane;
+        tile[buf][rr][cc * 32 + lane] = (r < rows && j < n) ? g[r * n + j] : 0.0f;
+      }
     }
-    __syncwarp();
-    const int cnt = (int)((n - j0) < 32 ? (n - j0) : 32);
-    for (int c = 0; c < cnt; ++c) acc = __fadd_rn(acc, tile[lane][c]);
-    __syncwarp();
+  };
+  float acc = 0.0f;
+  load(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t j0 = 0; j0 < n; j0 += RS_COLS) {
+    if (j0 + RS_COLS < n && warp != 0) load(j0 + RS_COLS, buf ^ 1);
+    if (warp == 0) {
+      const int cnt = (int)((n - j0) < RS_COLS ? (n - j0) : RS_COLS);
+      for (int c = 0; c < cnt; ++c) acc = __fadd_rn(acc, tile[buf][lane][c]);
+    }
+    __syncthreads();
+    if (j0 + RS_COLS < n && warp == 0) {
+      // warp 0 was summing; fetch its share of the next slab now
+#pragma unroll
+      for (int q = 0; q < RS_ROWS / 8; ++q) {
+        const int rr = 8 * q;
+        const int64_t r = r0 + rr;
+#pragma unroll
+        for (int cc = 0; cc < RS_COLS / 32; ++cc) {
+          const int64_t j = j0 + RS_COLS + cc * 32 + lane;
+          tile[buf ^ 1][rr][cc * 32 + lane] = (r < rows && j < n) ? g[r * n + j] : 0.0f;
+        }
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
   }
-  if (r0 + lane < rows) out[r0 + lane] = acc;
+  if (warp == 0 && r0 + lane < rows) out[r0 + lane] = acc;
 }
 
 template <int NC>
@@ -223,6 +308,27 @@ mcf_status ensure_tables_here() {
   g_tab_done[d] = true;
   return MCF_OK;
 }
+
+template <bool TA, bool TB, int BM, int BN, int TM, int TN>
+mcf_status gemm_launch(const float* a, int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m,
+                       int64_t n, int64_t k, const float* mask, cudaStream_t s) {
+  const dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM));
+  mcfg::k_gemm<TA, TB, BM, BN, TM, TN><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, mask);
+  return launched("ordered fp32 gemm kernel");
+}
+
+// the largest tile that still gives ~one CTA per SM (the chains cannot be
+// split, so small outputs take small tiles)
+template <bool TA, bool TB>
+mcf_status gemm_shape(const float* a, int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, const float* mask, cudaStream_t s) {
+  const int64_t want = (int64_t)mcfr::sm_count() * 4 / 5;
+  auto ctas = [&](int bm, int bn) { return ((m + bm - 1) / bm) * ((n + bn - 1) / bn); };
+  if (ctas(128, 128) >= want) return gemm_launch<TA, TB, 128, 128, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  if (ctas(128, 64) >= want) return gemm_launch<TA, TB, 128, 64, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  if (ctas(64, 64) >= want) return gemm_launch<TA, TB, 64, 64, 4, 4>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  return gemm_launch<TA, TB, 32, 32, 2, 2>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+}
 }  // namespace
 
 extern "C" {
@@ -244,7 +350,7 @@ mcf_status mcf_mlp_cross_entropy(const float* logits, const int* labels, int64_t
   mcfg::k_ce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(logits, labels, classes, n, (float)n_global, grad, terms);
   mcf_status st = launched("mlp cross-entropy kernel");
   if (st != MCF_OK || !term_sum) return st;
-  mcfg::k_seqsum<<<1, 32, 0, s>>>(terms, n, term_sum);
+  mcfg::k_seqsum<<<1, 256, 0, s>>>(terms, n, term_sum);
   return launched("mlp loss sum kernel");
 }
 
@@ -252,17 +358,15 @@ mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_
                                 float* c, int64_t ldc, int64_t m, int64_t n, int64_t k, const float* relu_mask,
                                 mcf_stream s) {
   if (m * n == 0) return MCF_OK;
-  const dim3 grid((unsigned)((n + mcfg::GB - 1) / mcfg::GB), (unsigned)((m + mcfg::GB - 1) / mcfg::GB));
-  if (trans_a && trans_b) mcfg::k_gemm<true, true><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
-  else if (trans_a) mcfg::k_gemm<true, false><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
-  else if (trans_b) mcfg::k_gemm<false, true><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
-  else mcfg::k_gemm<false, false><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask);
-  return launched("ordered fp32 gemm kernel");
+  if (trans_a && trans_b) return gemm_shape<true, true>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
+  if (trans_a) return gemm_shape<true, false>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
+  if (trans_b) return gemm_shape<false, true>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
+  return gemm_shape<false, false>(a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
 }
 
 mcf_status mcf_rowsum_f32_ordered(const float* g, int64_t rows, int64_t n, float* out, mcf_stream s) {
   if (rows == 0) return MCF_OK;
-  mcfg::k_rowsum<<<(unsigned)((rows + 31) / 32), 32, 0, s>>>(g, rows, n, out);
+  mcfg::k_rowsum<<<(unsigned)((rows + mcfg::RS_ROWS - 1) / mcfg::RS_ROWS), 256, 0, s>>>(g, rows, n, out);
   return launched("row-sum kernel");
 }
 

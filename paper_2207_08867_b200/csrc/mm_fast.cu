@@ -468,6 +468,15 @@ mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t
                                        n, xd, wd, ea, eb, flag, s);
     if (st != MCF_OK) return st;
     const double sg = offset_sigma(k);
+    if (m <= 32) {
+      // short A (e.g. an MLP's 10-class output layer): 16-row tiles, so the
+      // outputs spread over ~one CTA per SM instead of one mostly empty row block
+      st = launch_mm<AccP2<1>, float, 2, 16, 64, 16, 2, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea, eb,
+                                                           sg, flag, 0);
+      if (st != MCF_OK) return st;
+      return launch_mm<AccP2X<1>, float, 2, 16, 64, 16, 2, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea,
+                                                              eb, sg, flag, 1);
+    }
     st = launch_mm<AccP2<1>, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea, eb,
                                                           sg, flag, 0);
     if (st != MCF_OK) return st;

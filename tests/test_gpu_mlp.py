@@ -87,3 +87,84 @@ def test_data_parallel_shards_sum_to_full_batch():
     scale = full.grads.flat.abs().max().item()
     assert diff <= 1e-5 * scale, (diff, scale)
     assert abs(loss_sum - la) <= 1e-5 * abs(la)
+
+
+def _ordered_gemm_np(A, B):
+    """matmul2d (ndarray.hpp:147-165): fl_mul then fl_add, k increasing, from 0."""
+    acc = np.zeros((A.shape[0], B.shape[1]), np.float32)
+    for k in range(A.shape[1]):
+        acc = (acc + (A[:, k, None] * B[None, k, :]).astype(np.float32)).astype(np.float32)
+    return (np.float32(0) + acc).astype(np.float32)
+
+
+# shapes chosen so each tile configuration of mcf_gemm_f32_ordered runs
+# (128x128, 128x64, 64x64, 32x32 -- picked by the CTA count) with ragged edges
+@pytest.mark.parametrize("m,n,k", [(2000, 1300, 37), (1100, 1100, 40), (700, 800, 21), (10, 1024, 300)])
+@pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (0, 0), (1, 1)])
+def test_ordered_gemm_bitwise(m, n, k, ta, tb):
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(m + 7 * n + k + 100 * ta + 10 * tb)
+    A = (rng.standard_normal((m, k)) * np.exp2(rng.integers(-6, 6, (m, k)))).astype(np.float32)
+    B = (rng.standard_normal((k, n)) * np.exp2(rng.integers(-6, 6, (k, n)))).astype(np.float32)
+    mask = rng.standard_normal((m, n)).astype(np.float32)
+    want = _ordered_gemm_np(A, B)
+    want_masked = np.where(mask > 0, want, np.float32(0)).astype(np.float32)
+    a_st = np.ascontiguousarray(A.T if ta else A)
+    b_st = np.ascontiguousarray(B.T if tb else B)
+    da, db = torch.from_numpy(a_st).cuda(), torch.from_numpy(b_st).cuda()
+    dm = torch.from_numpy(mask).cuda()
+    lib = mcf.lib()
+    for use_mask, ref in ((False, want), (True, want_masked)):
+        dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+        rc = lib.mcf_gemm_f32_ordered(ta, tb, da.data_ptr(), a_st.shape[1], db.data_ptr(), b_st.shape[1],
+                                      dc.data_ptr(), n, m, n, k, dm.data_ptr() if use_mask else None, None)
+        assert rc == 0, lib.mcf_last_error()
+        torch.cuda.synchronize()
+        assert_bits(dc.cpu().numpy(), ref, f"gemm ta={ta} tb={tb} {m}x{n}x{k} mask={use_mask}")
+
+
+@pytest.mark.parametrize("rows,n", [(1024, 8192), (37, 300), (10, 129)])
+def test_ordered_rowsum_bitwise(rows, n):
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(rows * 3 + n)
+    g = (rng.standard_normal((rows, n)) * np.exp2(rng.integers(-10, 10, (rows, n)))).astype(np.float32)
+    want = np.zeros(rows, np.float32)
+    for j in range(n):
+        want = (want + g[:, j]).astype(np.float32)
+    dg = torch.from_numpy(g).cuda()
+    out = torch.empty(rows, dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_rowsum_f32_ordered(dg.data_ptr(), rows, n, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert_bits(out.cpu().numpy(), want, "row sums")
+
+
+def test_loss_sum_is_left_to_right_over_slabs():
+    """The loss's binary32 sum runs left to right from 0 (autodiff.hpp:572)
+    across the kernel's 2048-term shared-memory slabs."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(5)
+    classes, n = 10, 5000
+    logits = torch.from_numpy((rng.standard_normal((classes, n)) * 4).astype(np.float32)).cuda()
+    labels = torch.from_numpy(rng.integers(0, classes, n).astype(np.int32)).cuda()
+    grad = torch.empty((classes, n), dtype=torch.float32, device="cuda")
+    terms = torch.empty(n, dtype=torch.float32, device="cuda")
+    tsum = torch.empty(1, dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_mlp_cross_entropy(logits.data_ptr(), labels.data_ptr(), classes, n, n, grad.data_ptr(),
+                                     terms.data_ptr(), tsum.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    t = terms.cpu().numpy()
+    acc = np.float32(0)
+    for v in t:
+        acc = np.float32(acc + v)
+    assert_bits(tsum.cpu().numpy(), np.array([acc], np.float32), "loss sum")
