@@ -58,8 +58,11 @@ typedef enum mcf_prec { MCF_B16 = 0, MCF_B32 = 1, MCF_B64 = 2 } mcf_prec; /* pre
 typedef enum mcf_reduce { /* linalg.hpp:23 */
   MCF_SEQUENTIAL = 0,    /* reference order, bit-identical to the reference */
   MCF_PAIRWISE_TREE = 1, /* reference tree order, bit-identical */
-  MCF_FAST = 2           /* GPU order: compensated binary64 accumulation on the
-                            FP64 pipe; within the reference's error bound */
+  MCF_FAST = 2,          /* GPU order, within the reference's error bound: the
+                            INT8 tensor-core splitting (mm_ozaki.cu) for binary32
+                            nc=2 matrix products, else the compensated binary64
+                            accumulation on the FP64 pipe */
+  MCF_FAST_FP64 = 3      /* MCF_FAST restricted to the FP64-pipe kernels */
 } mcf_reduce;
 
 /* ---- library ------------------------------------------------------------- */
@@ -147,6 +150,14 @@ mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t
 /* out[b,:] = sum_k x[b,k,:] * y[b,k,:]  (batched MC x MC dots) */
 mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch,
                         int64_t k, void* out, int strategy, mcf_stream stream);
+/* Digits per operand of the MCF_FAST tensor-core splitting (mm_ozaki.cu). */
+int mcf_fast_tc_digits(void);
+/* Instrumentation: one MC(nc=2, binary32) x T product on the tensor-core
+ * path with per-phase device times (phase_ms[4]: B digits, A digits, int8
+ * GEMMs, recombination + fallback) and the number of outputs recomputed by
+ * the fallback.  Synchronises the stream. */
+mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
+                              double* phase_ms, int64_t* fallback_outputs, mcf_stream stream);
 /* FP64-pipe instructions per multiply-add of the MCF_FAST kernel for this
  * operand kind (mcmc = 0: MC x Tensor, 1: MC x MC); 0 = no fast kernel. */
 int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);

@@ -30,7 +30,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libmcf_b200.so")
 
 B16, B32, B64 = 0, 1, 2
-SEQUENTIAL, PAIRWISE_TREE, FAST = 0, 1, 2
+SEQUENTIAL, PAIRWISE_TREE, FAST, FAST_FP64 = 0, 1, 2, 3
 
 
 class UnsupportedOperation(NotImplementedError):
@@ -67,6 +67,8 @@ _SIGS = {
     "mcf_h_bmm_mcn": [_int, _p, _int, _p, _i64, _i64, _i64, _i64, _int, _p, _int],
     "mcf_h_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _int],
     "mcf_fast_ops_per_mad": [_int, _int, _int],
+    "mcf_fast_tc_digits": [],
+    "mcf_fast_mm_phases": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
     "mcf_probe_pipe_rates": [_p, _p],
     "mcf_mlp_bias_act": [_p, _int, _p, _i64, _i64, _int, _p, _p, _p],
     "mcf_mlp_cross_entropy": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],

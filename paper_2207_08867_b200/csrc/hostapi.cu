@@ -146,11 +146,12 @@ mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64
   char* d = static_cast<char*>(mcfr::workspace(align(bx) + align(bw) + align(bo) + 256, 0));
   if (!d) return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot allocate device workspace");
   char *dx = d, *dw = d + align(bx), *dout = dw + align(bw);
-  if (strategy == MCF_FAST && p == MCF_B32 && nc == 2 && batch == 1 && m >= 1024 && k > 0 &&
-      mcfr::ensure_device_tables() == MCF_OK) {
-    // the headline shape: row-chunked so the copies overlap the FP64 mm
+  if ((strategy == MCF_FAST || strategy == MCF_FAST_FP64) && p == MCF_B32 && nc == 2 && batch == 1 &&
+      m >= 1024 && k > 0 && mcfr::ensure_device_tables() == MCF_OK) {
+    // the headline shape: row-chunked so the copies overlap the product
     const cudaStream_t comp[2] = {mcfr::side_stream(4), mcfr::side_stream(5)};
-    const mcf_status st = mcfr::mm_fast_mct_host(
+    auto pipe = strategy == MCF_FAST ? mcfr::ozaki_host : mcfr::mm_fast_mct_host;
+    const mcf_status st = pipe(
         static_cast<const float*>(x), static_cast<const float*>(w), m, k, n, static_cast<float*>(out),
         reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dw), reinterpret_cast<float*>(dout),
         mcfr::side_stream(3), comp, mcfr::side_stream(6));

@@ -335,14 +335,16 @@ mcf_status mcf_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t
   if (st != MCF_OK) return st;
   if (batch < 0 || m < 0 || k < 0 || n < 0)
     return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: negative dimension");
-  if (strategy != MCF_SEQUENTIAL && strategy != MCF_PAIRWISE_TREE && strategy != MCF_FAST)
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_PAIRWISE_TREE && strategy != MCF_FAST &&
+      strategy != MCF_FAST_FP64)
     return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcn: unknown reduction strategy");
   if (batch * m * n == 0) return MCF_OK;
   if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
-  if (strategy == MCF_FAST) {
+  if (strategy == MCF_FAST || strategy == MCF_FAST_FP64) {
     if (nc >= 2 && k > 0) {
+      const bool tc = strategy == MCF_FAST;
       const mcf_status fs = n == 1 ? mcfr::mv_fast_mct(p, x, nc, w, batch, m, k, w_batched, out, stream)
-                                   : mcfr::mm_fast_mct(p, x, nc, w, batch, m, k, n, w_batched, out, stream);
+                                   : mcfr::mm_fast_mct(p, x, nc, w, batch, m, k, n, w_batched, out, stream, tc);
       if (fs != MCF_ERR_UNSUPPORTED) return fs;
     }
     strategy = MCF_SEQUENTIAL;  // no fast kernel for this shape: reference order
@@ -367,12 +369,12 @@ mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t
   const mcf_status st = check_lin(p, nc, "mm_mcmc");
   if (st != MCF_OK) return st;
   if (m < 0 || k < 0 || n < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcmc: negative dimension");
-  if (strategy != MCF_SEQUENTIAL && strategy != MCF_FAST)
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_FAST && strategy != MCF_FAST_FP64)
     return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_mcmc: unknown reduction strategy");
   if (m * n == 0) return MCF_OK;
   if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
-  if (strategy == MCF_FAST && k > 0) {
-    const mcf_status fs = mcfr::mm_fast_mcmc(p, x, y, nc, m, k, n, out, stream);
+  if ((strategy == MCF_FAST || strategy == MCF_FAST_FP64) && k > 0) {
+    const mcf_status fs = mcfr::mm_fast_mcmc(p, x, y, nc, m, k, n, out, stream, strategy == MCF_FAST);
     if (fs != MCF_ERR_UNSUPPORTED) return fs;
   }
   switch (p) {
@@ -387,11 +389,11 @@ mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
   const mcf_status st = check_lin(p, nc, "dot_mcmc");
   if (st != MCF_OK) return st;
   if (batch < 0 || k < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "dot_mcmc: negative dimension");
-  if (strategy != MCF_SEQUENTIAL && strategy != MCF_FAST)
+  if (strategy != MCF_SEQUENTIAL && strategy != MCF_FAST && strategy != MCF_FAST_FP64)
     return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "dot_mcmc: unknown reduction strategy");
   if (batch == 0) return MCF_OK;
   if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
-  if (strategy == MCF_FAST && k > 0) {
+  if ((strategy == MCF_FAST || strategy == MCF_FAST_FP64) && k > 0) {
     const mcf_status fs = mcfr::dot_fast_mcmc(p, x, y, nc, batch, k, out, stream);
     if (fs != MCF_ERR_UNSUPPORTED) return fs;
   }
@@ -403,5 +405,15 @@ mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
 }
 
 int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) { return mcfr::mm_fast_ops_per_mad(mcmc, p, nc); }
+
+int mcf_fast_tc_digits(void) { return mcfr::ozaki_digits(); }
+
+mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
+                              double* phase_ms, int64_t* fallback_outputs, mcf_stream stream) {
+  if (!x || !w || !out || !phase_ms || !fallback_outputs)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mm_phases: null argument");
+  if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  return mcfr::ozaki_phases(x, w, m, k, n, out, phase_ms, fallback_outputs, stream);
+}
 
 }  // extern "C"

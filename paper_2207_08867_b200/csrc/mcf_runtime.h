@@ -48,14 +48,23 @@ mcf_status ensure_stack(std::size_t bytes);
 // MCF_ERR_UNSUPPORTED without a message when it has no instantiation for the
 // call, and the C-ABI then runs the reference-order kernel instead.
 mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
-                       int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s);
+                       int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s, bool tc = true);
 mcf_status mv_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
                        int64_t k, int w_batched, void* out, cudaStream_t s);
 mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
-                        int64_t n, void* out, cudaStream_t s);
+                        int64_t n, void* out, cudaStream_t s, bool tc = true);
 mcf_status dot_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch, int64_t k,
                          void* out, cudaStream_t s);
 int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
+// INT8 tensor-core (Ozaki) path of MCF_FAST (mm_ozaki.cu)
+bool ozaki_supported(int64_t m, int64_t k, int64_t n);
+mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n, float* out,
+                    cudaStream_t s);
+int ozaki_digits();
+mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, double* ms,
+                        int64_t* fallback, cudaStream_t s);
+mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout, float* dx,
+                      float* dw, float* dout, cudaStream_t cin, const cudaStream_t comp[2], cudaStream_t cout);
 // host-buffer MC(nc=2, binary32) x T, pipelined over row chunks (hostapi.cu)
 mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout,
                             float* dx, float* dw, float* dout, cudaStream_t cin, const cudaStream_t comp[2],

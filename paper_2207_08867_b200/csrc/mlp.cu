@@ -110,16 +110,24 @@ __global__ void __launch_bounds__(256) k_seqsum(const float* __restrict__ terms,
 // fragment loads are 128-bit and conflict-free.  K tiles of 16 staged
 // through shared memory (k-major, both operands), the next tile prefetched
 // into registers while the current one is consumed.
-constexpr int GK = 16, GT = 256;
+constexpr int GT = 256;
 
-template <bool TA, bool TB, int BM, int BN, int TM, int TN>
+// row (col) of the tile owned by fragment index u of thread t (T per thread):
+// T == 1 -> t; else two halves of T/2, at t*T/2 and B/2 + t*T/2
+template <int T, int B>
+__device__ __forceinline__ int frag_pos(int t, int u) {
+  if constexpr (T == 1) return t;
+  else return u < T / 2 ? t * (T / 2) + u : B / 2 + t * (T / 2) + (u - T / 2);
+}
+
+template <bool TA, bool TB, int BM, int BN, int TM, int TN, int GK>
 __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
                                              int64_t ldb, float* __restrict__ c, int64_t ldc, int64_t M, int64_t N,
                                              int64_t K, const float* __restrict__ mask) {
   static_assert(BM == 16 * TM && BN == 16 * TN, "16 x 16 threads");
-  constexpr int PA = BM + 4, PB = BN + 4;       // rows stay 16-byte aligned
+  constexpr int PA = BM + 4, PB = BN + 4;              // rows stay 16-byte aligned
   constexpr int LA = BM * GK / GT, LB = BN * GK / GT;  // elements per thread per tile
-  constexpr int HM = TM / 2, HN = TN / 2;
+  static_assert(LA * GT == BM * GK && LB * GT == BN * GK, "whole tiles per thread");
   __shared__ __align__(16) float As[2][GK][PA];
   __shared__ __align__(16) float Bs[2][GK][PB];
   const int tid = threadIdx.x;
@@ -159,6 +167,17 @@ __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_
   for (int u = 0; u < TM; ++u)
 #pragma unroll
     for (int v = 0; v < TN; ++v) acc[u][v] = 0.0f;
+  auto step = [&](int buf, int kk) {
+    float av[TM], bv[TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u) av[u] = As[buf][kk][frag_pos<TM, BM>(ty, u)];
+#pragma unroll
+    for (int v = 0; v < TN; ++v) bv[v] = Bs[buf][kk][frag_pos<TN, BN>(tx, v)];
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+  };
   fetch(0);
   stash(0);
   __syncthreads();
@@ -166,23 +185,13 @@ __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_
   for (int64_t k0 = 0; k0 < K; k0 += GK) {
     const bool more = k0 + GK < K;
     if (more) fetch(k0 + GK);
-    const int kmax = (int)((K - k0) < GK ? (K - k0) : GK);  // exactly K terms per chain
-    for (int kk = 0; kk < kmax; ++kk) {
-      float av[TM], bv[TN];
+    if (K - k0 >= GK) {
 #pragma unroll
-      for (int u = 0; u < HM; ++u) {
-        av[u] = As[buf][kk][ty * HM + u];
-        av[HM + u] = As[buf][kk][BM / 2 + ty * HM + u];
-      }
-#pragma unroll
-      for (int v = 0; v < HN; ++v) {
-        bv[v] = Bs[buf][kk][tx * HN + v];
-        bv[HN + v] = Bs[buf][kk][BN / 2 + tx * HN + v];
-      }
-#pragma unroll
-      for (int u = 0; u < TM; ++u)
-#pragma unroll
-        for (int v = 0; v < TN; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+      for (int kk = 0; kk < GK; ++kk) step(buf, kk);
+    } else {
+      // exactly K terms per chain: the last partial tile stops at K
+      const int kmax = (int)(K - k0);
+      for (int kk = 0; kk < kmax; ++kk) step(buf, kk);
     }
     if (more) {
       stash(buf ^ 1);
@@ -192,11 +201,11 @@ __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_
   }
 #pragma unroll
   for (int u = 0; u < TM; ++u) {
-    const int64_t gi = i0 + (u < HM ? ty * HM + u : BM / 2 + ty * HM + (u - HM));
+    const int64_t gi = i0 + frag_pos<TM, BM>(ty, u);
     if (gi >= M) continue;
 #pragma unroll
     for (int v = 0; v < TN; ++v) {
-      const int64_t gj = j0 + (v < HN ? tx * HN + v : BN / 2 + tx * HN + (v - HN));
+      const int64_t gj = j0 + frag_pos<TN, BN>(tx, v);
       if (gj >= N) continue;
       float r = __fadd_rn(0.0f, acc[u][v]);
       if (mask) r = mask[gi * ldc + gj] > 0.0f ? __fadd_rn(0.0f, r) : 0.0f;
@@ -309,25 +318,27 @@ mcf_status ensure_tables_here() {
   return MCF_OK;
 }
 
-template <bool TA, bool TB, int BM, int BN, int TM, int TN>
+template <bool TA, bool TB, int BM, int BN, int TM, int TN, int GK>
 mcf_status gemm_launch(const float* a, int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m,
                        int64_t n, int64_t k, const float* mask, cudaStream_t s) {
   const dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM));
-  mcfg::k_gemm<TA, TB, BM, BN, TM, TN><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, mask);
+  mcfg::k_gemm<TA, TB, BM, BN, TM, TN, GK><<<grid, mcfg::GT, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, k, mask);
   return launched("ordered fp32 gemm kernel");
 }
 
 // the largest tile that still gives ~one CTA per SM (the chains cannot be
-// split, so small outputs take small tiles)
+// split, so small outputs take small tiles, with longer K tiles to cover
+// the load latency)
 template <bool TA, bool TB>
 mcf_status gemm_shape(const float* a, int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m,
                       int64_t n, int64_t k, const float* mask, cudaStream_t s) {
   const int64_t want = (int64_t)mcfr::sm_count() * 4 / 5;
   auto ctas = [&](int bm, int bn) { return ((m + bm - 1) / bm) * ((n + bn - 1) / bn); };
-  if (ctas(128, 128) >= want) return gemm_launch<TA, TB, 128, 128, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
-  if (ctas(128, 64) >= want) return gemm_launch<TA, TB, 128, 64, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
-  if (ctas(64, 64) >= want) return gemm_launch<TA, TB, 64, 64, 4, 4>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
-  return gemm_launch<TA, TB, 32, 32, 2, 2>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  if (ctas(128, 128) >= want) return gemm_launch<TA, TB, 128, 128, 8, 8, 16>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  if (ctas(128, 64) >= want) return gemm_launch<TA, TB, 128, 64, 8, 4, 16>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  if (ctas(64, 64) >= want) return gemm_launch<TA, TB, 64, 64, 4, 4, 32>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  if (ctas(32, 32) >= want) return gemm_launch<TA, TB, 32, 32, 2, 2, 64>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
+  return gemm_launch<TA, TB, 16, 16, 1, 1, 64>(a, lda, b, ldb, c, ldc, m, n, k, mask, s);
 }
 }  // namespace
 

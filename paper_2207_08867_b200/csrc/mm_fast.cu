@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(256) k_probe(double* out, int iters, double a)
 
 extern "C" int mcf_probe_pipe_rates(double* fp64_ops_per_s, double* fp32_ops_per_s) {
   using namespace mcfg;
-  const int sms = mcfr::sm_count(), blocks = sms * 8, threads = 256, iters = 2048;
+  const int sms = mcfr::sm_count(), blocks = sms * 8, threads = 256, iters = 8192;
   double* buf = nullptr;
   if (cudaMalloc(&buf, (size_t)blocks * threads * sizeof(double)) != cudaSuccess) return 1;
   cudaEvent_t e0, e1;
@@ -412,7 +413,7 @@ extern "C" int mcf_probe_pipe_rates(double* fp64_ops_per_s, double* fp32_ops_per
   cudaEventCreate(&e1);
   double rates[2] = {0, 0};
   for (int kind = 0; kind < 2; ++kind) {
-    for (int rep = 0; rep < 3; ++rep) {
+    for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(e0);
       if (kind == 0) k_probe<true><<<blocks, threads>>>(buf, iters, 0.999999);
       else k_probe<false><<<blocks, threads>>>(buf, iters, 0.999999);
@@ -436,6 +437,36 @@ extern "C" int mcf_probe_pipe_rates(double* fp64_ops_per_s, double* fp32_ops_per
 
 namespace mcfr {
 
+// the offset-accumulation pair (AccP2 runs when the widening flag is clear,
+// AccP2X when it is set; the other exits at once), tile chosen by shape.
+// MCF_MM_TILE (tuning knob) forces a tile: a = 128x64/8x4 (256 thr),
+// b = 64x64/4x4 (256 thr, 2 CTAs/SM), c = 128x64/4x4 (512 thr).
+template <int NB>
+mcf_status launch_p2(const double* xd, const double* wd, void* out, int64_t batch, int64_t m, int64_t n, int64_t k,
+                     int64_t a_bs, int64_t b_bs, int64_t c_bs, cudaStream_t s, const int* ea, const int* eb,
+                     double sg, const int* flag) {
+  using namespace mcfg;
+  static const char tile = [] {
+    const char* e = getenv("MCF_MM_TILE");
+    return e && *e ? e[0] : 'a';
+  }();
+#define MCF_P2(BM, BN, TM, TN, MINB)                                                                              \
+  do {                                                                                                            \
+    mcf_status st = launch_mm<AccP2<NB>, float, 2, BM, BN, 16, TM, TN, MINB>(xd, wd, out, batch, m, n, k, a_bs,   \
+                                                                            b_bs, c_bs, s, ea, eb, sg, flag, 0);  \
+    if (st != MCF_OK) return st;                                                                                  \
+    return launch_mm<AccP2X<NB>, float, 2, BM, BN, 16, TM, TN, MINB>(xd, wd, out, batch, m, n, k, a_bs, b_bs,     \
+                                                                     c_bs, s, ea, eb, sg, flag, 1);               \
+  } while (0)
+  // short A (e.g. an MLP's 10-class output layer): 16-row tiles, so the
+  // outputs spread over ~one CTA per SM instead of one mostly empty row block
+  if (m <= 32) MCF_P2(16, 64, 2, 4, 1);
+  if (tile == 'b') MCF_P2(64, 64, 4, 4, 2);
+  if (tile == 'c') MCF_P2(128, 64, 4, 4, 1);
+  MCF_P2(128, 64, 8, 4, 1);
+#undef MCF_P2
+}
+
 // FP64-pipe instructions per multiply-add of the kernel a fast call uses
 int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) {
   using namespace mcfg;
@@ -447,8 +478,21 @@ int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) {
 // MC x Tensor; MCF_ERR_UNSUPPORTED (no message) when no fast instantiation
 // covers the call, so the caller can fall back to the reference-order kernel.
 mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
-                       int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s) {
+                       int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s, bool tc) {
   using namespace mcfg;
+  if (tc && p == MCF_B32 && nc == 2 && ozaki_supported(m, k, n)) {
+    // INT8 tensor-core path (mm_ozaki.cu), one product per batch entry
+    const float* xf = static_cast<const float*>(x);
+    const float* wf = static_cast<const float*>(w);
+    float* of = static_cast<float*>(out);
+    for (int64_t b = 0; b < batch; ++b) {
+      const mcf_status st = mm_ozaki(xf + b * m * k * 2, 2, wf + (w_batched ? b * k * n : 0), 1, m, k, n,
+                                     of + b * m * n * 2, s);
+      if (st == MCF_ERR_UNSUPPORTED) break;  // no int8 GEMM for the shape: FP64 pipe below
+      if (st != MCF_OK) return st;
+      if (b + 1 == batch) return MCF_OK;
+    }
+  }
   if (p != MCF_B32 || (nc != 2 && nc != 3) || n % 2 != 0 || (k * nc) % 2 != 0)
     return MCF_ERR_UNSUPPORTED;
   const int64_t xa = batch * m * k * nc, wb = (w_batched ? batch : 1) * k * n;
@@ -467,21 +511,7 @@ mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t
     mcf_status st = widen_scaled<2, 1>(static_cast<const float*>(x), static_cast<const float*>(w), batch * m, k, k,
                                        n, xd, wd, ea, eb, flag, s);
     if (st != MCF_OK) return st;
-    const double sg = offset_sigma(k);
-    if (m <= 32) {
-      // short A (e.g. an MLP's 10-class output layer): 16-row tiles, so the
-      // outputs spread over ~one CTA per SM instead of one mostly empty row block
-      st = launch_mm<AccP2<1>, float, 2, 16, 64, 16, 2, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea, eb,
-                                                           sg, flag, 0);
-      if (st != MCF_OK) return st;
-      return launch_mm<AccP2X<1>, float, 2, 16, 64, 16, 2, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea,
-                                                              eb, sg, flag, 1);
-    }
-    st = launch_mm<AccP2<1>, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea, eb,
-                                                          sg, flag, 0);
-    if (st != MCF_OK) return st;
-    return launch_mm<AccP2X<1>, float, 2, 128, 64, 16, 8, 4>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea,
-                                                             eb, sg, flag, 1);
+    return launch_p2<1>(xd, wd, out, batch, m, n, k, a_bs, b_bs, c_bs, s, ea, eb, offset_sigma(k), flag);
   }
   mcf_status st = nc == 2 ? widen<float, 2, false>(x, xd, batch * m * k, s)
                           : widen<float, 3, false>(x, xd, batch * m * k, s);
@@ -549,10 +579,7 @@ mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t
     PIPE_TRY(cu(cudaStreamWaitEvent(cs, ex, 0), "wait"));
     PIPE_TRY(cu(cudaMemcpyAsync(fl, flag_b, sizeof(int), cudaMemcpyDeviceToDevice, cs), "flag"));
     PIPE_TRY(widen_scaled_a<2>(dx + r0 * k * 2, rows, k, xd + r0 * k * 2, ea + r0, fl, cs));
-    PIPE_TRY((launch_mm<AccP2<1>, float, 2, 128, 64, 16, 8, 4>(xd + r0 * k * 2, wd, dout + r0 * n * 2, 1, rows, n, k,
-                                                               0, 0, 0, cs, ea + r0, eb, sg, fl, 0)));
-    PIPE_TRY((launch_mm<AccP2X<1>, float, 2, 128, 64, 16, 8, 4>(xd + r0 * k * 2, wd, dout + r0 * n * 2, 1, rows, n,
-                                                                k, 0, 0, 0, cs, ea + r0, eb, sg, fl, 1)));
+    PIPE_TRY(launch_p2<1>(xd + r0 * k * 2, wd, dout + r0 * n * 2, 1, rows, n, k, 0, 0, 0, cs, ea + r0, eb, sg, fl));
     PIPE_TRY(cu(cudaEventRecord(em, cs), "event"));
     PIPE_TRY(cu(cudaStreamWaitEvent(cout, em, 0), "wait"));
     PIPE_TRY(cu(cudaMemcpyAsync(hout + r0 * n * 2, dout + r0 * n * 2, rows * n * 2 * sizeof(float),
@@ -563,8 +590,13 @@ mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t
 }
 
 mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
-                        int64_t n, void* out, cudaStream_t s) {
+                        int64_t n, void* out, cudaStream_t s, bool tc) {
   using namespace mcfg;
+  if (tc && p == MCF_B32 && nc == 2 && ozaki_supported(m, k, n)) {
+    const mcf_status st = mm_ozaki(static_cast<const float*>(x), 2, static_cast<const float*>(y), 2, m, k, n,
+                                   static_cast<float*>(out), s);
+    if (st != MCF_ERR_UNSUPPORTED) return st;
+  }
   const bool f32 = p == MCF_B32 && nc == 2, f16 = p == MCF_B16 && nc == 3;
   if ((!f32 && !f16) || n % 2 != 0 || k % 2 != 0) return MCF_ERR_UNSUPPORTED;
   const int w = f32 ? 2 : 1;  // binary64 words per element after widening
@@ -581,11 +613,7 @@ mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
     st = widen_scaled<2, 2>(static_cast<const float*>(x), static_cast<const float*>(y), m, k, k, n, xd, yd, ea, eb,
                             flag, s);
     if (st != MCF_OK) return st;
-    const double sg = offset_sigma(k);
-    st = launch_mm<AccP2<2>, float, 2, 128, 64, 16, 8, 4>(xd, yd, out, 1, m, n, k, 0, 0, 0, s, ea, eb, sg, flag, 0);
-    if (st != MCF_OK) return st;
-    return launch_mm<AccP2X<2>, float, 2, 128, 64, 16, 8, 4>(xd, yd, out, 1, m, n, k, 0, 0, 0, s, ea, eb, sg, flag,
-                                                             1);
+    return launch_p2<2>(xd, yd, out, 1, m, n, k, 0, 0, 0, s, ea, eb, offset_sigma(k), flag);
   }
   st = widen<__half, 3, true>(x, xd, m * k, s);
   if (st == MCF_OK) st = widen<__half, 3, true>(y, yd, k * n, s);

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import torch
 
-from . import B16, B32, B64, FAST, PAIRWISE_TREE, SEQUENTIAL, UnsupportedOperation, _check, lib  # noqa: F401
+from . import B16, B32, B64, FAST, FAST_FP64, PAIRWISE_TREE, SEQUENTIAL, UnsupportedOperation, _check, lib  # noqa: F401
 
 __all__ = [
     "two_sum", "two_prod", "renormalize", "simple_renorm", "approx", "negate", "grow_expn",

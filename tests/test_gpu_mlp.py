@@ -98,8 +98,8 @@ def _ordered_gemm_np(A, B):
 
 
 # shapes chosen so each tile configuration of mcf_gemm_f32_ordered runs
-# (128x128, 128x64, 64x64, 32x32 -- picked by the CTA count) with ragged edges
-@pytest.mark.parametrize("m,n,k", [(2000, 1300, 37), (1100, 1100, 40), (700, 800, 21), (10, 1024, 300)])
+# (128x128, 128x64, 64x64, 32x32, 16x16 -- picked by the CTA count) with ragged edges
+@pytest.mark.parametrize("m,n,k", [(2000, 1300, 37), (1100, 1100, 40), (700, 800, 21), (300, 500, 70), (10, 1024, 300)])
 @pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (0, 0), (1, 1)])
 def test_ordered_gemm_bitwise(m, n, k, ta, tb):
     import torch
