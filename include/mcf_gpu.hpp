@@ -201,7 +201,7 @@ MCTensor<P> mm_mcn(const MCTensor<P>& x, const NdArray& w, const ReductionPlan& 
                         detail::strategy_of(plan));
 }
 
-// GPU-order plan (FP64 pipe), same shapes and checks as mm_mcn
+// GPU-order plan (MCF_FAST: INT8 tensor-core splitting where supported, else the FP64 pipe), same shapes and checks as mm_mcn
 template <class P>
 MCTensor<P> mm_mcn_fast(const MCTensor<P>& x, const NdArray& w) {
   mcf::detail::require_rank(x.shape(), 2, "mm_mcn");

@@ -7,31 +7,36 @@
 // product is computed as an error-free integer splitting (Ozaki scheme):
 //
 //   * every row i of A is scaled by 2^-ea[i] and every column j of B by
-//     2^-eb[j] (powers of two, exact) so all values lie in (-1, 1);
-//   * each scaled value v = c0 + c1 (exact binary64 pair) becomes kS signed
-//     digits d_s in [-64, 64] with weights 2^(-6-7s) (round to nearest, the
-//     remainder carried exactly), |v - sum| <= 2^(-7 kS) (1 + 2^-50);
-//   * for each diagonal q = s + t < kS one int8 GEMM with the digit planes
-//     concatenated along K gives C_q = sum_{s+t=q} A_s B_t exactly in int32
-//     ((q+1) Kp 64^2 < 2^31 for Kp <= 50000);
-//   * C = sum_q C_q 2^(-12-7q) is formed exactly in double-double, scaled
-//     back and split greedily into the nc output components.
+//     2^-eb[j] (powers of two, exact) so all values lie in (-1/2, 1/2);
+//   * each scaled value v = c0 + c1 (exact binary64 pair) becomes kS = 9
+//     balanced base-256 digits: v = sum_s d_s 2^(-7-8s) + r, d_0 in [-64, 64],
+//     d_s in [-128, 127], |r| <= 2^-72 (1 + 2^-50);
+//   * K is cut into chunks of kc <= 14400; for each chunk and each diagonal
+//     q = s + t < kS one int8 GEMM whose K dimension is the q+1 digit planes
+//     of the chunk laid end to end gives C_cq = sum_{s+t=q} A_s B_t exactly in
+//     int32 ((q+1) kc 2^14 < 2^31);
+//   * C = sum_{c,q} C_cq 2^(-14-8q) is formed exactly (int64 over chunks,
+//     then double-double), scaled back and split greedily into the two
+//     binary32 output components.
 //
-// Error per product <= (kS + 1.1) 2^(-7 kS) (scaled units), so per output
-// <= K (kS + 1.1) 2^(-7 kS).  Outputs whose magnitude is not at least 2^51
-// times that bound (cancellation; rows or columns holding Inf/NaN) are put on
-// a work list and recomputed by a warp each in double-double from the fp32
-// operands, so every output has relative error <= 2^-51 before the final
-// split -- the same bound the reference's own nc=2 result representation sets.
+// Error per product <= 2^-73 + 2^-73 + 8.04 2^-72 <= 2^-68.8 (scaled units)
+// -- the truncations of both operands and the dropped diagonals q >= kS --
+// so per output <= K 2^-68.8.  Outputs whose magnitude is not at least 2^50
+// times that bound (cancellation; rows or columns holding Inf/NaN) are listed
+// per row and recomputed by the fallback kernel in double-double from the
+// binary32 operands, so every output has relative error <= 2^-50 before the
+// final split -- the resolution of the reference's own nc=2 result (its
+// measured max relative error is 2^-49.1).
 //
-// The int8 GEMMs are plain library GEMMs (cuBLASLt IMMA, TN, int32 out); the
-// digit extraction, the transposes, the recombination + split and the
+// The int8 GEMMs are plain library GEMMs (cuBLASLt IMMA, TN, s8 x s8 -> s32);
+// the scaling, digit extraction, transposes, recombination + split and the
 // cancellation fallback are this file's kernels.
 #include <cublasLt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -45,28 +50,54 @@ namespace mcfg {
 namespace oz {
 namespace {
 
-constexpr int kS = 10;             // digits per operand
-constexpr int kSlab = 32;          // transpose tile of the column slicer
-constexpr int64_t kMaxKp = 50000;  // int32 headroom: kS * Kp * 64 * 64 < 2^31
+constexpr int kS = 9;                // digits per operand
+constexpr int kSlab = 32;            // transpose tile of the column slicer
+constexpr int64_t kMaxChunk = 14400; // int32 headroom: kS * kc * 2^14 < 2^31
 
 __device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
-// 2^e > m (m >= 0 finite), 0 for m == 0 or non-finite (those rows / columns
-// go to the fallback list)
-__device__ __forceinline__ int exp_above_d(double m) { return m > 0.0 && isfinite(m) ? ilogb(m) + 1 : 0; }
+// 2^e > 2 m (m >= 0 finite): scaled values lie in (-1/2, 1/2); 0 for m == 0
+// or non-finite (those rows / columns go to the fallback list)
+__device__ __forceinline__ int exp_above_d(double m) { return m > 0.0 && isfinite(m) ? ilogb(m) + 2 : 0; }
 
-// kS signed digits of hi + lo (|hi + lo| < 1): digit s has weight 2^(-6-7s)
-__device__ __forceinline__ void digits(double hi, double lo, int (&d)[kS]) {
-  double h = __dmul_rn(hi, 64.0), l = __dmul_rn(lo, 64.0);
+// one 24-bit limb (plus the carry from below) -> `cnt` balanced base-256
+// digits, least significant first at d[cnt-1]; returns the carry out
+__device__ __forceinline__ int limb_digits(int x, int* d, int cnt) {
 #pragma unroll
-  for (int s = 0; s < kS; ++s) {
-    const double a = rint(h);
-    d[s] = (int)a;
-    double sh, sl;
-    dsum(__dsub_rn(h, a), l, sh, sl);
-    h = __dmul_rn(sh, 128.0);
-    l = __dmul_rn(sl, 128.0);
+  for (int s = cnt - 1; s >= 0; --s) {
+    const int t = ((x + 128) & 255) - 128;
+    d[s] = t;
+    x = (x - t) >> 8;
   }
+  return x;
+}
+
+// kS digits of v = hi + lo (|v| < 1/2, exact pair).  Three binary64 steps give
+// the limbs H = rint(v 2^23), M = rint(r1 2^24), L = rint(r2 2^24)
+// (|H| <= 2^22, |M|, |L| <= 2^23, r1 = v 2^23 - H, r2 = r1 2^24 - M, all
+// |r| <= 1/2 (1 + tiny)), v = H 2^-23 + M 2^-47 + L 2^-71 + r3 2^-71; the
+// limbs are then cut into digits bottom-up with integer operations.
+__device__ __forceinline__ void digits(double hi, double lo, int (&d)[kS]) {
+  const double h = __dmul_rn(hi, 0x1p23), hl = __dmul_rn(lo, 0x1p23);
+  const double H = rint(h);
+  double r1, r1l;
+  dsum(__dsub_rn(h, H), hl, r1, r1l);
+  const double m = __dmul_rn(r1, 0x1p24), ml = __dmul_rn(r1l, 0x1p24);
+  const double M = rint(m);
+  double r2, r2l;
+  dsum(__dsub_rn(m, M), ml, r2, r2l);
+  const double L = rint(__dmul_rn(r2, 0x1p24));
+  int c = limb_digits(__double2int_rn(L), d + 6, 3);
+  c = limb_digits(__double2int_rn(M) + c, d + 3, 3);
+  // top limb: two balanced digits, the remainder (|.| <= 64) is d_0
+  int x = __double2int_rn(H) + c;
+#pragma unroll
+  for (int s = 2; s >= 1; --s) {
+    const int t = ((x + 128) & 255) - 128;
+    d[s] = t;
+    x = (x - t) >> 8;
+  }
+  d[0] = x;
 }
 
 template <int NC>
@@ -82,7 +113,22 @@ __device__ __forceinline__ void load_pair(const float* p, double& hi, double& lo
   }
 }
 
-// row exponents of A (rows x k, NC comps): warp per row, max of |c0| + |c1|
+// K chunking: kc (multiple of 16) and the number of chunks; a row of digit
+// planes is [chunk 0: kS planes of kc bytes][chunk 1: ...]
+struct KGeo {
+  int64_t k, kc, nkc;
+  __host__ __device__ int64_t row_bytes() const { return kS * kc * nkc; }
+};
+
+KGeo kgeo(int64_t k) {
+  const int64_t k16 = (k + 15) / 16 * 16;
+  const int64_t nkc = (k16 + kMaxChunk - 1) / kMaxChunk;
+  const int64_t kc = ((k16 + nkc - 1) / nkc + 15) / 16 * 16;
+  return KGeo{k, kc, nkc};
+}
+
+// row exponents of A (rows x k, NC comps, row stride lda elements): warp per
+// row, max of |c0| + |c1|
 template <int NC>
 __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int64_t rows, int64_t k,
                                                  int* __restrict__ e, int* __restrict__ nf) {
@@ -106,10 +152,11 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
   }
 }
 
-// column maxima of B (k x n, NC comps): slabs of 64 rows, atomicMax on the
-// binary64 bit pattern (monotone for non-negative values; cm starts at 0)
+// column maxima of B (k x n, NC comps, row stride ldb elements): slabs of 64
+// rows, atomicMax on the binary64 bit pattern (monotone for non-negative
+// values; cm starts at 0)
 template <int NC>
-__global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int64_t k, int64_t n,
+__global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int64_t k, int64_t n, int64_t ldb,
                                                  unsigned long long* __restrict__ cm, int* __restrict__ nf) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -118,7 +165,7 @@ __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int
   bool bad = false;
   for (int64_t t = t0; t < t1; ++t) {
     double hi, lo, mag;
-    load_pair<NC>(b + (t * n + j) * NC, hi, lo, mag);
+    load_pair<NC>(b + (t * ldb + j) * NC, hi, lo, mag);
     bad |= !isfinite(mag);
     m = fmax(m, mag);
   }
@@ -132,12 +179,13 @@ __global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __rest
   if (j < n) e[j] = exp_above_d(__longlong_as_double((long long)cm[j]));
 }
 
-// A (rows x k, NC comps) -> digit planes, row-major rows of kS * kp bytes:
-// out[i, s * kp + k] = digit s of A[i, k] 2^-e[i]; zero for k >= K.
-// Each thread makes 4 consecutive k (one 32-bit store per digit).
+// A (rows x k, NC comps) -> digit planes, one row of g.row_bytes() per row:
+// byte [i][c kS kc + s kc + kk] = digit s of A[i, c kc + kk] 2^-e[i]; zero
+// for k >= K.  Each thread makes 4 consecutive k (one 32-bit store per digit).
 template <int NC>
-__global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a, int64_t rows, int64_t k, int64_t kp,
+__global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a, int64_t rows, KGeo g,
                                                      const int* __restrict__ e, int8_t* __restrict__ out) {
+  const int64_t kp = g.kc * g.nkc;
   const int64_t q4 = kp / 4;
   const int64_t total = rows * q4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -149,92 +197,104 @@ __global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a,
     for (int s = 0; s < kS; ++s) packed[s] = 0u;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (k0 + u >= k) break;
+      if (k0 + u >= g.k) break;
       double hi, lo, mag;
-      load_pair<NC>(a + (i * k + k0 + u) * NC, hi, lo, mag);
-      int d[kS];
+      load_pair<NC>(a + (i * g.k + k0 + u) * NC, hi, lo, mag);
       if (isfinite(mag)) {
+        int d[kS];
         digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
-      } else {
 #pragma unroll
-        for (int s = 0; s < kS; ++s) d[s] = 0;
+        for (int s = 0; s < kS; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
       }
-#pragma unroll
-      for (int s = 0; s < kS; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
     }
-    int8_t* row = out + i * (kS * kp) + k0;
+    const int64_t c = k0 / g.kc, kk = k0 % g.kc;
+    int8_t* row = out + i * g.row_bytes() + c * kS * g.kc + kk;
 #pragma unroll
-    for (int s = 0; s < kS; ++s) *reinterpret_cast<unsigned*>(row + s * kp) = packed[s];
+    for (int s = 0; s < kS; ++s) *reinterpret_cast<unsigned*>(row + s * g.kc) = packed[s];
   }
 }
 
-// B (k x n, NC comps, row-major) -> digit planes transposed, rows of kS * kp
-// bytes per column j with the planes in reverse order,
-//   out[j, (kS - 1 - t) * kp + k] = digit t of B[k, j] 2^-e[j],
-// so the diagonal-q operand (planes q, q-1, .., 0) is one contiguous run; and
-// bt[j, k, :] = B[k, j, :] (binary32, for the fallback list).
+// B (k x n, NC comps, row stride ldb elements) -> digit planes transposed,
+// one row of g.row_bytes() per column j with each chunk's planes in reverse
+// order, byte [j][c kS kc + (kS-1-t) kc + kk] = digit t of B[c kc + kk, j] 2^-e[j],
+// so the diagonal-q operand of a chunk (planes q, .., 0) is one contiguous
+// run; and bt[j, k, :] = B[k, j, :] (binary32, for the fallback list).
+// CTA tile 32 k x 32 j: lane = column (coalesced loads along n), each thread
+// four consecutive k packed into one 32-bit word per digit; shared rows
+// padded to 9 words so the lanes' stores hit distinct banks.
 template <int NC>
-__global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b, int64_t k, int64_t n, int64_t kp,
+__global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b, int64_t n, int64_t ldb, KGeo g,
                                                      const int* __restrict__ e, int8_t* __restrict__ out,
                                                      float* __restrict__ bt) {
-  __shared__ __align__(16) int8_t dg[kS][kSlab][kSlab];  // [t][j][k]
-  __shared__ float tv[kSlab][kSlab * NC + 1];             // [j][k * NC + c]
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+  __shared__ unsigned dg[kS][kSlab][kSlab / 4 + 1];  // [t][j][k / 4]
+  __shared__ float tv[kSlab][kSlab * NC + 1];        // [j][k * NC + c]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps x 4 k each
   const int64_t k0 = (int64_t)blockIdx.y * kSlab, j0 = (int64_t)blockIdx.x * kSlab;
   const int64_t j = j0 + tx;
   const double sc = j < n ? pow2d(-e[j]) : 1.0;
+  unsigned packed[kS];
 #pragma unroll
-  for (int r = 0; r < kSlab / 8; ++r) {
-    const int kk = ty + 8 * r;
+  for (int t = 0; t < kS; ++t) packed[t] = 0u;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int kk = ty * 4 + u;
     const int64_t gk = k0 + kk;
-    int d[kS];
-#pragma unroll
-    for (int s = 0; s < kS; ++s) d[s] = 0;
-    if (gk < k && j < n) {
+    if (gk < g.k && j < n) {
       double hi, lo, mag;
-      load_pair<NC>(b + (gk * n + j) * NC, hi, lo, mag);
+      load_pair<NC>(b + (gk * ldb + j) * NC, hi, lo, mag);
 #pragma unroll
-      for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * n + j) * NC + c];
-      if (isfinite(mag)) digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
+      for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * ldb + j) * NC + c];
+      if (isfinite(mag)) {
+        int d[kS];
+        digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
+#pragma unroll
+        for (int t = 0; t < kS; ++t) packed[t] |= ((unsigned)(d[t] & 0xff)) << (8 * u);
+      }
     }
-#pragma unroll
-    for (int s = 0; s < kS; ++s) dg[s][tx][kk] = (int8_t)d[s];
   }
+#pragma unroll
+  for (int t = 0; t < kS; ++t) dg[t][tx][ty] = packed[t];
   __syncthreads();
   // digit rows: kS * 32 rows (t, jj) of 32 bytes; 8 threads x 4 bytes per row
+  const int64_t kp = g.kc * g.nkc;
   for (int w = threadIdx.x; w < kS * kSlab * 8; w += blockDim.x) {
     const int row = w / 8, part = w % 8;
     const int t = row / kSlab, jj = row % kSlab;
-    const int64_t gj = j0 + jj;
-    if (gj >= n || k0 + part * 4 >= kp) continue;
-    *reinterpret_cast<unsigned*>(out + gj * (kS * kp) + (kS - 1 - t) * kp + k0 + part * 4) =
-        *reinterpret_cast<const unsigned*>(&dg[t][jj][part * 4]);
+    const int64_t gj = j0 + jj, gk = k0 + part * 4;
+    if (gj >= n || gk >= kp) continue;
+    const int64_t c = gk / g.kc, kk = gk % g.kc;
+    *reinterpret_cast<unsigned*>(out + gj * g.row_bytes() + c * kS * g.kc + (kS - 1 - t) * g.kc + kk) =
+        dg[t][jj][part];
   }
   // transposed binary32 copy
   for (int w = threadIdx.x; w < kSlab * kSlab * NC; w += blockDim.x) {
     const int jj = w / (kSlab * NC), rest = w % (kSlab * NC);
     const int kk = rest / NC;
     const int64_t gj = j0 + jj, gk = k0 + kk;
-    if (gj < n && gk < k) bt[(gj * k + gk) * NC + rest % NC] = tv[jj][rest];
+    if (gj < n && gk < g.k) bt[(gj * g.k + gk) * NC + rest % NC] = tv[jj][rest];
   }
 }
 
-// C = sum_q C_q 2^(-12-7q) (exact double-double), scaled back, split into
-// two binary32 components; ill-conditioned / non-finite outputs are listed
-// for the fallback instead.
+// C = sum_{c,q} C_cq 2^(-14-8q) (int64 over chunks, then exact double-double),
+// scaled back, split into two binary32 components written with row stride
+// ldo; ill-conditioned / non-finite outputs are listed per row
+// (rlist[i * n + slot] = j, rcnt[i] entries) for the fallback.
 __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
-                                                 const int* __restrict__ ea, const int* __restrict__ eb,
+                                                 int nkc, const int* __restrict__ ea, const int* __restrict__ eb,
                                                  const int* __restrict__ rnf, const int* __restrict__ cnf,
-                                                 double thr, float* __restrict__ out, int* __restrict__ list,
-                                                 int* __restrict__ count) {
-  const int64_t mn = m * n;
+                                                 double thr, float* __restrict__ out, int64_t ldo,
+                                                 int* __restrict__ rlist, int* __restrict__ rcnt) {
+  const int64_t mn = m * n, plane = m * ldc;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < mn; x += stride) {
     const int64_t i = x / n, j = x % n;
+    const int64_t off = i * ldc + j;
     double hi = 0.0, lo = 0.0;
 #pragma unroll
     for (int q = kS - 1; q >= 0; --q) {
-      const double t = __dmul_rn((double)cq[q * m * ldc + i * ldc + j], pow2d(-12 - 7 * q));
+      long long acc = cq[q * plane + off];
+      for (int c = 1; c < nkc; ++c) acc += cq[((int64_t)c * kS + q) * plane + off];
+      const double t = __dmul_rn((double)acc, pow2d(-14 - 8 * q));
       double s, err;
       dsum(hi, t, s, err);
       hi = s;
@@ -243,30 +303,31 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
     double s2, e2;
     dsum(hi, lo, s2, e2);
     if (rnf[i] | cnf[j] || !(fabs(s2) >= thr)) {
-      list[atomicAdd(count, 1)] = (int)x;
+      rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
       continue;
     }
     const double sc = pow2d(ea[i] + eb[j]);
     const double v[2] = {__dmul_rn(s2, sc), __dmul_rn(e2, sc)};
-    split_out<float, 2, 2>(v, out + x * 2);
+    split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
   }
 }
 
-// the listed outputs, a warp each: products of binary32 components are exact
+// the listed outputs: a CTA per row (its warps share the row of A through
+// L1), a warp per listed output.  Products of binary32 components are exact
 // in binary64; each lane keeps a double-double (two_sum into S, errors into
-// C), lanes merge by an xor butterfly (the same value on every lane)
+// C), lanes merge by an xor butterfly (the same value on every lane).
 template <int NCA, int NCB>
 __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, const float* __restrict__ bt,
-                                                  int64_t n, int64_t k, const int* __restrict__ list,
-                                                  const int* __restrict__ count, float* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int cnt = *count;
-  for (int64_t w = gw; w < cnt; w += nw) {
-    const int64_t x = list[w];
-    const int64_t i = x / n, j = x % n;
-    const float* ar = a + i * k * NCA;
+                                                  int64_t n, int64_t k, const int* __restrict__ rlist,
+                                                  const int* __restrict__ rcnt, float* __restrict__ out,
+                                                  int64_t ldo) {
+  const int64_t i = blockIdx.x;
+  const int cnt = rcnt[i];
+  if (cnt == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const float* ar = a + i * k * NCA;
+  for (int w = warp; w < cnt; w += nw) {
+    const int64_t j = rlist[i * n + w];
     const float* br = bt + j * k * NCB;
     double S = 0.0, C = 0.0;
     for (int64_t t = lane; t < k; t += 32) {
@@ -274,7 +335,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
       for (int ca = 0; ca < NCA; ++ca)
 #pragma unroll
         for (int cb = 0; cb < NCB; ++cb) {
-          const double p = __dmul_rn((double)ar[t * NCA + ca], (double)br[t * NCB + cb]);
+          const double p = __dmul_rn((double)__ldg(ar + t * NCA + ca), (double)br[t * NCB + cb]);
           double e;
           dsum(S, p, S, e);
           C = __dadd_rn(C, e);
@@ -289,7 +350,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
     }
     if (lane == 0) {
       const double v[2] = {S, C};
-      split_out<float, 2, 2>(v, out + x * 2);
+      split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
     }
   }
 }
@@ -309,8 +370,9 @@ mcf_status lt_fail(const char* what, int code) {
   return mcfr::fail(MCF_ERR_CUDA, std::string("mm_fast int8 GEMM: ") + what + " (status " + std::to_string(code) + ")");
 }
 
-// C (rows_c x cols_c, col-major, ld rows_c, int32) = opA^T(A) . B, with
-// A: kd x rows_c int8 col-major (ld lda), B: kd x cols_c int8 col-major (ld ldb)
+// C (rows_c x cols_c, col-major, ld rows_c, int32) = A^T B with
+// A: kd x rows_c int8 col-major (ld lda), B: kd x cols_c int8 col-major (ld ldb).
+// MCF_ERR_UNSUPPORTED (no message) when cuBLASLt has no algorithm for the shape.
 mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int* C, int64_t rows_c,
                    int64_t cols_c, int64_t kd, cudaStream_t s) {
   int dev = 0;
@@ -390,32 +452,35 @@ char* oz_workspace(std::size_t bytes, cudaStream_t s) {
 }
 
 std::size_t al(std::size_t b) { return (b + 255) & ~std::size_t(255); }
+int64_t pad16(int64_t v) { return (v + 15) / 16 * 16; }
 
 }  // namespace
 
-// Prepared B operand: digit planes, column exponents, non-finite flags and
-// the transposed binary32 copy.  Built once; shared by row chunks of A.
+// Prepared B operand (a block of n columns of a k x ldb matrix): digit
+// planes, column exponents, non-finite flags and the transposed binary32
+// copy.  Built once; shared by every row chunk of A.
 struct PreparedB {
   const int8_t* planes = nullptr;
   const float* bt = nullptr;
   const int* eb = nullptr;
   const int* cnf = nullptr;
-  int64_t k = 0, kp = 0, n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
+  KGeo g{};
+  int64_t n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
   int ncb = 1;
 };
 
-int64_t pad16(int64_t v) { return (v + 15) / 16 * 16; }
-
 std::size_t b_bytes(int64_t k, int64_t n, int ncb) {
-  const int64_t kp = pad16(k), np = pad16(n);
-  return al(np * kS * kp) + al(n * k * ncb * 4) + al(n * 4) * 2 + al(n * 8);
+  const KGeo g = kgeo(k);
+  return al(pad16(n) * g.row_bytes()) + al(n * k * ncb * 4) + al(n * 4) * 2 + al(n * 8);
 }
 
-mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, char* buf, PreparedB& pb, cudaStream_t s) {
-  const int64_t kp = pad16(k), np = pad16(n);
+mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb, char* buf, PreparedB& pb,
+                     cudaStream_t s) {
+  const KGeo g = kgeo(k);
+  const int64_t np = pad16(n);
   int8_t* planes = reinterpret_cast<int8_t*>(buf);
-  buf += al(np * kS * kp);
-  if (np > n && cudaMemsetAsync(planes + n * kS * kp, 0, (np - n) * kS * kp, s) != cudaSuccess)
+  buf += al(np * g.row_bytes());
+  if (np > n && cudaMemsetAsync(planes + n * g.row_bytes(), 0, (np - n) * g.row_bytes(), s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the padding columns");
   float* bt = reinterpret_cast<float*>(buf);
   buf += al(n * k * ncb * 4);
@@ -427,71 +492,77 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, char* buf, P
   if (cudaMemsetAsync(cnf, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cm, 0, n * 8, s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the column maxima");
   const dim3 gm((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
-  if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, cm, cnf);
-  else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, cm, cnf);
+  if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
+  else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
   k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, eb);
-  const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)((kp + kSlab - 1) / kSlab));
-  if (ncb == 2) k_slice_cols<2><<<gs, 256, 0, s>>>(w, k, n, kp, eb, planes, bt);
-  else k_slice_cols<1><<<gs, 256, 0, s>>>(w, k, n, kp, eb, planes, bt);
-  for (int i = 0; i < 4; ++i) mcfr::note_launch();
-  pb = PreparedB{planes, bt, eb, cnf, k, kp, n, np, ncb};
+  const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)((g.kc * g.nkc + kSlab - 1) / kSlab));
+  if (ncb == 2) k_slice_cols<2><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt);
+  else k_slice_cols<1><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt);
+  for (int i = 0; i < 3; ++i) mcfr::note_launch();
+  pb = PreparedB{planes, bt, eb, cnf, g, n, np, ncb};
   return mcfr::check_launch("mm_fast B digit kernels");
 }
 
 std::size_t rows_bytes(int64_t m, int64_t k, int64_t n) {
-  const int64_t kp = pad16(k), np = pad16(n);
-  return al(m * kS * kp) + al((int64_t)kS * m * np * 4) + al(m * n * 4) + al(m * 4) * 2 + 256;
+  const KGeo g = kgeo(k);
+  return al(m * g.row_bytes()) + al((int64_t)kS * g.nkc * m * pad16(n) * 4) + al(m * n * 4) + al(m * 4) * 3;
 }
 
-// out (m x n x 2 binary32) = A (m x k x nca) . B for a prepared B
-// ev (optional, 4 events): recorded before the A digits, before the GEMMs,
-// after the GEMMs and at the end (phase timing for the benchmark)
-mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, char* buf, cudaStream_t s,
-                cudaEvent_t* ev = nullptr) {
-  const int64_t k = pb.k, kp = pb.kp, n = pb.n, np = pb.np;
+// out (m x n x 2 binary32, row stride ldo elements) = A (m x k x nca) . B for
+// a prepared B.  ev (optional, 4 events): recorded before the A digits,
+// before the GEMMs, after the GEMMs and at the end (phase timing).
+mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo, char* buf,
+                cudaStream_t s, cudaEvent_t* ev = nullptr) {
+  const KGeo g = pb.g;
+  const int64_t k = g.k, n = pb.n, np = pb.np;
   int8_t* planes = reinterpret_cast<int8_t*>(buf);
-  buf += al(m * kS * kp);
+  buf += al(m * g.row_bytes());
   int* cq = reinterpret_cast<int*>(buf);
-  buf += al((int64_t)kS * m * np * 4);
-  int* list = reinterpret_cast<int*>(buf);
+  buf += al((int64_t)kS * g.nkc * m * np * 4);
+  int* rlist = reinterpret_cast<int*>(buf);
   buf += al(m * n * 4);
   int* ea = reinterpret_cast<int*>(buf);
   buf += al(m * 4);
   int* rnf = reinterpret_cast<int*>(buf);
   buf += al(m * 4);
-  int* count = reinterpret_cast<int*>(buf);
+  int* rcnt = reinterpret_cast<int*>(buf);
   if (ev) cudaEventRecord(ev[0], s);
-  if (cudaMemsetAsync(count, 0, sizeof(int), s) != cudaSuccess)
-    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counter");
+  if (cudaMemsetAsync(rcnt, 0, m * sizeof(int), s) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counters");
   const unsigned gr = (unsigned)((m + 7) / 8);
   if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, ea, rnf);
   else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, ea, rnf);
-  const int gsl = mcfr::grid_for(m * (kp / 4), 256, 8);
-  if (nca == 2) k_slice_rows<2><<<gsl, 256, 0, s>>>(x, m, k, kp, ea, planes);
-  else k_slice_rows<1><<<gsl, 256, 0, s>>>(x, m, k, kp, ea, planes);
+  const int gsl = mcfr::grid_for(m * (g.kc * g.nkc / 4), 256, 8);
+  if (nca == 2) k_slice_rows<2><<<gsl, 256, 0, s>>>(x, m, g, ea, planes);
+  else k_slice_rows<1><<<gsl, 256, 0, s>>>(x, m, g, ea, planes);
   mcfr::note_launch();
   mcfr::note_launch();
   mcf_status st = mcfr::check_launch("mm_fast A digit kernels");
   if (st != MCF_OK) return st;
-  // diagonal q: A planes 0..q (the first (q+1) kp bytes of each row) against
-  // B planes q..0 (the last (q+1) kp bytes of each column row); C_q is
-  // produced as an n x m column-major = m x n row-major int32 matrix
+  // chunk c, diagonal q: A planes 0..q of the chunk (its first (q+1) kc
+  // bytes) against B planes q..0 (the chunk's last (q+1) kc bytes); C_cq is
+  // an np x m column-major = m x np row-major int32 matrix
   if (ev) cudaEventRecord(ev[1], s);
-  for (int q = 0; q < kS; ++q) {
-    st = gemm_s8(pb.planes + (int64_t)(kS - 1 - q) * kp, kS * kp, planes, kS * kp, cq + (int64_t)q * m * np, np, m,
-                 (int64_t)(q + 1) * kp, s);
-    if (st != MCF_OK) return st;
-  }
+  const int64_t ld = g.row_bytes();
+  for (int64_t c = 0; c < g.nkc; ++c)
+    for (int q = 0; q < kS; ++q) {
+      const int64_t base = c * kS * g.kc;
+      st = gemm_s8(pb.planes + base + (int64_t)(kS - 1 - q) * g.kc, ld, planes + base, ld,
+                   cq + (c * kS + q) * m * np, np, m, (int64_t)(q + 1) * g.kc, s);
+      if (st != MCF_OK) return st;
+    }
   if (ev) cudaEventRecord(ev[2], s);
-  // fallback threshold (scaled units): 2^51 K (kS + 1.1) 2^(-7 kS)
-  const double thr = ldexp((double)k * (kS + 1.1), 51 - 7 * kS);
-  k_combine<<<mcfr::grid_for(m * n, 256, 8), 256, 0, s>>>(cq, m, n, np, ea, pb.eb, rnf, pb.cnf, thr, out, list, count);
+  // fallback threshold (scaled units): 2^50 K 2^-68.8, so every combined
+  // output has relative error <= 2^-50 before the split
+  const double thr = ldexp((double)k * 1.15, 50 - 69);
+  k_combine<<<mcfr::grid_for(m * n, 256, 8), 256, 0, s>>>(cq, m, n, np, (int)g.nkc, ea, pb.eb, rnf, pb.cnf, thr,
+                                                          out, ldo, rlist, rcnt);
   mcfr::note_launch();
-  const int gf = mcfr::sm_count() * 8;
-  if (nca == 2 && pb.ncb == 2) k_fallback<2, 2><<<gf, 256, 0, s>>>(x, pb.bt, n, k, list, count, out);
-  else if (nca == 2) k_fallback<2, 1><<<gf, 256, 0, s>>>(x, pb.bt, n, k, list, count, out);
-  else if (pb.ncb == 2) k_fallback<1, 2><<<gf, 256, 0, s>>>(x, pb.bt, n, k, list, count, out);
-  else k_fallback<1, 1><<<gf, 256, 0, s>>>(x, pb.bt, n, k, list, count, out);
+  const unsigned gf = (unsigned)m;
+  if (nca == 2 && pb.ncb == 2) k_fallback<2, 2><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
+  else if (nca == 2) k_fallback<2, 1><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
+  else if (pb.ncb == 2) k_fallback<1, 2><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
+  else k_fallback<1, 1><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
   mcfr::note_launch();
   if (ev) cudaEventRecord(ev[3], s);
   return mcfr::check_launch("mm_fast combine kernels");
@@ -503,7 +574,7 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
 namespace mcfr {
 
 bool ozaki_supported(int64_t m, int64_t k, int64_t n) {
-  return m > 0 && n > 0 && k > 0 && (k + 15) / 16 * 16 <= mcfg::oz::kMaxKp && m * n < (int64_t(1) << 31);
+  return m > 0 && n > 0 && k > 0 && m * n < (int64_t(1) << 31) && k < (int64_t(1) << 31);
 }
 
 // one-call MC(nc=2, binary32) x T / MC(nc=2) product on the INT8 tensor cores
@@ -514,9 +585,9 @@ mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m,
   char* ws = oz_workspace(bb + rows_bytes(m, k, n), s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
   PreparedB pb;
-  mcf_status st = prepare_b(w, ncb, k, n, ws, pb, s);
+  mcf_status st = prepare_b(w, ncb, k, n, n, ws, pb, s);
   if (st != MCF_OK) return st;
-  return rows(x, nca, m, pb, out, ws + bb, s);
+  return rows(x, nca, m, pb, out, n, ws + bb, s);
 }
 
 int ozaki_digits() { return mcfg::oz::kS; }
@@ -534,8 +605,8 @@ mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, in
   for (auto& e : ev) cudaEventCreate(&e);
   cudaEventRecord(ev[4], s);
   PreparedB pb;
-  mcf_status st = prepare_b(w, 1, k, n, ws, pb, s);
-  if (st == MCF_OK) st = rows(x, 2, m, pb, out, ws + bb, s, ev);
+  mcf_status st = prepare_b(w, 1, k, n, n, ws, pb, s);
+  if (st == MCF_OK) st = rows(x, 2, m, pb, out, n, ws + bb, s, ev);
   if (st == MCF_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(MCF_ERR_CUDA, "mm_fast: sync");
   if (st == MCF_OK) {
     float t = 0.f;
@@ -545,41 +616,58 @@ mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, in
       cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
       ms[i + 1] = t;
     }
-    // the fallback counter sits at the end of the rows region
-    const int64_t kp = pad16(k), np = pad16(n);
-    const char* cnt = ws + bb + al(m * kS * kp) + al((int64_t)kS * m * np * 4) + al(m * n * 4) + al(m * 4) * 2;
-    int c = 0;
-    cudaMemcpy(&c, cnt, sizeof(int), cudaMemcpyDeviceToHost);
+    // the per-row fallback counters sit at the end of the rows region
+    const KGeo g = kgeo(k);
+    const char* cnt = ws + bb + al(m * g.row_bytes()) + al((int64_t)kS * g.nkc * m * pad16(n) * 4) +
+                      al(m * n * 4) + al(m * 4) * 2;
+    std::vector<int> rc(m);
+    cudaMemcpy(rc.data(), cnt, m * sizeof(int), cudaMemcpyDeviceToHost);
+    int64_t c = 0;
+    for (int v : rc) c += v;
     *fallback = c;
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return st;
 }
 
-}  // namespace mcfr
-
-namespace mcfr {
-
-// Host-buffer MC(nc=2, binary32) x T on the tensor-core path, pipelined over
-// row chunks: B is copied and prepared once; chunk c's H2D copy (cin), digit
-// planes + GEMMs + combine (comp[c % 2], each with its own workspace region)
-// and D2H copy (cout) overlap the neighbouring chunks.
+// Host-buffer MC(nc=2, binary32) x T on the tensor-core path, pipelined in
+// two dimensions: B is sent and prepared in column blocks (each block is
+// independent: per-column scaling), A in row chunks; the copy stream sends B
+// block 0, A chunk 0, the remaining B blocks, then the remaining A chunks, so
+// the first (chunk, block) product starts after two pieces instead of all of
+// B.  Products alternate between two compute streams (each with its own
+// workspace region); each product's D2H copy (a strided 2-D copy) runs on the
+// copy-out stream as soon as it is done.
 mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout, float* dx,
                       float* dw, float* dout, cudaStream_t cin, const cudaStream_t comp[2], cudaStream_t cout) {
   using namespace mcfg::oz;
   if (!ozaki_supported(m, k, n)) return MCF_ERR_UNSUPPORTED;
-  const int64_t rc = std::min<int64_t>(m, std::max<int64_t>(1024, (m + 3) / 4));
+  static const int64_t chunk_env = [] {
+    const char* e = getenv("MCF_OZ_CHUNK");  // tuning knob: rows per chunk
+    return e ? atoll(e) : 0LL;
+  }();
+  static const int64_t blocks_env = [] {
+    const char* e = getenv("MCF_OZ_BLOCKS");  // tuning knob: column blocks of B
+    return e ? atoll(e) : 0LL;
+  }();
+  const int64_t rc = std::min<int64_t>(m, chunk_env > 0 ? chunk_env : std::max<int64_t>(1024, (m + 3) / 4));
   const int nch = (int)((m + rc - 1) / rc);
-  const std::size_t bb = b_bytes(k, n, 1), rb = rows_bytes(rc, k, n);
-  char* ws = oz_workspace(bb + 2 * rb, comp[0]);
+  const int64_t nbk = blocks_env > 0 ? blocks_env : 1;  // measured: column blocks do not pay at config 2
+  const int64_t bw = pad16((n + nbk - 1) / nbk);
+  const int nb = (int)((n + bw - 1) / bw);
+  const std::size_t bb = b_bytes(k, bw, 1), rb = rows_bytes(rc, k, bw);
+  char* ws = oz_workspace(nb * al(bb) + 2 * rb, comp[0]);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
-  std::vector<cudaEvent_t> ev(2 * nch + 2, nullptr);
-  for (auto& e : ev)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+  std::vector<cudaEvent_t> evb(nb, nullptr), evp(nb, nullptr), eva(nch, nullptr), evt(nch * nb, nullptr);
+  std::vector<cudaEvent_t*> all;
+  for (auto* v : {&evb, &evp, &eva, &evt})
+    for (auto& e : *v) all.push_back(&e);
+  for (auto* e : all)
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
       return fail(MCF_ERR_CUDA, "mm_fast: cannot create pipeline events");
   auto done = [&](mcf_status st) {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
+    for (auto* e : all)
+      if (*e) cudaEventDestroy(*e);
     return st;
   };
   auto cu = [&](cudaError_t e, const char* what) {
@@ -591,26 +679,54 @@ mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, in
     const mcf_status _s = (expr);      \
     if (_s != MCF_OK) return done(_s); \
   } while (0)
-  OZ_TRY(cu(cudaMemcpyAsync(dw, hw, k * n * sizeof(float), cudaMemcpyHostToDevice, cin), "H2D w"));
-  OZ_TRY(cu(cudaEventRecord(ev[0], cin), "event"));
-  OZ_TRY(cu(cudaStreamWaitEvent(comp[0], ev[0], 0), "wait"));
-  PreparedB pb;
-  OZ_TRY(prepare_b(dw, 1, k, n, ws, pb, comp[0]));
-  OZ_TRY(cu(cudaEventRecord(ev[1], comp[0]), "event"));
-  OZ_TRY(cu(cudaStreamWaitEvent(comp[1], ev[1], 0), "wait"));
-  for (int c = 0; c < nch; ++c) {
+  std::vector<PreparedB> pb(nb);
+  auto send_b = [&](int b) -> mcf_status {
+    const int64_t j0 = b * bw, w = std::min<int64_t>(bw, n - j0);
+    mcf_status st = cu(cudaMemcpy2DAsync(dw + j0, n * sizeof(float), hw + j0, n * sizeof(float), w * sizeof(float), k,
+                                         cudaMemcpyHostToDevice, cin), "H2D w");
+    if (st == MCF_OK) st = cu(cudaEventRecord(evb[b], cin), "event");
+    cudaStream_t ps = comp[b & 1];
+    if (st == MCF_OK) st = cu(cudaStreamWaitEvent(ps, evb[b], 0), "wait");
+    if (st == MCF_OK) st = prepare_b(dw + j0, 1, k, w, n, ws + b * al(bb), pb[b], ps);
+    if (st == MCF_OK) st = cu(cudaEventRecord(evp[b], ps), "event");
+    return st;
+  };
+  auto send_a = [&](int c) -> mcf_status {
     const int64_t r0 = c * rc, rows_c = std::min<int64_t>(rc, m - r0);
-    cudaStream_t cs = comp[c & 1];
-    cudaEvent_t ex = ev[2 + 2 * c], em = ev[3 + 2 * c];
-    OZ_TRY(cu(cudaMemcpyAsync(dx + r0 * k * 2, hx + r0 * k * 2, rows_c * k * 2 * sizeof(float),
-                              cudaMemcpyHostToDevice, cin), "H2D x"));
-    OZ_TRY(cu(cudaEventRecord(ex, cin), "event"));
-    OZ_TRY(cu(cudaStreamWaitEvent(cs, ex, 0), "wait"));
-    OZ_TRY(rows(dx + r0 * k * 2, 2, rows_c, pb, dout + r0 * n * 2, ws + bb + (c & 1) * rb, cs));
-    OZ_TRY(cu(cudaEventRecord(em, cs), "event"));
-    OZ_TRY(cu(cudaStreamWaitEvent(cout, em, 0), "wait"));
-    OZ_TRY(cu(cudaMemcpyAsync(hout + r0 * n * 2, dout + r0 * n * 2, rows_c * n * 2 * sizeof(float),
-                              cudaMemcpyDeviceToHost, cout), "D2H out"));
+    mcf_status st = cu(cudaMemcpyAsync(dx + r0 * k * 2, hx + r0 * k * 2, rows_c * k * 2 * sizeof(float),
+                                       cudaMemcpyHostToDevice, cin), "H2D x");
+    if (st == MCF_OK) st = cu(cudaEventRecord(eva[c], cin), "event");
+    return st;
+  };
+  int task = 0;
+  auto product = [&](int c, int b) -> mcf_status {
+    const int64_t r0 = c * rc, rows_c = std::min<int64_t>(rc, m - r0);
+    const int64_t j0 = b * bw, w = std::min<int64_t>(bw, n - j0);
+    cudaStream_t cs = comp[task & 1];
+    char* region = ws + nb * al(bb) + (task & 1) * rb;
+    ++task;
+    mcf_status st = cu(cudaStreamWaitEvent(cs, eva[c], 0), "wait");
+    if (st == MCF_OK) st = cu(cudaStreamWaitEvent(cs, evp[b], 0), "wait");
+    if (st == MCF_OK) st = rows(dx + r0 * k * 2, 2, rows_c, pb[b], dout + (r0 * n + j0) * 2, n, region, cs);
+    cudaEvent_t et = evt[c * nb + b];
+    if (st == MCF_OK) st = cu(cudaEventRecord(et, cs), "event");
+    if (st == MCF_OK) st = cu(cudaStreamWaitEvent(cout, et, 0), "wait");
+    if (st == MCF_OK)
+      st = cu(cudaMemcpy2DAsync(hout + (r0 * n + j0) * 2, n * 2 * sizeof(float), dout + (r0 * n + j0) * 2,
+                                n * 2 * sizeof(float), w * 2 * sizeof(float), rows_c, cudaMemcpyDeviceToHost,
+                                cout), "D2H out");
+    return st;
+  };
+  OZ_TRY(send_b(0));
+  OZ_TRY(send_a(0));
+  OZ_TRY(product(0, 0));
+  for (int b = 1; b < nb; ++b) {
+    OZ_TRY(send_b(b));
+    OZ_TRY(product(0, b));
+  }
+  for (int c = 1; c < nch; ++c) {
+    OZ_TRY(send_a(c));
+    for (int b = 0; b < nb; ++b) OZ_TRY(product(c, b));
   }
 #undef OZ_TRY
   return done(cu(cudaStreamSynchronize(cout), "sync"));

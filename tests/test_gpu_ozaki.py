@@ -1,7 +1,7 @@
 """MCF_FAST on the INT8 tensor cores (mm_ozaki.cu) against the oracle.
 
-The tensor-core path splits the row/column-scaled operands into ten signed
-7-bit digits, multiplies digit planes exactly in int32 and recombines in
+The tensor-core path splits the row/column-scaled operands into nine balanced
+base-256 digits, multiplies digit planes exactly in int32 and recombines in
 double-double; outputs too small for the split's error bound (cancellation)
 and rows / columns holding Inf or NaN are recomputed by the fallback kernel.
 Bar (BASELINE.json north star): median and max relative error each <= 4x the
@@ -157,3 +157,18 @@ def test_deterministic_and_chunking_invariant(gr):
     assert_bits(sub, a[1000:1100], "row block alone")
     h = mcf.host.mm_mcn(x, w, strategy=mcf.FAST)
     assert_bits(h, a, "host pipeline")
+
+
+def test_long_k_is_cut_into_int32_safe_chunks(gr, port):
+    """K beyond one int8 GEMM's int32 headroom (9 digits x kc x 2^14 < 2^31,
+    kc <= 14400): the digit planes are cut into K chunks whose partial
+    products are summed in int64 before the recombination."""
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(37)
+    m, k, n = 6, 20000, 20
+    x = split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    w = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    got = gr.run("mm_mcn", x, w, plan=mcf.FAST)
+    rows, cols = np.repeat(np.arange(m), n), np.tile(np.arange(n), m)
+    _within_4x(port, x, w, rows, cols, got.reshape(-1, 2), "K = 20000 (two chunks)")
