@@ -53,6 +53,7 @@ namespace {
 constexpr int kS = 9;                // digits per operand
 constexpr int kSlab = 32;            // transpose tile of the column slicer
 constexpr int64_t kMaxChunk = 14400; // int32 headroom: kS * kc * 2^14 < 2^31
+constexpr int64_t kMaxChunks = 16;    // combine: 16 chunk sums x 2^16.01 x 2^31 < 2^53
 
 __device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
@@ -120,10 +121,11 @@ struct KGeo {
   __host__ __device__ int64_t row_bytes() const { return kS * kc * nkc; }
 };
 
+// kc is a multiple of 32, so a 32-wide k tile never straddles two chunks
 KGeo kgeo(int64_t k) {
-  const int64_t k16 = (k + 15) / 16 * 16;
-  const int64_t nkc = (k16 + kMaxChunk - 1) / kMaxChunk;
-  const int64_t kc = ((k16 + nkc - 1) / nkc + 15) / 16 * 16;
+  const int64_t k32 = (k + 31) / 32 * 32;
+  const int64_t nkc = (k32 + kMaxChunk - 1) / kMaxChunk;
+  const int64_t kc = ((k32 + nkc - 1) / nkc + 31) / 32 * 32;
   return KGeo{k, kc, nkc};
 }
 
@@ -136,19 +138,22 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   double m = 0.0;
-  bool bad = false;
+  bool bad = false, split = false;
   for (int64_t t = lane; t < k; t += 32) {
     double hi, lo, mag;
     load_pair<NC>(a + (r * k + t) * NC, hi, lo, mag);
     bad |= !isfinite(mag);
+    split |= lo != 0.0;
     m = fmax(m, mag);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
   bad = __any_sync(0xffffffffu, bad);
+  split = __any_sync(0xffffffffu, split);
   if (lane == 0) {
     e[r] = exp_above_d(m);
-    nf[r] = bad ? 1 : 0;
+    // bit 0: a non-finite element; bit 1: some c0 + c1 is not one binary64
+    nf[r] = (bad ? 1 : 0) | (split ? 2 : 0);
   }
 }
 
@@ -185,21 +190,22 @@ __global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __rest
 template <int NC>
 __global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a, int64_t rows, KGeo g,
                                                      const int* __restrict__ e, int8_t* __restrict__ out) {
-  const int64_t kp = g.kc * g.nkc;
-  const int64_t q4 = kp / 4;
-  const int64_t total = rows * q4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
-    const int64_t i = q / q4, k0 = (q % q4) * 4;
+  // grid: x covers the padded row in 4-k groups, y (strided) the rows
+  const int kp = (int)(g.kc * g.nkc), kc = (int)g.kc, k = (int)g.k;
+  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k0 >= kp) return;
+  const int c = k0 / kc, kk = k0 - c * kc;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     const double sc = pow2d(-e[i]);
     unsigned packed[kS];
 #pragma unroll
     for (int s = 0; s < kS; ++s) packed[s] = 0u;
+    const float* ar = a + i * k * NC;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (k0 + u >= g.k) break;
+      if (k0 + u >= k) break;
       double hi, lo, mag;
-      load_pair<NC>(a + (i * g.k + k0 + u) * NC, hi, lo, mag);
+      load_pair<NC>(ar + (k0 + u) * NC, hi, lo, mag);
       if (isfinite(mag)) {
         int d[kS];
         digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
@@ -207,10 +213,9 @@ __global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a,
         for (int s = 0; s < kS; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
       }
     }
-    const int64_t c = k0 / g.kc, kk = k0 % g.kc;
-    int8_t* row = out + i * g.row_bytes() + c * kS * g.kc + kk;
+    int8_t* row = out + i * g.row_bytes() + c * kS * kc + kk;
 #pragma unroll
-    for (int s = 0; s < kS; ++s) *reinterpret_cast<unsigned*>(row + s * g.kc) = packed[s];
+    for (int s = 0; s < kS; ++s) *reinterpret_cast<unsigned*>(row + s * kc) = packed[s];
   }
 }
 
@@ -255,16 +260,17 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
 #pragma unroll
   for (int t = 0; t < kS; ++t) dg[t][tx][ty] = packed[t];
   __syncthreads();
-  // digit rows: kS * 32 rows (t, jj) of 32 bytes; 8 threads x 4 bytes per row
-  const int64_t kp = g.kc * g.nkc;
+  // digit rows: kS * 32 rows (t, jj) of 32 bytes; 8 threads x 4 bytes per
+  // row.  The tile's 32 k lie in one chunk (kc is a multiple of 32).
+  const int kc = (int)g.kc, c = (int)(k0 / kc), kk0 = (int)(k0 - (int64_t)c * kc);
+  const int64_t rb = g.row_bytes();
+  int8_t* base = out + (int64_t)c * kS * kc + kk0;
   for (int w = threadIdx.x; w < kS * kSlab * 8; w += blockDim.x) {
-    const int row = w / 8, part = w % 8;
+    const int row = w >> 3, part = w & 7;
     const int t = row / kSlab, jj = row % kSlab;
-    const int64_t gj = j0 + jj, gk = k0 + part * 4;
-    if (gj >= n || gk >= kp) continue;
-    const int64_t c = gk / g.kc, kk = gk % g.kc;
-    *reinterpret_cast<unsigned*>(out + gj * g.row_bytes() + c * kS * g.kc + (kS - 1 - t) * g.kc + kk) =
-        dg[t][jj][part];
+    const int64_t gj = j0 + jj;
+    if (gj >= n) continue;
+    *reinterpret_cast<unsigned*>(base + gj * rb + (kS - 1 - t) * kc + part * 4) = dg[t][jj][part];
   }
   // transposed binary32 copy
   for (int w = threadIdx.x; w < kSlab * kSlab * NC; w += blockDim.x) {
@@ -275,71 +281,144 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
   }
 }
 
-// C = sum_{c,q} C_cq 2^(-14-8q) (int64 over chunks, then exact double-double),
-// scaled back, split into two binary32 components written with row stride
-// ldo; ill-conditioned / non-finite outputs are listed per row
-// (rlist[i * n + slot] = j, rcnt[i] entries) for the fallback.
+// C = sum_{c,q} C_cq 2^(-14-8q), scaled back, split into two binary32
+// components written with row stride ldo; ill-conditioned / non-finite
+// outputs are listed per row (rlist[i * n + slot] = j, rcnt[i] entries) for
+// the fallback.  The nine diagonal sums (int64 over K chunks) are grouped in
+// threes in integer arithmetic, G = S_q 2^16 + S_q+1 2^8 + S_q+2 (|G| < 2^51,
+// exact in binary64), and the three groups (weights 2^-30, 2^-54, 2^-78) are
+// added exactly in double-double.  Grid: x covers a row, y (strided) rows.
 __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
                                                  int nkc, const int* __restrict__ ea, const int* __restrict__ eb,
                                                  const int* __restrict__ rnf, const int* __restrict__ cnf,
                                                  double thr, float* __restrict__ out, int64_t ldo,
                                                  int* __restrict__ rlist, int* __restrict__ rcnt) {
-  const int64_t mn = m * n, plane = m * ldc;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < mn; x += stride) {
-    const int64_t i = x / n, j = x % n;
-    const int64_t off = i * ldc + j;
-    double hi = 0.0, lo = 0.0;
+  static_assert(kS == 9, "three groups of three diagonals");
+  // four consecutive columns per thread: 16-byte loads from each plane (ldc
+  // is a multiple of 16; padded columns hold zeros and are not written)
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= n) return;
+  const int64_t plane = m * ldc;
+  int fj[4], nfj[4];
 #pragma unroll
-    for (int q = kS - 1; q >= 0; --q) {
-      long long acc = cq[q * plane + off];
-      for (int c = 1; c < nkc; ++c) acc += cq[((int64_t)c * kS + q) * plane + off];
-      const double t = __dmul_rn((double)acc, pow2d(-14 - 8 * q));
-      double s, err;
-      dsum(hi, t, s, err);
-      hi = s;
-      lo = __dadd_rn(lo, err);
+  for (int u = 0; u < 4; ++u) {
+    fj[u] = j0 + u < n ? eb[j0 + u] : 0;
+    nfj[u] = j0 + u < n ? cnf[j0 + u] : 0;
+  }
+  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+    const int64_t off = i * ldc + j0;
+    long long sq[kS][4];
+#pragma unroll
+    for (int q = 0; q < kS; ++q) {
+      const int4 v = *reinterpret_cast<const int4*>(cq + q * plane + off);
+      sq[q][0] = v.x;
+      sq[q][1] = v.y;
+      sq[q][2] = v.z;
+      sq[q][3] = v.w;
     }
-    double s2, e2;
-    dsum(hi, lo, s2, e2);
-    if (rnf[i] | cnf[j] || !(fabs(s2) >= thr)) {
-      rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
-      continue;
+    for (int c = 1; c < nkc; ++c)
+#pragma unroll
+      for (int q = 0; q < kS; ++q) {
+        const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * kS + q) * plane + off);
+        sq[q][0] += v.x;
+        sq[q][1] += v.y;
+        sq[q][2] += v.z;
+        sq[q][3] += v.w;
+      }
+    const int ei = ea[i], fi = rnf[i] & 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u;
+      if (j >= n) break;
+      double g[3];
+#pragma unroll
+      for (int w = 0; w < 3; ++w)
+        g[w] = (double)(sq[3 * w][u] * 65536 + sq[3 * w + 1][u] * 256 + sq[3 * w + 2][u]);
+      double hi, lo, s2, e2;
+      dsum(__dmul_rn(g[1], 0x1p-54), __dmul_rn(g[2], 0x1p-78), hi, lo);
+      dsum(__dmul_rn(g[0], 0x1p-30), hi, s2, e2);
+      e2 = __dadd_rn(e2, lo);
+      dsum(s2, e2, s2, e2);
+      if (fi | nfj[u] || !(fabs(s2) >= thr)) {
+        rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
+        continue;
+      }
+      const double sc = pow2d(ei + fj[u]);
+      const double v[2] = {__dmul_rn(s2, sc), __dmul_rn(e2, sc)};
+      split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
     }
-    const double sc = pow2d(ea[i] + eb[j]);
-    const double v[2] = {__dmul_rn(s2, sc), __dmul_rn(e2, sc)};
-    split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
   }
 }
 
-// the listed outputs: a CTA per row (its warps share the row of A through
-// L1), a warp per listed output.  Products of binary32 components are exact
-// in binary64; each lane keeps a double-double (two_sum into S, errors into
-// C), lanes merge by an xor butterfly (the same value on every lane).
-template <int NCA, int NCB>
+// the listed outputs: a CTA per row, a warp per listed output.  The CTA
+// stages its row of A in shared memory (SMEM; rows too long for it read A
+// through L1), each lane streams its k's of the column with eight loads in
+// flight.  Products of binary32 components are exact in binary64; each lane
+// keeps eight double-doubles (k = lane + 32 (8 r + u) goes to accumulator u:
+// two_sum into S, errors into C), merged in a fixed order and then across the
+// lanes by an xor butterfly (the same value on every lane): deterministic.
+template <int NCA, int NCB, bool SMEM>
 __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, const float* __restrict__ bt,
                                                   int64_t n, int64_t k, const int* __restrict__ rlist,
-                                                  const int* __restrict__ rcnt, float* __restrict__ out,
-                                                  int64_t ldo) {
+                                                  const int* __restrict__ rcnt, const int* __restrict__ rnf,
+                                                  float* __restrict__ out, int64_t ldo) {
+  extern __shared__ __align__(16) float arow[];
   const int64_t i = blockIdx.x;
   const int cnt = rcnt[i];
   if (cnt == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const float* ar = a + i * k * NCA;
+  const float* ag = a + i * k * NCA;
+  if constexpr (SMEM) {
+    for (int64_t t = threadIdx.x; t < k * NCA; t += blockDim.x) arow[t] = ag[t];
+    __syncthreads();
+  }
+  const float* ar = SMEM ? arow : ag;
+  // every c0 + c1 of the row one binary64 (and B single-component): one
+  // two_prod per k instead of a two_sum per component product
+  const bool pair = NCA == 2 && NCB == 1 && !(rnf[i] & 2);
+  constexpr int U = 8;
   for (int w = warp; w < cnt; w += nw) {
     const int64_t j = rlist[i * n + w];
     const float* br = bt + j * k * NCB;
-    double S = 0.0, C = 0.0;
-    for (int64_t t = lane; t < k; t += 32) {
+    double S8[U], C8[U];
 #pragma unroll
-      for (int ca = 0; ca < NCA; ++ca)
+    for (int u = 0; u < U; ++u) S8[u] = C8[u] = 0.0;
+    for (int64_t t0 = lane; t0 < k; t0 += 32 * U) {
+      float bv[U][NCB];
 #pragma unroll
-        for (int cb = 0; cb < NCB; ++cb) {
-          const double p = __dmul_rn((double)__ldg(ar + t * NCA + ca), (double)br[t * NCB + cb]);
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) bv[u][cb] = t0 + 32 * u < k ? br[(t0 + 32 * u) * NCB + cb] : 0.0f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t t = t0 + 32 * u;
+        if (t >= k) break;
+        if (pair) {
+          const double v = __dadd_rn((double)ar[t * 2], (double)ar[t * 2 + 1]);  // exact
+          const double bb = (double)bv[u][0];
+          const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);  // v b = p + pe exactly
           double e;
-          dsum(S, p, S, e);
-          C = __dadd_rn(C, e);
+          dsum(S8[u], p, S8[u], e);
+          C8[u] = __dadd_rn(C8[u], __dadd_rn(e, pe));
+        } else {
+#pragma unroll
+          for (int ca = 0; ca < NCA; ++ca)
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) {
+              const double p = __dmul_rn((double)ar[t * NCA + ca], (double)bv[u][cb]);
+              double e;
+              dsum(S8[u], p, S8[u], e);
+              C8[u] = __dadd_rn(C8[u], e);
+            }
         }
+      }
+    }
+    double S = S8[0], C = C8[0];
+#pragma unroll
+    for (int u = 1; u < U; ++u) {
+      double e;
+      dsum(S, S8[u], S, e);
+      C = __dadd_rn(__dadd_rn(C, C8[u]), e);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -353,6 +432,25 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
       split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
     }
   }
+}
+
+template <int NCA, int NCB>
+mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n, int64_t k, const int* rlist,
+                           const int* rcnt, const int* rnf, float* out, int64_t ldo, cudaStream_t s) {
+  const std::size_t sm = (std::size_t)k * NCA * sizeof(float);
+  constexpr std::size_t kMaxSmem = 200u << 10;
+  if (sm <= kMaxSmem) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+      attr = true;
+    }
+    k_fallback<NCA, NCB, true><<<(unsigned)m, 256, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, out, ldo);
+  } else {
+    k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, out, ldo);
+  }
+  mcfr::note_launch();
+  return MCF_OK;
 }
 
 // ---- cuBLASLt int8 GEMMs ------------------------------------------------------------------
@@ -532,7 +630,8 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   const unsigned gr = (unsigned)((m + 7) / 8);
   if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, ea, rnf);
   else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, ea, rnf);
-  const int gsl = mcfr::grid_for(m * (g.kc * g.nkc / 4), 256, 8);
+  const int64_t gx = (g.kc * g.nkc / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
+  const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
   if (nca == 2) k_slice_rows<2><<<gsl, 256, 0, s>>>(x, m, g, ea, planes);
   else k_slice_rows<1><<<gsl, 256, 0, s>>>(x, m, g, ea, planes);
   mcfr::note_launch();
@@ -555,15 +654,15 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   // fallback threshold (scaled units): 2^50 K 2^-68.8, so every combined
   // output has relative error <= 2^-50 before the split
   const double thr = ldexp((double)k * 1.15, 50 - 69);
-  k_combine<<<mcfr::grid_for(m * n, 256, 8), 256, 0, s>>>(cq, m, n, np, (int)g.nkc, ea, pb.eb, rnf, pb.cnf, thr,
+  const int64_t gcx = (n + 1023) / 1024;
+  const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
+  k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, ea, pb.eb, rnf, pb.cnf, thr,
                                                           out, ldo, rlist, rcnt);
   mcfr::note_launch();
-  const unsigned gf = (unsigned)m;
-  if (nca == 2 && pb.ncb == 2) k_fallback<2, 2><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
-  else if (nca == 2) k_fallback<2, 1><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
-  else if (pb.ncb == 2) k_fallback<1, 2><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
-  else k_fallback<1, 1><<<gf, 256, 0, s>>>(x, pb.bt, n, k, rlist, rcnt, out, ldo);
-  mcfr::note_launch();
+  if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
+  else if (nca == 2) launch_fallback<2, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
+  else if (pb.ncb == 2) launch_fallback<1, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
+  else launch_fallback<1, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
   if (ev) cudaEventRecord(ev[3], s);
   return mcfr::check_launch("mm_fast combine kernels");
 }
@@ -574,7 +673,7 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
 namespace mcfr {
 
 bool ozaki_supported(int64_t m, int64_t k, int64_t n) {
-  return m > 0 && n > 0 && k > 0 && m * n < (int64_t(1) << 31) && k < (int64_t(1) << 31);
+  return m > 0 && n > 0 && k > 0 && m * n < (int64_t(1) << 31) && mcfg::oz::kgeo(k).nkc <= mcfg::oz::kMaxChunks;
 }
 
 // one-call MC(nc=2, binary32) x T / MC(nc=2) product on the INT8 tensor cores
