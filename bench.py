@@ -375,7 +375,7 @@ def run_ours(args):
 
     digits = lib.mcf_fast_tc_digits()
     kp = (K + 15) // 16 * 16
-    gemm_equiv = digits * (digits + 1) // 2
+    gemm_equiv = lib.mcf_fast_tc_gemm_equivalents(1)
     int8_ops = 2.0 * rows * N * kp * gemm_equiv
     phases = []
     fb = C.c_int64(0)
@@ -469,7 +469,8 @@ def run_ours(args):
                          "unit": "TOPS (int8)", "frac": round(achieved / peak_i8, 3),
                          "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
                          "traffic_source": traffic_src,
-                         "kernel": "int8 digit GEMMs (cuBLASLt IMMA, s8 x s8 -> s32), %d per step" % digits,
+                         "kernel": "int8 digit GEMMs (cuBLASLt IMMA, s8 x s8 -> s32), %d per step, %d GEMM-equivalents"
+                                   % (digits, gemm_equiv),
                          "algorithmic_int8_ops_per_step": int8_ops,
                          "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (B200 dense INT8 = 2x dense BF16)",
                          "step_phases_ms": {"b_digits": round(med[0], 3), "a_digits": round(med[1], 3),

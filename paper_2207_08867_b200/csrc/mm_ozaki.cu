@@ -50,7 +50,8 @@ namespace mcfg {
 namespace oz {
 namespace {
 
-constexpr int kS = 9;                // digits per operand
+constexpr int kS = 9;                // digits of A (and of an MC B); diagonals kept: q < kS
+constexpr int kSB1 = 6;              // digits of a single-component (binary32) B
 constexpr int kSlab = 32;            // transpose tile of the column slicer
 constexpr int64_t kMaxChunk = 14400; // int32 headroom: kS * kc * 2^14 < 2^31
 constexpr int64_t kMaxChunks = 16;    // combine: 16 chunk sums x 2^16.01 x 2^31 < 2^53
@@ -78,7 +79,10 @@ __device__ __forceinline__ int limb_digits(int x, int* d, int cnt) {
 // (|H| <= 2^22, |M|, |L| <= 2^23, r1 = v 2^23 - H, r2 = r1 2^24 - M, all
 // |r| <= 1/2 (1 + tiny)), v = H 2^-23 + M 2^-47 + L 2^-71 + r3 2^-71; the
 // limbs are then cut into digits bottom-up with integer operations.
-__device__ __forceinline__ void digits(double hi, double lo, int (&d)[kS]) {
+// Returns true when v differs from its first six digits (digits 6..8 or the
+// final remainder nonzero): a binary32 B element within 2^24 of its column's
+// scale is exact in six.
+__device__ __forceinline__ bool digits(double hi, double lo, int (&d)[kS]) {
   const double h = __dmul_rn(hi, 0x1p23), hl = __dmul_rn(lo, 0x1p23);
   const double H = rint(h);
   double r1, r1l;
@@ -87,7 +91,8 @@ __device__ __forceinline__ void digits(double hi, double lo, int (&d)[kS]) {
   const double M = rint(m);
   double r2, r2l;
   dsum(__dsub_rn(m, M), ml, r2, r2l);
-  const double L = rint(__dmul_rn(r2, 0x1p24));
+  const double l24 = __dmul_rn(r2, 0x1p24);
+  const double L = rint(l24);
   int c = limb_digits(__double2int_rn(L), d + 6, 3);
   c = limb_digits(__double2int_rn(M) + c, d + 3, 3);
   // top limb: two balanced digits, the remainder (|.| <= 64) is d_0
@@ -99,6 +104,7 @@ __device__ __forceinline__ void digits(double hi, double lo, int (&d)[kS]) {
     x = (x - t) >> 8;
   }
   d[0] = x;
+  return (d[6] | d[7] | d[8]) != 0 || l24 != L || r2l != 0.0;
 }
 
 template <int NC>
@@ -118,7 +124,7 @@ __device__ __forceinline__ void load_pair(const float* p, double& hi, double& lo
 // planes is [chunk 0: kS planes of kc bytes][chunk 1: ...]
 struct KGeo {
   int64_t k, kc, nkc;
-  __host__ __device__ int64_t row_bytes() const { return kS * kc * nkc; }
+  __host__ __device__ int64_t row_bytes(int planes = kS) const { return planes * kc * nkc; }
 };
 
 // kc is a multiple of 32, so a 32-wide k tile never straddles two chunks
@@ -227,19 +233,20 @@ __global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a,
 // CTA tile 32 k x 32 j: lane = column (coalesced loads along n), each thread
 // four consecutive k packed into one 32-bit word per digit; shared rows
 // padded to 9 words so the lanes' stores hit distinct banks.
-template <int NC>
+template <int NC, int SB>
 __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b, int64_t n, int64_t ldb, KGeo g,
                                                      const int* __restrict__ e, int8_t* __restrict__ out,
-                                                     float* __restrict__ bt) {
-  __shared__ unsigned dg[kS][kSlab][kSlab / 4 + 1];  // [t][j][k / 4]
+                                                     float* __restrict__ bt, int* __restrict__ cinx) {
+  __shared__ unsigned dg[SB][kSlab][kSlab / 4 + 1];  // [t][j][k / 4]
   __shared__ float tv[kSlab][kSlab * NC + 1];        // [j][k * NC + c]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps x 4 k each
   const int64_t k0 = (int64_t)blockIdx.y * kSlab, j0 = (int64_t)blockIdx.x * kSlab;
   const int64_t j = j0 + tx;
   const double sc = j < n ? pow2d(-e[j]) : 1.0;
-  unsigned packed[kS];
+  unsigned packed[SB];
+  int inexact = 0;
 #pragma unroll
-  for (int t = 0; t < kS; ++t) packed[t] = 0u;
+  for (int t = 0; t < SB; ++t) packed[t] = 0u;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int kk = ty * 4 + u;
@@ -251,33 +258,33 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
       for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * ldb + j) * NC + c];
       if (isfinite(mag)) {
         int d[kS];
-        digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
+        const bool tail = digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
+        if (SB < kS && tail) ++inexact;
 #pragma unroll
-        for (int t = 0; t < kS; ++t) packed[t] |= ((unsigned)(d[t] & 0xff)) << (8 * u);
+        for (int t = 0; t < SB; ++t) packed[t] |= ((unsigned)(d[t] & 0xff)) << (8 * u);
       }
     }
   }
+  if (SB < kS && inexact) atomicAdd(cinx + j, inexact);
 #pragma unroll
-  for (int t = 0; t < kS; ++t) dg[t][tx][ty] = packed[t];
+  for (int t = 0; t < SB; ++t) dg[t][tx][ty] = packed[t];
   __syncthreads();
-  // digit rows: kS * 32 rows (t, jj) of 32 bytes; 8 threads x 4 bytes per
-  // row.  The tile's 32 k lie in one chunk (kc is a multiple of 32).
+  // digit rows: SB * 32 rows (t, jj) of 32 bytes, 8 threads x 4 bytes per
+  // row: thread (jj = tid / 8, part = tid % 8) writes plane t = r in round r.
+  // The tile's 32 k lie in one chunk (kc is a multiple of 32).
   const int kc = (int)g.kc, c = (int)(k0 / kc), kk0 = (int)(k0 - (int64_t)c * kc);
-  const int64_t rb = g.row_bytes();
-  int8_t* base = out + (int64_t)c * kS * kc + kk0;
-  for (int w = threadIdx.x; w < kS * kSlab * 8; w += blockDim.x) {
-    const int row = w >> 3, part = w & 7;
-    const int t = row / kSlab, jj = row % kSlab;
-    const int64_t gj = j0 + jj;
-    if (gj >= n) continue;
-    *reinterpret_cast<unsigned*>(base + gj * rb + (kS - 1 - t) * kc + part * 4) = dg[t][jj][part];
+  const int jj = threadIdx.x >> 3, part = threadIdx.x & 7;
+  const int64_t gj = j0 + jj;
+  if (gj < n) {
+    int8_t* dst = out + gj * g.row_bytes(SB) + (int64_t)c * SB * kc + kk0 + part * 4;
+#pragma unroll
+    for (int t = 0; t < SB; ++t) *reinterpret_cast<unsigned*>(dst + (SB - 1 - t) * kc) = dg[t][jj][part];
   }
-  // transposed binary32 copy
+  // transposed binary32 copy: thread (jj = tid / 8 + 32 r / ..., k) rows of 32 NC floats
   for (int w = threadIdx.x; w < kSlab * kSlab * NC; w += blockDim.x) {
-    const int jj = w / (kSlab * NC), rest = w % (kSlab * NC);
-    const int kk = rest / NC;
-    const int64_t gj = j0 + jj, gk = k0 + kk;
-    if (gj < n && gk < g.k) bt[(gj * g.k + gk) * NC + rest % NC] = tv[jj][rest];
+    const int wj = w / (kSlab * NC), rest = w - wj * (kSlab * NC);
+    const int64_t gj2 = j0 + wj, gk = k0 + rest / NC;
+    if (gj2 < n && gk < g.k) bt[(gj2 * g.k + gk) * NC + rest % NC] = tv[wj][rest];
   }
 }
 
@@ -291,7 +298,8 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
 __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
                                                  int nkc, const int* __restrict__ ea, const int* __restrict__ eb,
                                                  const int* __restrict__ rnf, const int* __restrict__ cnf,
-                                                 double thr, float* __restrict__ out, int64_t ldo,
+                                                 const int* __restrict__ cinx, double thr, double thr_inexact,
+                                                 float* __restrict__ out, int64_t ldo,
                                                  int* __restrict__ rlist, int* __restrict__ rcnt) {
   static_assert(kS == 9, "three groups of three diagonals");
   // four consecutive columns per thread: 16-byte loads from each plane (ldc
@@ -300,10 +308,14 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
   if (j0 >= n) return;
   const int64_t plane = m * ldc;
   int fj[4], nfj[4];
+  double thj[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     fj[u] = j0 + u < n ? eb[j0 + u] : 0;
     nfj[u] = j0 + u < n ? cnf[j0 + u] : 0;
+    // columns with elements not exact in their digits: their truncation adds
+    // at most 2^-48 (1.01) x 1/2 per such element to every output
+    thj[u] = thr + (cinx && j0 + u < n ? thr_inexact * cinx[j0 + u] : 0.0);
   }
   for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
     const int64_t off = i * ldc + j0;
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
       dsum(__dmul_rn(g[0], 0x1p-30), hi, s2, e2);
       e2 = __dadd_rn(e2, lo);
       dsum(s2, e2, s2, e2);
-      if (fi | nfj[u] || !(fabs(s2) >= thr)) {
+      if (fi | nfj[u] || !(fabs(s2) >= thj[u])) {
         rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
         continue;
       }
@@ -562,23 +574,29 @@ struct PreparedB {
   const float* bt = nullptr;
   const int* eb = nullptr;
   const int* cnf = nullptr;
+  const int* cinx = nullptr;  // per column: elements not exact in sb digits (sb < kS)
   KGeo g{};
   int64_t n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
-  int ncb = 1;
+  int ncb = 1, sb = kS;
 };
+
+// digits kept for B: six for binary32 columns (exact for elements within
+// 2^24 of the column scale; the others are counted), nine for MC columns
+int b_digits(int ncb) { return ncb == 1 ? kSB1 : kS; }
 
 std::size_t b_bytes(int64_t k, int64_t n, int ncb) {
   const KGeo g = kgeo(k);
-  return al(pad16(n) * g.row_bytes()) + al(n * k * ncb * 4) + al(n * 4) * 2 + al(n * 8);
+  return al(pad16(n) * g.row_bytes(b_digits(ncb))) + al(n * k * ncb * 4) + al(n * 4) * 3 + al(n * 8);
 }
 
 mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb, char* buf, PreparedB& pb,
                      cudaStream_t s) {
   const KGeo g = kgeo(k);
-  const int64_t np = pad16(n);
+  const int sb = b_digits(ncb);
+  const int64_t np = pad16(n), rbb = g.row_bytes(sb);
   int8_t* planes = reinterpret_cast<int8_t*>(buf);
-  buf += al(np * g.row_bytes());
-  if (np > n && cudaMemsetAsync(planes + n * g.row_bytes(), 0, (np - n) * g.row_bytes(), s) != cudaSuccess)
+  buf += al(np * rbb);
+  if (np > n && cudaMemsetAsync(planes + n * rbb, 0, (np - n) * rbb, s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the padding columns");
   float* bt = reinterpret_cast<float*>(buf);
   buf += al(n * k * ncb * 4);
@@ -586,18 +604,21 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   buf += al(n * 4);
   int* cnf = reinterpret_cast<int*>(buf);
   buf += al(n * 4);
+  int* cinx = reinterpret_cast<int*>(buf);
+  buf += al(n * 4);
   unsigned long long* cm = reinterpret_cast<unsigned long long*>(buf);
-  if (cudaMemsetAsync(cnf, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cm, 0, n * 8, s) != cudaSuccess)
+  if (cudaMemsetAsync(cnf, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cm, 0, n * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(cinx, 0, n * 4, s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the column maxima");
   const dim3 gm((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
   if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
   else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
   k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, eb);
   const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)((g.kc * g.nkc + kSlab - 1) / kSlab));
-  if (ncb == 2) k_slice_cols<2><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt);
-  else k_slice_cols<1><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt);
+  if (ncb == 2) k_slice_cols<2, kS><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt, cinx);
+  else k_slice_cols<1, kSB1><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt, cinx);
   for (int i = 0; i < 3; ++i) mcfr::note_launch();
-  pb = PreparedB{planes, bt, eb, cnf, g, n, np, ncb};
+  pb = PreparedB{planes, bt, eb, cnf, sb < kS ? cinx : nullptr, g, n, np, ncb, sb};
   return mcfr::check_launch("mm_fast B digit kernels");
 }
 
@@ -638,25 +659,33 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   mcfr::note_launch();
   mcf_status st = mcfr::check_launch("mm_fast A digit kernels");
   if (st != MCF_OK) return st;
-  // chunk c, diagonal q: A planes 0..q of the chunk (its first (q+1) kc
-  // bytes) against B planes q..0 (the chunk's last (q+1) kc bytes); C_cq is
-  // an np x m column-major = m x np row-major int32 matrix
+  // chunk c, diagonal q: the pairs (s, t = q - s) with t <= sb - 1.  A planes
+  // q - th .. q of the chunk (contiguous, ascending s) against B planes th ..
+  // 0 (stored in reverse order, so also contiguous); C_cq is an np x m
+  // column-major = m x np row-major int32 matrix
   if (ev) cudaEventRecord(ev[1], s);
-  const int64_t ld = g.row_bytes();
+  const int sb = pb.sb;
+  const int64_t lda = g.row_bytes(), ldb = g.row_bytes(sb);
   for (int64_t c = 0; c < g.nkc; ++c)
     for (int q = 0; q < kS; ++q) {
-      const int64_t base = c * kS * g.kc;
-      st = gemm_s8(pb.planes + base + (int64_t)(kS - 1 - q) * g.kc, ld, planes + base, ld,
-                   cq + (c * kS + q) * m * np, np, m, (int64_t)(q + 1) * g.kc, s);
+      const int th = q < sb - 1 ? q : sb - 1;
+      st = gemm_s8(pb.planes + c * sb * g.kc + (int64_t)(sb - 1 - th) * g.kc, ldb,
+                   planes + c * kS * g.kc + (int64_t)(q - th) * g.kc, lda, cq + (c * kS + q) * m * np, np, m,
+                   (int64_t)(th + 1) * g.kc, s);
       if (st != MCF_OK) return st;
     }
   if (ev) cudaEventRecord(ev[2], s);
-  // fallback threshold (scaled units): 2^50 K 2^-68.8, so every combined
-  // output has relative error <= 2^-50 before the split
-  const double thr = ldexp((double)k * 1.15, 50 - 69);
+  // fallback threshold (scaled units): 2^50 x the error bound per output.
+  // Per product: A's truncation 2^-73, B's 2^-73 (nine digits; zero for the
+  // exact elements of a six-digit B), the dropped pairs s + t >= 9:
+  // 8.03 2^-72 (nine B digits) or 5.02 2^-72 (six).  Inexact B elements add
+  // 2^-48 (1.01) / 2 to every output of their column (thr_inexact each).
+  const double per_prod = sb == kS ? 9.03 : 5.52;
+  const double thr = ldexp((double)k * per_prod, 50 - 72);
+  const double thr_inexact = ldexp(0.505, 50 - 48);
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
-  k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, ea, pb.eb, rnf, pb.cnf, thr,
+  k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, ea, pb.eb, rnf, pb.cnf, pb.cinx, thr, thr_inexact,
                                                           out, ldo, rlist, rcnt);
   mcfr::note_launch();
   if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
@@ -681,15 +710,53 @@ mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m,
                     cudaStream_t s) {
   using namespace mcfg::oz;
   const std::size_t bb = b_bytes(k, n, ncb);
-  char* ws = oz_workspace(bb + rows_bytes(m, k, n), s);
+  static const int halves_env = [] {
+    const char* e = getenv("MCF_OZ_SPLIT");  // tuning knob: row parts on parallel streams
+    return e ? atoi(e) : 1;  // measured: 2 parts gain 0.5% at config 2
+  }();
+  const int parts = m >= 2048 ? std::max(1, std::min(halves_env, 4)) : 1;
+  const int64_t rp = (m + parts - 1) / parts;
+  const std::size_t rb = rows_bytes(rp, k, n);
+  char* ws = oz_workspace(bb + parts * al(rb), s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
   PreparedB pb;
   mcf_status st = prepare_b(w, ncb, k, n, n, ws, pb, s);
-  if (st != MCF_OK) return st;
-  return rows(x, nca, m, pb, out, n, ws + bb, s);
+  if (st != MCF_OK || parts == 1) return st != MCF_OK ? st : rows(x, nca, m, pb, out, n, ws + bb, s);
+  // row parts on the caller's stream and side streams (forked and joined by
+  // events): one part's recombination / fallback overlaps the next part's
+  // GEMMs, whose last wave leaves SMs idle
+  cudaEvent_t fork = nullptr, join[4] = {};
+  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+  cudaEventRecord(fork, s);
+  for (int p = 0; p < parts && st == MCF_OK; ++p) {
+    const int64_t r0 = p * rp, rows_p = std::min<int64_t>(rp, m - r0);
+    cudaStream_t ps = p == 0 ? s : side_stream(8 + p);
+    if (p > 0) cudaStreamWaitEvent(ps, fork, 0);
+    st = rows(x + r0 * k * nca, nca, rows_p, pb, out + r0 * n * 2, n, ws + bb + p * al(rb), ps);
+    if (p > 0) {
+      cudaEventCreateWithFlags(&join[p], cudaEventDisableTiming);
+      cudaEventRecord(join[p], ps);
+    }
+  }
+  for (int p = 1; p < parts; ++p)
+    if (join[p]) {
+      cudaStreamWaitEvent(s, join[p], 0);
+      cudaEventDestroy(join[p]);
+    }
+  cudaEventDestroy(fork);
+  return st;
 }
 
 int ozaki_digits() { return mcfg::oz::kS; }
+
+// int8 GEMM-equivalents (M x N x K each) per product: pairs (s, t) with
+// s + t < kS, s < kS, t < b_digits
+int ozaki_gemm_equivalents(int ncb) {
+  using namespace mcfg::oz;
+  int c = 0;
+  for (int q = 0; q < kS; ++q) c += std::min(q, b_digits(ncb) - 1) + 1;
+  return c;
+}
 
 // one product with phase timing: ms[0] B digits, ms[1] A digits, ms[2] the
 // int8 GEMMs, ms[3] recombination + fallback; *fallback = listed outputs
