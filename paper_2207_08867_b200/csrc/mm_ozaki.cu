@@ -319,36 +319,39 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
   }
   for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
     const int64_t off = i * ldc + j0;
-    long long sq[kS][4];
+    // per group of three diagonals: load (summing K chunks), fold into one
+    // exact integer per column, convert -- few live registers, so many rows
+    // of loads stay in flight
+    double g[3][4];
 #pragma unroll
-    for (int q = 0; q < kS; ++q) {
-      const int4 v = *reinterpret_cast<const int4*>(cq + q * plane + off);
-      sq[q][0] = v.x;
-      sq[q][1] = v.y;
-      sq[q][2] = v.z;
-      sq[q][3] = v.w;
-    }
-    for (int c = 1; c < nkc; ++c)
+    for (int w = 0; w < 3; ++w) {
+      long long gv[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int q = 0; q < kS; ++q) {
-        const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * kS + q) * plane + off);
-        sq[q][0] += v.x;
-        sq[q][1] += v.y;
-        sq[q][2] += v.z;
-        sq[q][3] += v.w;
+      for (int r = 0; r < 3; ++r) {
+        const int q = 3 * w + r;
+        const int4 v0 = *reinterpret_cast<const int4*>(cq + q * plane + off);
+        long long t[4] = {v0.x, v0.y, v0.z, v0.w};
+        for (int c = 1; c < nkc; ++c) {
+          const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * kS + q) * plane + off);
+          t[0] += v.x;
+          t[1] += v.y;
+          t[2] += v.z;
+          t[3] += v.w;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gv[u] = gv[u] * 256 + t[u];
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) g[w][u] = (double)gv[u];
+    }
     const int ei = ea[i], fi = rnf[i] & 1;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u;
       if (j >= n) break;
-      double g[3];
-#pragma unroll
-      for (int w = 0; w < 3; ++w)
-        g[w] = (double)(sq[3 * w][u] * 65536 + sq[3 * w + 1][u] * 256 + sq[3 * w + 2][u]);
       double hi, lo, s2, e2;
-      dsum(__dmul_rn(g[1], 0x1p-54), __dmul_rn(g[2], 0x1p-78), hi, lo);
-      dsum(__dmul_rn(g[0], 0x1p-30), hi, s2, e2);
+      dsum(__dmul_rn(g[1][u], 0x1p-54), __dmul_rn(g[2][u], 0x1p-78), hi, lo);
+      dsum(__dmul_rn(g[0][u], 0x1p-30), hi, s2, e2);
       e2 = __dadd_rn(e2, lo);
       dsum(s2, e2, s2, e2);
       if (fi | nfj[u] || !(fabs(s2) >= thj[u])) {
@@ -381,7 +384,25 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const float* ag = a + i * k * NCA;
   if constexpr (SMEM) {
-    for (int64_t t = threadIdx.x; t < k * NCA; t += blockDim.x) arow[t] = ag[t];
+    // 16-byte loads, eight in flight per thread before the stores
+    const int64_t nf = k * NCA;
+    if ((reinterpret_cast<uintptr_t>(ag) & 15) == 0) {
+      const int64_t n4 = nf / 4;
+      const float4* a4 = reinterpret_cast<const float4*>(ag);
+      float4* s4 = reinterpret_cast<float4*>(arow);
+      for (int64_t t0 = threadIdx.x; t0 < n4; t0 += 8 * blockDim.x) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t0 + u * blockDim.x < n4) v[u] = __ldg(a4 + t0 + u * blockDim.x);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t0 + u * blockDim.x < n4) s4[t0 + u * blockDim.x] = v[u];
+      }
+      for (int64_t t = n4 * 4 + threadIdx.x; t < nf; t += blockDim.x) arow[t] = ag[t];
+    } else {
+      for (int64_t t = threadIdx.x; t < nf; t += blockDim.x) arow[t] = ag[t];
+    }
     __syncthreads();
   }
   const float* ar = SMEM ? arow : ag;
