@@ -112,6 +112,17 @@ __global__ void __launch_bounds__(256) k_seqsum(const float* __restrict__ terms,
 // into registers while the current one is consumed.
 constexpr int GT = 256;
 
+// (a b0, a b1), each product rounded to binary32 (mul.rn.f32x2 on sm_100a;
+// ptxas issues FMUL2 with the scalar a as a broadcast operand).  The result
+// feeds separate FADDs: no contraction into FFMA2 is possible there.
+__device__ __forceinline__ void mul2_bcast(float a, float b0, float b1, float& p0, float& p1) {
+  unsigned long long ap, bp, pp;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(a), "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bp) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(pp) : "l"(ap), "l"(bp));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(pp));
+}
+
 // row (col) of the tile owned by fragment index u of thread t (T per thread):
 // T == 1 -> t; else two halves of T/2, at t*T/2 and B/2 + t*T/2
 template <int T, int B>
@@ -173,10 +184,26 @@ __global__ void __launch_bounds__(GT) k_gemm(const float* __restrict__ a, int64_
     for (int u = 0; u < TM; ++u) av[u] = As[buf][kk][frag_pos<TM, BM>(ty, u)];
 #pragma unroll
     for (int v = 0; v < TN; ++v) bv[v] = Bs[buf][kk][frag_pos<TN, BN>(tx, v)];
+    if constexpr (TN % 2 == 0) {
+      // packed products: one FMUL2 (scalar a broadcast against a pair of b)
+      // per two multiply-adds, then the two ordered FADDs -- the roundings
+      // are the scalar ones (fl_mul then fl_add), three instructions
+      // instead of four
 #pragma unroll
-    for (int u = 0; u < TM; ++u)
+      for (int u = 0; u < TM; ++u)
 #pragma unroll
-      for (int v = 0; v < TN; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+        for (int v = 0; v < TN; v += 2) {
+          float p0, p1;
+          mul2_bcast(av[u], bv[v], bv[v + 1], p0, p1);
+          acc[u][v] = __fadd_rn(acc[u][v], p0);
+          acc[u][v + 1] = __fadd_rn(acc[u][v + 1], p1);
+        }
+    } else {
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(av[u], bv[v]));
+    }
   };
   fetch(0);
   stash(0);
