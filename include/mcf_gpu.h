@@ -188,6 +188,13 @@ mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_
 /* out[r] = sum_j g[r, j] in order (bias gradient, autodiff.hpp:287-292) */
 mcf_status mcf_rowsum_f32_ordered(const float* g, int64_t rows, int64_t n, float* out,
                                   mcf_stream stream);
+/* Plan MCF_FAST versions of the two above (the reference-order plan needs
+ * neither): FP32 GEMM in cuBLAS order (no TF32) with the same operands and
+ * optional ReLU mask, and a tree-ordered row sum. */
+mcf_status mcf_gemm_f32_fast(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb,
+                             float* c, int64_t ldc, int64_t m, int64_t n, int64_t k, const float* relu_mask,
+                             mcf_stream stream);
+mcf_status mcf_rowsum_f32_fast(const float* g, int64_t rows, int64_t n, float* out, mcf_stream stream);
 /* MC-SGD, momentum 0: w <- grow_expn(w, -lr * g) in place
  * [replaces optim.hpp:54-77 + mc_ops.hpp:509-513] */
 mcf_status mcf_sgd_grow(float* w, int nc, const float* g, int64_t numel, float lr, mcf_stream stream);

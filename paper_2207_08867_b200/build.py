@@ -33,7 +33,8 @@ NVFLAGS = ARCH + [
 CXXFLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-I" + os.path.join(CUDA, "include"),
             "-I" + os.path.join(ROOT, "include")]
 
-CU_SOURCES = ["elementwise.cu", "linalg.cu", "mm_fast.cu", "mm_ozaki.cu", "stream_fast.cu", "mlp.cu", "hostapi.cu"]
+CU_SOURCES = ["elementwise.cu", "linalg.cu", "mm_fast.cu", "mm_ozaki.cu", "stream_fast.cu", "mlp.cu", "mlp_fast.cu",
+              "hostapi.cu"]
 CXX_SOURCES = ["runtime.cpp"]
 
 
@@ -79,7 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for (_, log), s in zip(results, srcs):
             if log.strip():
                 print(f"--- {s}\n{log}", file=sys.stderr)
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lquadmath", "-lcudart", "-lcublasLt",
+    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lquadmath", "-lcudart", "-lcublasLt", "-lcublas",
                                                      "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -480,8 +480,10 @@ int mm_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) {
 mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
                        int64_t k, int64_t n, int w_batched, void* out, cudaStream_t s, bool tc) {
   using namespace mcfg;
-  if (tc && p == MCF_B32 && nc == 2 && ozaki_supported(m, k, n)) {
-    // INT8 tensor-core path (mm_ozaki.cu), one product per batch entry
+  // INT8 tensor-core path (mm_ozaki.cu), one product per batch entry.  Short
+  // A (m < 64, e.g. an MLP's 10-class layer) stays on the FP64 pipe: the int8
+  // GEMMs degenerate to GEMV kernels there (measured 0.68 ms vs 0.09 ms).
+  if (tc && p == MCF_B32 && nc == 2 && m >= 64 && ozaki_supported(m, k, n)) {
     const float* xf = static_cast<const float*>(x);
     const float* wf = static_cast<const float*>(w);
     float* of = static_cast<float*>(out);

@@ -11,16 +11,18 @@ training step is a fixed sequence of C-ABI calls on feature-major activations
             order), h = approx(add_mcn(Z, b)), A = relu(h)   (mcf_mlp_bias_act)
   loss      mcf_mlp_cross_entropy (terms, gradient / N_global, ordered sum)
   backward  dW = G A_prev^T, dA = approx(W)^T G masked by h_prev > 0,
-            db = row sums of G  (ordered binary32: mcf_gemm_f32_ordered,
-            mcf_rowsum_f32_ordered -- matmul2d semantics)
+            db = row sums of G  (reference-order plan: ordered binary32,
+            mcf_gemm_f32_ordered / mcf_rowsum_f32_ordered -- matmul2d
+            semantics; plan FAST: mcf_gemm_f32_fast / mcf_rowsum_f32_fast)
   exchange  data parallel: one flat binary32 gradient buffer, all_reduce(sum)
             over the process group (NCCL over NVLink on GPUs)
   update    mcf_sgd_grow: w <- grow_expn(w, -lr * g), identical on every rank
 
 Single process with the reference-order plan, every step is bit-identical to
 the reference's own training loop (tests/test_gpu_mlp.py); with plan FAST the
-forward products carry the compensated binary64 accumulation and the loss
-trajectory stays within the reference's rounding spread.
+forward MC products run on the INT8 tensor-core splitting (the FP64 pipe for
+short layers), the backward on FP32 library GEMMs, and the loss trajectory
+stays within the reference's rounding spread.
 """
 from __future__ import annotations
 
@@ -29,7 +31,7 @@ import ctypes as C
 import numpy as np
 import torch
 
-from . import B32, FAST, SEQUENTIAL, _check, lib
+from . import B32, FAST, FAST_FP64, SEQUENTIAL, _check, lib
 from . import data as _data
 
 
@@ -141,21 +143,24 @@ class MCMLP:
         # loss + dL/dlogits
         _check(lib_.mcf_mlp_cross_entropy(B["H"][L - 1].data_ptr(), labels.data_ptr(), self.dims[-1], n, n_global,
                                           B["G"][L - 1].data_ptr(), B["terms"].data_ptr(), B["loss"].data_ptr(), s))
-        # backward
+        # backward: the reference-order plan reproduces matmul2d's rounding
+        # sequence; plan FAST uses FP32 library GEMMs and tree row sums
+        fast = self.plan in (FAST, FAST_FP64)
+        gemm = lib_.mcf_gemm_f32_fast if fast else lib_.mcf_gemm_f32_ordered
+        rowsum = lib_.mcf_rowsum_f32_fast if fast else lib_.mcf_rowsum_f32_ordered
         gv = self.grads.views
         for l in range(L - 1, -1, -1):
             out_dim, in_dim = self.dims[l + 1], self.dims[l]
             G = B["G"][l]
             # dW (out x in) = G (out x n) . A_prev^T  (A_prev is in x n)
-            _check(lib_.mcf_gemm_f32_ordered(0, 1, G.data_ptr(), n, acts[l].data_ptr(), n, gv[2 * l].data_ptr(),
-                                             in_dim, out_dim, in_dim, n, None, s))
-            _check(lib_.mcf_rowsum_f32_ordered(G.data_ptr(), out_dim, n, gv[2 * l + 1].data_ptr(), s))
+            _check(gemm(0, 1, G.data_ptr(), n, acts[l].data_ptr(), n, gv[2 * l].data_ptr(), in_dim, out_dim, in_dim, n,
+                        None, s))
+            _check(rowsum(G.data_ptr(), out_dim, n, gv[2 * l + 1].data_ptr(), s))
             if l > 0:
                 _check(lib_.mcf_approx(B32, self.W[l].data_ptr(), nc, B["Wa"][l].data_ptr(), out_dim * in_dim, s))
                 # dA_prev (in x n) = approx(W)^T (in x out) . G (out x n), ReLU mask = H_{l-1}
-                _check(lib_.mcf_gemm_f32_ordered(1, 0, B["Wa"][l].data_ptr(), in_dim, G.data_ptr(), n,
-                                                 B["G"][l - 1].data_ptr(), n, in_dim, n, out_dim,
-                                                 B["H"][l - 1].data_ptr(), s))
+                _check(gemm(1, 0, B["Wa"][l].data_ptr(), in_dim, G.data_ptr(), n, B["G"][l - 1].data_ptr(), n, in_dim,
+                            n, out_dim, B["H"][l - 1].data_ptr(), s))
         self.grads.all_reduce(B["loss"])
         for l in range(L):
             _check(lib_.mcf_sgd_grow(self.W[l].data_ptr(), nc, gv[2 * l].data_ptr(), self.W[l].numel() // nc,

@@ -168,3 +168,34 @@ def test_loss_sum_is_left_to_right_over_slabs():
     for v in t:
         acc = np.float32(acc + v)
     assert_bits(tsum.cpu().numpy(), np.array([acc], np.float32), "loss sum")
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0)])
+def test_fast_plan_backward_gemm_and_rowsum(ta, tb):
+    """Plan FAST's backward pieces (FP32 library GEMM + ReLU mask, tree row
+    sums) against a binary64 reference: binary32-level relative error."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(9 + ta)
+    m, n, k = 300, 500, 700
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    mask = rng.standard_normal((m, n)).astype(np.float32)
+    want = np.where(mask > 0, A.astype(np.float64) @ B.astype(np.float64), 0.0)
+    a_st = np.ascontiguousarray(A.T if ta else A)
+    b_st = np.ascontiguousarray(B.T if tb else B)
+    da, db, dm = (torch.from_numpy(v).cuda() for v in (a_st, b_st, mask))
+    dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_gemm_f32_fast(ta, tb, da.data_ptr(), a_st.shape[1], db.data_ptr(), b_st.shape[1], dc.data_ptr(),
+                                 n, m, n, k, dm.data_ptr(), None) == 0, lib.mcf_last_error()
+    out = torch.empty(m, dtype=torch.float32, device="cuda")
+    assert lib.mcf_rowsum_f32_fast(dc.data_ptr(), m, n, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    got = dc.cpu().numpy().astype(np.float64)
+    scale = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64))
+    assert np.all(np.abs(got - want) <= 1e-5 * scale), "gemm_f32_fast"
+    rs = got.sum(axis=1)
+    assert np.allclose(out.cpu().numpy(), rs, rtol=1e-5, atol=1e-5 * np.abs(got).sum(axis=1).max()), "rowsum"
