@@ -298,11 +298,16 @@ def other_configs(torch, mcf, hbm_gbs, f64_peak):
         a, b = split(va), split(vb)
         del va, vb
         ms = _dev_time(torch, lambda: mcf.mm_mcmc(a, b, plan=mcf.FAST), reps)
-        ops = mcf.lib().mcf_fast_ops_per_mad(1, mcf.B32 if nc == 2 else mcf.B16, nc)
-        res[f"config4_mcmc_{tag}"] = {"M=N=K": N4, "ms": round(ms, 2),
-                                       "GFLOP/s_eff": round(2 * N4 ** 3 / ms / 1e6, 1),
-                                       "fp64_ops_per_mad": ops,
-                                       "frac_fp64_peak": round(ops * N4 ** 3 / (ms * 1e-3) / 1e12 / f64_peak, 3)}
+        entry = {"M=N=K": N4, "ms": round(ms, 2), "GFLOP/s_eff": round(2 * N4 ** 3 / ms / 1e6, 1)}
+        if nc == 2:  # binary32 nc=2: int8 tensor-core splitting of both operands
+            ge = mcf.lib().mcf_fast_tc_gemm_equivalents(2)
+            entry.update({"path": "int8 tensor cores", "int8_gemm_equivalents": ge,
+                          "int8_TOPS_step": round(2 * N4 ** 3 * ge / (ms * 1e-3) / 1e12, 1)})
+        else:  # binary16 nc=3: pre-summed operands, one FMA per MAD on the FP64 pipe
+            ops = mcf.lib().mcf_fast_ops_per_mad(1, mcf.B16, nc)
+            entry.update({"path": "fp64 pipe", "fp64_ops_per_mad": ops,
+                          "frac_fp64_peak": round(ops * N4 ** 3 / (ms * 1e-3) / 1e12 / f64_peak, 3)})
+        res[f"config4_mcmc_{tag}"] = entry
         del a, b
         torch.cuda.empty_cache()
     return res
@@ -451,7 +456,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         ew = elementwise_suite(torch, mcf, hbm)
         if not args.no_extras:
-            others = other_configs(torch, mcf, hbm, peak64)
+            others = other_configs(torch, mcf, hbm, f64.value / 1e12)
         gf, t, nrows, kind = reference_sample(a_h, b_h, cpu_threads())
         cpu = {"value": round(gf, 4), "unit": UNIT, "cores": cpu_threads(), "kind": kind,
                "sample": f"{nrows} full output rows of the 4096^3 product, one row per host thread ({t:.1f} s)"}
