@@ -300,7 +300,7 @@ def other_configs(torch, mcf, hbm_gbs, f64_peak):
         ms = _dev_time(torch, lambda: mcf.mm_mcmc(a, b, plan=mcf.FAST), reps)
         entry = {"M=N=K": N4, "ms": round(ms, 2), "GFLOP/s_eff": round(2 * N4 ** 3 / ms / 1e6, 1)}
         if nc == 2:  # binary32 nc=2: int8 tensor-core splitting of both operands
-            ge = mcf.lib().mcf_fast_tc_gemm_equivalents(2)
+            ge = mcf.lib().mcf_fast_tc_gemm_equivalents(2, N4)
             entry.update({"path": "int8 tensor cores", "int8_gemm_equivalents": ge,
                           "int8_TOPS_step": round(2 * N4 ** 3 * ge / (ms * 1e-3) / 1e12, 1)})
         else:  # binary16 nc=3: pre-summed operands, one FMA per MAD on the FP64 pipe
@@ -380,7 +380,7 @@ def run_ours(args):
 
     digits = lib.mcf_fast_tc_digits()
     kp = (K + 15) // 16 * 16
-    gemm_equiv = lib.mcf_fast_tc_gemm_equivalents(1)
+    gemm_equiv = lib.mcf_fast_tc_gemm_equivalents(1, K)
     int8_ops = 2.0 * rows * N * kp * gemm_equiv
     phases = []
     fb = C.c_int64(0)

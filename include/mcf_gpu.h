@@ -152,9 +152,10 @@ mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
                         int64_t k, void* out, int strategy, mcf_stream stream);
 /* Digits of the MC operand in the MCF_FAST tensor-core splitting (mm_ozaki.cu). */
 int mcf_fast_tc_digits(void);
-/* int8 GEMM-equivalents (M x N x K each) of one tensor-core product whose
- * second operand has b_components components per element (1: Tensor, 2: MC). */
-int mcf_fast_tc_gemm_equivalents(int b_components);
+/* int8 GEMM-equivalents (M x N x K each) of one tensor-core product of
+ * depth k whose second operand has b_components components per element
+ * (1: Tensor, 2: MC). */
+int mcf_fast_tc_gemm_equivalents(int b_components, int64_t k);
 /* Instrumentation: one MC(nc=2, binary32) x T product on the tensor-core
  * path with per-phase device times (phase_ms[4]: B digits, A digits, int8
  * GEMMs, recombination + fallback) and the number of outputs recomputed by

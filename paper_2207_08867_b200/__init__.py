@@ -68,7 +68,7 @@ _SIGS = {
     "mcf_h_mm_mcmc": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _int],
     "mcf_fast_ops_per_mad": [_int, _int, _int],
     "mcf_fast_tc_digits": [],
-    "mcf_fast_tc_gemm_equivalents": [_int],
+    "mcf_fast_tc_gemm_equivalents": [_int, _i64],
     "mcf_fast_mm_phases": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
     "mcf_probe_pipe_rates": [_p, _p],
     "mcf_mlp_bias_act": [_p, _int, _p, _i64, _i64, _int, _p, _p, _p],

@@ -408,7 +408,9 @@ int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) { return mcfr::mm_fast_op
 
 int mcf_fast_tc_digits(void) { return mcfr::ozaki_digits(); }
 
-int mcf_fast_tc_gemm_equivalents(int b_components) { return mcfr::ozaki_gemm_equivalents(b_components); }
+int mcf_fast_tc_gemm_equivalents(int b_components, int64_t k) {
+  return mcfr::ozaki_gemm_equivalents(b_components, k);
+}
 
 mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
                               double* phase_ms, int64_t* fallback_outputs, mcf_stream stream) {

@@ -50,7 +50,8 @@ namespace mcfg {
 namespace oz {
 namespace {
 
-constexpr int kS = 9;                // digits of A (and of an MC B); diagonals kept: q < kS
+constexpr int kS = 9;                // digits of A (and of an MC B)
+constexpr int kQmax = 10;            // diagonals kept: q < nq, nq = 9, or 10 for long K
 constexpr int kSB1 = 6;              // digits of a single-component (binary32) B
 constexpr int kSlab = 32;            // transpose tile of the column slicer
 constexpr int64_t kMaxChunk = 14400; // int32 headroom: kS * kc * 2^14 < 2^31
@@ -173,15 +174,17 @@ __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int
   if (j >= n) return;
   const int64_t t0 = (int64_t)blockIdx.y * 64, t1 = t0 + 64 < k ? t0 + 64 : k;
   double m = 0.0;
-  bool bad = false;
+  bool bad = false, split = false;
   for (int64_t t = t0; t < t1; ++t) {
     double hi, lo, mag;
     load_pair<NC>(b + (t * ldb + j) * NC, hi, lo, mag);
     bad |= !isfinite(mag);
+    split |= lo != 0.0;
     m = fmax(m, mag);
   }
   if (m > 0.0) atomicMax(cm + j, (unsigned long long)__double_as_longlong(m));
-  if (bad) nf[j] = 1;
+  // bit 0: a non-finite element; bit 1: some c0 + c1 is not one binary64
+  if (bad || split) atomicOr(nf + j, (bad ? 1 : 0) | (split ? 2 : 0));
 }
 
 __global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __restrict__ cm, int64_t n,
@@ -296,12 +299,13 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
 // exact in binary64), and the three groups (weights 2^-30, 2^-54, 2^-78) are
 // added exactly in double-double.  Grid: x covers a row, y (strided) rows.
 __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
-                                                 int nkc, const int* __restrict__ ea, const int* __restrict__ eb,
-                                                 const int* __restrict__ rnf, const int* __restrict__ cnf,
-                                                 const int* __restrict__ cinx, double thr, double thr_inexact,
+                                                 int nkc, int nq, const int* __restrict__ ea,
+                                                 const int* __restrict__ eb, const int* __restrict__ rnf,
+                                                 const int* __restrict__ cnf, const int* __restrict__ cinx,
+                                                 double thr, double thr_inexact,
                                                  float* __restrict__ out, int64_t ldo,
                                                  int* __restrict__ rlist, int* __restrict__ rcnt) {
-  static_assert(kS == 9, "three groups of three diagonals");
+  static_assert(kS == 9, "three groups of three diagonals (+ an optional tenth)");
   // four consecutive columns per thread: 16-byte loads from each plane (ldc
   // is a multiple of 16; padded columns hold zeros and are not written)
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     fj[u] = j0 + u < n ? eb[j0 + u] : 0;
-    nfj[u] = j0 + u < n ? cnf[j0 + u] : 0;
+    nfj[u] = j0 + u < n ? cnf[j0 + u] & 1 : 0;
     // columns with elements not exact in their digits: their truncation adds
     // at most 2^-48 (1.01) x 1/2 per such element to every output
     thj[u] = thr + (cinx && j0 + u < n ? thr_inexact * cinx[j0 + u] : 0.0);
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
         const int4 v0 = *reinterpret_cast<const int4*>(cq + q * plane + off);
         long long t[4] = {v0.x, v0.y, v0.z, v0.w};
         for (int c = 1; c < nkc; ++c) {
-          const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * kS + q) * plane + off);
+          const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * nq + q) * plane + off);
           t[0] += v.x;
           t[1] += v.y;
           t[2] += v.z;
@@ -344,13 +348,29 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
 #pragma unroll
       for (int u = 0; u < 4; ++u) g[w][u] = (double)gv[u];
     }
+    // the tenth diagonal (long K), weight 2^-86
+    double g9[4] = {0.0, 0.0, 0.0, 0.0};
+    if (nq > kS) {
+      long long t[4] = {0, 0, 0, 0};
+      for (int c = 0; c < nkc; ++c) {
+        const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * nq + kS) * plane + off);
+        t[0] += v.x;
+        t[1] += v.y;
+        t[2] += v.z;
+        t[3] += v.w;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) g9[u] = (double)t[u];
+    }
     const int ei = ea[i], fi = rnf[i] & 1;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u;
       if (j >= n) break;
-      double hi, lo, s2, e2;
-      dsum(__dmul_rn(g[1][u], 0x1p-54), __dmul_rn(g[2][u], 0x1p-78), hi, lo);
+      double hi, lo, h2, l2, s2, e2;
+      dsum(__dmul_rn(g[2][u], 0x1p-78), __dmul_rn(g9[u], 0x1p-86), h2, l2);
+      dsum(__dmul_rn(g[1][u], 0x1p-54), h2, hi, lo);
+      lo = __dadd_rn(lo, l2);
       dsum(__dmul_rn(g[0][u], 0x1p-30), hi, s2, e2);
       e2 = __dadd_rn(e2, lo);
       dsum(s2, e2, s2, e2);
@@ -376,7 +396,8 @@ template <int NCA, int NCB, bool SMEM>
 __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, const float* __restrict__ bt,
                                                   int64_t n, int64_t k, const int* __restrict__ rlist,
                                                   const int* __restrict__ rcnt, const int* __restrict__ rnf,
-                                                  float* __restrict__ out, int64_t ldo) {
+                                                  const int* __restrict__ cnf, float* __restrict__ out,
+                                                  int64_t ldo) {
   extern __shared__ __align__(16) float arow[];
   const int64_t i = blockIdx.x;
   const int cnt = rcnt[i];
@@ -408,11 +429,15 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
   const float* ar = SMEM ? arow : ag;
   // every c0 + c1 of the row one binary64 (and B single-component): one
   // two_prod per k instead of a two_sum per component product
-  const bool pair = NCA == 2 && NCB == 1 && !(rnf[i] & 2);
+  const bool rpair = NCA == 2 && !(rnf[i] & 2);
   constexpr int U = 8;
   for (int w = warp; w < cnt; w += nw) {
     const int64_t j = rlist[i * n + w];
     const float* br = bt + j * k * NCB;
+    // every c0 + c1 of the row (and of the column, for an MC B) one binary64:
+    // one two_prod per k (exact: <= 53 x 53 bits) instead of a two_sum per
+    // component product
+    const bool pair = rpair && (NCB == 1 || !(cnf[j] & 2));
     double S8[U], C8[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) S8[u] = C8[u] = 0.0;
@@ -428,7 +453,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
         if (t >= k) break;
         if (pair) {
           const double v = __dadd_rn((double)ar[t * 2], (double)ar[t * 2 + 1]);  // exact
-          const double bb = (double)bv[u][0];
+          const double bb = NCB == 1 ? (double)bv[u][0] : __dadd_rn((double)bv[u][0], (double)bv[u][NCB - 1]);
           const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);  // v b = p + pe exactly
           double e;
           dsum(S8[u], p, S8[u], e);
@@ -469,7 +494,8 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
 
 template <int NCA, int NCB>
 mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n, int64_t k, const int* rlist,
-                           const int* rcnt, const int* rnf, float* out, int64_t ldo, cudaStream_t s) {
+                           const int* rcnt, const int* rnf, const int* cnf, float* out, int64_t ldo,
+                           cudaStream_t s) {
   const std::size_t sm = (std::size_t)k * NCA * sizeof(float);
   constexpr std::size_t kMaxSmem = 200u << 10;
   if (sm <= kMaxSmem) {
@@ -478,9 +504,9 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
       cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
       attr = true;
     }
-    k_fallback<NCA, NCB, true><<<(unsigned)m, 256, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, out, ldo);
+    k_fallback<NCA, NCB, true><<<(unsigned)m, 256, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo);
   } else {
-    k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, out, ldo);
+    k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo);
   }
   mcfr::note_launch();
   return MCF_OK;
@@ -505,7 +531,7 @@ mcf_status lt_fail(const char* what, int code) {
 // A: kd x rows_c int8 col-major (ld lda), B: kd x cols_c int8 col-major (ld ldb).
 // MCF_ERR_UNSUPPORTED (no message) when cuBLASLt has no algorithm for the shape.
 mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int* C, int64_t rows_c,
-                   int64_t cols_c, int64_t kd, cudaStream_t s) {
+                   int64_t cols_c, int64_t kd, cudaStream_t s, int accumulate = 0) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_lt_mu);
@@ -552,7 +578,7 @@ mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
     }
     it = lt.algos.emplace(key, res.algo).first;
   }
-  const int32_t alpha = 1, beta = 0;
+  const int32_t alpha = 1, beta = accumulate ? 1 : 0;
   st = cublasLtMatmul(lt.h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &it->second, lt.ws, lt.ws_bytes, s);
   cleanup();
   if (st != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtMatmul", st);
@@ -643,9 +669,24 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   return mcfr::check_launch("mm_fast B digit kernels");
 }
 
+// diagonals kept: a tenth for long K, where the fallback's per-output cost
+// (K) times its share (~sqrt K) outgrows one more GEMM-equivalent set
+int diagonals(int64_t k) { return k > 8192 ? kQmax : kS; }
+
 std::size_t rows_bytes(int64_t m, int64_t k, int64_t n) {
   const KGeo g = kgeo(k);
-  return al(m * g.row_bytes()) + al((int64_t)kS * g.nkc * m * pad16(n) * 4) + al(m * n * 4) + al(m * 4) * 3;
+  return al(m * g.row_bytes()) + al((int64_t)kQmax * g.nkc * m * pad16(n) * 4) + al(m * n * 4) + al(m * 4) * 3;
+}
+
+// error bound per product, units of 2^-72: A's truncation (2^-73), B's (2^-73
+// with nine digits; zero for the exact elements of a six-digit B) and the
+// dropped pairs s + t >= nq (|d_s w_s| <= 2^-8s for s >= 1)
+double per_product_bound(int sb, int nq) {
+  double e = 0.5 + (sb == kS ? 0.5 : 0.0);
+  for (int s = 1; s < kS; ++s)
+    for (int t = 1; t < sb; ++t)
+      if (s + t >= nq) e += ldexp(1.0, 72 - 8 * (s + t));
+  return e * 1.01;
 }
 
 // out (m x n x 2 binary32, row stride ldo elements) = A (m x k x nca) . B for
@@ -658,7 +699,7 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   int8_t* planes = reinterpret_cast<int8_t*>(buf);
   buf += al(m * g.row_bytes());
   int* cq = reinterpret_cast<int*>(buf);
-  buf += al((int64_t)kS * g.nkc * m * np * 4);
+  buf += al((int64_t)kQmax * g.nkc * m * np * 4);
   int* rlist = reinterpret_cast<int*>(buf);
   buf += al(m * n * 4);
   int* ea = reinterpret_cast<int*>(buf);
@@ -685,34 +726,47 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   // 0 (stored in reverse order, so also contiguous); C_cq is an np x m
   // column-major = m x np row-major int32 matrix
   if (ev) cudaEventRecord(ev[1], s);
-  const int sb = pb.sb;
+  const int sb = pb.sb, nq = diagonals(k);
   const int64_t lda = g.row_bytes(), ldb = g.row_bytes(sb);
+  // One GEMM per diagonal over the concatenated digit planes.  Tuning knob
+  // MCF_OZ_PAIRWISE=1: one GEMM per digit pair (depth kc) accumulating into
+  // C_q (beta = 1; the same exact int32 sums) -- measured no faster at config
+  // 4 (265 ms both) and slower at config 2 (2.77 vs 2.27 ms), so off.
+  static const bool pairwise = [] {
+    const char* e = getenv("MCF_OZ_PAIRWISE");
+    return e && atoi(e) == 1;
+  }();
   for (int64_t c = 0; c < g.nkc; ++c)
-    for (int q = 0; q < kS; ++q) {
-      const int th = q < sb - 1 ? q : sb - 1;
-      st = gemm_s8(pb.planes + c * sb * g.kc + (int64_t)(sb - 1 - th) * g.kc, ldb,
-                   planes + c * kS * g.kc + (int64_t)(q - th) * g.kc, lda, cq + (c * kS + q) * m * np, np, m,
-                   (int64_t)(th + 1) * g.kc, s);
+    for (int q = 0; q < nq; ++q) {
+      // pairs (q - t, t), t in [tl, th]: A planes q - th .. q - tl ascending,
+      // B planes th .. tl (stored reversed: ascending positions)
+      const int th = q < sb - 1 ? q : sb - 1, tl = q > kS - 1 ? q - (kS - 1) : 0;
+      const int8_t* bp = pb.planes + c * sb * g.kc + (int64_t)(sb - 1 - th) * g.kc;
+      const int8_t* ap = planes + c * kS * g.kc + (int64_t)(q - th) * g.kc;
+      int* cp = cq + (c * nq + q) * m * np;
+      if (pairwise) {
+        for (int u = 0; u <= th - tl && st == MCF_OK; ++u)
+          st = gemm_s8(bp + u * g.kc, ldb, ap + u * g.kc, lda, cp, np, m, g.kc, s, u > 0);
+      } else {
+        st = gemm_s8(bp, ldb, ap, lda, cp, np, m, (int64_t)(th - tl + 1) * g.kc, s);
+      }
       if (st != MCF_OK) return st;
     }
   if (ev) cudaEventRecord(ev[2], s);
-  // fallback threshold (scaled units): 2^50 x the error bound per output.
-  // Per product: A's truncation 2^-73, B's 2^-73 (nine digits; zero for the
-  // exact elements of a six-digit B), the dropped pairs s + t >= 9:
-  // 8.03 2^-72 (nine B digits) or 5.02 2^-72 (six).  Inexact B elements add
-  // 2^-48 (1.01) / 2 to every output of their column (thr_inexact each).
-  const double per_prod = sb == kS ? 9.03 : 5.52;
-  const double thr = ldexp((double)k * per_prod, 50 - 72);
+  // fallback threshold (scaled units): 2^50 x the error bound per output
+  // (per product bound x K); inexact elements of a six-digit B add 2^-48
+  // (1.01) / 2 to every output of their column (thr_inexact each)
+  const double thr = ldexp((double)k * per_product_bound(sb, nq), 50 - 72);
   const double thr_inexact = ldexp(0.505, 50 - 48);
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
-  k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, ea, pb.eb, rnf, pb.cnf, pb.cinx, thr, thr_inexact,
+  k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, nq, ea, pb.eb, rnf, pb.cnf, pb.cinx, thr, thr_inexact,
                                                           out, ldo, rlist, rcnt);
   mcfr::note_launch();
-  if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
-  else if (nca == 2) launch_fallback<2, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
-  else if (pb.ncb == 2) launch_fallback<1, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
-  else launch_fallback<1, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, out, ldo, s);
+  if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
+  else if (nca == 2) launch_fallback<2, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
+  else if (pb.ncb == 2) launch_fallback<1, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
+  else launch_fallback<1, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
   if (ev) cudaEventRecord(ev[3], s);
   return mcfr::check_launch("mm_fast combine kernels");
 }
@@ -772,10 +826,10 @@ int ozaki_digits() { return mcfg::oz::kS; }
 
 // int8 GEMM-equivalents (M x N x K each) per product: pairs (s, t) with
 // s + t < kS, s < kS, t < b_digits
-int ozaki_gemm_equivalents(int ncb) {
+int ozaki_gemm_equivalents(int ncb, int64_t k) {
   using namespace mcfg::oz;
   int c = 0;
-  for (int q = 0; q < kS; ++q) c += std::min(q, b_digits(ncb) - 1) + 1;
+  for (int q = 0; q < diagonals(k); ++q) c += std::min(q, b_digits(ncb) - 1) - std::max(0, q - (kS - 1)) + 1;
   return c;
 }
 
@@ -805,7 +859,7 @@ mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, in
     }
     // the per-row fallback counters sit at the end of the rows region
     const KGeo g = kgeo(k);
-    const char* cnt = ws + bb + al(m * g.row_bytes()) + al((int64_t)kS * g.nkc * m * pad16(n) * 4) +
+    const char* cnt = ws + bb + al(m * g.row_bytes()) + al((int64_t)kQmax * g.nkc * m * pad16(n) * 4) +
                       al(m * n * 4) + al(m * 4) * 2;
     std::vector<int> rc(m);
     cudaMemcpy(rc.data(), cnt, m * sizeof(int), cudaMemcpyDeviceToHost);
