@@ -62,17 +62,45 @@ def make_batch(n, in_dim=784, classes=10, seed_x=3001, seed_y=3002):
 
 class GradExchange:
     """Flat binary32 gradient buffer + sum all-reduce across a process group.
-    Works for any torch device/backend (NCCL on B200s, gloo on CPU tests)."""
+    Works for any torch device/backend (NCCL on B200s, gloo on CPU tests).
+
+    Buckets: reduce_bucket(b) starts an asynchronous all-reduce of a
+    contiguous run of views as soon as the backward pass has written them
+    (one layer's dW and db), so the exchange of layer l overlaps the
+    backward GEMMs of layer l-1; finish() waits for every bucket
+    (and reduces the loss sum).  all_reduce() is the one-shot form."""
 
     def __init__(self, shapes, device, group=None):
         self.shapes = shapes
         sizes = [int(np.prod(s)) for s in shapes]
         self.flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
-        self.views, off = [], 0
+        self.views, self.offsets, off = [], [], 0
         for s, n in zip(shapes, sizes):
             self.views.append(self.flat[off:off + n].view(*s))
+            self.offsets.append((off, off + n))
             off += n
         self.group = group
+        self._pending = []
+
+    def reduce_bucket(self, first_view: int, last_view: int):
+        """Start the sum all-reduce of views first_view..last_view (inclusive)."""
+        if self.world() <= 1:
+            return
+        import torch.distributed as dist
+
+        a, b = self.offsets[first_view][0], self.offsets[last_view][1]
+        self._pending.append(dist.all_reduce(self.flat[a:b], op=dist.ReduceOp.SUM, group=self.group,
+                                             async_op=True))
+
+    def finish(self, loss_sum: torch.Tensor = None):
+        """Wait for the started buckets; reduce the loss sum."""
+        for h in self._pending:
+            h.wait()
+        self._pending = []
+        if self.world() > 1 and loss_sum is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(loss_sum, op=dist.ReduceOp.SUM, group=self.group)
 
     def world(self):
         if self.group is None:
@@ -156,12 +184,13 @@ class MCMLP:
             _check(gemm(0, 1, G.data_ptr(), n, acts[l].data_ptr(), n, gv[2 * l].data_ptr(), in_dim, out_dim, in_dim, n,
                         None, s))
             _check(rowsum(G.data_ptr(), out_dim, n, gv[2 * l + 1].data_ptr(), s))
+            self.grads.reduce_bucket(2 * l, 2 * l + 1)  # overlaps the next layer's backward
             if l > 0:
                 _check(lib_.mcf_approx(B32, self.W[l].data_ptr(), nc, B["Wa"][l].data_ptr(), out_dim * in_dim, s))
                 # dA_prev (in x n) = approx(W)^T (in x out) . G (out x n), ReLU mask = H_{l-1}
                 _check(gemm(1, 0, B["Wa"][l].data_ptr(), in_dim, G.data_ptr(), n, B["G"][l - 1].data_ptr(), n, in_dim,
                             n, out_dim, B["H"][l - 1].data_ptr(), s))
-        self.grads.all_reduce(B["loss"])
+        self.grads.finish(B["loss"])
         for l in range(L):
             _check(lib_.mcf_sgd_grow(self.W[l].data_ptr(), nc, gv[2 * l].data_ptr(), self.W[l].numel() // nc,
                                      C.c_float(self.lr), s))

@@ -41,7 +41,10 @@ def _worker(rank, world, port, outdir):
         v.copy_(torch.randn(v.shape, generator=g))
     mine = ex.flat.clone()
     loss = torch.tensor([float(rank + 1)])
-    ex.all_reduce(loss)
+    # per-layer buckets, started in backward order, as MCMLP.step does
+    ex.reduce_bucket(2, 3)
+    ex.reduce_bucket(0, 1)
+    ex.finish(loss)
     # every rank's contribution, gathered for the check
     parts = [torch.zeros_like(mine) for _ in range(world)]
     dist.all_gather(parts, mine)
