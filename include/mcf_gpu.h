@@ -189,6 +189,17 @@ mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_
 /* out[r] = sum_j g[r, j] in order (bias gradient, autodiff.hpp:287-292) */
 mcf_status mcf_rowsum_f32_ordered(const float* g, int64_t rows, int64_t n, float* out,
                                   mcf_stream stream);
+/* ---- MC activations (autodiff.hpp) ------------------- */
+/* mc_relu_op forward (autodiff.hpp:340-350): the components of every element
+ * whose approx() is <= 0 are zeroed; bit-identical. */
+mcf_status mcf_mc_relu(mcf_prec p, const void* x, int nc, void* out, int64_t numel, mcf_stream stream);
+/* mc_softmax (autodiff.hpp:383-413) over the middle index of an (outer, n,
+ * inner) view of x (the reference's rank-1 / rank-2 tensor and axis: rows x
+ * cols with axis -1 is (rows, cols, 1), axis 0 is (1, rows, cols)):
+ * bit-identical, with the correctly rounded exp of exp_mcn. */
+mcf_status mcf_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner, void* out,
+                          mcf_stream stream);
+
 /* Plan MCF_FAST versions of the two above (the reference-order plan needs
  * neither): FP32 GEMM in cuBLAS order (no TF32) with the same operands and
  * optional ReLU mask, and a tree-ordered row sum. */

@@ -97,6 +97,8 @@ class Oracle:
             "dot_mcmc": [_int, _p, _p, _int, _i64, _i64, _p],
             "mm_mcmc_sampled": [_int, _p, _p, _int, _i64, _i64, _i64, _p, _p, _i64, _p],
             "matmul2d": [_int, _p, _p, _i64, _i64, _i64, _p],
+            "mc_relu": [_int, _p, _int, _p, _i64],
+            "mc_softmax": [_int, _p, _int, _i64, _i64, _i64, _p, _int],
         }.items():
             f = self._f(name)
             f.argtypes = args
@@ -268,6 +270,24 @@ class Oracle:
         M, K = a.shape; N = b.shape[1]
         out = np.empty((M, N), a.dtype)
         self._check(self._f("matmul2d")(prec_of(a), _ptr(a), _ptr(b), M, K, N, _ptr(out)), "matmul2d")
+        return out
+
+    # ---- MC activations (autodiff.hpp:340-413) ------------------------------------
+    def mc_relu(self, x):
+        x = np.ascontiguousarray(x); nc = x.shape[-1]; out = np.empty_like(x)
+        self._check(self._f("mc_relu")(prec_of(x), _ptr(x), nc, _ptr(out), x.size // nc), "mc_relu")
+        return out
+
+    def mc_softmax(self, x, axis=-1, exp_mode=EXP_LIBM):
+        """x: (n, nc) or (rows, cols, nc); softmax over `axis` of the value shape."""
+        x = np.ascontiguousarray(x); nc = x.shape[-1]; shp = x.shape[:-1]
+        if len(shp) == 1:
+            outer, n, inner = 1, shp[0], 1
+        else:
+            ax = axis % 2
+            outer, n, inner = (shp[0], shp[1], 1) if ax == 1 else (1, shp[0], shp[1])
+        out = np.empty_like(x)
+        self._check(self._f("mc_softmax")(prec_of(x), _ptr(x), nc, outer, n, inner, _ptr(out), exp_mode), "mc_softmax")
         return out
 
     # ---- port-only helpers -------------------------------------------------------

@@ -327,6 +327,23 @@ static double q_relerr(__float128 got, __float128 truth) {
   return truth == 0 ? (double)d : (double)(d / fabsq(truth));
 }
 
+int mcfo_mc_relu(int prec, const void* x, int nc, void* out, int64_t numel) {
+  if (BAD_NC(nc)) return 1;
+  DISPATCH(prec, b16_op_relu(x, nc, out, numel), b32_op_relu(x, nc, out, numel), b64_op_relu(x, nc, out, numel));
+}
+
+int mcfo_mc_softmax(int prec, const void* x, int nc, int64_t outer, int64_t n, int64_t inner, void* out,
+                    int exp_mode) {
+  if (BAD_NC(nc) || outer < 0 || n < 0 || inner < 0) return 1;
+  if (exp_mode == MCFO_EXP_CR) {
+    DISPATCH(prec, b16_op_softmax(x, nc, outer, n, inner, out, cr_exp_plain),
+             b32_op_softmax(x, nc, outer, n, inner, out, cr_exp_plain),
+             b64_op_softmax(x, nc, outer, n, inner, out, cr_exp_plain));
+  }
+  DISPATCH(prec, b16_op_softmax(x, nc, outer, n, inner, out, exp), b32_op_softmax(x, nc, outer, n, inner, out, exp),
+           b64_op_softmax(x, nc, outer, n, inner, out, exp));
+}
+
 int mcfo_relerr_mm_mct(int prec, const void* x, int nc, const void* w, int64_t m, int64_t k,
                        int64_t n, const int64_t* rows, const int64_t* cols, int64_t nsamp,
                        const void* cand, int cand_nc, double* relerr) {

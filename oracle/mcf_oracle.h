@@ -81,7 +81,12 @@ enum { MCFO_SEQUENTIAL = 0, MCFO_PAIRWISE_TREE = 1 };
                            const int64_t* cols, int64_t nsamp, void* out);               \
   /* plain working-precision matmul2d (ndarray.hpp:147-165) */                           \
   int pfx##matmul2d(int prec, const void* a, const void* b, int64_t m, int64_t k,        \
-                    int64_t n, void* out);
+                    int64_t n, void* out);                                               \
+  /* mc_relu_op forward (autodiff.hpp:340-350) */                                        \
+  int pfx##mc_relu(int prec, const void* x, int nc, void* out, int64_t numel);           \
+  /* mc_softmax (autodiff.hpp:383-413) over the middle index of (outer, n, inner) */     \
+  int pfx##mc_softmax(int prec, const void* x, int nc, int64_t outer, int64_t n,         \
+                      int64_t inner, void* out, int exp_mode);
 
 MCFO_DECL(mcfo_)
 MCFO_DECL(mcfref_)

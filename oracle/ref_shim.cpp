@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "mcf_oracle.h"
+#include "mcfloat/autodiff.hpp"
 #include "mcfloat/linalg.hpp"
 #include "mcfloat/mc_ops.hpp"
 #include "mcfloat/nn.hpp"
@@ -340,6 +341,33 @@ int mcfref_matmul2d(int prec, const void* a, const void* b, std::int64_t m, std:
                                  to_nd<P>(b, 0, k * n, Shape{K, N}))
                     .vec(),
                 out, 0);
+  });
+}
+
+// mc_relu_op (autodiff.hpp:340-350) through the reference's tape: an MC
+// parameter leaf, the op, its MC value
+int mcfref_mc_relu(int prec, const void* x, int nc, void* out, std::int64_t numel) {
+  return with_prec(prec, [&]<class P>() {
+    MCTensor<P> p = to_mct<P>(x, 0, numel, nc);
+    mcf::Tape<P> tape;
+    const auto a = tape.mc_param(p);
+    const auto r = mcf::mc_relu_op(tape, a);
+    from_vec<P>(tape.mc_value(r).raw(), out, 0);
+  });
+}
+
+// mc_softmax (autodiff.hpp:383-413): the (outer, n, inner) view as the
+// reference's rank-1 / rank-2 tensor and axis
+int mcfref_mc_softmax(int prec, const void* x, int nc, std::int64_t outer, std::int64_t n, std::int64_t inner,
+                      void* out, int exp_mode) {
+  if (exp_mode != MCFO_EXP_LIBM) return 1;
+  if (outer != 1 && inner != 1) return 1;  // the reference takes rank 1 / 2 only
+  return with_prec(prec, [&]<class P>() {
+    const auto O = static_cast<std::size_t>(outer), N = static_cast<std::size_t>(n),
+               I = static_cast<std::size_t>(inner);
+    Shape shape = inner == 1 ? (outer == 1 ? Shape{N} : Shape{O, N}) : Shape{N, I};
+    const int axis = inner == 1 ? -1 : 0;
+    from_vec<P>(mcf::mc_softmax(to_mct<P>(x, 0, outer * n * inner, nc, shape), axis).raw(), out, 0);
   });
 }
 

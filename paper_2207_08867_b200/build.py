@@ -33,7 +33,7 @@ NVFLAGS = ARCH + [
 CXXFLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-I" + os.path.join(CUDA, "include"),
             "-I" + os.path.join(ROOT, "include")]
 
-CU_SOURCES = ["elementwise.cu", "linalg.cu", "mm_fast.cu", "mm_ozaki.cu", "stream_fast.cu", "mlp.cu", "mlp_fast.cu",
+CU_SOURCES = ["elementwise.cu", "linalg.cu", "mm_fast.cu", "mm_ozaki.cu", "stream_fast.cu", "mlp.cu", "mlp_fast.cu", "mc_nn.cu",
               "hostapi.cu"]
 CXX_SOURCES = ["runtime.cpp"]
 

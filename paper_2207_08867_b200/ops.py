@@ -16,7 +16,7 @@ __all__ = [
     "two_sum", "two_prod", "renormalize", "simple_renorm", "approx", "negate", "grow_expn",
     "scaling_n", "div_n", "add_mcn", "div_mcn", "mul_mcn", "mul_mcn_slow", "square_mcn",
     "exp_mcn", "dot_mcn", "mv_mcn", "mm_mcn", "bmm_mcn", "mm4d_mcn", "matmul_mcn", "addmm_mcn",
-    "mm_mcmc", "dot_mcmc", "from_float", "PREC",
+    "mm_mcmc", "dot_mcmc", "mc_relu", "mc_softmax", "from_float", "PREC",
 ]
 
 PREC = {torch.float16: B16, torch.float32: B32, torch.float64: B64}
@@ -210,6 +210,38 @@ def exp_mcn(x):
     nc = _nc(x)
     out = torch.empty_like(x)
     _check(lib().mcf_exp_mcn(_prec(x), _ptr(x), nc, _ptr(out), x.numel() // nc, _stream()))
+    return out
+
+
+# ---- MC activations (autodiff.hpp:340-413) -------------------------------------------
+
+def mc_relu(x):
+    """mc_relu_op forward: zero every component where approx() <= 0  [autodiff.hpp:340-350]."""
+    x = _c(x)
+    nc = _nc(x)
+    out = torch.empty_like(x)
+    _check(lib().mcf_mc_relu(_prec(x), _ptr(x), nc, _ptr(out), x.numel() // nc, _stream()))
+    return out
+
+
+def mc_softmax(x, axis=-1):
+    """Softmax over `axis` in MC arithmetic: max shift via grow_expn, exp_mcn,
+    add_mcn row sum, div_mcn  [autodiff.hpp:383-413].  Rank 1 / 2 values only."""
+    x = _c(x)
+    nc = _nc(x)
+    shp = tuple(x.shape[:-1])
+    rank = len(shp)
+    ax = axis + rank if axis < 0 else axis
+    if rank < 1 or rank > 2 or ax < 0 or ax >= rank:
+        raise ValueError("mc_softmax: supported on rank 1/2 tensors")
+    if rank == 1:
+        outer, n, inner = 1, shp[0], 1
+    elif ax == 1:
+        outer, n, inner = shp[0], shp[1], 1
+    else:
+        outer, n, inner = 1, shp[0], shp[1]
+    out = torch.empty_like(x)
+    _check(lib().mcf_mc_softmax(_prec(x), _ptr(x), nc, outer, n, inner, _ptr(out), _stream()))
     return out
 
 

@@ -136,3 +136,25 @@ def test_b16_rounding_matches_reference(port, ref):
     want = v.astype(np.float16).astype(np.float64)  # numpy's direct double->half RN
     assert np.array_equal(np.signbit(got), np.signbit(want))
     assert np.array_equal(got, want)
+
+
+# ---- MC activations: mc_relu_op, mc_softmax -----------------
+
+@pytest.mark.parametrize("bits,nc", [(32, 2), (32, 3), (16, 2), (64, 2), (32, 1), (64, 4)])
+def test_mc_relu_port_equals_reference(port, ref, bits, nc):
+    rng = np.random.default_rng(40 + nc + bits)
+    x = random_mc(rng, 500, nc, DT[bits], -3, 3)
+    x[::7] = 0
+    x[5, -1] = -abs(x[5, -1]) if nc > 1 else x[5, -1]
+    assert_bits(port.mc_relu(x), ref.mc_relu(x), f"mc_relu b{bits} nc{nc}")
+
+
+@pytest.mark.parametrize("bits,nc", [(32, 2), (32, 3), (16, 2), (64, 2), (32, 1)])
+@pytest.mark.parametrize("shape,axis", [((37,), -1), ((9, 23), -1), ((23, 9), 0)])
+def test_mc_softmax_port_equals_reference(port, ref, bits, nc, shape, axis):
+    rng = np.random.default_rng(50 + nc + bits + len(shape))
+    n = int(np.prod(shape))
+    x = random_mc(rng, n, nc, DT[bits], -2, 2).reshape(*shape, nc)
+    got = port.mc_softmax(x, axis, oracle.EXP_LIBM)
+    want = ref.mc_softmax(x, axis, oracle.EXP_LIBM)
+    assert_bits(got, want, f"mc_softmax b{bits} nc{nc} {shape} axis {axis}")
