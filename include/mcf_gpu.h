@@ -200,6 +200,10 @@ mcf_status mcf_mc_relu(mcf_prec p, const void* x, int nc, void* out, int64_t num
 mcf_status mcf_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner, void* out,
                           mcf_stream stream);
 
+/* host-buffer form of mcf_mc_softmax (mcf_h_elementwise takes "mc_relu") */
+mcf_status mcf_h_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner,
+                            void* out);
+
 /* Plan MCF_FAST versions of the two above (the reference-order plan needs
  * neither): FP32 GEMM in cuBLAS order (no TF32) with the same operands and
  * optional ReLU mask, and a tree-ordered row sum. */

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "mcf_gpu.h"
+#include "mcfloat/autodiff.hpp"
 #include "mcfloat/linalg.hpp"
 #include "mcfloat/mc_ops.hpp"
 
@@ -165,6 +166,32 @@ MCTensor<P> exp_mcn(const MCTensor<P>& x) {  // mc_ops.hpp:482-490 (correctly ro
 template <class P>
 MCTensor<P> negate(const MCTensor<P>& x) {  // mc_ops.hpp:376-381
   return detail::elementwise<P>("negate", &x, nullptr, nullptr, x.shape(), x.nc());
+}
+
+// ---- MC activations (autodiff.hpp) ------------------------------------------------
+
+// the value mc_relu_op (autodiff.hpp:340-350) puts on the tape: components
+// zeroed where approx() <= 0
+template <class P>
+MCTensor<P> mc_relu(const MCTensor<P>& x) {
+  mcf::detail::check_nc_limit(x.nc());
+  return detail::elementwise<P>("mc_relu", &x, nullptr, nullptr, x.shape(), x.nc());
+}
+
+// mc_softmax (autodiff.hpp:383-413), same rank / axis rules and message
+template <class P>
+MCTensor<P> mc_softmax(const MCTensor<P>& x, int axis = -1) {
+  std::size_t outer, n, inner;
+  mcf::detail::softmax_axis_dims(x, axis, outer, n, inner);
+  mcf::detail::check_nc_limit(x.nc());
+  using S = detail::Store<P>;
+  const auto xs = detail::pack<P>(x.raw());
+  std::vector<typename S::T> os(xs.size());
+  detail::check(mcf_h_mc_softmax(S::kPrec, xs.data(), x.nc(), static_cast<int64_t>(outer), static_cast<int64_t>(n),
+                                 static_cast<int64_t>(inner), os.data()));
+  MCTensor<P> out(x.shape(), x.nc());
+  detail::unpack<P>(os, out.raw());
+  return out;
 }
 
 // ---- contractions (linalg.hpp) ---------------------------------------------------

@@ -26,7 +26,8 @@ struct Op {
 
 const Op kOps[] = {{"grow_expn", 0}, {"scaling_n", 0},  {"div_n", 3},        {"add_mcn", 1},
                    {"div_mcn", 1},   {"mul_mcn", 1},    {"mul_mcn_slow", 1}, {"square_mcn", 2},
-                   {"exp_mcn", 2},   {"negate", 2},     {"approx", 4},       {"scaling_n_expanded", 5}};
+                   {"exp_mcn", 2},   {"negate", 2},     {"approx", 4},       {"scaling_n_expanded", 5},
+                   {"mc_relu", 2}};
 
 mcf_status run_chunk(const std::string& op, mcf_prec p, const void* x, int ncx, const void* y,
                      int ncy, const void* v, int64_t vn, void* out, int64_t n, cudaStream_t s) {
@@ -42,6 +43,7 @@ mcf_status run_chunk(const std::string& op, mcf_prec p, const void* x, int ncx, 
   if (op == "exp_mcn") return mcf_exp_mcn(p, x, ncx, out, n, s);
   if (op == "negate") return mcf_negate(p, x, ncx, out, n, s);
   if (op == "approx") return mcf_approx(p, x, ncx, out, n, s);
+  if (op == "mc_relu") return mcf_mc_relu(p, x, ncx, out, n, s);
   return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mcf_h_elementwise: unknown operator " + op);
 }
 
@@ -162,6 +164,23 @@ mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64
   if (bw) TRY(cuda_ok(cudaMemcpyAsync(dw, w, bw, cudaMemcpyHostToDevice, s), "H2D w"));
   TRY(mcf_bmm_mcn(p, dx, nc, dw, batch, m, k, n, w_batched, dout, strategy, 1, s));
   if (bo) TRY(cuda_ok(cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, s), "D2H out"));
+  return cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
+mcf_status mcf_h_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner,
+                            void* out) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mc_softmax: unknown precision");
+  if (mcfr::bad_nc(nc)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
+  if (outer < 0 || n < 0 || inner < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mc_softmax: negative dimension");
+  const std::size_t bytes = (std::size_t)outer * n * inner * nc * mcfr::elem_bytes(p);
+  if (bytes == 0) return MCF_OK;
+  char* d = static_cast<char*>(mcfr::workspace(2 * bytes + 512, 0));
+  if (!d) return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot allocate device workspace");
+  cudaStream_t s = mcfr::side_stream(0);
+  char* dout = d + ((bytes + 255) & ~std::size_t(255));
+  TRY(cuda_ok(cudaMemcpyAsync(d, x, bytes, cudaMemcpyHostToDevice, s), "H2D x"));
+  TRY(mcf_mc_softmax(p, d, nc, outer, n, inner, dout, s));
+  TRY(cuda_ok(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s), "D2H out"));
   return cuda_ok(cudaStreamSynchronize(s), "sync");
 }
 

@@ -73,6 +73,28 @@ static void run(int nc) {
   same(gpu::mul_mcn_slow(x, y), mul_mcn_slow(x, y), tag("mul_mcn_slow"));
   same(gpu::square_mcn(x), square_mcn(x), tag("square_mcn"));
   same(gpu::negate(x), negate(x), tag("negate"));
+  {
+    // mc_relu_op's value, through the reference's tape
+    MCTensor<P> px = x;
+    Tape<P> tape;
+    const auto r = mc_relu_op(tape, tape.mc_param(px));
+    same(gpu::mc_relu(x), tape.mc_value(r), tag("mc_relu"));
+    // mc_softmax: the GPU's exp is correctly rounded, the reference's is libm:
+    // compare the evaluated values (the expansions may differ in the last bit
+    // of a component where libm's exp is not correctly rounded)
+    MCTensor<P> a(Shape{6, 9}, nc);
+    for (std::size_t e = 0; e < a.numel(); ++e)
+      detail::expansion_of_double<P>(rng.uniform(-3.0, 3.0), a.comps(e), nc);
+    for (int axis : {-1, 0}) {
+      const NdArray g = gpu::mc_softmax(a, axis).approx(), w = mc_softmax(a, axis).approx();
+      double worst = 0;
+      for (std::size_t i = 0; i < g.numel(); ++i) worst = std::fmax(worst, std::fabs(g[i] - w[i]) / std::fabs(w[i]));
+      const bool ok = worst <= std::ldexp(1.0, -P::significand_bits + 2);
+      std::printf("%-40s %s %s\n", tag(axis < 0 ? "mc_softmax axis -1" : "mc_softmax axis 0"), P::name,
+                  ok ? "ok" : "MISMATCH");
+      g_fail += ok ? 0 : 1;
+    }
+  }
   if (nc < 8) {
     MCTensor<P> a(Shape{19, 33}, nc);
     for (std::size_t e = 0; e < a.numel(); ++e)
