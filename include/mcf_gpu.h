@@ -173,6 +173,14 @@ int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
  * [replaces autodiff.hpp:255-276 mc_linear_op forward + :133-144 relu]. */
 mcf_status mcf_mlp_bias_act(const float* z, int nc, const float* bias, int64_t out_dim, int64_t n,
                             int relu, float* h, float* act, mcf_stream stream);
+/* One MCLinear forward + ReLU (mc_linear_op, autodiff.hpp:255-268; Tape::relu
+ * :133-144): h = approx(add_mcn(W . A_prev, bias)), act = relu ? max(h, 0) : h
+ * (act may be null).  Under MCF_FAST on the tensor-core shapes the bias /
+ * approx / ReLU run in the product's recombination epilogue and z is unused;
+ * otherwise z (out_dim x n x nc) receives the MC product. */
+mcf_status mcf_mlp_linear_fwd(const float* w, int nc, const float* a_prev, int64_t out_dim, int64_t in_dim,
+                              int64_t n, const float* bias, int relu, float* z, float* h, float* act, int strategy,
+                              mcf_stream stream);
 /* cross-entropy over logits (classes x n): per-sample terms, gradient
  * (softmax - onehot) / n_global, and (optionally) the left-to-right sum of the
  * terms [replaces autodiff.hpp:541-582]. */

@@ -61,6 +61,8 @@ bool ozaki_supported(int64_t m, int64_t k, int64_t n);
 mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n, float* out,
                     cudaStream_t s);
 int ozaki_digits();
+mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t k, int64_t n, const float* bias,
+                             int relu, float* h, float* act, cudaStream_t s);
 int ozaki_gemm_equivalents(int ncb, int64_t k);
 mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, double* ms,
                         int64_t* fallback, cudaStream_t s);

@@ -380,6 +380,23 @@ mcf_status mcf_mlp_bias_act(const float* z, int nc, const float* bias, int64_t o
   return launched("mlp_bias_act kernel");
 }
 
+// one MCLinear forward (mc_linear_op, autodiff.hpp:255-268) + Tape::relu:
+// Z = W (out x in, MC) . A_prev (in x n), h = approx(add_mcn(Z, bias)),
+// act = relu ? max(h, 0) : h.  Plan MCF_FAST on the tensor-core shapes fuses
+// the bias / approx / ReLU into the product's recombination (Z is never
+// written); otherwise Z (out x n x nc) is the caller's buffer.
+mcf_status mcf_mlp_linear_fwd(const float* w, int nc, const float* a_prev, int64_t out_dim, int64_t in_dim,
+                              int64_t n, const float* bias, int relu, float* z, float* h, float* act, int strategy,
+                              mcf_stream s) {
+  if (strategy == MCF_FAST && nc == 2) {
+    const mcf_status st = mcfr::mm_ozaki_bias_act(w, a_prev, out_dim, in_dim, n, bias, relu, h, act, s);
+    if (st != MCF_ERR_UNSUPPORTED) return st;
+  }
+  const mcf_status st = mcf_bmm_mcn(MCF_B32, w, nc, a_prev, 1, out_dim, in_dim, n, 0, z, strategy, 1, s);
+  if (st != MCF_OK) return st;
+  return mcf_mlp_bias_act(z, nc, bias, out_dim, n, relu, h, act, s);
+}
+
 mcf_status mcf_mlp_cross_entropy(const float* logits, const int* labels, int64_t classes, int64_t n,
                                  int64_t n_global, float* grad, float* terms, float* term_sum, mcf_stream s) {
   if (n == 0) return MCF_OK;

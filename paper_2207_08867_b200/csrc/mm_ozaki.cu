@@ -44,6 +44,8 @@
 #include <vector>
 
 #include "mcf_accum.cuh"
+#include "mcf_fast.cuh"
+#include "mcf_lit.cuh"
 #include "mcf_runtime.h"
 
 namespace mcfg {
@@ -291,6 +293,33 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
   }
 }
 
+// Optional fused epilogue of an MC-MLP layer (mc_linear_op, autodiff.hpp:265-
+// 268, then Tape::relu): z = the product's two components, r = add_mcn(z,
+// bias[i]) (mc_ops.hpp:440-446; bias is MC nc=2 per output row), h =
+// approx(r); h and act = relu ? max(h, 0) : h are written instead of z.
+struct Epilogue {
+  const float* bias = nullptr;  // (m, 2); null: write the product's components
+  float* h = nullptr;
+  float* act = nullptr;  // optional
+  int relu = 0;
+};
+
+__device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j, float* out, int64_t ldo,
+                                     const Epilogue& ep) {
+  if (!ep.bias) {
+    split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
+    return;
+  }
+  float z[2], b[2], r[2];
+  split_out<float, 2, 2>(v, z);
+  b[0] = ep.bias[i * 2];
+  b[1] = ep.bias[i * 2 + 1];
+  if (!fast::add<PB32, 2>(z, b, r)) lit::add<PB32>(z, 2, b, 2, r, 2);
+  const float hv = fast::approx<PB32, 2>(r);
+  ep.h[i * ldo + j] = hv;
+  if (ep.act) ep.act[i * ldo + j] = ep.relu ? (hv > 0.0f ? hv : 0.0f) : hv;  // Tape::relu, autodiff.hpp:134
+}
+
 // C = sum_{c,q} C_cq 2^(-14-8q), scaled back, split into two binary32
 // components written with row stride ldo; ill-conditioned / non-finite
 // outputs are listed per row (rlist[i * n + slot] = j, rcnt[i] entries) for
@@ -304,7 +333,7 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
                                                  const int* __restrict__ cnf, const int* __restrict__ cinx,
                                                  double thr, double thr_inexact,
                                                  float* __restrict__ out, int64_t ldo,
-                                                 int* __restrict__ rlist, int* __restrict__ rcnt) {
+                                                 int* __restrict__ rlist, int* __restrict__ rcnt, Epilogue ep) {
   static_assert(kS == 9, "three groups of three diagonals (+ an optional tenth)");
   // four consecutive columns per thread: 16-byte loads from each plane (ldc
   // is a multiple of 16; padded columns hold zeros and are not written)
@@ -380,7 +409,7 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
       }
       const double sc = pow2d(ei + fj[u]);
       const double v[2] = {__dmul_rn(s2, sc), __dmul_rn(e2, sc)};
-      split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
+      emit(v, i, j, out, ldo, ep);
     }
   }
 }
@@ -397,7 +426,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
                                                   int64_t n, int64_t k, const int* __restrict__ rlist,
                                                   const int* __restrict__ rcnt, const int* __restrict__ rnf,
                                                   const int* __restrict__ cnf, float* __restrict__ out,
-                                                  int64_t ldo) {
+                                                  int64_t ldo, Epilogue ep) {
   extern __shared__ __align__(16) float arow[];
   const int64_t i = blockIdx.x;
   const int cnt = rcnt[i];
@@ -487,7 +516,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
     }
     if (lane == 0) {
       const double v[2] = {S, C};
-      split_out<float, 2, 2>(v, out + (i * ldo + j) * 2);
+      emit(v, i, j, out, ldo, ep);
     }
   }
 }
@@ -495,7 +524,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
 template <int NCA, int NCB>
 mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n, int64_t k, const int* rlist,
                            const int* rcnt, const int* rnf, const int* cnf, float* out, int64_t ldo,
-                           cudaStream_t s) {
+                           const Epilogue& ep, cudaStream_t s) {
   const std::size_t sm = (std::size_t)k * NCA * sizeof(float);
   constexpr std::size_t kMaxSmem = 200u << 10;
   if (sm <= kMaxSmem) {
@@ -504,9 +533,9 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
       cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
       attr = true;
     }
-    k_fallback<NCA, NCB, true><<<(unsigned)m, 256, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo);
+    k_fallback<NCA, NCB, true><<<(unsigned)m, 256, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   } else {
-    k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo);
+    k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   }
   mcfr::note_launch();
   return MCF_OK;
@@ -693,7 +722,7 @@ double per_product_bound(int sb, int nq) {
 // a prepared B.  ev (optional, 4 events): recorded before the A digits,
 // before the GEMMs, after the GEMMs and at the end (phase timing).
 mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo, char* buf,
-                cudaStream_t s, cudaEvent_t* ev = nullptr) {
+                cudaStream_t s, cudaEvent_t* ev = nullptr, const Epilogue& ep = Epilogue{}) {
   const KGeo g = pb.g;
   const int64_t k = g.k, n = pb.n, np = pb.np;
   int8_t* planes = reinterpret_cast<int8_t*>(buf);
@@ -761,12 +790,12 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
   k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, nq, ea, pb.eb, rnf, pb.cnf, pb.cinx, thr, thr_inexact,
-                                                          out, ldo, rlist, rcnt);
+                                                          out, ldo, rlist, rcnt, ep);
   mcfr::note_launch();
-  if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
-  else if (nca == 2) launch_fallback<2, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
-  else if (pb.ncb == 2) launch_fallback<1, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
-  else launch_fallback<1, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, s);
+  if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
+  else if (nca == 2) launch_fallback<2, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
+  else if (pb.ncb == 2) launch_fallback<1, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
+  else launch_fallback<1, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
   if (ev) cudaEventRecord(ev[3], s);
   return mcfr::check_launch("mm_fast combine kernels");
 }
@@ -820,6 +849,27 @@ mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m,
     }
   cudaEventDestroy(fork);
   return st;
+}
+
+// MC-MLP layer forward on the tensor-core path with the bias / approx / ReLU
+// epilogue fused into the recombination: h = approx(add_mcn(W . A, bias)),
+// act = relu(h); the MC product itself is never written
+mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t k, int64_t n, const float* bias,
+                             int relu, float* h, float* act, cudaStream_t s) {
+  using namespace mcfg::oz;
+  if (m < 64 || !ozaki_supported(m, k, n)) return MCF_ERR_UNSUPPORTED;
+  const std::size_t bb = b_bytes(k, n, 1);
+  char* ws = oz_workspace(bb + rows_bytes(m, k, n), s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
+  PreparedB pb;
+  mcf_status st = prepare_b(a, 1, k, n, n, ws, pb, s);
+  if (st != MCF_OK) return st;
+  Epilogue ep;
+  ep.bias = bias;
+  ep.h = h;
+  ep.act = act;
+  ep.relu = relu;
+  return rows(w, 2, m, pb, nullptr, n, ws + bb, s, nullptr, ep);
 }
 
 int ozaki_digits() { return mcfg::oz::kS; }

@@ -161,11 +161,11 @@ class MCMLP:
         acts = [xt]
         for l in range(L):
             out_dim, in_dim = self.dims[l + 1], self.dims[l]
-            _check(lib_.mcf_bmm_mcn(B32, self.W[l].data_ptr(), nc, acts[l].data_ptr(), 1, out_dim, in_dim, n, 0,
-                                    B["Z"][l].data_ptr(), self.plan, 1, s))
             last = l == L - 1
-            _check(lib_.mcf_mlp_bias_act(B["Z"][l].data_ptr(), nc, self.b[l].data_ptr(), out_dim, n, 0 if last else 1,
-                                         B["H"][l].data_ptr(), None if last else B["A"][l].data_ptr(), s))
+            _check(lib_.mcf_mlp_linear_fwd(self.W[l].data_ptr(), nc, acts[l].data_ptr(), out_dim, in_dim, n,
+                                           self.b[l].data_ptr(), 0 if last else 1, B["Z"][l].data_ptr(),
+                                           B["H"][l].data_ptr(), None if last else B["A"][l].data_ptr(), self.plan,
+                                           s))
             if not last:
                 acts.append(B["A"][l])
         # loss + dL/dlogits

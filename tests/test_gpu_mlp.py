@@ -199,3 +199,35 @@ def test_fast_plan_backward_gemm_and_rowsum(ta, tb):
     assert np.all(np.abs(got - want) <= 1e-5 * scale), "gemm_f32_fast"
     rs = got.sum(axis=1)
     assert np.allclose(out.cpu().numpy(), rs, rtol=1e-5, atol=1e-5 * np.abs(got).sum(axis=1).max()), "rowsum"
+
+
+@pytest.mark.parametrize("relu", [0, 1])
+def test_fused_linear_forward_equals_product_then_bias_act(relu):
+    """Plan FAST's fused layer (bias / approx / ReLU in the tensor-core
+    product's epilogue, fallback outputs included) gives the same bits as the
+    product written out and mcf_mlp_bias_act applied to it."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(80 + relu)
+    out_dim, in_dim, n = 200, 300, 500
+    w = torch.from_numpy(split(rng.uniform(-0.1, 0.1, out_dim * in_dim), 2, np.float32)
+                         .reshape(out_dim, in_dim, 2)).cuda()
+    a = torch.from_numpy(np.maximum(rng.standard_normal((in_dim, n)), 0).astype(np.float32)).cuda()
+    b = torch.from_numpy(split(rng.uniform(-0.1, 0.1, out_dim), 2, np.float32).reshape(out_dim, 2)).cuda()
+    lib = mcf.lib()
+    f32 = dict(dtype=torch.float32, device="cuda")
+    z = torch.empty((out_dim, n, 2), **f32)
+    h1, a1 = torch.empty((out_dim, n), **f32), torch.empty((out_dim, n), **f32)
+    h2, a2 = torch.empty((out_dim, n), **f32), torch.empty((out_dim, n), **f32)
+    assert lib.mcf_mlp_linear_fwd(w.data_ptr(), 2, a.data_ptr(), out_dim, in_dim, n, b.data_ptr(), relu,
+                                  z.data_ptr(), h1.data_ptr(), a1.data_ptr(), mcf.FAST, None) == 0
+    assert lib.mcf_bmm_mcn(mcf.B32, w.data_ptr(), 2, a.data_ptr(), 1, out_dim, in_dim, n, 0, z.data_ptr(),
+                           mcf.FAST, 1, None) == 0
+    assert lib.mcf_mlp_bias_act(z.data_ptr(), 2, b.data_ptr(), out_dim, n, relu, h2.data_ptr(), a2.data_ptr(),
+                                None) == 0
+    torch.cuda.synchronize()
+    assert_bits(h1.cpu().numpy(), h2.cpu().numpy(), "h")
+    assert_bits(a1.cpu().numpy(), a2.cpu().numpy(), "act")
