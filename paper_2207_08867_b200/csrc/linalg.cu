@@ -217,6 +217,98 @@ __global__ void __launch_bounds__(kThreads) k_bmm_exact(const ST<P>* __restrict_
   }
 }
 
+// ---- pairwise tree as a warp-parallel split-K ------------
+// DotCore::reduce_range (linalg.hpp:59-76) halves [lo, hi) at mid = lo +
+// (hi - lo) / 2 down to runs of <= leaf_arity terms and merges with
+// add_kernel(left, right).  A warp per output reproduces that tree exactly:
+// lane l takes the depth-5 node its bits select (MSB = the root's choice),
+// reduces it with the same recursion, and the lanes merge back up the five
+// top levels with shuffles -- left child (lower lane) as add_kernel's x --
+// skipping levels whose node was already a leaf.  32-way parallel per output
+// for long K / few outputs; bit-identical to the reference's tree.
+
+template <class P, int NC>
+__device__ __noinline__ bool tree_range(const ST<P>* x, int64_t xa, const ST<P>* w, int64_t wa, int64_t ws,
+                                        int64_t lo, int64_t hi, int64_t leafn, RT<P> (&acc)[NC + 1]) {
+  if (hi - lo <= leafn) {
+    bool ok = fast_term<P, NC>(x, xa + lo, P::ld(w[wa + lo * ws]), acc);
+    RT<P> t[NC + 1];
+    for (int64_t k = lo + 1; k < hi; ++k) {
+      ok &= fast_term<P, NC>(x, xa + k, P::ld(w[wa + k * ws]), t);
+      ok &= fast::add_ordered<P, NC + 1, NC + 1>(acc, t, acc);
+    }
+    return ok;
+  }
+  const int64_t mid = lo + (hi - lo) / 2;
+  RT<P> rhs[NC + 1];
+  bool ok = tree_range<P, NC>(x, xa, w, wa, ws, lo, mid, leafn, acc);
+  ok &= tree_range<P, NC>(x, xa, w, wa, ws, mid, hi, leafn, rhs);
+  ok &= fast::add_ordered<P, NC + 1, NC + 1>(acc, rhs, acc);
+  return ok;
+}
+
+template <class P, int NC>
+__global__ void __launch_bounds__(kThreads) k_bmm_tree(const ST<P>* __restrict__ x, const ST<P>* __restrict__ w,
+                                                       int64_t batch, int64_t m, int64_t k, int64_t n,
+                                                       int w_batched, ST<P>* __restrict__ out, int leaf) {
+  constexpr int D = 5;  // top levels resolved across the 32 lanes
+  const int lane = threadIdx.x & 31;
+  const int64_t total = batch * m * n;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t leafn = leaf > 1 ? leaf : 1;
+  for (int64_t o = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < total; o += warps) {
+    const int64_t b = o / (m * n), r = o % (m * n), i = r / n, j = r % n;
+    const int64_t xa = (b * m + i) * k;
+    const int64_t wa = (w_batched ? b * k * n : 0) + j;
+    RT<P> res[NC];
+    bool ok = true;
+    if (k == 0) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) res[c] = RT<P>(0);
+    } else {
+      // descend to this lane's depth-5 node; internal[d] = node at depth d split
+      int64_t lo = 0, hi = k;
+      unsigned internal = 0;
+      int depth = 0;
+      for (; depth < D; ++depth) {
+        if (hi - lo <= leafn) break;
+        internal |= 1u << depth;
+        const int64_t mid = lo + (hi - lo) / 2;
+        if ((lane >> (D - 1 - depth)) & 1) lo = mid;
+        else hi = mid;
+      }
+      // a node that stopped splitting above depth 5 is held by the lane whose
+      // remaining bits are zero; the other lanes of its subtree carry nothing
+      const bool holder = depth == D || (lane & ((1 << (D - depth)) - 1)) == 0;
+      RT<P> acc[NC + 1];
+#pragma unroll
+      for (int c = 0; c <= NC; ++c) acc[c] = RT<P>(0);
+      if (holder) ok = tree_range<P, NC>(x, xa, w, wa, n, lo, hi, leafn, acc);
+      // merge up: level d (depth D-1 .. 0), partner differs in bit (D-1-d)
+      for (int d = D - 1; d >= 0; --d) {
+        const int bit = 1 << (D - 1 - d);
+        RT<P> rhs[NC + 1];
+#pragma unroll
+        for (int c = 0; c <= NC; ++c) rhs[c] = __shfl_xor_sync(0xffffffffu, acc[c], bit);
+        // the depth-d node on this lane's path; only meaningful on lanes whose
+        // bits below (D-1-d) are zero, which hold its left child
+        if ((internal >> d) & 1 && (lane & (2 * bit - 1)) == 0) ok &= fast::add_ordered<P, NC + 1, NC + 1>(acc, rhs, acc);
+      }
+      ok &= fast::renorm<P, NC + 1, NC>(acc, res);
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+    if (lane == 0) {
+      if (bad != 0) {
+        RT<P> r2[lit::kMaxNc];
+        lit_dot<P>(x, xa, w, wa, n, NC, k, MCF_PAIRWISE_TREE, leaf, r2);
+        for (int c = 0; c < NC; ++c) out[o * NC + c] = P::sv(r2[c]);
+      } else {
+        for (int c = 0; c < NC; ++c) out[o * NC + c] = P::sv(res[c]);
+      }
+    }
+  }
+}
+
 // MC x MC, recipe B: out[i, j] = sum_k x[xa_i + k*xs] * y[ya_j + k*ys]
 // dot: (x, y both (batch, k, nc)); mm: x (m, k, nc), y (k, n, nc)
 template <class P, int NC>
@@ -263,6 +355,16 @@ int per_sm(K kernel) {
 template <class P, int NC>
 mcf_status launch_bmm(const void* x, int nc, const void* w, int64_t batch, int64_t m, int64_t k,
                       int64_t n, int w_batched, void* out, int strategy, int leaf, cudaStream_t s) {
+  if constexpr (NC >= 2) {
+    if (strategy == MCF_PAIRWISE_TREE) {
+      auto tk = k_bmm_tree<P, NC>;
+      const int grid = mcfr::grid_for(batch * m * n * 32, kThreads, 8);
+      tk<<<grid, kThreads, 0, s>>>(static_cast<const ST<P>*>(x), static_cast<const ST<P>*>(w), batch, m, k, n,
+                                   w_batched, static_cast<ST<P>*>(out), leaf);
+      mcfr::note_launch();
+      return mcfr::check_launch("mcf bmm tree kernel");
+    }
+  }
   auto kern = k_bmm_exact<P, NC>;
   static const int occ = per_sm(kern);
   const int grid = mcfr::grid_for(batch * m * n, kThreads, occ);

@@ -60,6 +60,21 @@ def test_pairwise_tree_bitwise(gr, port, nc):
         assert_bits(got, port.bmm_mcn(x, w, oracle.PAIRWISE_TREE, leaf), f"tree leaf={leaf}")
 
 
+@pytest.mark.parametrize("k,leaf", [(1, 1), (7, 1), (31, 2), (33, 1), (100, 40), (3000, 1), (4097, 5), (20000, 64)])
+def test_pairwise_tree_warp_split_bitwise(gr, port, k, leaf):
+    """The warp-parallel tree (5 levels across lanes, leaves and deeper levels
+    per lane) on K that leave some top-level nodes as leaves, odd splits and
+    long K: the same tree as linalg.hpp:59-76, bit for bit."""
+    import paper_2207_08867_b200 as mcf
+
+    for nc in (2, 3):
+        rng = np.random.default_rng(k + leaf + nc)
+        x = random_mc(rng, 3 * k, nc, np.float32, -3, 3).reshape(3, k, nc)
+        w = wp(rng, (k, 2), 32)
+        got = gr.run("mm_mcn", x, w, plan=(mcf.PAIRWISE_TREE, leaf))
+        assert_bits(got, port.bmm_mcn(x, w, oracle.PAIRWISE_TREE, leaf), f"tree k={k} leaf={leaf} nc={nc}")
+
+
 def test_single_component_equals_plain_matmul(gr, port):
     """T/test_linalg.cpp:297-314: nc=1 mm == matmul2d bitwise."""
     rng = np.random.default_rng(48)
