@@ -593,10 +593,27 @@ mcf_status launch_lit(const Args& a) {
   return mcfr::check_launch("mcf elementwise kernel (literal)");
 }
 
-// fast paths exist for binary32 with nc 1..4 and equal operand nc
+// register fast paths: binary32 with nc 1..4 and binary64 with nc 1..3
+// (SURVEY 8f row 3), equal operand nc; everything else runs the literal
+// kernels.  The fast paths' preconditions are checked per element at run
+// time with the literal restatement as the fallback, so they are exact for
+// any precision; binary16 keeps the literal kernels (one rounding per op).
 template <int OP, class P>
 mcf_status dispatch(const Args& a) {
   if (a.numel == 0) return MCF_OK;
+  if constexpr (std::is_same<P, PB64>::value) {
+    if constexpr (OP != kApprox && OP != kSimple && OP != kRenorm && OP != kScaleX) {
+      const bool same_nc = !OpTraits<OP>::kY || a.ncx == a.ncy;
+      if (same_nc) {
+        switch (a.ncx) {
+          case 1: return launch_fast<OP, P, 1, 1>(a);
+          case 2: return launch_fast<OP, P, 2, 2>(a);
+          case 3: return launch_fast<OP, P, 3, 3>(a);
+          default: break;
+        }
+      }
+    }
+  }
   if constexpr (std::is_same<P, PB32>::value) {
     if constexpr (OP == kRenorm) {
       if (a.ncx == a.onc) {

@@ -204,3 +204,19 @@ def test_host_entry_points_match_device(port):
     assert_bits(mcf.host.div_n(v, yd), port.div_n(v, yd), "host div_n")
     assert_bits(mcf.host.scaling_n(x, v[:1]), port.scaling_n(x, v[:1]), "host scaling scalar")
     assert_bits(mcf.host.approx(x), port.approx(x), "host approx")
+
+
+@pytest.mark.parametrize("nc", [2, 3])
+def test_binary64_fast_paths_full_tiles(gr, port, nc):
+    """Binary64 register fast paths on enough elements for
+    the TMA tile kernel, plus a ragged tail, every operator bitwise."""
+    x, y, yd, v = _inputs(900 + nc, 300_001, nc, 64, False)
+    for name, args, ref in (("grow_expn", (x, v), port.grow_expn(x, v)),
+                            ("scaling_n", (x, v), port.scaling_n(x, v)),
+                            ("div_n", (v, yd), port.div_n(v, yd)),
+                            ("add_mcn", (x, y), port.add_mcn(x, y)),
+                            ("div_mcn", (x, yd), port.div_mcn(x, yd)),
+                            ("mul_mcn", (x, y), port.mul_mcn(x, y)),
+                            ("square_mcn", (x,), port.square_mcn(x)),
+                            ("exp_mcn", (np.clip(x, -10, 10),), port.exp_mcn(np.clip(x, -10, 10), oracle.EXP_CR))):
+        assert_bits(gr.run(name, *args), ref, f"b64 nc{nc} {name}")
