@@ -23,6 +23,7 @@
 #include "mcfloat/mc_ops.hpp"
 #include "mcfloat/nn.hpp"
 #include "mcfloat/optim.hpp"
+#include "mcfloat/serialize.hpp"
 
 namespace {
 
@@ -369,6 +370,28 @@ int mcfref_mc_softmax(int prec, const void* x, int nc, std::int64_t outer, std::
     const int axis = inner == 1 ? -1 : 0;
     from_vec<P>(mcf::mc_softmax(to_mct<P>(x, 0, outer * n * inner, nc, shape), axis).raw(), out, 0);
   });
+}
+
+// mct_to_json (serialize.hpp:40-54) dumped as write_json_file does (indent 2);
+// returns the string length, or -1 if it does not fit
+std::int64_t mcfref_mct_to_json(int prec, const void* x, int nc, const std::int64_t* shape, int rank, char* buf,
+                                std::int64_t cap) {
+  std::int64_t len = -1;
+  with_prec(prec, [&]<class P>() {
+    Shape sh;
+    std::int64_t numel = 1;
+    for (int d = 0; d < rank; ++d) {
+      sh.push_back(static_cast<std::size_t>(shape[d]));
+      numel *= shape[d];
+    }
+    const std::string s = mcf::mct_to_json(to_mct<P>(x, 0, numel, nc, sh)).dump(2);
+    if (static_cast<std::int64_t>(s.size()) < cap) {
+      std::memcpy(buf, s.data(), s.size());
+      buf[s.size()] = 0;
+      len = static_cast<std::int64_t>(s.size());
+    }
+  });
+  return len;
 }
 
 // ---- timing entry points (bench.py cpu_baseline / --impl reference) ----------

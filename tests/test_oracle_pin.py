@@ -158,3 +158,33 @@ def test_mc_softmax_port_equals_reference(port, ref, bits, nc, shape, axis):
     got = port.mc_softmax(x, axis, oracle.EXP_LIBM)
     want = ref.mc_softmax(x, axis, oracle.EXP_LIBM)
     assert_bits(got, want, f"mc_softmax b{bits} nc{nc} {shape} axis {axis}")
+
+
+# ---- mct blobs: serialize.hpp ------------------------------
+
+@pytest.mark.parametrize("bits,nc,shape", [(32, 2, (3, 4)), (16, 3, (5,)), (64, 1, (2, 2, 2)), (32, 8, (1,))])
+def test_mct_json_matches_reference(ref, bits, nc, shape):
+    import ctypes as C
+    import json
+
+    import torch
+
+    from paper_2207_08867_b200 import serialize
+
+    rng = np.random.default_rng(bits + nc)
+    x = random_mc(rng, int(np.prod(shape)), nc, DT[bits], -8, 8).reshape(*shape, nc)
+    x.reshape(-1)[:3] = [0.0, -0.0, np.inf]
+    f = ref.lib.mcfref_mct_to_json
+    f.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_char_p, C.c_int64]
+    f.restype = C.c_int64
+    shp = np.array(shape, np.int64)
+    buf = C.create_string_buffer(1 << 20)
+    n = f(oracle.prec_of(x), x.ctypes.data, nc, shp.ctypes.data, len(shape), buf, len(buf))
+    assert n > 0
+    want = json.loads(buf.value.decode())
+    got = serialize.mct_to_json(torch.from_numpy(x))
+    assert got == want
+    back = serialize.mct_from_json(want, f"b{bits}").numpy()
+    assert_bits(back, x, "round trip")
+    with pytest.raises(ValueError, match="does not match requested"):
+        serialize.mct_from_json(want, "b64" if bits != 64 else "b32")
