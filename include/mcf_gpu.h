@@ -208,6 +208,15 @@ mcf_status mcf_mc_relu(mcf_prec p, const void* x, int nc, void* out, int64_t num
 mcf_status mcf_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner, void* out,
                           mcf_stream stream);
 
+/* Hyperbolic half-space distances (hyperbolic.hpp:160-226):
+ * for pairs (u[p], v[p]) of an (n, dim) MC embedding table, arg[p] =
+ * halfspace_arg (the fused per-coordinate add / square / add fold, height
+ * product, scale, div, grow, approx; bit-identical) and, if dist is not null,
+ * dist[p] = arcosh_guarded(arg[p]) (device log/log1p: within four units in
+ * the last place of P of the host libm result).  u, v, arg, dist: device arrays. */
+mcf_status mcf_halfspace_arg(mcf_prec p, const void* table, int nc, int64_t n, int64_t dim, const int64_t* u,
+                             const int64_t* v, int64_t npairs, double* arg, double* dist, mcf_stream stream);
+
 /* host-buffer form of mcf_mc_softmax (mcf_h_elementwise takes "mc_relu") */
 mcf_status mcf_h_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner,
                             void* out);

@@ -99,6 +99,7 @@ class Oracle:
             "matmul2d": [_int, _p, _p, _i64, _i64, _i64, _p],
             "mc_relu": [_int, _p, _int, _p, _i64],
             "mc_softmax": [_int, _p, _int, _i64, _i64, _i64, _p, _int],
+            "halfspace_arg": [_int, _p, _int, _i64, _i64, _p, _p, _i64, _p],
         }.items():
             f = self._f(name)
             f.argtypes = args
@@ -288,6 +289,15 @@ class Oracle:
             outer, n, inner = (shp[0], shp[1], 1) if ax == 1 else (1, shp[0], shp[1])
         out = np.empty_like(x)
         self._check(self._f("mc_softmax")(prec_of(x), _ptr(x), nc, outer, n, inner, _ptr(out), exp_mode), "mc_softmax")
+        return out
+
+    def halfspace_arg(self, table, u, v):
+        """table (n, dim, nc); u, v pair indices -> float64 arcosh arguments."""
+        table = np.ascontiguousarray(table); n, dim, nc = table.shape
+        u = np.ascontiguousarray(u, np.int64); v = np.ascontiguousarray(v, np.int64)
+        out = np.empty(u.size, np.float64)
+        self._check(self._f("halfspace_arg")(prec_of(table), _ptr(table), nc, n, dim, _ptr(u), _ptr(v), u.size,
+                                             _ptr(out)), "halfspace_arg")
         return out
 
     # ---- port-only helpers -------------------------------------------------------

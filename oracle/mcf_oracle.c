@@ -344,6 +344,21 @@ int mcfo_mc_softmax(int prec, const void* x, int nc, int64_t outer, int64_t n, i
            b64_op_softmax(x, nc, outer, n, inner, out, exp));
 }
 
+int mcfo_halfspace_arg(int prec, const void* table, int nc, int64_t n, int64_t dim, const int64_t* u,
+                       const int64_t* v, int64_t npairs, double* out) {
+  if (BAD_NC(nc) || dim < 1) return 1;
+  for (int64_t p = 0; p < npairs; ++p) {
+    if (u[p] < 0 || u[p] >= n || v[p] < 0 || v[p] >= n) return 1;
+    switch (prec) {
+      case MCFO_B16: out[p] = b16_op_halfspace_arg(table, nc, dim, u[p], v[p]); break;
+      case MCFO_B32: out[p] = b32_op_halfspace_arg(table, nc, dim, u[p], v[p]); break;
+      case MCFO_B64: out[p] = b64_op_halfspace_arg(table, nc, dim, u[p], v[p]); break;
+      default: return 1;
+    }
+  }
+  return 0;
+}
+
 int mcfo_relerr_mm_mct(int prec, const void* x, int nc, const void* w, int64_t m, int64_t k,
                        int64_t n, const int64_t* rows, const int64_t* cols, int64_t nsamp,
                        const void* cand, int cand_nc, double* relerr) {

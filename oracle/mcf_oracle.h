@@ -86,7 +86,11 @@ enum { MCFO_SEQUENTIAL = 0, MCFO_PAIRWISE_TREE = 1 };
   int pfx##mc_relu(int prec, const void* x, int nc, void* out, int64_t numel);           \
   /* mc_softmax (autodiff.hpp:383-413) over the middle index of (outer, n, inner) */     \
   int pfx##mc_softmax(int prec, const void* x, int nc, int64_t outer, int64_t n,         \
-                      int64_t inner, void* out, int exp_mode);
+                      int64_t inner, void* out, int exp_mode);                           \
+  /* halfspace_arg (hyperbolic.hpp:183-212) for pairs (u[p], v[p]) of an (n, dim) */     \
+  /* MC table: the P value as a double per pair                                  */     \
+  int pfx##halfspace_arg(int prec, const void* table, int nc, int64_t n, int64_t dim,    \
+                         const int64_t* u, const int64_t* v, int64_t npairs, double* out);
 
 MCFO_DECL(mcfo_)
 MCFO_DECL(mcfref_)

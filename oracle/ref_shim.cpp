@@ -19,6 +19,7 @@
 
 #include "mcf_oracle.h"
 #include "mcfloat/autodiff.hpp"
+#include "mcfloat/hyperbolic.hpp"
 #include "mcfloat/linalg.hpp"
 #include "mcfloat/mc_ops.hpp"
 #include "mcfloat/nn.hpp"
@@ -392,6 +393,16 @@ std::int64_t mcfref_mct_to_json(int prec, const void* x, int nc, const std::int6
     }
   });
   return len;
+}
+
+int mcfref_halfspace_arg(int prec, const void* table, int nc, std::int64_t n, std::int64_t dim,
+                         const std::int64_t* u, const std::int64_t* v, std::int64_t npairs, double* out) {
+  return with_prec(prec, [&]<class P>() {
+    const auto t = to_mct<P>(table, 0, n * dim, nc, Shape{static_cast<std::size_t>(n), static_cast<std::size_t>(dim)});
+    for (std::int64_t p = 0; p < npairs; ++p)
+      out[p] = mcf::halfspace_arg(t, static_cast<std::size_t>(u[p]), static_cast<std::size_t>(v[p]),
+                                  static_cast<std::size_t>(dim));
+  });
 }
 
 // ---- timing entry points (bench.py cpu_baseline / --impl reference) ----------

@@ -78,6 +78,7 @@ _SIGS = {
     "mcf_gemm_f32_fast": [_int, _int, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _p],
     "mcf_rowsum_f32_fast": [_p, _i64, _i64, _p, _p],
     "mcf_mc_relu": [_int, _p, _int, _p, _i64, _p],
+    "mcf_halfspace_arg": [_int, _p, _int, _i64, _i64, _p, _p, _i64, _p, _p, _p],
     "mcf_mlp_linear_fwd": [_p, _int, _p, _i64, _i64, _i64, _p, _int, _p, _p, _p, _int, _p],
     "mcf_mc_softmax": [_int, _p, _int, _i64, _i64, _i64, _p, _p],
     "mcf_sgd_grow": [_p, _int, _p, _i64, C.c_float, _p],

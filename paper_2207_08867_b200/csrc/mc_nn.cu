@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <type_traits>
 
 #include "mcf_lit.cuh"
 #include "mcf_prec.cuh"
@@ -146,6 +147,80 @@ mcf_status softmax_prec(const void* xv, int nc, int64_t outer, int64_t n, int64_
   return mcfr::check_launch("mc_softmax kernels");
 }
 
+// ---- hyperbolic half-space distances (hyperbolic.hpp:160-226; 8f next row 4) ------
+
+template <class P>
+__device__ __forceinline__ double max_finite() {
+  if constexpr (std::is_same<P, PB16>::value) return 65504.0;
+  else if constexpr (std::is_same<P, PB32>::value) return 3.4028234663852886e38;
+  else return 1.7976931348623157e308;
+}
+
+// one pair per thread: the fused add / square / add fold over the
+// coordinates, the canonical-order height product, scale, div, grow, approx
+// (halfspace_arg, hyperbolic.hpp:183-212), then arcosh_guarded (:160-170)
+template <class P>
+__global__ void __launch_bounds__(128) k_halfspace(const ST<P>* __restrict__ table, int nc, int64_t n,
+                                                   int64_t dim, const int64_t* __restrict__ us,
+                                                   const int64_t* __restrict__ vs, int64_t npairs,
+                                                   double* __restrict__ arg_out, double* __restrict__ dist_out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npairs) return;
+  const int64_t u = us[p], v = vs[p];
+  if (u < 0 || u >= n || v < 0 || v >= n) {
+    arg_out[p] = __longlong_as_double(0x7ff8000000000000LL);
+    if (dist_out) dist_out[p] = arg_out[p];
+    return;
+  }
+  using R = RT<P>;
+  R xu[lit::kMaxNc], xv[lit::kMaxNc], neg[lit::kMaxNc], diff[lit::kMaxNc], sq[lit::kMaxNc], s[lit::kMaxNc];
+  R hu[lit::kMaxNc], hv[lit::kMaxNc], hprod[lit::kMaxNc], den[lit::kMaxNc], t[lit::kMaxNc], arg[lit::kMaxNc];
+  for (int i = 0; i < nc; ++i) s[i] = R(0);
+  for (int64_t c = 0; c < dim; ++c) {
+    load<P>(table, u * dim + c, nc, xu);
+    load<P>(table, v * dim + c, nc, xv);
+    for (int i = 0; i < nc; ++i) neg[i] = -xv[i];
+    lit::add<P>(xu, nc, neg, nc, diff, nc);
+    lit::square<P>(diff, nc, sq);
+    lit::add<P>(s, nc, sq, nc, s, nc);
+  }
+  load<P>(table, u * dim + dim - 1, nc, hu);
+  load<P>(table, v * dim + dim - 1, nc, hv);
+  bool swap = false;  // comps_less(hv, hu), hyperbolic.hpp:174-179
+  for (int i = 0; i < nc; ++i)
+    if (hv[i] != hu[i]) {
+      swap = hv[i] < hu[i];
+      break;
+    }
+  lit::mul_fast<P>(swap ? hv : hu, swap ? hu : hv, nc, hprod);
+  lit::scale<P>(hprod, nc, R(2), den, nc);
+  lit::div<P>(s, den, nc, t);
+  lit::grow<P>(t, nc, R(1), arg);
+  const double a0 = P::to_d(lit::approx<P>(arg, nc));
+  arg_out[p] = a0;
+  if (dist_out) {
+    double a = a0 < 1.0 ? 1.0 : a0;
+    if (a > max_finite<P>()) a = max_finite<P>();
+    double d;
+    if (a <= 1.0 + 1e-12) {
+      d = sqrt(2.0 * (a - 1.0));
+    } else {
+      const double inv = 1.0 / a;
+      d = log(a) + log1p(sqrt((1.0 - inv) * (1.0 + inv)));
+    }
+    dist_out[p] = P::to_d(P::rd(d));
+  }
+}
+
+template <class P>
+mcf_status halfspace_prec(const void* table, int nc, int64_t n, int64_t dim, const int64_t* u, const int64_t* v,
+                          int64_t npairs, double* arg, double* dist, cudaStream_t s) {
+  k_halfspace<P><<<(unsigned)((npairs + 127) / 128), 128, 0, s>>>(static_cast<const ST<P>*>(table), nc, n, dim, u, v,
+                                                                 npairs, arg, dist);
+  mcfr::note_launch();
+  return mcfr::check_launch("halfspace kernel");
+}
+
 }  // namespace
 }  // namespace mcfg
 
@@ -199,6 +274,27 @@ mcf_status mcf_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int6
     case MCF_B16: return mcfg::softmax_prec<mcfg::PB16>(x, nc, outer, n, inner, out, s);
     case MCF_B32: return mcfg::softmax_prec<mcfg::PB32>(x, nc, outer, n, inner, out, s);
     default: return mcfg::softmax_prec<mcfg::PB64>(x, nc, outer, n, inner, out, s);
+  }
+}
+
+// halfspace_arg for pairs (u[p], v[p]) of an (n, dim) MC table (hyperbolic.hpp:
+// 183-212): arg[p] bit-identical to the reference; dist[p] (optional) =
+// arcosh_guarded (:160-170) of it, binary64 log / log1p on the device (within
+// four units of P's last place of the host libm result).  Out-of-range indices
+// give NaN.
+mcf_status mcf_halfspace_arg(mcf_prec p, const void* table, int nc, int64_t n, int64_t dim, const int64_t* u,
+                             const int64_t* v, int64_t npairs, double* arg, double* dist, mcf_stream s) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "halfspace_arg: unknown precision");
+  if (mcfr::bad_nc(nc)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
+  if (n < 0 || dim < 1 || npairs < 0)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "halfspace_distance: table rank");
+  if (npairs == 0) return MCF_OK;
+  const mcf_status st = mcfr::ensure_device_tables();
+  if (st != MCF_OK) return st;
+  switch (p) {
+    case MCF_B16: return mcfg::halfspace_prec<mcfg::PB16>(table, nc, n, dim, u, v, npairs, arg, dist, s);
+    case MCF_B32: return mcfg::halfspace_prec<mcfg::PB32>(table, nc, n, dim, u, v, npairs, arg, dist, s);
+    default: return mcfg::halfspace_prec<mcfg::PB64>(table, nc, n, dim, u, v, npairs, arg, dist, s);
   }
 }
 

@@ -16,7 +16,8 @@ __all__ = [
     "two_sum", "two_prod", "renormalize", "simple_renorm", "approx", "negate", "grow_expn",
     "scaling_n", "div_n", "add_mcn", "div_mcn", "mul_mcn", "mul_mcn_slow", "square_mcn",
     "exp_mcn", "dot_mcn", "mv_mcn", "mm_mcn", "bmm_mcn", "mm4d_mcn", "matmul_mcn", "addmm_mcn",
-    "mm_mcmc", "dot_mcmc", "mc_relu", "mc_softmax", "from_float", "PREC",
+    "mm_mcmc", "dot_mcmc", "mc_relu", "mc_softmax", "halfspace_distance", "from_float",
+    "PREC",
 ]
 
 PREC = {torch.float16: B16, torch.float32: B32, torch.float64: B64}
@@ -243,6 +244,24 @@ def mc_softmax(x, axis=-1):
     out = torch.empty_like(x)
     _check(lib().mcf_mc_softmax(_prec(x), _ptr(x), nc, outer, n, inner, _ptr(out), _stream()))
     return out
+
+
+def halfspace_distance(table, u, v, return_arg=False):
+    """Half-space model distances between rows u[p] and v[p] of an (n, dim, nc)
+    MC embedding table  [hyperbolic.hpp:160-226]: the arcosh argument in MC
+    arithmetic (bit-identical), then arcosh_guarded in binary64."""
+    table = _c(table)
+    nc = _nc(table)
+    if table.dim() != 3:
+        raise ValueError("halfspace_distance: table rank")
+    n, dim = table.shape[0], table.shape[1]
+    u = torch.as_tensor(u, dtype=torch.int64, device=table.device).contiguous()
+    v = torch.as_tensor(v, dtype=torch.int64, device=table.device).contiguous()
+    arg = torch.empty(u.shape, dtype=torch.float64, device=table.device)
+    dist = torch.empty(u.shape, dtype=torch.float64, device=table.device)
+    _check(lib().mcf_halfspace_arg(_prec(table), _ptr(table), nc, n, dim, _ptr(u), _ptr(v), u.numel(), _ptr(arg),
+                                   _ptr(dist), _stream()))
+    return (dist, arg) if return_arg else dist
 
 
 # ---- contractions (linalg.hpp) ------------------------------------------------------

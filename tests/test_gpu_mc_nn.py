@@ -45,3 +45,45 @@ def test_mc_softmax_rejects_rank3(gr):
     x = torch.zeros((2, 3, 4, 2), dtype=torch.float32, device="cuda")
     with pytest.raises(ValueError, match="rank 1/2"):
         mcf.mc_softmax(x)
+
+
+def _arcosh_guarded(a, dt):
+    """hyperbolic.hpp:160-170 on the host (libm log / log1p), rounded to P."""
+    a = np.clip(a, 1.0, float(np.finfo(dt).max))
+    small = a <= 1.0 + 1e-12
+    with np.errstate(invalid="ignore"):
+        inv = 1.0 / a
+        big = np.log(a) + np.log1p(np.sqrt((1.0 - inv) * (1.0 + inv)))
+    return np.where(small, np.sqrt(2.0 * (a - 1.0)), big).astype(dt).astype(np.float64)
+
+
+@pytest.mark.parametrize("bits,nc,dim", [(32, 2, 3), (16, 2, 4), (64, 3, 2), (32, 1, 5), (64, 2, 6)])
+def test_halfspace_distance(gr, port, bits, nc, dim):
+    """Half-space model distances (hyperbolic.hpp:183-226):
+    the MC arcosh argument bit-identical to the oracle (pinned to the
+    reference), symmetric bitwise, the distance within four units of P's
+    last place of the host arcosh (two libm calls and a sum on each side)."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    dt = DT[bits]
+    rng = np.random.default_rng(bits * 10 + nc + dim)
+    n = 64
+    tab = random_mc(rng, n * dim, nc, dt, -2, 1).reshape(n, dim, nc)
+    tab[:, -1, 0] = np.abs(tab[:, -1, 0]) + dt(0.05)
+    tab[3] = tab[4]
+    u = rng.integers(0, n, 2000)
+    v = rng.integers(0, n, 2000)
+    u[:2], v[:2] = [3, 7], [4, 7]
+    dist, arg = mcf.halfspace_distance(torch.from_numpy(tab).cuda(), u, v, return_arg=True)
+    arg = arg.cpu().numpy()
+    want = port.halfspace_arg(tab, u, v)
+    assert np.array_equal(arg.view(np.uint64), want.view(np.uint64))
+    d2, _ = mcf.halfspace_distance(torch.from_numpy(tab).cuda(), v, u, return_arg=True)
+    assert np.array_equal(dist.cpu().numpy().view(np.uint64), d2.cpu().numpy().view(np.uint64)), "symmetry"
+    dh = _arcosh_guarded(want, dt)
+    dg = dist.cpu().numpy()
+    ulp = np.spacing(np.abs(dh).astype(dt)).astype(np.float64)
+    assert np.all(np.abs(dg - dh) <= 4 * ulp), "distance vs host arcosh"
+    assert dg[0] == 0.0 and dg[1] == 0.0  # coincident rows, same row

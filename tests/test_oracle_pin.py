@@ -188,3 +188,20 @@ def test_mct_json_matches_reference(ref, bits, nc, shape):
     assert_bits(back, x, "round trip")
     with pytest.raises(ValueError, match="does not match requested"):
         serialize.mct_from_json(want, "b64" if bits != 64 else "b32")
+
+
+# ---- hyperbolic distance pipeline: hyperbolic.hpp ---------------
+
+@pytest.mark.parametrize("bits,nc,dim", [(32, 2, 3), (16, 2, 4), (64, 3, 2), (32, 1, 5), (64, 2, 6)])
+def test_halfspace_arg_port_equals_reference(port, ref, bits, nc, dim):
+    rng = np.random.default_rng(bits * 10 + nc + dim)
+    n = 40
+    tab = random_mc(rng, n * dim, nc, DT[bits], -2, 1).reshape(n, dim, nc)
+    tab[:, -1, 0] = np.abs(tab[:, -1, 0]) + DT[bits](0.05)  # positive heights
+    tab[3] = tab[4]  # coincident rows
+    u = rng.integers(0, n, 300)
+    v = rng.integers(0, n, 300)
+    u[:2], v[:2] = [3, 7], [4, 7]
+    got = port.halfspace_arg(tab, u, v)
+    want = ref.halfspace_arg(tab, u, v)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
