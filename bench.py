@@ -420,6 +420,17 @@ def run_ours(args):
                  "fp64_pipe_peak_measured": round(f64.value / 1e12, 3)}
     step()  # leave `out` holding the headline path's result
     torch.cuda.synchronize()
+    # the north star's mm roofline "in MCF flops": the reference algorithm's
+    # 113.1 rounded FP ops per multiply-add (DotCore at nc=2)
+    # per unit time against the FP32 FMA pipe's peak (measured in this run)
+    ref_ops = 113.1
+    fp32_peak = f32.value / 1e12
+    mcf_flops = {"ops_per_mad": ref_ops, "fp32_fma_pipe_peak_TOPS": round(fp32_peak, 2),
+                 "tensor_core_path": round(ref_ops * rows * N * K / (ms * 1e-3) / 1e12 / fp32_peak, 2),
+                 "fp64_pipe_path": round(ref_ops * rows * N * K / (ms64 * 1e-3) / 1e12 / fp32_peak, 2),
+                 "target": 0.5,
+                 "note": "fraction of the FP32 FMA-pipe peak in the reference's own flops (north star: >= 0.5); "
+                         "above 1 because the GPU algorithms need far fewer operations per multiply-add"}
 
     # e2e through the host-buffer C-ABI, pinned buffers, copies inside the timed region
     a_pin = torch.from_numpy(a_h[r0:r1]).pin_memory()
@@ -482,6 +493,7 @@ def run_ours(args):
                                             "int8_gemms": round(med[2], 3), "combine_fallback": round(med[3], 3)},
                          "fallback_outputs": int(fb.value)},
             "fp64_pipe_path": fp64_path,
+            "mcf_flops_roofline": mcf_flops,
             "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes},
             "gpu_launches": launches,
