@@ -180,12 +180,15 @@ def run_reference(args):
 
 # ---- our arm ---------------------------------------------------------------------
 
-def elementwise_suite(torch, mcf, hbm_gbs):
-    """Config 0 (2^24 elements, fp32 nc=2): device time per operator."""
+def elementwise_suite(torch, mcf, hbm_gbs, rank=0, world=1):
+    """Config 0 (2^24 elements, fp32 nc=2): device time per operator.  With
+    world > 1 every rank takes its flat range [r N / W, (r+1) N / W) (no
+    collective); the time is the max over ranks and the GB/s the whole job's."""
     from paper_2207_08867_b200 import data
 
     n = 1 << 24
-    x, y, yd, v, xe = (torch.from_numpy(t).cuda() for t in data.config0(n))
+    lo, hi = rank * n // world, (rank + 1) * n // world
+    x, y, yd, v, xe = (torch.from_numpy(t[lo:hi]).cuda() for t in data.config0(n))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ops = {
         "grow_expn": (lambda: mcf.grow_expn(x, v), 20), "scaling_n": (lambda: mcf.scaling_n(x, v), 20),
@@ -200,6 +203,8 @@ def elementwise_suite(torch, mcf, hbm_gbs):
         ts = []
         for _ in range(5):
             flush.zero_()
+            if world > 1:
+                torch.distributed.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             f()
@@ -207,8 +212,12 @@ def elementwise_suite(torch, mcf, hbm_gbs):
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         ms = statistics.median(ts)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
         gbs = bpe * n / ms / 1e6
-        res[name] = {"us": round(ms * 1e3, 1), "GB/s": round(gbs, 1), "frac_hbm": round(gbs / hbm_gbs, 3),
+        res[name] = {"us": round(ms * 1e3, 1), "GB/s": round(gbs, 1), "frac_hbm": round(gbs / hbm_gbs / world, 3),
                      "bytes_per_elem": bpe}
     del x, y, yd, v, xe, flush
     return res
@@ -462,10 +471,10 @@ def run_ours(args):
     ew = None
     cpu = None
     others = None
+    del a, b, out, a_pin, b_pin, o_pin
+    torch.cuda.empty_cache()
+    ew = elementwise_suite(torch, mcf, hbm, rank, world)  # flat-range shards across ranks
     if rank == 0 and world == 1:
-        del a, b, out, a_pin, b_pin, o_pin
-        torch.cuda.empty_cache()
-        ew = elementwise_suite(torch, mcf, hbm)
         if not args.no_extras:
             others = other_configs(torch, mcf, hbm, f64.value / 1e12)
         gf, t, nrows, kind = reference_sample(a_h, b_h, cpu_threads())
@@ -502,8 +511,9 @@ def run_ours(args):
         if cpu:
             line["cpu_baseline"] = cpu
         if ew:
-            line["elementwise"] = {"config": "config0: 2^24 elements, fp32 nc=2, bit-exact vs reference",
-                                   "hbm_peak_gbs": hbm, "ops": ew}
+            line["elementwise"] = {"config": "config0: 2^24 elements, fp32 nc=2, bit-exact vs reference"
+                                             + (f", flat range over {world} GPUs" if world > 1 else ""),
+                                   "hbm_peak_gbs": hbm, "frac_hbm_per_gpu": True, "ops": ew}
         if others:
             line["other_configs"] = others
         print(json.dumps(line), flush=True)
