@@ -547,7 +547,7 @@ struct Lt {
   cublasLtHandle_t h = nullptr;
   void* ws = nullptr;
   std::size_t ws_bytes = 0;
-  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t>, cublasLtMatmulAlgo_t> algos;
+  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t>, cublasLtMatmulAlgo_t> algos;
 };
 std::mutex g_lt_mu;
 std::map<int, Lt> g_lt;
@@ -590,7 +590,7 @@ mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
     cleanup();
     return lt_fail("descriptors", st);
   }
-  const auto key = std::make_tuple(rows_c, cols_c, kd, lda);
+  const auto key = std::make_tuple(rows_c, cols_c, kd, lda, ldb);
   auto it = lt.algos.find(key);
   if (it == lt.algos.end()) {
     cublasLtMatmulPreference_t pref = nullptr;

@@ -45,3 +45,23 @@ if "copies" in sys.argv:
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / 5
         print(f"{name}: {a.numel() * 4 / dt / 1e9:.1f} GB/s")
+if "duplex" in sys.argv:
+    d1 = torch.empty(a.shape, dtype=a.dtype, device="cuda")
+    d2 = torch.empty(a.shape, dtype=a.dtype, device="cuda")
+    h2 = torch.empty(a.shape, dtype=a.dtype).pin_memory()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(2):
+        with torch.cuda.stream(s1):
+            d1.copy_(a, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        with torch.cuda.stream(s1):
+            d1.copy_(a, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 5
+    print(f"duplex: {2 * a.numel() * 4 / dt / 1e9:.1f} GB/s total ({a.numel() * 4 / dt / 1e9:.1f} each way)")
