@@ -34,6 +34,12 @@ template <class P>
 using ST = typename P::st;
 
 constexpr int kThreads = 128;
+#ifndef MCF_DOT_PU
+#define MCF_DOT_PU 2
+#endif
+// blind sweeps before the tested ones in the DotCore accumulation (see
+// mcf_fast.cuh sweeps(): any value below the pass cap gives the same bits)
+constexpr int kDotPU = MCF_DOT_PU;
 
 // ---- literal DotCore (runtime nc; fallback and non-instantiated shapes) ----
 
@@ -147,7 +153,7 @@ __device__ __forceinline__ bool fast_dot_seq(const ST<P>* x, int64_t xa, const S
   bool ok = fast_term<P, NC>(x, xa, P::ld(w[wa]), acc);
   for (int64_t k = 1; k < len; ++k) {
     ok &= fast_term<P, NC>(x, xa + k, P::ld(w[wa + k * ws]), t);
-    ok &= fast::add_ordered<P, NC + 1, NC + 1>(acc, t, acc);
+    ok &= fast::add_ordered<P, NC + 1, NC + 1, kDotPU>(acc, t, acc);
   }
   ok &= fast::renorm<P, NC + 1, NC>(acc, out);
   return ok;
