@@ -18,6 +18,7 @@
 
 #include "mcf_exp.cuh"
 #include "mcf_fast.cuh"
+#include "mcf_g2.cuh"
 #include "mcf_lit.cuh"
 #include "mcf_prec.cuh"
 #include "mcf_runtime.h"
@@ -89,9 +90,26 @@ struct OpTraits {
   static constexpr bool kV = OP == kGrow || OP == kScale || OP == kScaleX || OP == kDivN;
 };
 
+// binary32 nc = 2 operators with a certified shortcut (mcf_g2.cuh); an element
+// it declines runs the register path below, then the literal one
+template <int OP, class P, int NC, int ONC>
+constexpr bool kG2 = std::is_same<P, PB32>::value && NC == 2 && ONC == 2 &&
+                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp);
+
 template <int OP, class P, int NC, int ONC>
 __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[NC], RT<P> v,
                                          RT<P> (&o)[ONC]) {
+  if constexpr (kG2<OP, P, NC, ONC>) {
+    using Q = g2::QF32;
+    bool ok;
+    if constexpr (OP == kScale) ok = g2::scale<Q>(x[0], x[1], v, o[0], o[1]);
+    else if constexpr (OP == kSquare) ok = g2::square<Q>(x[0], x[1], o[0], o[1]);
+    else if constexpr (OP == kDiv) ok = g2::div<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
+    else if constexpr (OP == kDivN) ok = g2::div<Q>(v, 0.0f, x[0], x[1], o[0], o[1]);  // x holds the divisor
+    else if constexpr (OP == kMul) ok = g2::mul<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
+    else ok = g2::exp_b32(x[0], x[1], o[0], o[1]);
+    if (__builtin_expect(ok, 1)) return true;
+  }
   if constexpr (OP == kGrow) return fast::grow<P, NC>(x, v, o);
   else if constexpr (OP == kScale || OP == kScaleX) return fast::scale<P, NC, ONC>(x, v, o);
   else if constexpr (OP == kDivN) {

@@ -159,7 +159,8 @@ __device__ __forceinline__ double cr_exp(double x) {
   double yh, yl;
   fast2(ph, pl, yh, yl);
   if (near_midpoint(yh, yl, 0x1p-88)) return slow(x);
-  return scalbn(yh, m);  // |x| <= 704: normal range, exact
+  // |x| <= 704: |m| <= 1016, 2^m and the result are normal, so the product is exact
+  return __dmul_rn(yh, __longlong_as_double((long long)(m + 1023) << 52));
 }
 
 }  // namespace mcfg

@@ -1,0 +1,287 @@
+// mcf_g2.cuh -- certified shortcuts for nc = 2 MCF operators (binary32 fast tier).
+//
+// Why this is exact.  The reference's renorm_kernel (mc_ops.hpp:68-92) only
+// uses error-free two_sum steps and zero compaction, so (no overflow, no
+// underflowed products) the nonzero components c_0, c_1, ... it ends with sum
+// EXACTLY to S, the exact sum of its input terms.  When the loop ends because
+// the sequence is compressed (fl(c_i + c_{i+1}) == c_i, mc_ops.hpp:56-62),
+// every |c_{i+1}| is at most h(c_i), half the gap from c_i to its neighbour
+// on c_{i+1}'s side, and h(c) <= 2^-p |c|.  Hence |S - c_0| <= h(c_0) / (1 -
+// 2^-p): S lies in c_0's rounding interval widened by a factor 1 + 2^-(p-1).
+// If a candidate A satisfies |S - A| < h(A) (1 - 2^-(p-1)), S is strictly
+// inside A's own interval and outside every neighbour's widened one, so
+// c_0 = A.  The same argument on c_1, c_2, ... (sum S - c_0) certifies c_1.
+// The reference output is the first two nonzeros padded with +0, so:
+//
+//     out = (A, B)   whenever  |S - A| and |S - A - B| pass those margins.
+//
+// Each operator below computes candidates A, B and the exact remainders with
+// error-free transforms (ordered so the candidates are nearly always right),
+// tests the two margins, and returns false when any precondition or margin
+// fails; the caller then runs the register path (mcf_fast.cuh), which replays
+// the reference's passes.  That the reference loop always ends compressed on
+// these term sets (it never reaches its pass cap) and that the candidates
+// equal its output whenever the margins pass is checked exhaustively in small
+// precisions and by sampling at p = 24 by tools/g2_verify.cpp, which runs
+// this same header on an emulated-precision policy.
+//
+// Policy Q: T, add, sub, mul, div, fma, abs, finite, hbd(t, d) = half the gap
+// from t to its neighbour on d's side, hb(t) = the smaller of the two half
+// gaps (both 0 for zero / subnormal t), shrink(h) = h (1 - 2^-(p-2)), big(p) (|p| >= 2^-100:
+// a product that large has an exact low part, and a quotient that large is
+// normal), canon(x) (-0 -> +0, the reference's padding).
+#pragma once
+
+#if defined(__CUDACC__)
+#include "mcf_exp.cuh"
+#define G2_HD __host__ __device__ __forceinline__
+#else
+#define G2_HD inline
+#endif
+
+namespace mcfg {
+namespace g2 {
+
+template <class Q>
+using T_ = typename Q::T;
+
+// eft.hpp:31-38
+template <class Q>
+G2_HD void two_sum(T_<Q> a, T_<Q> b, T_<Q>& s, T_<Q>& e) {
+  s = Q::add(a, b);
+  const T_<Q> bv = Q::sub(s, a);
+  const T_<Q> av = Q::sub(s, bv);
+  e = Q::add(Q::sub(a, av), Q::sub(b, bv));
+}
+
+// Dekker: exact when |a| >= |b| (or a == 0)
+template <class Q>
+G2_HD void fast_two_sum(T_<Q> a, T_<Q> b, T_<Q>& s, T_<Q>& e) {
+  s = Q::add(a, b);
+  e = Q::sub(b, Q::sub(s, a));
+}
+
+// eft.hpp:75-80
+template <class Q>
+G2_HD void two_prod(T_<Q> a, T_<Q> b, T_<Q>& p, T_<Q>& e) {
+  p = Q::mul(a, b);
+  e = Q::fma(a, b, -p);
+}
+
+// fl(x0 + x1) == x0: the reference's compressed predicate for a pair
+template <class Q>
+G2_HD bool compressed(T_<Q> x0, T_<Q> x1) {
+  return Q::add(x0, x1) == x0;
+}
+
+// the product a*b (p = fl(ab)) has an exact low part: p is large enough or a
+// factor is zero (then the product is exactly zero)
+template <class Q>
+G2_HD bool prod_ok(T_<Q> p, T_<Q> a, T_<Q> b) {
+  return Q::big(p) | (a == T_<Q>(0)) | (b == T_<Q>(0));
+}
+
+// Certify out = (A, C1) from S = A + B + R0 + rest exactly, rest_abs >= |rest|
+// (a rounded-to-nearest sum of magnitudes: the (1 - 2^-(p-2)) factor of thr
+// absorbs its rounding).
+//   (C1, F) = two_sum(B, R0);  S = A + C1 + F + rest
+// Margins: |C1| < thr(A) certifies c_0 = A (|S - A| <= |C1| (1 + 2^-p));
+//          |F| + rest < thr(C1) certifies c_1 = C1.
+// Exact midpoints (frequent: a sum of two binary32 values one binade apart
+// rounds with an error of exactly half an ulp): if S is exactly halfway between
+// two neighbours, the only compressed expansion of S starts with the EVEN
+// neighbour (an odd c_0 would need |c_1| = h, which fl(c_0 + c_1) rounds
+// away, or |c_1| < h with a tail too small to reach h), i.e. c_0 = fl(A + C1)
+// under ties-to-even, c_1 = the exact rest.  Same at the second level with
+// C1 = fl(B + R0).  A zero candidate is only accepted when everything below it
+// is zero (the reference pads +0).
+// REST: a remainder beyond R0 exists; DIR: use the exact half gap on C1's
+// side at the top (needed where the lead is often a power of two: the
+// division's partial products q (y0 + y1) ~ r0, e.g. 1 / y); CANON: final
+// output (a zero component is the reference's +0 padding).
+// The all-zero case passes through the tie clauses (h = 0 for a zero lead).
+template <class Q, bool REST, bool DIR, bool CANON>
+G2_HD bool finish(T_<Q> A, T_<Q> B, T_<Q> R0, T_<Q> rest_abs, T_<Q>& o0, T_<Q>& o1) {
+  T_<Q> C1, F;
+  two_sum<Q>(B, R0, C1, F);
+  // tie at the top: fl(A + C1) is the even neighbour; otherwise it is A
+  const T_<Q> A2 = Q::add(A, C1);
+  const T_<Q> C2 = A2 == A ? C1 : -C1;
+  const T_<Q> below = REST ? Q::add(Q::abs(F), rest_abs) : Q::abs(F);
+  // half gaps: toward C2 at the top (S - A2 has C2's sign) or the smaller
+  // one, and the smaller one below (exact unless C2 is a power of two)
+  const T_<Q> h0 = DIR ? Q::hbd(A2, C2) : Q::hb(A2), h1 = Q::hb(C2);
+  const bool ok0 = (Q::abs(C2) < Q::shrink(h0)) | ((below == T_<Q>(0)) & (Q::abs(C2) == h0));
+  const bool tie1 = REST ? (rest_abs == T_<Q>(0)) & (below == h1) : (below == h1);
+  const bool ok1 = (below < Q::shrink(h1)) | tie1;
+  o0 = CANON ? Q::canon(A2) : A2;
+  o1 = CANON ? Q::canon(C2) : C2;
+  return ok0 & ok1;
+}
+
+// exact product x v (x a compressed pair, underflow guarded by the caller)
+// rounded to two components: S = A + U + w + ew after the sweep below.
+// |fl(e0 + p1)| <= 2^-22 |p0| (x compressed), so the top sum is a fast one.
+template <class Q, bool DIR, bool CANON>
+G2_HD bool scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
+  T_<Q> p0, e0, p1, e1, a, ea, A, U, w, ew;
+  two_prod<Q>(x0, v, p0, e0);
+  two_prod<Q>(x1, v, p1, e1);
+  two_sum<Q>(e0, p1, a, ea);
+  fast_two_sum<Q>(p0, a, A, U);  // S = A + U + ea + e1
+  two_sum<Q>(ea, e1, w, ew);     // S = A + U + w + ew
+  return finish<Q, true, DIR, CANON>(A, U, w, Q::abs(ew), o0, o1);
+}
+
+// mc_ops.hpp:143-169 ScalingN, nc = 2 -> 2: renorm(scale_raw(x, v)), S = x v.
+// Products are exact when the smaller one, |x1 v| (or |x0 v| when x1 = 0), is
+// at least 2^-100 or zero because a factor is.
+template <class Q>
+G2_HD bool scale(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
+  const T_<Q> xs = x1 == T_<Q>(0) ? x0 : x1;
+  const bool ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(xs, v)) | (xs == T_<Q>(0)) | (v == T_<Q>(0)));
+  return scale_core<Q, false, true>(x0, x1, v, o0, o1) & ok & Q::finite(o0);
+}
+
+// mc_ops.hpp:256-282 Square-MCN, nc = 2: terms x0^2 (p, e), 2 x0 x1 (2p', 2e'),
+// fl(x1^2).  x compressed => |e + 2p'| <= 2^-22 |p| (fast sum).
+template <class Q>
+G2_HD bool square(T_<Q> x0, T_<Q> x1, T_<Q>& o0, T_<Q>& o1) {
+  T_<Q> p, e, pp, ep, a, ea, A, U, w, ew, w2, ew2;
+  two_prod<Q>(x0, x0, p, e);
+  two_prod<Q>(x0, x1, pp, ep);
+  const T_<Q> g = Q::mul(x1, x1);
+  pp = Q::add(pp, pp);  // exact doubling (mc_ops.hpp:270); overflow -> non-finite -> declined
+  ep = Q::add(ep, ep);
+  two_sum<Q>(e, pp, a, ea);
+  fast_two_sum<Q>(p, a, A, U);  // S = A + U + ea + 2e' + g
+  two_sum<Q>(ep, g, w, ew);
+  two_sum<Q>(ea, w, w2, ew2);   // S = A + U + w2 + ew2 + ew
+  const T_<Q> xs = x1 == T_<Q>(0) ? x0 : x1;
+  const bool ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(x0, xs)) | (x0 == T_<Q>(0)));
+  return finish<Q, true, false, true>(A, U, w2, Q::add(Q::abs(ew2), Q::abs(ew)), o0, o1) & ok &
+         Q::finite(o0);
+}
+
+// add_kernel(r, sc) -> 2 for the division step: D = r0 + sc0 is exact
+// (Sterbenz: sc0 = -RN(q (y0 + y1)) with q = RN(r0 / y0), so |sc0| is within
+// (1 +- 2^-24)^3 of |r0|), S = D + r1 + sc1.
+template <class Q>
+G2_HD bool add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
+  T_<Q> a, ea, A, U, V, eV, A2, V2;
+  two_sum<Q>(r1, s1, a, ea);
+  two_sum<Q>(D, a, A, U);      // S = A + U + ea
+  two_sum<Q>(U, ea, V, eV);    // S = A + V + eV
+  two_sum<Q>(A, V, A2, V2);    // S = A2 + V2 + eV  (A2 = RN(A + V))
+  return finish<Q, false, false, false>(A2, V2, eV, T_<Q>(0), o0, o1);
+}
+
+// mc_ops.hpp:188-207 div_kernel, nc = 2 (x, y compressed pairs).  Underflow
+// guard: every product is q_d y_j with |q_1| < |q_0| and |y1| < |y0|, so the
+// smallest nonzero one is the last nonzero digit times the last nonzero
+// divisor component; it must be >= 2^-100, and a nonzero digit >= 2^-100
+// (normal with margin: the Sterbenz step relies on its relative rounding).
+template <class Q>
+G2_HD bool div(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
+  // digit 0
+  const T_<Q> q0 = Q::div(x0, y0);
+  T_<Q> s0, s1, r0, r1;
+  bool ok = scale_core<Q, true, false>(y0, y1, -q0, s0, s1);
+  ok &= add_step<Q>(Q::add(x0, s0), x1, s1, r0, r1);
+  // digit 1
+  const T_<Q> q1 = Q::div(r0, y0);
+  ok &= scale_core<Q, true, false>(y0, y1, -q1, s0, s1);
+  ok &= add_step<Q>(Q::add(r0, s0), r1, s1, r0, r1);
+  // guard digit, then renorm(q0, q1, q2 -> 2)
+  const T_<Q> q2 = Q::div(r0, y0);
+  T_<Q> a, ea, A, U;
+  two_sum<Q>(q1, q2, a, ea);
+  two_sum<Q>(q0, a, A, U);  // S = A + U + ea
+  ok &= finish<Q, false, false, true>(A, U, ea, T_<Q>(0), o0, o1);
+  const T_<Q> ql = q1 == T_<Q>(0) ? q0 : q1, yl = y1 == T_<Q>(0) ? y0 : y1;
+  ok &= compressed<Q>(x0, x1) & compressed<Q>(y0, y1) & (Q::big(ql) | (q0 == T_<Q>(0))) &
+        (Q::big(Q::mul(ql, yl)) | (q0 == T_<Q>(0)));
+  return ok & Q::finite(o0);
+}
+
+// mc_ops.hpp:216-230 Mul-MCN (fast): x / (1 / y), zero fast path
+template <class Q>
+G2_HD bool mul(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
+  if (Q::add(y1, y0) == T_<Q>(0) || Q::add(x1, x0) == T_<Q>(0)) {
+    o0 = T_<Q>(0);
+    o1 = T_<Q>(0);
+    return true;
+  }
+  T_<Q> c0, c1;
+  bool ok = div<Q>(T_<Q>(1), T_<Q>(0), y0, y1, c0, c1);
+  ok &= div<Q>(x0, x1, c0, c1, o0, o1);
+  return ok;
+}
+
+#if defined(__CUDACC__)
+// binary32 on sm_100a: native round-to-nearest intrinsics (never contracted),
+// no FTZ (the library builds with -ftz=false)
+struct QF32 {
+  using T = float;
+  __device__ __forceinline__ static T add(T a, T b) { return __fadd_rn(a, b); }
+  __device__ __forceinline__ static T sub(T a, T b) { return __fsub_rn(a, b); }
+  __device__ __forceinline__ static T mul(T a, T b) { return __fmul_rn(a, b); }
+  __device__ __forceinline__ static T div(T a, T b) { return __fdiv_rn(a, b); }
+  __device__ __forceinline__ static T fma(T a, T b, T c) { return __fmaf_rn(a, b, c); }
+  __device__ __forceinline__ static T abs(T a) { return fabsf(a); }
+  __device__ __forceinline__ static bool finite(T a) { return isfinite(a); }
+  __device__ __forceinline__ static bool big(T a) { return fabsf(a) >= 0x1p-100f; }
+  __device__ __forceinline__ static T canon(T a) { return __fadd_rn(a, 0.0f); }
+  // 2^floor(log2 RN(|t| f)) 2^-24 with f = 1 - 2^-24, which drops a power of
+  // two into the binade below: ulp(t)/2, or ulp(t)/4 at a power of two (the
+  // gap below); 0 for zero and subnormal t
+  __device__ __forceinline__ static T hb(T t) {
+    const float u = __fmul_rn(fabsf(t), 1.0f - 0x1p-24f);
+    return __fmul_rn(__uint_as_float(__float_as_uint(u) & 0x7f800000u), 0x1p-24f);
+  }
+  // the same toward d's side: f = 1 when d has t's sign (the gap above)
+  __device__ __forceinline__ static T hbd(T t, T d) {
+    const bool away = (int)(__float_as_uint(d) ^ __float_as_uint(t)) >= 0;
+    const float u = __fmul_rn(fabsf(t), away ? 1.0f : 1.0f - 0x1p-24f);
+    return __fmul_rn(__uint_as_float(__float_as_uint(u) & 0x7f800000u), 0x1p-24f);
+  }
+  __device__ __forceinline__ static T shrink(T h) { return __fmul_rn(h, 1.0f - 0x1p-22f); }
+};
+
+// fl_exp<B32>(x1) = RN32(exp(x1)) for a small second component (|x1| <= 2^-12):
+// exp(x1) - 1 from a degree-4 polynomial in binary64 (truncation <= 2^-67,
+// evaluation ~2^-64 absolute), then RN32, accepted only when 1 + p is farther
+// than 2^-50 from a binary32 midpoint (the double rounding through binary64
+// and the approximation then cannot change the result).
+__device__ __forceinline__ bool exp_small_b32(float x1, float& f) {
+  const double d = (double)x1;
+  double p = __fma_rn(d, 1.0 / 24.0, 1.0 / 6.0);
+  p = __fma_rn(d, p, 0.5);
+  p = __fma_rn(__dmul_rn(d, d), p, d);
+  const double s = __dadd_rn(1.0, p);
+  f = __double2float_rn(s);
+  const double h = s >= 1.0 ? 0x1p-24 : 0x1p-25;  // half the binary32 spacing at f
+  return (fabsf(x1) <= 0x1p-12f) & (fabs(__dsub_rn(s, (double)f)) < h - 0x1p-50);
+}
+
+// mc_ops.hpp:303-313 Exp-MCN, nc = 2: expansion_of_double(exp(x0)) (exact
+// greedy split of the correctly rounded binary64 exp, mcf_exp.cuh), then for
+// x1 != 0 scale_kernel(out, fl_exp(x1)) through the certified scale.
+__device__ __forceinline__ bool exp_b32(float x0, float x1, float& o0, float& o1) {
+  const double E = cr_exp((double)x0);
+  const float e0 = __double2float_rn(E);
+  const float e1 = __double2float_rn(__dsub_rn(E, (double)e0));
+  if (x1 == 0.0f) {
+    o0 = e0;
+    o1 = e1;
+    return isfinite(e0);
+  }
+  float f;
+  bool ok = exp_small_b32(x1, f);
+  ok &= scale<QF32>(e0, e1, f, o0, o1);
+  return ok;
+}
+#endif
+
+}  // namespace g2
+}  // namespace mcfg

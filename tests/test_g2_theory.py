@@ -1,0 +1,61 @@
+"""CPU check of the certified binary32 nc=2 tier (csrc/mcf_g2.cuh).
+
+tools/g2_verify.cpp runs the SAME header on an emulated binary format with p
+significand bits and compares it with the reference's algorithms restated in
+that format (renorm_kernel with its pass cap, scale_raw, add_kernel,
+div_kernel, mul_fast_kernel, square_kernel; mc_ops.hpp:41-282):
+
+* exhaustively over every compressed operand pair in an exponent window for
+  small p, where every rounding boundary, tie and power of two is hit;
+* on sampled config-0 operands at p = 24.
+
+Required: no accepted case differs from the reference bit for bit, and the
+reference never ends a renormalization at its pass cap (the certification
+argument assumes it ends compressed).  At p = 24 the shortcut must accept
+essentially every config-0 element (it is the fast path).
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def g2v(tmp_path_factory):
+    exe = str(tmp_path_factory.mktemp("g2") / "g2v")
+    src = os.path.join(ROOT, "tools", "g2_verify.cpp")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fopenmp", src, "-o", exe], check=True)
+    return exe
+
+
+def _run(exe, *args):
+    r = subprocess.run([exe, *map(str, args)], capture_output=True, text=True, timeout=600)
+    rows = {}
+    for line in r.stdout.splitlines():
+        m = re.match(r"p=\s*(\d+) (\w+)\s+cases\s+(\d+)\s+accepted\s+([\d.]+)%\s+mismatches (\d+)\s+cap-hits (\d+)", line)
+        if m:
+            rows[m.group(2)] = dict(cases=int(m.group(3)), acc=float(m.group(4)), bad=int(m.group(5)),
+                                    cap=int(m.group(6)))
+    assert set(rows) == {"scale", "square", "div", "mul"}, r.stdout + r.stderr
+    return rows, r.returncode
+
+
+@pytest.mark.parametrize("p,k", [(4, 5), (5, 3)])
+def test_exhaustive_small_precision(g2v, p, k):
+    rows, rc = _run(g2v, "small", p, k)
+    for op, r in rows.items():
+        assert r["bad"] == 0, (op, r)
+        assert r["cap"] == 0, (op, r)
+        assert r["cases"] > 0 and r["acc"] > 0, (op, r)
+    assert rc == 0
+
+
+def test_sampled_binary32(g2v):
+    rows, rc = _run(g2v, "sample", 24, 300000)
+    for op, r in rows.items():
+        assert r["bad"] == 0 and r["cap"] == 0, (op, r)
+        assert r["acc"] > 99.99, (op, r)
+    assert rc == 0

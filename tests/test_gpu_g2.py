@@ -1,0 +1,72 @@
+"""The certified binary32 nc=2 tier (csrc/mcf_g2.cuh) under inputs built to sit
+on its margins: exact quotients and reciprocals (remainders exactly zero),
+half-ulp ties in the second component, powers of two (where the gap below is
+half the gap above), products near the 2^-100 underflow guard and near
+overflow, zero second components, mixed with config-0 values.  Every element
+must be bit-identical to the oracle whether the shortcut accepts it or the
+register / literal path takes over.
+"""
+import numpy as np
+import pytest
+
+from mcgen import assert_bits, config_values, split
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gr():
+    import gpu_util
+
+    return gpu_util
+
+
+def _pairs(rng, n, lo=-8, hi=8):
+    """compressed binary32 pairs of several kinds, shuffled together"""
+    k = n // 8
+    out = []
+    out.append(split(config_values(rng, k, lo, hi), 2, np.float32))  # generic
+    ints = rng.integers(1, 1 << 12, k) * rng.choice([-1.0, 1.0], k) * np.exp2(rng.integers(-6, 7, k))
+    out.append(split(ints, 2, np.float32))  # short significands: exact products / quotients
+    p2 = rng.choice([-1.0, 1.0], k) * np.exp2(rng.integers(-20, 21, k).astype(np.float64))
+    out.append(split(p2, 2, np.float32))  # powers of two
+    # second component exactly half an ulp of an even leading component (a tie)
+    c0 = config_values(rng, k, lo, hi).astype(np.float32)
+    c0 = (c0.view(np.uint32) & np.uint32(0xFFFFFFFE)).view(np.float32)
+    ulp = np.spacing(np.abs(c0)).astype(np.float64)
+    t = np.stack([c0, (rng.choice([-0.5, 0.5], k) * ulp).astype(np.float32)], -1)
+    out.append(t)
+    # powers of two with a second component toward zero (gap below is halved)
+    c0 = (rng.choice([-1.0, 1.0], k) * np.exp2(rng.integers(-8, 9, k).astype(np.float64))).astype(np.float32)
+    c1 = (-np.sign(c0) * np.spacing(np.abs(c0)) * rng.uniform(0.05, 0.25, k)).astype(np.float32)
+    out.append(np.stack([c0, c1], -1))
+    out.append(split(config_values(rng, k, -52, -45), 2, np.float32))  # products near 2^-100
+    out.append(split(config_values(rng, k, 58, 66), 2, np.float32))  # products near overflow
+    z = split(config_values(rng, n - 7 * k, lo, hi), 2, np.float32)
+    z[:, 1] = 0
+    out.append(z)
+    a = np.concatenate(out)
+    return a[rng.permutation(a.shape[0])]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_g2_ops_bitwise_on_margins(gr, port, seed):
+    rng = np.random.default_rng(900 + seed)
+    n = 1 << 17
+    x = _pairs(rng, n)
+    y = _pairs(rng, n)
+    ok = np.abs(y[:, 0]) > 0
+    y = y[ok]
+    x = x[: y.shape[0]]
+    v = x[rng.permutation(x.shape[0]), 0].copy()
+    assert_bits(gr.run("scaling_n", x, v), port.scaling_n(x, v), "scaling_n")
+    assert_bits(gr.run("square_mcn", x), port.square_mcn(x), "square_mcn")
+    assert_bits(gr.run("div_n", v, y), port.div_n(v, y), "div_n")
+    assert_bits(gr.run("div_mcn", x, y), port.div_mcn(x, y), "div_mcn")
+    assert_bits(gr.run("mul_mcn", x, y), port.mul_mcn(x, y), "mul_mcn")
+    # exact quotients: x = k * y with short k, and reciprocals of powers of two
+    kk = split(rng.integers(1, 64, y.shape[0]).astype(np.float64), 2, np.float32)
+    xy = gr.run("mul_mcn_slow", kk, y)
+    assert_bits(gr.run("div_mcn", xy, y), port.div_mcn(xy, y), "div_mcn exact quotients")
+    one = np.ones(y.shape[0], np.float32)
+    assert_bits(gr.run("div_n", one, y), port.div_n(one, y), "div_n reciprocals")
