@@ -127,6 +127,32 @@ static __device__ __noinline__ double slow(double x) {
 
 }  // namespace expd
 
+// RN(ln2/2048 - kL1) to 53 bits: k * kL2F rounds once inside an fma
+constexpr double kL2F = 0x1.d1cf79abc9e3bp-43;
+
+// RN64(exp(x)) from a short evaluation (~2^-63.9 relative: reduction rounding
+// 2^-65.5, degree-4 truncation 2^-69, evaluation 2^-66, table product 2^-66,
+// dropped tl * p 2^-65.5) with no retry: returns false when the value could
+// lie within 2^-61 of a binary64 midpoint (about 2^-8 of arguments) or
+// |x| > 704; the caller then takes the correctly rounded path below.
+__device__ __forceinline__ bool rn_exp_fast(double x, double& E) {
+  using namespace expd;
+  const double kd = rint(__dmul_rn(x, kInvL));
+  const int k = (int)kd;
+  const double rh = __fma_rn(-kd, kL1, x);  // exact
+  const double r = __fma_rn(-kd, kL2F, rh);
+  double p = __fma_rn(r, 1.0 / 24.0, 1.0 / 6.0);
+  p = __fma_rn(r, p, 0.5);
+  p = __fma_rn(__dmul_rn(r, r), p, r);  // exp(r) - 1
+  const int j = k & 2047;
+  const int m = (k - j) >> 11;
+  const double2 t = g_exp_tab[j];
+  double yh, yl;
+  fast2(t.x, __fma_rn(t.x, p, t.y), yh, yl);
+  E = __dmul_rn(yh, __longlong_as_double((long long)(m + 1023) << 52));
+  return (fabs(x) <= 704.0) && !near_midpoint(yh, yl, 0x1p-61);
+}
+
 __device__ __forceinline__ double cr_exp(double x) {
   using namespace expd;
   if (!(fabs(x) <= 704.0)) {

@@ -265,10 +265,12 @@ __device__ __forceinline__ bool exp_small_b32(float x1, float& f) {
 }
 
 // mc_ops.hpp:303-313 Exp-MCN, nc = 2: expansion_of_double(exp(x0)) (exact
-// greedy split of the correctly rounded binary64 exp, mcf_exp.cuh), then for
+// greedy split of the correctly rounded binary64 exp: the short evaluation
+// of mcf_exp.cuh, certified away from binary64 midpoints), then for
 // x1 != 0 scale_kernel(out, fl_exp(x1)) through the certified scale.
 __device__ __forceinline__ bool exp_b32(float x0, float x1, float& o0, float& o1) {
-  const double E = cr_exp((double)x0);
+  double E;
+  if (!rn_exp_fast((double)x0, E)) return false;  // near a binary64 midpoint: register path (cr_exp)
   const float e0 = __double2float_rn(E);
   const float e1 = __double2float_rn(__dsub_rn(E, (double)e0));
   if (x1 == 0.0f) {
