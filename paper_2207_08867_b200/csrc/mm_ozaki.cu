@@ -356,6 +356,20 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
     // exact integer per column, convert -- few live registers, so many rows
     // of loads stay in flight
     double g[3][4];
+    if (nkc == 1) {
+      // one K chunk (K <= 14400, config 2): all nine planes' loads in flight at once
+      int4 v[kS];
+#pragma unroll
+      for (int q = 0; q < kS; ++q) v[q] = __ldcs(reinterpret_cast<const int4*>(cq + q * plane + off));
+#pragma unroll
+      for (int w = 0; w < 3; ++w) {
+        const int4 a = v[3 * w], b = v[3 * w + 1], c = v[3 * w + 2];
+        g[w][0] = (double)(((long long)a.x * 256 + b.x) * 256 + c.x);
+        g[w][1] = (double)(((long long)a.y * 256 + b.y) * 256 + c.y);
+        g[w][2] = (double)(((long long)a.z * 256 + b.z) * 256 + c.z);
+        g[w][3] = (double)(((long long)a.w * 256 + b.w) * 256 + c.w);
+      }
+    } else
 #pragma unroll
     for (int w = 0; w < 3; ++w) {
       long long gv[4] = {0, 0, 0, 0};
@@ -414,13 +428,18 @@ __global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int
   }
 }
 
-// the listed outputs: a CTA per row, a warp per listed output.  The CTA
-// stages its row of A in shared memory (SMEM; rows too long for it read A
-// through L1), each lane streams its k's of the column with eight loads in
-// flight.  Products of binary32 components are exact in binary64; each lane
-// keeps eight double-doubles (k = lane + 32 (8 r + u) goes to accumulator u:
-// two_sum into S, errors into C), merged in a fixed order and then across the
-// lanes by an xor butterfly (the same value on every lane): deterministic.
+// the listed outputs: a CTA per row.  The CTA stages its row of A in shared
+// memory (SMEM; rows too long for it read A through L1).  A row lists few
+// outputs (config 2: 3.6 on average), so each listed output's k range is cut
+// into G segments (G a power of two with cnt G <= 8 warps; G = 1 when the row
+// lists 5 or more) and every warp takes one (output, segment) item: more
+// loads in flight per SM, which is what bounds this latency-bound kernel.
+// Each lane streams its k's of the column with eight loads in flight.
+// Products of binary32 components are exact in binary64; each lane keeps
+// eight double-doubles (k = lane + 32 (8 r + u) goes to accumulator u: two_sum
+// into S, errors into C), merged in a fixed order, across the lanes by an xor
+// butterfly, and across the segments in segment order through shared memory:
+// deterministic (G depends only on the row's own list).
 template <int NCA, int NCB, bool SMEM>
 __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, const float* __restrict__ bt,
                                                   int64_t n, int64_t k, const int* __restrict__ rlist,
@@ -428,6 +447,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
                                                   const int* __restrict__ cnf, float* __restrict__ out,
                                                   int64_t ldo, Epilogue ep) {
   extern __shared__ __align__(16) float arow[];
+  __shared__ double2 part[8][8];
   const int64_t i = blockIdx.x;
   const int cnt = rcnt[i];
   if (cnt == 0) return;
@@ -460,26 +480,63 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
   // two_prod per k instead of a two_sum per component product
   const bool rpair = NCA == 2 && !(rnf[i] & 2);
   constexpr int U = 8;
-  for (int w = warp; w < cnt; w += nw) {
-    const int64_t j = rlist[i * n + w];
+  // segments per output: cnt * G <= nw (nw = 8), k split on 32 U boundaries
+  const int G = cnt >= 5 ? 1 : cnt >= 3 ? 2 : cnt == 2 ? 4 : 8;
+  const int64_t seg = ((k + G - 1) / G + 32 * U - 1) / (32 * U) * (32 * U);
+  for (int w = warp; w < cnt * G; w += nw) {
+    const int o = w / G, g = w - o * G;
+    const int64_t j = rlist[i * n + o];
     const float* br = bt + j * k * NCB;
     // every c0 + c1 of the row (and of the column, for an MC B) one binary64:
     // one two_prod per k (exact: <= 53 x 53 bits) instead of a two_sum per
     // component product
     const bool pair = rpair && (NCB == 1 || !(cnf[j] & 2));
+    const int64_t kb = g * seg, ke = k < kb + seg ? k : kb + seg;
     double S8[U], C8[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) S8[u] = C8[u] = 0.0;
-    for (int64_t t0 = lane; t0 < k; t0 += 32 * U) {
+    // binary32 B, pair rows, 16-byte aligned column with k % 4 == 0: four k
+    // per lane per load (k = 4 lane + 128 (8 r + u) + q -> accumulator u), so
+    // a warp keeps 4 KiB of B in flight
+    const bool vec = NCB == 1 && NCA == 2 && SMEM && pair && (k & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(br) & 15) == 0;
+    if (vec) {
+      for (int64_t t0 = kb + 4 * lane; t0 < ke; t0 += 128 * U) {
+        float4 bq[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          bq[u] = t0 + 128 * u < ke ? __ldg(reinterpret_cast<const float4*>(br + t0 + 128 * u))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t t = t0 + 128 * u;
+          if (t >= ke) break;
+          const float4 a01 = *reinterpret_cast<const float4*>(ar + t * 2);
+          const float4 a23 = *reinterpret_cast<const float4*>(ar + t * 2 + 4);
+          const float av[8] = {a01.x, a01.y, a01.z, a01.w, a23.x, a23.y, a23.z, a23.w};
+          const float bvq[4] = {bq[u].x, bq[u].y, bq[u].z, bq[u].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double v = __dadd_rn((double)av[2 * q], (double)av[2 * q + 1]);  // exact
+            const double bb = (double)bvq[q];
+            const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);
+            double e;
+            dsum(S8[u], p, S8[u], e);
+            C8[u] = __dadd_rn(C8[u], __dadd_rn(e, pe));
+          }
+        }
+      }
+    }
+    for (int64_t t0 = kb + lane; !vec && t0 < ke; t0 += 32 * U) {
       float bv[U][NCB];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int cb = 0; cb < NCB; ++cb) bv[u][cb] = t0 + 32 * u < k ? br[(t0 + 32 * u) * NCB + cb] : 0.0f;
+        for (int cb = 0; cb < NCB; ++cb) bv[u][cb] = t0 + 32 * u < ke ? br[(t0 + 32 * u) * NCB + cb] : 0.0f;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t t = t0 + 32 * u;
-        if (t >= k) break;
+        if (t >= ke) break;
         if (pair) {
           const double v = __dadd_rn((double)ar[t * 2], (double)ar[t * 2 + 1]);  // exact
           const double bb = NCB == 1 ? (double)bv[u][0] : __dadd_rn((double)bv[u][0], (double)bv[u][NCB - 1]);
@@ -514,9 +571,27 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
       dsum(S, oS, S, e);
       C = __dadd_rn(__dadd_rn(C, oC), e);
     }
-    if (lane == 0) {
+    if (G == 1) {
+      if (lane == 0) {
+        const double v[2] = {S, C};
+        emit(v, i, j, out, ldo, ep);
+      }
+    } else if (lane == 0) {
+      part[o][g] = make_double2(S, C);
+    }
+  }
+  if (G > 1) {
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const int o = threadIdx.x;
+      double S = part[o][0].x, C = part[o][0].y;
+      for (int g = 1; g < G; ++g) {
+        double e;
+        dsum(S, part[o][g].x, S, e);
+        C = __dadd_rn(__dadd_rn(C, part[o][g].y), e);
+      }
       const double v[2] = {S, C};
-      emit(v, i, j, out, ldo, ep);
+      emit(v, i, rlist[i * n + o], out, ldo, ep);
     }
   }
 }
