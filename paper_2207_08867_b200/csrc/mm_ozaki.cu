@@ -779,7 +779,7 @@ int diagonals(int64_t k) { return k > 8192 ? kQmax : kS; }
 
 std::size_t rows_bytes(int64_t m, int64_t k, int64_t n) {
   const KGeo g = kgeo(k);
-  return al(m * g.row_bytes()) + al((int64_t)kQmax * g.nkc * m * pad16(n) * 4) + al(m * n * 4) + al(m * 4) * 3;
+  return al(m * g.row_bytes()) + al((int64_t)kQmax * g.nkc * m * pad16(n) * 4) + al(m * pad16(n) * 4) + al(m * 4) * 3;
 }
 
 // error bound per product, units of 2^-72: A's truncation (2^-73), B's (2^-73
@@ -793,38 +793,76 @@ double per_product_bound(int sb, int nq) {
   return e * 1.01;
 }
 
+// workspace layout of one row block (see rows_bytes)
+struct RowsWs {
+  int8_t* planes;
+  int* cq;
+  int* rlist;
+  int* ea;
+  int* rnf;
+  int* rcnt;
+};
+RowsWs rows_ws(char* buf, int64_t m, const KGeo& g, int64_t np) {
+  RowsWs w;
+  w.planes = reinterpret_cast<int8_t*>(buf);
+  buf += al(m * g.row_bytes());
+  w.cq = reinterpret_cast<int*>(buf);
+  buf += al((int64_t)kQmax * g.nkc * m * np * 4);
+  w.rlist = reinterpret_cast<int*>(buf);
+  buf += al(m * (np > 0 ? np : 1) * 4);
+  w.ea = reinterpret_cast<int*>(buf);
+  buf += al(m * 4);
+  w.rnf = reinterpret_cast<int*>(buf);
+  buf += al(m * 4);
+  w.rcnt = reinterpret_cast<int*>(buf);
+  return w;
+}
+
+// A's row exponents and digit planes (independent of B: may run concurrently
+// with prepare_b on another stream)
+mcf_status a_digits(const float* x, int nca, int64_t m, const KGeo& g, const RowsWs& w, cudaStream_t s) {
+  if (cudaMemsetAsync(w.rcnt, 0, m * sizeof(int), s) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counters");
+  const int64_t k = g.k;
+  const unsigned gr = (unsigned)((m + 7) / 8);
+  if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, w.ea, w.rnf);
+  else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, w.ea, w.rnf);
+  const int64_t gx = (g.kc * g.nkc / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
+  const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
+  if (nca == 2) k_slice_rows<2><<<gsl, 256, 0, s>>>(x, m, g, w.ea, w.planes);
+  else k_slice_rows<1><<<gsl, 256, 0, s>>>(x, m, g, w.ea, w.planes);
+  mcfr::note_launch();
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_fast A digit kernels");
+}
+
+mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo,
+                         const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep);
+
 // out (m x n x 2 binary32, row stride ldo elements) = A (m x k x nca) . B for
 // a prepared B.  ev (optional, 4 events): recorded before the A digits,
 // before the GEMMs, after the GEMMs and at the end (phase timing).
 mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo, char* buf,
                 cudaStream_t s, cudaEvent_t* ev = nullptr, const Epilogue& ep = Epilogue{}) {
+  const RowsWs w = rows_ws(buf, m, pb.g, pb.np);
+  if (ev) cudaEventRecord(ev[0], s);
+  const mcf_status st = a_digits(x, nca, m, pb.g, w, s);
+  if (st != MCF_OK) return st;
+  return rows_products(x, nca, m, pb, out, ldo, w, s, ev, ep);
+}
+
+// the GEMMs, recombination and fallback of a row block whose A digits are done
+mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo,
+                         const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep) {
   const KGeo g = pb.g;
   const int64_t k = g.k, n = pb.n, np = pb.np;
-  int8_t* planes = reinterpret_cast<int8_t*>(buf);
-  buf += al(m * g.row_bytes());
-  int* cq = reinterpret_cast<int*>(buf);
-  buf += al((int64_t)kQmax * g.nkc * m * np * 4);
-  int* rlist = reinterpret_cast<int*>(buf);
-  buf += al(m * n * 4);
-  int* ea = reinterpret_cast<int*>(buf);
-  buf += al(m * 4);
-  int* rnf = reinterpret_cast<int*>(buf);
-  buf += al(m * 4);
-  int* rcnt = reinterpret_cast<int*>(buf);
-  if (ev) cudaEventRecord(ev[0], s);
-  if (cudaMemsetAsync(rcnt, 0, m * sizeof(int), s) != cudaSuccess)
-    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counters");
-  const unsigned gr = (unsigned)((m + 7) / 8);
-  if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, ea, rnf);
-  else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, ea, rnf);
-  const int64_t gx = (g.kc * g.nkc / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
-  const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
-  if (nca == 2) k_slice_rows<2><<<gsl, 256, 0, s>>>(x, m, g, ea, planes);
-  else k_slice_rows<1><<<gsl, 256, 0, s>>>(x, m, g, ea, planes);
-  mcfr::note_launch();
-  mcfr::note_launch();
-  mcf_status st = mcfr::check_launch("mm_fast A digit kernels");
-  if (st != MCF_OK) return st;
+  int8_t* planes = w.planes;
+  int* cq = w.cq;
+  int* rlist = w.rlist;
+  int* ea = w.ea;
+  int* rnf = w.rnf;
+  int* rcnt = w.rcnt;
+  mcf_status st = MCF_OK;
   // chunk c, diagonal q: the pairs (s, t = q - s) with t <= sb - 1.  A planes
   // q - th .. q of the chunk (contiguous, ascending s) against B planes th ..
   // 0 (stored in reverse order, so also contiguous); C_cq is an np x m
@@ -899,8 +937,26 @@ mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m,
   char* ws = oz_workspace(bb + parts * al(rb), s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
   PreparedB pb;
+  if (parts == 1) {
+    // A's digits on a side stream while B is prepared on the caller's
+    const RowsWs rw = rows_ws(ws + bb, m, kgeo(k), pad16(n));
+    cudaStream_t as = side_stream(12);
+    cudaEvent_t fork = nullptr, adone = nullptr;
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&adone, cudaEventDisableTiming);
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(as, fork, 0);
+    mcf_status st = a_digits(x, nca, m, kgeo(k), rw, as);
+    cudaEventRecord(adone, as);
+    if (st == MCF_OK) st = prepare_b(w, ncb, k, n, n, ws, pb, s);
+    cudaStreamWaitEvent(s, adone, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(adone);
+    if (st != MCF_OK) return st;
+    return rows_products(x, nca, m, pb, out, n, rw, s, nullptr, Epilogue{});
+  }
   mcf_status st = prepare_b(w, ncb, k, n, n, ws, pb, s);
-  if (st != MCF_OK || parts == 1) return st != MCF_OK ? st : rows(x, nca, m, pb, out, n, ws + bb, s);
+  if (st != MCF_OK) return st;
   // row parts on the caller's stream and side streams (forked and joined by
   // events): one part's recombination / fallback overlaps the next part's
   // GEMMs, whose last wave leaves SMs idle
@@ -984,8 +1040,7 @@ mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, in
     }
     // the per-row fallback counters sit at the end of the rows region
     const KGeo g = kgeo(k);
-    const char* cnt = ws + bb + al(m * g.row_bytes()) + al((int64_t)kQmax * g.nkc * m * pad16(n) * 4) +
-                      al(m * n * 4) + al(m * 4) * 2;
+    const char* cnt = reinterpret_cast<const char*>(rows_ws(ws + bb, m, g, pad16(n)).rcnt);
     std::vector<int> rc(m);
     cudaMemcpy(rc.data(), cnt, m * sizeof(int), cudaMemcpyDeviceToHost);
     int64_t c = 0;
