@@ -100,29 +100,34 @@ G2_HD bool prod_ok(T_<Q> p, T_<Q> a, T_<Q> b) {
 // division's partial products q (y0 + y1) ~ r0, e.g. 1 / y); CANON: final
 // output (a zero component is the reference's +0 padding).
 // The all-zero case passes through the tie clauses (h = 0 for a zero lead).
-template <class Q, bool REST, bool DIR, bool CANON>
+// TIE0 = false drops the top-level tie clause where exact midpoints are rare
+// (an exact tie there then takes the fallback).  B is usually much larger than
+// R0, so (C1, F) comes from a fast two-sum guarded by |B| >= |R0|.
+template <class Q, bool REST, bool DIR, bool CANON, bool TIE0 = true>
 G2_HD bool finish(T_<Q> A, T_<Q> B, T_<Q> R0, T_<Q> rest_abs, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> C1, F;
-  two_sum<Q>(B, R0, C1, F);
+  fast_two_sum<Q>(B, R0, C1, F);
+  const bool ord = Q::abs(B) >= Q::abs(R0);
   // tie at the top: fl(A + C1) is the even neighbour; otherwise it is A
-  const T_<Q> A2 = Q::add(A, C1);
-  const T_<Q> C2 = A2 == A ? C1 : -C1;
+  const T_<Q> A2 = TIE0 ? Q::add(A, C1) : A;
+  const T_<Q> C2 = !TIE0 || A2 == A ? C1 : -C1;
   const T_<Q> below = REST ? Q::add(Q::abs(F), rest_abs) : Q::abs(F);
   // half gaps: toward C2 at the top (S - A2 has C2's sign) or the smaller
   // one, and the smaller one below (exact unless C2 is a power of two)
   const T_<Q> h0 = DIR ? Q::hbd(A2, C2) : Q::hb(A2), h1 = Q::hb(C2);
-  const bool ok0 = (Q::abs(C2) < Q::shrink(h0)) | ((below == T_<Q>(0)) & (Q::abs(C2) == h0));
+  const bool ok0 = (Q::abs(C2) < Q::shrink(h0)) | (TIE0 & (below == T_<Q>(0)) & (Q::abs(C2) == h0)) |
+                   (!TIE0 & (A2 == T_<Q>(0)) & (C2 == T_<Q>(0)) & (below == T_<Q>(0)));
   const bool tie1 = REST ? (rest_abs == T_<Q>(0)) & (below == h1) : (below == h1);
   const bool ok1 = (below < Q::shrink(h1)) | tie1;
   o0 = CANON ? Q::canon(A2) : A2;
   o1 = CANON ? Q::canon(C2) : C2;
-  return ok0 & ok1;
+  return ok0 & ok1 & ord;
 }
 
 // exact product x v (x a compressed pair, underflow guarded by the caller)
 // rounded to two components: S = A + U + w + ew after the sweep below.
 // |fl(e0 + p1)| <= 2^-22 |p0| (x compressed), so the top sum is a fast one.
-template <class Q, bool DIR, bool CANON>
+template <class Q, bool DIR, bool CANON, bool TIE0 = true>
 G2_HD bool scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> p0, e0, p1, e1, a, ea, A, U, w, ew;
   two_prod<Q>(x0, v, p0, e0);
@@ -130,7 +135,7 @@ G2_HD bool scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
   two_sum<Q>(e0, p1, a, ea);
   fast_two_sum<Q>(p0, a, A, U);  // S = A + U + ea + e1
   two_sum<Q>(ea, e1, w, ew);     // S = A + U + w + ew
-  return finish<Q, true, DIR, CANON>(A, U, w, Q::abs(ew), o0, o1);
+  return finish<Q, true, DIR, CANON, TIE0>(A, U, w, Q::abs(ew), o0, o1);
 }
 
 // mc_ops.hpp:143-169 ScalingN, nc = 2 -> 2: renorm(scale_raw(x, v)), S = x v.
@@ -172,8 +177,8 @@ G2_HD bool add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
   two_sum<Q>(r1, s1, a, ea);
   two_sum<Q>(D, a, A, U);      // S = A + U + ea
   two_sum<Q>(U, ea, V, eV);    // S = A + V + eV
-  two_sum<Q>(A, V, A2, V2);    // S = A2 + V2 + eV  (A2 = RN(A + V))
-  return finish<Q, false, false, false>(A2, V2, eV, T_<Q>(0), o0, o1);
+  fast_two_sum<Q>(A, V, A2, V2);  // S = A2 + V2 + eV  (A2 = RN(A + V); |A| >= |V| checked)
+  return finish<Q, false, false, false>(A2, V2, eV, T_<Q>(0), o0, o1) & (Q::abs(A) >= Q::abs(V));
 }
 
 // mc_ops.hpp:188-207 div_kernel, nc = 2 (x, y compressed pairs).  Underflow
@@ -186,18 +191,19 @@ G2_HD bool div(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
   // digit 0
   const T_<Q> q0 = Q::div(x0, y0);
   T_<Q> s0, s1, r0, r1;
-  bool ok = scale_core<Q, true, false>(y0, y1, -q0, s0, s1);
+  bool ok = scale_core<Q, true, false, false>(y0, y1, -q0, s0, s1);
   ok &= add_step<Q>(Q::add(x0, s0), x1, s1, r0, r1);
   // digit 1
   const T_<Q> q1 = Q::div(r0, y0);
-  ok &= scale_core<Q, true, false>(y0, y1, -q1, s0, s1);
+  ok &= scale_core<Q, true, false, false>(y0, y1, -q1, s0, s1);
   ok &= add_step<Q>(Q::add(r0, s0), r1, s1, r0, r1);
   // guard digit, then renorm(q0, q1, q2 -> 2)
   const T_<Q> q2 = Q::div(r0, y0);
   T_<Q> a, ea, A, U;
-  two_sum<Q>(q1, q2, a, ea);
-  two_sum<Q>(q0, a, A, U);  // S = A + U + ea
-  ok &= finish<Q, false, false, true>(A, U, ea, T_<Q>(0), o0, o1);
+  fast_two_sum<Q>(q1, q2, a, ea);  // |q2| < |q1| < |q0| (checked)
+  fast_two_sum<Q>(q0, a, A, U);    // S = A + U + ea
+  ok &= finish<Q, false, false, true>(A, U, ea, T_<Q>(0), o0, o1) & (Q::abs(q1) >= Q::abs(q2)) &
+        (Q::abs(q0) >= Q::abs(a));
   const T_<Q> ql = q1 == T_<Q>(0) ? q0 : q1, yl = y1 == T_<Q>(0) ? y0 : y1;
   ok &= compressed<Q>(x0, x1) & compressed<Q>(y0, y1) & (Q::big(ql) | (q0 == T_<Q>(0))) &
         (Q::big(Q::mul(ql, yl)) | (q0 == T_<Q>(0)));
