@@ -129,13 +129,15 @@ G2_HD bool finish(T_<Q> A, T_<Q> B, T_<Q> R0, T_<Q> rest_abs, T_<Q>& o0, T_<Q>& 
 // |fl(e0 + p1)| <= 2^-22 |p0| (x compressed), so the top sum is a fast one.
 template <class Q, bool DIR, bool CANON, bool TIE0 = true>
 G2_HD bool scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
-  T_<Q> p0, e0, p1, e1, a, ea, A, U, w, ew;
+  T_<Q> p0, e0, p1, e1, a, ea, A, U;
   two_prod<Q>(x0, v, p0, e0);
   two_prod<Q>(x1, v, p1, e1);
   two_sum<Q>(e0, p1, a, ea);
   fast_two_sum<Q>(p0, a, A, U);  // S = A + U + ea + e1
-  two_sum<Q>(ea, e1, w, ew);     // S = A + U + w + ew
-  return finish<Q, true, DIR, CANON, TIE0>(A, U, w, Q::abs(ew), o0, o1);
+  // w = fl(ea + e1) (both ~2^-48 |A|) is exact up to |ew| <= 2^-p |w|; that
+  // bound stands in for the exact rest (0 exactly when w == 0: the sum was exact)
+  const T_<Q> w = Q::add(ea, e1);
+  return finish<Q, true, DIR, CANON, TIE0>(A, U, w, Q::ulpb(w), o0, o1);
 }
 
 // mc_ops.hpp:143-169 ScalingN, nc = 2 -> 2: renorm(scale_raw(x, v)), S = x v.
@@ -252,6 +254,8 @@ struct QF32 {
     return __fmul_rn(__uint_as_float(__float_as_uint(u) & 0x7f800000u), 0x1p-24f);
   }
   __device__ __forceinline__ static T shrink(T h) { return __fmul_rn(h, 1.0f - 0x1p-22f); }
+  // bound on the rounding error of a binary32 result w: 2^-24 |w| >= h(w)
+  __device__ __forceinline__ static T ulpb(T w) { return __fmul_rn(fabsf(w), 0x1p-24f); }
 };
 
 // fl_exp<B32>(x1) = RN32(exp(x1)) for a small second component (|x1| <= 2^-12):

@@ -57,6 +57,7 @@ struct QE {
     std::frexp(u, &e);
     return std::ldexp(1.0, e - 1 - P);
   }
+  static T ulpb(T w) { return std::fabs(w) * std::ldexp(1.0, -P); }
   static T shrink(T h) { return rn(h * (1.0 - std::ldexp(1.0, -(P - 2)))); }
 };
 
