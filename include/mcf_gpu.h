@@ -187,6 +187,9 @@ mcf_status mcf_mlp_linear_fwd(const float* w, int nc, const float* a_prev, int64
 mcf_status mcf_mlp_cross_entropy(const float* logits, const int* labels, int64_t classes, int64_t n,
                                  int64_t n_global, float* grad, float* terms, float* term_sum,
                                  mcf_stream stream);
+/* the left-to-right binary32 sum of n loss terms (autodiff.hpp:572), alone:
+ * lets a caller run it on a side stream, off the backward's critical path. */
+mcf_status mcf_mlp_loss_sum(const float* terms, int64_t n, float* term_sum, mcf_stream stream);
 /* C = op(A) op(B) in binary32 with the reduction index increasing, fl_mul then
  * fl_add (matmul2d, ndarray.hpp:147-165); relu_mask (optional, C's shape)
  * zeroes entries whose mask <= 0 (ReLU backward) [mc_linear_op backward,

@@ -73,6 +73,7 @@ _SIGS = {
     "mcf_probe_pipe_rates": [_p, _p],
     "mcf_mlp_bias_act": [_p, _int, _p, _i64, _i64, _int, _p, _p, _p],
     "mcf_mlp_cross_entropy": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
+    "mcf_mlp_loss_sum": [_p, _i64, _p, _p],
     "mcf_gemm_f32_ordered": [_int, _int, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _p],
     "mcf_rowsum_f32_ordered": [_p, _i64, _i64, _p, _p],
     "mcf_gemm_f32_fast": [_int, _int, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _p, _p],

@@ -61,6 +61,9 @@ bool ozaki_supported(int64_t m, int64_t k, int64_t n);
 mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n, float* out,
                     cudaStream_t s);
 int ozaki_digits();
+// binary32 GEMM through four-digit int8 products (plan FAST's MLP backward)
+mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                       int64_t ldc, int64_t m, int64_t n, int64_t k, const float* mask, cudaStream_t s);
 mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t k, int64_t n, const float* bias,
                              int relu, float* h, float* act, cudaStream_t s);
 int ozaki_gemm_equivalents(int ncb, int64_t k);

@@ -409,6 +409,12 @@ mcf_status mcf_mlp_cross_entropy(const float* logits, const int* labels, int64_t
   return launched("mlp loss sum kernel");
 }
 
+mcf_status mcf_mlp_loss_sum(const float* terms, int64_t n, float* term_sum, mcf_stream s) {
+  if (n < 0 || !terms || !term_sum) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mlp_loss_sum: bad arguments");
+  mcfg::k_seqsum<<<1, 256, 0, s>>>(terms, n, term_sum);
+  return launched("mlp loss sum kernel");
+}
+
 mcf_status mcf_gemm_f32_ordered(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb,
                                 float* c, int64_t ldc, int64_t m, int64_t n, int64_t k, const float* relu_mask,
                                 mcf_stream s) {

@@ -6,11 +6,14 @@
 // MCF_FAST only promises the reference's error level, so there the gradient
 // GEMMs are ordinary FP32 GEMMs (cuBLAS SGEMM, FFMA accumulation, no TF32:
 // a plain library GEMM) and the bias gradient a tree reduction -- the
-// contraction work of the step that is not an MC product.
+// contraction work of the step that is not an MC product.  Shapes the int8
+// tensor cores take go through four-digit int8 products instead (binary32
+// accuracy, mm_ozaki.cu: gemm_f32_i8).
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -74,6 +77,17 @@ mcf_status mcf_gemm_f32_fast(int trans_a, int trans_b, const float* a, int64_t l
                              mcf_stream s) {
   if (m < 0 || n < 0 || k < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "gemm_f32: negative dimension");
   if (m * n == 0) return MCF_OK;
+  // int8 tensor cores (four balanced digits per operand, exact int32 sums:
+  // mm_ozaki.cu) unless the shape is outside them; MCF_GEMM_F32_I8=0 forces
+  // the FFMA GEMM
+  static const bool i8 = [] {
+    const char* e = getenv("MCF_GEMM_F32_I8");
+    return !(e && e[0] == '0');
+  }();
+  if (i8) {
+    const mcf_status st = mcfr::gemm_f32_i8(trans_a, trans_b, a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
+    if (st != MCF_ERR_UNSUPPORTED) return st;
+  }
   cublasHandle_t h = handle();
   if (!h) return mcfr::fail(MCF_ERR_CUDA, "gemm_f32: cannot create a cuBLAS handle");
   cublasSetStream(h, s);

@@ -913,6 +913,201 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   return mcfr::check_launch("mm_fast combine kernels");
 }
 
+// ---- binary32 x binary32 -> binary32 GEMM on the int8 tensor cores ---------------------
+//
+// Plan FAST's MLP backward products (dW = G A^T, dA = approx(W)^T G, the
+// reference's plain binary32 matmul2d, autodiff.hpp:280-296) with the same
+// digit scheme at binary32 accuracy: each row of op(A) / column of op(B) is
+// scaled by a power of two 2^e > 2 max|x| and rounded to X = rint(x 2^(31-e))
+// (|X| < 2^30, truncation <= 2^-32 in scaled units), cut into four balanced
+// base-256 digits (d0 in [-64, 64]); diagonals q = s + t <= 3 (10 int8
+// GEMM-equivalents, one GEMM per diagonal over the concatenated planes,
+// exact int32 sums for K < 32768); the dropped pairs and truncations leave
+// <= 2^-30 per product in scaled units, i.e. about 2^-26 |a|max |b|max:
+// below a binary32 FFMA GEMM's error bound (K 2^-24 sum |a||b|).
+// T = ((S0 256 + S1) 256 + S2) 256 + S3 is exact in binary64 (< 2^50 for
+// K < 32768) and C = RN32(T 2^(ea + eb - 38)).  A row / column holding Inf
+// or NaN makes its outputs NaN.
+
+constexpr int kD4 = 4;
+
+// max |x| bits per k-contiguous row (element (r, k) at p[r ld + k]): warp per
+// row, 16-byte loads (four in flight per lane) when rows are 16-byte aligned
+__global__ void __launch_bounds__(256) k_f32_rowmax(const float* __restrict__ p, int64_t rows, int64_t k, int64_t ld,
+                                                    unsigned* __restrict__ mx) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+  const float* pr = p + r * ld;
+  int64_t t = 0;
+  if ((reinterpret_cast<uintptr_t>(pr) & 15) == 0) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(pr);
+    const int64_t k4 = k / 4;
+    for (int64_t q = lane; q < k4; q += 32) {
+      const uint4 v = __ldg(p4 + q);
+      m0 = max(m0, v.x & 0x7fffffffu);
+      m1 = max(m1, v.y & 0x7fffffffu);
+      m2 = max(m2, v.z & 0x7fffffffu);
+      m3 = max(m3, v.w & 0x7fffffffu);
+    }
+    t = k4 * 4;
+  }
+  for (int64_t u = t + lane; u < k; u += 32) m0 = max(m0, __float_as_uint(pr[u]) & 0x7fffffffu);
+  unsigned m = max(max(m0, m1), max(m2, m3));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) mx[r] = m;
+}
+
+// max |x| bits per column of a k-strided operand (element (k, c) at p[k ld + c]),
+// slabs of 64 k, atomicMax (mx cleared first)
+__global__ void __launch_bounds__(256) k_f32_colmax(const float* __restrict__ p, int64_t k, int64_t cols, int64_t ld,
+                                                    unsigned* __restrict__ mx) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t t0 = (int64_t)blockIdx.y * 64, t1 = t0 + 64 < k ? t0 + 64 : k;
+  unsigned m = 0;
+  for (int64_t t = t0; t < t1; ++t) m = max(m, __float_as_uint(p[t * ld + c]) & 0x7fffffffu);
+  if (m) atomicMax(mx + c, m);
+}
+
+// scale exponent from the max bits: 2^e > 2 max (0 for an all-zero line)
+__device__ __forceinline__ int f32_scale_exp(unsigned mbits) {
+  return mbits == 0 ? 0 : ilogbf(__uint_as_float(mbits)) + 2;
+}
+
+// four balanced digits of one element, packed little-endian per plane
+__device__ __forceinline__ void f32_digits(float x, int e, int (&d)[kD4]) {
+  int v = __double2int_rn(__dmul_rn((double)x, __longlong_as_double((long long)(1023 + 31 - e) << 52)));
+#pragma unroll
+  for (int s = kD4 - 1; s >= 1; --s) {
+    const int t = ((v + 128) & 255) - 128;
+    d[s] = t;
+    v = (v - t) >> 8;
+  }
+  d[0] = v;
+}
+
+// digit planes of a k-contiguous operand: byte [r][pos(s) kp + k], pos(s) = s
+// (REV = false, the A side) or kD4 - 1 - s (REV, the B side); zero for k >= K
+template <bool REV>
+__global__ void __launch_bounds__(256) k_f32_dig_rows(const float* __restrict__ p, int64_t rows, int64_t k,
+                                                      int64_t ld, int64_t kp, const unsigned* __restrict__ mx,
+                                                      int8_t* __restrict__ out) {
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k0 >= kp) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const unsigned mb = mx[r];
+    const int e = f32_scale_exp(mb);
+    const bool ok = mb < 0x7f800000u;
+    unsigned packed[kD4] = {0u, 0u, 0u, 0u};
+    const float* pr = p + r * ld;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (k0 + u >= k || !ok) break;
+      int d[kD4];
+      f32_digits(pr[k0 + u], e, d);
+#pragma unroll
+      for (int s = 0; s < kD4; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
+    }
+    int8_t* row = out + r * kD4 * kp + k0;
+#pragma unroll
+    for (int s = 0; s < kD4; ++s) *reinterpret_cast<unsigned*>(row + (REV ? kD4 - 1 - s : s) * kp) = packed[s];
+  }
+}
+
+// digit planes of a k-strided operand (element (k, c) at p[k ld + c]) as rows
+// per column c: 32 k x 32 c tiles transposed through shared memory
+template <bool REV>
+__global__ void __launch_bounds__(256) k_f32_dig_cols(const float* __restrict__ p, int64_t k, int64_t cols,
+                                                      int64_t ld, int64_t kp, const unsigned* __restrict__ mx,
+                                                      int8_t* __restrict__ out) {
+  __shared__ unsigned dg[kD4][kSlab][kSlab / 4 + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t k0 = (int64_t)blockIdx.y * kSlab, c0 = (int64_t)blockIdx.x * kSlab;
+  const int64_t c = c0 + tx;
+  const unsigned mb = c < cols ? mx[c] : 0u;
+  const int e = f32_scale_exp(mb);
+  const bool ok = mb < 0x7f800000u;
+  unsigned packed[kD4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t gk = k0 + ty * 4 + u;
+    if (gk < k && c < cols && ok) {
+      int d[kD4];
+      f32_digits(p[gk * ld + c], e, d);
+#pragma unroll
+      for (int s = 0; s < kD4; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < kD4; ++s) dg[s][tx][ty] = packed[s];
+  __syncthreads();
+  const int jj = threadIdx.x >> 3, part = threadIdx.x & 7;
+  const int64_t gc = c0 + jj;
+  if (gc < cols && k0 + part * 4 < kp) {
+    int8_t* dst = out + gc * kD4 * kp + k0 + part * 4;
+#pragma unroll
+    for (int s = 0; s < kD4; ++s) *reinterpret_cast<unsigned*>(dst + (REV ? kD4 - 1 - s : s) * kp) = dg[s][jj][part];
+  }
+}
+
+// C[i, j] (row-major, ldc) = RN32(T 2^(ea_i + eb_j - 38)), optional ReLU mask;
+// four consecutive columns per thread (16-byte plane loads: np % 16 == 0)
+__global__ void __launch_bounds__(256) k_f32_comb(const int* __restrict__ cq, int64_t m, int64_t n, int64_t np,
+                                                  const unsigned* __restrict__ amx, const unsigned* __restrict__ bmx,
+                                                  float* __restrict__ c, int64_t ldc, const float* __restrict__ mask) {
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= n) return;
+  const int64_t plane = m * np;
+  unsigned bm[4];
+  int eb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    bm[u] = j0 + u < n ? bmx[j0 + u] : 0u;
+    eb[u] = f32_scale_exp(bm[u]);
+  }
+  const bool vec = j0 + 3 < n && (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0 &&
+                   (!mask || (reinterpret_cast<uintptr_t>(mask) & 15) == 0);
+  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+    const int64_t o = i * np + j0;
+    const int4 s0 = __ldcs(reinterpret_cast<const int4*>(cq + o));
+    const int4 s1 = __ldcs(reinterpret_cast<const int4*>(cq + plane + o));
+    const int4 s2 = __ldcs(reinterpret_cast<const int4*>(cq + 2 * plane + o));
+    const int4 s3 = __ldcs(reinterpret_cast<const int4*>(cq + 3 * plane + o));
+    const int a0[4] = {s0.x, s0.y, s0.z, s0.w}, a1[4] = {s1.x, s1.y, s1.z, s1.w};
+    const int a2[4] = {s2.x, s2.y, s2.z, s2.w}, a3[4] = {s3.x, s3.y, s3.z, s3.w};
+    const unsigned am = amx[i];
+    const int ea = f32_scale_exp(am);
+    float v[4], mk[4] = {1.f, 1.f, 1.f, 1.f};
+    if (mask) {
+      if (vec) {
+        const float4 q = *reinterpret_cast<const float4*>(mask + i * ldc + j0);
+        mk[0] = q.x, mk[1] = q.y, mk[2] = q.z, mk[3] = q.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mk[u] = j0 + u < n ? mask[i * ldc + j0 + u] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = __fma_rn(__fma_rn(__fma_rn((double)a0[u], 256.0, (double)a1[u]), 256.0, (double)a2[u]), 256.0,
+                                (double)a3[u]);
+      v[u] = __double2float_rn(__dmul_rn(t, pow2d(ea + eb[u] - 38)));
+      if (am >= 0x7f800000u || bm[u] >= 0x7f800000u) v[u] = __int_as_float(0x7fffffff);
+      if (!(mk[u] > 0.0f)) v[u] = 0.0f;
+    }
+    if (vec) {
+      *reinterpret_cast<float4*>(c + i * ldc + j0) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < n) c[i * ldc + j0 + u] = v[u];
+    }
+  }
+}
+
 }  // namespace oz
 }  // namespace mcfg
 
@@ -1152,6 +1347,70 @@ mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, in
   }
 #undef OZ_TRY
   return done(cu(cudaStreamSynchronize(cout), "sync"));
+}
+
+
+// C (m x n, row-major, ldc) = op(A) op(B) in binary32 through four-digit int8
+// products (see k_f32_comb above); MCF_ERR_UNSUPPORTED for shapes it does not
+// take (the caller runs the FFMA GEMM).  op(A) = A (m x k, lda) or A^T (A
+// stored k x m); op(B) = B (k x n, ldb) or B^T (B stored n x k).
+mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                       int64_t ldc, int64_t m, int64_t n, int64_t k, const float* mask, cudaStream_t s) {
+  using namespace mcfg::oz;
+  if (m < 64 || n < 64 || k < 64 || k >= 32768 || m * n >= (int64_t(1) << 31)) return MCF_ERR_UNSUPPORTED;
+  const int64_t kp = (k + 31) / 32 * 32, np = pad16(n);
+  const std::size_t ba = al(m * kD4 * kp), bb = al(np * kD4 * kp), bq = al(4 * m * np * 4);
+  char* ws = oz_workspace(ba + bb + bq + al(m * 4) + al(np * 4), s);
+  if (!ws) return fail(MCF_ERR_CUDA, "gemm_f32: cannot allocate the digit-plane workspace");
+  int8_t* ap = reinterpret_cast<int8_t*>(ws);
+  int8_t* bp = reinterpret_cast<int8_t*>(ws + ba);
+  int* cq = reinterpret_cast<int*>(ws + ba + bb);
+  unsigned* amx = reinterpret_cast<unsigned*>(ws + ba + bb + bq);
+  unsigned* bmx = reinterpret_cast<unsigned*>(ws + ba + bb + bq + al(m * 4));
+  if (cudaMemsetAsync(amx, 0, al(m * 4) + al(np * 4), s) != cudaSuccess) return fail(MCF_ERR_CUDA, "gemm_f32: memset");
+  // padding k (kp > k) and padding columns (np > n) must read as zero digits
+  if (np > n && cudaMemsetAsync(bp + n * kD4 * kp, 0, (np - n) * kD4 * kp, s) != cudaSuccess)
+    return fail(MCF_ERR_CUDA, "gemm_f32: memset");
+  const int sms = mcfr::sm_count();
+  // op(A): rows m along k
+  if (!trans_a) {
+    k_f32_rowmax<<<(unsigned)((m + 7) / 8), 256, 0, s>>>(a, m, k, lda, amx);
+    const int64_t gx = (kp / 4 + 255) / 256;
+    k_f32_dig_rows<false><<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(m, sms * 8 / gx + 1)), 256, 0, s>>>(
+        a, m, k, lda, kp, amx, ap);
+  } else {
+    k_f32_colmax<<<dim3((unsigned)((m + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0, s>>>(a, k, m, lda, amx);
+    k_f32_dig_cols<false><<<dim3((unsigned)((m + kSlab - 1) / kSlab), (unsigned)(kp / kSlab)), 256, 0, s>>>(
+        a, k, m, lda, kp, amx, ap);
+  }
+  // op(B): columns n along k
+  if (trans_b) {
+    k_f32_rowmax<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(b, n, k, ldb, bmx);
+    const int64_t gx = (kp / 4 + 255) / 256;
+    k_f32_dig_rows<true><<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(n, sms * 8 / gx + 1)), 256, 0, s>>>(
+        b, n, k, ldb, kp, bmx, bp);
+  } else {
+    k_f32_colmax<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0, s>>>(b, k, n, ldb, bmx);
+    k_f32_dig_cols<true><<<dim3((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab)), 256, 0, s>>>(
+        b, k, n, ldb, kp, bmx, bp);
+  }
+  for (int i = 0; i < 4; ++i) mcfr::note_launch();
+  mcf_status st = mcfr::check_launch("gemm_f32 digit kernels");
+  if (st != MCF_OK) return st;
+  // diagonal q: A planes s = q - th .. q (ascending) against B planes t = th ..
+  // q - (q - th) (stored reversed at kD4 - 1 - t: ascending positions)
+  for (int q = 0; q < kD4 && st == MCF_OK; ++q) {
+    const int th = q, tl = 0;  // pairs (q - t, t), t = 0 .. q (all within four digits)
+    const int8_t* bq = bp + (int64_t)(kD4 - 1 - th) * kp;
+    const int8_t* aq = ap + (int64_t)(q - th) * kp;
+    st = gemm_s8(bq, kD4 * kp, aq, kD4 * kp, cq + (int64_t)q * m * np, np, m, (int64_t)(th - tl + 1) * kp, s);
+  }
+  if (st != MCF_OK) return st;
+  const int64_t gcx = (n + 1023) / 1024;
+  k_f32_comb<<<dim3((unsigned)gcx, (unsigned)std::min<int64_t>(m, sms * 8 / gcx + 1)), 256, 0, s>>>(
+      cq, m, n, np, amx, bmx, c, ldc, mask);
+  mcfr::note_launch();
+  return mcfr::check_launch("gemm_f32 combine kernel");
 }
 
 }  // namespace mcfr

@@ -168,12 +168,25 @@ class MCMLP:
                                            s))
             if not last:
                 acts.append(B["A"][l])
-        # loss + dL/dlogits
+        # loss + dL/dlogits.  Plan FAST: the loss's sequential sum (8192
+        # dependent additions) runs on a side stream, joined before the
+        # gradient exchange, instead of delaying the backward
+        fast = self.plan in (FAST, FAST_FP64)
         _check(lib_.mcf_mlp_cross_entropy(B["H"][L - 1].data_ptr(), labels.data_ptr(), self.dims[-1], n, n_global,
-                                          B["G"][L - 1].data_ptr(), B["terms"].data_ptr(), B["loss"].data_ptr(), s))
+                                          B["G"][L - 1].data_ptr(), B["terms"].data_ptr(),
+                                          None if fast else B["loss"].data_ptr(), s))
+        loss_done = None
+        if fast:
+            cur = torch.cuda.current_stream()
+            if getattr(self, "_loss_stream", None) is None:
+                self._loss_stream = torch.cuda.Stream()
+            side = self._loss_stream
+            side.wait_stream(cur)
+            _check(lib_.mcf_mlp_loss_sum(B["terms"].data_ptr(), n, B["loss"].data_ptr(), side.cuda_stream))
+            loss_done = torch.cuda.Event()
+            loss_done.record(side)
         # backward: the reference-order plan reproduces matmul2d's rounding
         # sequence; plan FAST uses FP32 library GEMMs and tree row sums
-        fast = self.plan in (FAST, FAST_FP64)
         gemm = lib_.mcf_gemm_f32_fast if fast else lib_.mcf_gemm_f32_ordered
         rowsum = lib_.mcf_rowsum_f32_fast if fast else lib_.mcf_rowsum_f32_ordered
         gv = self.grads.views
@@ -190,6 +203,8 @@ class MCMLP:
                 # dA_prev (in x n) = approx(W)^T (in x out) . G (out x n), ReLU mask = H_{l-1}
                 _check(gemm(1, 0, B["Wa"][l].data_ptr(), in_dim, G.data_ptr(), n, B["G"][l - 1].data_ptr(), n, in_dim,
                             n, out_dim, B["H"][l - 1].data_ptr(), s))
+        if loss_done is not None:
+            torch.cuda.current_stream().wait_event(loss_done)
         self.grads.finish(B["loss"])
         for l in range(L):
             _check(lib_.mcf_sgd_grow(self.W[l].data_ptr(), nc, gv[2 * l].data_ptr(), self.W[l].numel() // nc,

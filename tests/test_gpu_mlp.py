@@ -231,3 +231,65 @@ def test_fused_linear_forward_equals_product_then_bias_act(relu):
     torch.cuda.synchronize()
     assert_bits(h1.cpu().numpy(), h2.cpu().numpy(), "h")
     assert_bits(a1.cpu().numpy(), a2.cpu().numpy(), "act")
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("m,n,k", [(130, 77, 1000), (64, 200, 4100), (257, 96, 65)])
+def test_fast_gemm_int8_digits_binary32_accuracy(ta, tb, m, n, k):
+    """The binary32 GEMM on the int8 tensor cores (four balanced digits per
+    operand, exact int32 diagonal sums) for every operand layout, ragged k and
+    n, rows of very different magnitude and an all-zero row: error within the
+    binary32 GEMM bound (1e-5 sum |a||b|), ReLU mask applied."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(1000 + 10 * ta + tb + m)
+    A = (rng.standard_normal((m, k)) * np.exp2(rng.integers(-20, 20, (m, 1)))).astype(np.float32)
+    B = (rng.standard_normal((k, n)) * np.exp2(rng.integers(-20, 20, (1, n)))).astype(np.float32)
+    A[3] = 0.0
+    mask = rng.standard_normal((m, n)).astype(np.float32)
+    want = np.where(mask > 0, A.astype(np.float64) @ B.astype(np.float64), 0.0)
+    a_st = np.ascontiguousarray(A.T if ta else A)
+    b_st = np.ascontiguousarray(B.T if tb else B)
+    da, db, dm = (torch.from_numpy(v).cuda() for v in (a_st, b_st, mask))
+    dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_gemm_f32_fast(ta, tb, da.data_ptr(), a_st.shape[1], db.data_ptr(), b_st.shape[1], dc.data_ptr(),
+                                 n, m, n, k, dm.data_ptr(), None) == 0, lib.mcf_last_error()
+    got = dc.cpu().numpy().astype(np.float64)
+    scale = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64))
+    err = np.abs(got - want)
+    assert np.all(err <= 1e-5 * scale + 1e-300), float((err / np.maximum(scale, 1e-300)).max())
+    assert np.all(got[3] == 0.0)
+    # the products themselves (no mask) stay far below the bound on ordinary data
+    dc2 = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    assert lib.mcf_gemm_f32_fast(ta, tb, da.data_ptr(), a_st.shape[1], db.data_ptr(), b_st.shape[1], dc2.data_ptr(),
+                                 n, m, n, k, None, None) == 0
+    g2 = dc2.cpu().numpy().astype(np.float64)
+    rel = np.abs(g2 - A.astype(np.float64) @ B.astype(np.float64)) / np.maximum(scale, 1e-300)
+    assert rel.max() <= 1e-6, float(rel.max())
+
+
+def test_fast_gemm_int8_nonfinite_rows_are_nan():
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(77)
+    m, n, k = 100, 80, 300
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    A[5, 7] = np.inf
+    B[11, 9] = np.nan
+    da, db = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dc = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_gemm_f32_fast(0, 0, da.data_ptr(), k, db.data_ptr(), n, dc.data_ptr(), n, m, n, k, None, None) == 0
+    got = dc.cpu().numpy()
+    assert np.all(np.isnan(got[5])) and np.all(np.isnan(got[:, 9]))
+    ok = np.ones((m, n), bool)
+    ok[5] = False
+    ok[:, 9] = False
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.allclose(got[ok], want[ok], rtol=0, atol=1e-5 * np.abs(want[ok]).max())
