@@ -94,7 +94,7 @@ struct OpTraits {
 // it declines runs the register path below, then the literal one
 template <int OP, class P, int NC, int ONC>
 constexpr bool kG2 = std::is_same<P, PB32>::value && NC == 2 && ONC == 2 &&
-                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp);
+                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp || OP == kAdd);
 
 template <int OP, class P, int NC, int ONC>
 __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[NC], RT<P> v,
@@ -107,6 +107,7 @@ __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[
     else if constexpr (OP == kDiv) ok = g2::div<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kDivN) ok = g2::div<Q>(v, 0.0f, x[0], x[1], o[0], o[1]);  // x holds the divisor
     else if constexpr (OP == kMul) ok = g2::mul<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
+    else if constexpr (OP == kAdd) ok = g2::add<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else ok = g2::exp_b32(x[0], x[1], o[0], o[1]);
     if (__builtin_expect(ok, 1)) return true;
   }

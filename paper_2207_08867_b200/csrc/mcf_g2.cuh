@@ -103,11 +103,15 @@ G2_HD bool prod_ok(T_<Q> p, T_<Q> a, T_<Q> b) {
 // TIE0 = false drops the top-level tie clause where exact midpoints are rare
 // (an exact tie there then takes the fallback).  B is usually much larger than
 // R0, so (C1, F) comes from a fast two-sum guarded by |B| >= |R0|.
-template <class Q, bool REST, bool DIR, bool CANON, bool TIE0 = true>
+// SWAP: no structural order between B and R0: the fast two-sum takes the
+// larger magnitude first instead of guarding.
+template <class Q, bool REST, bool DIR, bool CANON, bool TIE0 = true, bool SWAP = false>
 G2_HD bool finish(T_<Q> A, T_<Q> B, T_<Q> R0, T_<Q> rest_abs, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> C1, F;
-  fast_two_sum<Q>(B, R0, C1, F);
-  const bool ord = Q::abs(B) >= Q::abs(R0);
+  const bool ge = Q::abs(B) >= Q::abs(R0);
+  if (SWAP) fast_two_sum<Q>(ge ? B : R0, ge ? R0 : B, C1, F);
+  else fast_two_sum<Q>(B, R0, C1, F);
+  const bool ord = SWAP || ge;
   // tie at the top: fl(A + C1) is the even neighbour; otherwise it is A
   const T_<Q> A2 = TIE0 ? Q::add(A, C1) : A;
   const T_<Q> C2 = !TIE0 || A2 == A ? C1 : -C1;
@@ -148,6 +152,24 @@ G2_HD bool scale(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
   const T_<Q> xs = x1 == T_<Q>(0) ? x0 : x1;
   const bool ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(xs, v)) | (xs == T_<Q>(0)) | (v == T_<Q>(0)));
   return scale_core<Q, false, true>(x0, x1, v, o0, o1) & ok & Q::finite(o0);
+}
+
+// mc_ops.hpp:173-184 add_kernel, nc = 2 -> 2 (Add-MCN; also the MLP's bias
+// add): S = x0 + x1 + y0 + y1 through four exact two-sums, the top candidate
+// re-rounded with the tail (A = fl(s + u)), the last two error terms bounded.
+template <class Q, bool CANON = true>
+G2_HD bool add(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
+  T_<Q> s, e, t, f, u, g, A, U;
+  two_sum<Q>(x0, y0, s, e);
+  two_sum<Q>(x1, y1, t, f);
+  two_sum<Q>(e, t, u, g);  // S = s + u + g + f
+  two_sum<Q>(s, u, A, U);  // S = A + U + g + f
+  // w = fl(g + f) is exact when either term is zero (frequent: f is often
+  // an exact half-ulp tie residue with g = 0), else within 2^-p |w|
+  const T_<Q> w = Q::add(g, f);
+  const T_<Q> rest = (g == T_<Q>(0)) | (f == T_<Q>(0)) ? T_<Q>(0) : Q::ulpb(w);
+  const bool ok = compressed<Q>(x0, x1) & compressed<Q>(y0, y1);
+  return finish<Q, true, false, CANON, true, true>(A, U, w, rest, o0, o1) & ok & Q::finite(o0);
 }
 
 // mc_ops.hpp:256-282 Square-MCN, nc = 2: terms x0^2 (p, e), 2 x0 x1 (2p', 2e'),

@@ -45,6 +45,7 @@
 
 #include "mcf_accum.cuh"
 #include "mcf_fast.cuh"
+#include "mcf_g2.cuh"
 #include "mcf_lit.cuh"
 #include "mcf_runtime.h"
 
@@ -314,7 +315,9 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
   split_out<float, 2, 2>(v, z);
   b[0] = ep.bias[i * 2];
   b[1] = ep.bias[i * 2 + 1];
-  if (!fast::add<PB32, 2>(z, b, r)) lit::add<PB32>(z, 2, b, 2, r, 2);
+  // certified shortcut first (mcf_g2.cuh), then the register path, then the literal one
+  if (!g2::add<g2::QF32>(z[0], z[1], b[0], b[1], r[0], r[1]) && !fast::add<PB32, 2>(z, b, r))
+    lit::add<PB32>(z, 2, b, 2, r, 2);
   const float hv = fast::approx<PB32, 2>(r);
   ep.h[i * ldo + j] = hv;
   if (ep.act) ep.act[i * ldo + j] = ep.relu ? (hv > 0.0f ? hv : 0.0f) : hv;  // Tape::relu, autodiff.hpp:134
@@ -327,7 +330,7 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
 // threes in integer arithmetic, G = S_q 2^16 + S_q+1 2^8 + S_q+2 (|G| < 2^51,
 // exact in binary64), and the three groups (weights 2^-30, 2^-54, 2^-78) are
 // added exactly in double-double.  Grid: x covers a row, y (strided) rows.
-__global__ void __launch_bounds__(256) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
+__global__ void __launch_bounds__(256, 3) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
                                                  int nkc, int nq, const int* __restrict__ ea,
                                                  const int* __restrict__ eb, const int* __restrict__ rnf,
                                                  const int* __restrict__ cnf, const int* __restrict__ cinx,
@@ -931,20 +934,19 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
 
 constexpr int kD4 = 4;
 
-// max |x| bits per k-contiguous row (element (r, k) at p[r ld + k]): warp per
-// row, 16-byte loads (four in flight per lane) when rows are 16-byte aligned
+// max |x| bits per k-contiguous row (element (r, k) at p[r ld + k]): a CTA per
+// row, 16-byte loads when the row is 16-byte aligned
 __global__ void __launch_bounds__(256) k_f32_rowmax(const float* __restrict__ p, int64_t rows, int64_t k, int64_t ld,
                                                     unsigned* __restrict__ mx) {
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+  __shared__ unsigned part[8];
+  const int64_t r = blockIdx.x;
   unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
   const float* pr = p + r * ld;
   int64_t t = 0;
   if ((reinterpret_cast<uintptr_t>(pr) & 15) == 0) {
     const uint4* p4 = reinterpret_cast<const uint4*>(pr);
     const int64_t k4 = k / 4;
-    for (int64_t q = lane; q < k4; q += 32) {
+    for (int64_t q = threadIdx.x; q < k4; q += blockDim.x) {
       const uint4 v = __ldg(p4 + q);
       m0 = max(m0, v.x & 0x7fffffffu);
       m1 = max(m1, v.y & 0x7fffffffu);
@@ -953,11 +955,17 @@ __global__ void __launch_bounds__(256) k_f32_rowmax(const float* __restrict__ p,
     }
     t = k4 * 4;
   }
-  for (int64_t u = t + lane; u < k; u += 32) m0 = max(m0, __float_as_uint(pr[u]) & 0x7fffffffu);
+  for (int64_t u = t + threadIdx.x; u < k; u += blockDim.x) m0 = max(m0, __float_as_uint(pr[u]) & 0x7fffffffu);
   unsigned m = max(max(m0, m1), max(m2, m3));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if (lane == 0) mx[r] = m;
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned a = part[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a = max(a, part[w]);
+    mx[r] = a;
+  }
 }
 
 // max |x| bits per column of a k-strided operand (element (k, c) at p[k ld + c]),
@@ -1374,7 +1382,7 @@ mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, co
   const int sms = mcfr::sm_count();
   // op(A): rows m along k
   if (!trans_a) {
-    k_f32_rowmax<<<(unsigned)((m + 7) / 8), 256, 0, s>>>(a, m, k, lda, amx);
+    k_f32_rowmax<<<(unsigned)m, 256, 0, s>>>(a, m, k, lda, amx);
     const int64_t gx = (kp / 4 + 255) / 256;
     k_f32_dig_rows<false><<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(m, sms * 8 / gx + 1)), 256, 0, s>>>(
         a, m, k, lda, kp, amx, ap);
@@ -1385,7 +1393,7 @@ mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, co
   }
   // op(B): columns n along k
   if (trans_b) {
-    k_f32_rowmax<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(b, n, k, ldb, bmx);
+    k_f32_rowmax<<<(unsigned)n, 256, 0, s>>>(b, n, k, ldb, bmx);
     const int64_t gx = (kp / 4 + 255) / 256;
     k_f32_dig_rows<true><<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(n, sms * 8 / gx + 1)), 256, 0, s>>>(
         b, n, k, ldb, kp, bmx, bp);

@@ -39,7 +39,7 @@ def _run(exe, *args):
         if m:
             rows[m.group(2)] = dict(cases=int(m.group(3)), acc=float(m.group(4)), bad=int(m.group(5)),
                                     cap=int(m.group(6)))
-    assert set(rows) == {"scale", "square", "div", "mul"}, r.stdout + r.stderr
+    assert set(rows) == {"scale", "square", "div", "mul", "add"}, r.stdout + r.stderr
     return rows, r.returncode
 
 
@@ -57,5 +57,7 @@ def test_sampled_binary32(g2v):
     rows, rc = _run(g2v, "sample", 24, 300000)
     for op, r in rows.items():
         assert r["bad"] == 0 and r["cap"] == 0, (op, r)
-        assert r["acc"] > 99.99, (op, r)
+        # add: half the samples are near-cancelling sums; ties with two nonzero
+        # tail terms decline (~0.3% of random sums)
+        assert r["acc"] > (99.5 if op == "add" else 99.99), (op, r)
     assert rc == 0

@@ -60,6 +60,10 @@ def test_g2_ops_bitwise_on_margins(gr, port, seed):
     x = x[: y.shape[0]]
     v = x[rng.permutation(x.shape[0]), 0].copy()
     assert_bits(gr.run("scaling_n", x, v), port.scaling_n(x, v), "scaling_n")
+    assert_bits(gr.run("add_mcn", x, y), port.add_mcn(x, y), "add_mcn")
+    xn = x.copy()
+    xn[: y.shape[0] // 2, 0] = -y[: y.shape[0] // 2, 0]  # cancelling leads
+    assert_bits(gr.run("add_mcn", xn, y), port.add_mcn(xn, y), "add_mcn cancelling")
     assert_bits(gr.run("square_mcn", x), port.square_mcn(x), "square_mcn")
     assert_bits(gr.run("div_n", v, y), port.div_n(v, y), "div_n")
     assert_bits(gr.run("div_mcn", x, y), port.div_mcn(x, y), "div_mcn")

@@ -242,7 +242,7 @@ int main(int argc, char** argv) {
     auto X = pairs(K, 1);
     const int M = 1 << (P - 1);
     printf("p=%d: %zu compressed pairs\n", P, X.size());
-    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"};
+    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"};
 #pragma omp parallel for schedule(dynamic, 16)
     for (long long i = 0; i < (long long)X.size(); ++i) {
       const double x[2] = {X[i].first, X[i].second};
@@ -258,18 +258,23 @@ int main(int argc, char** argv) {
         const double y[2] = {X[j].first, X[j].second};
         check(sd, [&](double* o) { ref_div(x, y, o); },
               [&](double* o) { return g2::div<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "div");
+        for (int sh = -3; sh <= 3; sh += 3) {  // relative exponent of y
+          const double ys[2] = {std::ldexp(y[0], sh), std::ldexp(y[1], sh)};
+          check(sa, [&](double* o) { ref_add(x, ys, o); },
+                [&](double* o) { return g2::add<QE>(x[0], x[1], ys[0], ys[1], o[0], o[1]); }, "add");
+        }
         if ((i + j) % 3 == 0)
           check(sm, [&](double* o) { ref_mul(x, y, o); },
                 [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
       }
     }
-    report(ss), report(sq), report(sd), report(sm);
-    return (ss.bad | sq.bad | sd.bad | sm.bad | ss.cap | sq.cap | sd.cap | sm.cap) ? 1 : 0;
+    report(ss), report(sq), report(sd), report(sm), report(sa);
+    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap) ? 1 : 0;
   }
   // sampled, config-0 style operands: v = U(-1,1) 2^U(-8,8) split greedily into p-bit comps
   P = argc > 2 ? atoi(argv[2]) : 24;
   const long long N = argc > 3 ? atoll(argv[3]) : 2000000;
-  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"};
+  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"};
 #pragma omp parallel
   {
     std::mt19937_64 g(1234 + 7919 * (unsigned long long)omp_get_thread_num());
@@ -296,8 +301,13 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::div<QE>(vv[0], vv[1], y[0], y[1], o[0], o[1]); }, "divn");
       check(sm, [&](double* o) { ref_mul(x, y, o); },
             [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
+      check(sa, [&](double* o) { ref_add(x, y, o); },
+            [&](double* o) { return g2::add<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "add");
+      const double yn[2] = {-x[0], -x[1] * 0.5};  // near-cancelling sums
+      check(sa, [&](double* o) { ref_add(x, yn, o); },
+            [&](double* o) { return g2::add<QE>(x[0], x[1], yn[0], yn[1], o[0], o[1]); }, "add");
     }
   }
-  report(ss), report(sq), report(sd), report(sm);
-  return (ss.bad | sq.bad | sd.bad | sm.bad | ss.cap | sq.cap | sd.cap | sm.cap) ? 1 : 0;
+  report(ss), report(sq), report(sd), report(sm), report(sa);
+  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap) ? 1 : 0;
 }
