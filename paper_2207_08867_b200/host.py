@@ -121,3 +121,47 @@ def mm_mcmc(x, y, strategy=0, out=None):
         out = np.empty((m, n, nc), x.dtype)
     _check(lib().mcf_h_mm_mcmc(_prec(x), _p(x), _p(y), nc, m, k, n, _p(out), strategy))
     return out
+
+
+# ---- the reference's test predicates (value checks on host arrays) -----------
+
+_SIG = {np.dtype(np.float16): 11, np.dtype(np.float32): 24, np.dtype(np.float64): 53}
+_MIN_POS = {np.dtype(np.float16): 2.0**-24, np.dtype(np.float32): 2.0**-149, np.dtype(np.float64): 2.0**-1074}
+
+
+def ulp(x, dtype):
+    """ulp<P>(x) (precision.hpp:200-206): the spacing of P at |x|, clamped to the
+    subnormal quantum; min_pos for zero and non-finite x.  Elementwise, binary64."""
+    dt = np.dtype(dtype)
+    x = np.asarray(x, np.float64)
+    with np.errstate(all="ignore"):
+        e = np.floor(np.log2(np.abs(np.where(np.isfinite(x) & (x != 0), x, 1.0))))
+        # log2 can round at the top of a binade: correct with exact comparisons
+        e = np.where(np.exp2(e) > np.abs(x), e - 1, e)
+        e = np.where(np.exp2(e + 1) <= np.abs(x), e + 1, e)
+        sp = np.exp2(e - (_SIG[dt] - 1))
+    sp = np.maximum(sp, _MIN_POS[dt])
+    return np.where((x == 0) | ~np.isfinite(x), _MIN_POS[dt], sp)
+
+
+def satisfies_invariants(x) -> bool:
+    """satisfies_invariants<P> (mc_ops.hpp:537-554) on an MC array (..., nc):
+    every component finite, zeros only as a trailing suffix, no nonzero
+    component below P's subnormal quantum, and |c_i| <= ulp(c_{i-1})."""
+    x = np.asarray(x)
+    dt = x.dtype
+    c = x.reshape(-1, x.shape[-1]).astype(np.float64)
+    if not np.all(np.isfinite(c)):
+        return False
+    nz = c != 0
+    # a zero followed by a nonzero component
+    seen_zero = np.logical_or.accumulate(~nz, axis=1)
+    if np.any(nz[:, 1:] & seen_zero[:, :-1]):
+        return False
+    if np.any(nz & (np.abs(c) < _MIN_POS[dt])):
+        return False
+    if c.shape[1] > 1:
+        bad = nz[:, 1:] & (np.abs(c[:, 1:]) > ulp(c[:, :-1], dt))
+        if np.any(bad):
+            return False
+    return True
