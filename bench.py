@@ -312,10 +312,11 @@ def other_configs(torch, mcf, hbm_gbs, f64_peak):
             ge = mcf.lib().mcf_fast_tc_gemm_equivalents(2, N4)
             entry.update({"path": "int8 tensor cores", "int8_gemm_equivalents": ge,
                           "int8_TOPS_step": round(2 * N4 ** 3 * ge / (ms * 1e-3) / 1e12, 1)})
-        else:  # binary16 nc=3: pre-summed operands, one FMA per MAD on the FP64 pipe
-            ops = mcf.lib().mcf_fast_ops_per_mad(1, mcf.B16, nc)
-            entry.update({"path": "fp64 pipe", "fp64_ops_per_mad": ops,
-                          "frac_fp64_peak": round(ops * N4 ** 3 / (ms * 1e-3) / 1e12 / f64_peak, 3)})
+        else:  # binary16 nc=3: exact binary64 pre-sums, five int8 digits, 15 GEMM-equivalents
+            eq = 15
+            entry.update({"path": "int8 tensor cores (five digits per pre-summed element)",
+                          "int8_gemm_equivalents": eq,
+                          "int8_TOPS_step": round(2 * eq * N4 ** 3 / (ms * 1e-3) / 1e12, 1)})
         res[f"config4_mcmc_{tag}"] = entry
         del a, b
         torch.cuda.empty_cache()

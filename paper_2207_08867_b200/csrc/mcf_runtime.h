@@ -61,6 +61,9 @@ bool ozaki_supported(int64_t m, int64_t k, int64_t n);
 mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n, float* out,
                     cudaStream_t s);
 int ozaki_digits();
+// MC binary16 (nc <= 3) x MC binary16 through five-digit int8 products (config 4's variant)
+mcf_status mm_b16_i8(const void* x, const void* y, int nc, int64_t m, int64_t k, int64_t n, void* out,
+                     cudaStream_t s);
 // binary32 GEMM through four-digit int8 products (plan FAST's MLP backward)
 mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                        int64_t ldc, int64_t m, int64_t n, int64_t k, const float* mask, cudaStream_t s);

@@ -599,6 +599,10 @@ mcf_status mm_fast_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
                                    static_cast<float*>(out), s);
     if (st != MCF_ERR_UNSUPPORTED) return st;
   }
+  if (tc && p == MCF_B16 && nc <= 3) {
+    const mcf_status st = mm_b16_i8(x, y, nc, m, k, n, out, s);
+    if (st != MCF_ERR_UNSUPPORTED) return st;
+  }
   const bool f32 = p == MCF_B32 && nc == 2, f16 = p == MCF_B16 && nc == 3;
   if ((!f32 && !f16) || n % 2 != 0 || k % 2 != 0) return MCF_ERR_UNSUPPORTED;
   const int w = f32 ? 2 : 1;  // binary64 words per element after widening

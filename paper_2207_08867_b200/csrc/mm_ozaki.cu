@@ -1116,6 +1116,172 @@ __global__ void __launch_bounds__(256) k_f32_comb(const int* __restrict__ cq, in
   }
 }
 
+// ---- binary16 MC x MC (nc <= 3) on the int8 tensor cores ---------------------------------
+//
+// Config 4's binary16 variant.  Every binary16 value is a multiple of 2^-24
+// below 2^16, so an element's components sum exactly in binary64 (<= 42
+// bits).  That value is scaled per row of A / column of B (2^e > 2 max),
+// rounded to X = rint(v 2^(39-e)) (|X| < 2^38, truncation <= 2^-40 in scaled
+// units) and cut into five balanced base-256 digits; diagonals q = s + t <= 4
+// (15 int8 GEMM-equivalents, exact int32 sums for K < 26214), the dropped
+// pairs leave < 2^-37 per product (scaled): far inside the 4x-of-recipe-B
+// contract (recipe B's own error is ~2^-10 median at this format).  The
+// five diagonal sums combine exactly in int64 (< 2^59), go to a
+// double-double and are split greedily into nc binary16 components.
+
+constexpr int kD5 = 5;
+
+template <int NC>
+__device__ __forceinline__ double b16_val(const __half* p) {
+  double v = (double)__half2float(p[0]);
+#pragma unroll
+  for (int c = 1; c < NC; ++c) v = __dadd_rn(v, (double)__half2float(p[c]));  // exact
+  return v;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_b16_rowmax(const __half* __restrict__ x, int64_t k,
+                                                    unsigned long long* __restrict__ mx) {
+  __shared__ unsigned long long part[8];
+  const int64_t r = blockIdx.x;
+  unsigned long long m = 0;
+  for (int64_t t = threadIdx.x; t < k; t += blockDim.x)
+    m = max(m, (unsigned long long)__double_as_longlong(fabs(b16_val<NC>(x + (r * k + t) * NC))));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, part[w]);
+    mx[r] = max(part[0], m);
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_b16_colmax(const __half* __restrict__ y, int64_t k, int64_t n,
+                                                    unsigned long long* __restrict__ mx) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t t0 = (int64_t)blockIdx.y * 64, t1 = t0 + 64 < k ? t0 + 64 : k;
+  unsigned long long m = 0;
+  for (int64_t t = t0; t < t1; ++t)
+    m = max(m, (unsigned long long)__double_as_longlong(fabs(b16_val<NC>(y + (t * n + j) * NC))));
+  if (m) atomicMax(mx + j, m);
+}
+
+__device__ __forceinline__ int b16_scale_exp(unsigned long long mbits) {
+  return mbits == 0 ? 0 : ilogb(__longlong_as_double((long long)mbits)) + 2;
+}
+
+__device__ __forceinline__ void b16_digits(double v, int e, int (&d)[kD5]) {
+  long long x = __double2ll_rn(__dmul_rn(v, __longlong_as_double((long long)(1023 + 39 - e) << 52)));
+#pragma unroll
+  for (int s = kD5 - 1; s >= 1; --s) {
+    const long long t = ((x + 128) & 255) - 128;
+    d[s] = (int)t;
+    x = (x - t) >> 8;
+  }
+  d[0] = (int)x;
+}
+
+// A (m x k x NC) rows -> planes [i][s kp + kk]
+template <int NC>
+__global__ void __launch_bounds__(256) k_b16_dig_rows(const __half* __restrict__ x, int64_t rows, int64_t k,
+                                                      int64_t kp, const unsigned long long* __restrict__ mx,
+                                                      int8_t* __restrict__ out) {
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k0 >= kp) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const unsigned long long mb = mx[r];
+    const int e = b16_scale_exp(mb);
+    const bool ok = mb < 0x7ff0000000000000ull;
+    unsigned packed[kD5] = {0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (k0 + u >= k || !ok) break;
+      int d[kD5];
+      b16_digits(b16_val<NC>(x + (r * k + k0 + u) * NC), e, d);
+#pragma unroll
+      for (int s = 0; s < kD5; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
+    }
+    int8_t* row = out + r * kD5 * kp + k0;
+#pragma unroll
+    for (int s = 0; s < kD5; ++s) *reinterpret_cast<unsigned*>(row + s * kp) = packed[s];
+  }
+}
+
+// B (k x n x NC) columns -> planes [j][(kD5 - 1 - t) kp + kk] (32 x 32 tiles)
+template <int NC>
+__global__ void __launch_bounds__(256) k_b16_dig_cols(const __half* __restrict__ y, int64_t k, int64_t n,
+                                                      int64_t kp, const unsigned long long* __restrict__ mx,
+                                                      int8_t* __restrict__ out) {
+  __shared__ unsigned dg[kD5][kSlab][kSlab / 4 + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t k0 = (int64_t)blockIdx.y * kSlab, c0 = (int64_t)blockIdx.x * kSlab;
+  const int64_t c = c0 + tx;
+  const unsigned long long mb = c < n ? mx[c] : 0ull;
+  const int e = b16_scale_exp(mb);
+  const bool ok = mb < 0x7ff0000000000000ull;
+  unsigned packed[kD5] = {0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t gk = k0 + ty * 4 + u;
+    if (gk < k && c < n && ok) {
+      int d[kD5];
+      b16_digits(b16_val<NC>(y + (gk * n + c) * NC), e, d);
+#pragma unroll
+      for (int s = 0; s < kD5; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < kD5; ++s) dg[s][tx][ty] = packed[s];
+  __syncthreads();
+  const int jj = threadIdx.x >> 3, part = threadIdx.x & 7;
+  const int64_t gc = c0 + jj;
+  if (gc < n && k0 + part * 4 < kp) {
+    int8_t* dst = out + gc * kD5 * kp + k0 + part * 4;
+#pragma unroll
+    for (int s = 0; s < kD5; ++s) *reinterpret_cast<unsigned*>(dst + (kD5 - 1 - s) * kp) = dg[s][jj][part];
+  }
+}
+
+// out[i, j, :] (binary16, NC comps) from T' = sum_q S_q 256^(4 - q) (int64,
+// exact), value = T' 2^(ea + eb - 46), greedy split of the double-double
+template <int NC>
+__global__ void __launch_bounds__(256) k_b16_comb(const int* __restrict__ cq, int64_t m, int64_t n, int64_t np,
+                                                  const unsigned long long* __restrict__ amx,
+                                                  const unsigned long long* __restrict__ bmx,
+                                                  __half* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t plane = m * np;
+  const unsigned long long bm = bmx[j];
+  const int eb = b16_scale_exp(bm);
+  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+    const int64_t o = i * np + j;
+    long long t = cq[o];
+#pragma unroll
+    for (int q = 1; q < kD5; ++q) t = t * 256 + cq[q * plane + o];
+    const unsigned long long am = amx[i];
+    const double sc = pow2d(b16_scale_exp(am) + eb - 46);
+    const double hi = __ll2double_rn(t);
+    const double lo = __ll2double_rn(t - (long long)hi);  // exact: |t - hi| <= 2^10
+    double r = __dadd_rn(__dmul_rn(hi, sc), __dmul_rn(lo, sc));
+    double rl = __dsub_rn(__dmul_rn(lo, sc), __dsub_rn(r, __dmul_rn(hi, sc)));
+    const bool bad = am >= 0x7ff0000000000000ull || bm >= 0x7ff0000000000000ull;
+    __half* oe = out + (i * n + j) * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const __half h = __double2half(r);
+      const double hv = (double)__half2float(h);
+      oe[c] = bad ? __float2half(__int_as_float(0x7fffffff)) : h;
+      const double nr = __dadd_rn(__dsub_rn(r, hv), rl);  // r - hv exact when h is finite
+      rl = __dsub_rn(rl, __dsub_rn(nr, __dsub_rn(r, hv)));
+      r = isfinite(hv) ? nr : 0.0;
+    }
+  }
+}
+
 }  // namespace oz
 }  // namespace mcfg
 
@@ -1419,6 +1585,61 @@ mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, co
       cq, m, n, np, amx, bmx, c, ldc, mask);
   mcfr::note_launch();
   return mcfr::check_launch("gemm_f32 combine kernel");
+}
+
+
+// MC binary16 (nc <= 3) x MC binary16 through five-digit int8 products;
+// MCF_ERR_UNSUPPORTED outside its shapes (the caller runs the FP64 path)
+mcf_status mm_b16_i8(const void* x, const void* y, int nc, int64_t m, int64_t k, int64_t n, void* out,
+                     cudaStream_t s) {
+  using namespace mcfg::oz;
+  if (nc < 1 || nc > 3 || m < 64 || n < 64 || k < 64 || k >= 26000 || m * n >= (int64_t(1) << 31))
+    return MCF_ERR_UNSUPPORTED;
+  const int64_t kp = (k + 31) / 32 * 32, np = pad16(n);
+  const std::size_t ba = al(m * kD5 * kp), bb = al(np * kD5 * kp), bq = al((int64_t)kD5 * m * np * 4);
+  char* ws = oz_workspace(ba + bb + bq + al(m * 8) + al(np * 8), s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_mcmc: cannot allocate the digit-plane workspace");
+  int8_t* ap = reinterpret_cast<int8_t*>(ws);
+  int8_t* bp = reinterpret_cast<int8_t*>(ws + ba);
+  int* cq = reinterpret_cast<int*>(ws + ba + bb);
+  auto* amx = reinterpret_cast<unsigned long long*>(ws + ba + bb + bq);
+  auto* bmx = reinterpret_cast<unsigned long long*>(ws + ba + bb + bq + al(m * 8));
+  if (cudaMemsetAsync(amx, 0, al(m * 8) + al(np * 8), s) != cudaSuccess ||
+      (np > n && cudaMemsetAsync(bp + n * kD5 * kp, 0, (np - n) * kD5 * kp, s) != cudaSuccess))
+    return fail(MCF_ERR_CUDA, "mm_mcmc: memset");
+  const __half* xh = static_cast<const __half*>(x);
+  const __half* yh = static_cast<const __half*>(y);
+  const int sms = mcfr::sm_count();
+  const int64_t gx = (kp / 4 + 255) / 256;
+  const dim3 gdr((unsigned)gx, (unsigned)std::min<int64_t>(m, sms * 8 / gx + 1));
+  const dim3 gcm((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
+  const dim3 gdc((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
+  switch (nc) {
+#define B16_PREP(NC)                                                           \
+  case NC:                                                                     \
+    k_b16_rowmax<NC><<<(unsigned)m, 256, 0, s>>>(xh, k, amx);                  \
+    k_b16_dig_rows<NC><<<gdr, 256, 0, s>>>(xh, m, k, kp, amx, ap);             \
+    k_b16_colmax<NC><<<gcm, 256, 0, s>>>(yh, k, n, bmx);                       \
+    k_b16_dig_cols<NC><<<gdc, 256, 0, s>>>(yh, k, n, kp, bmx, bp);             \
+    break;
+    B16_PREP(1)
+    B16_PREP(2)
+    B16_PREP(3)
+#undef B16_PREP
+  }
+  for (int i = 0; i < 4; ++i) mcfr::note_launch();
+  mcf_status st = mcfr::check_launch("mm_mcmc binary16 digit kernels");
+  for (int q = 0; q < kD5 && st == MCF_OK; ++q)
+    st = gemm_s8(bp + (int64_t)(kD5 - 1 - q) * kp, kD5 * kp, ap, kD5 * kp, cq + (int64_t)q * m * np, np, m,
+                 (int64_t)(q + 1) * kp, s);
+  if (st != MCF_OK) return st;
+  const dim3 gc((unsigned)((n + 255) / 256), (unsigned)std::min<int64_t>(m, sms * 8 / ((n + 255) / 256) + 1));
+  __half* oh = static_cast<__half*>(out);
+  if (nc == 1) k_b16_comb<1><<<gc, 256, 0, s>>>(cq, m, n, np, amx, bmx, oh);
+  else if (nc == 2) k_b16_comb<2><<<gc, 256, 0, s>>>(cq, m, n, np, amx, bmx, oh);
+  else k_b16_comb<3><<<gc, 256, 0, s>>>(cq, m, n, np, amx, bmx, oh);
+  mcfr::note_launch();
+  return mcfr::check_launch("mm_mcmc binary16 combine kernel");
 }
 
 }  // namespace mcfr

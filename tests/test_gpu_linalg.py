@@ -286,3 +286,26 @@ def test_host_pipelined_fast_mm_equals_device_path(gr, port):
     gerr = port.relerr_mm_mct(x2, w, rows, cols, got.reshape(-1, 2))
     rerr = port.relerr_mm_mct(x2, w, rows, cols, ref)
     _check_within_4x(gerr, rerr, "host pipeline, inexact chunk")
+
+
+@pytest.mark.parametrize("nc", [1, 2, 3])
+def test_fast_mm_mcmc_fp16_int8_path_within_recipe_b_error(gr, port, nc):
+    """Binary16 MC x MC on the int8 tensor cores (five digits per pre-summed
+    element, shapes >= 64): within 4x of recipe B's error, both operands with
+    rows / columns of very different scales."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(70 + nc)
+    m, k, n = 96, 2048, 80
+    xs = rng.uniform(-1, 1, (m, k)) / 64 * np.exp2(rng.integers(-3, 4, (m, 1)))
+    ys = rng.uniform(-1, 1, (k, n)) / 64 * np.exp2(rng.integers(-3, 4, (1, n)))
+    x = split(xs.reshape(-1), nc, np.float16).reshape(m, k, nc)
+    y = split(ys.reshape(-1), nc, np.float16).reshape(k, n, nc)
+    got = gr.run("mm_mcmc", x, y, plan=mcf.FAST)
+    rows = np.repeat(np.arange(m), n)
+    cols = np.tile(np.arange(n), m)
+    ref = port.mm_mcmc_sampled(x, y, rows, cols)
+    gerr = port.relerr_mm_mcmc(x, y, rows, cols, got.reshape(-1, nc))
+    rerr = port.relerr_mm_mcmc(x, y, rows, cols, ref)
+    _check_within_4x(gerr, rerr, f"mm MC x MC fp16 nc={nc}, int8 path")
