@@ -96,10 +96,39 @@ template <int OP, class P, int NC, int ONC>
 constexpr bool kG2 = std::is_same<P, PB32>::value && NC == 2 && ONC == 2 &&
                      (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp || OP == kAdd);
 
+// the ops whose certified shortcut runs two elements at once (FADD2 / FMUL2 /
+// FFMA2); exp keeps a per-element binary64 exp and runs one at a time
+// (measured on B200, 2^24 config-0 elements: Mul-MCN's chained divisions
+// need 79 registers packed, one ring per SM, 294 us against 275 us scalar at
+// two rings, so it stays scalar)
 template <int OP, class P, int NC, int ONC>
+constexpr bool kG2Pair = kG2<OP, P, NC, ONC> && OP != kExp && OP != kMul;
+
+// two binary32 nc = 2 elements (x = e0c0 e0c1 e1c0 e1c1, v = v0 v1) through the
+// packed certified shortcut; returns which were accepted
+template <int OP>
+__device__ __forceinline__ g2::M2 run_g2_pair(const float (&x)[4], const float (&y)[4], float v0, float v1,
+                                              float (&o)[4]) {
+  using Q = g2::QF32x2;
+  const float2 x0 = make_float2(x[0], x[2]), x1 = make_float2(x[1], x[3]);
+  const float2 y0 = make_float2(y[0], y[2]), y1 = make_float2(y[1], y[3]);
+  const float2 v = make_float2(v0, v1);
+  float2 o0, o1;
+  g2::M2 ok;
+  if constexpr (OP == kScale) ok = g2::scale<Q>(x0, x1, v, o0, o1);
+  else if constexpr (OP == kSquare) ok = g2::square<Q>(x0, x1, o0, o1);
+  else if constexpr (OP == kDiv) ok = g2::div<Q>(x0, x1, y0, y1, o0, o1);
+  else if constexpr (OP == kDivN) ok = g2::div<Q>(v, Q::c(0.0), x0, x1, o0, o1);  // x holds the divisor
+  else if constexpr (OP == kMul) ok = g2::mul<Q>(x0, x1, y0, y1, o0, o1);
+  else ok = g2::add<Q>(x0, x1, y0, y1, o0, o1);
+  o[0] = o0.x, o[1] = o1.x, o[2] = o0.y, o[3] = o1.y;
+  return ok;
+}
+
+template <int OP, class P, int NC, int ONC, bool TRY_G2 = true>
 __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[NC], RT<P> v,
                                          RT<P> (&o)[ONC]) {
-  if constexpr (kG2<OP, P, NC, ONC>) {
+  if constexpr (TRY_G2 && kG2<OP, P, NC, ONC>) {
     using Q = g2::QF32;
     bool ok;
     if constexpr (OP == kScale) ok = g2::scale<Q>(x[0], x[1], v, o[0], o[1]);
@@ -353,9 +382,14 @@ struct Geo {
 
 }  // namespace tma
 
+// the packed certified ops need the registers of one ring per SM: at two
+// rings (56 registers) ptxas splits FADD2 / FMUL2 / FFMA2 back into scalars
+template <int OP, class P, int NC, int ONC>
+constexpr int kTmaCtas = kG2Pair<OP, P, NC, ONC> ? 1 : tma::kCtasPerSm;
+
 // vmode here is 0 (v per element) or 1 (scalar v); `tiles` full tiles only
 template <int OP, class P, int NC, int ONC>
-__global__ void __launch_bounds__(tma::kConsumerWarps * 32 + 32, tma::kCtasPerSm)
+__global__ void __launch_bounds__(tma::kConsumerWarps * 32 + 32, (kTmaCtas<OP, P, NC, ONC>))
     k_tma(const ST<P>* __restrict__ x, const ST<P>* __restrict__ y, const ST<P>* __restrict__ v,
           int vmode, ST<P>* __restrict__ out, int64_t tiles) {
   using G = tma::Geo<P, NC, OP>;
@@ -416,19 +450,53 @@ __global__ void __launch_bounds__(tma::kConsumerWarps * 32 + 32, tma::kCtasPerSm
       }
       ST<P> os[EPT * ONC];
       unsigned bail = 0;
+      if constexpr (kG2Pair<OP, P, NC, ONC> && EPT == 2) {
+        // both elements through the packed certified shortcut; a declined one
+        // re-runs the register path alone
+        float xp[4], yp[4], op[4];
 #pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        RT<P> xa[NC], ya[NC], oa[ONC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          xa[c] = P::ld(xs[i * NC + c]);
-          ya[c] = G::kY ? P::ld(ys[i * NC + c]) : RT<P>(0);
+        for (int c = 0; c < 4; ++c) {
+          xp[c] = xs[c];
+          yp[c] = G::kY ? ys[c] : 0.0f;
         }
-        RT<P> ve = RT<P>(0);
-        if constexpr (G::kV) ve = vmode == 0 ? P::ld(vv[i]) : vscalar;
-        if (!run_fast<OP, P, NC, ONC>(xa, ya, ve, oa)) bail |= 1u << i;
+        float v0 = 0.0f, v1 = 0.0f;
+        if constexpr (G::kV) {
+          v0 = vmode == 0 ? vv[0] : vscalar;
+          v1 = vmode == 0 ? vv[1] : vscalar;
+        }
+        const g2::M2 ok = run_g2_pair<OP>(xp, yp, v0, v1, op);
 #pragma unroll
-        for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
+        for (int c = 0; c < 4; ++c) os[c] = op[c];
+        const bool acc[2] = {ok.x, ok.y};
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          if (!acc[i]) {
+            RT<P> xa[NC], ya[NC], oa[ONC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              xa[c] = P::ld(xs[i * NC + c]);
+              ya[c] = G::kY ? P::ld(ys[i * NC + c]) : RT<P>(0);
+            }
+            const RT<P> ve = i == 0 ? v0 : v1;
+            if (!run_fast<OP, P, NC, ONC, false>(xa, ya, ve, oa)) bail |= 1u << i;
+#pragma unroll
+            for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          RT<P> xa[NC], ya[NC], oa[ONC];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            xa[c] = P::ld(xs[i * NC + c]);
+            ya[c] = G::kY ? P::ld(ys[i * NC + c]) : RT<P>(0);
+          }
+          RT<P> ve = RT<P>(0);
+          if constexpr (G::kV) ve = vmode == 0 ? P::ld(vv[i]) : vscalar;
+          if (!run_fast<OP, P, NC, ONC>(xa, ya, ve, oa)) bail |= 1u << i;
+#pragma unroll
+          for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
+        }
       }
       ST<P>* og = out + (t * G::kTile + l0) * ONC;
       store_stream<ST<P>, EPT * ONC>(og, os);
@@ -577,7 +645,10 @@ mcf_status launch_fast(const Args& a) {
         return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot reserve shared memory for the TMA ring");
       attr = true;
     }
-    const int64_t slots = (int64_t)mcfr::sm_count() * tma::kCtasPerSm;
+    // two rings per SM, except ScalingN packed (measured 59 us at one ring,
+    // 66 us at two): the packed ops are compiled for one ring (so ptxas keeps
+    // FADD2 / FMUL2 / FFMA2) and fit two at their register counts
+    const int64_t slots = (int64_t)mcfr::sm_count() * (kG2Pair<OP, P, NC, ONC> && OP == kScale ? 1 : tma::kCtasPerSm);
     const int grid = (int)(tiles < slots ? tiles : slots);
     kt<<<grid, tma::kConsumerWarps * 32 + 32, G::kSmem, a.stream>>>(x, y, v, vmode, out, tiles);
     mcfr::note_launch();

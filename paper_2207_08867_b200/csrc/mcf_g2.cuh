@@ -44,6 +44,8 @@ namespace g2 {
 
 template <class Q>
 using T_ = typename Q::T;
+template <class Q>
+using B_ = typename Q::B;  // per-element flags (bool, or a pair of bools)
 
 // eft.hpp:31-38
 template <class Q>
@@ -65,20 +67,13 @@ G2_HD void fast_two_sum(T_<Q> a, T_<Q> b, T_<Q>& s, T_<Q>& e) {
 template <class Q>
 G2_HD void two_prod(T_<Q> a, T_<Q> b, T_<Q>& p, T_<Q>& e) {
   p = Q::mul(a, b);
-  e = Q::fma(a, b, -p);
+  e = Q::fma(a, b, Q::neg(p));
 }
 
 // fl(x0 + x1) == x0: the reference's compressed predicate for a pair
 template <class Q>
-G2_HD bool compressed(T_<Q> x0, T_<Q> x1) {
-  return Q::add(x0, x1) == x0;
-}
-
-// the product a*b (p = fl(ab)) has an exact low part: p is large enough or a
-// factor is zero (then the product is exactly zero)
-template <class Q>
-G2_HD bool prod_ok(T_<Q> p, T_<Q> a, T_<Q> b) {
-  return Q::big(p) | (a == T_<Q>(0)) | (b == T_<Q>(0));
+G2_HD B_<Q> compressed(T_<Q> x0, T_<Q> x1) {
+  return Q::eq(Q::add(x0, x1), x0);
 }
 
 // Certify out = (A, C1) from S = A + B + R0 + rest exactly, rest_abs >= |rest|
@@ -106,33 +101,39 @@ G2_HD bool prod_ok(T_<Q> p, T_<Q> a, T_<Q> b) {
 // SWAP: no structural order between B and R0: the fast two-sum takes the
 // larger magnitude first instead of guarding.
 template <class Q, bool REST, bool DIR, bool CANON, bool TIE0 = true, bool SWAP = false>
-G2_HD bool finish(T_<Q> A, T_<Q> B, T_<Q> R0, T_<Q> rest_abs, T_<Q>& o0, T_<Q>& o1) {
+G2_HD B_<Q> finish(T_<Q> A, T_<Q> B, T_<Q> R0, T_<Q> rest_abs, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> C1, F;
-  const bool ge = Q::abs(B) >= Q::abs(R0);
-  if (SWAP) fast_two_sum<Q>(ge ? B : R0, ge ? R0 : B, C1, F);
+  const B_<Q> ge = Q::ge(Q::abs(B), Q::abs(R0));
+  if (SWAP) fast_two_sum<Q>(Q::sel(ge, B, R0), Q::sel(ge, R0, B), C1, F);
   else fast_two_sum<Q>(B, R0, C1, F);
-  const bool ord = SWAP || ge;
+  const T_<Q> zero = Q::c(0.0);
   // tie at the top: fl(A + C1) is the even neighbour; otherwise it is A
-  const T_<Q> A2 = TIE0 ? Q::add(A, C1) : A;
-  const T_<Q> C2 = !TIE0 || A2 == A ? C1 : -C1;
+  T_<Q> A2 = A, C2 = C1;
+  if (TIE0) {
+    A2 = Q::add(A, C1);
+    C2 = Q::sel(Q::eq(A2, A), C1, Q::neg(C1));
+  }
   const T_<Q> below = REST ? Q::add(Q::abs(F), rest_abs) : Q::abs(F);
   // half gaps: toward C2 at the top (S - A2 has C2's sign) or the smaller
   // one, and the smaller one below (exact unless C2 is a power of two)
   const T_<Q> h0 = DIR ? Q::hbd(A2, C2) : Q::hb(A2), h1 = Q::hb(C2);
-  const bool ok0 = (Q::abs(C2) < Q::shrink(h0)) | (TIE0 & (below == T_<Q>(0)) & (Q::abs(C2) == h0)) |
-                   (!TIE0 & (A2 == T_<Q>(0)) & (C2 == T_<Q>(0)) & (below == T_<Q>(0)));
-  const bool tie1 = REST ? (rest_abs == T_<Q>(0)) & (below == h1) : (below == h1);
-  const bool ok1 = (below < Q::shrink(h1)) | tie1;
+  const B_<Q> z0 = Q::eq(below, zero);
+  B_<Q> ok0 = Q::lt(Q::abs(C2), Q::shrink(h0));
+  if (TIE0) ok0 = ok0 | (z0 & Q::eq(Q::abs(C2), h0));
+  else ok0 = ok0 | (Q::eq(A2, zero) & Q::eq(C2, zero) & z0);
+  B_<Q> tie1 = Q::eq(below, h1);
+  if (REST) tie1 = tie1 & Q::eq(rest_abs, zero);
+  const B_<Q> ok1 = Q::lt(below, Q::shrink(h1)) | tie1;
   o0 = CANON ? Q::canon(A2) : A2;
   o1 = CANON ? Q::canon(C2) : C2;
-  return ok0 & ok1 & ord;
+  return SWAP ? ok0 & ok1 : ok0 & ok1 & ge;
 }
 
 // exact product x v (x a compressed pair, underflow guarded by the caller)
 // rounded to two components: S = A + U + w + ew after the sweep below.
 // |fl(e0 + p1)| <= 2^-22 |p0| (x compressed), so the top sum is a fast one.
 template <class Q, bool DIR, bool CANON, bool TIE0 = true>
-G2_HD bool scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
+G2_HD B_<Q> scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> p0, e0, p1, e1, a, ea, A, U;
   two_prod<Q>(x0, v, p0, e0);
   two_prod<Q>(x1, v, p1, e1);
@@ -148,9 +149,10 @@ G2_HD bool scale_core(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
 // Products are exact when the smaller one, |x1 v| (or |x0 v| when x1 = 0), is
 // at least 2^-100 or zero because a factor is.
 template <class Q>
-G2_HD bool scale(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
-  const T_<Q> xs = x1 == T_<Q>(0) ? x0 : x1;
-  const bool ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(xs, v)) | (xs == T_<Q>(0)) | (v == T_<Q>(0)));
+G2_HD B_<Q> scale(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
+  const T_<Q> zero = Q::c(0.0);
+  const T_<Q> xs = Q::sel(Q::eq(x1, zero), x0, x1);
+  const B_<Q> ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(xs, v)) | Q::eq(xs, zero) | Q::eq(v, zero));
   return scale_core<Q, false, true>(x0, x1, v, o0, o1) & ok & Q::finite(o0);
 }
 
@@ -158,7 +160,7 @@ G2_HD bool scale(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
 // add): S = x0 + x1 + y0 + y1 through four exact two-sums, the top candidate
 // re-rounded with the tail (A = fl(s + u)), the last two error terms bounded.
 template <class Q, bool CANON = true>
-G2_HD bool add(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
+G2_HD B_<Q> add(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> s, e, t, f, u, g, A, U;
   two_sum<Q>(x0, y0, s, e);
   two_sum<Q>(x1, y1, t, f);
@@ -166,16 +168,17 @@ G2_HD bool add(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
   two_sum<Q>(s, u, A, U);  // S = A + U + g + f
   // w = fl(g + f) is exact when either term is zero (frequent: f is often
   // an exact half-ulp tie residue with g = 0), else within 2^-p |w|
+  const T_<Q> zero = Q::c(0.0);
   const T_<Q> w = Q::add(g, f);
-  const T_<Q> rest = (g == T_<Q>(0)) | (f == T_<Q>(0)) ? T_<Q>(0) : Q::ulpb(w);
-  const bool ok = compressed<Q>(x0, x1) & compressed<Q>(y0, y1);
+  const T_<Q> rest = Q::sel(Q::eq(g, zero) | Q::eq(f, zero), zero, Q::ulpb(w));
+  const B_<Q> ok = compressed<Q>(x0, x1) & compressed<Q>(y0, y1);
   return finish<Q, true, false, CANON, true, true>(A, U, w, rest, o0, o1) & ok & Q::finite(o0);
 }
 
 // mc_ops.hpp:256-282 Square-MCN, nc = 2: terms x0^2 (p, e), 2 x0 x1 (2p', 2e'),
 // fl(x1^2).  x compressed => |e + 2p'| <= 2^-22 |p| (fast sum).
 template <class Q>
-G2_HD bool square(T_<Q> x0, T_<Q> x1, T_<Q>& o0, T_<Q>& o1) {
+G2_HD B_<Q> square(T_<Q> x0, T_<Q> x1, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> p, e, pp, ep, a, ea, A, U, w, ew, w2, ew2;
   two_prod<Q>(x0, x0, p, e);
   two_prod<Q>(x0, x1, pp, ep);
@@ -186,23 +189,23 @@ G2_HD bool square(T_<Q> x0, T_<Q> x1, T_<Q>& o0, T_<Q>& o1) {
   fast_two_sum<Q>(p, a, A, U);  // S = A + U + ea + 2e' + g
   two_sum<Q>(ep, g, w, ew);
   two_sum<Q>(ea, w, w2, ew2);   // S = A + U + w2 + ew2 + ew
-  const T_<Q> xs = x1 == T_<Q>(0) ? x0 : x1;
-  const bool ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(x0, xs)) | (x0 == T_<Q>(0)));
-  return finish<Q, true, false, true>(A, U, w2, Q::add(Q::abs(ew2), Q::abs(ew)), o0, o1) & ok &
-         Q::finite(o0);
+  const T_<Q> zero = Q::c(0.0);
+  const T_<Q> xs = Q::sel(Q::eq(x1, zero), x0, x1);
+  const B_<Q> ok = compressed<Q>(x0, x1) & (Q::big(Q::mul(x0, xs)) | Q::eq(x0, zero));
+  return finish<Q, true, false, true>(A, U, w2, Q::add(Q::abs(ew2), Q::abs(ew)), o0, o1) & ok & Q::finite(o0);
 }
 
 // add_kernel(r, sc) -> 2 for the division step: D = r0 + sc0 is exact
 // (Sterbenz: sc0 = -RN(q (y0 + y1)) with q = RN(r0 / y0), so |sc0| is within
 // (1 +- 2^-24)^3 of |r0|), S = D + r1 + sc1.
 template <class Q>
-G2_HD bool add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
+G2_HD B_<Q> add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> a, ea, A, U, V, eV, A2, V2;
   two_sum<Q>(r1, s1, a, ea);
   two_sum<Q>(D, a, A, U);      // S = A + U + ea
   two_sum<Q>(U, ea, V, eV);    // S = A + V + eV
   fast_two_sum<Q>(A, V, A2, V2);  // S = A2 + V2 + eV  (A2 = RN(A + V); |A| >= |V| checked)
-  return finish<Q, false, false, false>(A2, V2, eV, T_<Q>(0), o0, o1) & (Q::abs(A) >= Q::abs(V));
+  return finish<Q, false, false, false>(A2, V2, eV, Q::c(0.0), o0, o1) & Q::ge(Q::abs(A), Q::abs(V));
 }
 
 // mc_ops.hpp:188-207 div_kernel, nc = 2 (x, y compressed pairs).  Underflow
@@ -211,41 +214,41 @@ G2_HD bool add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
 // divisor component; it must be >= 2^-100, and a nonzero digit >= 2^-100
 // (normal with margin: the Sterbenz step relies on its relative rounding).
 template <class Q>
-G2_HD bool div(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
+G2_HD B_<Q> div(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
   // digit 0
   const T_<Q> q0 = Q::div(x0, y0);
   T_<Q> s0, s1, r0, r1;
-  bool ok = scale_core<Q, true, false, false>(y0, y1, -q0, s0, s1);
-  ok &= add_step<Q>(Q::add(x0, s0), x1, s1, r0, r1);
+  B_<Q> ok = scale_core<Q, true, false, false>(y0, y1, Q::neg(q0), s0, s1);
+  ok = ok & add_step<Q>(Q::add(x0, s0), x1, s1, r0, r1);
   // digit 1
   const T_<Q> q1 = Q::div(r0, y0);
-  ok &= scale_core<Q, true, false, false>(y0, y1, -q1, s0, s1);
-  ok &= add_step<Q>(Q::add(r0, s0), r1, s1, r0, r1);
+  ok = ok & scale_core<Q, true, false, false>(y0, y1, Q::neg(q1), s0, s1);
+  ok = ok & add_step<Q>(Q::add(r0, s0), r1, s1, r0, r1);
   // guard digit, then renorm(q0, q1, q2 -> 2)
   const T_<Q> q2 = Q::div(r0, y0);
   T_<Q> a, ea, A, U;
   fast_two_sum<Q>(q1, q2, a, ea);  // |q2| < |q1| < |q0| (checked)
   fast_two_sum<Q>(q0, a, A, U);    // S = A + U + ea
-  ok &= finish<Q, false, false, true>(A, U, ea, T_<Q>(0), o0, o1) & (Q::abs(q1) >= Q::abs(q2)) &
-        (Q::abs(q0) >= Q::abs(a));
-  const T_<Q> ql = q1 == T_<Q>(0) ? q0 : q1, yl = y1 == T_<Q>(0) ? y0 : y1;
-  ok &= compressed<Q>(x0, x1) & compressed<Q>(y0, y1) & (Q::big(ql) | (q0 == T_<Q>(0))) &
-        (Q::big(Q::mul(ql, yl)) | (q0 == T_<Q>(0)));
+  ok = ok & finish<Q, false, false, true>(A, U, ea, Q::c(0.0), o0, o1) & Q::ge(Q::abs(q1), Q::abs(q2)) &
+       Q::ge(Q::abs(q0), Q::abs(a));
+  const T_<Q> zero = Q::c(0.0);
+  const B_<Q> q0z = Q::eq(q0, zero);
+  const T_<Q> ql = Q::sel(Q::eq(q1, zero), q0, q1), yl = Q::sel(Q::eq(y1, zero), y0, y1);
+  ok = ok & compressed<Q>(x0, x1) & compressed<Q>(y0, y1) & (Q::big(ql) | q0z) & (Q::big(Q::mul(ql, yl)) | q0z);
   return ok & Q::finite(o0);
 }
 
 // mc_ops.hpp:216-230 Mul-MCN (fast): x / (1 / y), zero fast path
 template <class Q>
-G2_HD bool mul(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
-  if (Q::add(y1, y0) == T_<Q>(0) || Q::add(x1, x0) == T_<Q>(0)) {
-    o0 = T_<Q>(0);
-    o1 = T_<Q>(0);
-    return true;
-  }
+G2_HD B_<Q> mul(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
+  const T_<Q> zero = Q::c(0.0);
+  const B_<Q> z = Q::eq(Q::add(y1, y0), zero) | Q::eq(Q::add(x1, x0), zero);
   T_<Q> c0, c1;
-  bool ok = div<Q>(T_<Q>(1), T_<Q>(0), y0, y1, c0, c1);
-  ok &= div<Q>(x0, x1, c0, c1, o0, o1);
-  return ok;
+  B_<Q> ok = div<Q>(Q::c(1.0), zero, y0, y1, c0, c1);
+  ok = ok & div<Q>(x0, x1, c0, c1, o0, o1);
+  o0 = Q::sel(z, zero, o0);
+  o1 = Q::sel(z, zero, o1);
+  return ok | z;
 }
 
 #if defined(__CUDACC__)
@@ -253,6 +256,13 @@ G2_HD bool mul(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
 // no FTZ (the library builds with -ftz=false)
 struct QF32 {
   using T = float;
+  using B = bool;
+  __device__ __forceinline__ static T c(double v) { return (float)v; }
+  __device__ __forceinline__ static T neg(T a) { return -a; }
+  __device__ __forceinline__ static T sel(B m, T a, T b) { return m ? a : b; }
+  __device__ __forceinline__ static B eq(T a, T b) { return a == b; }
+  __device__ __forceinline__ static B lt(T a, T b) { return a < b; }
+  __device__ __forceinline__ static B ge(T a, T b) { return a >= b; }
   __device__ __forceinline__ static T add(T a, T b) { return __fadd_rn(a, b); }
   __device__ __forceinline__ static T sub(T a, T b) { return __fsub_rn(a, b); }
   __device__ __forceinline__ static T mul(T a, T b) { return __fmul_rn(a, b); }
@@ -278,6 +288,50 @@ struct QF32 {
   __device__ __forceinline__ static T shrink(T h) { return __fmul_rn(h, 1.0f - 0x1p-22f); }
   // bound on the rounding error of a binary32 result w: 2^-24 |w| >= h(w)
   __device__ __forceinline__ static T ulpb(T w) { return __fmul_rn(fabsf(w), 0x1p-24f); }
+};
+
+// Two elements in lockstep on the packed binary32 pipes (FADD2 / FMUL2 /
+// FFMA2: one instruction per pair, IEEE round-to-nearest per lane, no FTZ);
+// divisions, comparisons and selects stay per element.
+struct M2 {
+  bool x, y;
+};
+__device__ __forceinline__ M2 operator&(M2 a, M2 b) { return {a.x && b.x, a.y && b.y}; }
+__device__ __forceinline__ M2 operator|(M2 a, M2 b) { return {a.x || b.x, a.y || b.y}; }
+
+struct QF32x2 {
+  using T = float2;
+  using B = M2;
+  __device__ __forceinline__ static T c(double v) { return make_float2((float)v, (float)v); }
+  __device__ __forceinline__ static T neg(T a) { return make_float2(-a.x, -a.y); }
+  __device__ __forceinline__ static T add(T a, T b) { return __fadd2_rn(a, b); }
+  __device__ __forceinline__ static T sub(T a, T b) { return __fadd2_rn(a, neg(b)); }
+  __device__ __forceinline__ static T mul(T a, T b) { return __fmul2_rn(a, b); }
+  __device__ __forceinline__ static T fma(T a, T b, T c) { return __ffma2_rn(a, b, c); }
+  __device__ __forceinline__ static T div(T a, T b) { return make_float2(__fdiv_rn(a.x, b.x), __fdiv_rn(a.y, b.y)); }
+  __device__ __forceinline__ static T abs(T a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+  __device__ __forceinline__ static T sel(B m, T a, T b) { return make_float2(m.x ? a.x : b.x, m.y ? a.y : b.y); }
+  __device__ __forceinline__ static B eq(T a, T b) { return {a.x == b.x, a.y == b.y}; }
+  __device__ __forceinline__ static B lt(T a, T b) { return {a.x < b.x, a.y < b.y}; }
+  __device__ __forceinline__ static B ge(T a, T b) { return {a.x >= b.x, a.y >= b.y}; }
+  __device__ __forceinline__ static B finite(T a) { return {(bool)isfinite(a.x), (bool)isfinite(a.y)}; }
+  __device__ __forceinline__ static B big(T a) { return {fabsf(a.x) >= 0x1p-100f, fabsf(a.y) >= 0x1p-100f}; }
+  __device__ __forceinline__ static T canon(T a) { return __fadd2_rn(a, c(0.0)); }
+  __device__ __forceinline__ static float exp_mask(float u) {
+    return __uint_as_float(__float_as_uint(u) & 0x7f800000u);
+  }
+  __device__ __forceinline__ static T hb(T t) {
+    const float2 u = __fmul2_rn(abs(t), c(1.0 - 0x1p-24));
+    return __fmul2_rn(make_float2(exp_mask(u.x), exp_mask(u.y)), c(0x1p-24));
+  }
+  __device__ __forceinline__ static T hbd(T t, T d) {
+    const float fx = (int)(__float_as_uint(d.x) ^ __float_as_uint(t.x)) >= 0 ? 1.0f : 1.0f - 0x1p-24f;
+    const float fy = (int)(__float_as_uint(d.y) ^ __float_as_uint(t.y)) >= 0 ? 1.0f : 1.0f - 0x1p-24f;
+    const float2 u = __fmul2_rn(abs(t), make_float2(fx, fy));
+    return __fmul2_rn(make_float2(exp_mask(u.x), exp_mask(u.y)), c(0x1p-24));
+  }
+  __device__ __forceinline__ static T shrink(T h) { return __fmul2_rn(h, c(1.0 - 0x1p-22)); }
+  __device__ __forceinline__ static T ulpb(T w) { return __fmul2_rn(abs(w), c(0x1p-24)); }
 };
 
 // fl_exp<B32>(x1) = RN32(exp(x1)) for a small second component (|x1| <= 2^-12):
@@ -312,7 +366,7 @@ __device__ __forceinline__ bool exp_b32(float x0, float x1, float& o0, float& o1
   }
   float f;
   bool ok = exp_small_b32(x1, f);
-  ok &= scale<QF32>(e0, e1, f, o0, o1);
+  ok = ok & scale<QF32>(e0, e1, f, o0, o1);
   return ok;
 }
 #endif

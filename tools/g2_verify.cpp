@@ -37,6 +37,13 @@ static double rn(double x) {
 
 struct QE {
   using T = double;
+  using B = bool;
+  static T c(double v) { return v; }
+  static T neg(T a) { return -a; }
+  static T sel(B m, T a, T b) { return m ? a : b; }
+  static B eq(T a, T b) { return a == b; }
+  static B lt(T a, T b) { return a < b; }
+  static B ge(T a, T b) { return a >= b; }
   static T add(T a, T b) { return rn(a + b); }
   static T sub(T a, T b) { return rn(a - b); }
   static T mul(T a, T b) { return rn(a * b); }
