@@ -94,7 +94,8 @@ struct OpTraits {
 // it declines runs the register path below, then the literal one
 template <int OP, class P, int NC, int ONC>
 constexpr bool kG2 = std::is_same<P, PB32>::value && NC == 2 && ONC == 2 &&
-                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp || OP == kAdd);
+                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp || OP == kAdd ||
+                      OP == kGrow);
 
 // the ops whose certified shortcut runs two elements at once (FADD2 / FMUL2 /
 // FFMA2); exp keeps a per-element binary64 exp and runs one at a time
@@ -120,6 +121,7 @@ __device__ __forceinline__ g2::M2 run_g2_pair(const float (&x)[4], const float (
   else if constexpr (OP == kDiv) ok = g2::div<Q>(x0, x1, y0, y1, o0, o1);
   else if constexpr (OP == kDivN) ok = g2::div<Q>(v, Q::c(0.0), x0, x1, o0, o1);  // x holds the divisor
   else if constexpr (OP == kMul) ok = g2::mul<Q>(x0, x1, y0, y1, o0, o1);
+  else if constexpr (OP == kGrow) ok = g2::grow<Q>(x0, x1, v, o0, o1);
   else ok = g2::add<Q>(x0, x1, y0, y1, o0, o1);
   o[0] = o0.x, o[1] = o1.x, o[2] = o0.y, o[3] = o1.y;
   return ok;
@@ -137,6 +139,7 @@ __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[
     else if constexpr (OP == kDivN) ok = g2::div<Q>(v, 0.0f, x[0], x[1], o[0], o[1]);  // x holds the divisor
     else if constexpr (OP == kMul) ok = g2::mul<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kAdd) ok = g2::add<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
+    else if constexpr (OP == kGrow) ok = g2::grow<Q>(x[0], x[1], v, o[0], o[1]);
     else ok = g2::exp_b32(x[0], x[1], o[0], o[1]);
     if (__builtin_expect(ok, 1)) return true;
   }
@@ -645,10 +648,10 @@ mcf_status launch_fast(const Args& a) {
         return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot reserve shared memory for the TMA ring");
       attr = true;
     }
-    // two rings per SM, except ScalingN packed (measured 59 us at one ring,
-    // 66 us at two): the packed ops are compiled for one ring (so ptxas keeps
-    // FADD2 / FMUL2 / FFMA2) and fit two at their register counts
-    const int64_t slots = (int64_t)mcfr::sm_count() * (kG2Pair<OP, P, NC, ONC> && OP == kScale ? 1 : tma::kCtasPerSm);
+    // two rings per SM, except packed ScalingN and Grow-ExpN (measured 59 us
+    // at one ring, 66 us at two): the packed ops are compiled for one ring (so
+    // ptxas keeps FADD2 / FMUL2 / FFMA2) and fit two at their register counts
+    const int64_t slots = (int64_t)mcfr::sm_count() * (kG2Pair<OP, P, NC, ONC> && (OP == kScale || OP == kGrow) ? 1 : tma::kCtasPerSm);
     const int grid = (int)(tiles < slots ? tiles : slots);
     kt<<<grid, tma::kConsumerWarps * 32 + 32, G::kSmem, a.stream>>>(x, y, v, vmode, out, tiles);
     mcfr::note_launch();

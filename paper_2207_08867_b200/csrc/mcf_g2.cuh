@@ -156,6 +156,23 @@ G2_HD B_<Q> scale(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
   return scale_core<Q, false, true>(x0, x1, v, o0, o1) & ok & Q::finite(o0);
 }
 
+// mc_ops.hpp:118-138 Grow-ExpN, nc = 2: the ladder (two exact two-sums from
+// the smallest component up) gives S = h0 + h1 + h2 exactly; its compressed
+// shortcut equals renorm_kernel whenever it applies, so the certificate on
+// (h0, h1, h2) is the reference's result.
+// (h1 + h2 can reach past h0's rounding interval when v is as large as x0:
+// the top is re-rounded with the tail first, as in add.)
+template <class Q>
+G2_HD B_<Q> grow(T_<Q> x0, T_<Q> x1, T_<Q> v, T_<Q>& o0, T_<Q>& o1) {
+  T_<Q> q, h0, h1, h2, u, g, A, U;
+  two_sum<Q>(x1, v, q, h2);
+  two_sum<Q>(x0, q, h0, h1);
+  two_sum<Q>(h1, h2, u, g);
+  two_sum<Q>(h0, u, A, U);  // S = A + U + g
+  return finish<Q, false, false, true, true, true>(A, U, g, Q::c(0.0), o0, o1) & compressed<Q>(x0, x1) &
+         Q::finite(o0);
+}
+
 // mc_ops.hpp:173-184 add_kernel, nc = 2 -> 2 (Add-MCN; also the MLP's bias
 // add): S = x0 + x1 + y0 + y1 through four exact two-sums, the top candidate
 // re-rounded with the tail (A = fl(s + u)), the last two error terms bounded.
@@ -354,20 +371,21 @@ __device__ __forceinline__ bool exp_small_b32(float x1, float& f) {
 // greedy split of the correctly rounded binary64 exp: the short evaluation
 // of mcf_exp.cuh, certified away from binary64 midpoints), then for
 // x1 != 0 scale_kernel(out, fl_exp(x1)) through the certified scale.
+// Branch-free: both outcomes are computed and selected (x1 == 0 skips the
+// scaling in the reference; a declined element, e.g. near a binary64
+// midpoint of exp(x0), takes the register path with the correctly rounded exp).
 __device__ __forceinline__ bool exp_b32(float x0, float x1, float& o0, float& o1) {
   double E;
-  if (!rn_exp_fast((double)x0, E)) return false;  // near a binary64 midpoint: register path (cr_exp)
+  const bool oke = rn_exp_fast((double)x0, E);
   const float e0 = __double2float_rn(E);
   const float e1 = __double2float_rn(__dsub_rn(E, (double)e0));
-  if (x1 == 0.0f) {
-    o0 = e0;
-    o1 = e1;
-    return isfinite(e0);
-  }
-  float f;
-  bool ok = exp_small_b32(x1, f);
-  ok = ok & scale<QF32>(e0, e1, f, o0, o1);
-  return ok;
+  float f, s0, s1;
+  const bool okf = exp_small_b32(x1, f);
+  const bool oks = scale<QF32>(e0, e1, f, s0, s1);
+  const bool z = x1 == 0.0f;
+  o0 = z ? e0 : s0;
+  o1 = z ? e1 : s1;
+  return oke & (z ? (bool)isfinite(e0) : okf & oks);
 }
 #endif
 

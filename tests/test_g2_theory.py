@@ -3,7 +3,7 @@
 tools/g2_verify.cpp runs the SAME header on an emulated binary format with p
 significand bits and compares it with the reference's algorithms restated in
 that format (renorm_kernel with its pass cap, scale_raw, add_kernel,
-div_kernel, mul_fast_kernel, square_kernel; mc_ops.hpp:41-282):
+div_kernel, mul_fast_kernel, square_kernel, grow_kernel; mc_ops.hpp:41-282):
 
 * exhaustively over every compressed operand pair in an exponent window for
   small p, where every rounding boundary, tie and power of two is hit;
@@ -39,7 +39,7 @@ def _run(exe, *args):
         if m:
             rows[m.group(2)] = dict(cases=int(m.group(3)), acc=float(m.group(4)), bad=int(m.group(5)),
                                     cap=int(m.group(6)))
-    assert set(rows) == {"scale", "square", "div", "mul", "add"}, r.stdout + r.stderr
+    assert set(rows) == {"scale", "square", "div", "mul", "add", "grow"}, r.stdout + r.stderr
     return rows, r.returncode
 
 

@@ -138,6 +138,25 @@ static void ref_scale(const double* x, double v, double* out) {
   const int m = scale_raw(x, 2, v, st);
   renorm(st, m, out, 2);
 }
+static void ref_grow(const double* x, double v, double* out) {  // mc_ops.hpp:118-138, nc = 2
+  double h[3];
+  double q = v;
+  for (int k = 2; k >= 1; --k) {
+    const TS r = two_sum(x[k - 1], q);
+    q = r.s;
+    h[k] = r.e;
+  }
+  h[0] = q;
+  double c[3];
+  int m = 0;
+  for (int i = 0; i < 3; ++i)
+    if (h[i] != 0.0) c[m++] = h[i];
+  if (is_compressed(c, m)) {
+    for (int i = 0; i < 2; ++i) out[i] = i < m ? c[i] : 0.0;
+  } else {
+    renorm(h, 3, out, 2);
+  }
+}
 static void ref_add(const double* x, const double* y, double* out) {  // :173-184
   double h[8];
   int i = 0, j = 0, k = 0;
@@ -249,7 +268,7 @@ int main(int argc, char** argv) {
     auto X = pairs(K, 1);
     const int M = 1 << (P - 1);
     printf("p=%d: %zu compressed pairs\n", P, X.size());
-    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"};
+    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"};
 #pragma omp parallel for schedule(dynamic, 16)
     for (long long i = 0; i < (long long)X.size(); ++i) {
       const double x[2] = {X[i].first, X[i].second};
@@ -260,6 +279,11 @@ int main(int argc, char** argv) {
           const double v = s * std::ldexp(M + a, -(P - 1));
           check(ss, [&](double* o) { ref_scale(x, v, o); },
                 [&](double* o) { return g2::scale<QE>(x[0], x[1], v, o[0], o[1]); }, "sc");
+          for (int sh = -(P + 3); sh <= 2; ++sh) {  // grow by values around every component
+            const double vg = std::ldexp(v, sh);
+            check(sg, [&](double* o) { ref_grow(x, vg, o); },
+                  [&](double* o) { return g2::grow<QE>(x[0], x[1], vg, o[0], o[1]); }, "grow");
+          }
         }
       for (size_t j = 0; j < X.size(); ++j) {
         const double y[2] = {X[j].first, X[j].second};
@@ -275,13 +299,14 @@ int main(int argc, char** argv) {
                 [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
       }
     }
-    report(ss), report(sq), report(sd), report(sm), report(sa);
-    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap) ? 1 : 0;
+    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg);
+    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap |
+            sg.cap) ? 1 : 0;
   }
   // sampled, config-0 style operands: v = U(-1,1) 2^U(-8,8) split greedily into p-bit comps
   P = argc > 2 ? atoi(argv[2]) : 24;
   const long long N = argc > 3 ? atoll(argv[3]) : 2000000;
-  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"};
+  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"};
 #pragma omp parallel
   {
     std::mt19937_64 g(1234 + 7919 * (unsigned long long)omp_get_thread_num());
@@ -310,11 +335,14 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
       check(sa, [&](double* o) { ref_add(x, y, o); },
             [&](double* o) { return g2::add<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "add");
+      check(sg, [&](double* o) { ref_grow(x, v, o); },
+            [&](double* o) { return g2::grow<QE>(x[0], x[1], v, o[0], o[1]); }, "grow");
       const double yn[2] = {-x[0], -x[1] * 0.5};  // near-cancelling sums
       check(sa, [&](double* o) { ref_add(x, yn, o); },
             [&](double* o) { return g2::add<QE>(x[0], x[1], yn[0], yn[1], o[0], o[1]); }, "add");
     }
   }
-  report(ss), report(sq), report(sd), report(sm), report(sa);
-  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap) ? 1 : 0;
+  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg);
+  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap |
+          sg.cap) ? 1 : 0;
 }
