@@ -119,7 +119,7 @@ __device__ __forceinline__ g2::M2 run_g2_pair(const float (&x)[4], const float (
   if constexpr (OP == kScale) ok = g2::scale<Q>(x0, x1, v, o0, o1);
   else if constexpr (OP == kSquare) ok = g2::square<Q>(x0, x1, o0, o1);
   else if constexpr (OP == kDiv) ok = g2::div<Q>(x0, x1, y0, y1, o0, o1);
-  else if constexpr (OP == kDivN) ok = g2::div<Q>(v, Q::c(0.0), x0, x1, o0, o1);  // x holds the divisor
+  else if constexpr (OP == kDivN) ok = g2::div<Q, true>(v, Q::c(0.0), x0, x1, o0, o1);  // x holds the divisor
   else if constexpr (OP == kMul) ok = g2::mul<Q>(x0, x1, y0, y1, o0, o1);
   else if constexpr (OP == kGrow) ok = g2::grow<Q>(x0, x1, v, o0, o1);
   else ok = g2::add<Q>(x0, x1, y0, y1, o0, o1);
@@ -136,7 +136,7 @@ __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[
     if constexpr (OP == kScale) ok = g2::scale<Q>(x[0], x[1], v, o[0], o[1]);
     else if constexpr (OP == kSquare) ok = g2::square<Q>(x[0], x[1], o[0], o[1]);
     else if constexpr (OP == kDiv) ok = g2::div<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
-    else if constexpr (OP == kDivN) ok = g2::div<Q>(v, 0.0f, x[0], x[1], o[0], o[1]);  // x holds the divisor
+    else if constexpr (OP == kDivN) ok = g2::div<Q, true>(v, 0.0f, x[0], x[1], o[0], o[1]);  // x holds the divisor
     else if constexpr (OP == kMul) ok = g2::mul<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kAdd) ok = g2::add<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kGrow) ok = g2::grow<Q>(x[0], x[1], v, o[0], o[1]);

@@ -215,9 +215,16 @@ G2_HD B_<Q> square(T_<Q> x0, T_<Q> x1, T_<Q>& o0, T_<Q>& o1) {
 // add_kernel(r, sc) -> 2 for the division step: D = r0 + sc0 is exact
 // (Sterbenz: sc0 = -RN(q (y0 + y1)) with q = RN(r0 / y0), so |sc0| is within
 // (1 +- 2^-24)^3 of |r0|), S = D + r1 + sc1.
-template <class Q>
+// R1ZERO: the remainder's second component is known to be zero (the first
+// step of a division whose numerator is a single binary32, e.g. div_n, 1 / y):
+// S = D + s1 is one exact two-sum, and finish re-rounds its top.
+template <class Q, bool R1ZERO = false>
 G2_HD B_<Q> add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
   T_<Q> a, ea, A, U, V, eV, A2, V2;
+  if constexpr (R1ZERO) {
+    two_sum<Q>(D, s1, A, U);  // S = A + U exactly
+    return finish<Q, false, false, false>(A, U, Q::c(0.0), Q::c(0.0), o0, o1);
+  }
   two_sum<Q>(r1, s1, a, ea);
   two_sum<Q>(D, a, A, U);      // S = A + U + ea
   two_sum<Q>(U, ea, V, eV);    // S = A + V + eV
@@ -230,13 +237,13 @@ G2_HD B_<Q> add_step(T_<Q> D, T_<Q> r1, T_<Q> s1, T_<Q>& o0, T_<Q>& o1) {
 // smallest nonzero one is the last nonzero digit times the last nonzero
 // divisor component; it must be >= 2^-100, and a nonzero digit >= 2^-100
 // (normal with margin: the Sterbenz step relies on its relative rounding).
-template <class Q>
+template <class Q, bool X1ZERO = false>
 G2_HD B_<Q> div(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
   // digit 0
   const T_<Q> q0 = Q::div(x0, y0);
   T_<Q> s0, s1, r0, r1;
   B_<Q> ok = scale_core<Q, true, false, false>(y0, y1, Q::neg(q0), s0, s1);
-  ok = ok & add_step<Q>(Q::add(x0, s0), x1, s1, r0, r1);
+  ok = ok & add_step<Q, X1ZERO>(Q::add(x0, s0), x1, s1, r0, r1);
   // digit 1
   const T_<Q> q1 = Q::div(r0, y0);
   ok = ok & scale_core<Q, true, false, false>(y0, y1, Q::neg(q1), s0, s1);
@@ -261,7 +268,7 @@ G2_HD B_<Q> mul(T_<Q> x0, T_<Q> x1, T_<Q> y0, T_<Q> y1, T_<Q>& o0, T_<Q>& o1) {
   const T_<Q> zero = Q::c(0.0);
   const B_<Q> z = Q::eq(Q::add(y1, y0), zero) | Q::eq(Q::add(x1, x0), zero);
   T_<Q> c0, c1;
-  B_<Q> ok = div<Q>(Q::c(1.0), zero, y0, y1, c0, c1);
+  B_<Q> ok = div<Q, true>(Q::c(1.0), zero, y0, y1, c0, c1);
   ok = ok & div<Q>(x0, x1, c0, c1, o0, o1);
   o0 = Q::sel(z, zero, o0);
   o1 = Q::sel(z, zero, o1);

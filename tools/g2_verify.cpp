@@ -274,6 +274,11 @@ int main(int argc, char** argv) {
       const double x[2] = {X[i].first, X[i].second};
       check(sq, [&](double* o) { ref_square(x, o); },
             [&](double* o) { return g2::square<QE>(x[0], x[1], o[0], o[1]); }, "sq");
+      for (int a = 0; a < M; ++a) {  // div_n: a single-component numerator over x as divisor
+        const double vn[2] = {std::ldexp(M + a, -(P - 1)), 0.0};
+        check(sd, [&](double* o) { ref_div(vn, x, o); },
+              [&](double* o) { return g2::div<QE, true>(vn[0], vn[1], x[0], x[1], o[0], o[1]); }, "divn");
+      }
       for (int s = -1; s <= 1; s += 2)
         for (int a = 0; a < M; ++a) {
           const double v = s * std::ldexp(M + a, -(P - 1));
@@ -330,7 +335,7 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::div<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "div");
       const double vv[2] = {v2[0], 0.0};
       check(sd, [&](double* o) { ref_div(vv, y, o); },
-            [&](double* o) { return g2::div<QE>(vv[0], vv[1], y[0], y[1], o[0], o[1]); }, "divn");
+            [&](double* o) { return g2::div<QE, true>(vv[0], vv[1], y[0], y[1], o[0], o[1]); }, "divn");
       check(sm, [&](double* o) { ref_mul(x, y, o); },
             [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
       check(sa, [&](double* o) { ref_add(x, y, o); },
