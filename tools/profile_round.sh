@@ -14,6 +14,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
 ncu --set full --clock-control none --import-source on -k regex:cutlass -s 8 -c 1 -o gpurun_out/prof_gemm_$TAG $CMD > gpurun_out/ncu_gemm_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_slice|k_combine|k_fallback|k_rowexp|k_colmax" -c 6 -o gpurun_out/prof_oz_$TAG $CMD > gpurun_out/ncu_oz_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_tma|k_fast" -c 8 -o gpurun_out/prof_ew_$TAG $CMD > gpurun_out/ncu_ew_$TAG.log 2>&1
+# the headline step alone (kernel shares of one step)
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/step_launches_$TAG.csv python tools/headline_steps.py > /dev/null 2>&1
+python tools/step_shares.py gpurun_out/step_launches_$TAG.csv > gpurun_out/step_shares_$TAG.md 2>&1
 MLP="python tools/mlp_time.py 8192"
 $MLP > gpurun_out/plain_mlp_$TAG.log 2>&1 && \
 ncu --set full --clock-control none -k regex:"k_gemm|k_bias_act|k_ce|k_rowsum|k_sgd" -c 10 -o gpurun_out/prof_mlp_$TAG $MLP > gpurun_out/ncu_mlp_$TAG.log 2>&1
