@@ -623,8 +623,9 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
 
 struct Lt {
   cublasLtHandle_t h = nullptr;
-  void* ws = nullptr;
+  void* ws = nullptr;  // the first stream's workspace
   std::size_t ws_bytes = 0;
+  std::map<cudaStream_t, void*> ws_by_stream;  // GEMMs may run concurrently on several streams
   std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t>, cublasLtMatmulAlgo_t> algos;
 };
 std::mutex g_lt_mu;
@@ -686,7 +687,16 @@ mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, i
     it = lt.algos.emplace(key, res.algo).first;
   }
   const int32_t alpha = 1, beta = accumulate ? 1 : 0;
-  st = cublasLtMatmul(lt.h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &it->second, lt.ws, lt.ws_bytes, s);
+  void*& wss = lt.ws_by_stream[s];
+  if (!wss) {
+    if (lt.ws_by_stream.size() == 1) wss = lt.ws;
+    else if (cudaMalloc(&wss, lt.ws_bytes) != cudaSuccess) {
+      wss = nullptr;
+      cleanup();
+      return lt_fail("workspace", 0);
+    }
+  }
+  st = cublasLtMatmul(lt.h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &it->second, wss, lt.ws_bytes, s);
   cleanup();
   if (st != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtMatmul", st);
   mcfr::note_launch();
@@ -881,6 +891,30 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
     const char* e = getenv("MCF_OZ_PAIRWISE");
     return e && atoi(e) == 1;
   }();
+  // A short row block gives the int8 GEMMs few output tiles (512 x 4096:
+  // 32 tiles of 256 x 256 for 148 SMs); the diagonals' GEMMs are independent
+  // (separate int32 planes), so then they run concurrently on side streams.
+  const int64_t tiles = ((np + 255) / 256) * ((m + 255) / 256);
+  static const int conc = [] {  // MCF_OZ_CONC=0: one stream (A/B measurements)
+    const char* e = getenv("MCF_OZ_CONC");
+    return e ? atoi(e) : 4;
+  }();
+  // (measured: at 32 tiles four streams take a 512-row product from 0.65 to
+  // 0.46 ms; at 64 and 128 tiles concurrency does not pay)
+  const int ns = 3 * tiles > mcfr::sm_count()
+                     ? 1
+                     : (int)std::max<int64_t>(1, std::min<int64_t>(std::min(conc, 4), mcfr::sm_count() / std::max<int64_t>(tiles, 1)));
+  cudaStream_t gs[4] = {s, s, s, s};
+  cudaEvent_t fork_ev = nullptr, join_ev[4] = {};
+  if (ns > 1 && !pairwise) {
+    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+    cudaEventRecord(fork_ev, s);
+    for (int i = 1; i < ns; ++i) {
+      gs[i] = mcfr::side_stream(12 + i);
+      cudaStreamWaitEvent(gs[i], fork_ev, 0);
+    }
+  }
+  int gi = 0;
   for (int64_t c = 0; c < g.nkc; ++c)
     for (int q = 0; q < nq; ++q) {
       // pairs (q - t, t), t in [tl, th]: A planes q - th .. q - tl ascending,
@@ -893,10 +927,20 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
         for (int u = 0; u <= th - tl && st == MCF_OK; ++u)
           st = gemm_s8(bp + u * g.kc, ldb, ap + u * g.kc, lda, cp, np, m, g.kc, s, u > 0);
       } else {
-        st = gemm_s8(bp, ldb, ap, lda, cp, np, m, (int64_t)(th - tl + 1) * g.kc, s);
+        st = gemm_s8(bp, ldb, ap, lda, cp, np, m, (int64_t)(th - tl + 1) * g.kc, gs[gi++ % ns]);
       }
-      if (st != MCF_OK) return st;
+      if (st != MCF_OK) break;
     }
+  if (fork_ev) {
+    for (int i = 1; i < ns; ++i) {
+      cudaEventCreateWithFlags(&join_ev[i], cudaEventDisableTiming);
+      cudaEventRecord(join_ev[i], gs[i]);
+      cudaStreamWaitEvent(s, join_ev[i], 0);
+      cudaEventDestroy(join_ev[i]);
+    }
+    cudaEventDestroy(fork_ev);
+  }
+  if (st != MCF_OK) return st;
   if (ev) cudaEventRecord(ev[2], s);
   // fallback threshold (scaled units): 2^50 x the error bound per output
   // (per product bound x K); inexact elements of a six-digit B add 2^-48
