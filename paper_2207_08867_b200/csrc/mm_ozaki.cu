@@ -111,6 +111,30 @@ __device__ __forceinline__ bool digits(double hi, double lo, int (&d)[kS]) {
   return (d[6] | d[7] | d[8]) != 0 || l24 != L || r2l != 0.0;
 }
 
+// The first six digits of a single binary64 v (|v| < 1/2) when they are the
+// whole story: v 2^47 an integer (r2 = 0 below: no third limb, no carry into
+// the second), which is every binary32 element within 2^24 of its column's
+// scale.  Then the digits equal digits()'s first six (the balanced base-256
+// representation of v 2^47) and false is returned for the rest, which take
+// digits().  Two limbs instead of three, six digit cuts instead of nine.
+__device__ __forceinline__ bool digits6_exact(double v, int (&d)[kS]) {
+  const double h = __dmul_rn(v, 0x1p23);
+  const double H = rint(h);
+  const double m = __dmul_rn(__dsub_rn(h, H), 0x1p24);  // exact: h - H has <= 29 bits
+  const double M = rint(m);
+  if (m != M) return false;
+  const int c = limb_digits(__double2int_rn(M), d + 3, 3);
+  int x = __double2int_rn(H) + c;
+#pragma unroll
+  for (int s = 2; s >= 1; --s) {
+    const int t = ((x + 128) & 255) - 128;
+    d[s] = t;
+    x = (x - t) >> 8;
+  }
+  d[0] = x;
+  return true;
+}
+
 template <int NC>
 __device__ __forceinline__ void load_pair(const float* p, double& hi, double& lo, double& mag) {
   if constexpr (NC == 1) {
@@ -264,7 +288,9 @@ __global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b,
       for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * ldb + j) * NC + c];
       if (isfinite(mag)) {
         int d[kS];
-        const bool tail = digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
+        bool tail = false;
+        if (!(NC == 1 && SB == kSB1 && digits6_exact(__dmul_rn(hi, sc), d)))
+          tail = digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
         if (SB < kS && tail) ++inexact;
 #pragma unroll
         for (int t = 0; t < SB; ++t) packed[t] |= ((unsigned)(d[t] & 0xff)) << (8 * u);
