@@ -309,3 +309,23 @@ def test_fast_mm_mcmc_fp16_int8_path_within_recipe_b_error(gr, port, nc):
     gerr = port.relerr_mm_mcmc(x, y, rows, cols, got.reshape(-1, nc))
     rerr = port.relerr_mm_mcmc(x, y, rows, cols, ref)
     _check_within_4x(gerr, rerr, f"mm MC x MC fp16 nc={nc}, int8 path")
+
+
+def test_fast_mm_mcmc_fp16_int8_path_nonfinite_rows_and_columns(gr):
+    """A row of A or a column of B holding Inf / NaN makes exactly that row /
+    column of the binary16 int8-path product non-finite; the rest is finite."""
+    import paper_2207_08867_b200 as mcf
+    from mcgen import split
+
+    rng = np.random.default_rng(99)
+    m, k, n = 80, 256, 72
+    x = split(rng.uniform(-1, 1, m * k) / 64, 3, np.float16).reshape(m, k, 3)
+    y = split(rng.uniform(-1, 1, k * n) / 64, 3, np.float16).reshape(k, n, 3)
+    x[7, 3, 0] = np.inf
+    y[5, 11, 0] = np.nan
+    got = gr.run("mm_mcmc", x, y, plan=mcf.FAST).astype(np.float64).sum(axis=-1)
+    bad = np.zeros((m, n), bool)
+    bad[7, :] = True
+    bad[:, 11] = True
+    assert np.all(~np.isfinite(got[bad]))
+    assert np.all(np.isfinite(got[~bad]))
