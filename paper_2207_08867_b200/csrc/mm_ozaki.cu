@@ -529,6 +529,35 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
     // a warp keeps 4 KiB of B in flight
     const bool vec = NCB == 1 && NCA == 2 && SMEM && pair && (k & 3) == 0 &&
                      (reinterpret_cast<uintptr_t>(br) & 15) == 0;
+    // MC B (nc = 2, every c0 + c1 of the column one binary64): two k per
+    // 16-byte load (k = 2 lane + 64 (8 r + u) + q -> accumulator u)
+    const bool vec2 = NCB == 2 && NCA == 2 && SMEM && pair && (k & 1) == 0 &&
+                      (reinterpret_cast<uintptr_t>(br) & 15) == 0;
+    if (vec2) {
+      for (int64_t t0 = kb + 2 * lane; t0 < ke; t0 += 64 * U) {
+        float4 bq[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          bq[u] = t0 + 64 * u < ke ? __ldg(reinterpret_cast<const float4*>(br + (t0 + 64 * u) * NCB))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t t = t0 + 64 * u;
+          if (t >= ke) break;
+          const float4 a01 = *reinterpret_cast<const float4*>(ar + t * 2);
+          const float av[4] = {a01.x, a01.y, a01.z, a01.w}, bvq[4] = {bq[u].x, bq[u].y, bq[u].z, bq[u].w};
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double v = __dadd_rn((double)av[2 * q], (double)av[2 * q + 1]);     // exact
+            const double bb = __dadd_rn((double)bvq[2 * q], (double)bvq[2 * q + 1]);  // exact (pair column)
+            const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);
+            double e;
+            dsum(S8[u], p, S8[u], e);
+            C8[u] = __dadd_rn(C8[u], __dadd_rn(e, pe));
+          }
+        }
+      }
+    }
     if (vec) {
       for (int64_t t0 = kb + 4 * lane; t0 < ke; t0 += 128 * U) {
         float4 bq[U];
@@ -556,7 +585,7 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
         }
       }
     }
-    for (int64_t t0 = kb + lane; !vec && t0 < ke; t0 += 32 * U) {
+    for (int64_t t0 = kb + lane; !vec && !vec2 && t0 < ke; t0 += 32 * U) {
       float bv[U][NCB];
 #pragma unroll
       for (int u = 0; u < U; ++u)
