@@ -956,8 +956,17 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   }();
   // (measured: at 32 tiles four streams take a 512-row product from 0.65 to
   // 0.46 ms; at 64 and 128 tiles concurrency does not pay)
+  // Products with many tiles still leave each GEMM's last wave partly empty
+  // (4096 x 4096: 256 tiles of 256 x 256 over 74 two-SM clusters = 3.46
+  // waves); two streams let one diagonal's tiles fill the other's tail
+  // (measured: config 2 2.19 -> 2.13 ms, the MLP step 2.04 -> 1.94 ms; three
+  // streams no better).  MCF_OZ_CONC_BIG overrides.
+  static const int conc_big = [] {
+    const char* e = getenv("MCF_OZ_CONC_BIG");
+    return e ? std::max(1, std::min(4, atoi(e))) : 2;
+  }();
   const int ns = 3 * tiles > mcfr::sm_count()
-                     ? 1
+                     ? conc_big
                      : (int)std::max<int64_t>(1, std::min<int64_t>(std::min(conc, 4), mcfr::sm_count() / std::max<int64_t>(tiles, 1)));
   cudaStream_t gs[4] = {s, s, s, s};
   cudaEvent_t fork_ev = nullptr, join_ev[4] = {};
