@@ -1632,6 +1632,44 @@ mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, in
 }
 
 
+// Independent int8 GEMMs of one product spread over up to four streams
+// forked from s and joined back (same rule as rows_products: short products
+// use up to four, full-size ones two for wave-tail filling).
+struct GemmFork {
+  cudaStream_t st[4];
+  int ns = 1, next = 0;
+  cudaEvent_t fork = nullptr;
+  cudaStream_t base;
+  GemmFork(cudaStream_t s, int64_t rows_c, int64_t cols_c) : base(s) {
+    const int64_t tiles = ((rows_c + 255) / 256) * ((cols_c + 255) / 256);
+    const int sms = mcfr::sm_count();
+    ns = 3 * tiles > sms ? 2 : (int)std::max<int64_t>(1, std::min<int64_t>(4, sms / std::max<int64_t>(tiles, 1)));
+    for (auto& x : st) x = s;
+    if (ns > 1) {
+      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+      cudaEventRecord(fork, s);
+      for (int i = 1; i < ns; ++i) {
+        st[i] = mcfr::side_stream(12 + i);
+        cudaStreamWaitEvent(st[i], fork, 0);
+      }
+    }
+  }
+  cudaStream_t take() { return st[next++ % ns]; }
+  void join() {
+    if (!fork) return;
+    for (int i = 1; i < ns; ++i) {
+      cudaEvent_t j;
+      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+      cudaEventRecord(j, st[i]);
+      cudaStreamWaitEvent(base, j, 0);
+      cudaEventDestroy(j);
+    }
+    cudaEventDestroy(fork);
+    fork = nullptr;
+  }
+  ~GemmFork() { join(); }
+};
+
 // C (m x n, row-major, ldc) = op(A) op(B) in binary32 through four-digit int8
 // products (see k_f32_comb above); MCF_ERR_UNSUPPORTED for shapes it does not
 // take (the caller runs the FFMA GEMM).  op(A) = A (m x k, lda) or A^T (A
@@ -1681,11 +1719,15 @@ mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, co
   if (st != MCF_OK) return st;
   // diagonal q: A planes s = q - th .. q (ascending) against B planes t = th ..
   // q - (q - th) (stored reversed at kD4 - 1 - t: ascending positions)
-  for (int q = 0; q < kD4 && st == MCF_OK; ++q) {
-    const int th = q, tl = 0;  // pairs (q - t, t), t = 0 .. q (all within four digits)
-    const int8_t* bq = bp + (int64_t)(kD4 - 1 - th) * kp;
-    const int8_t* aq = ap + (int64_t)(q - th) * kp;
-    st = gemm_s8(bq, kD4 * kp, aq, kD4 * kp, cq + (int64_t)q * m * np, np, m, (int64_t)(th - tl + 1) * kp, s);
+  {
+    GemmFork gf(s, np, m);
+    for (int q = 0; q < kD4 && st == MCF_OK; ++q) {
+      const int th = q, tl = 0;  // pairs (q - t, t), t = 0 .. q (all within four digits)
+      const int8_t* bq = bp + (int64_t)(kD4 - 1 - th) * kp;
+      const int8_t* aq = ap + (int64_t)(q - th) * kp;
+      st = gemm_s8(bq, kD4 * kp, aq, kD4 * kp, cq + (int64_t)q * m * np, np, m, (int64_t)(th - tl + 1) * kp,
+                   gf.take());
+    }
   }
   if (st != MCF_OK) return st;
   const int64_t gcx = (n + 1023) / 1024;
@@ -1737,9 +1779,12 @@ mcf_status mm_b16_i8(const void* x, const void* y, int nc, int64_t m, int64_t k,
   }
   for (int i = 0; i < 4; ++i) mcfr::note_launch();
   mcf_status st = mcfr::check_launch("mm_mcmc binary16 digit kernels");
-  for (int q = 0; q < kD5 && st == MCF_OK; ++q)
-    st = gemm_s8(bp + (int64_t)(kD5 - 1 - q) * kp, kD5 * kp, ap, kD5 * kp, cq + (int64_t)q * m * np, np, m,
-                 (int64_t)(q + 1) * kp, s);
+  {
+    GemmFork gf(s, np, m);
+    for (int q = 0; q < kD5 && st == MCF_OK; ++q)
+      st = gemm_s8(bp + (int64_t)(kD5 - 1 - q) * kp, kD5 * kp, ap, kD5 * kp, cq + (int64_t)q * m * np, np, m,
+                   (int64_t)(q + 1) * kp, gf.take());
+  }
   if (st != MCF_OK) return st;
   const dim3 gc((unsigned)((n + 255) / 256), (unsigned)std::min<int64_t>(m, sms * 8 / ((n + 255) / 256) + 1));
   __half* oh = static_cast<__half*>(out);
