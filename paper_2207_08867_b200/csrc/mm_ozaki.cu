@@ -974,7 +974,9 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
     cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
     cudaEventRecord(fork_ev, s);
     for (int i = 1; i < ns; ++i) {
-      gs[i] = mcfr::side_stream(12 + i);
+      // the host pipeline's second compute stream (slot 5) forks to its own
+      // side streams, so two chunk products do not queue behind each other
+      gs[i] = mcfr::side_stream((s == mcfr::side_stream(5) ? 16 : 12) + i);
       cudaStreamWaitEvent(gs[i], fork_ev, 0);
     }
   }

@@ -23,7 +23,7 @@ thread_local int64_t t_launches = 0;
 std::mutex g_mu;
 
 constexpr int kMaxDev = 64;
-constexpr int kSlots = 16;
+constexpr int kSlots = 24;
 struct DevState {
   void* ws[kSlots] = {};
   std::size_t ws_bytes[kSlots] = {};
