@@ -190,19 +190,38 @@ class MCMLP:
         gemm = lib_.mcf_gemm_f32_fast if fast else lib_.mcf_gemm_f32_ordered
         rowsum = lib_.mcf_rowsum_f32_fast if fast else lib_.mcf_rowsum_f32_ordered
         gv = self.grads.views
+        # plan FAST: a layer's weight / bias gradients (and their all-reduce
+        # bucket) run on a side stream while the main stream computes the
+        # gradient for the layer below (dW and dA only share G)
+        cur = torch.cuda.current_stream()
+        wside = None
+        if fast:
+            if getattr(self, "_grad_stream", None) is None:
+                self._grad_stream = torch.cuda.Stream()
+            wside = self._grad_stream
         for l in range(L - 1, -1, -1):
             out_dim, in_dim = self.dims[l + 1], self.dims[l]
             G = B["G"][l]
+            ws = s
+            if wside is not None:
+                wside.wait_stream(cur)  # G (and the activations) are ready
+                ws = wside.cuda_stream
             # dW (out x in) = G (out x n) . A_prev^T  (A_prev is in x n)
             _check(gemm(0, 1, G.data_ptr(), n, acts[l].data_ptr(), n, gv[2 * l].data_ptr(), in_dim, out_dim, in_dim, n,
-                        None, s))
-            _check(rowsum(G.data_ptr(), out_dim, n, gv[2 * l + 1].data_ptr(), s))
-            self.grads.reduce_bucket(2 * l, 2 * l + 1)  # overlaps the next layer's backward
+                        None, ws))
+            _check(rowsum(G.data_ptr(), out_dim, n, gv[2 * l + 1].data_ptr(), ws))
+            if wside is not None:
+                with torch.cuda.stream(wside):
+                    self.grads.reduce_bucket(2 * l, 2 * l + 1)  # overlaps the next layer's backward
+            else:
+                self.grads.reduce_bucket(2 * l, 2 * l + 1)  # overlaps the next layer's backward
             if l > 0:
                 _check(lib_.mcf_approx(B32, self.W[l].data_ptr(), nc, B["Wa"][l].data_ptr(), out_dim * in_dim, s))
                 # dA_prev (in x n) = approx(W)^T (in x out) . G (out x n), ReLU mask = H_{l-1}
                 _check(gemm(1, 0, B["Wa"][l].data_ptr(), in_dim, G.data_ptr(), n, B["G"][l - 1].data_ptr(), n, in_dim,
                             n, out_dim, B["H"][l - 1].data_ptr(), s))
+        if wside is not None:
+            cur.wait_stream(wside)
         if loss_done is not None:
             torch.cuda.current_stream().wait_event(loss_done)
         self.grads.finish(B["loss"])
