@@ -1472,14 +1472,27 @@ mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t 
   char* ws = oz_workspace(bb + rows_bytes(m, k, n), s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
   PreparedB pb;
-  mcf_status st = prepare_b(a, 1, k, n, n, ws, pb, s);
+  // W's digits on a side stream while the activations are prepared
+  const RowsWs rw = rows_ws(ws + bb, m, kgeo(k), pad16(n));
+  cudaStream_t as = side_stream(12);
+  cudaEvent_t fork = nullptr, adone = nullptr;
+  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&adone, cudaEventDisableTiming);
+  cudaEventRecord(fork, s);
+  cudaStreamWaitEvent(as, fork, 0);
+  mcf_status st = a_digits(w, 2, m, kgeo(k), rw, as);
+  cudaEventRecord(adone, as);
+  if (st == MCF_OK) st = prepare_b(a, 1, k, n, n, ws, pb, s);
+  cudaStreamWaitEvent(s, adone, 0);
+  cudaEventDestroy(fork);
+  cudaEventDestroy(adone);
   if (st != MCF_OK) return st;
   Epilogue ep;
   ep.bias = bias;
   ep.h = h;
   ep.act = act;
   ep.relu = relu;
-  return rows(w, 2, m, pb, nullptr, n, ws + bb, s, nullptr, ep);
+  return rows_products(w, 2, m, pb, nullptr, n, rw, s, nullptr, ep);
 }
 
 int ozaki_digits() { return mcfg::oz::kS; }
