@@ -464,6 +464,9 @@ __global__ void __launch_bounds__(256, 3) k_combine(const int* __restrict__ cq, 
 // lists 5 or more) and every warp takes one (output, segment) item: more
 // loads in flight per SM, which is what bounds this latency-bound kernel.
 // Each lane streams its k's of the column with eight loads in flight.
+// A row whose every c0 + c1 is one binary64 is staged as those sums (same
+// bytes; three FP64-pipe instructions per k fewer in the loops: the fallback's
+// median launch 29.0 -> 26.0 us in the config-2 bench, measured on B200).
 // Products of binary32 components are exact in binary64; each lane keeps
 // eight double-doubles (k = lane + 32 (8 r + u) goes to accumulator u: two_sum
 // into S, errors into C), merged in a fixed order, across the lanes by an xor
@@ -482,6 +485,12 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
   if (cnt == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const float* ag = a + i * k * NCA;
+  // every c0 + c1 of the row one binary64 (and B single-component): one
+  // two_prod per k instead of a two_sum per component product
+  const bool rpair = NCA == 2 && !(rnf[i] & 2);
+  // such a row is staged as its binary64 sums c0 + c1 (exact; same bytes)
+  const bool dstage = SMEM && rpair;
+  double* ad = reinterpret_cast<double*>(arow);
   if constexpr (SMEM) {
     // 16-byte loads, eight in flight per thread before the stores
     const int64_t nf = k * NCA;
@@ -496,18 +505,28 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
           if (t0 + u * blockDim.x < n4) v[u] = __ldg(a4 + t0 + u * blockDim.x);
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (t0 + u * blockDim.x < n4) s4[t0 + u * blockDim.x] = v[u];
+          if (t0 + u * blockDim.x < n4) {
+            if (dstage)
+              reinterpret_cast<double2*>(arow)[t0 + u * blockDim.x] =
+                  make_double2(__dadd_rn((double)v[u].x, (double)v[u].y), __dadd_rn((double)v[u].z, (double)v[u].w));
+            else
+              s4[t0 + u * blockDim.x] = v[u];
+          }
       }
-      for (int64_t t = n4 * 4 + threadIdx.x; t < nf; t += blockDim.x) arow[t] = ag[t];
+      if (dstage) {
+        for (int64_t t = n4 * 2 + threadIdx.x; t < k; t += blockDim.x)
+          ad[t] = __dadd_rn((double)ag[2 * t], (double)ag[2 * t + 1]);
+      } else {
+        for (int64_t t = n4 * 4 + threadIdx.x; t < nf; t += blockDim.x) arow[t] = ag[t];
+      }
+    } else if (dstage) {
+      for (int64_t t = threadIdx.x; t < k; t += blockDim.x) ad[t] = __dadd_rn((double)ag[2 * t], (double)ag[2 * t + 1]);
     } else {
       for (int64_t t = threadIdx.x; t < nf; t += blockDim.x) arow[t] = ag[t];
     }
     __syncthreads();
   }
   const float* ar = SMEM ? arow : ag;
-  // every c0 + c1 of the row one binary64 (and B single-component): one
-  // two_prod per k instead of a two_sum per component product
-  const bool rpair = NCA == 2 && !(rnf[i] & 2);
   constexpr int U = 8;
   // segments per output: cnt * G <= nw (nw = 8), k split on 32 U boundaries
   const int G = cnt >= 5 ? 1 : cnt >= 3 ? 2 : cnt == 2 ? 4 : 8;
@@ -544,11 +563,12 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
         for (int u = 0; u < U; ++u) {
           const int64_t t = t0 + 64 * u;
           if (t >= ke) break;
-          const float4 a01 = *reinterpret_cast<const float4*>(ar + t * 2);
-          const float av[4] = {a01.x, a01.y, a01.z, a01.w}, bvq[4] = {bq[u].x, bq[u].y, bq[u].z, bq[u].w};
+          const double2 a01 = *reinterpret_cast<const double2*>(ad + t);
+          const double av[2] = {a01.x, a01.y};
+          const float bvq[4] = {bq[u].x, bq[u].y, bq[u].z, bq[u].w};
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const double v = __dadd_rn((double)av[2 * q], (double)av[2 * q + 1]);     // exact
+            const double v = av[q];
             const double bb = __dadd_rn((double)bvq[2 * q], (double)bvq[2 * q + 1]);  // exact (pair column)
             const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);
             double e;
@@ -569,13 +589,13 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
         for (int u = 0; u < U; ++u) {
           const int64_t t = t0 + 128 * u;
           if (t >= ke) break;
-          const float4 a01 = *reinterpret_cast<const float4*>(ar + t * 2);
-          const float4 a23 = *reinterpret_cast<const float4*>(ar + t * 2 + 4);
-          const float av[8] = {a01.x, a01.y, a01.z, a01.w, a23.x, a23.y, a23.z, a23.w};
+          const double2 a01 = *reinterpret_cast<const double2*>(ad + t);
+          const double2 a23 = *reinterpret_cast<const double2*>(ad + t + 2);
+          const double av[4] = {a01.x, a01.y, a23.x, a23.y};
           const float bvq[4] = {bq[u].x, bq[u].y, bq[u].z, bq[u].w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const double v = __dadd_rn((double)av[2 * q], (double)av[2 * q + 1]);  // exact
+            const double v = av[q];
             const double bb = (double)bvq[q];
             const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);
             double e;
@@ -596,12 +616,23 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
         const int64_t t = t0 + 32 * u;
         if (t >= ke) break;
         if (pair) {
-          const double v = __dadd_rn((double)ar[t * 2], (double)ar[t * 2 + 1]);  // exact
+          const double v = dstage ? ad[t] : __dadd_rn((double)ar[t * 2], (double)ar[t * 2 + 1]);  // exact
           const double bb = NCB == 1 ? (double)bv[u][0] : __dadd_rn((double)bv[u][0], (double)bv[u][NCB - 1]);
           const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);  // v b = p + pe exactly
           double e;
           dsum(S8[u], p, S8[u], e);
           C8[u] = __dadd_rn(C8[u], __dadd_rn(e, pe));
+        } else if (dstage) {
+          // staged row, multi-component column: v b_cb = p + pe exactly per component
+          const double v = ad[t];
+#pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) {
+            const double bb = (double)bv[u][cb];
+            const double p = __dmul_rn(v, bb), pe = __fma_rn(v, bb, -p);
+            double e;
+            dsum(S8[u], p, S8[u], e);
+            C8[u] = __dadd_rn(C8[u], __dadd_rn(e, pe));
+          }
         } else {
 #pragma unroll
           for (int ca = 0; ca < NCA; ++ca)
