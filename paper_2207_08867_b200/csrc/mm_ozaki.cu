@@ -465,8 +465,8 @@ __global__ void __launch_bounds__(256, 3) k_combine(const int* __restrict__ cq, 
 // loads in flight per SM, which is what bounds this latency-bound kernel.
 // Each lane streams its k's of the column with eight loads in flight.
 // A row whose every c0 + c1 is one binary64 is staged as those sums (same
-// bytes; three FP64-pipe instructions per k fewer in the loops: the fallback's
-// median launch 29.0 -> 26.0 us in the config-2 bench, measured on B200).
+// bytes; three FP64-pipe instructions per k fewer in the loops: config 2's
+// launch 123.7 -> 112.4 us under ncu on B200, cold caches).
 // Products of binary32 components are exact in binary64; each lane keeps
 // eight double-doubles (k = lane + 32 (8 r + u) goes to accumulator u: two_sum
 // into S, errors into C), merged in a fixed order, across the lanes by an xor
