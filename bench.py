@@ -10,8 +10,9 @@ rows are sharded across ranks (strong scaling, no data-path collective).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 The JSON line carries, besides the contract keys:
-  roofline      the mm kernel against the FP64 FMA pipe (the pipe it runs on),
-                counted in the kernel's own FP64 ops per multiply-add
+  roofline      the int8 digit GEMMs (the step's dominant kernels) against
+                B200's nominal dense INT8 rate, the measured library rates
+                beside it; fp64_pipe_path gives the FP64-pipe plan for context
   cpu_baseline  the reference's own C++ (oracle/_ref, compiled here from
                 /root/reference) timed on this box's host cores on a bounded
                 sample of the same product
@@ -43,6 +44,34 @@ def peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def int8_library_peak(torch, stream, shapes=((8192, 8192, 8192), (4096, 4096, 16384), (4096, 4096, 4096)),
+                      reps=20):
+    """cuBLASLt int8 x int8 -> int32 (torch._int_mm; B column-major, as the
+    digit GEMMs use it) at each (m, n, k) of `shapes`, best of `reps` launches
+    timed with CUDA events on `stream`: the best TOPS (2 m n k per launch)."""
+    best_tops = 0.0
+    try:
+        g = torch.Generator(device="cuda").manual_seed(7)
+        with torch.cuda.stream(stream):
+            for m, n, k in shapes:
+                x = torch.randint(-128, 128, (m, k), dtype=torch.int8, device="cuda", generator=g)
+                y = torch.randint(-128, 128, (n, k), dtype=torch.int8, device="cuda", generator=g).t()
+                torch._int_mm(x, y)
+                best = float("inf")
+                for _ in range(reps):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    torch._int_mm(x, y)
+                    e1.record(stream)
+                    e1.synchronize()
+                    best = min(best, e0.elapsed_time(e1))
+                best_tops = max(best_tops, 2.0 * m * n * k / (best * 1e-3) / 1e12)
+                del x, y
+    except Exception:
+        pass
+    return best_tops
 
 
 def ncu_traffic():
@@ -404,7 +433,17 @@ def run_ours(args):
     med = [statistics.median(p[i] for p in phases) for i in range(4)]
     gemm_ms = med[2]
     achieved = int8_ops / (gemm_ms * 1e-3) / 1e12
-    peak_i8 = 2.0 * float(pk.get("bf16_tflops", 1674.8))
+    # int8 peak: MEASURED_PEAKS.json holds only bf16, and its cuBLAS 8192^3
+    # figure x 2 can sit below what cuBLASLt's IMMA reaches on the same pod, so
+    # the int8 library GEMM is also measured live (8192^3, best of 10) and the
+    # larger of the two is the denominator
+    peak_bf16x2 = 2.0 * float(pk.get("bf16_tflops", 1674.8))
+    peak_i8_live = int8_library_peak(torch, stream)
+    # both measured figures sit below what the digit GEMMs themselves reach
+    # (r01l: 3.25 / 3.17 vs 3.35 POPS), so neither is a ceiling: the denominator
+    # is B200's nominal dense INT8 rate (4.5 POPS, 2x dense BF16), the measured
+    # figures stay in the line beside it
+    peak_i8 = max(4500.0, peak_bf16x2, peak_i8_live)
     # context: the same product on the FP64 pipe (MCF_FAST_FP64, offset accumulation)
     f64 = C.c_double(0.0)
     f32 = C.c_double(0.0)
@@ -498,7 +537,11 @@ def run_ours(args):
                          "kernel": "int8 digit GEMMs (cuBLASLt IMMA, s8 x s8 -> s32), %d per step, %d GEMM-equivalents"
                                    % (digits, gemm_equiv),
                          "algorithmic_int8_ops_per_step": int8_ops,
-                         "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (B200 dense INT8 = 2x dense BF16)",
+                         "peak_source": "B200 nominal dense INT8 (4.5 POPS); measured figures below it in "
+                                        "peak_measured (the digit GEMMs exceed both)",
+                         "peak_measured": {"2x_MEASURED_PEAKS_bf16": round(peak_bf16x2, 1),
+                                           "cublaslt_int8_live_best_of_8192^3_4096^2x16384_4096^3": round(peak_i8_live, 1),
+                                           "frac_vs_live_int8": round(achieved / peak_i8_live, 3) if peak_i8_live else None},
                          "step_phases_ms": {"b_digits": round(med[0], 3), "a_digits": round(med[1], 3),
                                             "int8_gemms": round(med[2], 3), "combine_fallback": round(med[3], 3)},
                          "fallback_outputs": int(fb.value)},
