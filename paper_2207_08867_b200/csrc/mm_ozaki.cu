@@ -460,7 +460,8 @@ __global__ void __launch_bounds__(256, 3) k_combine(const int* __restrict__ cq, 
 // the listed outputs: a CTA per row.  The CTA stages its row of A in shared
 // memory (SMEM; rows too long for it read A through L1).  A row lists few
 // outputs (config 2: 3.6 on average), so each listed output's k range is cut
-// into G segments (G a power of two with cnt G <= 8 warps; G = 1 when the row
+// into G segments (G a power of two with cnt G <= 8 items, spread over the
+// CTA's warps; G = 1 when the row
 // lists 5 or more) and every warp takes one (output, segment) item: more
 // loads in flight per SM, which is what bounds this latency-bound kernel.
 // Each lane streams its k's of the column with eight loads in flight.
@@ -528,7 +529,8 @@ __global__ void __launch_bounds__(256) k_fallback(const float* __restrict__ a, c
   }
   const float* ar = SMEM ? arow : ag;
   constexpr int U = 8;
-  // segments per output: cnt * G <= nw (nw = 8), k split on 32 U boundaries
+  // segments per output: cnt * G <= 8 items (taken by the nw warps in turn; G
+  // depends only on cnt, so the result does not depend on nw), k split on 32 U boundaries
   const int G = cnt >= 5 ? 1 : cnt >= 3 ? 2 : cnt == 2 ? 4 : 8;
   const int64_t seg = ((k + G - 1) / G + 32 * U - 1) / (32 * U) * (32 * U);
   for (int w = warp; w < cnt * G; w += nw) {
@@ -697,7 +699,10 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
       cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
       attr = true;
     }
-    k_fallback<NCA, NCB, true><<<(unsigned)m, 256, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
+    // 128-thread CTAs (four per SM at 126 registers): one CTA's staging
+    // overlaps another's B streaming; config 2's launch 112 -> 98 us under ncu
+    // (cold; 256 and 64 threads both 111-115 us, r01m)
+    k_fallback<NCA, NCB, true><<<(unsigned)m, 128, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   } else {
     k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   }
