@@ -699,10 +699,13 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
       cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
       attr = true;
     }
-    // 128-thread CTAs (four per SM at 126 registers): one CTA's staging
-    // overlaps another's B streaming; config 2's launch 112 -> 98 us under ncu
-    // (cold; 256 and 64 threads both 111-115 us, r01m)
-    k_fallback<NCA, NCB, true><<<(unsigned)m, 128, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
+    // 128-thread CTAs (four per SM at 126 registers) while four rows fit in
+    // shared memory: one CTA's staging overlaps another's B streaming; config
+    // 2's launch 112 -> 98 us under ncu (cold; 256 and 64 threads both 111-115
+    // us, r01m).  Longer rows keep 256 threads, so the SM's warp count does
+    // not halve when shared memory allows fewer CTAs.
+    const int thr = sm <= (48u << 10) ? 128 : 256;
+    k_fallback<NCA, NCB, true><<<(unsigned)m, thr, sm, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   } else {
     k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   }
