@@ -150,15 +150,26 @@ mcf_status mcf_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t
 /* out[b,:] = sum_k x[b,k,:] * y[b,k,:]  (batched MC x MC dots) */
 mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t batch,
                         int64_t k, void* out, int strategy, mcf_stream stream);
-/* Digits of the MC operand in the MCF_FAST tensor-core splitting (mm_ozaki.cu). */
+/* MCF_FAST tensor-core scheme (mm_ozaki.cu): the binary32 nc=2 MC x T / MC x MC
+ * contractions are exact integer products by Chinese remaindering over n
+ * moduli (one int8 GEMM each).  mcf_fast_tc_digits: moduli of a K = 4096
+ * MC x T product (kept for ABI compatibility). */
 int mcf_fast_tc_digits(void);
-/* int8 GEMM-equivalents (M x N x K each) of one tensor-core product of
- * depth k whose second operand has b_components components per element
- * (1: Tensor, 2: MC). */
+/* int8 GEMMs (M x N x K each) of one tensor-core product of depth k whose
+ * second operand has b_components components per element (1: Tensor, 2: MC). */
 int mcf_fast_tc_gemm_equivalents(int b_components, int64_t k);
+/* Host-only introspection (no device needed): the plan of a depth-k product
+ * (moduli count, integer bits kept of A and of B); returns the moduli count
+ * (0: k outside the scheme). */
+int mcf_fast_tc_plan(int64_t k, int b_components, int* moduli, int* bits_a, int* bits_b);
+/* The reconstruction constants of n moduli: moduli[n], w_slices[n * S] (the
+ * symmetric CRT weights in S balanced 11-bit slices), m_slices[S] (the
+ * modulus product M), q_scale = RN32(2^(L-11) / M), m_bits = L; returns S
+ * (0 for n outside 1..22).  Null pointers are skipped. */
+int mcf_fast_tc_crt_table(int n, int* moduli, float* w_slices, float* m_slices, float* q_scale, int* m_bits);
 /* Instrumentation: one MC(nc=2, binary32) x T product on the tensor-core
- * path with per-phase device times (phase_ms[4]: B digits, A digits, int8
- * GEMMs, recombination + fallback) and the number of outputs recomputed by
+ * path with per-phase device times (phase_ms[4]: B residues, A residues, int8
+ * GEMMs, reconstruction + fallback) and the number of outputs recomputed by
  * the fallback.  Synchronises the stream. */
 mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
                               double* phase_ms, int64_t* fallback_outputs, mcf_stream stream);

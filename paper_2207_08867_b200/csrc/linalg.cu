@@ -520,6 +520,14 @@ int mcf_fast_tc_gemm_equivalents(int b_components, int64_t k) {
   return mcfr::ozaki_gemm_equivalents(b_components, k);
 }
 
+int mcf_fast_tc_plan(int64_t k, int b_components, int* moduli, int* bits_a, int* bits_b) {
+  return mcfr::ozaki_crt_info(k, b_components, moduli, bits_a, bits_b);
+}
+
+int mcf_fast_tc_crt_table(int n, int* moduli, float* w_slices, float* m_slices, float* q_scale, int* m_bits) {
+  return mcfr::ozaki_crt_table(n, moduli, w_slices, m_slices, q_scale, m_bits);
+}
+
 mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
                               double* phase_ms, int64_t* fallback_outputs, mcf_stream stream) {
   if (!x || !w || !out || !phase_ms || !fallback_outputs)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "../../include/mcf_gpu.h"
@@ -20,6 +21,10 @@ void note_launch();
 mcf_status check_launch(const char* what);
 
 int sm_count();
+// fn() once per (device, tag), thread-safe (per-device kernel attributes and
+// __constant__ tables: both are per-device state).  Tags: see kOnce* below.
+void per_device_once(int tag, const std::function<void()>& fn);
+enum : int { kOnceEwSmem = 0, kOnceMmSmem = 1, kOnceFallbackSmem = 2, kOnceCrtTables = 3, kOnceTcGemm = 4 };
 // grid for a grid-stride kernel: enough CTAs to fill every SM `per_sm` deep,
 // never more than needed to cover `work_items` with `threads` each.
 inline int grid_for(int64_t work_items, int threads, int per_sm) {
@@ -70,6 +75,8 @@ mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, co
 mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t k, int64_t n, const float* bias,
                              int relu, float* h, float* act, cudaStream_t s);
 int ozaki_gemm_equivalents(int ncb, int64_t k);
+int ozaki_crt_info(int64_t k, int ncb, int* n, int* pa, int* pb);
+int ozaki_crt_table(int n, int* moduli, float* w, float* mh, float* cq, int* bits);
 mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, double* ms,
                         int64_t* fallback, cudaStream_t s);
 mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout, float* dx,
@@ -82,6 +89,8 @@ mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t
 // device workspace for the host-buffer entry points (grows, per device)
 void* workspace(std::size_t bytes, int slot);
 cudaStream_t side_stream(int slot);
+// reusable fork / join event, per host thread and device (slot < 16)
+cudaEvent_t tl_event(int slot);
 void* pinned(std::size_t bytes, int slot);
 
 }  // namespace mcfr

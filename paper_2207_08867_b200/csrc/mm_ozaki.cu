@@ -4,37 +4,45 @@
 // arithmetic; its error is set by the nc-component result (2^-51.7
 // median / 2^-49.1 max at nc=2 fp32).  On B200 the fastest exact arithmetic
 // for a GEMM is the INT8 tensor core (int32 accumulation is exact), so the
-// product is computed as an error-free integer splitting (Ozaki scheme):
+// product is computed as an exact integer product by Chinese remaindering
+// (the modular integer splitting known as Ozaki scheme II):
 //
 //   * every row i of A is scaled by 2^-ea[i] and every column j of B by
-//     2^-eb[j] (powers of two, exact) so all values lie in (-1/2, 1/2);
-//   * each scaled value v = c0 + c1 (exact binary64 pair) becomes kS = 9
-//     balanced base-256 digits: v = sum_s d_s 2^(-7-8s) + r, d_0 in [-64, 64],
-//     d_s in [-128, 127], |r| <= 2^-72 (1 + 2^-50);
-//   * K is cut into chunks of kc <= 14400; for each chunk and each diagonal
-//     q = s + t < kS one int8 GEMM whose K dimension is the q+1 digit planes
-//     of the chunk laid end to end gives C_cq = sum_{s+t=q} A_s B_t exactly in
-//     int32 ((q+1) kc 2^14 < 2^31);
-//   * C = sum_{c,q} C_cq 2^(-14-8q) is formed exactly (int64 over chunks,
-//     then double-double), scaled back and split greedily into the two
-//     binary32 output components.
+//     2^-eb[j] (powers of two above twice the line's max |c0 + c1|, exact), so
+//     all values lie in (-1/2, 1/2), and rounded to integers
+//     A' = round(A 2^pa) (|A'| < 2^(pa-1), error <= 0.51 units) and
+//     B' = round(B 2^pb); a binary32 B keeps pb = 48 bits, exact for every
+//     element within 2^23 binades of its column's scale (the others are
+//     counted per column and their rounding enters that column's bound);
+//   * n pairwise coprime moduli m_t <= 256 with M = prod m_t >= 4 K 2^(pa+pb-2)
+//     (17 at config 2): for each t one int8 GEMM of the symmetric residues
+//     A' mod m_t, B' mod m_t (|r| <= 128, exact int32 sums for K < 2^17) gives
+//     C' mod m_t;
+//   * C' = sum_t r_t w_t - q M (w_t the CRT weights, q = round(T / M)) is
+//     formed exactly: the weights are cut into nine balanced 11-bit slices, so
+//     every slice sum T_j = sum_t r_t w_tj and D_j = T_j - q M_j is an exact
+//     binary32 integer, and the slices are joined by a binary64 Horner pass
+//     whose partial sums are exact while they matter (|C'| <= M/4);
+//   * C = C' 2^(ea+eb-pa-pb), split greedily into the binary32 components.
 //
-// Error per product <= 2^-73 + 2^-73 + 8.04 2^-72 <= 2^-68.8 (scaled units)
-// -- the truncations of both operands and the dropped diagonals q >= kS --
-// so per output <= K 2^-68.8.  Outputs whose magnitude is not at least 2^50
-// times that bound (cancellation; rows or columns holding Inf/NaN) are listed
-// per row and recomputed by the fallback kernel in double-double from the
-// binary32 operands, so every output has relative error <= 2^-50 before the
-// final split -- the resolution of the reference's own nc=2 result (its
-// measured max relative error is 2^-49.1).
+// Error per output (scaled units) <= K 2^-(pa+1) (+ the counted inexact B
+// elements): 2^-62 at config 2, ~30x tighter than the nine-digit splitting
+// this replaces, with 17 int8 GEMMs instead of 39 GEMM-equivalents.  Outputs
+// whose magnitude is not at least 2^50 times their bound (cancellation) and
+// rows / columns holding Inf or NaN are listed per row and recomputed by the
+// fallback kernel in double-double from the binary32 operands, so every
+// output has relative error <= 2^-50 before the final split -- the resolution
+// of the reference's own nc=2 result (its measured max is 2^-49.1).
 //
-// The int8 GEMMs are plain library GEMMs (cuBLASLt IMMA, TN, s8 x s8 -> s32);
-// the scaling, digit extraction, transposes, recombination + split and the
-// cancellation fallback are this file's kernels.
+// The int8 GEMMs are plain library GEMMs (cuBLASLt IMMA, TN, s8 x s8 -> s32,
+// one strided-batched call over the moduli); the scaling, residue extraction,
+// transposes, CRT reconstruction + split and the cancellation fallback are
+// this file's kernels.
 #include <cublasLt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <map>
@@ -53,87 +61,13 @@ namespace mcfg {
 namespace oz {
 namespace {
 
-constexpr int kS = 9;                // digits of A (and of an MC B)
-constexpr int kQmax = 10;            // diagonals kept: q < nq, nq = 9, or 10 for long K
-constexpr int kSB1 = 6;              // digits of a single-component (binary32) B
-constexpr int kSlab = 32;            // transpose tile of the column slicer
-constexpr int64_t kMaxChunk = 14400; // int32 headroom: kS * kc * 2^14 < 2^31
-constexpr int64_t kMaxChunks = 16;    // combine: 16 chunk sums x 2^16.01 x 2^31 < 2^53
+constexpr int kSlab = 32;  // transpose tile of the column kernels
 
 __device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
 // 2^e > 2 m (m >= 0 finite): scaled values lie in (-1/2, 1/2); 0 for m == 0
 // or non-finite (those rows / columns go to the fallback list)
 __device__ __forceinline__ int exp_above_d(double m) { return m > 0.0 && isfinite(m) ? ilogb(m) + 2 : 0; }
-
-// one 24-bit limb (plus the carry from below) -> `cnt` balanced base-256
-// digits, least significant first at d[cnt-1]; returns the carry out
-__device__ __forceinline__ int limb_digits(int x, int* d, int cnt) {
-#pragma unroll
-  for (int s = cnt - 1; s >= 0; --s) {
-    const int t = ((x + 128) & 255) - 128;
-    d[s] = t;
-    x = (x - t) >> 8;
-  }
-  return x;
-}
-
-// kS digits of v = hi + lo (|v| < 1/2, exact pair).  Three binary64 steps give
-// the limbs H = rint(v 2^23), M = rint(r1 2^24), L = rint(r2 2^24)
-// (|H| <= 2^22, |M|, |L| <= 2^23, r1 = v 2^23 - H, r2 = r1 2^24 - M, all
-// |r| <= 1/2 (1 + tiny)), v = H 2^-23 + M 2^-47 + L 2^-71 + r3 2^-71; the
-// limbs are then cut into digits bottom-up with integer operations.
-// Returns true when v differs from its first six digits (digits 6..8 or the
-// final remainder nonzero): a binary32 B element within 2^24 of its column's
-// scale is exact in six.
-__device__ __forceinline__ bool digits(double hi, double lo, int (&d)[kS]) {
-  const double h = __dmul_rn(hi, 0x1p23), hl = __dmul_rn(lo, 0x1p23);
-  const double H = rint(h);
-  double r1, r1l;
-  dsum(__dsub_rn(h, H), hl, r1, r1l);
-  const double m = __dmul_rn(r1, 0x1p24), ml = __dmul_rn(r1l, 0x1p24);
-  const double M = rint(m);
-  double r2, r2l;
-  dsum(__dsub_rn(m, M), ml, r2, r2l);
-  const double l24 = __dmul_rn(r2, 0x1p24);
-  const double L = rint(l24);
-  int c = limb_digits(__double2int_rn(L), d + 6, 3);
-  c = limb_digits(__double2int_rn(M) + c, d + 3, 3);
-  // top limb: two balanced digits, the remainder (|.| <= 64) is d_0
-  int x = __double2int_rn(H) + c;
-#pragma unroll
-  for (int s = 2; s >= 1; --s) {
-    const int t = ((x + 128) & 255) - 128;
-    d[s] = t;
-    x = (x - t) >> 8;
-  }
-  d[0] = x;
-  return (d[6] | d[7] | d[8]) != 0 || l24 != L || r2l != 0.0;
-}
-
-// The first six digits of a single binary64 v (|v| < 1/2) when they are the
-// whole story: v 2^47 an integer (r2 = 0 below: no third limb, no carry into
-// the second), which is every binary32 element within 2^24 of its column's
-// scale.  Then the digits equal digits()'s first six (the balanced base-256
-// representation of v 2^47) and false is returned for the rest, which take
-// digits().  Two limbs instead of three, six digit cuts instead of nine.
-__device__ __forceinline__ bool digits6_exact(double v, int (&d)[kS]) {
-  const double h = __dmul_rn(v, 0x1p23);
-  const double H = rint(h);
-  const double m = __dmul_rn(__dsub_rn(h, H), 0x1p24);  // exact: h - H has <= 29 bits
-  const double M = rint(m);
-  if (m != M) return false;
-  const int c = limb_digits(__double2int_rn(M), d + 3, 3);
-  int x = __double2int_rn(H) + c;
-#pragma unroll
-  for (int s = 2; s >= 1; --s) {
-    const int t = ((x + 128) & 255) - 128;
-    d[s] = t;
-    x = (x - t) >> 8;
-  }
-  d[0] = x;
-  return true;
-}
 
 template <int NC>
 __device__ __forceinline__ void load_pair(const float* p, double& hi, double& lo, double& mag) {
@@ -148,23 +82,353 @@ __device__ __forceinline__ void load_pair(const float* p, double& hi, double& lo
   }
 }
 
-// K chunking: kc (multiple of 16) and the number of chunks; a row of digit
-// planes is [chunk 0: kS planes of kc bytes][chunk 1: ...]
-struct KGeo {
-  int64_t k, kc, nkc;
-  __host__ __device__ int64_t row_bytes(int planes = kS) const { return planes * kc * nkc; }
-};
+// ---- moduli and CRT constants ------------------------------------------------------------
 
-// kc is a multiple of 32, so a 32-wide k tile never straddles two chunks
-KGeo kgeo(int64_t k) {
-  const int64_t k32 = (k + 31) / 32 * 32;
-  const int64_t nkc = (k32 + kMaxChunk - 1) / kMaxChunk;
-  const int64_t kc = ((k32 + nkc - 1) / nkc + 31) / 32 * 32;
-  return KGeo{k, kc, nkc};
+constexpr int kMaxMod = 22;
+// pairwise coprime, largest first (256 = 2^8, 255 = 3 5 17, 253 = 11 23,
+// 247 = 13 19, 217 = 7 31, the rest prime); n moduli = the first n
+constexpr int kModuli[kMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223,
+                                  217, 211, 199, 197, 193, 191, 181, 179, 173, 167, 163};
+constexpr int kMinMod = 16;     // instantiated moduli counts: kMinMod .. kMaxMod
+constexpr int kSlices = 9;      // balanced 11-bit slices of the CRT weights
+constexpr float kMagic = 12582912.0f;  // 1.5 2^23: x + kMagic has x in its low mantissa bits (|x| < 2^22)
+
+struct CrtTab {
+  float w[kMaxMod][kSlices];  // slice j of the symmetric CRT weight w_t (weight 2^(L - 11 (j + 1)))
+  float mh[kSlices];          // slices of M
+  float cq;                   // RN32(2^(L - 11) / M)
+  int L;                      // bit length of M
+};
+__constant__ float c_pw[kMaxMod][6];  // 2^(12 j) mod m_t, symmetric (limb weights of the residue sums)
+__constant__ float c_c14[kMaxMod];    // 2^14 mod m_t, symmetric
+__constant__ float c_inv[kMaxMod];    // RN32(1 / m_t)
+__constant__ float c_mod[kMaxMod];
+__constant__ CrtTab c_crt[kMaxMod + 1];  // by moduli count
+
+// ---- host: exact CRT constants (small unsigned big integers) ----
+
+struct Big {  // non-negative, 32-bit words little-endian
+  uint32_t w[8] = {};
+};
+void big_mul(Big& x, uint32_t k) {
+  uint64_t c = 0;
+  for (auto& v : x.w) {
+    const uint64_t t = (uint64_t)v * k + c;
+    v = (uint32_t)t;
+    c = t >> 32;
+  }
+}
+uint32_t big_divmod(Big& x, uint32_t m) {  // x /= m; returns x mod m
+  uint64_t r = 0;
+  for (int i = 7; i >= 0; --i) {
+    const uint64_t t = (r << 32) | x.w[i];
+    x.w[i] = (uint32_t)(t / m);
+    r = t % m;
+  }
+  return (uint32_t)r;
+}
+int big_bitlen(const Big& x) {
+  for (int i = 7; i >= 0; --i)
+    if (x.w[i]) return 32 * i + 32 - __builtin_clz(x.w[i]);
+  return 0;
+}
+int big_bit(const Big& x, int b) { return b < 0 || b >= 256 ? 0 : (int)((x.w[b >> 5] >> (b & 31)) & 1u); }
+int big_bits(const Big& x, int lo, int cnt) {
+  int v = 0;
+  for (int i = cnt - 1; i >= 0; --i) v = 2 * v + big_bit(x, lo + i);
+  return v;
+}
+bool big_le(const Big& a, const Big& b) {
+  for (int i = 7; i >= 0; --i)
+    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  return true;
+}
+void big_sub(Big& a, const Big& b) {  // a -= b, b <= a
+  int64_t br = 0;
+  for (int i = 0; i < 8; ++i) {
+    int64_t t = (int64_t)a.w[i] - (int64_t)b.w[i] - br;
+    br = t < 0 ? 1 : 0;
+    a.w[i] = (uint32_t)(t + (br << 32));
+  }
+}
+double big_double(const Big& x) {
+  double d = 0.0;
+  for (int i = 7; i >= 0; --i) d = d * 4294967296.0 + (double)x.w[i];
+  return d;
+}
+int modinv(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
+  int t = 0, nt = 1, r = m, nr = a % m;
+  while (nr) {
+    const int q = r / nr, t2 = t - q * nt, r2 = r - q * nr;
+    t = nt, nt = t2, r = nr, nr = r2;
+  }
+  return t < 0 ? t + m : t;
+}
+int sym(int v, int m) {  // symmetric representative of v mod m
+  v %= m;
+  if (v < 0) v += m;
+  return v > m / 2 ? v - m : v;
+}
+// balanced slices of x (0 <= x < 2^L) at weights 2^(L - 11 (j + 1)), the last
+// one rounded: |x - sum_j d_j 2^(L - 11 (j + 1))| <= 2^(L - 11 kSlices - 1);
+// |d_j| <= 2^10 for j >= 1, d_0 <= 2^11 (x < 2^(L-1) gives d_0 <= 2^10)
+void slices(const Big& x, int L, float* out) {
+  int d[kSlices];
+  for (int j = 0; j < kSlices; ++j) d[j] = big_bits(x, L - 11 * (j + 1), 11);
+  if (big_bit(x, L - 11 * kSlices - 1)) ++d[kSlices - 1];
+  for (int j = kSlices - 1; j > 0; --j)
+    if (d[j] >= 1024) {
+      d[j] -= 2048;
+      ++d[j - 1];
+    }
+  for (int j = 0; j < kSlices; ++j) out[j] = (float)d[j];
 }
 
-// row exponents of A (rows x k, NC comps, row stride lda elements): warp per
-// row, max of |c0| + |c1|
+struct HostCrt {
+  CrtTab tab[kMaxMod + 1];
+  double log2m[kMaxMod + 1];
+  float pw[kMaxMod][6], c14[kMaxMod], inv[kMaxMod], mod[kMaxMod];
+};
+const HostCrt& host_crt() {
+  static const HostCrt h = [] {
+    HostCrt h{};
+    for (int t = 0; t < kMaxMod; ++t) {
+      const int m = kModuli[t];
+      int p = 1 % m;
+      for (int j = 0; j < 6; ++j) {
+        h.pw[t][j] = (float)sym(p, m);
+        for (int b = 0; b < 12; ++b) p = p * 2 % m;
+      }
+      int p14 = 1;
+      for (int b = 0; b < 14; ++b) p14 = p14 * 2 % m;
+      h.c14[t] = (float)sym(p14, m);
+      h.inv[t] = 1.0f / (float)m;
+      h.mod[t] = (float)m;
+    }
+    for (int n = 1; n <= kMaxMod; ++n) {
+      Big M;
+      M.w[0] = 1;
+      for (int t = 0; t < n; ++t) big_mul(M, (uint32_t)kModuli[t]);
+      const int L = big_bitlen(M);
+      CrtTab& tb = h.tab[n];
+      tb.L = L;
+      const double md = big_double(M);
+      h.log2m[n] = std::log2(md);
+      tb.cq = (float)(std::ldexp(1.0, L - 11) / md);
+      slices(M, L, tb.mh);
+      for (int t = 0; t < n; ++t) {
+        Big mt = M;
+        big_divmod(mt, (uint32_t)kModuli[t]);  // M / m_t
+        Big tmp = mt;
+        const int inv = modinv((int)big_divmod(tmp, (uint32_t)kModuli[t]), kModuli[t]);
+        Big w = mt;
+        big_mul(w, (uint32_t)inv);  // w_t = (M / m_t) ((M / m_t)^-1 mod m_t) < M
+        Big w2 = w;
+        big_mul(w2, 2);
+        const bool neg = !big_le(w2, M);  // symmetric: w_t - M when w_t > M / 2
+        if (neg) {
+          Big d = M;
+          big_sub(d, w);
+          w = d;
+        }
+        slices(w, L, tb.w[t]);
+        if (neg)
+          for (auto& v : tb.w[t]) v = -v;
+      }
+    }
+    return h;
+  }();
+  return h;
+}
+
+mcf_status upload_crt_tables() {
+  mcf_status st = MCF_OK;
+  mcfr::per_device_once(mcfr::kOnceCrtTables, [&] {
+    const HostCrt& h = host_crt();
+    if (cudaMemcpyToSymbol(c_pw, h.pw, sizeof(h.pw)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_c14, h.c14, sizeof(h.c14)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_inv, h.inv, sizeof(h.inv)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_mod, h.mod, sizeof(h.mod)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_crt, h.tab, sizeof(h.tab)) != cudaSuccess)
+      st = mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot upload the CRT tables");
+  });
+  return st;
+}
+
+// Moduli count and operand precisions of a K-long product.  A binary32 B keeps
+// pb = 48 bits; MC operands pa (= pb for an MC B).  Needs |C'| <= K 2^(pa-1)
+// 2^(pb-1) <= M / 4 (the reconstruction's margin) and a per-output bound
+// K 2^-(pa+1) (scaled) <= 2^-57, i.e. pa >= log2 K + 56; the limbs allow pa <= 73.
+struct CrtPlan {
+  int n = 0, pa = 0, pb = 0;
+};
+CrtPlan crt_plan(int64_t k, int ncb) {
+  int lk = 0;
+  while ((int64_t(1) << lk) < k) ++lk;
+  for (int n = kMinMod; n <= kMaxMod; ++n) {
+    const double avail = host_crt().log2m[n] - lk;  // >= pa + pb
+    int pa, pb;
+    if (ncb == 1) {
+      pb = 48;
+      pa = std::min(73, (int)std::floor(avail - pb));
+    } else {
+      pa = pb = std::min(73, (int)std::floor(avail / 2));
+    }
+    if (pa >= lk + 56) return CrtPlan{n, pa, pb};
+  }
+  return CrtPlan{};
+}
+
+// ---- device: residues ----
+
+// X = round((hi + lo) 2^p) for the scaled pair (|hi + lo| < 1/2 after the
+// line's scaling; sc = 2^(p - 48 - e) folds that scaling and the top limb's
+// weight into one exact product), p <= 73, as six balanced 12-bit limbs
+// l[j] (weight 2^(12 j); |l[j]| <= 2^11 + 1 for j < 5, |l[5]| <= 2^12 + 1)
+// as binary32 integers.  Three binary64 steps give H = rint(v 2^(p-48)),
+// M = rint(r1 2^24), L = rint(r2 2^24) with double-double remainders (exact),
+// X = H 2^48 + M 2^24 + L; l0i = the lowest limb as an integer (X mod 256 is
+// its low byte).  Returns true when X is not exactly (hi + lo) 2^p.
+__device__ __forceinline__ bool limbs(double hi, double lo, double sc, float (&l)[6], int& l0i) {
+  const double h = __dmul_rn(hi, sc), hl = __dmul_rn(lo, sc);
+  const double H = rint(h);
+  double r1, r1l;
+  dsum(__dsub_rn(h, H), hl, r1, r1l);
+  const double m = __dmul_rn(r1, 0x1p24), ml = __dmul_rn(r1l, 0x1p24);
+  const double M = rint(m);
+  double r2, r2l;
+  dsum(__dsub_rn(m, M), ml, r2, r2l);
+  const double l24 = __dmul_rn(r2, 0x1p24);
+  const double L = rint(l24);
+  const int v[3] = {__double2int_rn(L), __double2int_rn(M), __double2int_rn(H)};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int lo12 = ((v[q] + 2048) & 4095) - 2048, hi12 = (v[q] - lo12) >> 12;
+    // exact int -> float for |x| < 2^22 through the magic constant's mantissa
+    l[2 * q] = __fsub_rn(__int_as_float(lo12 + 0x4B400000), kMagic);
+    l[2 * q + 1] = __fsub_rn(__int_as_float(hi12 + 0x4B400000), kMagic);
+    if (q == 0) l0i = lo12;
+  }
+  return l24 != L || r2l != 0.0;
+}
+
+// kMagic + (X mod m_t), symmetric, for modulus t >= 1 (odd m_t): the limb sum
+// s (|s| < 2^20.9, exact in binary32) reduced by q = rint(s / m_t) from one
+// FFMA (|s RN(1/m) - s / m| < 2^-10.5 < 1 / (2 m), and s / m is never a half
+// integer for odd m, so q is exact); the low byte of the result's bits is the
+// residue as int8.
+template <int T>
+__device__ __forceinline__ unsigned res_bits(const float (&l)[6]) {
+  float s = __fmaf_rn(l[0], c_pw[T][0], kMagic);
+#pragma unroll
+  for (int j = 1; j < 6; ++j) s = __fmaf_rn(l[j], c_pw[T][j], s);
+  const float q = __fsub_rn(__fmaf_rn(__fsub_rn(s, kMagic), c_inv[T], kMagic), kMagic);
+  return __float_as_uint(__fmaf_rn(-q, c_mod[T], s));
+}
+
+// low bytes of four words -> one word (byte u = word u's low byte)
+__device__ __forceinline__ unsigned pack4(unsigned w0, unsigned w1, unsigned w2, unsigned w3) {
+  return __byte_perm(__byte_perm(w0, w1, 0x0040), __byte_perm(w2, w3, 0x0040), 0x5410);
+}
+
+template <int NMOD, int T = 0>
+__device__ __forceinline__ void residue_words(const float (&l)[4][6], const int (&l0i)[4], unsigned (&wd)[NMOD]) {
+  if constexpr (T < NMOD) {
+    if constexpr (T == 0) {  // m = 256: X mod 256 is the lowest limb's low byte
+      wd[0] = pack4((unsigned)l0i[0], (unsigned)l0i[1], (unsigned)l0i[2], (unsigned)l0i[3]);
+    } else {
+      wd[T] = pack4(res_bits<T>(l[0]), res_bits<T>(l[1]), res_bits<T>(l[2]), res_bits<T>(l[3]));
+    }
+    residue_words<NMOD, T + 1>(l, l0i, wd);
+  }
+}
+
+// A (rows x k, NC comps) -> residue planes [t][i][kp] (int8, zero for k >= K
+// and for non-finite elements; those rows are listed anyway).  Each thread
+// makes 4 consecutive k (one 32-bit store per plane); rows strided over y.
+template <int NC, int NMOD>
+__global__ void __launch_bounds__(256) k_res_rows(const float* __restrict__ a, int64_t rows, int64_t k, int64_t kp,
+                                                   int pa, const int* __restrict__ e, int8_t* __restrict__ out) {
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k0 >= kp) return;
+  const int64_t plane = rows * kp;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const double sc = pow2d(pa - 48 - e[i]);
+    float l[4][6];
+    int l0i[4];
+    const float* ar = a + i * k * NC;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double hi = 0.0, lo = 0.0, mag = 0.0;
+      if (k0 + u < k) load_pair<NC>(ar + (k0 + u) * NC, hi, lo, mag);
+      if (!isfinite(mag)) hi = lo = 0.0;
+      limbs(hi, lo, sc, l[u], l0i[u]);
+    }
+    unsigned wd[NMOD];
+    residue_words<NMOD>(l, l0i, wd);
+    int8_t* o = out + i * kp + k0;
+#pragma unroll
+    for (int t = 0; t < NMOD; ++t) *reinterpret_cast<unsigned*>(o + t * plane) = wd[t];
+  }
+}
+
+// B (k x n, NC comps, row stride ldb elements) -> residue planes transposed,
+// [t][j][kp] (K contiguous per column: the int8 GEMM's TN layout), and
+// bt[j, k, :] = B[k, j, :] (binary32, for the fallback list); per column the
+// count of elements whose rounding to pb bits is inexact (cinx).  CTA tile
+// 32 k x 32 j: lane = column (coalesced loads along n), each thread four
+// consecutive k packed into one 32-bit word per modulus; shared rows padded to
+// 9 words so the lanes' stores hit distinct banks.
+template <int NC, int NMOD>
+__global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, int64_t n, int64_t ldb, int64_t k,
+                                                   int64_t kp, int64_t np, int pb, const int* __restrict__ e,
+                                                   int8_t* __restrict__ out, float* __restrict__ bt,
+                                                   int* __restrict__ cinx) {
+  __shared__ unsigned dg[NMOD][kSlab][kSlab / 4 + 1];  // [t][j][k / 4]
+  __shared__ float tv[kSlab][kSlab * NC + 1];          // [j][k * NC + c]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps x 4 k each
+  const int64_t k0 = (int64_t)blockIdx.y * kSlab, j0 = (int64_t)blockIdx.x * kSlab;
+  const int64_t j = j0 + tx;
+  const double sc = j < n ? pow2d(pb - 48 - e[j]) : 1.0;
+  float l[4][6];
+  int l0i[4];
+  int inexact = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int kk = ty * 4 + u;
+    const int64_t gk = k0 + kk;
+    double hi = 0.0, lo = 0.0, mag = 0.0;
+    if (gk < k && j < n) {
+      load_pair<NC>(b + (gk * ldb + j) * NC, hi, lo, mag);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * ldb + j) * NC + c];
+    }
+    if (!isfinite(mag)) hi = lo = 0.0;
+    if (limbs(hi, lo, sc, l[u], l0i[u])) ++inexact;
+  }
+  if (inexact && j < n) atomicAdd(cinx + j, inexact);
+  unsigned wd[NMOD];
+  residue_words<NMOD>(l, l0i, wd);
+#pragma unroll
+  for (int t = 0; t < NMOD; ++t) dg[t][tx][ty] = wd[t];
+  __syncthreads();
+  // residue rows: thread (jj = tid / 8, part = tid % 8) writes 4 bytes of
+  // column j0 + jj's 32-k run in every plane
+  const int jj = threadIdx.x >> 3, part = threadIdx.x & 7;
+  const int64_t gj = j0 + jj;
+  if (gj < n) {
+    int8_t* dst = out + gj * kp + k0 + part * 4;
+#pragma unroll
+    for (int t = 0; t < NMOD; ++t) *reinterpret_cast<unsigned*>(dst + t * np * kp) = dg[t][jj][part];
+  }
+  for (int w = threadIdx.x; w < kSlab * kSlab * NC; w += blockDim.x) {
+    const int wj = w / (kSlab * NC), rest = w - wj * (kSlab * NC);
+    const int64_t gj2 = j0 + wj, gk = k0 + rest / NC;
+    if (gj2 < n && gk < k) bt[(gj2 * k + gk) * NC + rest % NC] = tv[wj][rest];
+  }
+}
+
+// row exponents of A (rows x k, NC comps): warp per row, max of |c0| + |c1|
 template <int NC>
 __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int64_t rows, int64_t k,
                                                  int* __restrict__ e, int* __restrict__ nf) {
@@ -220,106 +484,6 @@ __global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __rest
   if (j < n) e[j] = exp_above_d(__longlong_as_double((long long)cm[j]));
 }
 
-// A (rows x k, NC comps) -> digit planes, one row of g.row_bytes() per row:
-// byte [i][c kS kc + s kc + kk] = digit s of A[i, c kc + kk] 2^-e[i]; zero
-// for k >= K.  Each thread makes 4 consecutive k (one 32-bit store per digit).
-template <int NC>
-__global__ void __launch_bounds__(256) k_slice_rows(const float* __restrict__ a, int64_t rows, KGeo g,
-                                                     const int* __restrict__ e, int8_t* __restrict__ out) {
-  // grid: x covers the padded row in 4-k groups, y (strided) the rows
-  const int kp = (int)(g.kc * g.nkc), kc = (int)g.kc, k = (int)g.k;
-  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (k0 >= kp) return;
-  const int c = k0 / kc, kk = k0 - c * kc;
-  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
-    const double sc = pow2d(-e[i]);
-    unsigned packed[kS];
-#pragma unroll
-    for (int s = 0; s < kS; ++s) packed[s] = 0u;
-    const float* ar = a + i * k * NC;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (k0 + u >= k) break;
-      double hi, lo, mag;
-      load_pair<NC>(ar + (k0 + u) * NC, hi, lo, mag);
-      if (isfinite(mag)) {
-        int d[kS];
-        digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
-#pragma unroll
-        for (int s = 0; s < kS; ++s) packed[s] |= ((unsigned)(d[s] & 0xff)) << (8 * u);
-      }
-    }
-    int8_t* row = out + i * g.row_bytes() + c * kS * kc + kk;
-#pragma unroll
-    for (int s = 0; s < kS; ++s) *reinterpret_cast<unsigned*>(row + s * kc) = packed[s];
-  }
-}
-
-// B (k x n, NC comps, row stride ldb elements) -> digit planes transposed,
-// one row of g.row_bytes() per column j with each chunk's planes in reverse
-// order, byte [j][c kS kc + (kS-1-t) kc + kk] = digit t of B[c kc + kk, j] 2^-e[j],
-// so the diagonal-q operand of a chunk (planes q, .., 0) is one contiguous
-// run; and bt[j, k, :] = B[k, j, :] (binary32, for the fallback list).
-// CTA tile 32 k x 32 j: lane = column (coalesced loads along n), each thread
-// four consecutive k packed into one 32-bit word per digit; shared rows
-// padded to 9 words so the lanes' stores hit distinct banks.
-template <int NC, int SB>
-__global__ void __launch_bounds__(256) k_slice_cols(const float* __restrict__ b, int64_t n, int64_t ldb, KGeo g,
-                                                     const int* __restrict__ e, int8_t* __restrict__ out,
-                                                     float* __restrict__ bt, int* __restrict__ cinx) {
-  __shared__ unsigned dg[SB][kSlab][kSlab / 4 + 1];  // [t][j][k / 4]
-  __shared__ float tv[kSlab][kSlab * NC + 1];        // [j][k * NC + c]
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps x 4 k each
-  const int64_t k0 = (int64_t)blockIdx.y * kSlab, j0 = (int64_t)blockIdx.x * kSlab;
-  const int64_t j = j0 + tx;
-  const double sc = j < n ? pow2d(-e[j]) : 1.0;
-  unsigned packed[SB];
-  int inexact = 0;
-#pragma unroll
-  for (int t = 0; t < SB; ++t) packed[t] = 0u;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int kk = ty * 4 + u;
-    const int64_t gk = k0 + kk;
-    if (gk < g.k && j < n) {
-      double hi, lo, mag;
-      load_pair<NC>(b + (gk * ldb + j) * NC, hi, lo, mag);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * ldb + j) * NC + c];
-      if (isfinite(mag)) {
-        int d[kS];
-        bool tail = false;
-        if (!(NC == 1 && SB == kSB1 && digits6_exact(__dmul_rn(hi, sc), d)))
-          tail = digits(__dmul_rn(hi, sc), __dmul_rn(lo, sc), d);
-        if (SB < kS && tail) ++inexact;
-#pragma unroll
-        for (int t = 0; t < SB; ++t) packed[t] |= ((unsigned)(d[t] & 0xff)) << (8 * u);
-      }
-    }
-  }
-  if (SB < kS && inexact) atomicAdd(cinx + j, inexact);
-#pragma unroll
-  for (int t = 0; t < SB; ++t) dg[t][tx][ty] = packed[t];
-  __syncthreads();
-  // digit rows: SB * 32 rows (t, jj) of 32 bytes, 8 threads x 4 bytes per
-  // row: thread (jj = tid / 8, part = tid % 8) writes plane t = r in round r.
-  // The tile's 32 k lie in one chunk (kc is a multiple of 32).
-  const int kc = (int)g.kc, c = (int)(k0 / kc), kk0 = (int)(k0 - (int64_t)c * kc);
-  const int jj = threadIdx.x >> 3, part = threadIdx.x & 7;
-  const int64_t gj = j0 + jj;
-  if (gj < n) {
-    int8_t* dst = out + gj * g.row_bytes(SB) + (int64_t)c * SB * kc + kk0 + part * 4;
-#pragma unroll
-    for (int t = 0; t < SB; ++t) *reinterpret_cast<unsigned*>(dst + (SB - 1 - t) * kc) = dg[t][jj][part];
-  }
-  // transposed binary32 copy: thread (jj = tid / 8 + 32 r / ..., k) rows of 32 NC floats
-  for (int w = threadIdx.x; w < kSlab * kSlab * NC; w += blockDim.x) {
-    const int wj = w / (kSlab * NC), rest = w - wj * (kSlab * NC);
-    const int64_t gj2 = j0 + wj, gk = k0 + rest / NC;
-    if (gj2 < n && gk < g.k) bt[(gj2 * g.k + gk) * NC + rest % NC] = tv[wj][rest];
-  }
-}
-
 // Optional fused epilogue of an MC-MLP layer (mc_linear_op, autodiff.hpp:265-
 // 268, then Tape::relu): z = the product's two components, r = add_mcn(z,
 // bias[i]) (mc_ops.hpp:440-446; bias is MC nc=2 per output row), h =
@@ -349,113 +513,92 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
   if (ep.act) ep.act[i * ldo + j] = ep.relu ? (hv > 0.0f ? hv : 0.0f) : hv;  // Tape::relu, autodiff.hpp:134
 }
 
-// C = sum_{c,q} C_cq 2^(-14-8q), scaled back, split into two binary32
-// components written with row stride ldo; ill-conditioned / non-finite
-// outputs are listed per row (rlist[i * n + slot] = j, rcnt[i] entries) for
-// the fallback.  The nine diagonal sums (int64 over K chunks) are grouped in
-// threes in integer arithmetic, G = S_q 2^16 + S_q+1 2^8 + S_q+2 (|G| < 2^51,
-// exact in binary64), and the three groups (weights 2^-30, 2^-54, 2^-78) are
-// added exactly in double-double.  Grid: x covers a row, y (strided) rows.
-__global__ void __launch_bounds__(256, 3) k_combine(const int* __restrict__ cq, int64_t m, int64_t n, int64_t ldc,
-                                                 int nkc, int nq, const int* __restrict__ ea,
-                                                 const int* __restrict__ eb, const int* __restrict__ rnf,
-                                                 const int* __restrict__ cnf, const int* __restrict__ cinx,
-                                                 double thr, double thr_inexact,
-                                                 float* __restrict__ out, int64_t ldo,
-                                                 int* __restrict__ rlist, int* __restrict__ rcnt, Epilogue ep) {
-  static_assert(kS == 9, "three groups of three diagonals (+ an optional tenth)");
-  // four consecutive columns per thread: 16-byte loads from each plane (ldc
-  // is a multiple of 16; padded columns hold zeros and are not written)
+// C mod m_t (symmetric, |r| <= m_t / 2 + 1/2) of an int32 GEMM sum C (|C| <=
+// K 2^14): C = ch 2^14 + cl (cl balanced), s = ch (2^14 mod m_t) + cl is an
+// exact binary32 integer (|s| < 2^21 for K <= 2^14; below 2^24 for K < 2^17
+// with BIG, which reduces twice), then one rounded quotient as in res_bits.
+template <bool BIG>
+__device__ __forceinline__ float mod_c(int c, int t) {
+  const int cl = ((c + 8192) & 16383) - 8192, ch = (c - cl) >> 14;
+  const float fl = __fsub_rn(__int_as_float(cl + 0x4B400000), kMagic);
+  const float fh = __fsub_rn(__int_as_float(ch + 0x4B400000), kMagic);
+  float s = __fmaf_rn(fh, c_c14[t], fl);
+  if constexpr (BIG) {
+    const float q0 = __fsub_rn(__fmaf_rn(s, c_inv[t], kMagic), kMagic);
+    s = __fmaf_rn(-q0, c_mod[t], s);  // |s| <= 2 m
+  }
+  const float q = __fsub_rn(__fmaf_rn(s, c_inv[t], kMagic), kMagic);
+  return __fmaf_rn(-q, c_mod[t], s);
+}
+
+// CRT reconstruction of C' from the NMOD int32 GEMM planes cq[t][i][np]
+// (C' mod m_t), scaled back, split into two binary32 components written with
+// row stride ldo; ill-conditioned / non-finite outputs are listed per row
+// (rlist[i * n + slot] = j, rcnt[i] entries) for the fallback.
+//   T_j = sum_t r_t w_tj  (|T_j| < 2^21.5: exact binary32 sums)
+//   q   = rint((T_0 + T_1 2^-11) 2^(L-11) / M)   (error < 2^-10; |C'/M| <= 1/4)
+//   D_j = T_j - q M_j     (exact, |D_j| < 2^22.6)
+//   Y   = sum_j D_j 2^(11 (8 - j)) = C' / 2^(L-99) + tail (binary64 Horner:
+//         partial sums < 2^53 exact while the later terms can still cancel them)
+// Four consecutive columns per thread (16-byte plane loads; np % 16 == 0).
+template <int NMOD, bool BIG>
+__global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t m, int64_t n, int64_t np,
+                                             const int* __restrict__ ea, const int* __restrict__ eb,
+                                             const int* __restrict__ rnf, const int* __restrict__ cnf,
+                                             const int* __restrict__ cinx, double thr, double thr_inexact, int sexp,
+                                             float* __restrict__ out, int64_t ldo, int* __restrict__ rlist,
+                                             int* __restrict__ rcnt, Epilogue ep) {
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
-  const int64_t plane = m * ldc;
+  const int64_t plane = m * np;
   int fj[4], nfj[4];
   double thj[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     fj[u] = j0 + u < n ? eb[j0 + u] : 0;
     nfj[u] = j0 + u < n ? cnf[j0 + u] & 1 : 0;
-    // columns with elements not exact in their digits: their truncation adds
-    // at most 2^-48 (1.01) x 1/2 per such element to every output
     thj[u] = thr + (cinx && j0 + u < n ? thr_inexact * cinx[j0 + u] : 0.0);
   }
   for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
-    const int64_t off = i * ldc + j0;
-    // per group of three diagonals: load (summing K chunks), fold into one
-    // exact integer per column, convert -- few live registers, so many rows
-    // of loads stay in flight
-    double g[3][4];
-    if (nkc == 1) {
-      // one K chunk (K <= 14400, config 2): all nine planes' loads in flight at once
-      int4 v[kS];
+    const int64_t off = i * np + j0;
+    float T[4][kSlices];
 #pragma unroll
-      for (int q = 0; q < kS; ++q) v[q] = __ldcs(reinterpret_cast<const int4*>(cq + q * plane + off));
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int w = 0; w < 3; ++w) {
-        const int4 a = v[3 * w], b = v[3 * w + 1], c = v[3 * w + 2];
-        g[w][0] = (double)(((long long)a.x * 256 + b.x) * 256 + c.x);
-        g[w][1] = (double)(((long long)a.y * 256 + b.y) * 256 + c.y);
-        g[w][2] = (double)(((long long)a.z * 256 + b.z) * 256 + c.z);
-        g[w][3] = (double)(((long long)a.w * 256 + b.w) * 256 + c.w);
+      for (int j = 0; j < kSlices; ++j) T[u][j] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < NMOD; ++t) {
+      const int4 v = __ldcs(reinterpret_cast<const int4*>(cq + t * plane + off));
+      const int c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        // m = 256: the balanced low byte
+        const float r = t == 0 ? __fsub_rn(__int_as_float((((c[u] + 128) & 255) - 128) + 0x4B400000), kMagic)
+                               : mod_c<BIG>(c[u], t);
+#pragma unroll
+        for (int j = 0; j < kSlices; ++j) T[u][j] = __fmaf_rn(r, c_crt[NMOD].w[t][j], T[u][j]);
       }
-    } else
-#pragma unroll
-    for (int w = 0; w < 3; ++w) {
-      long long gv[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int q = 3 * w + r;
-        const int4 v0 = *reinterpret_cast<const int4*>(cq + q * plane + off);
-        long long t[4] = {v0.x, v0.y, v0.z, v0.w};
-        for (int c = 1; c < nkc; ++c) {
-          const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * nq + q) * plane + off);
-          t[0] += v.x;
-          t[1] += v.y;
-          t[2] += v.z;
-          t[3] += v.w;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) gv[u] = gv[u] * 256 + t[u];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) g[w][u] = (double)gv[u];
-    }
-    // the tenth diagonal (long K), weight 2^-86
-    double g9[4] = {0.0, 0.0, 0.0, 0.0};
-    if (nq > kS) {
-      long long t[4] = {0, 0, 0, 0};
-      for (int c = 0; c < nkc; ++c) {
-        const int4 v = *reinterpret_cast<const int4*>(cq + ((int64_t)c * nq + kS) * plane + off);
-        t[0] += v.x;
-        t[1] += v.y;
-        t[2] += v.z;
-        t[3] += v.w;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) g9[u] = (double)t[u];
     }
     const int ei = ea[i], fi = rnf[i] & 1;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u;
       if (j >= n) break;
-      double hi, lo, h2, l2, s2, e2;
-      dsum(__dmul_rn(g[2][u], 0x1p-78), __dmul_rn(g9[u], 0x1p-86), h2, l2);
-      dsum(__dmul_rn(g[1][u], 0x1p-54), h2, hi, lo);
-      lo = __dadd_rn(lo, l2);
-      dsum(__dmul_rn(g[0][u], 0x1p-30), hi, s2, e2);
-      e2 = __dadd_rn(e2, lo);
-      dsum(s2, e2, s2, e2);
-      if (fi | nfj[u] || !(fabs(s2) >= thj[u])) {
+      const float u0 = __fmaf_rn(T[u][1], 0x1p-11f, T[u][0]);
+      const float q = __fsub_rn(__fmaf_rn(u0, c_crt[NMOD].cq, kMagic), kMagic);
+      double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], T[u][0]);
+#pragma unroll
+      for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], T[u][s]));
+      if (fi | nfj[u] || !(fabs(y) >= thj[u])) {
         rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
         continue;
       }
-      const double sc = pow2d(ei + fj[u]);
-      const double v[2] = {__dmul_rn(s2, sc), __dmul_rn(e2, sc)};
+      const double v[2] = {__dmul_rn(y, pow2d(sexp + ei + fj[u])), 0.0};
       emit(v, i, j, out, ldo, ep);
     }
   }
 }
+
 
 // the listed outputs: a CTA per row.  The CTA stages its row of A in shared
 // memory (SMEM; rows too long for it read A through L1).  A row lists few
@@ -694,11 +837,9 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
   const std::size_t sm = (std::size_t)k * NCA * sizeof(float);
   constexpr std::size_t kMaxSmem = 200u << 10;
   if (sm <= kMaxSmem) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
-      attr = true;
-    }
+    // the attribute is per device (and per instantiation): set it on every
+    // call (cheap) rather than behind a process-wide flag
+    cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
     // 128-thread CTAs (four per SM at 126 registers) while four rows fit in
     // shared memory: one CTA's staging overlaps another's B streaming; config
     // 2's launch 112 -> 98 us under ncu (cold; 256 and 64 threads both 111-115
@@ -710,17 +851,24 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
     k_fallback<NCA, NCB, false><<<(unsigned)m, 256, 0, s>>>(x, bt, n, k, rlist, rcnt, rnf, cnf, out, ldo, ep);
   }
   mcfr::note_launch();
-  return MCF_OK;
+  return mcfr::check_launch("mm_fast fallback kernel");
 }
+
 
 // ---- cuBLASLt int8 GEMMs ------------------------------------------------------------------
 
+// matmul descriptor, layouts and heuristic algorithm of one (shape, batch)
+// key: built once and reused (read-only after creation)
+struct LtPlan {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  cublasLtMatmulAlgo_t algo{};
+};
 struct Lt {
   cublasLtHandle_t h = nullptr;
-  void* ws = nullptr;  // the first stream's workspace
   std::size_t ws_bytes = 0;
   std::map<cudaStream_t, void*> ws_by_stream;  // GEMMs may run concurrently on several streams
-  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t>, cublasLtMatmulAlgo_t> algos;
+  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t, int, int64_t, int64_t>, LtPlan> plans;
 };
 std::mutex g_lt_mu;
 std::map<int, Lt> g_lt;
@@ -729,75 +877,93 @@ mcf_status lt_fail(const char* what, int code) {
   return mcfr::fail(MCF_ERR_CUDA, std::string("mm_fast int8 GEMM: ") + what + " (status " + std::to_string(code) + ")");
 }
 
-// C (rows_c x cols_c, col-major, ld rows_c, int32) = A^T B with
-// A: kd x rows_c int8 col-major (ld lda), B: kd x cols_c int8 col-major (ld ldb).
+// C_b (rows_c x cols_c, col-major, ld rows_c, int32; C_b = C + b rows_c
+// cols_c) = A_b^T B_b for b < batch, with A_b: kd x rows_c int8 col-major (ld
+// lda, A_b = A + b sa), B_b: kd x cols_c int8 col-major (ld ldb, B + b sb).
 // MCF_ERR_UNSUPPORTED (no message) when cuBLASLt has no algorithm for the shape.
-mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int* C, int64_t rows_c,
-                   int64_t cols_c, int64_t kd, cudaStream_t s, int accumulate = 0) {
+mcf_status gemm_s8(const int8_t* A, int64_t lda, int64_t sa, const int8_t* B, int64_t ldb, int64_t sb, int* C,
+                   int64_t rows_c, int64_t cols_c, int64_t kd, int batch, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_lt_mu);
-  Lt& lt = g_lt[dev];
-  if (!lt.h) {
-    const cublasStatus_t st = cublasLtCreate(&lt.h);
-    if (st != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtCreate", st);
-    lt.ws_bytes = 64u << 20;
-    if (cudaMalloc(&lt.ws, lt.ws_bytes) != cudaSuccess) return lt_fail("workspace", 0);
-  }
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-  cublasStatus_t st = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I);
-  const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
-  if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
-  if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
-  if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, kd, rows_c, lda);
-  if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, kd, cols_c, ldb);
-  if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, rows_c, cols_c, rows_c);
-  auto cleanup = [&]() {
-    if (lc) cublasLtMatrixLayoutDestroy(lc);
-    if (lb) cublasLtMatrixLayoutDestroy(lb);
-    if (la) cublasLtMatrixLayoutDestroy(la);
-    if (op) cublasLtMatmulDescDestroy(op);
-  };
-  if (st != CUBLAS_STATUS_SUCCESS) {
-    cleanup();
-    return lt_fail("descriptors", st);
-  }
-  const auto key = std::make_tuple(rows_c, cols_c, kd, lda, ldb);
-  auto it = lt.algos.find(key);
-  if (it == lt.algos.end()) {
-    cublasLtMatmulPreference_t pref = nullptr;
-    cublasLtMatmulPreferenceCreate(&pref);
-    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &lt.ws_bytes,
-                                         sizeof(lt.ws_bytes));
-    cublasLtMatmulHeuristicResult_t res{};
-    int found = 0;
-    st = cublasLtMatmulAlgoGetHeuristic(lt.h, op, la, lb, lc, lc, pref, 1, &res, &found);
-    cublasLtMatmulPreferenceDestroy(pref);
-    if (st != CUBLAS_STATUS_SUCCESS || found == 0) {
-      cleanup();
-      return MCF_ERR_UNSUPPORTED;  // caller runs the FP64-pipe kernel instead
+  const LtPlan* pl = nullptr;
+  cublasLtHandle_t h = nullptr;
+  void* wss = nullptr;
+  std::size_t ws_bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_lt_mu);
+    Lt& lt = g_lt[dev];
+    if (!lt.h) {
+      const cublasStatus_t st = cublasLtCreate(&lt.h);
+      if (st != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtCreate", st);
+      lt.ws_bytes = 64u << 20;
     }
-    it = lt.algos.emplace(key, res.algo).first;
-  }
-  const int32_t alpha = 1, beta = accumulate ? 1 : 0;
-  void*& wss = lt.ws_by_stream[s];
-  if (!wss) {
-    if (lt.ws_by_stream.size() == 1) wss = lt.ws;
-    else if (cudaMalloc(&wss, lt.ws_bytes) != cudaSuccess) {
-      wss = nullptr;
-      cleanup();
+    const auto key = std::make_tuple(rows_c, cols_c, kd, lda, ldb, batch, sa, sb);
+    auto it = lt.plans.find(key);
+    if (it == lt.plans.end()) {
+      LtPlan p;
+      cublasStatus_t st = cublasLtMatmulDescCreate(&p.op, CUBLAS_COMPUTE_32I, CUDA_R_32I);
+      const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+      if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
+      if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
+      if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&p.la, CUDA_R_8I, kd, rows_c, lda);
+      if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&p.lb, CUDA_R_8I, kd, cols_c, ldb);
+      if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&p.lc, CUDA_R_32I, rows_c, cols_c, rows_c);
+      if (batch > 1) {
+        const int32_t bc = batch;
+        const int64_t sc = rows_c * cols_c;
+        for (auto* l : {p.la, p.lb, p.lc})
+          if (st == CUBLAS_STATUS_SUCCESS)
+            st = cublasLtMatrixLayoutSetAttribute(l, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
+        if (st == CUBLAS_STATUS_SUCCESS)
+          st = cublasLtMatrixLayoutSetAttribute(p.la, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sa, sizeof(sa));
+        if (st == CUBLAS_STATUS_SUCCESS)
+          st = cublasLtMatrixLayoutSetAttribute(p.lb, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sb, sizeof(sb));
+        if (st == CUBLAS_STATUS_SUCCESS)
+          st = cublasLtMatrixLayoutSetAttribute(p.lc, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &sc, sizeof(sc));
+      }
+      int found = 0;
+      cublasLtMatmulHeuristicResult_t res{};
+      if (st == CUBLAS_STATUS_SUCCESS) {
+        cublasLtMatmulPreference_t pref = nullptr;
+        cublasLtMatmulPreferenceCreate(&pref);
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &lt.ws_bytes,
+                                             sizeof(lt.ws_bytes));
+        st = cublasLtMatmulAlgoGetHeuristic(lt.h, p.op, p.la, p.lb, p.lc, p.lc, pref, 1, &res, &found);
+        cublasLtMatmulPreferenceDestroy(pref);
+      }
+      if (st != CUBLAS_STATUS_SUCCESS || found == 0) {
+        if (p.lc) cublasLtMatrixLayoutDestroy(p.lc);
+        if (p.lb) cublasLtMatrixLayoutDestroy(p.lb);
+        if (p.la) cublasLtMatrixLayoutDestroy(p.la);
+        if (p.op) cublasLtMatmulDescDestroy(p.op);
+        return MCF_ERR_UNSUPPORTED;  // caller runs the FP64-pipe kernel instead
+      }
+      p.algo = res.algo;
+      it = lt.plans.emplace(key, p).first;
+    }
+    pl = &it->second;  // std::map nodes are stable
+    h = lt.h;
+    void*& w = lt.ws_by_stream[s];
+    if (!w && cudaMalloc(&w, lt.ws_bytes) != cudaSuccess) {
+      w = nullptr;
       return lt_fail("workspace", 0);
     }
+    wss = w;
+    ws_bytes = lt.ws_bytes;
   }
-  st = cublasLtMatmul(lt.h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &it->second, wss, lt.ws_bytes, s);
-  cleanup();
+  const int32_t alpha = 1, beta = 0;
+  const cublasStatus_t st = cublasLtMatmul(h, pl->op, &alpha, A, pl->la, B, pl->lb, &beta, C, pl->lc, C, pl->lc,
+                                           &pl->algo, wss, ws_bytes, s);
   if (st != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtMatmul", st);
   mcfr::note_launch();
   return MCF_OK;
 }
+mcf_status gemm_s8(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int* C, int64_t rows_c, int64_t cols_c,
+                   int64_t kd, cudaStream_t s) {
+  return gemm_s8(A, lda, 0, B, ldb, 0, C, rows_c, cols_c, kd, 1, s);
+}
 
-// per-(device, stream) workspace for the digit planes and partial products
+// per-(device, stream) workspace for the residue planes and partial products
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, std::pair<void*, std::size_t>> g_ws;
 
@@ -821,41 +987,52 @@ char* oz_workspace(std::size_t bytes, cudaStream_t s) {
 
 std::size_t al(std::size_t b) { return (b + 255) & ~std::size_t(255); }
 int64_t pad16(int64_t v) { return (v + 15) / 16 * 16; }
+int64_t pad32(int64_t v) { return (v + 31) / 32 * 32; }
 
 }  // namespace
 
-// Prepared B operand (a block of n columns of a k x ldb matrix): digit
+// Prepared B operand (a block of n columns of a k x ldb matrix): residue
 // planes, column exponents, non-finite flags and the transposed binary32
 // copy.  Built once; shared by every row chunk of A.
 struct PreparedB {
-  const int8_t* planes = nullptr;
+  const int8_t* planes = nullptr;  // [plan.n][np][kp]
   const float* bt = nullptr;
   const int* eb = nullptr;
   const int* cnf = nullptr;
-  const int* cinx = nullptr;  // per column: elements not exact in sb digits (sb < kS)
-  KGeo g{};
-  int64_t n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
-  int ncb = 1, sb = kS;
+  const int* cinx = nullptr;  // per column: elements not exact in pb bits (binary32 B)
+  int64_t k = 0, kp = 0, n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
+  int ncb = 1;
+  CrtPlan plan{};
 };
 
-// digits kept for B: six for binary32 columns (exact for elements within
-// 2^24 of the column scale; the others are counted), nine for MC columns
-int b_digits(int ncb) { return ncb == 1 ? kSB1 : kS; }
-
 std::size_t b_bytes(int64_t k, int64_t n, int ncb) {
-  const KGeo g = kgeo(k);
-  return al(pad16(n) * g.row_bytes(b_digits(ncb))) + al(n * k * ncb * 4) + al(n * 4) * 3 + al(n * 8);
+  const CrtPlan pl = crt_plan(k, ncb);
+  return al(pl.n * pad16(n) * pad32(k)) + al(n * k * ncb * 4) + al(n * 4) * 3 + al(n * 8);
 }
+
+#define OZ_NMOD_SWITCH(N, ...)                         \
+  switch (N) {                                         \
+    case 16: { constexpr int NM = 16; __VA_ARGS__; } break; \
+    case 17: { constexpr int NM = 17; __VA_ARGS__; } break; \
+    case 18: { constexpr int NM = 18; __VA_ARGS__; } break; \
+    case 19: { constexpr int NM = 19; __VA_ARGS__; } break; \
+    case 20: { constexpr int NM = 20; __VA_ARGS__; } break; \
+    case 21: { constexpr int NM = 21; __VA_ARGS__; } break; \
+    default: { constexpr int NM = 22; __VA_ARGS__; } break; \
+  }
 
 mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb, char* buf, PreparedB& pb,
                      cudaStream_t s) {
-  const KGeo g = kgeo(k);
-  const int sb = b_digits(ncb);
-  const int64_t np = pad16(n), rbb = g.row_bytes(sb);
+  mcf_status st = upload_crt_tables();
+  if (st != MCF_OK) return st;
+  const CrtPlan pl = crt_plan(k, ncb);
+  const int64_t np = pad16(n), kp = pad32(k);
   int8_t* planes = reinterpret_cast<int8_t*>(buf);
-  buf += al(np * rbb);
-  if (np > n && cudaMemsetAsync(planes + n * rbb, 0, (np - n) * rbb, s) != cudaSuccess)
-    return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the padding columns");
+  buf += al(pl.n * np * kp);
+  if (np > n)
+    for (int t = 0; t < pl.n; ++t)
+      if (cudaMemsetAsync(planes + (t * np + n) * kp, 0, (np - n) * kp, s) != cudaSuccess)
+        return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the padding columns");
   float* bt = reinterpret_cast<float*>(buf);
   buf += al(n * k * ncb * 4);
   int* eb = reinterpret_cast<int*>(buf);
@@ -872,32 +1049,17 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
   else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
   k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, eb);
-  const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)((g.kc * g.nkc + kSlab - 1) / kSlab));
-  if (ncb == 2) k_slice_cols<2, kS><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt, cinx);
-  else k_slice_cols<1, kSB1><<<gs, 256, 0, s>>>(w, n, ldb, g, eb, planes, bt, cinx);
+  const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
+  OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
+                 else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
   for (int i = 0; i < 3; ++i) mcfr::note_launch();
-  pb = PreparedB{planes, bt, eb, cnf, sb < kS ? cinx : nullptr, g, n, np, ncb, sb};
-  return mcfr::check_launch("mm_fast B digit kernels");
+  pb = PreparedB{planes, bt, eb, cnf, ncb == 1 ? cinx : nullptr, k, kp, n, np, ncb, pl};
+  return mcfr::check_launch("mm_fast B residue kernels");
 }
 
-// diagonals kept: a tenth for long K, where the fallback's per-output cost
-// (K) times its share (~sqrt K) outgrows one more GEMM-equivalent set
-int diagonals(int64_t k) { return k > 8192 ? kQmax : kS; }
-
-std::size_t rows_bytes(int64_t m, int64_t k, int64_t n) {
-  const KGeo g = kgeo(k);
-  return al(m * g.row_bytes()) + al((int64_t)kQmax * g.nkc * m * pad16(n) * 4) + al(m * pad16(n) * 4) + al(m * 4) * 3;
-}
-
-// error bound per product, units of 2^-72: A's truncation (2^-73), B's (2^-73
-// with nine digits; zero for the exact elements of a six-digit B) and the
-// dropped pairs s + t >= nq (|d_s w_s| <= 2^-8s for s >= 1)
-double per_product_bound(int sb, int nq) {
-  double e = 0.5 + (sb == kS ? 0.5 : 0.0);
-  for (int s = 1; s < kS; ++s)
-    for (int t = 1; t < sb; ++t)
-      if (s + t >= nq) e += ldexp(1.0, 72 - 8 * (s + t));
-  return e * 1.01;
+std::size_t rows_bytes(int64_t m, int64_t k, int64_t n, int ncb) {
+  const CrtPlan pl = crt_plan(k, ncb);
+  return al(pl.n * m * pad32(k)) + al((int64_t)pl.n * m * pad16(n) * 4) + al(m * pad16(n) * 4) + al(m * 4) * 3;
 }
 
 // workspace layout of one row block (see rows_bytes)
@@ -909,12 +1071,12 @@ struct RowsWs {
   int* rnf;
   int* rcnt;
 };
-RowsWs rows_ws(char* buf, int64_t m, const KGeo& g, int64_t np) {
+RowsWs rows_ws(char* buf, int64_t m, int64_t kp, int64_t np, int nmod) {
   RowsWs w;
   w.planes = reinterpret_cast<int8_t*>(buf);
-  buf += al(m * g.row_bytes());
+  buf += al(nmod * m * kp);
   w.cq = reinterpret_cast<int*>(buf);
-  buf += al((int64_t)kQmax * g.nkc * m * np * 4);
+  buf += al((int64_t)nmod * m * np * 4);
   w.rlist = reinterpret_cast<int*>(buf);
   buf += al(m * (np > 0 ? np : 1) * 4);
   w.ea = reinterpret_cast<int*>(buf);
@@ -925,144 +1087,80 @@ RowsWs rows_ws(char* buf, int64_t m, const KGeo& g, int64_t np) {
   return w;
 }
 
-// A's row exponents and digit planes (independent of B: may run concurrently
-// with prepare_b on another stream)
-mcf_status a_digits(const float* x, int nca, int64_t m, const KGeo& g, const RowsWs& w, cudaStream_t s) {
+// A's row exponents and residue planes (independent of B: may run
+// concurrently with prepare_b on another stream)
+mcf_status a_residues(const float* x, int nca, int64_t m, int64_t k, const CrtPlan& pl, const RowsWs& w,
+                      cudaStream_t s) {
+  mcf_status st = upload_crt_tables();
+  if (st != MCF_OK) return st;
   if (cudaMemsetAsync(w.rcnt, 0, m * sizeof(int), s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counters");
-  const int64_t k = g.k;
+  const int64_t kp = pad32(k);
   const unsigned gr = (unsigned)((m + 7) / 8);
   if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, w.ea, w.rnf);
   else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, w.ea, w.rnf);
-  const int64_t gx = (g.kc * g.nkc / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
+  const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
   const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
-  if (nca == 2) k_slice_rows<2><<<gsl, 256, 0, s>>>(x, m, g, w.ea, w.planes);
-  else k_slice_rows<1><<<gsl, 256, 0, s>>>(x, m, g, w.ea, w.planes);
+  OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
+                 else k_res_rows<1, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes));
   mcfr::note_launch();
   mcfr::note_launch();
-  return mcfr::check_launch("mm_fast A digit kernels");
+  return mcfr::check_launch("mm_fast A residue kernels");
 }
 
 mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo,
                          const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep);
 
 // out (m x n x 2 binary32, row stride ldo elements) = A (m x k x nca) . B for
-// a prepared B.  ev (optional, 4 events): recorded before the A digits,
+// a prepared B.  ev (optional, 4 events): recorded before the A residues,
 // before the GEMMs, after the GEMMs and at the end (phase timing).
 mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo, char* buf,
                 cudaStream_t s, cudaEvent_t* ev = nullptr, const Epilogue& ep = Epilogue{}) {
-  const RowsWs w = rows_ws(buf, m, pb.g, pb.np);
+  const RowsWs w = rows_ws(buf, m, pb.kp, pb.np, pb.plan.n);
   if (ev) cudaEventRecord(ev[0], s);
-  const mcf_status st = a_digits(x, nca, m, pb.g, w, s);
+  const mcf_status st = a_residues(x, nca, m, pb.k, pb.plan, w, s);
   if (st != MCF_OK) return st;
   return rows_products(x, nca, m, pb, out, ldo, w, s, ev, ep);
 }
 
-// the GEMMs, recombination and fallback of a row block whose A digits are done
+// the GEMMs, reconstruction and fallback of a row block whose A residues are done
 mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo,
                          const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep) {
-  const KGeo g = pb.g;
-  const int64_t k = g.k, n = pb.n, np = pb.np;
-  int8_t* planes = w.planes;
-  int* cq = w.cq;
-  int* rlist = w.rlist;
-  int* ea = w.ea;
-  int* rnf = w.rnf;
-  int* rcnt = w.rcnt;
-  mcf_status st = MCF_OK;
-  // chunk c, diagonal q: the pairs (s, t = q - s) with t <= sb - 1.  A planes
-  // q - th .. q of the chunk (contiguous, ascending s) against B planes th ..
-  // 0 (stored in reverse order, so also contiguous); C_cq is an np x m
-  // column-major = m x np row-major int32 matrix
+  const CrtPlan pl = pb.plan;
+  const int64_t k = pb.k, kp = pb.kp, n = pb.n, np = pb.np;
   if (ev) cudaEventRecord(ev[1], s);
-  const int sb = pb.sb, nq = diagonals(k);
-  const int64_t lda = g.row_bytes(), ldb = g.row_bytes(sb);
-  // One GEMM per diagonal over the concatenated digit planes.  Tuning knob
-  // MCF_OZ_PAIRWISE=1: one GEMM per digit pair (depth kc) accumulating into
-  // C_q (beta = 1; the same exact int32 sums) -- measured no faster at config
-  // 4 (265 ms both) and slower at config 2 (2.77 vs 2.27 ms), so off.
-  static const bool pairwise = [] {
-    const char* e = getenv("MCF_OZ_PAIRWISE");
-    return e && atoi(e) == 1;
-  }();
-  // A short row block gives the int8 GEMMs few output tiles (512 x 4096:
-  // 32 tiles of 256 x 256 for 148 SMs); the diagonals' GEMMs are independent
-  // (separate int32 planes), so then they run concurrently on side streams.
-  const int64_t tiles = ((np + 255) / 256) * ((m + 255) / 256);
-  static const int conc = [] {  // MCF_OZ_CONC=0: one stream (A/B measurements)
-    const char* e = getenv("MCF_OZ_CONC");
-    return e ? atoi(e) : 4;
-  }();
-  // (measured: at 32 tiles four streams take a 512-row product from 0.65 to
-  // 0.46 ms; at 64 and 128 tiles concurrency does not pay)
-  // Products with many tiles still leave each GEMM's last wave partly empty
-  // (4096 x 4096: 256 tiles of 256 x 256 over 74 two-SM clusters = 3.46
-  // waves); two streams let one diagonal's tiles fill the other's tail
-  // (measured: config 2 2.19 -> 2.13 ms, the MLP step 2.04 -> 1.94 ms; three
-  // streams no better).  MCF_OZ_CONC_BIG overrides.
-  static const int conc_big = [] {
-    const char* e = getenv("MCF_OZ_CONC_BIG");
-    return e ? std::max(1, std::min(4, atoi(e))) : 2;
-  }();
-  const int ns = 3 * tiles > mcfr::sm_count()
-                     ? conc_big
-                     : (int)std::max<int64_t>(1, std::min<int64_t>(std::min(conc, 4), mcfr::sm_count() / std::max<int64_t>(tiles, 1)));
-  cudaStream_t gs[4] = {s, s, s, s};
-  cudaEvent_t fork_ev = nullptr, join_ev[4] = {};
-  if (ns > 1 && !pairwise) {
-    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
-    cudaEventRecord(fork_ev, s);
-    for (int i = 1; i < ns; ++i) {
-      // the host pipeline's second compute stream (slot 5) forks to its own
-      // side streams, so two chunk products do not queue behind each other
-      gs[i] = mcfr::side_stream((s == mcfr::side_stream(5) ? 16 : 12) + i);
-      cudaStreamWaitEvent(gs[i], fork_ev, 0);
-    }
-  }
-  int gi = 0;
-  for (int64_t c = 0; c < g.nkc; ++c)
-    for (int q = 0; q < nq; ++q) {
-      // pairs (q - t, t), t in [tl, th]: A planes q - th .. q - tl ascending,
-      // B planes th .. tl (stored reversed: ascending positions)
-      const int th = q < sb - 1 ? q : sb - 1, tl = q > kS - 1 ? q - (kS - 1) : 0;
-      const int8_t* bp = pb.planes + c * sb * g.kc + (int64_t)(sb - 1 - th) * g.kc;
-      const int8_t* ap = planes + c * kS * g.kc + (int64_t)(q - th) * g.kc;
-      int* cp = cq + (c * nq + q) * m * np;
-      if (pairwise) {
-        for (int u = 0; u <= th - tl && st == MCF_OK; ++u)
-          st = gemm_s8(bp + u * g.kc, ldb, ap + u * g.kc, lda, cp, np, m, g.kc, s, u > 0);
-      } else {
-        st = gemm_s8(bp, ldb, ap, lda, cp, np, m, (int64_t)(th - tl + 1) * g.kc, gs[gi++ % ns]);
-      }
-      if (st != MCF_OK) break;
-    }
-  if (fork_ev) {
-    for (int i = 1; i < ns; ++i) {
-      cudaEventCreateWithFlags(&join_ev[i], cudaEventDisableTiming);
-      cudaEventRecord(join_ev[i], gs[i]);
-      cudaStreamWaitEvent(s, join_ev[i], 0);
-      cudaEventDestroy(join_ev[i]);
-    }
-    cudaEventDestroy(fork_ev);
-  }
+  // one strided-batched GEMM over the moduli: C_t (np x m col-major = m x np
+  // row-major) = B_t^T-planes . A_t-planes
+  mcf_status st = gemm_s8(pb.planes, kp, np * kp, w.planes, kp, m * kp, w.cq, np, m, kp, pl.n, s);
   if (st != MCF_OK) return st;
   if (ev) cudaEventRecord(ev[2], s);
-  // fallback threshold (scaled units): 2^50 x the error bound per output
-  // (per product bound x K); inexact elements of a six-digit B add 2^-48
-  // (1.01) / 2 to every output of their column (thr_inexact each)
-  const double thr = ldexp((double)k * per_product_bound(sb, nq), 50 - 72);
-  const double thr_inexact = ldexp(0.505, 50 - 48);
+  // error bound per output in C' units (2^-(pa+pb) scaled): A's rounding
+  // (<= 0.51) times |B'| < 2^(pb-1), B's (<= 0.51 for an MC B; for a binary32
+  // B only its counted inexact elements, each <= 0.51 2^(pa-1)), their
+  // product, and the CRT slices' tail (<= 2^12 units of 2^(L - 99)).  The
+  // fallback threshold is 2^50 times it, in units of Y = C' / 2^(L-99).
+  const int L = host_crt().tab[pl.n].L;
+  const double per = 0.51 * std::ldexp(1.0, pl.pb - 1) + (pb.ncb == 2 ? 0.51 * std::ldexp(1.0, pl.pa - 1) : 0.0) + 0.27;
+  const double e_y = (double)k * per * std::ldexp(1.0, 99 - L) + 4096.0;
+  const double thr = std::ldexp(e_y * 1.0001, 50);
+  const double thr_inexact = std::ldexp(0.51 * std::ldexp(1.0, pl.pa - 1) * std::ldexp(1.0, 99 - L) * 1.0001, 50);
+  const int sexp = L - 99 - pl.pa - pl.pb;
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
-  k_combine<<<gc, 256, 0, s>>>(cq, m, n, np, (int)g.nkc, nq, ea, pb.eb, rnf, pb.cnf, pb.cinx, thr, thr_inexact,
-                                                          out, ldo, rlist, rcnt, ep);
+  const bool big = k > 16384;
+  OZ_NMOD_SWITCH(pl.n,
+                 if (big) k_crt<NM, true><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, thr,
+                                                             thr_inexact, sexp, out, ldo, w.rlist, w.rcnt, ep);
+                 else k_crt<NM, false><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, thr,
+                                                          thr_inexact, sexp, out, ldo, w.rlist, w.rcnt, ep));
   mcfr::note_launch();
-  if (nca == 2 && pb.ncb == 2) launch_fallback<2, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
-  else if (nca == 2) launch_fallback<2, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
-  else if (pb.ncb == 2) launch_fallback<1, 2>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
-  else launch_fallback<1, 1>(x, pb.bt, m, n, k, rlist, rcnt, rnf, pb.cnf, out, ldo, ep, s);
+  if (nca == 2 && pb.ncb == 2) st = launch_fallback<2, 2>(x, pb.bt, m, n, k, w.rlist, w.rcnt, w.rnf, pb.cnf, out, ldo, ep, s);
+  else if (nca == 2) st = launch_fallback<2, 1>(x, pb.bt, m, n, k, w.rlist, w.rcnt, w.rnf, pb.cnf, out, ldo, ep, s);
+  else if (pb.ncb == 2) st = launch_fallback<1, 2>(x, pb.bt, m, n, k, w.rlist, w.rcnt, w.rnf, pb.cnf, out, ldo, ep, s);
+  else st = launch_fallback<1, 1>(x, pb.bt, m, n, k, w.rlist, w.rcnt, w.rnf, pb.cnf, out, ldo, ep, s);
+  if (st != MCF_OK) return st;
   if (ev) cudaEventRecord(ev[3], s);
-  return mcfr::check_launch("mm_fast combine kernels");
+  return mcfr::check_launch("mm_fast reconstruction kernels");
 }
 
 // ---- binary32 x binary32 -> binary32 GEMM on the int8 tensor cores ---------------------
@@ -1437,94 +1535,57 @@ __global__ void __launch_bounds__(256) k_b16_comb(const int* __restrict__ cq, in
 namespace mcfr {
 
 bool ozaki_supported(int64_t m, int64_t k, int64_t n) {
-  return m > 0 && n > 0 && k > 0 && m * n < (int64_t(1) << 31) && mcfg::oz::kgeo(k).nkc <= mcfg::oz::kMaxChunks;
+  // K <= 65536: the reconstruction's residue sums stay exact binary32 integers
+  return m > 0 && n > 0 && k > 0 && k <= 65536 && m * n < (int64_t(1) << 31) && mcfg::oz::crt_plan(k, 2).n > 0 &&
+         mcfg::oz::crt_plan(k, 1).n > 0;
+}
+
+// A's residues on a side stream while B is prepared on the caller's stream
+// (thread-local fork / join events, no per-call event creation)
+static mcf_status prepare_both(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n,
+                               char* ws, std::size_t bb, mcfg::oz::PreparedB& pb, mcfg::oz::RowsWs& rw,
+                               cudaStream_t s) {
+  using namespace mcfg::oz;
+  const CrtPlan pl = crt_plan(k, ncb);
+  rw = rows_ws(ws + bb, m, pad32(k), pad16(n), pl.n);
+  cudaStream_t as = side_stream(12);
+  cudaEvent_t fork = tl_event(0), adone = tl_event(1);
+  cudaEventRecord(fork, s);
+  cudaStreamWaitEvent(as, fork, 0);
+  mcf_status st = a_residues(x, nca, m, k, pl, rw, as);
+  cudaEventRecord(adone, as);
+  if (st == MCF_OK) st = prepare_b(w, ncb, k, n, n, ws, pb, s);
+  cudaStreamWaitEvent(s, adone, 0);
+  return st;
 }
 
 // one-call MC(nc=2, binary32) x T / MC(nc=2) product on the INT8 tensor cores
 mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n, float* out,
                     cudaStream_t s) {
   using namespace mcfg::oz;
-  const std::size_t bb = b_bytes(k, n, ncb);
-  static const int halves_env = [] {
-    const char* e = getenv("MCF_OZ_SPLIT");  // tuning knob: row parts on parallel streams
-    return e ? atoi(e) : 1;  // measured: 2 parts gain 0.5% at config 2
-  }();
-  const int parts = m >= 2048 ? std::max(1, std::min(halves_env, 4)) : 1;
-  const int64_t rp = (m + parts - 1) / parts;
-  const std::size_t rb = rows_bytes(rp, k, n);
-  char* ws = oz_workspace(bb + parts * al(rb), s);
-  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
+  const std::size_t bb = al(b_bytes(k, n, ncb));
+  char* ws = oz_workspace(bb + al(rows_bytes(m, k, n, ncb)), s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
   PreparedB pb;
-  if (parts == 1) {
-    // A's digits on a side stream while B is prepared on the caller's
-    const RowsWs rw = rows_ws(ws + bb, m, kgeo(k), pad16(n));
-    cudaStream_t as = side_stream(12);
-    cudaEvent_t fork = nullptr, adone = nullptr;
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&adone, cudaEventDisableTiming);
-    cudaEventRecord(fork, s);
-    cudaStreamWaitEvent(as, fork, 0);
-    mcf_status st = a_digits(x, nca, m, kgeo(k), rw, as);
-    cudaEventRecord(adone, as);
-    if (st == MCF_OK) st = prepare_b(w, ncb, k, n, n, ws, pb, s);
-    cudaStreamWaitEvent(s, adone, 0);
-    cudaEventDestroy(fork);
-    cudaEventDestroy(adone);
-    if (st != MCF_OK) return st;
-    return rows_products(x, nca, m, pb, out, n, rw, s, nullptr, Epilogue{});
-  }
-  mcf_status st = prepare_b(w, ncb, k, n, n, ws, pb, s);
+  RowsWs rw;
+  const mcf_status st = prepare_both(x, nca, w, ncb, m, k, n, ws, bb, pb, rw, s);
   if (st != MCF_OK) return st;
-  // row parts on the caller's stream and side streams (forked and joined by
-  // events): one part's recombination / fallback overlaps the next part's
-  // GEMMs, whose last wave leaves SMs idle
-  cudaEvent_t fork = nullptr, join[4] = {};
-  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-  cudaEventRecord(fork, s);
-  for (int p = 0; p < parts && st == MCF_OK; ++p) {
-    const int64_t r0 = p * rp, rows_p = std::min<int64_t>(rp, m - r0);
-    cudaStream_t ps = p == 0 ? s : side_stream(8 + p);
-    if (p > 0) cudaStreamWaitEvent(ps, fork, 0);
-    st = rows(x + r0 * k * nca, nca, rows_p, pb, out + r0 * n * 2, n, ws + bb + p * al(rb), ps);
-    if (p > 0) {
-      cudaEventCreateWithFlags(&join[p], cudaEventDisableTiming);
-      cudaEventRecord(join[p], ps);
-    }
-  }
-  for (int p = 1; p < parts; ++p)
-    if (join[p]) {
-      cudaStreamWaitEvent(s, join[p], 0);
-      cudaEventDestroy(join[p]);
-    }
-  cudaEventDestroy(fork);
-  return st;
+  return rows_products(x, nca, m, pb, out, n, rw, s, nullptr, Epilogue{});
 }
 
 // MC-MLP layer forward on the tensor-core path with the bias / approx / ReLU
-// epilogue fused into the recombination: h = approx(add_mcn(W . A, bias)),
+// epilogue fused into the reconstruction: h = approx(add_mcn(W . A, bias)),
 // act = relu(h); the MC product itself is never written
 mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t k, int64_t n, const float* bias,
                              int relu, float* h, float* act, cudaStream_t s) {
   using namespace mcfg::oz;
   if (m < 64 || !ozaki_supported(m, k, n)) return MCF_ERR_UNSUPPORTED;
-  const std::size_t bb = b_bytes(k, n, 1);
-  char* ws = oz_workspace(bb + rows_bytes(m, k, n), s);
-  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
+  const std::size_t bb = al(b_bytes(k, n, 1));
+  char* ws = oz_workspace(bb + al(rows_bytes(m, k, n, 1)), s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
   PreparedB pb;
-  // W's digits on a side stream while the activations are prepared
-  const RowsWs rw = rows_ws(ws + bb, m, kgeo(k), pad16(n));
-  cudaStream_t as = side_stream(12);
-  cudaEvent_t fork = nullptr, adone = nullptr;
-  cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&adone, cudaEventDisableTiming);
-  cudaEventRecord(fork, s);
-  cudaStreamWaitEvent(as, fork, 0);
-  mcf_status st = a_digits(w, 2, m, kgeo(k), rw, as);
-  cudaEventRecord(adone, as);
-  if (st == MCF_OK) st = prepare_b(a, 1, k, n, n, ws, pb, s);
-  cudaStreamWaitEvent(s, adone, 0);
-  cudaEventDestroy(fork);
-  cudaEventDestroy(adone);
+  RowsWs rw;
+  const mcf_status st = prepare_both(w, 2, a, 1, m, k, n, ws, bb, pb, rw, s);
   if (st != MCF_OK) return st;
   Epilogue ep;
   ep.bias = bias;
@@ -1534,26 +1595,46 @@ mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t 
   return rows_products(w, 2, m, pb, nullptr, n, rw, s, nullptr, ep);
 }
 
-int ozaki_digits() { return mcfg::oz::kS; }
-
-// int8 GEMM-equivalents (M x N x K each) per product: pairs (s, t) with
-// s + t < kS, s < kS, t < b_digits
-int ozaki_gemm_equivalents(int ncb, int64_t k) {
+// host-side introspection of the CRT scheme (no device needed): the plan of a
+// K-long product and the constants of an n-moduli reconstruction
+int ozaki_crt_info(int64_t k, int ncb, int* n, int* pa, int* pb) {
+  const mcfg::oz::CrtPlan pl = mcfg::oz::crt_plan(k, ncb);
+  if (n) *n = pl.n;
+  if (pa) *pa = pl.pa;
+  if (pb) *pb = pl.pb;
+  return pl.n;
+}
+int ozaki_crt_table(int n, int* moduli, float* w, float* mh, float* cq, int* bits) {
   using namespace mcfg::oz;
-  int c = 0;
-  for (int q = 0; q < diagonals(k); ++q) c += std::min(q, b_digits(ncb) - 1) - std::max(0, q - (kS - 1)) + 1;
-  return c;
+  if (n < 1 || n > kMaxMod) return 0;
+  const HostCrt& h = host_crt();
+  for (int t = 0; t < n; ++t) {
+    if (moduli) moduli[t] = kModuli[t];
+    for (int j = 0; j < kSlices; ++j)
+      if (w) w[t * kSlices + j] = h.tab[n].w[t][j];
+  }
+  for (int j = 0; j < kSlices; ++j)
+    if (mh) mh[j] = h.tab[n].mh[j];
+  if (cq) *cq = h.tab[n].cq;
+  if (bits) *bits = h.tab[n].L;
+  return kSlices;
 }
 
-// one product with phase timing: ms[0] B digits, ms[1] A digits, ms[2] the
-// int8 GEMMs, ms[3] recombination + fallback; *fallback = listed outputs
+// moduli of a K = 4096 MC x T product (ABI compatibility: mcf_fast_tc_digits)
+int ozaki_digits() { return mcfg::oz::crt_plan(4096, 1).n; }
+
+// int8 GEMMs (M x N x K each) per product: one per modulus
+int ozaki_gemm_equivalents(int ncb, int64_t k) { return mcfg::oz::crt_plan(k, ncb).n; }
+
+// one product with phase timing: ms[0] B residues, ms[1] A residues, ms[2] the
+// int8 GEMMs, ms[3] reconstruction + fallback; *fallback = listed outputs
 mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, double* ms,
                         int64_t* fallback, cudaStream_t s) {
   using namespace mcfg::oz;
   if (!ozaki_supported(m, k, n)) return fail(MCF_ERR_UNSUPPORTED, "mm_fast: shape outside the tensor-core path");
-  const std::size_t bb = b_bytes(k, n, 1);
-  char* ws = oz_workspace(bb + rows_bytes(m, k, n), s);
-  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
+  const std::size_t bb = al(b_bytes(k, n, 1));
+  char* ws = oz_workspace(bb + al(rows_bytes(m, k, n, 1)), s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
   cudaEvent_t ev[5];
   for (auto& e : ev) cudaEventCreate(&e);
   cudaEventRecord(ev[4], s);
@@ -1569,11 +1650,9 @@ mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, in
       cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
       ms[i + 1] = t;
     }
-    // the per-row fallback counters sit at the end of the rows region
-    const KGeo g = kgeo(k);
-    const char* cnt = reinterpret_cast<const char*>(rows_ws(ws + bb, m, g, pad16(n)).rcnt);
+    const RowsWs rw = rows_ws(ws + bb, m, pb.kp, pb.np, pb.plan.n);
     std::vector<int> rc(m);
-    cudaMemcpy(rc.data(), cnt, m * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaMemcpy(rc.data(), rw.rcnt, m * sizeof(int), cudaMemcpyDeviceToHost);
     int64_t c = 0;
     for (int v : rc) c += v;
     *fallback = c;
@@ -1608,9 +1687,9 @@ mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, in
   const int64_t nbk = blocks_env > 0 ? blocks_env : 1;  // measured: column blocks do not pay at config 2
   const int64_t bw = pad16((n + nbk - 1) / nbk);
   const int nb = (int)((n + bw - 1) / bw);
-  const std::size_t bb = b_bytes(k, bw, 1), rb = rows_bytes(rc, k, bw);
+  const std::size_t bb = al(b_bytes(k, bw, 1)), rb = al(rows_bytes(rc, k, bw, 1));
   char* ws = oz_workspace(nb * al(bb) + 2 * rb, comp[0]);
-  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the digit-plane workspace");
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
   std::vector<cudaEvent_t> evb(nb, nullptr), evp(nb, nullptr), eva(nch, nullptr), evt(nch * nb, nullptr);
   std::vector<cudaEvent_t*> all;
   for (auto* v : {&evb, &evp, &eva, &evt})

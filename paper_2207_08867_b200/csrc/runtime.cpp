@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <random>
 #include <string>
@@ -107,6 +108,27 @@ cudaStream_t side_stream(int slot) {
   DevState& s = g_dev[cur_dev()];
   if (!s.streams[slot]) cudaStreamCreateWithFlags(&s.streams[slot], cudaStreamNonBlocking);
   return s.streams[slot];
+}
+
+// fn() exactly once per (device, tag); concurrent callers on the same device
+// wait until it has finished (std::call_once)
+namespace {
+constexpr int kOnceTags = 16;
+std::once_flag g_once[kMaxDev][kOnceTags];
+}  // namespace
+void per_device_once(int tag, const std::function<void()>& fn) {
+  std::call_once(g_once[cur_dev()][tag % kOnceTags], fn);
+}
+
+// thread-local, per-device reusable fork/join events (disable-timing): a wait
+// captures the event's state when it is enqueued, so re-recording the same
+// event later on the same host thread is safe
+cudaEvent_t tl_event(int slot) {
+  constexpr int kEv = 16;
+  thread_local cudaEvent_t ev[kMaxDev][kEv] = {};
+  cudaEvent_t& e = ev[cur_dev()][slot % kEv];
+  if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
 }
 
 mcf_status ensure_stack(std::size_t bytes) {

@@ -293,3 +293,42 @@ def test_fast_gemm_int8_nonfinite_rows_are_nan():
     ok[:, 9] = False
     want = A.astype(np.float64) @ B.astype(np.float64)
     assert np.allclose(got[ok], want[ok], rtol=0, atol=1e-5 * np.abs(want[ok]).max())
+
+
+def test_config3_fast_tracks_reference_within_spread():
+    """Config 3's network (784-1024-1024-10, nc=2, the bench's init and data
+    generators) at a reduced batch of 512 for 6 steps: plan FAST (int8
+    tensor-core forward with the fused bias / approx / ReLU epilogue, int8
+    digit backward GEMMs) against the reference-order plan, which is
+    bit-identical to the reference (test_reference_order_training_is_bitwise).
+    Bound per step: 4x the reference's own summation-order spread,
+    measured as the same reference-order run on the batch in reversed sample
+    order (every binary32 gradient sum over the batch and the loss sum run in
+    the other order), running max over the steps so far, floored at 1 ulp of
+    the loss."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+    from paper_2207_08867_b200 import mlp
+
+    dims, n, steps = [784, 1024, 1024, 10], 512, 6
+    params = mlp.init_params(dims, 2)
+    xb, yb = mlp.make_batch(n)
+
+    def run(plan, order):
+        model = mlp.MCMLP(dims, params, lr=0.01, plan=plan)
+        xt = torch.from_numpy(np.ascontiguousarray(xb[order].T)).cuda()
+        yt = torch.from_numpy(np.ascontiguousarray(yb[order])).cuda()
+        return np.array([model.loss_value(model.step(xt, yt, n), n) for _ in range(steps)], np.float64)
+
+    fwd = np.arange(n)
+    ref = run(mcf.SEQUENTIAL, fwd)
+    ref_rev = run(mcf.SEQUENTIAL, fwd[::-1])
+    fast = run(mcf.FAST, fwd)
+    spread = np.maximum.accumulate(np.abs(ref - ref_rev))
+    ulp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    bound = 4 * np.maximum(spread, ulp)
+    diff = np.abs(fast - ref)
+    print("reference losses", ref, "\nreversed-order spread", spread, "\nFAST diff", diff)
+    assert np.all(diff <= bound), (diff, bound)
+    assert ref[-1] < ref[0]  # it trains
