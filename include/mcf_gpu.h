@@ -173,6 +173,13 @@ int mcf_fast_tc_crt_table(int n, int* moduli, float* w_slices, float* m_slices, 
  * the fallback.  Synchronises the stream. */
 mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
                               double* phase_ms, int64_t* fallback_outputs, mcf_stream stream);
+/* The hand-written tcgen05 int8 GEMM (tc_gemm.cu) behind the tensor-core
+ * path, exposed for tests and probes: out_b = a_b . b_b^T for b < batch with
+ * a: [batch][m][kp], b: [batch][n][kp] int8 (kp % 16 == 0), out: [batch][m][ldo]
+ * int32 when moduli is null, else the symmetric int8 residues out_b mod
+ * moduli[b] (moduli are those of mcf_fast_tc_crt_table, batch <= 32). */
+mcf_status mcf_tc_gemm_s8(const void* a, const void* b, void* out, int64_t m, int64_t n, int64_t kp, int batch,
+                          int64_t ldo, const int* moduli, mcf_stream stream);
 /* FP64-pipe instructions per multiply-add of the MCF_FAST kernel for this
  * operand kind (mcmc = 0: MC x Tensor, 1: MC x MC); 0 = no fast kernel. */
 int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);

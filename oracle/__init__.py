@@ -127,6 +127,28 @@ class Oracle:
             L.mcfref_time_dot_mcmc.restype = C.c_double
             L.mcfref_mlp_train.argtypes = [_p, _int, _int, _p, _p, _p, _i64, _int, C.c_double, _p, _p]
             L.mcfref_mlp_train.restype = _int
+            L.mcfref_rng_uniform.argtypes = [C.c_uint64, _i64, _p]
+            L.mcfref_rng_uniform.restype = None
+            L.mcfref_rng_normal.argtypes = [C.c_uint64, _i64, _p]
+            L.mcfref_rng_normal.restype = None
+            L.mcfref_rng_below.argtypes = [C.c_uint64, C.c_uint64, _i64, _p]
+            L.mcfref_rng_below.restype = None
+
+    # ---- the reference's own Rng (rng.hpp:13-65), ref back end only ----------
+    def rng_uniform(self, seed, n):
+        out = np.empty(n, np.float64)
+        self.lib.mcfref_rng_uniform(seed, n, _ptr(out))
+        return out
+
+    def rng_normal(self, seed, n):
+        out = np.empty(n, np.float64)
+        self.lib.mcfref_rng_normal(seed, n, _ptr(out))
+        return out
+
+    def rng_below(self, seed, bound, n):
+        out = np.empty(n, np.uint64)
+        self.lib.mcfref_rng_below(seed, bound, n, _ptr(out))
+        return out
 
     @staticmethod
     def _check(rc, what):

@@ -563,4 +563,20 @@ int mcfref_mlp_train(const int* dims, int nlayers, int nc, const float* params, 
   return 0;
 }
 
+
+// the reference's own generator (rng.hpp:13-65): the bench's reference arm
+// draws its inputs here, so it never loads the product library
+void mcfref_rng_uniform(std::uint64_t seed, std::int64_t n, double* out) {
+  mcf::Rng g(seed);
+  for (std::int64_t i = 0; i < n; ++i) out[i] = g.uniform();
+}
+void mcfref_rng_normal(std::uint64_t seed, std::int64_t n, double* out) {
+  mcf::Rng g(seed);
+  for (std::int64_t i = 0; i < n; ++i) out[i] = g.normal();
+}
+void mcfref_rng_below(std::uint64_t seed, std::uint64_t bound, std::int64_t n, std::uint64_t* out) {
+  mcf::Rng g(seed);
+  for (std::int64_t i = 0; i < n; ++i) out[i] = g.below(bound);
+}
+
 }  // extern "C"

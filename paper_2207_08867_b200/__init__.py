@@ -72,6 +72,7 @@ _SIGS = {
     "mcf_fast_mm_phases": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
     "mcf_fast_tc_plan": [_i64, _int, _p, _p, _p],
     "mcf_fast_tc_crt_table": [_int, _p, _p, _p, _p, _p],
+    "mcf_tc_gemm_s8": [_p, _p, _p, _i64, _i64, _i64, _int, _i64, _p, _p],
     "mcf_probe_pipe_rates": [_p, _p],
     "mcf_mlp_bias_act": [_p, _int, _p, _i64, _i64, _int, _p, _p, _p],
     "mcf_mlp_cross_entropy": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],

@@ -600,6 +600,72 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
 }
 
 
+// k_crt on residues the tcgen05 GEMM's epilogue already reduced (int8 planes
+// rq[t][i][ldr], tc_gemm.cu): one 32-bit load per plane per thread (four
+// columns), the slice sums as packed FFMA2 over column pairs; the rest as
+// k_crt.
+template <int NMOD>
+__global__ void __launch_bounds__(256) k_crt8(const int8_t* __restrict__ rq, int64_t m, int64_t n, int64_t ldr,
+                                              const int* __restrict__ ea, const int* __restrict__ eb,
+                                              const int* __restrict__ rnf, const int* __restrict__ cnf,
+                                              const int* __restrict__ cinx, double thr, double thr_inexact, int sexp,
+                                              float* __restrict__ out, int64_t ldo, int* __restrict__ rlist,
+                                              int* __restrict__ rcnt, Epilogue ep) {
+  const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= n) return;
+  const int64_t plane = m * ldr;
+  int fj[4], nfj[4];
+  double thj[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    fj[u] = j0 + u < n ? eb[j0 + u] : 0;
+    nfj[u] = j0 + u < n ? cnf[j0 + u] & 1 : 0;
+    thj[u] = thr + (cinx && j0 + u < n ? thr_inexact * cinx[j0 + u] : 0.0);
+  }
+  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+    const int64_t off = i * ldr + j0;
+    float2 T[2][kSlices];  // [column pair][slice] = (column 2p, column 2p + 1)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < kSlices; ++j) T[h][j] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int t = 0; t < NMOD; ++t) {
+      const unsigned wv = __ldcs(reinterpret_cast<const unsigned*>(rq + t * plane + off));
+      float r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)  // sign-extended byte u, exact int -> float through kMagic
+        r[u] = __fsub_rn(__int_as_float(((int)(wv << (24 - 8 * u)) >> 24) + 0x4B400000), kMagic);
+#pragma unroll
+      for (int j = 0; j < kSlices; ++j) {
+        const float2 w2 = make_float2(c_crt[NMOD].w[t][j], c_crt[NMOD].w[t][j]);
+        T[0][j] = __ffma2_rn(make_float2(r[0], r[1]), w2, T[0][j]);
+        T[1][j] = __ffma2_rn(make_float2(r[2], r[3]), w2, T[1][j]);
+      }
+    }
+    const int ei = ea[i], fi = rnf[i] & 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u;
+      if (j >= n) break;
+      float Tu[kSlices];
+#pragma unroll
+      for (int s = 0; s < kSlices; ++s) Tu[s] = (u & 1) ? T[u >> 1][s].y : T[u >> 1][s].x;
+      const float u0 = __fmaf_rn(Tu[1], 0x1p-11f, Tu[0]);
+      const float q = __fsub_rn(__fmaf_rn(u0, c_crt[NMOD].cq, kMagic), kMagic);
+      double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], Tu[0]);
+#pragma unroll
+      for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], Tu[s]));
+      if (fi | nfj[u] || !(fabs(y) >= thj[u])) {
+        rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
+        continue;
+      }
+      const double v[2] = {__dmul_rn(y, pow2d(sexp + ei + fj[u])), 0.0};
+      emit(v, i, j, out, ldo, ep);
+    }
+  }
+}
+
 // the listed outputs: a CTA per row.  The CTA stages its row of A in shared
 // memory (SMEM; rows too long for it read A through L1).  A row lists few
 // outputs (config 2: 3.6 on average), so each listed output's k range is cut
@@ -1129,9 +1195,22 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   const CrtPlan pl = pb.plan;
   const int64_t k = pb.k, kp = pb.kp, n = pb.n, np = pb.np;
   if (ev) cudaEventRecord(ev[1], s);
-  // one strided-batched GEMM over the moduli: C_t (np x m col-major = m x np
-  // row-major) = B_t^T-planes . A_t-planes
-  mcf_status st = gemm_s8(pb.planes, kp, np * kp, w.planes, kp, m * kp, w.cq, np, m, kp, pl.n, s);
+  // The residue GEMMs: by default the hand-written tcgen05 kernel
+  // (tc_gemm.cu), whose epilogue reduces each int32 sum modulo its modulus and
+  // writes int8 residues (planes [t][m][np]); MCF_OZ_GEMM=cublaslt runs one
+  // strided-batched cuBLASLt GEMM writing the int32 sums instead (kept for
+  // A/B measurement): C_t (np x m col-major = m x np row-major).
+  static const bool use_lt = [] {
+    const char* e = getenv("MCF_OZ_GEMM");
+    return e && std::string(e) == "cublaslt";
+  }();
+  mcf_status st;
+  if (use_lt) {
+    st = gemm_s8(pb.planes, kp, np * kp, w.planes, kp, m * kp, w.cq, np, m, kp, pl.n, s);
+  } else {
+    st = mcfr::tc_gemm_s8(w.planes, pb.planes, w.cq, m, n, kp, pl.n, np, kModuli, s, np);
+    if (st == MCF_ERR_UNSUPPORTED) st = mcfr::fail(MCF_ERR_CUDA, "mm_fast: the tcgen05 residue GEMM cannot run this shape");
+  }
   if (st != MCF_OK) return st;
   if (ev) cudaEventRecord(ev[2], s);
   // error bound per output in C' units (2^-(pa+pb) scaled): A's rounding
@@ -1148,6 +1227,11 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
   const bool big = k > 16384;
+  if (!use_lt) {
+    OZ_NMOD_SWITCH(pl.n, k_crt8<NM><<<gc, 256, 0, s>>>(reinterpret_cast<const int8_t*>(w.cq), m, n, np, w.ea, pb.eb,
+                                                       w.rnf, pb.cnf, pb.cinx, thr, thr_inexact, sexp, out, ldo,
+                                                       w.rlist, w.rcnt, ep));
+  } else
   OZ_NMOD_SWITCH(pl.n,
                  if (big) k_crt<NM, true><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, thr,
                                                              thr_inexact, sexp, out, ldo, w.rlist, w.rcnt, ep);

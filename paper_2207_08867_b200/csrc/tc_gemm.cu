@@ -1,0 +1,384 @@
+// tc_gemm.cu -- hand-written tcgen05 int8 GEMM for sm_100a (the residue GEMMs
+// of the MCF_FAST tensor-core contraction, mm_ozaki.cu).
+//
+//   C_b (m x n, int32) = A_b (m x kp, int8, K contiguous) . B_b (n x kp)^T
+//   for b < batch; epilogue either writes C_b (int32) or, for the CRT scheme,
+//   C_b mod m_b as symmetric int8 residues (the reconstruction then reads a
+//   quarter of the bytes and no reduction is left to do).
+//
+// Structure (one CTA per SM, persistent over (b, row block, column block)
+// tiles of 128 x 256):
+//   warp 0      TMA producer: 128-byte K blocks of A (128 rows) and B (256
+//               rows) into a 4-stage shared-memory ring, SWIZZLE_128B,
+//               mbarrier transaction counts;
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
+//               .cta_group::1.kind::i8 (M 128, N 256, K 32; four per stage)
+//               into one of two TMEM accumulators (2 x 256 columns), and
+//               tcgen05.commit frees the stage / hands the accumulator over;
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (each warp its 32 TMEM lanes
+//               = rows), exact int32 -> residue reduction, 32-byte stores,
+//               then releases the accumulator (double buffering overlaps a
+//               tile's epilogue with the next tile's MMAs).
+// int32 accumulation of int8 products is exact (|C| <= K 2^14 < 2^31 for
+// K < 2^17).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <mutex>
+
+#include "mcf_runtime.h"
+
+namespace mcfg {
+namespace tc {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 128;  // BK: bytes (= int8 elements) per stage per row
+constexpr int kStages = 4;
+constexpr int kABytes = BM * BK, kBBytes = BN * BK, kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+constexpr int kTmemCols = 512;
+constexpr int kMaxBatch = 32;
+constexpr float kMagic = 12582912.0f;  // 1.5 2^23
+
+struct Params {
+  int m, n, kp, batch, tiles_m, tiles_n;
+  int64_t ldo;           // output row stride (elements)
+  int mode;              // 0: int32 C, 1: int8 residues C mod m_b
+  void* out;             // [batch][m][ldo]
+  float mod[kMaxBatch];  // modulus of batch entry b (mode 1)
+  float inv[kMaxBatch];  // RN32(1 / m_b)
+  float c14[kMaxBatch];  // 2^14 mod m_b, symmetric
+  int big;               // |C| may exceed 2^28 (K > 2^14): two-step reduction
+};
+
+// ---- PTX helpers ----
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// K-major operand in the canonical SWIZZLE_128B layout (8-row atoms of 128 B,
+// atoms 1024 B apart): start >> 4, LBO 1 (16 B, unused when swizzled), SBO
+// 1024 >> 4, version 1 (sm_100), layout type 2 = SWIZZLE_128B
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+// kind::i8 instruction descriptor: D s32 (c_format 2), A / B s8 (format 1),
+// both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+
+#define TMEM_LD32(taddr, v)                                                                                     \
+  asm volatile(                                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                        \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),        \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),   \
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),              \
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),              \
+        "=r"(v[30]), "=r"(v[31])                                                                                \
+      : "r"(taddr))
+
+// C mod m (symmetric) of an exact int32 sum, as kMagic + r (low byte = r as
+// int8); the same arithmetic as mm_ozaki.cu's mod_c (CPU-pinned in
+// tests/test_crt_scheme.py)
+__device__ __forceinline__ uint32_t mod_bits(int c, float m, float inv, float c14, bool big) {
+  const int cl = ((c + 8192) & 16383) - 8192, ch = (c - cl) >> 14;
+  const float fl = __fsub_rn(__int_as_float(cl + 0x4B400000), kMagic);
+  const float fh = __fsub_rn(__int_as_float(ch + 0x4B400000), kMagic);
+  float s = __fmaf_rn(fh, c14, fl);
+  if (big) {
+    const float q0 = __fsub_rn(__fmaf_rn(s, inv, kMagic), kMagic);
+    s = __fmaf_rn(-q0, m, s);
+  }
+  const float q = __fsub_rn(__fmaf_rn(s, inv, kMagic), kMagic);
+  return __float_as_uint(__fmaf_rn(-q, m, __fadd_rn(s, kMagic)));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_gemm_s8(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the SWIZZLE_128B atoms
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);  // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int per_b = p.tiles_m * p.tiles_n;
+  const int total = per_b * p.batch;
+  const int kblocks = (p.kp + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_expect_tx(full + stage, kStageBytes);
+          tma_load_3d(sa + stage * kABytes, &ta, kb * BK, mb * BM, b, full + stage);
+          tma_load_3d(sb + stage * kBBytes, &tb, kb * BK, nb * BN, b, full + stage);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(tempty + acc, aphase ^ 1);
+        fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * kABytes), b0 = smem_u32(sb + stage * kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            umma_i8(d, smem_desc(a0 + kk * 32), smem_desc(b0 + kk * 32), (kb | kk) != 0);
+          umma_commit(empty + stage);  // the stage is free once these MMAs have read it
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull + acc);  // accumulator complete
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 = tile rows
+    const int q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+      mbar_wait(tfull + acc, aphase);
+      fence_after();
+      const int row = mb * BM + row_in_tile;
+      const bool row_ok = row < p.m;
+      const float fm = p.mod[b < kMaxBatch ? b : 0], fi = p.inv[b < kMaxBatch ? b : 0],
+                  fc = p.c14[b < kMaxBatch ? b : 0];
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int col = nb * BN + c * 32;
+        if (!row_ok || col >= p.n) continue;
+        if (p.mode == 0) {
+          int* o = static_cast<int*>(p.out) + ((int64_t)b * p.m + row) * p.ldo + col;
+#pragma unroll
+          for (int u = 0; u < 32; u += 4)
+            if (col + u < p.n) *reinterpret_cast<int4*>(o + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+        } else {
+          uint32_t w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t r0 = mod_bits((int)v[4 * u], fm, fi, fc, p.big),
+                           r1 = mod_bits((int)v[4 * u + 1], fm, fi, fc, p.big),
+                           r2 = mod_bits((int)v[4 * u + 2], fm, fi, fc, p.big),
+                           r3 = mod_bits((int)v[4 * u + 3], fm, fi, fc, p.big);
+            w[u] = __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+          }
+          int8_t* o = static_cast<int8_t*>(p.out) + ((int64_t)b * p.m + row) * p.ldo + col;
+          *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (col + 16 < p.n) *reinterpret_cast<uint4*>(o + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// [batch][rows][kp] int8, box 128 (K bytes) x box_rows x 1, SWIZZLE_128B
+bool make_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t kp, int batch, int box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)(rows * kp)};
+  const cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1u};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+}  // namespace tc
+}  // namespace mcfg
+
+namespace mcfr {
+
+// C_b = A_b . B_b^T (b < batch) on the hand-written tcgen05 kernel.
+// a: [batch][m][kp], b: [batch][b_rows][kp] int8 (the first n rows used) (kp % 16 == 0, 16-byte aligned
+// bases); out: [batch][m][ldo] int32 (moduli == nullptr) or int8 residues
+// C_b mod moduli[b] (symmetric).  MCF_ERR_UNSUPPORTED when the shape or the
+// driver's tensor-map entry point is unavailable.
+mcf_status tc_gemm_s8(const int8_t* a, const int8_t* b, void* out, int64_t m, int64_t n, int64_t kp, int batch,
+                      int64_t ldo, const int* moduli, cudaStream_t s, int64_t b_rows) {
+  if (b_rows < n) b_rows = n;  // rows per plane of b (>= n: padded columns)
+  using namespace mcfg::tc;
+  if (m <= 0 || n <= 0 || kp <= 0 || kp % 16 != 0 || batch < 1 || (moduli && batch > kMaxBatch) ||
+      kp >= (int64_t(1) << 17) || m >= (int64_t(1) << 31) || n >= (int64_t(1) << 31))
+    return MCF_ERR_UNSUPPORTED;
+  // the epilogue's 16-byte stores: int32 rows a multiple of 4 elements,
+  // residue rows of 16 bytes, 16-byte aligned bases
+  if (ldo < n || ldo % (moduli ? 16 : 4) != 0 || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+    return MCF_ERR_UNSUPPORTED;
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, a, m, kp, batch, BM) || !make_map(&tb, b, b_rows, kp, batch, BN)) return MCF_ERR_UNSUPPORTED;
+  Params p{};
+  p.m = (int)m;
+  p.n = (int)n;
+  p.kp = (int)kp;
+  p.batch = batch;
+  p.tiles_m = (int)((m + BM - 1) / BM);
+  p.tiles_n = (int)((n + BN - 1) / BN);
+  p.ldo = ldo;
+  p.mode = moduli ? 1 : 0;
+  p.out = out;
+  p.big = kp > 16384;
+  if (moduli)
+    for (int i = 0; i < batch; ++i) {
+      const int mm = moduli[i];
+      int p14 = 1;
+      for (int t = 0; t < 14; ++t) p14 = p14 * 2 % mm;
+      if (p14 > mm / 2) p14 -= mm;
+      p.mod[i] = (float)mm;
+      p.inv[i] = 1.0f / (float)mm;
+      p.c14[i] = (float)p14;
+    }
+  const int smem = kStages * kStageBytes + 1024 + 256;
+  per_device_once(kOnceTcGemm, [&] {
+    cudaFuncSetAttribute(k_tc_gemm_s8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * batch;
+  const int grid = (int)std::min<int64_t>(tiles, sm_count());
+  k_tc_gemm_s8<<<grid, kThreads, smem, s>>>(ta, tb, p);
+  note_launch();
+  return check_launch("tcgen05 int8 GEMM");
+}
+
+}  // namespace mcfr
+
+extern "C" {
+
+// probe / test entry point: int32 products (moduli == null) or residues
+mcf_status mcf_tc_gemm_s8(const void* a, const void* b, void* out, int64_t m, int64_t n, int64_t kp, int batch,
+                          int64_t ldo, const int* moduli, mcf_stream stream) {
+  if (!a || !b || !out) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "tc_gemm_s8: null argument");
+  const mcf_status st = mcfr::tc_gemm_s8(static_cast<const int8_t*>(a), static_cast<const int8_t*>(b), out, m, n, kp,
+                                         batch, ldo, moduli, static_cast<cudaStream_t>(stream));
+  if (st == MCF_ERR_UNSUPPORTED) return mcfr::fail(st, "tc_gemm_s8: shape or driver entry point unsupported");
+  return st;
+}
+
+}  // extern "C"
