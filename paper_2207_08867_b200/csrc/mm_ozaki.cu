@@ -281,42 +281,65 @@ CrtPlan crt_plan(int64_t k, int ncb) {
 
 // ---- device: residues ----
 
-// X = round((hi + lo) 2^p) for the scaled pair (|hi + lo| < 1/2 after the
-// line's scaling; sc = 2^(p - 48 - e) folds that scaling and the top limb's
-// weight into one exact product), p <= 73, as six balanced 12-bit limbs
-// l[j] (weight 2^(12 j); |l[j]| <= 2^11 + 1 for j < 5, |l[5]| <= 2^12 + 1)
-// as binary32 integers.  Three binary64 steps give H = rint(v 2^(p-48)),
-// M = rint(r1 2^24), L = rint(r2 2^24) with double-double remainders (exact),
-// X = H 2^48 + M 2^24 + L; l0i = the lowest limb as an integer (X mod 256 is
-// its low byte).  Returns true when X is not exactly (hi + lo) 2^p.
-__device__ __forceinline__ bool limbs(double hi, double lo, double sc, float (&l)[6], int& l0i) {
-  const double h = __dmul_rn(hi, sc), hl = __dmul_rn(lo, sc);
-  const double H = rint(h);
-  double r1, r1l;
-  dsum(__dsub_rn(h, H), hl, r1, r1l);
-  const double m = __dmul_rn(r1, 0x1p24), ml = __dmul_rn(r1l, 0x1p24);
-  const double M = rint(m);
-  double r2, r2l;
-  dsum(__dsub_rn(m, M), ml, r2, r2l);
-  const double l24 = __dmul_rn(r2, 0x1p24);
-  const double L = rint(l24);
-  const int v[3] = {__double2int_rn(L), __double2int_rn(M), __double2int_rn(H)};
+// 2^v as a binary32 (v in [-126, 127])
+__device__ __forceinline__ float pow2f(int v) { return __int_as_float((127 + v) << 23); }
+
+// Six balanced 12-bit limbs of round(x 2^s) for two binary32 values at once
+// (x finite; 2^s applied as two exact binary32 products sa sb, so that
+// |x 2^s| < 2^72 never overflows): from the top, t_j = rint(r 2^-12j) by
+// magic-constant rounding (exact while |r 2^-12j| < 2^22), r -= t_j 2^12j
+// (exact: the remainder is a multiple of r's ulp and no larger than r), all
+// packed FFMA2 / FADD2 -- no binary64 work.  The last step rounds the
+// fraction (error <= 1/2); rem is what is left (nonzero: inexact), scaled the
+// input as scaled (zero with x nonzero: underflow, also inexact).  |t_j| <=
+// 2^11 for j < 5, |t_5| <= 2^12.
+__device__ __forceinline__ void limbs2(float2 x, float sa, float sb, float2 (&l)[6], float2& rem, float2& xs) {
+  float2 r = __fmul2_rn(__fmul2_rn(x, make_float2(sa, sa)), make_float2(sb, sb));
+  xs = r;
+  const float2 mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    const int lo12 = ((v[q] + 2048) & 4095) - 2048, hi12 = (v[q] - lo12) >> 12;
-    // exact int -> float for |x| < 2^22 through the magic constant's mantissa
-    l[2 * q] = __fsub_rn(__int_as_float(lo12 + 0x4B400000), kMagic);
-    l[2 * q + 1] = __fsub_rn(__int_as_float(hi12 + 0x4B400000), kMagic);
-    if (q == 0) l0i = lo12;
+  for (int j = 5; j >= 0; --j) {
+    const float dn = pow2f(-12 * j), up = -pow2f(12 * j);
+    const float2 t = __fadd2_rn(__ffma2_rn(r, make_float2(dn, dn), mg), nmg);
+    r = __ffma2_rn(t, make_float2(up, up), r);
+    l[j] = t;
   }
-  return l24 != L || r2l != 0.0;
+  rem = r;
+}
+
+// the limbs of X = round(c0 2^s) + round(c1 2^s) (each rounding <= 1/2; c1 = 0
+// for NC = 1) for two elements; returns the number of inexact elements
+template <int NC>
+__device__ __forceinline__ int limbs_pair(const float (&c0)[2], const float (&c1)[2], float sa, float sb,
+                                          float2 (&l)[6]) {
+  float2 rem, xs;
+  limbs2(make_float2(c0[0], c0[1]), sa, sb, l, rem, xs);
+  int inexact = (rem.x != 0.0f || (xs.x == 0.0f && c0[0] != 0.0f)) + (rem.y != 0.0f || (xs.y == 0.0f && c0[1] != 0.0f));
+  if constexpr (NC == 2) {
+    float2 l1[6], rem1, xs1;
+    limbs2(make_float2(c1[0], c1[1]), sa, sb, l1, rem1, xs1);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) l[j] = __fadd2_rn(l[j], l1[j]);  // |sum| <= 2^12 (2^13 for j = 5): exact
+    inexact += (rem1.x != 0.0f || (xs1.x == 0.0f && c1[0] != 0.0f)) + (rem1.y != 0.0f || (xs1.y == 0.0f && c1[1] != 0.0f));
+  }
+  return inexact;
+}
+
+// the lowest limb as an integer (X mod 256 is its low byte; |l0| < 2^22)
+__device__ __forceinline__ int limb_int(float v) { return __float_as_int(__fadd_rn(v, kMagic)) - 0x4B400000; }
+
+// scale factors 2^(p - e) as two binary32 powers of two
+__device__ __forceinline__ void scale_pair(int p, int e, float& sa, float& sb) {
+  const int s = p - e, s1 = s < 127 ? s : 127;
+  sa = pow2f(s1);
+  sb = pow2f(s - s1);
 }
 
 // kMagic + (X mod m_t), symmetric, for modulus t >= 1 (odd m_t): the limb sum
-// s (|s| < 2^20.9, exact in binary32) reduced by q = rint(s / m_t) from one
-// FFMA (|s RN(1/m) - s / m| < 2^-10.5 < 1 / (2 m), and s / m is never a half
-// integer for odd m, so q is exact); the low byte of the result's bits is the
-// residue as int8.
+// s (|s| <= 127 (2^13 + 5 2^12) < 2^22, exact in binary32, and s + kMagic
+// exact) reduced by q = rint(s / m_t) from one FFMA (|s RN(1/m) - s / m| <=
+// |s| 2^-24 / m < 1 / (2 m), and s / m is never a half integer for odd m, so
+// q is exact); the low byte of the result's bits is the residue as int8.
 template <int T>
 __device__ __forceinline__ unsigned res_bits(const float (&l)[6]) {
   float s = __fmaf_rn(l[0], c_pw[T][0], kMagic);
@@ -326,20 +349,35 @@ __device__ __forceinline__ unsigned res_bits(const float (&l)[6]) {
   return __float_as_uint(__fmaf_rn(-q, c_mod[T], s));
 }
 
+// res_bits for two elements at once: packed FFMA2 / FADD2 with the weights
+// as scalar (broadcast) operands, the same roundings per lane -- half the
+// issue slots of the scalar form (the residue kernels are issue-bound)
+template <int T>
+__device__ __forceinline__ float2 res_bits2(const float2 (&l)[6]) {
+  const float2 mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
+  float2 s = __ffma2_rn(l[0], make_float2(c_pw[T][0], c_pw[T][0]), mg);
+#pragma unroll
+  for (int j = 1; j < 6; ++j) s = __ffma2_rn(l[j], make_float2(c_pw[T][j], c_pw[T][j]), s);
+  const float2 q = __fadd2_rn(__ffma2_rn(__fadd2_rn(s, nmg), make_float2(c_inv[T], c_inv[T]), mg), nmg);
+  return __ffma2_rn(q, make_float2(-c_mod[T], -c_mod[T]), s);
+}
+
 // low bytes of four words -> one word (byte u = word u's low byte)
 __device__ __forceinline__ unsigned pack4(unsigned w0, unsigned w1, unsigned w2, unsigned w3) {
   return __byte_perm(__byte_perm(w0, w1, 0x0040), __byte_perm(w2, w3, 0x0040), 0x5410);
 }
 
 template <int NMOD, int T = 0>
-__device__ __forceinline__ void residue_words(const float (&l)[4][6], const int (&l0i)[4], unsigned (&wd)[NMOD]) {
+__device__ __forceinline__ void residue_words(const float2 (&l01)[6], const float2 (&l23)[6], const int (&l0i)[4],
+                                              unsigned (&wd)[NMOD]) {
   if constexpr (T < NMOD) {
     if constexpr (T == 0) {  // m = 256: X mod 256 is the lowest limb's low byte
       wd[0] = pack4((unsigned)l0i[0], (unsigned)l0i[1], (unsigned)l0i[2], (unsigned)l0i[3]);
     } else {
-      wd[T] = pack4(res_bits<T>(l[0]), res_bits<T>(l[1]), res_bits<T>(l[2]), res_bits<T>(l[3]));
+      const float2 a = res_bits2<T>(l01), b = res_bits2<T>(l23);
+      wd[T] = pack4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(b.x), __float_as_uint(b.y));
     }
-    residue_words<NMOD, T + 1>(l, l0i, wd);
+    residue_words<NMOD, T + 1>(l01, l23, l0i, wd);
   }
 }
 
@@ -353,19 +391,31 @@ __global__ void __launch_bounds__(256) k_res_rows(const float* __restrict__ a, i
   if (k0 >= kp) return;
   const int64_t plane = rows * kp;
   for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
-    const double sc = pow2d(pa - 48 - e[i]);
-    float l[4][6];
-    int l0i[4];
+    float sa, sb;
+    scale_pair(pa, e[i], sa, sb);
+    float c[NC][4];
     const float* ar = a + i * k * NC;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      double hi = 0.0, lo = 0.0, mag = 0.0;
-      if (k0 + u < k) load_pair<NC>(ar + (k0 + u) * NC, hi, lo, mag);
-      if (!isfinite(mag)) hi = lo = 0.0;
-      limbs(hi, lo, sc, l[u], l0i[u]);
+      bool fin = k0 + u < k;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) c[q][u] = fin ? __ldg(ar + (k0 + u) * NC + q) : 0.0f;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) fin = fin && isfinite(c[q][u]);
+      if (!fin)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) c[q][u] = 0.0f;
     }
+    float2 l01[6], l23[6];
+    {
+      const float a0[2] = {c[0][0], c[0][1]}, a1[2] = {c[NC - 1][0], c[NC - 1][1]};
+      const float b0[2] = {c[0][2], c[0][3]}, b1[2] = {c[NC - 1][2], c[NC - 1][3]};
+      limbs_pair<NC>(a0, a1, sa, sb, l01);
+      limbs_pair<NC>(b0, b1, sa, sb, l23);
+    }
+    const int l0i[4] = {limb_int(l01[0].x), limb_int(l01[0].y), limb_int(l23[0].x), limb_int(l23[0].y)};
     unsigned wd[NMOD];
-    residue_words<NMOD>(l, l0i, wd);
+    residue_words<NMOD>(l01, l23, l0i, wd);
     int8_t* o = out + i * kp + k0;
 #pragma unroll
     for (int t = 0; t < NMOD; ++t) *reinterpret_cast<unsigned*>(o + t * plane) = wd[t];
@@ -389,26 +439,36 @@ __global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, i
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps x 4 k each
   const int64_t k0 = (int64_t)blockIdx.y * kSlab, j0 = (int64_t)blockIdx.x * kSlab;
   const int64_t j = j0 + tx;
-  const double sc = j < n ? pow2d(pb - 48 - e[j]) : 1.0;
-  float l[4][6];
-  int l0i[4];
-  int inexact = 0;
+  float sa = 1.0f, sb = 1.0f;
+  if (j < n) scale_pair(pb, e[j], sa, sb);
+  float c[NC][4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int kk = ty * 4 + u;
     const int64_t gk = k0 + kk;
-    double hi = 0.0, lo = 0.0, mag = 0.0;
-    if (gk < k && j < n) {
-      load_pair<NC>(b + (gk * ldb + j) * NC, hi, lo, mag);
+    bool fin = gk < k && j < n;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) tv[tx][kk * NC + c] = b[(gk * ldb + j) * NC + c];
+    for (int q = 0; q < NC; ++q) {
+      c[q][u] = fin ? b[(gk * ldb + j) * NC + q] : 0.0f;
+      tv[tx][kk * NC + q] = c[q][u];
     }
-    if (!isfinite(mag)) hi = lo = 0.0;
-    if (limbs(hi, lo, sc, l[u], l0i[u])) ++inexact;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) fin = fin && isfinite(c[q][u]);
+    if (!fin)
+#pragma unroll
+      for (int q = 0; q < NC; ++q) c[q][u] = 0.0f;
   }
+  float2 l01[6], l23[6];
+  int inexact;
+  {
+    const float a0[2] = {c[0][0], c[0][1]}, a1[2] = {c[NC - 1][0], c[NC - 1][1]};
+    const float b0[2] = {c[0][2], c[0][3]}, b1[2] = {c[NC - 1][2], c[NC - 1][3]};
+    inexact = limbs_pair<NC>(a0, a1, sa, sb, l01) + limbs_pair<NC>(b0, b1, sa, sb, l23);
+  }
+  const int l0i[4] = {limb_int(l01[0].x), limb_int(l01[0].y), limb_int(l23[0].x), limb_int(l23[0].y)};
   if (inexact && j < n) atomicAdd(cinx + j, inexact);
   unsigned wd[NMOD];
-  residue_words<NMOD>(l, l0i, wd);
+  residue_words<NMOD>(l01, l23, l0i, wd);
 #pragma unroll
   for (int t = 0; t < NMOD; ++t) dg[t][tx][ty] = wd[t];
   __syncthreads();
@@ -428,60 +488,88 @@ __global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, i
   }
 }
 
-// row exponents of A (rows x k, NC comps): warp per row, max of |c0| + |c1|
+// ulp exponent of a binary32 (subnormals: -149); a nonzero c with
+// ulp_exp(c) + s >= 0 is an integer after scaling by 2^s
+__device__ __forceinline__ int ulp_exp(float c) {
+  const int eb = (__float_as_int(c) >> 23) & 0xff;
+  return (eb > 0 ? eb : 1) - 150;
+}
+
+// row exponents of A (rows x k, NC comps): warp per row, max of |c0| + |c1|;
+// flags nf[r]: bit 0 a non-finite element, bit 1 some c0 + c1 is not one
+// binary64, bit 2 (NC = 2) some nonzero c0 is not an integer at the scale
+// 2^(p - e) (then both components may round: 1 unit per element instead of
+// 1/2 in the error bound)
 template <int NC>
-__global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int64_t rows, int64_t k,
+__global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int64_t rows, int64_t k, int p,
                                                  int* __restrict__ e, int* __restrict__ nf) {
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   double m = 0.0;
   bool bad = false, split = false;
+  int umin = 1 << 20;
   for (int64_t t = lane; t < k; t += 32) {
     double hi, lo, mag;
     load_pair<NC>(a + (r * k + t) * NC, hi, lo, mag);
     bad |= !isfinite(mag);
     split |= lo != 0.0;
     m = fmax(m, mag);
+    const float c0 = a[(r * k + t) * NC];
+    if (NC == 2 && c0 != 0.0f) umin = min(umin, ulp_exp(c0));
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  for (int off = 16; off > 0; off >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, off));
+  }
   bad = __any_sync(0xffffffffu, bad);
   split = __any_sync(0xffffffffu, split);
   if (lane == 0) {
-    e[r] = exp_above_d(m);
-    // bit 0: a non-finite element; bit 1: some c0 + c1 is not one binary64
-    nf[r] = (bad ? 1 : 0) | (split ? 2 : 0);
+    const int ex = exp_above_d(m);
+    e[r] = ex;
+    nf[r] = (bad ? 1 : 0) | (split ? 2 : 0) | (NC == 2 && umin + p - ex < 0 ? 4 : 0);
   }
 }
 
 // column maxima of B (k x n, NC comps, row stride ldb elements): slabs of 64
 // rows, atomicMax on the binary64 bit pattern (monotone for non-negative
-// values; cm starts at 0)
+// values; cm starts at 0); cu = the column's least ulp exponent of a nonzero
+// c0 (NC = 2; starts at INT_MAX)
 template <int NC>
 __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int64_t k, int64_t n, int64_t ldb,
-                                                 unsigned long long* __restrict__ cm, int* __restrict__ nf) {
+                                                 unsigned long long* __restrict__ cm, int* __restrict__ nf,
+                                                 int* __restrict__ cu) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t t0 = (int64_t)blockIdx.y * 64, t1 = t0 + 64 < k ? t0 + 64 : k;
   double m = 0.0;
   bool bad = false, split = false;
+  int umin = 1 << 20;
   for (int64_t t = t0; t < t1; ++t) {
     double hi, lo, mag;
     load_pair<NC>(b + (t * ldb + j) * NC, hi, lo, mag);
     bad |= !isfinite(mag);
     split |= lo != 0.0;
     m = fmax(m, mag);
+    const float c0 = b[(t * ldb + j) * NC];
+    if (NC == 2 && c0 != 0.0f) umin = min(umin, ulp_exp(c0));
   }
   if (m > 0.0) atomicMax(cm + j, (unsigned long long)__double_as_longlong(m));
+  if (NC == 2 && umin < (1 << 20)) atomicMin(cu + j, umin);
   // bit 0: a non-finite element; bit 1: some c0 + c1 is not one binary64
   if (bad || split) atomicOr(nf + j, (bad ? 1 : 0) | (split ? 2 : 0));
 }
 
-__global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __restrict__ cm, int64_t n,
-                                                 int* __restrict__ e) {
+// column exponents; flag bit 2 (MC B) as k_rowexp's at the scale 2^(p - e)
+__global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __restrict__ cm, int64_t n, int p,
+                                                 const int* __restrict__ cu, int* __restrict__ e,
+                                                 int* __restrict__ nf) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) e[j] = exp_above_d(__longlong_as_double((long long)cm[j]));
+  if (j >= n) return;
+  const int ex = exp_above_d(__longlong_as_double((long long)cm[j]));
+  e[j] = ex;
+  if (cu && cu[j] + p - ex < 0) nf[j] |= 4;
 }
 
 // Optional fused epilogue of an MC-MLP layer (mc_linear_op, autodiff.hpp:265-
@@ -512,6 +600,18 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
   ep.h[i * ldo + j] = hv;
   if (ep.act) ep.act[i * ldo + j] = ep.relu ? (hv > 0.0f ? hv : 0.0f) : hv;  // Tape::relu, autodiff.hpp:134
 }
+
+// fallback thresholds in units of Y = C' / 2^(L-99): 2^50 x the per-output
+// error bound.  base: A's rounding (1/2 unit per element) times |B'| plus
+// B's for an MC B; xa / xb: the extra 1/2 unit per element of a row / MC
+// column whose leading components are not integers at the scale (flag bit 2);
+// inexact: per counted inexact element of a binary32 B column
+struct Thresholds {
+  double base, xa, xb, inexact;
+  __device__ __forceinline__ double at(int rowflags, int colflags, int inx) const {
+    return base + ((rowflags & 4) ? xa : 0.0) + ((colflags & 4) ? xb : 0.0) + inexact * inx;
+  }
+};
 
 // C mod m_t (symmetric, |r| <= m_t / 2 + 1/2) of an int32 GEMM sum C (|C| <=
 // K 2^14): C = ch 2^14 + cl (cl balanced), s = ch (2^14 mod m_t) + cl is an
@@ -545,19 +645,18 @@ template <int NMOD, bool BIG>
 __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t m, int64_t n, int64_t np,
                                              const int* __restrict__ ea, const int* __restrict__ eb,
                                              const int* __restrict__ rnf, const int* __restrict__ cnf,
-                                             const int* __restrict__ cinx, double thr, double thr_inexact, int sexp,
+                                             const int* __restrict__ cinx, Thresholds th, int sexp,
                                              float* __restrict__ out, int64_t ldo, int* __restrict__ rlist,
                                              int* __restrict__ rcnt, Epilogue ep) {
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   const int64_t plane = m * np;
-  int fj[4], nfj[4];
-  double thj[4];
+  int fj[4], cfj[4], inx[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     fj[u] = j0 + u < n ? eb[j0 + u] : 0;
-    nfj[u] = j0 + u < n ? cnf[j0 + u] & 1 : 0;
-    thj[u] = thr + (cinx && j0 + u < n ? thr_inexact * cinx[j0 + u] : 0.0);
+    cfj[u] = j0 + u < n ? cnf[j0 + u] : 0;
+    inx[u] = cinx && j0 + u < n ? cinx[j0 + u] : 0;
   }
   for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
     const int64_t off = i * np + j0;
@@ -579,7 +678,7 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
         for (int j = 0; j < kSlices; ++j) T[u][j] = __fmaf_rn(r, c_crt[NMOD].w[t][j], T[u][j]);
       }
     }
-    const int ei = ea[i], fi = rnf[i] & 1;
+    const int ei = ea[i], fi = rnf[i];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u;
@@ -589,7 +688,7 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
       double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], T[u][0]);
 #pragma unroll
       for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], T[u][s]));
-      if (fi | nfj[u] || !(fabs(y) >= thj[u])) {
+      if (((fi | cfj[u]) & 1) || !(fabs(y) >= th.at(fi, cfj[u], inx[u]))) {
         rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
         continue;
       }
@@ -601,68 +700,88 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
 
 
 // k_crt on residues the tcgen05 GEMM's epilogue already reduced (int8 planes
-// rq[t][i][ldr], tc_gemm.cu): one 32-bit load per plane per thread (four
-// columns), the slice sums as packed FFMA2 over column pairs; the rest as
-// k_crt.
+// rq[t][i][ldr], tc_gemm.cu).  One row per thread-block row: thread =
+// (row i, four columns), no loop over rows, so the 17 independent 32-bit
+// plane loads of many rows are in flight per SM (the r02b capture of the
+// row-looping version was latency-bound: 0.94 eligible warps per scheduler);
+// the slice sums are packed FFMA2 over column pairs with the weights as
+// scalar operands; the two components of the four outputs leave as two
+// 16-byte stores.
 template <int NMOD>
-__global__ void __launch_bounds__(256) k_crt8(const int8_t* __restrict__ rq, int64_t m, int64_t n, int64_t ldr,
-                                              const int* __restrict__ ea, const int* __restrict__ eb,
-                                              const int* __restrict__ rnf, const int* __restrict__ cnf,
-                                              const int* __restrict__ cinx, double thr, double thr_inexact, int sexp,
-                                              float* __restrict__ out, int64_t ldo, int* __restrict__ rlist,
-                                              int* __restrict__ rcnt, Epilogue ep) {
+__global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, int64_t m, int64_t n, int64_t ldr,
+                                                 const int* __restrict__ ea, const int* __restrict__ eb,
+                                                 const int* __restrict__ rnf, const int* __restrict__ cnf,
+                                                 const int* __restrict__ cinx, Thresholds th, int sexp,
+                                                 float* __restrict__ out, int64_t ldo, int* __restrict__ rlist,
+                                                 int* __restrict__ rcnt, Epilogue ep) {
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int64_t i = blockIdx.y;
   if (j0 >= n) return;
-  const int64_t plane = m * ldr;
-  int fj[4], nfj[4];
-  double thj[4];
+  const int64_t plane = m * ldr, off = i * ldr + j0;
+  unsigned wv[NMOD];
+#pragma unroll
+  for (int t = 0; t < NMOD; ++t) wv[t] = __ldcs(reinterpret_cast<const unsigned*>(rq + t * plane + off));
+  float2 T[2][kSlices];  // [column pair][slice] = (column 2p, column 2p + 1)
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < kSlices; ++j) T[h][j] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int t = 0; t < NMOD; ++t) {
+    float r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)  // sign-extended byte u, exact int -> float through kMagic
+      r[u] = __fsub_rn(__int_as_float(((int)(wv[t] << (24 - 8 * u)) >> 24) + 0x4B400000), kMagic);
+#pragma unroll
+    for (int j = 0; j < kSlices; ++j) {
+      const float c = c_crt[NMOD].w[t][j];
+      T[0][j] = __ffma2_rn(make_float2(r[0], r[1]), make_float2(c, c), T[0][j]);
+      T[1][j] = __ffma2_rn(make_float2(r[2], r[3]), make_float2(c, c), T[1][j]);
+    }
+  }
+  const int ei = ea[i], fi = rnf[i];
+  float res[4][2];
+  bool done[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    fj[u] = j0 + u < n ? eb[j0 + u] : 0;
-    nfj[u] = j0 + u < n ? cnf[j0 + u] & 1 : 0;
-    thj[u] = thr + (cinx && j0 + u < n ? thr_inexact * cinx[j0 + u] : 0.0);
-  }
-  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
-    const int64_t off = i * ldr + j0;
-    float2 T[2][kSlices];  // [column pair][slice] = (column 2p, column 2p + 1)
+    const int64_t j = j0 + u;
+    done[u] = false;
+    res[u][0] = res[u][1] = 0.0f;
+    if (j >= n) continue;
+    float Tu[kSlices];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int sl = 0; sl < kSlices; ++sl) Tu[sl] = (u & 1) ? T[u >> 1][sl].y : T[u >> 1][sl].x;
+    const float u0 = __fmaf_rn(Tu[1], 0x1p-11f, Tu[0]);
+    const float q = __fsub_rn(__fmaf_rn(u0, c_crt[NMOD].cq, kMagic), kMagic);
+    double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], Tu[0]);
 #pragma unroll
-      for (int j = 0; j < kSlices; ++j) T[h][j] = make_float2(0.0f, 0.0f);
-#pragma unroll
-    for (int t = 0; t < NMOD; ++t) {
-      const unsigned wv = __ldcs(reinterpret_cast<const unsigned*>(rq + t * plane + off));
-      float r[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)  // sign-extended byte u, exact int -> float through kMagic
-        r[u] = __fsub_rn(__int_as_float(((int)(wv << (24 - 8 * u)) >> 24) + 0x4B400000), kMagic);
-#pragma unroll
-      for (int j = 0; j < kSlices; ++j) {
-        const float2 w2 = make_float2(c_crt[NMOD].w[t][j], c_crt[NMOD].w[t][j]);
-        T[0][j] = __ffma2_rn(make_float2(r[0], r[1]), w2, T[0][j]);
-        T[1][j] = __ffma2_rn(make_float2(r[2], r[3]), w2, T[1][j]);
-      }
+    for (int sl = 1; sl < kSlices; ++sl) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[sl], Tu[sl]));
+    const int fc = cnf[j];
+    if (((fi | fc) & 1) || !(fabs(y) >= th.at(fi, fc, cinx ? cinx[j] : 0))) {
+      rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
+      done[u] = true;  // the fallback writes it
+      continue;
     }
-    const int ei = ea[i], fi = rnf[i] & 1;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t j = j0 + u;
-      if (j >= n) break;
-      float Tu[kSlices];
-#pragma unroll
-      for (int s = 0; s < kSlices; ++s) Tu[s] = (u & 1) ? T[u >> 1][s].y : T[u >> 1][s].x;
-      const float u0 = __fmaf_rn(Tu[1], 0x1p-11f, Tu[0]);
-      const float q = __fsub_rn(__fmaf_rn(u0, c_crt[NMOD].cq, kMagic), kMagic);
-      double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], Tu[0]);
-#pragma unroll
-      for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], Tu[s]));
-      if (fi | nfj[u] || !(fabs(y) >= thj[u])) {
-        rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
-        continue;
-      }
-      const double v[2] = {__dmul_rn(y, pow2d(sexp + ei + fj[u])), 0.0};
+    const double v[2] = {__dmul_rn(y, pow2d(sexp + ei + eb[j])), 0.0};
+    if (ep.bias) {
       emit(v, i, j, out, ldo, ep);
+      done[u] = true;
+    } else {
+      split_out<float, 2, 2>(v, res[u]);
     }
+  }
+  if (ep.bias) return;
+  float* o = out + (i * ldo + j0) * 2;
+  if (j0 + 3 < n && !(done[0] | done[1] | done[2] | done[3]) && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+    reinterpret_cast<float4*>(o)[0] = make_float4(res[0][0], res[0][1], res[1][0], res[1][1]);
+    reinterpret_cast<float4*>(o)[1] = make_float4(res[2][0], res[2][1], res[3][0], res[3][1]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u < n && !done[u]) {
+        o[2 * u] = res[u][0];
+        o[2 * u + 1] = res[u][1];
+      }
   }
 }
 
@@ -921,6 +1040,7 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
 }
 
 
+
 // ---- cuBLASLt int8 GEMMs ------------------------------------------------------------------
 
 // matmul descriptor, layouts and heuristic algorithm of one (shape, batch)
@@ -1073,7 +1193,7 @@ struct PreparedB {
 
 std::size_t b_bytes(int64_t k, int64_t n, int ncb) {
   const CrtPlan pl = crt_plan(k, ncb);
-  return al(pl.n * pad16(n) * pad32(k)) + al(n * k * ncb * 4) + al(n * 4) * 3 + al(n * 8);
+  return al(pl.n * pad16(n) * pad32(k)) + al(n * k * ncb * 4) + al(n * 4) * 4 + al(n * 8);
 }
 
 #define OZ_NMOD_SWITCH(N, ...)                         \
@@ -1108,13 +1228,15 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   int* cinx = reinterpret_cast<int*>(buf);
   buf += al(n * 4);
   unsigned long long* cm = reinterpret_cast<unsigned long long*>(buf);
+  buf += al(n * 8);
+  int* cu = reinterpret_cast<int*>(buf);
   if (cudaMemsetAsync(cnf, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cm, 0, n * 8, s) != cudaSuccess ||
-      cudaMemsetAsync(cinx, 0, n * 4, s) != cudaSuccess)
+      cudaMemsetAsync(cinx, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cu, 0x7f, n * 4, s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the column maxima");
   const dim3 gm((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
-  if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
-  else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf);
-  k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, eb);
+  if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu);
+  else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu);
+  k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, pl.pb, ncb == 2 ? cu : nullptr, eb, cnf);
   const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
   OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
                  else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
@@ -1163,8 +1285,8 @@ mcf_status a_residues(const float* x, int nca, int64_t m, int64_t k, const CrtPl
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counters");
   const int64_t kp = pad32(k);
   const unsigned gr = (unsigned)((m + 7) / 8);
-  if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, w.ea, w.rnf);
-  else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, w.ea, w.rnf);
+  if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
+  else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
   const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
   const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
   OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
@@ -1219,24 +1341,29 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   // product, and the CRT slices' tail (<= 2^12 units of 2^(L - 99)).  The
   // fallback threshold is 2^50 times it, in units of Y = C' / 2^(L-99).
   const int L = host_crt().tab[pl.n].L;
-  const double per = 0.51 * std::ldexp(1.0, pl.pb - 1) + (pb.ncb == 2 ? 0.51 * std::ldexp(1.0, pl.pa - 1) : 0.0) + 0.27;
-  const double e_y = (double)k * per * std::ldexp(1.0, 99 - L) + 4096.0;
-  const double thr = std::ldexp(e_y * 1.0001, 50);
-  const double thr_inexact = std::ldexp(0.51 * std::ldexp(1.0, pl.pa - 1) * std::ldexp(1.0, 99 - L) * 1.0001, 50);
+  const double yu = std::ldexp(1.0, 99 - L) * 1.0001 * std::ldexp(1.0, 50);  // C' units -> Y units, x 2^50
+  Thresholds th;
+  const double ta = 0.51 * std::ldexp(1.0, pl.pb - 1), tb = 0.51 * std::ldexp(1.0, pl.pa - 1);
+  th.base = ((double)k * (ta + (pb.ncb == 2 ? tb : 0.0) + 1.1) * std::ldexp(1.0, 99 - L) + 4096.0) * 1.0001 *
+            std::ldexp(1.0, 50);
+  th.xa = (double)k * ta * yu;
+  th.xb = pb.ncb == 2 ? (double)k * tb * yu : 0.0;
+  th.inexact = tb * yu;
   const int sexp = L - 99 - pl.pa - pl.pb;
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
   const bool big = k > 16384;
   if (!use_lt) {
-    OZ_NMOD_SWITCH(pl.n, k_crt8<NM><<<gc, 256, 0, s>>>(reinterpret_cast<const int8_t*>(w.cq), m, n, np, w.ea, pb.eb,
-                                                       w.rnf, pb.cnf, pb.cinx, thr, thr_inexact, sexp, out, ldo,
+    const dim3 gc8((unsigned)((n + 1023) / 1024), (unsigned)m);
+    OZ_NMOD_SWITCH(pl.n, k_crt8<NM><<<gc8, 256, 0, s>>>(reinterpret_cast<const int8_t*>(w.cq), m, n, np, w.ea, pb.eb,
+                                                       w.rnf, pb.cnf, pb.cinx, th, sexp, out, ldo,
                                                        w.rlist, w.rcnt, ep));
   } else
   OZ_NMOD_SWITCH(pl.n,
-                 if (big) k_crt<NM, true><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, thr,
-                                                             thr_inexact, sexp, out, ldo, w.rlist, w.rcnt, ep);
-                 else k_crt<NM, false><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, thr,
-                                                          thr_inexact, sexp, out, ldo, w.rlist, w.rcnt, ep));
+                 if (big) k_crt<NM, true><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, th,
+                                                             sexp, out, ldo, w.rlist, w.rcnt, ep);
+                 else k_crt<NM, false><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, th,
+                                                          sexp, out, ldo, w.rlist, w.rcnt, ep));
   mcfr::note_launch();
   if (nca == 2 && pb.ncb == 2) st = launch_fallback<2, 2>(x, pb.bt, m, n, k, w.rlist, w.rcnt, w.rnf, pb.cnf, out, ldo, ep, s);
   else if (nca == 2) st = launch_fallback<2, 1>(x, pb.bt, m, n, k, w.rlist, w.rcnt, w.rnf, pb.cnf, out, ldo, ep, s);

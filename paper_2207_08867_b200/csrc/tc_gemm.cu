@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "mcf_runtime.h"
@@ -285,6 +286,207 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- CTA-pair variant (cta_group::2): one 256 x 256 tile per pair of SMs ----
+//
+// The two CTAs of a cluster share each MMA: CTA r stages rows r*128.. of the
+// tile's A and rows r*128.. of its B (N) half, so per SM the stage is 32 KB
+// (six stages) and the tensor core reads half of B from the peer.  The
+// leader (rank 0) issues tcgen05.mma.cta_group::2 (M 256, N 256); both CTAs'
+// TMA loads complete on the leader's full barrier (peer bit cleared), the
+// leader's commits multicast to both CTAs' empty / accumulator-full
+// barriers, and both CTAs' epilogue warps release the accumulator on the
+// leader's barrier (8 arrivals).  Each CTA's TMEM holds its own 128 rows.
+constexpr int kStages2 = 6;
+constexpr int kHalfBytes = 128 * BK;  // 16 KB: 128 rows x 128 bytes
+constexpr int kStage2 = 2 * kHalfBytes;
+constexpr uint32_t kIdesc2 =
+    (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void umma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc2), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_tc_gemm_s8_pair(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + kStages2 * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2);
+  uint64_t* empty = full + kStages2;
+  uint64_t* tfull = empty + kStages2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);  // four epilogue warps in each CTA of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int tiles_m2 = (p.m + 255) / 256;
+  const int per_b = tiles_m2 * p.tiles_n;
+  const int total = per_b * p.batch;
+  const int kblocks = (p.kp + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < total; tile += npairs) {
+        const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (leader) mbar_expect_tx(full + stage, 2 * kStage2);
+          tma_load_3d_pair(sa + stage * kHalfBytes, &ta, kb * BK, mb * 256 + (int)rank * 128, b, full + stage);
+          tma_load_3d_pair(sb + stage * kHalfBytes, &tb, kb * BK, nb * 256 + (int)rank * 128, b, full + stage);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int tile = pair; tile < total; tile += npairs) {
+        mbar_wait(tempty + acc, aphase ^ 1);
+        fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * kHalfBytes), b0 = smem_u32(sb + stage * kHalfBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            umma_i8_pair(d, smem_desc(a0 + kk * 32), smem_desc(b0 + kk * 32), (kb | kk) != 0);
+          umma_commit_pair(empty + stage);
+          if (++stage == kStages2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(tfull + acc);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row_in_tile = (int)rank * 128 + q * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = pair; tile < total; tile += npairs) {
+      const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+      mbar_wait(tfull + acc, aphase);
+      fence_after();
+      const int row = mb * 256 + row_in_tile;
+      const bool row_ok = row < p.m;
+      const float fm = p.mod[b < kMaxBatch ? b : 0], fi = p.inv[b < kMaxBatch ? b : 0],
+                  fc = p.c14[b < kMaxBatch ? b : 0];
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int col = nb * BN + c * 32;
+        if (!row_ok || col >= p.n) continue;
+        if (p.mode == 0) {
+          int* o = static_cast<int*>(p.out) + ((int64_t)b * p.m + row) * p.ldo + col;
+#pragma unroll
+          for (int u = 0; u < 32; u += 4)
+            if (col + u < p.n) *reinterpret_cast<int4*>(o + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+        } else {
+          uint32_t w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t r0 = mod_bits((int)v[4 * u], fm, fi, fc, p.big),
+                           r1 = mod_bits((int)v[4 * u + 1], fm, fi, fc, p.big),
+                           r2 = mod_bits((int)v[4 * u + 2], fm, fi, fc, p.big),
+                           r3 = mod_bits((int)v[4 * u + 3], fm, fi, fc, p.big);
+            w[u] = __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+          }
+          int8_t* o = static_cast<int8_t*>(p.out) + ((int64_t)b * p.m + row) * p.ldo + col;
+          *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (col + 16 < p.n) *reinterpret_cast<uint4*>(o + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(tempty + acc);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -356,13 +558,33 @@ mcf_status tc_gemm_s8(const int8_t* a, const int8_t* b, void* out, int64_t m, in
       p.inv[i] = 1.0f / (float)mm;
       p.c14[i] = (float)p14;
     }
-  const int smem = kStages * kStageBytes + 1024 + 256;
-  per_device_once(kOnceTcGemm, [&] {
-    cudaFuncSetAttribute(k_tc_gemm_s8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
-  const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * batch;
-  const int grid = (int)std::min<int64_t>(tiles, sm_count());
-  k_tc_gemm_s8<<<grid, kThreads, smem, s>>>(ta, tb, p);
+  // MCF_TC_PAIR=0 selects the single-CTA kernel (A/B measurement)
+  static const bool pair = [] {
+    const char* e = getenv("MCF_TC_PAIR");
+    return !(e && atoi(e) == 0);
+  }();
+  if (pair) {
+    CUtensorMap tb2;
+    if (!make_map(&tb2, b, b_rows, kp, batch, 128)) return MCF_ERR_UNSUPPORTED;
+    const int smem = kStages2 * kStage2 + 1024 + 256;
+    per_device_once(kOnceTcGemm, [&] {
+      cudaFuncSetAttribute(k_tc_gemm_s8_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    const int64_t tiles = (int64_t)((m + 255) / 256) * p.tiles_n * batch;
+    const int grid = 2 * (int)std::min<int64_t>(tiles, sm_count() / 2);
+    // a.k.a. TMA box of 128 rows for both operands (each CTA loads half the tile)
+    CUtensorMap ta2;
+    if (!make_map(&ta2, a, m, kp, batch, 128)) return MCF_ERR_UNSUPPORTED;
+    k_tc_gemm_s8_pair<<<grid, kThreads, smem, s>>>(ta2, tb2, p);
+  } else {
+    const int smem = kStages * kStageBytes + 1024 + 256;
+    per_device_once(kOnceTcGemm + 8, [&] {
+      cudaFuncSetAttribute(k_tc_gemm_s8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n * batch;
+    const int grid = (int)std::min<int64_t>(tiles, sm_count());
+    k_tc_gemm_s8<<<grid, kThreads, smem, s>>>(ta, tb, p);
+  }
   note_launch();
   return check_launch("tcgen05 int8 GEMM");
 }

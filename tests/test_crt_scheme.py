@@ -145,54 +145,51 @@ def test_reconstruction_recovers_the_integer(n):
         assert err <= 2 ** (L - 99 + 12) + abs(Fraction(v)) * 2 ** -50, (v, float(err))
 
 
-def emulate_limbs(hi, lo, sc):
-    """mm_ozaki.cu limbs(): binary64 steps, then six balanced 12-bit limbs."""
-    def dsum(a, b):
-        s = a + b
-        bv = s - a
-        av = s - bv
-        return s, (a - av) + (b - bv)
-    h, hl = hi * sc, lo * sc
-    H = np.rint(h)
-    r1, r1l = dsum(h - H, hl)
-    m_, ml = r1 * 2.0 ** 24, r1l * 2.0 ** 24
-    Mv = np.rint(m_)
-    r2, r2l = dsum(m_ - Mv, ml)
-    l24 = r2 * 2.0 ** 24
-    Lv = np.rint(l24)
-    X = int(H) * 2 ** 48 + int(Mv) * 2 ** 24 + int(Lv)
-    limbs = []
-    for v in (int(Lv), int(Mv), int(H)):
-        lo12 = ((v + 2048) & 4095) - 2048
-        limbs += [lo12, (v - lo12) >> 12]
-    return X, limbs, (l24 != Lv) or (r2l != 0.0)
+def emulate_limbs2(x, s):
+    """mm_ozaki.cu limbs2() for one binary32 value: scale by 2^s as two exact
+    binary32 products, then six magic-constant roundings from the top (the
+    FFMA's single rounding replayed exactly with Fractions)."""
+    s1 = min(s, 127)
+    r = np.float32(np.float32(x) * np.float32(2.0 ** s1))
+    r = np.float32(r * np.float32(2.0 ** (s - s1)))
+    xs = r
+    limbs = [0] * 6
+    for j in range(5, -1, -1):
+        t = round(Fraction(float(r)) / 2 ** (12 * j))  # RN-even of the exact quotient (magic rounding)
+        rem = Fraction(float(r)) - t * 2 ** (12 * j)
+        assert rem == Fraction(float(np.float32(float(rem))))  # the remainder is exact in binary32
+        r = np.float32(float(rem))
+        limbs[j] = t
+    return limbs, r, xs
 
 
 def test_operand_residues_are_exact():
-    """A' = round(A 2^pa) from the pair (c0 + c1) 2^-e; residues of the limb sums
-    reduced by one rounded quotient equal the exact symmetric residues."""
+    """A' = round(c0 2^s) + round(c1 2^s) cut into six balanced 12-bit limbs
+    per component by binary32 magic-constant rounding; the limb sums' residues,
+    reduced by one rounded quotient, equal the exact symmetric residues; the
+    error is <= 1/2 per rounded component."""
     rng = np.random.default_rng(5)
     mods, *_ = table(22)
-    for p, e in ((72, 1), (73, -3), (48, 0), (67, 5)):
-        v = rng.uniform(-1, 1, 3000) * np.exp2(rng.uniform(-40, 0, 3000)) * 2.0 ** (e - 1)
+    for p, e in ((72, 1), (73, -3), (48, 0), (67, 5), (72, -140), (48, 100)):
+        v = rng.uniform(-1, 1, 1500) * np.exp2(rng.uniform(-60, 0, 1500)) * 2.0 ** (e - 1)
         c0 = v.astype(np.float32)
         c1 = (v - c0.astype(np.float64)).astype(np.float32)
-        sc = 2.0 ** (p - 48 - e)
         for a, b in zip(c0, c1):
-            hi = np.float64(a) + np.float64(b)
-            lo = (np.float64(a) - (hi - (hi - np.float64(a)))) + (np.float64(b) - (hi - np.float64(a)))
-            X, limbs, _ = emulate_limbs(hi, lo, sc)
+            la, ra, _ = emulate_limbs2(a, p - e)
+            lb, rb, _ = emulate_limbs2(b, p - e)
+            limbs = [x + y for x, y in zip(la, lb)]
+            X = sum(l * 2 ** (12 * j) for j, l in enumerate(limbs))
             exact = (Fraction(float(a)) + Fraction(float(b))) * Fraction(2) ** (p - e)
-            assert abs(X - exact) <= Fraction(51, 100)
-            assert abs(limbs[5]) <= 2 ** 12 + 1 and all(abs(l) <= 2 ** 11 + 1 for l in limbs[:5])
-            assert sum(l * 2 ** (12 * j) for j, l in enumerate(limbs)) == X
+            assert abs(X - exact) <= Fraction(1) and abs(X - exact) == abs(Fraction(float(ra)) + Fraction(float(rb)))
+            assert abs(limbs[5]) <= 2 ** 13 and all(abs(l) <= 2 ** 12 for l in limbs[:5])
             for m in mods[1:]:
                 cw = [np.float32(sym(2 ** (12 * j), m)) for j in range(6)]
-                s = np.float64(MAGIC)
+                sacc = Fraction(0)
                 for l, c in zip(limbs, cw):
-                    s = np.float64(np.float32(s + np.float64(l) * np.float64(c)))  # exact sums
-                sv = np.float32(s) - MAGIC
-                q = np.float32(np.float64(sv) * np.float64(np.float32(1.0) / np.float32(m)) + np.float64(MAGIC)) - MAGIC
-                r = int(np.float64(sv) - np.float64(q) * m)
+                    sacc += l * int(c)
+                assert abs(sacc) < 2 ** 22  # exact binary32 sums, s + kMagic exact
+                inv = np.float32(1.0) / np.float32(m)
+                q = round(sacc * Fraction(float(inv)))  # FFMA(s, RN(1/m), kMagic): one rounding to an integer
+                r = int(sacc - q * m)
                 assert r == sym(X, m), (m, X)
             assert (limbs[0] & 0xFF) == X % 256

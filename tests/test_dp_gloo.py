@@ -73,12 +73,69 @@ def test_gradient_allreduce_and_identical_updates(tmp_path):
     assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
 
 
-@pytest.mark.parametrize("m,world", [(4096, 1), (4096, 2), (4096, 8), (10, 8), (1023, 4)])
+@pytest.mark.parametrize("m,world", [(4096, 1), (4096, 2), (4096, 8), (10, 8), (1023, 4), (3, 8)])
 def test_row_shards_tile_the_output(m, world):
-    rows = []
-    for r in range(world):
-        r0, r1 = r * m // world, (r + 1) * m // world
-        rows.append((r0, r1))
+    from paper_2207_08867_b200.dist import row_range
+
+    rows = [row_range(m, r, world) for r in range(world)]
     assert rows[0][0] == 0 and rows[-1][1] == m
     for (a0, a1), (b0, b1) in zip(rows, rows[1:]):
         assert a1 == b0 and a0 <= a1
+    sizes = [b - a for a, b in rows]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _mm_worker(rank, world, port, outdir, mcmc):
+    """Config 4's layout on CPU: rank 0 owns B and broadcasts it once; every
+    rank computes its output row block (the oracle stands in for the GPU
+    product); the gathered rows must equal the single-process product bitwise,
+    and the reported time is the max over ranks."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    from paper_2207_08867_b200 import dist as pdist
+
+    port_ = oracle.Oracle("port")
+    m, k, n = 13, 40, 7
+    rng = np.random.default_rng(9)  # A is generated identically everywhere (each rank keeps its rows)
+    from mcgen import split
+
+    a = split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    if rank == 0:
+        bv = split(np.random.default_rng(10).uniform(-1, 1, k * n), 2, np.float32).reshape(k, n, 2)
+        b = torch.from_numpy(bv if mcmc else np.ascontiguousarray(bv[..., 0]))
+    else:
+        b = torch.zeros((k, n, 2) if mcmc else (k, n), dtype=torch.float32)
+    pdist.broadcast_(b, src=0)
+    r0, r1 = pdist.row_range(m, rank, world)
+    bn = b.numpy()
+    if mcmc:
+        rows_idx = np.repeat(np.arange(r0, r1), n)
+        cols_idx = np.tile(np.arange(n), r1 - r0)
+        local = port_.mm_mcmc_sampled(a, bn, rows_idx, cols_idx).reshape(r1 - r0, n, 2)
+    else:
+        local = port_.mm_mcn(np.ascontiguousarray(a[r0:r1]), bn)
+    full = pdist.gather_rows(torch.from_numpy(np.ascontiguousarray(local)), m)
+    t = pdist.max_over_ranks(float(rank + 1))
+    if rank == 0:
+        if mcmc:
+            ri, ci = np.repeat(np.arange(m), n), np.tile(np.arange(n), m)
+            want = port_.mm_mcmc_sampled(a, bn, ri, ci).reshape(m, n, 2)
+        else:
+            want = port_.mm_mcn(a, bn)
+        np.save(os.path.join(outdir, "full.npy"), full.numpy())
+        np.save(os.path.join(outdir, "want.npy"), want)
+        np.save(os.path.join(outdir, "t.npy"), np.array([t]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,mcmc", [(2, False), (3, True)])
+def test_row_sharded_product_with_broadcast_b(tmp_path, world, mcmc):
+    mp.spawn(_mm_worker, args=(world, _free_port(), str(tmp_path), mcmc), nprocs=world, join=True)
+    full, want = np.load(tmp_path / "full.npy"), np.load(tmp_path / "want.npy")
+    assert np.array_equal(full.view(np.uint32), want.view(np.uint32))
+    assert float(np.load(tmp_path / "t.npy")[0]) == world
