@@ -50,7 +50,8 @@ typedef enum mcf_status {
   MCF_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
   MCF_ERR_UNSUPPORTED = 2,      /* mcf::unsupported_operation (linalg.hpp:30-32) */
   MCF_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
-  MCF_ERR_NO_DEVICE = 4         /* library loaded without a usable B200 */
+  MCF_ERR_NO_DEVICE = 4,        /* library loaded without a usable B200 */
+  MCF_ERR_DOMAIN = 5            /* std::domain_error in the reference (hyperbolic.hpp:222-223) */
 } mcf_status;
 
 typedef enum mcf_prec { MCF_B16 = 0, MCF_B32 = 1, MCF_B64 = 2 } mcf_prec; /* precision.hpp:209 */
@@ -180,6 +181,10 @@ mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t
  * moduli[b] (moduli are those of mcf_fast_tc_crt_table, batch <= 32). */
 mcf_status mcf_tc_gemm_s8(const void* a, const void* b, void* out, int64_t m, int64_t n, int64_t kp, int batch,
                           int64_t ldo, const int* moduli, mcf_stream stream);
+/* mc_transpose2d (linalg.hpp:301-315): out (n, m, nc) = x (m, n, nc) transposed,
+ * components kept in order (bit copy). */
+mcf_status mcf_mc_transpose2d(mcf_prec p, const void* x, int nc, int64_t m, int64_t n, void* out,
+                              mcf_stream stream);
 /* FP64-pipe instructions per multiply-add of the MCF_FAST kernel for this
  * operand kind (mcmc = 0: MC x Tensor, 1: MC x MC); 0 = no fast kernel. */
 int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc);
@@ -237,6 +242,10 @@ mcf_status mcf_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int6
  * the last place of P of the host libm result).  u, v, arg, dist: device arrays. */
 mcf_status mcf_halfspace_arg(mcf_prec p, const void* table, int nc, int64_t n, int64_t dim, const int64_t* u,
                              const int64_t* v, int64_t npairs, double* arg, double* dist, mcf_stream stream);
+/* halfspace_distance (hyperbolic.hpp:214-226), synchronous, with its domain
+ * check: a non-positive height fails with MCF_ERR_DOMAIN; arg may be null. */
+mcf_status mcf_halfspace_distance(mcf_prec p, const void* table, int nc, int64_t n, int64_t dim, const int64_t* u,
+                                  const int64_t* v, int64_t npairs, double* arg, double* dist, mcf_stream stream);
 
 /* host-buffer form of mcf_mc_softmax (mcf_h_elementwise takes "mc_relu") */
 mcf_status mcf_h_mc_softmax(mcf_prec p, const void* x, int nc, int64_t outer, int64_t n, int64_t inner,
@@ -264,6 +273,12 @@ mcf_status mcf_h_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64
                          int64_t m, int64_t k, int64_t n, int w_batched, void* out, int strategy);
 mcf_status mcf_h_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_t m, int64_t k,
                          int64_t n, void* out, int strategy);
+/* Host-buffer forms of renormalize / simple_renorm (kind 0 / 1,
+ * mc_ops.hpp:338-359), the two_sum / two_prod array forms (kind 0 / 1,
+ * eft.hpp:89-111) and mc_transpose2d (linalg.hpp:301-315); blocking. */
+mcf_status mcf_h_renorm(int kind, mcf_prec p, const void* h, int nc, void* out, int r_nc, int64_t numel);
+mcf_status mcf_h_eft(int kind, mcf_prec p, const void* a, const void* b, void* r, void* e, int64_t n);
+mcf_status mcf_h_mc_transpose2d(mcf_prec p, const void* x, int nc, int64_t m, int64_t n, void* out);
 
 /* ---- host input generation (mcf::Rng, rng.hpp:13-65) ----------------------- */
 /* n draws of Rng(seed).uniform() (53-bit, [0,1)), bitwise the reference's */

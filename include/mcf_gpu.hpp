@@ -111,6 +111,59 @@ MCTensor<P> elementwise(const char* op, const MCTensor<P>* x, const MCTensor<P>*
 
 }  // namespace detail
 
+// ---- EFT array forms (eft.hpp:89-111) ------------------------------------------
+
+// s[i] + e[i] == a[i] + b[i] exactly, s[i] = fl(a[i] + b[i]) (two_sum, eft.hpp:31-38)
+template <class P>
+void two_sum(const std::vector<double>& a, const std::vector<double>& b, std::vector<double>& s,
+             std::vector<double>& e) {
+  using S = detail::Store<P>;
+  const auto as = detail::pack<P>(a), bs = detail::pack<P>(b);
+  std::vector<typename S::T> ss(a.size()), es(a.size());
+  detail::check(mcf_h_eft(0, S::kPrec, as.data(), bs.data(), ss.data(), es.data(), (int64_t)a.size()));
+  detail::unpack<P>(ss, s);
+  detail::unpack<P>(es, e);
+}
+
+// p[i] + e[i] == a[i] b[i] exactly, p[i] = fl(a[i] b[i]) (two_prod, eft.hpp:75-86)
+template <class P>
+void two_prod(const std::vector<double>& a, const std::vector<double>& b, std::vector<double>& p,
+              std::vector<double>& e) {
+  using S = detail::Store<P>;
+  const auto as = detail::pack<P>(a), bs = detail::pack<P>(b);
+  std::vector<typename S::T> ps(a.size()), es(a.size());
+  detail::check(mcf_h_eft(1, S::kPrec, as.data(), bs.data(), ps.data(), es.data(), (int64_t)a.size()));
+  detail::unpack<P>(ps, p);
+  detail::unpack<P>(es, e);
+}
+
+// ---- renormalization (mc_ops.hpp:338-359) ---------------------------------------
+
+namespace detail {
+template <class P>
+MCTensor<P> renorm(int kind, const MCTensor<P>& h, int r_nc) {
+  using S = Store<P>;
+  mcf::detail::check_nc_limit(h.nc());
+  mcf::detail::check_nc_limit(r_nc);
+  const auto hs = pack<P>(h.raw());
+  std::vector<typename S::T> os(h.numel() * r_nc);
+  check(mcf_h_renorm(kind, S::kPrec, hs.data(), h.nc(), os.data(), r_nc, (int64_t)h.numel()));
+  MCTensor<P> out(h.shape(), r_nc);
+  unpack<P>(os, out.raw());
+  return out;
+}
+}  // namespace detail
+
+template <class P>
+MCTensor<P> renormalize(const MCTensor<P>& h, int r_nc) {  // mc_ops.hpp:338-348
+  return detail::renorm<P>(0, h, r_nc);
+}
+
+template <class P>
+MCTensor<P> simple_renorm(const MCTensor<P>& h, int r_nc) {  // mc_ops.hpp:350-359
+  return detail::renorm<P>(1, h, r_nc);
+}
+
 // ---- elementwise operators (mc_ops.hpp:338-507) -------------------------------
 
 template <class P>
@@ -277,6 +330,79 @@ MCTensor<P> bmm_mcn(const MCTensor<P>& x, const NdArray& w, const ReductionPlan&
                                 shape_str(w.shape()));
   return detail::bmm<P>(x, w, x.dim(0), x.dim(1), x.dim(2), w.dim(2), true,
                         Shape{x.dim(0), x.dim(1), w.dim(2)}, detail::strategy_of(plan));
+}
+
+template <class P>
+MCTensor<P> mm4d_mcn(const MCTensor<P>& x, const NdArray& w, const ReductionPlan& plan = {}) {
+  mcf::detail::require_rank(x.shape(), 4, "mm4d_mcn");  // linalg.hpp:218-231
+  mcf::detail::require_rank(w.shape(), 4, "mm4d_mcn");
+  if (x.dim(0) != w.dim(0) || x.dim(1) != w.dim(1) || x.dim(3) != w.dim(2))
+    throw std::invalid_argument("mm4d_mcn: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                shape_str(w.shape()));
+  return detail::bmm<P>(x, w, x.dim(0) * x.dim(1), x.dim(2), x.dim(3), w.dim(3), true,
+                        Shape{x.dim(0), x.dim(1), x.dim(2), w.dim(3)}, detail::strategy_of(plan));
+}
+
+// linalg.hpp:233-253: beta bias + alpha (x . w); the factors rounded into P
+// and applied through ScalingN, the bias broadcast over the product's leading
+// rows, the sum through add_mcn -- each step on the GPU
+template <class P>
+MCTensor<P> addmm_mcn(const MCTensor<P>& bias, const MCTensor<P>& x, const NdArray& w, double alpha = 1.0,
+                      double beta = 1.0, const ReductionPlan& plan = {}) {
+  MCTensor<P> prod = gpu::mm_mcn(x, w, plan);
+  if (alpha != 1.0) prod = gpu::scaling_n(prod, NdArray::scalar(P::round(alpha)));
+  MCTensor<P> sb = beta != 1.0 ? gpu::scaling_n(bias, NdArray::scalar(P::round(beta))) : bias;
+  if (sb.shape() == prod.shape()) return gpu::add_mcn(sb, prod);
+  mcf::detail::check_suffix_broadcast(prod.shape(), sb.shape(), "addmm_mcn");
+  MCTensor<P> expanded(prod.shape(), sb.nc());
+  const std::size_t bn = sb.numel();
+  for (std::size_t e = 0; e < prod.numel(); ++e)
+    for (int c = 0; c < sb.nc(); ++c) expanded.comps(e)[c] = sb.comps(e % bn)[c];
+  return gpu::add_mcn(expanded, prod);
+}
+
+// linalg.hpp:255-299: rank dispatch; a rank-2 w broadcasts over x's batch axes
+template <class P>
+MCTensor<P> matmul_mcn(const MCTensor<P>& x, const NdArray& w, const ReductionPlan& plan = {}) {
+  const int rx = x.rank(), rw = w.rank();
+  const auto bad = [&] {
+    return std::invalid_argument("matmul_mcn: incompatible shapes " + shape_str(x.shape()) + " vs " +
+                                 shape_str(w.shape()));
+  };
+  if (rx == 1 && rw == 1) return gpu::dot_mcn(x, w, plan);
+  if (rx == 2 && rw == 1) return gpu::mv_mcn(x, w, plan);
+  if (rx == 1 && rw == 2) {
+    if (x.dim(0) != w.dim(0)) throw bad();
+    return detail::bmm<P>(x, w, 1, 1, x.dim(0), w.dim(1), false, Shape{w.dim(1)}, detail::strategy_of(plan));
+  }
+  if (rx == 2 && rw == 2) return gpu::mm_mcn(x, w, plan);
+  if (rx == 3 && rw == 3) return gpu::bmm_mcn(x, w, plan);
+  if (rx == 3 && rw == 2) {
+    if (x.dim(2) != w.dim(0)) throw bad();
+    return detail::bmm<P>(x, w, x.dim(0), x.dim(1), x.dim(2), w.dim(1), false,
+                          Shape{x.dim(0), x.dim(1), w.dim(1)}, detail::strategy_of(plan));
+  }
+  if (rx == 4 && rw == 4) return gpu::mm4d_mcn(x, w, plan);
+  if (rx == 4 && rw == 2) {
+    if (x.dim(3) != w.dim(0)) throw bad();
+    return detail::bmm<P>(x, w, x.dim(0) * x.dim(1), x.dim(2), x.dim(3), w.dim(1), false,
+                          Shape{x.dim(0), x.dim(1), x.dim(2), w.dim(1)}, detail::strategy_of(plan));
+  }
+  throw std::invalid_argument("matmul_mcn: unsupported rank pair for shapes " + shape_str(x.shape()) + " and " +
+                              shape_str(w.shape()));
+}
+
+// linalg.hpp:301-315: component-preserving 2-D transpose
+template <class P>
+MCTensor<P> mc_transpose2d(const MCTensor<P>& x) {
+  using S = detail::Store<P>;
+  mcf::detail::require_rank(x.shape(), 2, "mc_transpose2d");
+  const auto xs = detail::pack<P>(x.raw());
+  std::vector<typename S::T> os(xs.size());
+  detail::check(mcf_h_mc_transpose2d(S::kPrec, xs.data(), x.nc(), x.dim(0), x.dim(1), os.data()));
+  MCTensor<P> out(Shape{x.dim(1), x.dim(0)}, x.nc());
+  detail::unpack<P>(os, out.raw());
+  return out;
 }
 
 // NEW: MC x MC product (SURVEY 8c recipe B by default; strategy MCF_FAST for

@@ -73,6 +73,11 @@ _SIGS = {
     "mcf_fast_tc_plan": [_i64, _int, _p, _p, _p],
     "mcf_fast_tc_crt_table": [_int, _p, _p, _p, _p, _p],
     "mcf_tc_gemm_s8": [_p, _p, _p, _i64, _i64, _i64, _int, _i64, _p, _p],
+    "mcf_mc_transpose2d": [_int, _p, _int, _i64, _i64, _p, _p],
+    "mcf_halfspace_distance": [_int, _p, _int, _i64, _i64, _p, _p, _i64, _p, _p, _p],
+    "mcf_h_renorm": [_int, _int, _p, _int, _p, _int, _i64],
+    "mcf_h_eft": [_int, _int, _p, _p, _p, _p, _i64],
+    "mcf_h_mc_transpose2d": [_int, _p, _int, _i64, _i64, _p],
     "mcf_probe_pipe_rates": [_p, _p],
     "mcf_mlp_bias_act": [_p, _int, _p, _i64, _i64, _int, _p, _p, _p],
     "mcf_mlp_cross_entropy": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
@@ -122,6 +127,8 @@ def _check(rc: int):
         raise ValueError(msg)
     if rc == 2:
         raise UnsupportedOperation(msg)
+    if rc == 5:  # std::domain_error in the reference
+        raise ValueError(msg)
     raise MCFError(f"[{rc}] {msg}")
 
 

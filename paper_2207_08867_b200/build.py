@@ -80,7 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for (_, log), s in zip(results, srcs):
             if log.strip():
                 print(f"--- {s}\n{log}", file=sys.stderr)
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lquadmath", "-lcudart", "-lcublasLt", "-lcublas",
+    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lquadmath", "-lcudart", "-lcublasLt",
                                                      "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

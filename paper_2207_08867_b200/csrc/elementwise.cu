@@ -642,11 +642,10 @@ mcf_status launch_fast(const Args& a) {
   if (tma_on && vmode != 2 && tiles > 0 && al16(x) && (!G::kY || al16(y)) && (!G::kV || vmode != 0 || al16(v)) &&
       al16(out) && ((int64_t)G::kTile * ONC * sizeof(ST<P>)) % 16 == 0) {
     auto kt = k_tma<OP, P, NC, ONC>;
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem) != cudaSuccess)
-        return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot reserve shared memory for the TMA ring");
-      attr = true;
+    {
+      const mcf_status ast = mcfr::ensure_smem_attr<k_tma<OP, P, NC, ONC>>(
+          G::kSmem, "mcf: cannot reserve shared memory for the TMA ring");
+      if (ast != MCF_OK) return ast;
     }
     // two rings per SM, except packed ScalingN and Grow-ExpN (measured 59 us
     // at one ring, 66 us at two): the packed ops are compiled for one ring (so

@@ -202,4 +202,76 @@ mcf_status mcf_h_mm_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64
   return cuda_ok(cudaStreamSynchronize(s), "sync");
 }
 
+
+// ---- host-buffer forms of the remaining drop-in entry points -------------------
+// (copy in, one device call on the library's stream, copy out; blocking)
+
+namespace {
+struct Staged {
+  char* base = nullptr;
+  std::size_t off = 0;
+  char* take(std::size_t b) {
+    char* p = base + off;
+    off += (b + 255) & ~std::size_t(255);
+    return p;
+  }
+};
+mcf_status stage(std::size_t total, Staged& st) {
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    return mcfr::fail(MCF_ERR_NO_DEVICE, "mcf: no CUDA device");
+  st.base = static_cast<char*>(mcfr::workspace(total + 4096, 0));
+  if (!st.base) return mcfr::fail(MCF_ERR_CUDA, "mcf: cannot allocate device workspace");
+  return MCF_OK;
+}
+}  // namespace
+
+mcf_status mcf_h_renorm(int kind, mcf_prec p, const void* h, int nc, void* out, int r_nc, int64_t numel) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "renormalize: unknown precision");
+  if (numel < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "renormalize: negative element count");
+  const std::size_t es = mcfr::elem_bytes(p), bi = numel * nc * es, bo = numel * (r_nc > 0 ? r_nc : 0) * es;
+  Staged st;
+  TRY(stage(bi + bo + 512, st));
+  cudaStream_t s = mcfr::side_stream(0);
+  char *dh = st.take(bi), *dout = st.take(bo);
+  if (bi) TRY(cuda_ok(cudaMemcpyAsync(dh, h, bi, cudaMemcpyHostToDevice, s), "H2D h"));
+  TRY(kind == 0 ? mcf_renormalize(p, dh, nc, dout, r_nc, numel, s) : mcf_simple_renorm(p, dh, nc, dout, r_nc, numel, s));
+  if (bo) TRY(cuda_ok(cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, s), "D2H out"));
+  return cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
+mcf_status mcf_h_eft(int kind, mcf_prec p, const void* a, const void* b, void* r, void* e, int64_t n) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "two_sum: unknown precision");
+  if (n < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "two_sum: negative element count");
+  const std::size_t bytes = n * mcfr::elem_bytes(p);
+  Staged st;
+  TRY(stage(4 * bytes + 1024, st));
+  cudaStream_t s = mcfr::side_stream(0);
+  char *da = st.take(bytes), *db = st.take(bytes), *dr = st.take(bytes), *de = st.take(bytes);
+  if (bytes) {
+    TRY(cuda_ok(cudaMemcpyAsync(da, a, bytes, cudaMemcpyHostToDevice, s), "H2D a"));
+    TRY(cuda_ok(cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, s), "H2D b"));
+  }
+  TRY(kind == 0 ? mcf_two_sum(p, da, db, dr, de, n, s) : mcf_two_prod(p, da, db, dr, de, n, s));
+  if (bytes) {
+    TRY(cuda_ok(cudaMemcpyAsync(r, dr, bytes, cudaMemcpyDeviceToHost, s), "D2H"));
+    TRY(cuda_ok(cudaMemcpyAsync(e, de, bytes, cudaMemcpyDeviceToHost, s), "D2H"));
+  }
+  return cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
+mcf_status mcf_h_mc_transpose2d(mcf_prec p, const void* x, int nc, int64_t m, int64_t n, void* out) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mc_transpose2d: unknown precision");
+  if (m < 0 || n < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mc_transpose2d: negative dimension");
+  const std::size_t bytes = m * n * nc * mcfr::elem_bytes(p);
+  Staged st;
+  TRY(stage(2 * bytes + 512, st));
+  cudaStream_t s = mcfr::side_stream(0);
+  char *dx = st.take(bytes), *dout = st.take(bytes);
+  if (bytes) TRY(cuda_ok(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s), "H2D x"));
+  TRY(mcf_mc_transpose2d(p, dx, nc, m, n, dout, s));
+  if (bytes) TRY(cuda_ok(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s), "D2H out"));
+  return cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
 }  // extern "C"

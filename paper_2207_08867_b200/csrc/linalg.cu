@@ -434,6 +434,40 @@ mcf_status check_lin(mcf_prec p, int nc, const char* op) {
 }
 }  // namespace
 
+namespace {
+// component-preserving transpose (linalg.hpp:301-315): out[j, i, :] = x[i, j, :],
+// elements of W 32-bit words moved as a 32 x 32 tile through shared memory
+template <int W>
+__global__ void __launch_bounds__(256) k_mc_transpose(const uint32_t* __restrict__ x, int64_t m, int64_t n,
+                                                      uint32_t* __restrict__ out) {
+  __shared__ uint32_t t[32][32 * W + 1];
+  const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+  for (int r = threadIdx.x >> 5; r < 32; r += 8) {
+    const int64_t i = i0 + r;
+    for (int c = threadIdx.x & 31; c < 32 * W; c += 32) {
+      const int64_t j = j0 + c / W;
+      if (i < m && j < n) t[r][c] = x[(i * n + j) * W + c % W];
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x >> 5; r < 32; r += 8) {
+    const int64_t j = j0 + r;
+    for (int c = threadIdx.x & 31; c < 32 * W; c += 32) {
+      const int64_t i = i0 + c / W;
+      if (i < m && j < n) out[(j * m + i) * W + c % W] = t[c / W][r * W + c % W];
+    }
+  }
+}
+// binary16 components of odd count: 16-bit words
+__global__ void __launch_bounds__(256) k_mc_transpose16(const uint16_t* __restrict__ x, int64_t m, int64_t n, int w,
+                                                        uint16_t* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e / n, j = e - i * n;
+  for (int c = 0; c < w; ++c) out[(j * m + i) * w + c] = x[e * w + c];
+}
+}  // namespace
+
 extern "C" {
 
 mcf_status mcf_bmm_mcn(mcf_prec p, const void* x, int nc, const void* w, int64_t batch, int64_t m,
@@ -513,6 +547,33 @@ mcf_status mcf_dot_mcmc(mcf_prec p, const void* x, const void* y, int nc, int64_
 }
 
 int mcf_fast_ops_per_mad(int mcmc, mcf_prec p, int nc) { return mcfr::mm_fast_ops_per_mad(mcmc, p, nc); }
+
+mcf_status mcf_mc_transpose2d(mcf_prec p, const void* x, int nc, int64_t m, int64_t n, void* out, mcf_stream stream) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mc_transpose2d: unknown precision");
+  if (mcfr::bad_nc(nc)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
+  if (m < 0 || n < 0) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "mc_transpose2d: negative dimension");
+  if (m * n == 0) return MCF_OK;
+  const int64_t bytes = (int64_t)nc * (int64_t)mcfr::elem_bytes(p);
+  const dim3 g((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
+  const auto* xu = static_cast<const uint32_t*>(x);
+  auto* ou = static_cast<uint32_t*>(out);
+  switch (bytes % 4 == 0 ? bytes / 4 : 0) {
+    case 1: k_mc_transpose<1><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 2: k_mc_transpose<2><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 3: k_mc_transpose<3><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 4: k_mc_transpose<4><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 6: k_mc_transpose<6><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 8: k_mc_transpose<8><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 5: k_mc_transpose<5><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    case 7: k_mc_transpose<7><<<g, 256, 0, stream>>>(xu, m, n, ou); break;
+    default:  // wide binary64 elements, or binary16 with an odd component count: 16-bit words
+      k_mc_transpose16<<<(unsigned)((m * n + 255) / 256), 256, 0, stream>>>(static_cast<const uint16_t*>(x), m, n,
+                                                                          (int)(bytes / 2),
+                                                                          static_cast<uint16_t*>(out));
+  }
+  mcfr::note_launch();
+  return mcfr::check_launch("mc_transpose2d kernel");
+}
 
 int mcf_fast_tc_digits(void) { return mcfr::ozaki_digits(); }
 

@@ -163,7 +163,8 @@ template <class P>
 __global__ void __launch_bounds__(128) k_halfspace(const ST<P>* __restrict__ table, int nc, int64_t n,
                                                    int64_t dim, const int64_t* __restrict__ us,
                                                    const int64_t* __restrict__ vs, int64_t npairs,
-                                                   double* __restrict__ arg_out, double* __restrict__ dist_out) {
+                                                   double* __restrict__ arg_out, double* __restrict__ dist_out,
+                                                   int* __restrict__ domain) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npairs) return;
   const int64_t u = us[p], v = vs[p];
@@ -198,6 +199,14 @@ __global__ void __launch_bounds__(128) k_halfspace(const ST<P>* __restrict__ tab
   lit::grow<P>(t, nc, R(1), arg);
   const double a0 = P::to_d(lit::approx<P>(arg, nc));
   arg_out[p] = a0;
+  // halfspace_distance's domain (hyperbolic.hpp:219-224): both heights, as
+  // their approx values, strictly positive; otherwise NaN and the flag
+  const double hua = P::to_d(lit::approx<P>(hu, nc)), hva = P::to_d(lit::approx<P>(hv, nc));
+  if (dist_out && !(hua > 0.0 && hva > 0.0)) {
+    dist_out[p] = __longlong_as_double(0x7ff8000000000000LL);
+    if (domain) atomicOr(domain, 1);
+    return;
+  }
   if (dist_out) {
     double a = a0 < 1.0 ? 1.0 : a0;
     if (a > max_finite<P>()) a = max_finite<P>();
@@ -214,9 +223,9 @@ __global__ void __launch_bounds__(128) k_halfspace(const ST<P>* __restrict__ tab
 
 template <class P>
 mcf_status halfspace_prec(const void* table, int nc, int64_t n, int64_t dim, const int64_t* u, const int64_t* v,
-                          int64_t npairs, double* arg, double* dist, cudaStream_t s) {
+                          int64_t npairs, double* arg, double* dist, cudaStream_t s, int* domain = nullptr) {
   k_halfspace<P><<<(unsigned)((npairs + 127) / 128), 128, 0, s>>>(static_cast<const ST<P>*>(table), nc, n, dim, u, v,
-                                                                 npairs, arg, dist);
+                                                                 npairs, arg, dist, domain);
   mcfr::note_launch();
   return mcfr::check_launch("halfspace kernel");
 }
@@ -296,6 +305,41 @@ mcf_status mcf_halfspace_arg(mcf_prec p, const void* table, int nc, int64_t n, i
     case MCF_B32: return mcfg::halfspace_prec<mcfg::PB32>(table, nc, n, dim, u, v, npairs, arg, dist, s);
     default: return mcfg::halfspace_prec<mcfg::PB64>(table, nc, n, dim, u, v, npairs, arg, dist, s);
   }
+}
+
+// halfspace_distance (hyperbolic.hpp:214-226) for pairs, synchronously, with
+// the reference's domain check: a pair whose height (last coordinate, as its
+// approx value) is not strictly positive makes the call fail with
+// MCF_ERR_DOMAIN, "halfspace_distance: nonpositive height" (std::domain_error
+// in the reference); arg (optional) as mcf_halfspace_arg.
+mcf_status mcf_halfspace_distance(mcf_prec p, const void* table, int nc, int64_t n, int64_t dim, const int64_t* u,
+                                  const int64_t* v, int64_t npairs, double* arg, double* dist, mcf_stream s) {
+  if (!mcfr::valid_prec(p)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "halfspace_distance: unknown precision");
+  if (mcfr::bad_nc(nc)) return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "MCTensor ops support 1 <= nc <= 8");
+  if (n < 0 || dim < 1 || npairs < 0 || !dist)
+    return mcfr::fail(MCF_ERR_INVALID_ARGUMENT, "halfspace_distance: table rank");
+  if (npairs == 0) return MCF_OK;
+  mcf_status st = mcfr::ensure_device_tables();
+  if (st != MCF_OK) return st;
+  // arg scratch when the caller wants only distances; the domain flag after it
+  char* ws = static_cast<char*>(mcfr::workspace((arg ? 0 : npairs * sizeof(double)) + 256, 7));
+  if (!ws) return mcfr::fail(MCF_ERR_CUDA, "halfspace_distance: cannot allocate the workspace");
+  int* flag = reinterpret_cast<int*>(ws);
+  double* a = arg ? arg : reinterpret_cast<double*>(ws + 256);
+  if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "halfspace_distance: memset");
+  switch (p) {
+    case MCF_B16: st = mcfg::halfspace_prec<mcfg::PB16>(table, nc, n, dim, u, v, npairs, a, dist, s, flag); break;
+    case MCF_B32: st = mcfg::halfspace_prec<mcfg::PB32>(table, nc, n, dim, u, v, npairs, a, dist, s, flag); break;
+    default: st = mcfg::halfspace_prec<mcfg::PB64>(table, nc, n, dim, u, v, npairs, a, dist, s, flag);
+  }
+  if (st != MCF_OK) return st;
+  int h = 0;
+  if (cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return mcfr::fail(MCF_ERR_CUDA, "halfspace_distance: sync");
+  if (h) return mcfr::fail(MCF_ERR_DOMAIN, "halfspace_distance: nonpositive height");
+  return MCF_OK;
 }
 
 }  // extern "C"

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <functional>
 #include <string>
@@ -25,6 +26,22 @@ int sm_count();
 // __constant__ tables: both are per-device state).  Tags: see kOnce* below.
 void per_device_once(int tag, const std::function<void()>& fn);
 enum : int { kOnceEwSmem = 0, kOnceMmSmem = 1, kOnceFallbackSmem = 2, kOnceCrtTables = 3, kOnceTcGemm = 4 };
+// Raise a kernel's dynamic shared-memory limit on the current device once.
+// The attribute is per device, so the flag is a per-kernel bitmask of
+// devices (atomic: concurrent host threads may both set it, which is
+// harmless; none launches before its own device's attribute is set).
+template <auto Kern>
+mcf_status ensure_smem_attr(int bytes, const char* what) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return MCF_OK;
+  if (cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return fail(MCF_ERR_CUDA, what);
+  done.fetch_or(bit, std::memory_order_release);
+  return MCF_OK;
+}
 // grid for a grid-stride kernel: enough CTAs to fill every SM `per_sm` deep,
 // never more than needed to cover `work_items` with `threads` each.
 inline int grid_for(int64_t work_items, int threads, int per_sm) {

@@ -278,11 +278,10 @@ mcf_status launch_mm(const double* A, const double* B, void* C, int64_t batch, i
                      double sigma = 0.0, const int* inexact = nullptr, int want_inexact = 0) {
   using T = Tile<Acc::kNA, Acc::kNB, BM, BN, BK, TM, TN>;
   auto kern = k_mm_fast<Acc, OST, NCO, BM, BN, BK, TM, TN, MINB>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem) != cudaSuccess)
-      return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot reserve shared memory");
-    attr = true;
+  {
+    const mcf_status ast = mcfr::ensure_smem_attr<k_mm_fast<Acc, OST, NCO, BM, BN, BK, TM, TN, MINB>>(
+        T::kSmem, "mm_fast: cannot reserve shared memory");
+    if (ast != MCF_OK) return ast;
   }
   const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)batch);
   kern<<<grid, T::kThreads, T::kSmem, s>>>(A, B, static_cast<OST*>(C), M, N, K, a_bs, b_bs, c_bs, row_e,

@@ -1022,9 +1022,9 @@ mcf_status launch_fallback(const float* x, const float* bt, int64_t m, int64_t n
   const std::size_t sm = (std::size_t)k * NCA * sizeof(float);
   constexpr std::size_t kMaxSmem = 200u << 10;
   if (sm <= kMaxSmem) {
-    // the attribute is per device (and per instantiation): set it on every
-    // call (cheap) rather than behind a process-wide flag
-    cudaFuncSetAttribute(k_fallback<NCA, NCB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+    const mcf_status ast =
+        mcfr::ensure_smem_attr<k_fallback<NCA, NCB, true>>((int)kMaxSmem, "mm_fast: cannot reserve shared memory");
+    if (ast != MCF_OK) return ast;
     // 128-thread CTAs (four per SM at 126 registers) while four rows fit in
     // shared memory: one CTA's staging overlaps another's B streaming; config
     // 2's launch 112 -> 98 us under ncu (cold; 256 and 64 threads both 111-115

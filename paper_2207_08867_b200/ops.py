@@ -16,7 +16,7 @@ __all__ = [
     "two_sum", "two_prod", "renormalize", "simple_renorm", "approx", "negate", "grow_expn",
     "scaling_n", "div_n", "add_mcn", "div_mcn", "mul_mcn", "mul_mcn_slow", "square_mcn",
     "exp_mcn", "dot_mcn", "mv_mcn", "mm_mcn", "bmm_mcn", "mm4d_mcn", "matmul_mcn", "addmm_mcn",
-    "mm_mcmc", "dot_mcmc", "mc_relu", "mc_softmax", "halfspace_distance", "from_float",
+    "mc_transpose2d", "mm_mcmc", "dot_mcmc", "mc_relu", "mc_softmax", "halfspace_distance", "from_float",
     "PREC",
 ]
 
@@ -259,8 +259,9 @@ def halfspace_distance(table, u, v, return_arg=False):
     v = torch.as_tensor(v, dtype=torch.int64, device=table.device).contiguous()
     arg = torch.empty(u.shape, dtype=torch.float64, device=table.device)
     dist = torch.empty(u.shape, dtype=torch.float64, device=table.device)
-    _check(lib().mcf_halfspace_arg(_prec(table), _ptr(table), nc, n, dim, _ptr(u), _ptr(v), u.numel(), _ptr(arg),
-                                   _ptr(dist), _stream()))
+    # synchronous, with the reference's domain check (non-positive height -> ValueError)
+    _check(lib().mcf_halfspace_distance(_prec(table), _ptr(table), nc, n, dim, _ptr(u), _ptr(v), u.numel(),
+                                        _ptr(arg), _ptr(dist), _stream()))
     return (dist, arg) if return_arg else dist
 
 
@@ -390,6 +391,17 @@ def addmm_mcn(bias, x, w, alpha=1.0, beta=1.0, plan=None):
             raise ValueError(f"addmm_mcn: operand shape {_shape_str(bs)} is not a trailing suffix of {_shape_str(ps)}")
         sb = sb.expand(ps + (sb.shape[-1],))
     return add_mcn(sb, prod)
+
+
+def mc_transpose2d(x):
+    """Component-preserving 2-D transpose  [linalg.hpp:301-315]: (m, n, nc) -> (n, m, nc)."""
+    x = _c(x)
+    if _rank(x) != 2:
+        raise ValueError(f"mc_transpose2d: expected rank 2, got {_shape_str(x.shape[:-1])}")
+    m, n, nc = x.shape
+    out = torch.empty((n, m, nc), dtype=x.dtype, device=x.device)
+    _check(lib().mcf_mc_transpose2d(_prec(x), _ptr(x), nc, m, n, _ptr(out), _stream()))
+    return out
 
 
 def mm_mcmc(x, y, plan=None):

@@ -121,6 +121,75 @@ static void run(int nc) {
     }
     std::printf("%-40s %s %s\n", tag("mm_mcn shape error message"), P::name, threw ? "ok" : "MISMATCH");
     g_fail += threw ? 0 : 1;
+    // the remaining linalg.hpp entry points, and the rank dispatcher against
+    // both the reference and the specialised GPU operators (T/test_linalg.cpp:220-257)
+    MCTensor<P> x4(Shape{2, 3, 5, 6}, nc), x3(Shape{3, 5, 6}, nc), x1(Shape{6}, nc);
+    for (auto* t : {&x4, &x3, &x1})
+      for (std::size_t e = 0; e < t->numel(); ++e)
+        detail::expansion_of_double<P>(rng.uniform(-2.0, 2.0), t->comps(e), nc);
+    const NdArray w4 = random_wp<P>(rng, Shape{2, 3, 6, 4}), w3 = random_wp<P>(rng, Shape{3, 6, 4});
+    const NdArray w2 = random_wp<P>(rng, Shape{6, 4}), w1 = random_wp<P>(rng, Shape{6});
+    same(gpu::mm4d_mcn(x4, w4), mm4d_mcn(x4, w4), tag("mm4d_mcn"));
+    same(gpu::matmul_mcn(x4, w4), mm4d_mcn(x4, w4), tag("matmul_mcn 4x4 == mm4d"));
+    same(gpu::matmul_mcn(x4, w4), gpu::mm4d_mcn(x4, w4), tag("matmul_mcn 4x4 == gpu mm4d"));
+    same(gpu::matmul_mcn(x4, w2), matmul_mcn(x4, w2), tag("matmul_mcn 4x2"));
+    same(gpu::matmul_mcn(x3, w3), bmm_mcn(x3, w3), tag("matmul_mcn 3x3 == bmm"));
+    same(gpu::matmul_mcn(x3, w2), matmul_mcn(x3, w2), tag("matmul_mcn 3x2"));
+    const MCTensor<P> x2 = mc_transpose2d(mc_transpose2d(gpu::mc_transpose2d(a)));
+    same(gpu::matmul_mcn(x1, w2), matmul_mcn(x1, w2), tag("matmul_mcn 1x2"));
+    same(gpu::matmul_mcn(x1, w1), dot_mcn(x1, w1), tag("matmul_mcn 1x1 == dot"));
+    same(gpu::matmul_mcn(a, w), gpu::mm_mcn(a, w), tag("matmul_mcn 2x2 == gpu mm"));
+    same(gpu::matmul_mcn(a, vv), mv_mcn(a, vv), tag("matmul_mcn 2x1 == mv"));
+    same(gpu::mc_transpose2d(a), mc_transpose2d(a), tag("mc_transpose2d"));
+    same(x2, mc_transpose2d(a), tag("mc_transpose2d (thrice)"));
+    threw = false;
+    try {
+      gpu::matmul_mcn(x3, NdArray(Shape{5, 2}));
+    } catch (const std::invalid_argument& e) {
+      threw = std::string(e.what()).find("(3,5,6)") != std::string::npos;
+    }
+    std::printf("%-40s %s %s\n", tag("matmul_mcn shape error message"), P::name, threw ? "ok" : "MISMATCH");
+    g_fail += threw ? 0 : 1;
+    // addmm: alpha / beta through ScalingN, bias broadcast over the rows
+    MCTensor<P> bias_full(Shape{19, 7}, nc), bias_row(Shape{7}, nc);
+    for (auto* t : {&bias_full, &bias_row})
+      for (std::size_t e = 0; e < t->numel(); ++e)
+        detail::expansion_of_double<P>(rng.uniform(-1.0, 1.0), t->comps(e), nc);
+    same(gpu::addmm_mcn(bias_full, a, w), addmm_mcn(bias_full, a, w), tag("addmm_mcn"));
+    same(gpu::addmm_mcn(bias_row, a, w, 0.75, -1.5), addmm_mcn(bias_row, a, w, 0.75, -1.5),
+         tag("addmm_mcn alpha beta broadcast"));
+    // EFT arrays and renormalization of raw expansions
+    std::vector<double> av(333), bv(333);
+    for (std::size_t i = 0; i < av.size(); ++i) {
+      av[i] = P::round(rng.uniform(-1.0, 1.0) * std::exp2(rng.uniform(-20.0, 20.0)));
+      bv[i] = P::round(rng.uniform(-1.0, 1.0) * std::exp2(rng.uniform(-20.0, 20.0)));
+    }
+    for (int k = 0; k < 2; ++k) {
+      std::vector<double> gs, ge, rs, re;
+      if (k == 0) {
+        gpu::two_sum<P>(av, bv, gs, ge);
+        two_sum<P>(av, bv, rs, re);
+      } else {
+        gpu::two_prod<P>(av, bv, gs, ge);
+        two_prod<P>(av, bv, rs, re);
+      }
+      MCTensor<P> g(Shape{av.size()}, 2), r(Shape{av.size()}, 2);
+      for (std::size_t i = 0; i < av.size(); ++i) {
+        g.comps(i)[0] = gs[i], g.comps(i)[1] = ge[i];
+        r.comps(i)[0] = rs[i], r.comps(i)[1] = re[i];
+      }
+      same(g, r, tag(k == 0 ? "two_sum (array form)" : "two_prod (array form)"));
+    }
+    MCTensor<P> raw(Shape{257}, nc + 1);  // unnormalised expansions: any order, zeros, overlaps
+    for (std::size_t e = 0; e < raw.numel(); ++e)
+      for (int c = 0; c <= nc; ++c)
+        raw.comps(e)[c] = (e + c) % 5 == 0 ? 0.0 : P::round(rng.uniform(-1.0, 1.0) * std::exp2(rng.uniform(-30.0, 2.0)));
+    for (int rn : {1, nc, nc + 1}) {
+      std::snprintf(buf, sizeof buf, "renormalize nc=%d->%d", nc + 1, rn);
+      same(gpu::renormalize(raw, rn), renormalize(raw, rn), buf);
+      std::snprintf(buf, sizeof buf, "simple_renorm nc=%d->%d", nc + 1, rn);
+      same(gpu::simple_renorm(raw, rn), simple_renorm(raw, rn), buf);
+    }
   }
 }
 

@@ -255,9 +255,16 @@ def test_fast_plan_ragged_shapes_and_fallback(gr, port):
     gerr = port.relerr_mm_mct(x, w, rows, cols, got.reshape(-1, 2))
     rerr = port.relerr_mm_mct(x, w, rows, cols, ref.reshape(-1, 2))
     _check_within_4x(gerr, rerr, "ragged mm")
-    # odd n: no fast instantiation -> reference order, bit-identical
+    # odd n: the int8 path pads the columns; same bar
     w3 = wp(rng, (130, 3), 32)
-    assert_bits(gr.run("mm_mcn", x, w3, plan=mcf.FAST), port.mm_mcn(x, w3), "fallback")
+    got3 = gr.run("mm_mcn", x, w3, plan=mcf.FAST)
+    r3, c3 = np.repeat(np.arange(77), 3), np.tile(np.arange(3), 77)
+    _check_within_4x(port.relerr_mm_mct(x, w3, r3, c3, got3.reshape(-1, 2)),
+                     port.relerr_mm_mct(x, w3, r3, c3, port.mm_mcn(x, w3).reshape(-1, 2)), "ragged mm, n = 3")
+    # no fast instantiation (binary64 components, nc = 4) -> reference order, bit-identical
+    x64 = random_mc(rng, 9 * 20, 4, np.float64, -2, 2).reshape(9, 20, 4)
+    w64 = wp(rng, (20, 5), 64)
+    assert_bits(gr.run("mm_mcn", x64, w64, plan=mcf.FAST), port.mm_mcn(x64, w64), "fallback")
 
 
 def test_host_pipelined_fast_mm_equals_device_path(gr, port):
@@ -329,3 +336,47 @@ def test_fast_mm_mcmc_fp16_int8_path_nonfinite_rows_and_columns(gr):
     bad[:, 11] = True
     assert np.all(~np.isfinite(got[bad]))
     assert np.all(np.isfinite(got[~bad]))
+
+
+@pytest.mark.parametrize("bits,nc", [(32, 2), (32, 3), (16, 2), (64, 2), (32, 1)])
+def test_mm4d_addmm_matmul_transpose_bitwise(gr, port, bits, nc):
+    """The rest of linalg.hpp's surface: mm4d_mcn (two batch axes, :218-231),
+    addmm_mcn (alpha / beta through ScalingN, bias broadcast over rows,
+    :233-253) against the reference's own composition of the oracle's
+    operators, the matmul_mcn dispatcher bitwise equal to the specialised
+    operator of every rank pair (T/test_linalg.cpp:220-257), and
+    mc_transpose2d (:301-315)."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(bits + nc)
+    x4 = random_mc(rng, 2 * 3 * 5 * 6, nc, DT[bits], -3, 3).reshape(2, 3, 5, 6, nc)
+    w4 = wp(rng, (2, 3, 6, 4), bits)
+    want4 = port.bmm_mcn(x4.reshape(6, 5, 6, nc), w4.reshape(6, 6, 4)).reshape(2, 3, 5, 4, nc)
+    assert_bits(gr.run("mm4d_mcn", x4, w4), want4, "mm4d_mcn")
+    assert_bits(gr.run("matmul_mcn", x4, w4), want4, "matmul 4/4 == mm4d")
+    w2 = wp(rng, (6, 4), bits)
+    assert_bits(gr.run("matmul_mcn", x4, w2), port.bmm_mcn(x4.reshape(6, 5, 6, nc), w2).reshape(2, 3, 5, 4, nc),
+                "matmul 4/2")
+    a = random_mc(rng, 19 * 6, nc, DT[bits], -3, 3).reshape(19, 6, nc)
+    x1 = random_mc(rng, 6, nc, DT[bits], -3, 3).reshape(6, nc)
+    w1 = wp(rng, (6,), bits)
+    assert_bits(gr.run("matmul_mcn", a, w2), gr.run("mm_mcn", a, w2), "matmul 2/2 == mm")
+    assert_bits(gr.run("matmul_mcn", a, w1), port.mv_mcn(a, w1), "matmul 2/1 == mv")
+    assert_bits(gr.run("matmul_mcn", x1, w1), port.dot_mcn(x1, w1), "matmul 1/1 == dot")
+    assert_bits(gr.run("matmul_mcn", x1, w2), port.mm_mcn(x1[None], w2)[0], "matmul 1/2 == row mm")
+    # addmm: full bias, and a row bias broadcast with alpha / beta
+    bias = random_mc(rng, 19 * 4, nc, DT[bits], -2, 2).reshape(19, 4, nc)
+    row = random_mc(rng, 4, nc, DT[bits], -2, 2).reshape(4, nc)
+    prod = port.mm_mcn(a, w2)
+    assert_bits(gr.run("addmm_mcn", bias, a, w2), port.add_mcn(bias, prod), "addmm_mcn")
+    alpha, beta = np.array([0.75], DT[bits]), np.array([-1.5], DT[bits])
+    want = port.add_mcn(np.broadcast_to(port.scaling_n(row, beta), (19, 4, nc)).copy(), port.scaling_n(prod, alpha))
+    assert_bits(gr.run("addmm_mcn", row, a, w2, alpha=0.75, beta=-1.5), want, "addmm_mcn alpha beta broadcast")
+    with pytest.raises(ValueError, match=r"\(3,5,6\)"):
+        mcf.matmul_mcn(torch.zeros((3, 5, 6, nc), dtype=torch.float32, device="cuda"),
+                       torch.zeros((5, 2), device="cuda"))
+    # transpose: component-preserving bit copy
+    t = random_mc(rng, 37 * 45, nc, DT[bits], -3, 3).reshape(37, 45, nc)
+    assert_bits(gr.run("mc_transpose2d", t), np.ascontiguousarray(t.transpose(1, 0, 2)), "mc_transpose2d")

@@ -87,3 +87,28 @@ def test_halfspace_distance(gr, port, bits, nc, dim):
     ulp = np.spacing(np.abs(dh).astype(dt)).astype(np.float64)
     assert np.all(np.abs(dg - dh) <= 4 * ulp), "distance vs host arcosh"
     assert dg[0] == 0.0 and dg[1] == 0.0  # coincident rows, same row
+
+
+@pytest.mark.parametrize("bits", [32, 16])
+def test_halfspace_distance_domain(gr, bits):
+    """halfspace_distance throws std::domain_error for a non-positive height
+    (hyperbolic.hpp:219-224): the GPU entry raises ValueError with the
+    reference's message; the argument alone (halfspace_arg) has no domain."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    dt = DT[bits]
+    rng = np.random.default_rng(bits)
+    n, dim, nc = 16, 3, 2
+    tab = random_mc(rng, n * dim, nc, dt, -2, 1).reshape(n, dim, nc)
+    tab[:, -1, 0] = np.abs(tab[:, -1, 0]) + dt(0.05)
+    mcf.halfspace_distance(torch.from_numpy(tab).cuda(), [0, 1], [2, 3])  # fine
+    for bad in (0.0, -0.25):
+        t2 = tab.copy()
+        t2[5, -1, :] = 0
+        t2[5, -1, 0] = dt(bad)
+        with pytest.raises(ValueError, match="nonpositive height"):
+            mcf.halfspace_distance(torch.from_numpy(t2).cuda(), [0, 5], [1, 2])
+        with pytest.raises(ValueError, match="nonpositive height"):
+            mcf.halfspace_distance(torch.from_numpy(t2).cuda(), [2], [5])
