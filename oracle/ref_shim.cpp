@@ -579,4 +579,35 @@ void mcfref_rng_below(std::uint64_t seed, std::uint64_t bound, std::int64_t n, s
   for (std::int64_t i = 0; i < n; ++i) out[i] = g.below(bound);
 }
 
+// checkpoint_to_json (nn.hpp:207-214) of the reference's MC-MLP (MCSequential
+// of MCLinear + ReLU, as mcfref_mlp_train builds it) holding `params`, dumped
+// as write_json_file does; returns the length or -1 if it does not fit
+std::int64_t mcfref_mlp_checkpoint(const int* dims, int nlayers, int nc, const float* params, char* buf,
+                                   std::int64_t cap) {
+  using P = mcf::B32;
+  try {
+    mcf::Rng rng(1);
+    mcf::MCSequential<P> model;
+    std::vector<mcf::MCLinear<P>*> lins;
+    for (int l = 0; l < nlayers; ++l) {
+      auto lin = std::make_unique<mcf::MCLinear<P>>(dims[l], dims[l + 1], true, nc, rng);
+      lins.push_back(lin.get());
+      model.add(std::move(lin));
+      if (l + 1 < nlayers) model.add(std::make_unique<mcf::ReLULayer<P>>());
+    }
+    const float* p = params;
+    for (auto* lin : lins) {
+      for (auto& v : lin->weight().raw()) v = *p++;
+      for (auto& v : lin->bias()->raw()) v = *p++;
+    }
+    const std::string s = mcf::checkpoint_to_json(model).dump(2);
+    if (static_cast<std::int64_t>(s.size()) >= cap) return -1;
+    std::memcpy(buf, s.data(), s.size());
+    buf[s.size()] = 0;
+    return static_cast<std::int64_t>(s.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 }  // extern "C"

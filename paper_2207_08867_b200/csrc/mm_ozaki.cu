@@ -762,12 +762,17 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
       done[u] = true;  // the fallback writes it
       continue;
     }
-    const double v[2] = {__dmul_rn(y, pow2d(sexp + ei + eb[j])), 0.0};
+    const double yv = __dmul_rn(y, pow2d(sexp + ei + eb[j]));
     if (ep.bias) {
+      const double v[2] = {yv, 0.0};
       emit(v, i, j, out, ldo, ep);
       done[u] = true;
     } else {
-      split_out<float, 2, 2>(v, res[u]);
+      // the greedy split of a binary64 (split_out of (yv, 0) without the
+      // double-double steps): c0 = RN32(yv), c1 = RN32(yv - c0), the
+      // difference exact
+      res[u][0] = __double2float_rn(yv);
+      res[u][1] = __double2float_rn(__dsub_rn(yv, (double)res[u][0]));
     }
   }
   if (ep.bias) return;

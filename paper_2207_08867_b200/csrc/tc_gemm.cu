@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // leader's commits multicast to both CTAs' empty / accumulator-full
 // barriers, and both CTAs' epilogue warps release the accumulator on the
 // leader's barrier (8 arrivals).  Each CTA's TMEM holds its own 128 rows.
-constexpr int kStages2 = 6;
+constexpr int kStages2 = 7;  // 7 x 32 KB + alignment + barriers fit the 227 KB
 constexpr int kHalfBytes = 128 * BK;  // 16 KB: 128 rows x 128 bytes
 constexpr int kStage2 = 2 * kHalfBytes;
 constexpr uint32_t kIdesc2 =

@@ -239,9 +239,66 @@ class MCMLP:
         Python number may be evaluated as a multiplication by its reciprocal)."""
         return float(np.float32(loss_sum.item()) / np.float32(n_global))
 
+    def checkpoint(self) -> dict:
+        """The model's checkpoint blob, identical to the reference's (nn.hpp:207-214)."""
+        return checkpoint_to_json(self.dims, self.params_numpy(), self.nc)
+
+    def load_checkpoint(self, ckpt: dict) -> None:
+        """Restore the MC parameters bit-exact (nn.hpp:216-229)."""
+        for l, (w, b) in enumerate(load_checkpoint(self.dims, ckpt, self.nc)):
+            self.W[l].copy_(torch.from_numpy(w))
+            self.b[l].copy_(torch.from_numpy(b))
+
     def params_numpy(self):
         torch.cuda.synchronize()
         return [(w.cpu().numpy(), b.cpu().numpy()) for w, b in zip(self.W, self.b)]
 
 
-__all__ = ["init_params", "make_batch", "GradExchange", "MCMLP", "SEQUENTIAL", "FAST"]
+def model_config(dims, nc=2):
+    """MCSequential.config() of the MC-MLP (nn.hpp:74-80, 135, 190-194):
+    MCLinear layers with ReLU between them."""
+    layers = []
+    for l in range(len(dims) - 1):
+        layers.append({"type": "mclinear", "in": int(dims[l]), "out": int(dims[l + 1]), "bias": True, "nc": int(nc)})
+        if l + 2 < len(dims):
+            layers.append({"type": "relu"})
+    return {"type": "sequential", "layers": layers}
+
+
+def checkpoint_to_json(dims, params, nc=2) -> dict:
+    """checkpoint_to_json (nn.hpp:207-214): the topology manifest plus one mct
+    blob per parameter, named as MCSequential names them ("<layer index>.weight",
+    "<layer index>.bias"; ReLU layers hold no parameters).  params: list of
+    (W (out, in, nc), b (out, nc)) arrays or tensors, binary32 components."""
+    from . import serialize
+
+    blobs = {}
+    for l, (w, b) in enumerate(params):
+        idx = 2 * l  # a ReLU follows every layer but the last
+        w = torch.as_tensor(np.asarray(w.cpu() if torch.is_tensor(w) else w))
+        b = torch.as_tensor(np.asarray(b.cpu() if torch.is_tensor(b) else b))
+        blobs[f"{idx}.weight"] = serialize.mct_to_json(w)
+        blobs[f"{idx}.bias"] = serialize.mct_to_json(b)
+    return {"format": "mcf-checkpoint", "model": model_config(dims, nc), "params": blobs}
+
+
+def load_checkpoint(dims, ckpt: dict, nc=2):
+    """load_checkpoint (nn.hpp:216-229): the reference's checks and messages,
+    then the parameters bit-exact: list of (W, b) numpy arrays."""
+    from . import serialize
+
+    if not isinstance(ckpt, dict) or ckpt.get("format", "") != "mcf-checkpoint":
+        raise ValueError("load_checkpoint: not a checkpoint blob")
+    if ckpt.get("model") != model_config(dims, nc):
+        raise ValueError("load_checkpoint: model topology mismatch")
+    out = []
+    for l in range(len(dims) - 1):
+        idx = 2 * l
+        w = serialize.mct_from_json(ckpt["params"][f"{idx}.weight"], "b32").numpy()
+        b = serialize.mct_from_json(ckpt["params"][f"{idx}.bias"], "b32").numpy()
+        out.append((w, b))
+    return out
+
+
+__all__ = ["init_params", "make_batch", "GradExchange", "MCMLP", "SEQUENTIAL", "FAST", "model_config",
+           "checkpoint_to_json", "load_checkpoint"]

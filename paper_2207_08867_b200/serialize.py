@@ -47,9 +47,35 @@ def _np_float(dtype):
     return {torch.float16: np.float16, torch.float32: np.float32, torch.float64: np.float64}[dtype]
 
 
+def dumps(j: dict, indent: int = 2) -> str:
+    """The text of the reference's Json::dump(2) as the nlohmann build it links
+    emits it (checked byte for byte in tests/test_oracle_pin.py): object keys
+    sorted, 2-space indent, ": " after keys, arrays of numbers inline as
+    "[2,3]", other arrays one element per line."""
+    def num(v):
+        return isinstance(v, (int, float)) and not isinstance(v, bool)
+
+    def go(v, lvl):
+        pad, inner = " " * (indent * lvl), " " * (indent * (lvl + 1))
+        if isinstance(v, dict):
+            if not v:
+                return "{}"
+            items = [f"{inner}{json.dumps(k)}: {go(v[k], lvl + 1)}" for k in sorted(v)]
+            return "{\n" + ",\n".join(items) + "\n" + pad + "}"
+        if isinstance(v, (list, tuple)):
+            if not v:
+                return "[]"
+            if all(num(e) for e in v):
+                return "[" + ",".join(json.dumps(e) for e in v) + "]"
+            return "[\n" + ",\n".join(inner + go(e, lvl + 1) for e in v) + "\n" + pad + "]"
+        return json.dumps(v)
+
+    return go(j, 0)
+
+
 def write_json_file(path: str, j: dict) -> None:
     with open(path, "w") as f:
-        f.write(json.dumps(j, indent=2) + "\n")
+        f.write(dumps(j) + "\n")
 
 
 def read_json_file(path: str) -> dict:

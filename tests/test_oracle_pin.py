@@ -205,3 +205,37 @@ def test_halfspace_arg_port_equals_reference(port, ref, bits, nc, dim):
     got = port.halfspace_arg(tab, u, v)
     want = ref.halfspace_arg(tab, u, v)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_mlp_checkpoint_equals_reference(ref):
+    """The MC-MLP checkpoint (nn.hpp:207-229): paper_2207_08867_b200.mlp
+    writes the reference's checkpoint_to_json text byte for byte (keys sorted,
+    dump(2)) for the same parameters, reads it back bit-exact, and raises the
+    reference's errors on a foreign blob or a topology mismatch."""
+    import ctypes as C
+    import json
+
+    from paper_2207_08867_b200 import mlp, serialize
+
+    dims = [7, 5, 3]
+    params = mlp.init_params(dims, 2, seed=44)
+    params[0][0].reshape(-1)[:2] = [-0.0, np.float32(1e-40)]  # sign of zero and a subnormal survive
+    flat = np.concatenate([np.concatenate([w.ravel(), b.ravel()]) for w, b in params]).astype(np.float32)
+    f = ref.lib.mcfref_mlp_checkpoint
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_int64]
+    f.restype = C.c_int64
+    d = np.array(dims, np.int32)
+    buf = C.create_string_buffer(1 << 20)
+    n = f(d.ctypes.data, len(dims) - 1, 2, flat.ctypes.data, buf, len(buf))
+    assert n > 0
+    want = buf.value.decode()
+    got = mlp.checkpoint_to_json(dims, params)
+    assert serialize.dumps(got) == want
+    back = mlp.load_checkpoint(dims, json.loads(want))
+    for (w, b), (w2, b2) in zip(params, back):
+        assert_bits(w2, w, "W")
+        assert_bits(b2, b, "b")
+    with pytest.raises(ValueError, match="not a checkpoint blob"):
+        mlp.load_checkpoint(dims, {"format": "mct"})
+    with pytest.raises(ValueError, match="topology mismatch"):
+        mlp.load_checkpoint([7, 6, 3], got)
