@@ -1,6 +1,6 @@
 """Quick device timing of the elementwise suite (config 0: fp32 nc=2, 2^24)."""
 import sys, os, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_2207_08867_b200 as mcf
 
