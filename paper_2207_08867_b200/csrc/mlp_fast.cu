@@ -22,6 +22,72 @@
 namespace {
 
 
+// C (m x n) = A B^T for short A (m <= 32 rows, K contiguous: the 10-class
+// layer's dW = G A_prev^T, K = the batch): a warp per (row j of B, K chunk)
+// streams B's row with 16-byte loads, A's chunk staged in shared memory; each
+// lane keeps one partial sum per row of A; the lanes are merged by a
+// butterfly and the chunks by k_splitk_reduce in chunk order (deterministic).
+constexpr int kSkChunk = 1024;
+constexpr int kSkRows = 32;
+__global__ void __launch_bounds__(256) k_gemm_abt_splitk(const float* __restrict__ a, int64_t lda,
+                                                         const float* __restrict__ b, int64_t ldb, int64_t m, int64_t n,
+                                                         int64_t k, float* __restrict__ part) {
+  extern __shared__ float4 as4[];  // [m][kSkChunk / 4]
+  const int64_t k0 = (int64_t)blockIdx.y * kSkChunk, k1 = k0 + kSkChunk < k ? k0 + kSkChunk : k;
+  for (int idx = threadIdx.x; idx < m * kSkChunk; idx += blockDim.x) {
+    const int i = idx / kSkChunk, kk = idx - i * kSkChunk;
+    reinterpret_cast<float*>(as4)[idx] = k0 + kk < k1 ? a[i * lda + k0 + kk] : 0.0f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * 8 + warp;
+  if (j >= n) return;
+  float acc[kSkRows];
+#pragma unroll
+  for (int i = 0; i < kSkRows; ++i) acc[i] = 0.0f;
+  const float* br = b + j * ldb + k0;
+  const int len = (int)(k1 - k0);
+  const bool vec = ((reinterpret_cast<uintptr_t>(br) & 15) == 0);
+  for (int kk = lane * 4; kk < len; kk += 128) {
+    float4 q;
+    if (vec && kk + 3 < len) {
+      q = __ldg(reinterpret_cast<const float4*>(br + kk));
+    } else {
+      q.x = br[kk];
+      q.y = kk + 1 < len ? br[kk + 1] : 0.0f;
+      q.z = kk + 2 < len ? br[kk + 2] : 0.0f;
+      q.w = kk + 3 < len ? br[kk + 3] : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < kSkRows; ++i) {
+      if (i >= m) break;
+      const float4 av = as4[i * (kSkChunk / 4) + kk / 4];  // 16-byte shared loads, conflict-free
+      acc[i] = __fmaf_rn(av.x, q.x, acc[i]);
+      acc[i] = __fmaf_rn(av.y, q.y, acc[i]);
+      acc[i] = __fmaf_rn(av.z, q.z, acc[i]);
+      acc[i] = __fmaf_rn(av.w, q.w, acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kSkRows; ++i) {
+    if (i >= m) break;
+    float v = acc[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) part[((int64_t)blockIdx.y * m + i) * n + j] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ part, int chunks, int64_t m,
+                                                       int64_t n, float* __restrict__ c, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e / n, j = e - i * n;
+  float v = 0.0f;
+  for (int q = 0; q < chunks; ++q) v = __fadd_rn(v, part[(int64_t)q * m * n + e]);
+  c[i * ldc + j] = v;
+}
+
 // out[r] = sum_j g[r, j]: a CTA per row, tree reduction
 __global__ void __launch_bounds__(256) k_rowsum_tree(const float* __restrict__ g, int64_t n, float* __restrict__ out) {
   __shared__ float part[8];
@@ -62,8 +128,27 @@ mcf_status mcf_gemm_f32_fast(int trans_a, int trans_b, const float* a, int64_t l
     const mcf_status st = mcfr::gemm_f32_i8(trans_a, trans_b, a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
     if (st != MCF_ERR_UNSUPPORTED) return st;
   }
-  // outside the int8 path's shapes: the ordered FFMA GEMM (same operands,
-  // same optional ReLU mask; small here: k or m is 10)
+  // short A with a long K and no mask (the 10-class layer's dW: 10 x 1024, K =
+  // the batch): split-K FFMA, chunks merged in order
+  if (!trans_a && trans_b && !relu_mask && m <= kSkRows && k >= 2 * kSkChunk) {
+    const int chunks = (int)((k + kSkChunk - 1) / kSkChunk);
+    float* part = static_cast<float*>(mcfr::workspace((std::size_t)chunks * m * n * sizeof(float) + 256, 8));
+    if (!part) return mcfr::fail(MCF_ERR_CUDA, "gemm_f32: cannot allocate the split-K workspace");
+    const int smem = (int)(m * kSkChunk * sizeof(float));
+    if (smem > (48 << 10)) {
+      const mcf_status ast = mcfr::ensure_smem_attr<k_gemm_abt_splitk>(kSkRows * kSkChunk * (int)sizeof(float),
+                                                                       "gemm_f32: cannot reserve shared memory");
+      if (ast != MCF_OK) return ast;
+    }
+    k_gemm_abt_splitk<<<dim3((unsigned)((n + 7) / 8), (unsigned)chunks), 256, smem, s>>>(a, lda, b, ldb, m, n, k,
+                                                                                       part);
+    k_splitk_reduce<<<(unsigned)((m * n + 255) / 256), 256, 0, s>>>(part, chunks, m, n, c, ldc);
+    mcfr::note_launch();
+    mcfr::note_launch();
+    return mcfr::check_launch("gemm_f32 split-K kernels");
+  }
+  // the other shapes outside the int8 path (a dimension below 64 with a short
+  // K, e.g. the 10-class layer's dA, K = 10): the ordered FFMA GEMM
   return mcf_gemm_f32_ordered(trans_a, trans_b, a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
 }
 

@@ -726,17 +726,22 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int j = 0; j < kSlices; ++j) T[h][j] = make_float2(0.0f, 0.0f);
+  const float2 off2 = make_float2(-(kMagic + 128.0f), -(kMagic + 128.0f));
 #pragma unroll
   for (int t = 0; t < NMOD; ++t) {
-    float r[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)  // sign-extended byte u, exact int -> float through kMagic
-      r[u] = __fsub_rn(__int_as_float(((int)(wv[t] << (24 - 8 * u)) >> 24) + 0x4B400000), kMagic);
+    // byte u of the word is r + 128 after flipping its top bit; one PRMT puts
+    // it under kMagic's upper bytes (the float kMagic + 128 + r), one FADD2
+    // per pair takes the offset off (exact)
+    const unsigned x = wv[t] ^ 0x80808080u;
+    const float2 r01 = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(x, 0x4B400000u, 0x7650)),
+                                              __uint_as_float(__byte_perm(x, 0x4B400000u, 0x7651))), off2);
+    const float2 r23 = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(x, 0x4B400000u, 0x7652)),
+                                              __uint_as_float(__byte_perm(x, 0x4B400000u, 0x7653))), off2);
 #pragma unroll
     for (int j = 0; j < kSlices; ++j) {
       const float c = c_crt[NMOD].w[t][j];
-      T[0][j] = __ffma2_rn(make_float2(r[0], r[1]), make_float2(c, c), T[0][j]);
-      T[1][j] = __ffma2_rn(make_float2(r[2], r[3]), make_float2(c, c), T[1][j]);
+      T[0][j] = __ffma2_rn(r01, make_float2(c, c), T[0][j]);
+      T[1][j] = __ffma2_rn(r23, make_float2(c, c), T[1][j]);
     }
   }
   const int ei = ea[i], fi = rnf[i];
