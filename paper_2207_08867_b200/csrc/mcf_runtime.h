@@ -101,6 +101,10 @@ mcf_status ozaki_host(const float* hx, const float* hw, int64_t m, int64_t k, in
 // hand-written tcgen05 int8 GEMM (tc_gemm.cu): int32 products or residues
 mcf_status tc_gemm_s8(const int8_t* a, const int8_t* b, void* out, int64_t m, int64_t n, int64_t kp, int batch,
                       int64_t ldo, const int* moduli, cudaStream_t s, int64_t b_rows = -1);
+// the diagonal GEMMs of a digit-plane scheme in one tcgen05 launch (int32 out)
+mcf_status tc_gemm_s8_seg(const int8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int* out, int64_t m, int64_t n,
+                          int64_t b_rows, int nseg, const int* ka, const int* kb, const int* kd, int64_t ldo,
+                          cudaStream_t s);
 // host-buffer MC(nc=2, binary32) x T, pipelined over row chunks (hostapi.cu)
 mcf_status mm_fast_mct_host(const float* hx, const float* hw, int64_t m, int64_t k, int64_t n, float* hout,
                             float* dx, float* dw, float* dout, cudaStream_t cin, const cudaStream_t comp[2],

@@ -19,7 +19,7 @@
 //     A' mod m_t, B' mod m_t (|r| <= 128, exact int32 sums for K < 2^17) gives
 //     C' mod m_t;
 //   * C' = sum_t r_t w_t - q M (w_t the CRT weights, q = round(T / M)) is
-//     formed exactly: the weights are cut into nine balanced 11-bit slices, so
+//     formed exactly: the weights are cut into eight balanced 12-bit slices, so
 //     every slice sum T_j = sum_t r_t w_tj and D_j = T_j - q M_j is an exact
 //     binary32 integer, and the slices are joined by a binary64 Horner pass
 //     whose partial sums are exact while they matter (|C'| <= M/4);
@@ -90,19 +90,26 @@ constexpr int kMaxMod = 22;
 constexpr int kModuli[kMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223,
                                   217, 211, 199, 197, 193, 191, 181, 179, 173, 167, 163};
 constexpr int kMinMod = 16;     // instantiated moduli counts: kMinMod .. kMaxMod
-constexpr int kSlices = 9;      // balanced 11-bit slices of the CRT weights
+constexpr int kSlices = 8;      // balanced 12-bit slices of the CRT weights
+constexpr int kSliceBits = 12;
+constexpr int kYShift = kSlices * kSliceBits;  // Y = C' / 2^(L - kYShift)
 constexpr float kMagic = 12582912.0f;  // 1.5 2^23: x + kMagic has x in its low mantissa bits (|x| < 2^22)
 
 struct CrtTab {
-  float w[kMaxMod][kSlices];  // slice j of the symmetric CRT weight w_t (weight 2^(L - 11 (j + 1)))
+  float w[kMaxMod][kSlices];  // slice j of the symmetric CRT weight w_t (weight 2^(L - 12 (j + 1)))
   float mh[kSlices];          // slices of M
-  float cq;                   // RN32(2^(L - 11) / M)
+  float cq;                   // RN32(2^(L - 12) / M)
   int L;                      // bit length of M
 };
 __constant__ float c_pw[kMaxMod][6];  // 2^(12 j) mod m_t, symmetric (limb weights of the residue sums)
 __constant__ float c_c14[kMaxMod];    // 2^14 mod m_t, symmetric
 __constant__ float c_inv[kMaxMod];    // RN32(1 / m_t)
 __constant__ float c_mod[kMaxMod];
+// digit weights of the tensor-core residue kernels: c_coef8[t][k] = 2^w_k mod
+// m_t (symmetric, int8) for the 12 byte digits of the six limbs (w = 12 j for
+// the low byte of limb j, 12 j + 8 for its high part), zero for k >= 12 and
+// for t >= kMaxMod (padding moduli of the last n-tile)
+__constant__ int8_t c_coef8[24][16];
 __constant__ CrtTab c_crt[kMaxMod + 1];  // by moduli count
 
 // ---- host: exact CRT constants (small unsigned big integers) ----
@@ -169,16 +176,16 @@ int sym(int v, int m) {  // symmetric representative of v mod m
   if (v < 0) v += m;
   return v > m / 2 ? v - m : v;
 }
-// balanced slices of x (0 <= x < 2^L) at weights 2^(L - 11 (j + 1)), the last
-// one rounded: |x - sum_j d_j 2^(L - 11 (j + 1))| <= 2^(L - 11 kSlices - 1);
-// |d_j| <= 2^10 for j >= 1, d_0 <= 2^11 (x < 2^(L-1) gives d_0 <= 2^10)
+// balanced slices of x (0 <= x < 2^L) at weights 2^(L - 12 (j + 1)), the last
+// one rounded: |x - sum_j d_j 2^(L - 12 (j + 1))| <= 2^(L - 12 kSlices - 1);
+// |d_j| <= 2^11 for j >= 1, d_0 <= 2^12 (x < 2^(L-1) gives d_0 <= 2^11)
 void slices(const Big& x, int L, float* out) {
   int d[kSlices];
-  for (int j = 0; j < kSlices; ++j) d[j] = big_bits(x, L - 11 * (j + 1), 11);
-  if (big_bit(x, L - 11 * kSlices - 1)) ++d[kSlices - 1];
+  for (int j = 0; j < kSlices; ++j) d[j] = big_bits(x, L - kSliceBits * (j + 1), kSliceBits);
+  if (big_bit(x, L - kYShift - 1)) ++d[kSlices - 1];
   for (int j = kSlices - 1; j > 0; --j)
-    if (d[j] >= 1024) {
-      d[j] -= 2048;
+    if (d[j] >= (1 << (kSliceBits - 1))) {
+      d[j] -= 1 << kSliceBits;
       ++d[j - 1];
     }
   for (int j = 0; j < kSlices; ++j) out[j] = (float)d[j];
@@ -188,6 +195,7 @@ struct HostCrt {
   CrtTab tab[kMaxMod + 1];
   double log2m[kMaxMod + 1];
   float pw[kMaxMod][6], c14[kMaxMod], inv[kMaxMod], mod[kMaxMod];
+  int8_t coef8[24][16];
 };
 const HostCrt& host_crt() {
   static const HostCrt h = [] {
@@ -204,6 +212,12 @@ const HostCrt& host_crt() {
       h.c14[t] = (float)sym(p14, m);
       h.inv[t] = 1.0f / (float)m;
       h.mod[t] = (float)m;
+      for (int kd = 0; kd < 12; ++kd) {
+        const int w = 12 * (kd / 2) + 8 * (kd % 2);
+        int pw2 = 1 % m;
+        for (int b = 0; b < w; ++b) pw2 = pw2 * 2 % m;
+        h.coef8[t][kd] = (int8_t)sym(pw2, m);  // |sym| <= 127, and 0 / 1 for m = 256
+      }
     }
     for (int n = 1; n <= kMaxMod; ++n) {
       Big M;
@@ -214,7 +228,7 @@ const HostCrt& host_crt() {
       tb.L = L;
       const double md = big_double(M);
       h.log2m[n] = std::log2(md);
-      tb.cq = (float)(std::ldexp(1.0, L - 11) / md);
+      tb.cq = (float)(std::ldexp(1.0, L - kSliceBits) / md);
       slices(M, L, tb.mh);
       for (int t = 0; t < n; ++t) {
         Big mt = M;
@@ -249,7 +263,8 @@ mcf_status upload_crt_tables() {
         cudaMemcpyToSymbol(c_c14, h.c14, sizeof(h.c14)) != cudaSuccess ||
         cudaMemcpyToSymbol(c_inv, h.inv, sizeof(h.inv)) != cudaSuccess ||
         cudaMemcpyToSymbol(c_mod, h.mod, sizeof(h.mod)) != cudaSuccess ||
-        cudaMemcpyToSymbol(c_crt, h.tab, sizeof(h.tab)) != cudaSuccess)
+        cudaMemcpyToSymbol(c_crt, h.tab, sizeof(h.tab)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_coef8, h.coef8, sizeof(h.coef8)) != cudaSuccess)
       st = mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot upload the CRT tables");
   });
   return st;
@@ -378,6 +393,216 @@ __device__ __forceinline__ void residue_words(const float2 (&l01)[6], const floa
       wd[T] = pack4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(b.x), __float_as_uint(b.y));
     }
     residue_words<NMOD, T + 1>(l01, l23, l0i, wd);
+  }
+}
+
+// ---- residues on the tensor cores (mma.sync m16n8k16 s8) ----------------------
+//
+// The residue of X = sum_j l_j 2^(12 j) modulo m_t is sum_k d_k (2^w_k mod m_t)
+// reduced once, with the limbs cut into byte digits d (low byte of l_j,
+// balanced, and its high part (l_j - lo) / 256, |.| <= 32).  The 12 x 17
+// digit-weight products of an element are an int8 matrix product: 16
+// elements x 16 digits (12 used) times 16 digits x 8 moduli per mma.sync,
+// exact in int32 (|S| <= 6 128 127 + 6 32 127 < 2^17).  What stays on the FMA
+// pipe per element is the limb cutting and one exact reduction per modulus
+// (four FP32 ops), about half the FFMA work of the limb-sum form (res_bits2).
+// Mapping (m16n8 fragments: a0 / a1 = rows g / g+8, k group tq; c0, c1 / c2,
+// c3 = rows g / g+8, columns 2 tq, 2 tq + 1; g = lane / 4, tq = lane % 4):
+// m-tile row r of tile mt holds element 4 (r & 7) + 2 mt + (r >> 3) of a
+// 32-element group, so each thread ends with four CONSECUTIVE elements
+// (4 g .. 4 g + 3) for each of its six moduli: one 32-bit store per modulus.
+
+__device__ __forceinline__ void mma_s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+
+// integer limbs of round(x 2^s) (limbs2's steps on one value): li[j] as ints
+// read off the magic-rounded floats' bits; returns true when inexact
+__device__ __forceinline__ bool limbs_int(float x, float sa, float sb, int (&li)[6]) {
+  float r = __fmul_rn(__fmul_rn(x, sa), sb);
+  const bool under = r == 0.0f && x != 0.0f;
+#pragma unroll
+  for (int j = 5; j >= 0; --j) {
+    const float tm = __fmaf_rn(r, pow2f(-12 * j), kMagic);
+    r = __fmaf_rn(__fsub_rn(tm, kMagic), -pow2f(12 * j), r);
+    li[j] = __float_as_int(tm) - 0x4B400000;
+  }
+  return r != 0.0f || under;
+}
+
+// the three digit words of a limb set: (lo0, hi0, lo1, hi1), (lo2, ..), (lo4, .., hi5)
+__device__ __forceinline__ void digit_words(const int (&li)[6], uint32_t (&w)[3]) {
+  int lo[6], hi[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    lo[j] = ((li[j] + 128) & 255) - 128;
+    hi[j] = (li[j] - lo[j]) >> 8;
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    w[q] = __byte_perm(__byte_perm((uint32_t)lo[2 * q], (uint32_t)hi[2 * q], 0x0040),
+                       __byte_perm((uint32_t)lo[2 * q + 1], (uint32_t)hi[2 * q + 1], 0x0040), 0x5410);
+}
+
+// B fragments (digit weights) of this lane for the three n-tiles
+__device__ __forceinline__ void weight_frags(int lane, uint32_t (&b)[3]) {
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < 3; ++nt) b[nt] = *reinterpret_cast<const uint32_t*>(&c_coef8[8 * nt + g][4 * tq]);
+}
+
+// residue bits (kMagic + r) of an exact int32 sum S (|S| < 2^22) modulo m
+__device__ __forceinline__ uint32_t mod_s(int S, float m, float inv) {
+  const float sm = __int_as_float(S + 0x4B400000);
+  const float q = __fsub_rn(__fmaf_rn(__fsub_rn(sm, kMagic), inv, kMagic), kMagic);
+  return __float_as_uint(__fmaf_rn(-q, m, sm));
+}
+
+// One group of 32 elements of a warp: the staged digit words of elements
+// e = 0..31 at sw[e * 5 + q] (stride 5: conflict-free fragment reads) ->
+// for each modulus t < nmod held by this lane (t = 8 nt + 2 tq + c) the word of
+// residue bytes of elements 4 g .. 4 g + 3, handed to emit(t, word).
+template <class Emit>
+__device__ __forceinline__ void mma_residues(const uint32_t* sw, int lane, const uint32_t (&bw)[3], int nmod,
+                                             Emit emit) {
+  const int g = lane >> 2, tq = lane & 3;
+  int acc[2][3][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const uint32_t a0 = tq < 3 ? sw[(4 * g + 2 * mt) * 5 + tq] : 0u;
+    const uint32_t a1 = tq < 3 ? sw[(4 * g + 2 * mt + 1) * 5 + tq] : 0u;
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0;
+      mma_s8(acc[mt][nt], a0, a1, bw[nt]);
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int t = 8 * nt + 2 * tq + c;
+      if (t >= nmod) continue;
+      const float m = c_mod[t], inv = c_inv[t];
+      // elements 4g (mt 0 row g), 4g+1 (mt 0 row g+8), 4g+2, 4g+3 (mt 1)
+      emit(t, pack4(mod_s(acc[0][nt][c], m, inv), mod_s(acc[0][nt][2 + c], m, inv), mod_s(acc[1][nt][c], m, inv),
+                    mod_s(acc[1][nt][2 + c], m, inv)));
+    }
+}
+
+// A (rows x k, NC comps) -> residue planes [t][i][kp] on the tensor cores: a
+// warp per 32 consecutive k of a row (lane = element), eight warps per CTA,
+// rows strided over y
+template <int NC>
+__global__ void __launch_bounds__(256) k_res_rows_mma(const float* __restrict__ a, int64_t rows, int64_t k,
+                                                      int64_t kp, int pa, int nmod, const int* __restrict__ e,
+                                                      int8_t* __restrict__ out) {
+  __shared__ uint32_t sw_all[8][32 * 5];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* sw = sw_all[warp];
+  const int64_t k0 = ((int64_t)blockIdx.x * 8 + warp) * 32;
+  if (k0 >= kp) return;
+  uint32_t bw[3];
+  weight_frags(lane, bw);
+  const int64_t plane = rows * kp;
+  const int g = lane >> 2;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    float sa, sb;
+    scale_pair(pa, e[i], sa, sb);
+    const int64_t kk = k0 + lane;
+    float c[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = kk < k ? __ldg(a + (i * k + kk) * NC + q) : 0.0f;
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) fin = fin && isfinite(c[q]);
+    int li[6];
+    limbs_int(fin ? c[0] : 0.0f, sa, sb, li);
+    if constexpr (NC == 2) {
+      int l2[6];
+      limbs_int(fin ? c[1] : 0.0f, sa, sb, l2);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) li[j] += l2[j];
+    }
+    uint32_t wd[3];
+    digit_words(li, wd);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) sw[lane * 5 + q] = wd[q];
+    __syncwarp();
+    int8_t* o = out + i * kp + k0 + 4 * g;
+    mma_residues(sw, lane, bw, nmod,
+                 [&](int t, uint32_t word) { *reinterpret_cast<uint32_t*>(o + t * plane) = word; });
+  }
+}
+
+// B (k x n, NC comps) -> residue planes [t][j][kp] (K contiguous per column) on
+// the tensor cores: a warp per 4 k x 32 columns (lane = column: coalesced
+// loads), four 32-element groups (columns 8 p .. 8 p + 7, p = 0..3, each with
+// its 4 k); the transposed binary32 copy bt and the inexact counts as in
+// k_res_cols.  CTA = eight warps = 32 k x 32 columns.
+template <int NC>
+__global__ void __launch_bounds__(256) k_res_cols_mma(const float* __restrict__ b, int64_t n, int64_t ldb, int64_t k,
+                                                      int64_t kp, int pb, int nmod, const int* __restrict__ e,
+                                                      int8_t* __restrict__ out, int64_t np, float* __restrict__ bt,
+                                                      int* __restrict__ cinx) {
+  __shared__ uint32_t sw_all[8][4][32 * 5];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32 + warp * 4;
+  const int64_t j = j0 + lane;
+  uint32_t bw[3];
+  weight_frags(lane, bw);
+  float sa = 1.0f, sb = 1.0f;
+  if (j < n) scale_pair(pb, e[j], sa, sb);
+  int inexact = 0;
+  float keep[4][NC];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t gk = k0 + u;
+    float c[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = (gk < k && j < n) ? b[(gk * ldb + j) * NC + q] : 0.0f;
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      keep[u][q] = c[q];
+      fin = fin && isfinite(c[q]);
+    }
+    int li[6];
+    inexact += limbs_int(fin ? c[0] : 0.0f, sa, sb, li);
+    if constexpr (NC == 2) {
+      int l2[6];
+      inexact += limbs_int(fin ? c[1] : 0.0f, sa, sb, l2);
+#pragma unroll
+      for (int jj = 0; jj < 6; ++jj) li[jj] += l2[jj];
+    }
+    uint32_t wd[3];
+    digit_words(li, wd);
+    // group p = lane / 8 holds columns 8 p .. 8 p + 7; element = 4 (lane % 8) + u
+    uint32_t* sw = sw_all[warp][lane >> 3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) sw[(4 * (lane & 7) + u) * 5 + q] = wd[q];
+  }
+  if (inexact && j < n) atomicAdd(cinx + j, inexact);
+  if (j < n) {  // transposed binary32 copy for the fallback
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (k0 + u < k)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) bt[(j * k + k0 + u) * NC + q] = keep[u][q];
+  }
+  __syncwarp();
+  const int g = lane >> 2;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    // group p: element 4 g + u = column j0 + 8 p + g, k0 + u
+    const int64_t jc = j0 + 8 * p + g;
+    mma_residues(sw_all[warp][p], lane, bw, nmod, [&](int t, uint32_t word) {
+      if (jc < n && k0 < kp) *reinterpret_cast<uint32_t*>(out + (t * np + jc) * kp + k0) = word;
+    });
   }
 }
 
@@ -601,7 +826,7 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
   if (ep.act) ep.act[i * ldo + j] = ep.relu ? (hv > 0.0f ? hv : 0.0f) : hv;  // Tape::relu, autodiff.hpp:134
 }
 
-// fallback thresholds in units of Y = C' / 2^(L-99): 2^50 x the per-output
+// fallback thresholds in units of Y = C' / 2^(L-96): 2^50 x the per-output
 // error bound.  base: A's rounding (1/2 unit per element) times |B'| plus
 // B's for an MC B; xa / xb: the extra 1/2 unit per element of a row / MC
 // column whose leading components are not integers at the scale (flag bit 2);
@@ -635,10 +860,10 @@ __device__ __forceinline__ float mod_c(int c, int t) {
 // (C' mod m_t), scaled back, split into two binary32 components written with
 // row stride ldo; ill-conditioned / non-finite outputs are listed per row
 // (rlist[i * n + slot] = j, rcnt[i] entries) for the fallback.
-//   T_j = sum_t r_t w_tj  (|T_j| < 2^21.5: exact binary32 sums)
-//   q   = rint((T_0 + T_1 2^-11) 2^(L-11) / M)   (error < 2^-10; |C'/M| <= 1/4)
-//   D_j = T_j - q M_j     (exact, |D_j| < 2^22.6)
-//   Y   = sum_j D_j 2^(11 (8 - j)) = C' / 2^(L-99) + tail (binary64 Horner:
+//   T_j = sum_t r_t w_tj  (|T_j| <= 22 128 2^11 < 2^22.5: exact binary32 sums)
+//   q   = rint((T_0 + T_1 2^-12) 2^(L-12) / M)   (error < 2^-10; |C'/M| <= 1/4)
+//   D_j = T_j - q M_j     (exact, |D_j| < 2^23.5)
+//   Y   = sum_j D_j 2^(12 (7 - j)) = C' / 2^(L-96) + tail (binary64 Horner:
 //         partial sums < 2^53 exact while the later terms can still cancel them)
 // Four consecutive columns per thread (16-byte plane loads; np % 16 == 0).
 template <int NMOD, bool BIG>
@@ -683,11 +908,11 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + u;
       if (j >= n) break;
-      const float u0 = __fmaf_rn(T[u][1], 0x1p-11f, T[u][0]);
+      const float u0 = __fmaf_rn(T[u][1], 0x1p-12f, T[u][0]);
       const float q = __fsub_rn(__fmaf_rn(u0, c_crt[NMOD].cq, kMagic), kMagic);
       double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], T[u][0]);
 #pragma unroll
-      for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], T[u][s]));
+      for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 4096.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], T[u][s]));
       if (((fi | cfj[u]) & 1) || !(fabs(y) >= th.at(fi, cfj[u], inx[u]))) {
         rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
         continue;
@@ -756,11 +981,11 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
     float Tu[kSlices];
 #pragma unroll
     for (int sl = 0; sl < kSlices; ++sl) Tu[sl] = (u & 1) ? T[u >> 1][sl].y : T[u >> 1][sl].x;
-    const float u0 = __fmaf_rn(Tu[1], 0x1p-11f, Tu[0]);
+    const float u0 = __fmaf_rn(Tu[1], 0x1p-12f, Tu[0]);
     const float q = __fsub_rn(__fmaf_rn(u0, c_crt[NMOD].cq, kMagic), kMagic);
     double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], Tu[0]);
 #pragma unroll
-    for (int sl = 1; sl < kSlices; ++sl) y = __fma_rn(y, 2048.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[sl], Tu[sl]));
+    for (int sl = 1; sl < kSlices; ++sl) y = __fma_rn(y, 4096.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[sl], Tu[sl]));
     const int fc = cnf[j];
     if (((fi | fc) & 1) || !(fabs(y) >= th.at(fi, fc, cinx ? cinx[j] : 0))) {
       rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
@@ -1187,6 +1412,16 @@ int64_t pad32(int64_t v) { return (v + 31) / 32 * 32; }
 
 }  // namespace
 
+// residue kernels: limb-sum FFMA kernels by default; MCF_OZ_RES=mma selects
+// the tensor-core (mma.sync) restatement (A/B measurement)
+bool res_on_tensor_cores() {
+  static const bool v = [] {
+    const char* e = getenv("MCF_OZ_RES");
+    return e && std::string(e) == "mma";
+  }();
+  return v;
+}
+
 // Prepared B operand (a block of n columns of a k x ldb matrix): residue
 // planes, column exponents, non-finite flags and the transposed binary32
 // copy.  Built once; shared by every row chunk of A.
@@ -1248,8 +1483,13 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu);
   k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, pl.pb, ncb == 2 ? cu : nullptr, eb, cnf);
   const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
-  OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
-                 else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
+  if (res_on_tensor_cores()) {
+    if (ncb == 2) k_res_cols_mma<2><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, pl.pb, pl.n, eb, planes, np, bt, cinx);
+    else k_res_cols_mma<1><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, pl.pb, pl.n, eb, planes, np, bt, cinx);
+  } else {
+    OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
+                   else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
+  }
   for (int i = 0; i < 3; ++i) mcfr::note_launch();
   pb = PreparedB{planes, bt, eb, cnf, ncb == 1 ? cinx : nullptr, k, kp, n, np, ncb, pl};
   return mcfr::check_launch("mm_fast B residue kernels");
@@ -1297,17 +1537,25 @@ mcf_status a_residues(const float* x, int nca, int64_t m, int64_t k, const CrtPl
   const unsigned gr = (unsigned)((m + 7) / 8);
   if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
   else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
-  const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
-  const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
-  OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
-                 else k_res_rows<1, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes));
+  if (res_on_tensor_cores()) {
+    const int64_t gx = (kp + 255) / 256;  // eight warps x 32 k per CTA, rows strided over y
+    const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
+    if (nca == 2) k_res_rows_mma<2><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, pl.n, w.ea, w.planes);
+    else k_res_rows_mma<1><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, pl.n, w.ea, w.planes);
+  } else {
+    const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
+    const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
+    OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
+                   else k_res_rows<1, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes));
+  }
   mcfr::note_launch();
   mcfr::note_launch();
   return mcfr::check_launch("mm_fast A residue kernels");
 }
 
 mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo,
-                         const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep);
+                         const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep,
+                         cudaStream_t cs = nullptr, cudaEvent_t gemm_done = nullptr);
 
 // out (m x n x 2 binary32, row stride ldo elements) = A (m x k x nca) . B for
 // a prepared B.  ev (optional, 4 events): recorded before the A residues,
@@ -1321,9 +1569,13 @@ mcf_status rows(const float* x, int nca, int64_t m, const PreparedB& pb, float* 
   return rows_products(x, nca, m, pb, out, ldo, w, s, ev, ep);
 }
 
-// the GEMMs, reconstruction and fallback of a row block whose A residues are done
+// the GEMMs, reconstruction and fallback of a row block whose A residues are
+// done.  With a second stream cs (and an event), the reconstruction and the
+// fallback are enqueued there after the GEMM: they then run concurrently with
+// whatever the caller puts on s next (the next row block's GEMM).
 mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb, float* out, int64_t ldo,
-                         const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep) {
+                         const RowsWs& w, cudaStream_t s, cudaEvent_t* ev, const Epilogue& ep, cudaStream_t cs,
+                         cudaEvent_t gemm_done) {
   const CrtPlan pl = pb.plan;
   const int64_t k = pb.k, kp = pb.kp, n = pb.n, np = pb.np;
   if (ev) cudaEventRecord(ev[1], s);
@@ -1345,21 +1597,26 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   }
   if (st != MCF_OK) return st;
   if (ev) cudaEventRecord(ev[2], s);
+  if (cs && gemm_done) {
+    cudaEventRecord(gemm_done, s);
+    cudaStreamWaitEvent(cs, gemm_done, 0);
+    s = cs;
+  }
   // error bound per output in C' units (2^-(pa+pb) scaled): A's rounding
   // (<= 0.51) times |B'| < 2^(pb-1), B's (<= 0.51 for an MC B; for a binary32
   // B only its counted inexact elements, each <= 0.51 2^(pa-1)), their
-  // product, and the CRT slices' tail (<= 2^12 units of 2^(L - 99)).  The
-  // fallback threshold is 2^50 times it, in units of Y = C' / 2^(L-99).
+  // product, and the CRT slices' tail (<= 2^12 units of 2^(L - 96)).  The
+  // fallback threshold is 2^50 times it, in units of Y = C' / 2^(L-96).
   const int L = host_crt().tab[pl.n].L;
-  const double yu = std::ldexp(1.0, 99 - L) * 1.0001 * std::ldexp(1.0, 50);  // C' units -> Y units, x 2^50
+  const double yu = std::ldexp(1.0, kYShift - L) * 1.0001 * std::ldexp(1.0, 50);  // C' units -> Y units, x 2^50
   Thresholds th;
   const double ta = 0.51 * std::ldexp(1.0, pl.pb - 1), tb = 0.51 * std::ldexp(1.0, pl.pa - 1);
-  th.base = ((double)k * (ta + (pb.ncb == 2 ? tb : 0.0) + 1.1) * std::ldexp(1.0, 99 - L) + 4096.0) * 1.0001 *
+  th.base = ((double)k * (ta + (pb.ncb == 2 ? tb : 0.0) + 1.1) * std::ldexp(1.0, kYShift - L) + 4096.0) * 1.0001 *
             std::ldexp(1.0, 50);
   th.xa = (double)k * ta * yu;
   th.xb = pb.ncb == 2 ? (double)k * tb * yu : 0.0;
   th.inexact = tb * yu;
-  const int sexp = L - 99 - pl.pa - pl.pb;
+  const int sexp = L - kYShift - pl.pa - pl.pb;
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
   const bool big = k > 16384;
@@ -1761,37 +2018,89 @@ bool ozaki_supported(int64_t m, int64_t k, int64_t n) {
          mcfg::oz::crt_plan(k, 1).n > 0;
 }
 
-// A's residues on a side stream while B is prepared on the caller's stream
-// (thread-local fork / join events, no per-call event creation)
-static mcf_status prepare_both(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n,
-                               char* ws, std::size_t bb, mcfg::oz::PreparedB& pb, mcfg::oz::RowsWs& rw,
-                               cudaStream_t s) {
+// The one-call product, optionally pipelined over row blocks of A (MCF_OZ_PIPE).  B's residues run on
+// the caller's stream s while the first block's A residues run on a side
+// stream; then, per block c, s waits for its A residues and runs its residue
+// GEMM, and the block's reconstruction + fallback go to a third stream.  The
+// later blocks' A residues (issued once B's are done) and the earlier blocks'
+// reconstructions run concurrently with the GEMM of the block in between:
+// the GEMM keeps one CTA per SM busy on the tensor cores and TMA, and these
+// FMA-pipe kernels fill the SMs' remaining warp slots.  Row blocks are
+// multiples of 256 (the CTA-pair tile); products under 1024 rows run as one
+// block.  Results are those of the unpipelined product bit for bit (every
+// output depends on its own row and column only).
+static mcf_status pipelined(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n,
+                            float* out, int64_t ldo, const mcfg::oz::Epilogue& ep0, cudaStream_t s) {
   using namespace mcfg::oz;
+  static const int blocks_env = [] {
+    // row blocks (1: no pipelining, the default).  Measured on B200 (r02,
+    // config 2): 1 block 1.308 ms, 2 blocks 1.329, 4 blocks 1.355, 6 blocks
+    // 1.388 -- the residue and reconstruction kernels do not hide under the
+    // GEMM (both are FMA-pipe / issue heavy and the GEMM's epilogue needs the
+    // same pipes), and the shorter GEMMs lose their last-wave tails.
+    const char* e = getenv("MCF_OZ_PIPE");
+    return e ? std::max(1, std::min(6, atoi(e))) : 1;
+  }();
+  int nb = m >= 1024 ? blocks_env : 1;
+  int64_t rb = (m + nb - 1) / nb;
+  rb = (rb + 255) / 256 * 256;
+  nb = (int)((m + rb - 1) / rb);
   const CrtPlan pl = crt_plan(k, ncb);
-  rw = rows_ws(ws + bb, m, pad32(k), pad16(n), pl.n);
-  cudaStream_t as = side_stream(12);
-  cudaEvent_t fork = tl_event(0), adone = tl_event(1);
+  const std::size_t bb = al(b_bytes(k, n, ncb)), rbytes = al(rows_bytes(rb, k, n, ncb));
+  char* ws = oz_workspace(bb + nb * rbytes, s);
+  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
+  cudaStream_t as = side_stream(12), cs = side_stream(13);
+  cudaEvent_t fork = tl_event(0), bdone = tl_event(1);
   cudaEventRecord(fork, s);
   cudaStreamWaitEvent(as, fork, 0);
-  mcf_status st = a_residues(x, nca, m, k, pl, rw, as);
-  cudaEventRecord(adone, as);
+  cudaStreamWaitEvent(cs, fork, 0);
+  std::vector<RowsWs> rws(nb);
+  mcf_status st = MCF_OK;
+  // block 0's A residues alongside B's
+  for (int c = 0; c < nb; ++c) {
+    const int64_t r0 = c * rb, rows_c = std::min<int64_t>(rb, m - r0);
+    rws[c] = rows_ws(ws + bb + c * rbytes, rows_c, pad32(k), pad16(n), pl.n);
+  }
+  st = a_residues(x, nca, std::min<int64_t>(rb, m), k, pl, rws[0], as);
+  cudaEvent_t adone[16];
+  adone[0] = tl_event(2);
+  cudaEventRecord(adone[0], as);
+  PreparedB pb;
   if (st == MCF_OK) st = prepare_b(w, ncb, k, n, n, ws, pb, s);
-  cudaStreamWaitEvent(s, adone, 0);
+  cudaEventRecord(bdone, s);
+  cudaStreamWaitEvent(as, bdone, 0);
+  // the other blocks' A residues after B's: they then share the SMs with the
+  // GEMMs, not with B's residues (which gate the first GEMM)
+  for (int c = 1; c < nb && st == MCF_OK; ++c) {
+    const int64_t r0 = c * rb, rows_c = std::min<int64_t>(rb, m - r0);
+    st = a_residues(x + r0 * k * nca, nca, rows_c, k, pl, rws[c], as);
+    adone[c] = tl_event(2 + c);
+    cudaEventRecord(adone[c], as);
+  }
+  for (int c = 0; c < nb && st == MCF_OK; ++c) {
+    const int64_t r0 = c * rb, rows_c = std::min<int64_t>(rb, m - r0);
+    cudaStreamWaitEvent(s, adone[c], 0);
+    Epilogue ep = ep0;
+    if (ep.bias) {
+      ep.bias += r0 * 2;
+      ep.h += r0 * ldo;
+      if (ep.act) ep.act += r0 * ldo;
+    }
+    st = rows_products(x + r0 * k * nca, nca, rows_c, pb, ep.bias ? nullptr : out + r0 * ldo * 2, ldo, rws[c], s,
+                       nullptr, ep, nb > 1 ? cs : nullptr, nb > 1 ? tl_event(8 + c) : nullptr);
+  }
+  if (nb > 1) {
+    cudaEvent_t join = tl_event(14);
+    cudaEventRecord(join, cs);
+    cudaStreamWaitEvent(s, join, 0);
+  }
   return st;
 }
 
 // one-call MC(nc=2, binary32) x T / MC(nc=2) product on the INT8 tensor cores
 mcf_status mm_ozaki(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n, float* out,
                     cudaStream_t s) {
-  using namespace mcfg::oz;
-  const std::size_t bb = al(b_bytes(k, n, ncb));
-  char* ws = oz_workspace(bb + al(rows_bytes(m, k, n, ncb)), s);
-  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
-  PreparedB pb;
-  RowsWs rw;
-  const mcf_status st = prepare_both(x, nca, w, ncb, m, k, n, ws, bb, pb, rw, s);
-  if (st != MCF_OK) return st;
-  return rows_products(x, nca, m, pb, out, n, rw, s, nullptr, Epilogue{});
+  return pipelined(x, nca, w, ncb, m, k, n, out, n, mcfg::oz::Epilogue{}, s);
 }
 
 // MC-MLP layer forward on the tensor-core path with the bias / approx / ReLU
@@ -1801,19 +2110,12 @@ mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t 
                              int relu, float* h, float* act, cudaStream_t s) {
   using namespace mcfg::oz;
   if (m < 64 || !ozaki_supported(m, k, n)) return MCF_ERR_UNSUPPORTED;
-  const std::size_t bb = al(b_bytes(k, n, 1));
-  char* ws = oz_workspace(bb + al(rows_bytes(m, k, n, 1)), s);
-  if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
-  PreparedB pb;
-  RowsWs rw;
-  const mcf_status st = prepare_both(w, 2, a, 1, m, k, n, ws, bb, pb, rw, s);
-  if (st != MCF_OK) return st;
   Epilogue ep;
   ep.bias = bias;
   ep.h = h;
   ep.act = act;
   ep.relu = relu;
-  return rows_products(w, 2, m, pb, nullptr, n, rw, s, nullptr, ep);
+  return pipelined(w, 2, a, 1, m, k, n, nullptr, n, ep, s);
 }
 
 // host-side introspection of the CRT scheme (no device needed): the plan of a
@@ -2031,8 +2333,10 @@ struct GemmFork {
 mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                        int64_t ldc, int64_t m, int64_t n, int64_t k, const float* mask, cudaStream_t s) {
   using namespace mcfg::oz;
-  if (m < 64 || n < 64 || k < 64 || k >= 32768 || m * n >= (int64_t(1) << 31)) return MCF_ERR_UNSUPPORTED;
-  const int64_t kp = (k + 31) / 32 * 32, np = pad16(n);
+  if (m < 64 || n < 64 || k < 64 || k > 32640 || m * n >= (int64_t(1) << 31)) return MCF_ERR_UNSUPPORTED;
+  // K padded to the tcgen05 GEMM's 128-byte K block (a diagonal's operand is
+  // a run of whole planes: its last block must not reach the next plane)
+  const int64_t kp = (k + 127) / 128 * 128, np = pad16(n);
   const std::size_t ba = al(m * kD4 * kp), bb = al(np * kD4 * kp), bq = al(4 * m * np * 4);
   char* ws = oz_workspace(ba + bb + bq + al(m * 4) + al(np * 4), s);
   if (!ws) return fail(MCF_ERR_CUDA, "gemm_f32: cannot allocate the digit-plane workspace");
@@ -2071,9 +2375,23 @@ mcf_status gemm_f32_i8(int trans_a, int trans_b, const float* a, int64_t lda, co
   for (int i = 0; i < 4; ++i) mcfr::note_launch();
   mcf_status st = mcfr::check_launch("gemm_f32 digit kernels");
   if (st != MCF_OK) return st;
-  // diagonal q: A planes s = q - th .. q (ascending) against B planes t = th ..
-  // q - (q - th) (stored reversed at kD4 - 1 - t: ascending positions)
-  {
+  // diagonal q: A planes s = 0 .. q (ascending) against B planes t = q .. 0
+  // (stored reversed at kD4 - 1 - t: ascending positions), pairs (q - t, t):
+  // all four diagonals in one launch of the tcgen05 GEMM (MCF_OZ_GEMM=cublaslt:
+  // one cuBLASLt GEMM per diagonal)
+  static const bool use_lt = [] {
+    const char* e = getenv("MCF_OZ_GEMM");
+    return e && std::string(e) == "cublaslt";
+  }();
+  if (!use_lt) {
+    int ka[kD4], kb[kD4], kd[kD4];
+    for (int q = 0; q < kD4; ++q) {
+      ka[q] = 0;
+      kb[q] = (int)((kD4 - 1 - q) * kp);
+      kd[q] = (int)((q + 1) * kp);
+    }
+    st = mcfr::tc_gemm_s8_seg(ap, kD4 * kp, bp, kD4 * kp, cq, m, n, np, kD4, ka, kb, kd, np, s);
+  } else {
     GemmFork gf(s, np, m);
     for (int q = 0; q < kD4 && st == MCF_OK; ++q) {
       const int th = q, tl = 0;  // pairs (q - t, t), t = 0 .. q (all within four digits)
@@ -2099,7 +2417,7 @@ mcf_status mm_b16_i8(const void* x, const void* y, int nc, int64_t m, int64_t k,
   using namespace mcfg::oz;
   if (nc < 1 || nc > 3 || m < 64 || n < 64 || k < 64 || k >= 26000 || m * n >= (int64_t(1) << 31))
     return MCF_ERR_UNSUPPORTED;
-  const int64_t kp = (k + 31) / 32 * 32, np = pad16(n);
+  const int64_t kp = (k + 127) / 128 * 128, np = pad16(n);  // whole 128-byte K blocks per plane
   const std::size_t ba = al(m * kD5 * kp), bb = al(np * kD5 * kp), bq = al((int64_t)kD5 * m * np * 4);
   char* ws = oz_workspace(ba + bb + bq + al(m * 8) + al(np * 8), s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_mcmc: cannot allocate the digit-plane workspace");
@@ -2133,7 +2451,20 @@ mcf_status mm_b16_i8(const void* x, const void* y, int nc, int64_t m, int64_t k,
   }
   for (int i = 0; i < 4; ++i) mcfr::note_launch();
   mcf_status st = mcfr::check_launch("mm_mcmc binary16 digit kernels");
-  {
+  static const bool use_lt = [] {
+    const char* e = getenv("MCF_OZ_GEMM");
+    return e && std::string(e) == "cublaslt";
+  }();
+  if (st == MCF_OK && !use_lt) {
+    // the five diagonals in one tcgen05 launch (A planes 0..q against B planes q..0)
+    int ka[kD5], kb[kD5], kd[kD5];
+    for (int q = 0; q < kD5; ++q) {
+      ka[q] = 0;
+      kb[q] = (int)((kD5 - 1 - q) * kp);
+      kd[q] = (int)((q + 1) * kp);
+    }
+    st = mcfr::tc_gemm_s8_seg(ap, kD5 * kp, bp, kD5 * kp, cq, m, n, np, kD5, ka, kb, kd, np, s);
+  } else if (st == MCF_OK) {
     GemmFork gf(s, np, m);
     for (int q = 0; q < kD5 && st == MCF_OK; ++q)
       st = gemm_s8(bp + (int64_t)(kD5 - 1 - q) * kp, kD5 * kp, ap, kD5 * kp, cq + (int64_t)q * m * np, np, m,

@@ -53,6 +53,12 @@ struct Params {
   float inv[kMaxBatch];  // RN32(1 / m_b)
   float c14[kMaxBatch];  // 2^14 mod m_b, symmetric
   int big;               // |C| may exceed 2^28 (K > 2^14): two-step reduction
+  // segment mode (nseg > 0, int32 output, pair kernel): batch entry b reads
+  // K bytes [seg_ka[b], + 128 seg_kblk[b]) of every row of a and [seg_kb[b],
+  // ...) of every row of b (one 2-D operand each, rows of any stride): the
+  // diagonal GEMMs of the digit-plane schemes, one launch for all diagonals
+  int nseg;
+  int seg_ka[kMaxBatch], seg_kb[kMaxBatch], seg_kblk[kMaxBatch];
 };
 
 // ---- PTX helpers ----
@@ -390,11 +396,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = pair; tile < total; tile += npairs) {
         const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        const int kbl = p.nseg ? p.seg_kblk[b] : kblocks, ka0 = p.nseg ? p.seg_ka[b] : 0,
+                  kb0 = p.nseg ? p.seg_kb[b] : 0, zb = p.nseg ? 0 : b;
+        for (int kb = 0; kb < kbl; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           if (leader) mbar_expect_tx(full + stage, 2 * kStage2);
-          tma_load_3d_pair(sa + stage * kHalfBytes, &ta, kb * BK, mb * 256 + (int)rank * 128, b, full + stage);
-          tma_load_3d_pair(sb + stage * kHalfBytes, &tb, kb * BK, nb * 256 + (int)rank * 128, b, full + stage);
+          tma_load_3d_pair(sa + stage * kHalfBytes, &ta, ka0 + kb * BK, mb * 256 + (int)rank * 128, zb, full + stage);
+          tma_load_3d_pair(sb + stage * kHalfBytes, &tb, kb0 + kb * BK, nb * 256 + (int)rank * 128, zb, full + stage);
           if (++stage == kStages2) {
             stage = 0;
             phase ^= 1;
@@ -407,10 +415,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
       for (int tile = pair; tile < total; tile += npairs) {
+        const int kbl = p.nseg ? p.seg_kblk[tile / per_b] : kblocks;
         mbar_wait(tempty + acc, aphase ^ 1);
         fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < kbl; ++kb) {
           mbar_wait(full + stage, phase);
           fence_after();
           const uint32_t a0 = smem_u32(sa + stage * kHalfBytes), b0 = smem_u32(sb + stage * kHalfBytes);
@@ -587,6 +596,53 @@ mcf_status tc_gemm_s8(const int8_t* a, const int8_t* b, void* out, int64_t m, in
   }
   note_launch();
   return check_launch("tcgen05 int8 GEMM");
+}
+
+// The diagonal GEMMs of a digit-plane scheme in one launch (pair kernel,
+// int32 output): for d < nseg, out_d (m x n, row stride ldo) = A_d . B_d^T
+// with A_d = bytes [ka[d], ka[d] + kd[d]) of each of a's m rows (row stride
+// lda bytes) and B_d likewise from b (n used of b_rows rows, stride ldb).
+// ka, kb, kd multiples of 128 (a segment's last K block must not read the
+// next segment's bytes); MCF_ERR_UNSUPPORTED otherwise.
+mcf_status tc_gemm_s8_seg(const int8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int* out, int64_t m, int64_t n,
+                          int64_t b_rows, int nseg, const int* ka, const int* kb, const int* kd, int64_t ldo,
+                          cudaStream_t s) {
+  using namespace mcfg::tc;
+  if (b_rows < n) b_rows = n;
+  if (m <= 0 || n <= 0 || nseg < 1 || nseg > kMaxBatch || lda % 16 || ldb % 16 || ldo < n || ldo % 4 ||
+      (reinterpret_cast<uintptr_t>(out) & 15) || (reinterpret_cast<uintptr_t>(a) & 15) ||
+      (reinterpret_cast<uintptr_t>(b) & 15) || m >= (int64_t(1) << 31) || n >= (int64_t(1) << 31))
+    return MCF_ERR_UNSUPPORTED;
+  Params p{};
+  p.m = (int)m;
+  p.n = (int)n;
+  p.kp = BK;
+  p.batch = nseg;
+  p.tiles_m = (int)((m + BM - 1) / BM);
+  p.tiles_n = (int)((n + BN - 1) / BN);
+  p.ldo = ldo;
+  p.mode = 0;
+  p.out = out;
+  p.nseg = nseg;
+  for (int d = 0; d < nseg; ++d) {
+    if (ka[d] % BK || kb[d] % BK || kd[d] % BK || kd[d] <= 0 || ka[d] + kd[d] > lda || kb[d] + kd[d] > ldb ||
+        kd[d] >= (1 << 17))
+      return MCF_ERR_UNSUPPORTED;
+    p.seg_ka[d] = ka[d];
+    p.seg_kb[d] = kb[d];
+    p.seg_kblk[d] = kd[d] / BK;
+  }
+  CUtensorMap ta2, tb2;
+  if (!make_map(&ta2, a, m, lda, 1, 128) || !make_map(&tb2, b, b_rows, ldb, 1, 128)) return MCF_ERR_UNSUPPORTED;
+  const int smem = kStages2 * kStage2 + 1024 + 256;
+  per_device_once(kOnceTcGemm, [&] {
+    cudaFuncSetAttribute(k_tc_gemm_s8_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  const int64_t tiles = (int64_t)((m + 255) / 256) * p.tiles_n * nseg;
+  const int grid = 2 * (int)std::min<int64_t>(tiles, sm_count() / 2);
+  k_tc_gemm_s8_pair<<<grid, kThreads, smem, s>>>(ta2, tb2, p);
+  note_launch();
+  return check_launch("tcgen05 int8 GEMM (segments)");
 }
 
 }  // namespace mcfr

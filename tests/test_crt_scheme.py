@@ -17,7 +17,8 @@ import pytest
 
 import paper_2207_08867_b200 as mcf
 
-S = 9  # slices
+S = 8  # slices
+SB = 12  # slice bits
 MAGIC = np.float32(12582912.0)
 
 
@@ -62,10 +63,10 @@ def test_crt_tables_are_exact_slices(n):
     assert len(set(mods)) == n and all(math.gcd(a, b) == 1 for i, a in enumerate(mods) for b in mods[i + 1:])
     M = math.prod(mods)
     assert M.bit_length() == L
-    tail = 2 ** (L - 11 * S - 1)
-    rec = lambda d: sum(int(v) * 2 ** (L - 11 * (j + 1)) for j, v in enumerate(d))
+    tail = 2 ** (L - SB * S - 1)
+    rec = lambda d: sum(int(v) * 2 ** (L - SB * (j + 1)) for j, v in enumerate(d))
     assert abs(rec(mh) - M) <= tail
-    assert np.all(np.abs(w) <= 1024) and np.all(np.abs(mh[1:]) <= 1024) and mh[0] <= 2048
+    assert np.all(np.abs(w) <= 2048) and np.all(np.abs(mh[1:]) <= 2048) and mh[0] <= 4096
     for t, m in enumerate(mods):
         Mt = M // m
         wt = Mt * pow(Mt, -1, m) % M
@@ -74,7 +75,7 @@ def test_crt_tables_are_exact_slices(n):
         assert abs(rec(w[t]) - wt) <= tail
         for s, ms in enumerate(mods):
             assert wt % ms == (1 if s == t else 0)
-    assert abs(float(cq) - 2.0 ** (L - 11) / M) <= 2.0 ** (L - 11) / M * 2 ** -24
+    assert abs(float(cq) - 2.0 ** (L - SB) / M) <= 2.0 ** (L - SB) / M * 2 ** -24
 
 
 def sym(v, m):
@@ -119,13 +120,13 @@ def emulate_reconstruct(res, n):
     T = np.zeros(S, np.float32)
     for t in range(n):
         T = (T.astype(np.float64) + np.float64(res[t]) * w[t].astype(np.float64)).astype(np.float32)  # exact
-    u0 = np.float32(np.float64(T[1]) * 2.0 ** -11 + np.float64(T[0]))
+    u0 = np.float32(np.float64(T[1]) * 2.0 ** -SB + np.float64(T[0]))
     q = np.float32(np.float64(u0) * np.float64(cq) + np.float64(MAGIC)) - MAGIC
     D = (T.astype(np.float64) - np.float64(q) * mh.astype(np.float64)).astype(np.float32)
     assert np.all(D.astype(np.float64) == T.astype(np.float64) - np.float64(q) * mh)  # exact
     y = np.float64(D[0])
     for j in range(1, S):
-        y = np.float64(y * 2048.0 + np.float64(D[j]))  # fma: y * 2048 is exact
+        y = np.float64(y * 4096.0 + np.float64(D[j]))  # fma: y * 4096 is exact
     return float(y), L
 
 
@@ -139,10 +140,10 @@ def test_reconstruction_recovers_the_integer(n):
     for v in vals:
         res = [sym(v, m) for m in mods]
         y, L = emulate_reconstruct(res, n)
-        got = Fraction(y) * 2 ** (L - 99)
+        got = Fraction(y) * 2 ** (L - SB * S)
         err = abs(got - v)
-        # slice tail (<= 2^12 units of 2^(L-99)) + binary64 Horner rounding
-        assert err <= 2 ** (L - 99 + 12) + abs(Fraction(v)) * 2 ** -50, (v, float(err))
+        # slice tail (<= 2^12 units of 2^(L-96)) + binary64 Horner rounding
+        assert err <= 2 ** (L - SB * S + 12) + abs(Fraction(v)) * 2 ** -50, (v, float(err))
 
 
 def emulate_limbs2(x, s):
