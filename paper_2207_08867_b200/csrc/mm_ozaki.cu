@@ -105,11 +105,6 @@ __constant__ float c_pw[kMaxMod][6];  // 2^(12 j) mod m_t, symmetric (limb weigh
 __constant__ float c_c14[kMaxMod];    // 2^14 mod m_t, symmetric
 __constant__ float c_inv[kMaxMod];    // RN32(1 / m_t)
 __constant__ float c_mod[kMaxMod];
-// digit weights of the tensor-core residue kernels: c_coef8[t][k] = 2^w_k mod
-// m_t (symmetric, int8) for the 12 byte digits of the six limbs (w = 12 j for
-// the low byte of limb j, 12 j + 8 for its high part), zero for k >= 12 and
-// for t >= kMaxMod (padding moduli of the last n-tile)
-__constant__ int8_t c_coef8[24][16];
 __constant__ CrtTab c_crt[kMaxMod + 1];  // by moduli count
 
 // ---- host: exact CRT constants (small unsigned big integers) ----
@@ -195,7 +190,6 @@ struct HostCrt {
   CrtTab tab[kMaxMod + 1];
   double log2m[kMaxMod + 1];
   float pw[kMaxMod][6], c14[kMaxMod], inv[kMaxMod], mod[kMaxMod];
-  int8_t coef8[24][16];
 };
 const HostCrt& host_crt() {
   static const HostCrt h = [] {
@@ -212,12 +206,6 @@ const HostCrt& host_crt() {
       h.c14[t] = (float)sym(p14, m);
       h.inv[t] = 1.0f / (float)m;
       h.mod[t] = (float)m;
-      for (int kd = 0; kd < 12; ++kd) {
-        const int w = 12 * (kd / 2) + 8 * (kd % 2);
-        int pw2 = 1 % m;
-        for (int b = 0; b < w; ++b) pw2 = pw2 * 2 % m;
-        h.coef8[t][kd] = (int8_t)sym(pw2, m);  // |sym| <= 127, and 0 / 1 for m = 256
-      }
     }
     for (int n = 1; n <= kMaxMod; ++n) {
       Big M;
@@ -263,8 +251,7 @@ mcf_status upload_crt_tables() {
         cudaMemcpyToSymbol(c_c14, h.c14, sizeof(h.c14)) != cudaSuccess ||
         cudaMemcpyToSymbol(c_inv, h.inv, sizeof(h.inv)) != cudaSuccess ||
         cudaMemcpyToSymbol(c_mod, h.mod, sizeof(h.mod)) != cudaSuccess ||
-        cudaMemcpyToSymbol(c_crt, h.tab, sizeof(h.tab)) != cudaSuccess ||
-        cudaMemcpyToSymbol(c_coef8, h.coef8, sizeof(h.coef8)) != cudaSuccess)
+        cudaMemcpyToSymbol(c_crt, h.tab, sizeof(h.tab)) != cudaSuccess)
       st = mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot upload the CRT tables");
   });
   return st;
@@ -393,216 +380,6 @@ __device__ __forceinline__ void residue_words(const float2 (&l01)[6], const floa
       wd[T] = pack4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(b.x), __float_as_uint(b.y));
     }
     residue_words<NMOD, T + 1>(l01, l23, l0i, wd);
-  }
-}
-
-// ---- residues on the tensor cores (mma.sync m16n8k16 s8) ----------------------
-//
-// The residue of X = sum_j l_j 2^(12 j) modulo m_t is sum_k d_k (2^w_k mod m_t)
-// reduced once, with the limbs cut into byte digits d (low byte of l_j,
-// balanced, and its high part (l_j - lo) / 256, |.| <= 32).  The 12 x 17
-// digit-weight products of an element are an int8 matrix product: 16
-// elements x 16 digits (12 used) times 16 digits x 8 moduli per mma.sync,
-// exact in int32 (|S| <= 6 128 127 + 6 32 127 < 2^17).  What stays on the FMA
-// pipe per element is the limb cutting and one exact reduction per modulus
-// (four FP32 ops), about half the FFMA work of the limb-sum form (res_bits2).
-// Mapping (m16n8 fragments: a0 / a1 = rows g / g+8, k group tq; c0, c1 / c2,
-// c3 = rows g / g+8, columns 2 tq, 2 tq + 1; g = lane / 4, tq = lane % 4):
-// m-tile row r of tile mt holds element 4 (r & 7) + 2 mt + (r >> 3) of a
-// 32-element group, so each thread ends with four CONSECUTIVE elements
-// (4 g .. 4 g + 3) for each of its six moduli: one 32-bit store per modulus.
-
-__device__ __forceinline__ void mma_s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
-      : "r"(a0), "r"(a1), "r"(b0));
-}
-
-// integer limbs of round(x 2^s) (limbs2's steps on one value): li[j] as ints
-// read off the magic-rounded floats' bits; returns true when inexact
-__device__ __forceinline__ bool limbs_int(float x, float sa, float sb, int (&li)[6]) {
-  float r = __fmul_rn(__fmul_rn(x, sa), sb);
-  const bool under = r == 0.0f && x != 0.0f;
-#pragma unroll
-  for (int j = 5; j >= 0; --j) {
-    const float tm = __fmaf_rn(r, pow2f(-12 * j), kMagic);
-    r = __fmaf_rn(__fsub_rn(tm, kMagic), -pow2f(12 * j), r);
-    li[j] = __float_as_int(tm) - 0x4B400000;
-  }
-  return r != 0.0f || under;
-}
-
-// the three digit words of a limb set: (lo0, hi0, lo1, hi1), (lo2, ..), (lo4, .., hi5)
-__device__ __forceinline__ void digit_words(const int (&li)[6], uint32_t (&w)[3]) {
-  int lo[6], hi[6];
-#pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    lo[j] = ((li[j] + 128) & 255) - 128;
-    hi[j] = (li[j] - lo[j]) >> 8;
-  }
-#pragma unroll
-  for (int q = 0; q < 3; ++q)
-    w[q] = __byte_perm(__byte_perm((uint32_t)lo[2 * q], (uint32_t)hi[2 * q], 0x0040),
-                       __byte_perm((uint32_t)lo[2 * q + 1], (uint32_t)hi[2 * q + 1], 0x0040), 0x5410);
-}
-
-// B fragments (digit weights) of this lane for the three n-tiles
-__device__ __forceinline__ void weight_frags(int lane, uint32_t (&b)[3]) {
-  const int g = lane >> 2, tq = lane & 3;
-#pragma unroll
-  for (int nt = 0; nt < 3; ++nt) b[nt] = *reinterpret_cast<const uint32_t*>(&c_coef8[8 * nt + g][4 * tq]);
-}
-
-// residue bits (kMagic + r) of an exact int32 sum S (|S| < 2^22) modulo m
-__device__ __forceinline__ uint32_t mod_s(int S, float m, float inv) {
-  const float sm = __int_as_float(S + 0x4B400000);
-  const float q = __fsub_rn(__fmaf_rn(__fsub_rn(sm, kMagic), inv, kMagic), kMagic);
-  return __float_as_uint(__fmaf_rn(-q, m, sm));
-}
-
-// One group of 32 elements of a warp: the staged digit words of elements
-// e = 0..31 at sw[e * 5 + q] (stride 5: conflict-free fragment reads) ->
-// for each modulus t < nmod held by this lane (t = 8 nt + 2 tq + c) the word of
-// residue bytes of elements 4 g .. 4 g + 3, handed to emit(t, word).
-template <class Emit>
-__device__ __forceinline__ void mma_residues(const uint32_t* sw, int lane, const uint32_t (&bw)[3], int nmod,
-                                             Emit emit) {
-  const int g = lane >> 2, tq = lane & 3;
-  int acc[2][3][4];
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    const uint32_t a0 = tq < 3 ? sw[(4 * g + 2 * mt) * 5 + tq] : 0u;
-    const uint32_t a1 = tq < 3 ? sw[(4 * g + 2 * mt + 1) * 5 + tq] : 0u;
-#pragma unroll
-    for (int nt = 0; nt < 3; ++nt) {
-      acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0;
-      mma_s8(acc[mt][nt], a0, a1, bw[nt]);
-    }
-  }
-#pragma unroll
-  for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int t = 8 * nt + 2 * tq + c;
-      if (t >= nmod) continue;
-      const float m = c_mod[t], inv = c_inv[t];
-      // elements 4g (mt 0 row g), 4g+1 (mt 0 row g+8), 4g+2, 4g+3 (mt 1)
-      emit(t, pack4(mod_s(acc[0][nt][c], m, inv), mod_s(acc[0][nt][2 + c], m, inv), mod_s(acc[1][nt][c], m, inv),
-                    mod_s(acc[1][nt][2 + c], m, inv)));
-    }
-}
-
-// A (rows x k, NC comps) -> residue planes [t][i][kp] on the tensor cores: a
-// warp per 32 consecutive k of a row (lane = element), eight warps per CTA,
-// rows strided over y
-template <int NC>
-__global__ void __launch_bounds__(256) k_res_rows_mma(const float* __restrict__ a, int64_t rows, int64_t k,
-                                                      int64_t kp, int pa, int nmod, const int* __restrict__ e,
-                                                      int8_t* __restrict__ out) {
-  __shared__ uint32_t sw_all[8][32 * 5];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* sw = sw_all[warp];
-  const int64_t k0 = ((int64_t)blockIdx.x * 8 + warp) * 32;
-  if (k0 >= kp) return;
-  uint32_t bw[3];
-  weight_frags(lane, bw);
-  const int64_t plane = rows * kp;
-  const int g = lane >> 2;
-  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
-    float sa, sb;
-    scale_pair(pa, e[i], sa, sb);
-    const int64_t kk = k0 + lane;
-    float c[NC];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) c[q] = kk < k ? __ldg(a + (i * k + kk) * NC + q) : 0.0f;
-    bool fin = true;
-#pragma unroll
-    for (int q = 0; q < NC; ++q) fin = fin && isfinite(c[q]);
-    int li[6];
-    limbs_int(fin ? c[0] : 0.0f, sa, sb, li);
-    if constexpr (NC == 2) {
-      int l2[6];
-      limbs_int(fin ? c[1] : 0.0f, sa, sb, l2);
-#pragma unroll
-      for (int j = 0; j < 6; ++j) li[j] += l2[j];
-    }
-    uint32_t wd[3];
-    digit_words(li, wd);
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 3; ++q) sw[lane * 5 + q] = wd[q];
-    __syncwarp();
-    int8_t* o = out + i * kp + k0 + 4 * g;
-    mma_residues(sw, lane, bw, nmod,
-                 [&](int t, uint32_t word) { *reinterpret_cast<uint32_t*>(o + t * plane) = word; });
-  }
-}
-
-// B (k x n, NC comps) -> residue planes [t][j][kp] (K contiguous per column) on
-// the tensor cores: a warp per 4 k x 32 columns (lane = column: coalesced
-// loads), four 32-element groups (columns 8 p .. 8 p + 7, p = 0..3, each with
-// its 4 k); the transposed binary32 copy bt and the inexact counts as in
-// k_res_cols.  CTA = eight warps = 32 k x 32 columns.
-template <int NC>
-__global__ void __launch_bounds__(256) k_res_cols_mma(const float* __restrict__ b, int64_t n, int64_t ldb, int64_t k,
-                                                      int64_t kp, int pb, int nmod, const int* __restrict__ e,
-                                                      int8_t* __restrict__ out, int64_t np, float* __restrict__ bt,
-                                                      int* __restrict__ cinx) {
-  __shared__ uint32_t sw_all[8][4][32 * 5];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32 + warp * 4;
-  const int64_t j = j0 + lane;
-  uint32_t bw[3];
-  weight_frags(lane, bw);
-  float sa = 1.0f, sb = 1.0f;
-  if (j < n) scale_pair(pb, e[j], sa, sb);
-  int inexact = 0;
-  float keep[4][NC];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t gk = k0 + u;
-    float c[NC];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) c[q] = (gk < k && j < n) ? b[(gk * ldb + j) * NC + q] : 0.0f;
-    bool fin = true;
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      keep[u][q] = c[q];
-      fin = fin && isfinite(c[q]);
-    }
-    int li[6];
-    inexact += limbs_int(fin ? c[0] : 0.0f, sa, sb, li);
-    if constexpr (NC == 2) {
-      int l2[6];
-      inexact += limbs_int(fin ? c[1] : 0.0f, sa, sb, l2);
-#pragma unroll
-      for (int jj = 0; jj < 6; ++jj) li[jj] += l2[jj];
-    }
-    uint32_t wd[3];
-    digit_words(li, wd);
-    // group p = lane / 8 holds columns 8 p .. 8 p + 7; element = 4 (lane % 8) + u
-    uint32_t* sw = sw_all[warp][lane >> 3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) sw[(4 * (lane & 7) + u) * 5 + q] = wd[q];
-  }
-  if (inexact && j < n) atomicAdd(cinx + j, inexact);
-  if (j < n) {  // transposed binary32 copy for the fallback
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (k0 + u < k)
-#pragma unroll
-        for (int q = 0; q < NC; ++q) bt[(j * k + k0 + u) * NC + q] = keep[u][q];
-  }
-  __syncwarp();
-  const int g = lane >> 2;
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    // group p: element 4 g + u = column j0 + 8 p + g, k0 + u
-    const int64_t jc = j0 + 8 * p + g;
-    mma_residues(sw_all[warp][p], lane, bw, nmod, [&](int t, uint32_t word) {
-      if (jc < n && k0 < kp) *reinterpret_cast<uint32_t*>(out + (t * np + jc) * kp + k0) = word;
-    });
   }
 }
 
@@ -1412,16 +1189,6 @@ int64_t pad32(int64_t v) { return (v + 31) / 32 * 32; }
 
 }  // namespace
 
-// residue kernels: limb-sum FFMA kernels by default; MCF_OZ_RES=mma selects
-// the tensor-core (mma.sync) restatement (A/B measurement)
-bool res_on_tensor_cores() {
-  static const bool v = [] {
-    const char* e = getenv("MCF_OZ_RES");
-    return e && std::string(e) == "mma";
-  }();
-  return v;
-}
-
 // Prepared B operand (a block of n columns of a k x ldb matrix): residue
 // planes, column exponents, non-finite flags and the transposed binary32
 // copy.  Built once; shared by every row chunk of A.
@@ -1483,13 +1250,8 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu);
   k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, pl.pb, ncb == 2 ? cu : nullptr, eb, cnf);
   const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
-  if (res_on_tensor_cores()) {
-    if (ncb == 2) k_res_cols_mma<2><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, pl.pb, pl.n, eb, planes, np, bt, cinx);
-    else k_res_cols_mma<1><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, pl.pb, pl.n, eb, planes, np, bt, cinx);
-  } else {
-    OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
-                   else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
-  }
+  OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
+                 else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
   for (int i = 0; i < 3; ++i) mcfr::note_launch();
   pb = PreparedB{planes, bt, eb, cnf, ncb == 1 ? cinx : nullptr, k, kp, n, np, ncb, pl};
   return mcfr::check_launch("mm_fast B residue kernels");
@@ -1537,18 +1299,10 @@ mcf_status a_residues(const float* x, int nca, int64_t m, int64_t k, const CrtPl
   const unsigned gr = (unsigned)((m + 7) / 8);
   if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
   else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
-  if (res_on_tensor_cores()) {
-    const int64_t gx = (kp + 255) / 256;  // eight warps x 32 k per CTA, rows strided over y
-    const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
-    if (nca == 2) k_res_rows_mma<2><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, pl.n, w.ea, w.planes);
-    else k_res_rows_mma<1><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, pl.n, w.ea, w.planes);
-  } else {
-    const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
-    const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
-    OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
-                   else k_res_rows<1, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes));
-  }
-  mcfr::note_launch();
+  const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
+  const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
+  OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
+                 else k_res_rows<1, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes));  mcfr::note_launch();
   mcfr::note_launch();
   return mcfr::check_launch("mm_fast A residue kernels");
 }
