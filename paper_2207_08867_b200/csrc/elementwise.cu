@@ -19,6 +19,7 @@
 #include "mcf_exp.cuh"
 #include "mcf_fast.cuh"
 #include "mcf_g2.cuh"
+#include "mcf_w2.cuh"
 #include "mcf_lit.cuh"
 #include "mcf_prec.cuh"
 #include "mcf_runtime.h"
@@ -102,8 +103,13 @@ constexpr bool kG2 = std::is_same<P, PB32>::value && NC == 2 && ONC == 2 &&
 // (measured on B200, 2^24 config-0 elements: Mul-MCN's chained divisions
 // need 79 registers packed, one ring per SM, 294 us against 275 us scalar at
 // two rings, so it stays scalar)
+// the division-based ones first try the wide tier (mcf_w2.cuh: the long
+// division carried in binary64, one element at a time)
 template <int OP, class P, int NC, int ONC>
-constexpr bool kG2Pair = kG2<OP, P, NC, ONC> && OP != kExp && OP != kMul;
+constexpr bool kW2 = kG2<OP, P, NC, ONC> && (OP == kDiv || OP == kDivN || OP == kMul);
+
+template <int OP, class P, int NC, int ONC>
+constexpr bool kG2Pair = kG2<OP, P, NC, ONC> && OP != kExp && !kW2<OP, P, NC, ONC>;
 
 // two binary32 nc = 2 elements (x = e0c0 e0c1 e1c0 e1c1, v = v0 v1) through the
 // packed certified shortcut; returns which were accepted
@@ -130,6 +136,21 @@ __device__ __forceinline__ g2::M2 run_g2_pair(const float (&x)[4], const float (
 template <int OP, class P, int NC, int ONC, bool TRY_G2 = true>
 __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[NC], RT<P> v,
                                          RT<P> (&o)[ONC]) {
+  if constexpr (TRY_G2 && kW2<OP, P, NC, ONC>) {
+    using V = w2::VD;
+    bool ok;
+    if constexpr (OP == kDivN) {  // x holds the divisor
+      ok = w2::div<V, true>(v, 0.0f, x[0], x[1], true, __fadd_rn(x[0], x[1]) == x[0], o[0], o[1]);
+    } else {
+      const bool cx = __fadd_rn(x[0], x[1]) == x[0], cy = __fadd_rn(y[0], y[1]) == y[0];
+      if constexpr (OP == kDiv) ok = w2::div<V, false>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
+      else {
+        ok = w2::mul<V>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
+        if (__fadd_rn(y[1], y[0]) == 0.0f || __fadd_rn(x[1], x[0]) == 0.0f) o[0] = o[1] = 0.0f, ok = true;
+      }
+    }
+    if (__builtin_expect(ok, 1)) return true;
+  }
   if constexpr (TRY_G2 && kG2<OP, P, NC, ONC>) {
     using Q = g2::QF32;
     bool ok;

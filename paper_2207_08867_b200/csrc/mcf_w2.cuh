@@ -1,0 +1,255 @@
+// mcf_w2.cuh -- certified nc = 2 long division in a WIDE format (binary32
+// components carried in binary64): Div-MCN, DivN and Mul-MCN (fast) of
+// mc_ops.hpp:188-230 with every exact intermediate held in one wide value.
+//
+// Formats.  P = significand bits of the component format (24), W = those of
+// the wide format (53 = 2 P + 5).  A wide value is "P-bit" when it is a
+// component value.  rnp(t) rounds a wide t to P bits, nearest-even.
+//
+// What the reference computes (div_kernel, nc = 2; x, y compressed pairs, all
+// renormalizations ending compressed -- tools/g2_verify.cpp checks that they
+// do on these term sets -- and no component under- or overflowing):
+//   r = x;  for d = 0, 1:  q_d = fl(r_0 / y_0)
+//                          (s_0, s_1) = first two components of the compressed
+//                                       expansion of q_d (y_0 + y_1)    [scale_raw + renorm]
+//                          r = first two components of the compressed
+//                              expansion of r - s_0 - s_1               [add_kernel]
+//   q_2 = fl(r_0 / y_0);  out = first two components of q_0 + q_1 + q_2.
+// renorm_kernel only applies error-free two_sums and drops zeros, so each of
+// these expansions sums EXACTLY to the value named.  Two facts identify the
+// first two components of the compressed expansion (c_0, c_1, ...) of an
+// exactly known S (mcf_g2.cuh's argument, restated on wide values):
+//   (M) margin: with A = rnp(S), if |S - A| < h (1 - 2^-(P-2)), h = half the gap
+//       from A to its neighbour on S's side, then c_0 = A; an exact tie (|S - A|
+//       = h with S exact) gives the even neighbour, which rnp returns.  On a
+//       wide S this is a test on the low W - P bits L of S's own significand:
+//       |L - 2^(W-P-1)| > 2^(W-2P+1) = 64 units (a value just below a power of
+//       two lies in the lower binade, whose finer grid makes the test
+//       conservative); one more unit covers a wide S known to half a unit.
+//   (U) uniqueness: if S fits 2 P bits (the low W - 2P bits of its wide
+//       significand are zero) then (rnp(S), S - rnp(S)) is its ONLY compressed
+//       expansion: another one needs c_0 = the other neighbour, |c_1| = h and
+//       a c_2 of 2^-P h beyond it, i.e. more than 2 P bits.  No margin needed.
+// Exactness of the wide arithmetic: the product q Y (P x W bits) is ph + pl
+// (one multiply, one fma); t = (ph - rnp(ph)) + pl spans at most W bits, so it
+// is exact; r - s_0 is exact (Sterbenz: s_0 is within 2^-(P-2) of r); the one
+// sum that can fail to fit, (r - s_0) - s_1, is verified by recomputing both
+// operands from the result (exact iff both come back).  Quotient digits are
+// rnp(r_0 rY) with rY = 1 / y_0 to 2^-(W-3) (verified by its residual): the
+// true quotient of two P-bit values is never a P-bit midpoint, so 16 units of
+// margin certify the digit.
+// Anything else -- a failed test, operands outside a +-2^40 window (so that
+// nothing over- or underflows: the reference's products must have exact low
+// parts, |q y| >= 2^-100, and its digits must be normal), non-compressed or
+// non-finite operands -- returns false and the caller falls back to the
+// binary32 tier (mcf_g2.cuh), then the register and literal paths.
+//
+// Policy V: N (component type), W (wide type), wide(N), narrow(W) (exact on
+// P-bit values), add/sub/mul/fma/neg/abs on W, rcp_seed(W) (any approximation
+// of 1/y good to ~2^-16), rnp(W), away(W, m) (|L - mid| > m), tie(W) (L ==
+// mid), span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
+// rnpe (nearest-even), in_window / below_window on N, kP.
+#pragma once
+
+#include "mcf_g2.cuh"
+
+namespace mcfg {
+namespace w2 {
+
+template <class V>
+using W_ = typename V::W;
+template <class V>
+using N_ = typename V::N;
+
+// 1 / y0 to within 2^-(W-3) relative (checked), from a seed good to 2^-16
+template <class V>
+G2_HD bool recip(W_<V> y0, W_<V> seed, W_<V>& r) {
+  const W_<V> one = V::c(1.0);
+  W_<V> e = V::fma(V::neg(y0), seed, one);
+  r = V::fma(seed, e, seed);
+  e = V::fma(V::neg(y0), r, one);
+  r = V::fma(r, e, r);
+  e = V::fma(V::neg(y0), r, one);
+  return V::le(V::abs(e), V::tol_rcp());
+}
+
+// one digit of the long division: q = fl(r0 / y0), r <- r - trunc2(q (y0 + y1)).
+// PAIR = false: Y = y0 + y1 is one wide value (Y1 unused) and the product's
+// remainder t below s0 is exact.
+// PAIR = true: the divisor stays a pair (y0 + y1 need not fit the wide
+// format: Mul-MCN's reciprocal); q y0 and q y1 are exact wide products, their
+// sum is (ph, pl) by a fast two-sum (|y1| <= 2^-P |y0|), and t is known to
+// half a unit.  Either way 64 units of margin (strictly more: 65) certify s1.
+template <class V, bool PAIR>
+G2_HD bool digit(W_<V>& r, W_<V>& r0, W_<V> Y, W_<V> Y1, W_<V> rY, W_<V>& q) {
+  using W = W_<V>;
+  const W qt = V::mul(r0, rY);
+  q = V::rnp(qt);
+  bool ok = V::away(qt, 16);
+  W ph, pl;
+  if constexpr (PAIR) {
+    const W p0 = V::mul(q, Y), p1 = V::mul(q, Y1);  // exact (P x P bits)
+    ph = V::add(p0, p1);
+    pl = V::sub(p1, V::sub(ph, p0));               // exact (Dekker)
+  } else {
+    ph = V::mul(q, Y);
+    pl = V::fma(q, Y, V::neg(ph));                 // q Y = ph + pl exactly
+  }
+  const W s0 = V::rnp(ph);
+  ok &= V::away(ph, 64);                      // (M), |pl| <= half a unit
+  const W t = V::add(V::sub(ph, s0), pl);     // q (y0 + y1) - s0 (exact unless PAIR: then to half a unit)
+  const W s1 = V::rnp(t);
+  ok &= V::away(t, 64);                       // (M) below s0 (a tie is declined)
+  const W u = V::sub(r, s0);                  // exact (Sterbenz); |u| <= 2^-(P-2) |r0| (1 + 2^-(P-3))
+  const W v = V::sub(u, s1);
+  // v is exact when s1's last place is within W bits of v's first:
+  // |v| < 2^-(P-4) |r0| and u is a multiple of r's last place, so it is when
+  // |s1| >= 2^-2P |r0| (or s1 = 0)
+  ok &= V::ge(V::abs(s1), V::mul(V::abs(r0), V::two(-2 * V::kP))) | V::eq(s1, V::c(0.0));
+  ok &= V::span2p(v);                         // (U): (rnpe(v), v - rnpe(v)) is the new remainder
+  r = v;
+  r0 = V::rnpe(v);
+  return ok;
+}
+
+// x / y for wide X = x0 + x1 (x0 = X0 its lead) and the divisor as digit()
+// takes it; Yl = the last nonzero component of y.  Results are P-bit wide values.
+template <class V, bool PAIR>
+G2_HD bool div_core(W_<V> X, W_<V> X0, W_<V> Y, W_<V> Y1, W_<V> Yl, W_<V> rY, W_<V>& o0, W_<V>& o1) {
+  using W = W_<V>;
+  W r = X, r0 = X0, q0, q1;
+  bool ok = digit<V, PAIR>(r, r0, Y, Y1, rY, q0);
+  ok &= digit<V, PAIR>(r, r0, Y, Y1, rY, q1);
+  const W qt = V::mul(r0, rY);
+  const W q2 = V::rnp(qt);
+  ok &= V::away(qt, 16);
+  // out = first two components of S = q0 + q1 + q2.  u = fl(q1 + q2) and
+  // Q = fl(q0 + u) are within 0.51 units of Q's last place of S; with
+  // a = q0 - o0 (exact: zero or a step or two of q0's grid), a + q1 is exact
+  // (a != 0 needs |q1 + q2| >= h(q0) (1 - 2^-20), so with |q2| <= |q1| both
+  // are multiples of 2^-(2P+2) |q0| below 8 steps) and w = fl((a + q1) + q2)
+  // is within half a unit of S - o0.
+  ok &= V::ge(V::abs(q1), V::abs(q2));
+  const W Q = V::add(q0, V::add(q1, q2));
+  o0 = V::rnp(Q);
+  ok &= V::away(Q, 64);
+  const W w = V::add(V::add(V::sub(q0, o0), q1), q2);
+  o1 = V::rnp(w);
+  ok &= V::away(w, 64);
+  // range guards (the reference's arithmetic has a bounded exponent; the
+  // callers keep |y0| and |x0| inside 2^+-40): every product q_d y_j must have
+  // an exact low part and every digit must be normal.  The smallest product is
+  // (last nonzero of q0, q1) x (last nonzero of y); at 2^-86 it also makes that
+  // digit normal (|y| <= 2^40).  q2 is only ever divided out: normal or zero.
+  const W zero = V::c(0.0);
+  const W ql = V::eq(q1, zero) ? q0 : q1;
+  ok &= V::ge(V::abs(V::mul(ql, Yl)), V::two(-86)) | V::eq(q0, zero);
+  ok &= V::eq(q2, zero) | V::ge(V::abs(q2), V::two(-126));
+  return ok;
+}
+
+
+// mc_ops.hpp:188-207 div_kernel, nc = 2; cx / cy = the reference's compressed
+// predicate fl(c0 + c1) == c0 evaluated by the caller in the component format
+template <class V, bool X1ZERO>
+G2_HD bool div(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& o0, N_<V>& o1) {
+  using W = W_<V>;
+  const W zero = V::c(0.0);
+  const W X0 = V::wide(x0), Y0 = V::wide(y0), Y1 = V::wide(y1);
+  W X = X0;
+  bool ok = cx & cy;
+  if constexpr (!X1ZERO) {
+    const W X1 = V::wide(x1);
+    X = V::add(X0, X1);
+    ok &= V::eq(V::sub(X, X0), X1);           // x0 + x1 fits the wide format
+  }
+  const W Y = V::add(Y0, Y1);
+  ok &= V::eq(V::sub(Y, Y0), Y1);
+  ok &= V::in_window(y0) & V::below_window(x0);  // a tiny x0 fails the product guard of div_core
+  W rY;
+  ok &= recip<V>(Y0, V::rcp_seed(Y0), rY);
+  const W Yl = V::eq(Y1, zero) ? Y0 : Y1;
+  W w0, w1;
+  ok &= div_core<V, false>(X, X0, Y, Y1, Yl, rY, w0, w1);
+  o0 = V::canon(V::narrow(w0));
+  o1 = V::canon(V::narrow(w1));
+  return ok;
+}
+
+// mc_ops.hpp:216-230 Mul-MCN (fast): x / (1 / y), zero fast path decided by
+// the caller (zx / zy: approx(x) == 0, approx(y) == 0)
+template <class V>
+G2_HD bool mul(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& o0, N_<V>& o1) {
+  using W = W_<V>;
+  const W zero = V::c(0.0), one = V::c(1.0);
+  const W X0 = V::wide(x0), X1 = V::wide(x1), Y0 = V::wide(y0), Y1 = V::wide(y1);
+  const W X = V::add(X0, X1), Y = V::add(Y0, Y1);
+  bool ok = cx & cy & V::eq(V::sub(X, X0), X1) & V::eq(V::sub(Y, Y0), Y1);
+  ok &= V::in_window(y0) & V::below_window(x0);  // a tiny x0 fails the product guard of div_core
+  W rY;
+  ok &= recip<V>(Y0, V::rcp_seed(Y0), rY);
+  const W Yl = V::eq(Y1, zero) ? Y0 : Y1;
+  W c0, c1;
+  ok &= div_core<V, false>(one, one, Y, Y1, Yl, rY, c0, c1);  // recip = 1 / y (compressed by construction)
+  W rC;
+  ok &= recip<V>(c0, Y0, rC);                           // 1 / c0 ~ y0 (to 2^-(P-1)): seed y0
+  const W Cl = V::eq(c1, zero) ? c0 : c1;
+  W w0, w1;
+  ok &= div_core<V, true>(X, X0, c0, c1, Cl, rC, w0, w1);
+  o0 = V::canon(V::narrow(w0));
+  o1 = V::canon(V::narrow(w1));
+  return ok;
+}
+
+#if defined(__CUDACC__)
+// binary32 components in binary64 on sm_100a
+struct VD {
+  using N = float;
+  using W = double;
+  __device__ __forceinline__ static W c(double v) { return v; }
+  __device__ __forceinline__ static W two(int k) { return __hiloint2double((1023 + k) << 20, 0); }
+  __device__ __forceinline__ static W tol_rcp() { return 0x1p-50; }
+  __device__ __forceinline__ static W wide(N x) { return (double)x; }
+  __device__ __forceinline__ static N narrow(W x) { return __double2float_rn(x); }
+  __device__ __forceinline__ static N canon(N x) { return __fadd_rn(x, 0.0f); }
+  __device__ __forceinline__ static W neg(W a) { return -a; }
+  __device__ __forceinline__ static W abs(W a) { return fabs(a); }
+  __device__ __forceinline__ static W add(W a, W b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static W sub(W a, W b) { return __dsub_rn(a, b); }
+  __device__ __forceinline__ static W mul(W a, W b) { return __dmul_rn(a, b); }
+  __device__ __forceinline__ static W fma(W a, W b, W c) { return __fma_rn(a, b, c); }
+  __device__ __forceinline__ static bool eq(W a, W b) { return a == b; }
+  __device__ __forceinline__ static bool ge(W a, W b) { return a >= b; }
+  __device__ __forceinline__ static bool le(W a, W b) { return a <= b; }
+  // MUFU.RCP64H: ~20 bits from the high word
+  __device__ __forceinline__ static W rcp_seed(W y) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    return r;
+  }
+  static constexpr int kP = 24;
+  __device__ __forceinline__ static bool in_window(N a) { return (fabsf(a) >= 0x1p-40f) & (fabsf(a) <= 0x1p40f); }
+  __device__ __forceinline__ static bool below_window(N a) { return fabsf(a) <= 0x1p40f; }
+  // round to 24 bits on the bit pattern (sign-magnitude: add half a step to
+  // the magnitude, clear the 29 low bits; a carry runs into the exponent as
+  // it should).  rnp: ties away from zero (every use declines near-ties);
+  // rnpe: ties to even.
+  __device__ __forceinline__ static W rnp(W t) {
+    return __longlong_as_double((__double_as_longlong(t) + 0x10000000LL) & ~0x1fffffffLL);
+  }
+  __device__ __forceinline__ static W rnpe(W t) {
+    const long long b = __double_as_longlong(t);
+    return __longlong_as_double((b + 0x0fffffffLL + ((b >> 29) & 1LL)) & ~0x1fffffffLL);
+  }
+  // low 29 significand bits against the midpoint 2^28: (L - (2^28 - m)) > 2 m
+  // on the low word shifted up by 3 (which drops the three bits above L)
+  __device__ __forceinline__ static bool away(W t, int m) {
+    const unsigned l8 = (unsigned)__double2loint(t) << 3;
+    return l8 - ((0x10000000u - (unsigned)m) << 3) > (2u * (unsigned)m << 3);
+  }
+  __device__ __forceinline__ static bool span2p(W t) { return ((unsigned)__double2loint(t) & 0x1fu) == 0u; }
+};
+#endif
+
+}  // namespace w2
+}  // namespace mcfg

@@ -23,6 +23,7 @@
 #include <omp.h>
 
 #include "../paper_2207_08867_b200/csrc/mcf_g2.cuh"
+#include "../paper_2207_08867_b200/csrc/mcf_w2.cuh"
 
 static int P = 24;  // significand bits of the emulated format
 
@@ -66,6 +67,58 @@ struct QE {
   }
   static T ulpb(T w) { return std::fabs(w) * std::ldexp(1.0, -P); }
   static T shrink(T h) { return rn(h * (1.0 - std::ldexp(1.0, -(P - 2)))); }
+};
+
+// wide format of the mcf_w2.cuh tier: 2 P + 5 significand bits (53 for P = 24,
+// where the emulation is the host's own binary64 arithmetic)
+static int WB() { return 2 * P + 5; }
+static double rnw(double x) {
+  if (WB() >= 53 || x == 0 || !std::isfinite(x)) return x;
+  int e;
+  const double m = std::frexp(x, &e);
+  return std::ldexp(std::nearbyint(std::ldexp(m, WB())), e - WB());
+}
+static uint64_t wmant(double t) {  // the W-bit significand of a wide value as an integer
+  if (t == 0) return 0;
+  int e;
+  return (uint64_t)std::ldexp(std::frexp(std::fabs(t), &e), WB());
+}
+struct VE {
+  using N = double;
+  using W = double;
+  static W c(double v) { return v; }
+  static W two(int k) { return std::ldexp(1.0, k); }
+  static W tol_rcp() { return std::ldexp(1.0, -(WB() - 3)); }
+  static W wide(N x) { return x; }
+  static N narrow(W x) { return x; }
+  static N canon(N x) { return x + 0.0; }
+  static W neg(W a) { return -a; }
+  static W abs(W a) { return std::fabs(a); }
+  static W add(W a, W b) { return rnw(a + b); }
+  static W sub(W a, W b) { return rnw(a - b); }
+  static W mul(W a, W b) { return rnw(a * b); }
+  static W fma(W a, W b, W c) { return WB() >= 53 ? std::fma(a, b, c) : rnw(a * b + c); }
+  static bool eq(W a, W b) { return a == b; }
+  static bool ge(W a, W b) { return a >= b; }
+  static bool le(W a, W b) { return a <= b; }
+  static W rcp_seed(W y) { return rnw((1.0 / y) * (1.0 + std::ldexp(1.0, -16))); }
+  static constexpr int kP_dummy = 0;
+  struct KP { operator int() const { return P; } };
+  static constexpr KP kP{};
+  static bool in_window(N a) { return std::fabs(a) >= std::ldexp(1.0, -40) && std::fabs(a) <= std::ldexp(1.0, 40); }
+  static bool below_window(N a) { return std::fabs(a) <= std::ldexp(1.0, 40); }
+  static W rnpe(W t) { return rn(t); }
+  static W rnp(W t) {  // ties away from zero, as the device's pattern rounding
+    if (t == 0 || !std::isfinite(t)) return t;
+    int e;
+    const double m = std::frexp(std::fabs(t), &e);
+    return std::copysign(std::ldexp(std::floor(std::ldexp(m, P) + 0.5), e - P), t);
+  }
+  static bool away(W t, int m) {
+    const int64_t L = (int64_t)(wmant(t) & ((1ull << (WB() - P)) - 1)), mid = 1ll << (WB() - P - 1);
+    return std::llabs(L - mid) > m;
+  }
+  static bool span2p(W t) { return (wmant(t) & ((1ull << (WB() - 2 * P)) - 1)) == 0; }
 };
 
 // ---- the reference, restated generically (mc_ops.hpp) ----------------------
@@ -268,7 +321,7 @@ int main(int argc, char** argv) {
     auto X = pairs(K, 1);
     const int M = 1 << (P - 1);
     printf("p=%d: %zu compressed pairs\n", P, X.size());
-    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"};
+    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"};
 #pragma omp parallel for schedule(dynamic, 16)
     for (long long i = 0; i < (long long)X.size(); ++i) {
       const double x[2] = {X[i].first, X[i].second};
@@ -278,6 +331,8 @@ int main(int argc, char** argv) {
         const double vn[2] = {std::ldexp(M + a, -(P - 1)), 0.0};
         check(sd, [&](double* o) { ref_div(vn, x, o); },
               [&](double* o) { return g2::div<QE, true>(vn[0], vn[1], x[0], x[1], o[0], o[1]); }, "divn");
+        check(wd, [&](double* o) { ref_div(vn, x, o); },
+              [&](double* o) { return w2::div<VE, true>(vn[0], vn[1], x[0], x[1], true, true, o[0], o[1]); }, "divn");
       }
       for (int s = -1; s <= 1; s += 2)
         for (int a = 0; a < M; ++a) {
@@ -294,24 +349,29 @@ int main(int argc, char** argv) {
         const double y[2] = {X[j].first, X[j].second};
         check(sd, [&](double* o) { ref_div(x, y, o); },
               [&](double* o) { return g2::div<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "div");
+        check(wd, [&](double* o) { ref_div(x, y, o); },
+              [&](double* o) { return w2::div<VE, false>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
         for (int sh = -3; sh <= 3; sh += 3) {  // relative exponent of y
           const double ys[2] = {std::ldexp(y[0], sh), std::ldexp(y[1], sh)};
           check(sa, [&](double* o) { ref_add(x, ys, o); },
                 [&](double* o) { return g2::add<QE>(x[0], x[1], ys[0], ys[1], o[0], o[1]); }, "add");
         }
-        if ((i + j) % 3 == 0)
+        if ((i + j) % 3 == 0) {
           check(sm, [&](double* o) { ref_mul(x, y, o); },
                 [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
+          check(wm, [&](double* o) { ref_mul(x, y, o); },
+                [&](double* o) { return w2::mul<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
+        }
       }
     }
-    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg);
-    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap |
-            sg.cap) ? 1 : 0;
+    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm);
+    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+            sa.cap | sg.cap) ? 1 : 0;
   }
   // sampled, config-0 style operands: v = U(-1,1) 2^U(-8,8) split greedily into p-bit comps
   P = argc > 2 ? atoi(argv[2]) : 24;
   const long long N = argc > 3 ? atoll(argv[3]) : 2000000;
-  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"};
+  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"};
 #pragma omp parallel
   {
     std::mt19937_64 g(1234 + 7919 * (unsigned long long)omp_get_thread_num());
@@ -338,6 +398,12 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::div<QE, true>(vv[0], vv[1], y[0], y[1], o[0], o[1]); }, "divn");
       check(sm, [&](double* o) { ref_mul(x, y, o); },
             [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
+      check(wd, [&](double* o) { ref_div(x, y, o); },
+            [&](double* o) { return w2::div<VE, false>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
+      check(wd, [&](double* o) { ref_div(vv, y, o); },
+            [&](double* o) { return w2::div<VE, true>(vv[0], vv[1], y[0], y[1], true, true, o[0], o[1]); }, "divn");
+      check(wm, [&](double* o) { ref_mul(x, y, o); },
+            [&](double* o) { return w2::mul<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
       check(sa, [&](double* o) { ref_add(x, y, o); },
             [&](double* o) { return g2::add<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "add");
       check(sg, [&](double* o) { ref_grow(x, v, o); },
@@ -347,7 +413,7 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::add<QE>(x[0], x[1], yn[0], yn[1], o[0], o[1]); }, "add");
     }
   }
-  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg);
-  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | ss.cap | sq.cap | sd.cap | sm.cap | sa.cap |
-          sg.cap) ? 1 : 0;
+  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm);
+  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+          sa.cap | sg.cap) ? 1 : 0;
 }
