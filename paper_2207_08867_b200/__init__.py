@@ -27,7 +27,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmcf_b200.so")
+LIB_PATH = os.environ.get("MCF_LIB") or os.path.join(_PKG, "libmcf_b200.so")  # MCF_LIB: an alternative build (tuning probes)
 
 B16, B32, B64 = 0, 1, 2
 SEQUENTIAL, PAIRWISE_TREE, FAST, FAST_FP64 = 0, 1, 2, 3

@@ -161,7 +161,7 @@ __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[
     else if constexpr (OP == kMul) ok = g2::mul<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kAdd) ok = g2::add<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kGrow) ok = g2::grow<Q>(x[0], x[1], v, o[0], o[1]);
-    else ok = g2::exp_b32(x[0], x[1], o[0], o[1]);
+    else ok = w2::exp_b32(x[0], x[1], o[0], o[1]);
     if (__builtin_expect(ok, 1)) return true;
   }
   if constexpr (OP == kGrow) return fast::grow<P, NC>(x, v, o);
@@ -352,6 +352,12 @@ namespace tma {
 constexpr int kConsumerWarps = 16;
 constexpr int kCtasPerSm = 2;  // two rings per SM: 32 consumer warps hide FP latency
 constexpr int kSmemBudget = 100 * 1024;
+#ifndef MCF_W2_CTAS
+#define MCF_W2_CTAS 2
+#endif
+// rings per SM an operator is compiled for (the wide-tier ops are set below)
+template <int OP>
+constexpr int kCtasFor = (OP == kDiv || OP == kDivN || OP == kMul) ? MCF_W2_CTAS : kCtasPerSm;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -399,7 +405,7 @@ struct Geo {
   static constexpr int kYBytes = kY ? kXBytes : 0;
   static constexpr int kVBytes = kV ? kTile * (int)sizeof(typename P::st) : 0;
   static constexpr int kStageBytes = kXBytes + kYBytes + kVBytes;
-  static constexpr int kFit = kSmemBudget / kStageBytes;
+  static constexpr int kFit = (kCtasFor<OP> > 2 ? 72 * 1024 : kSmemBudget) / kStageBytes;
   static constexpr int kStages = kFit >= 8 ? 8 : (kFit >= 4 ? 4 : 2);  // power of two: cheap ring index
   static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
@@ -409,7 +415,7 @@ struct Geo {
 // the packed certified ops need the registers of one ring per SM: at two
 // rings (56 registers) ptxas splits FADD2 / FMUL2 / FFMA2 back into scalars
 template <int OP, class P, int NC, int ONC>
-constexpr int kTmaCtas = kG2Pair<OP, P, NC, ONC> ? 1 : tma::kCtasPerSm;
+constexpr int kTmaCtas = kG2Pair<OP, P, NC, ONC> ? 1 : kW2<OP, P, NC, ONC> ? MCF_W2_CTAS : tma::kCtasPerSm;
 
 // vmode here is 0 (v per element) or 1 (scalar v); `tiles` full tiles only
 template <int OP, class P, int NC, int ONC>
@@ -671,7 +677,9 @@ mcf_status launch_fast(const Args& a) {
     // two rings per SM, except packed ScalingN and Grow-ExpN (measured 59 us
     // at one ring, 66 us at two): the packed ops are compiled for one ring (so
     // ptxas keeps FADD2 / FMUL2 / FFMA2) and fit two at their register counts
-    const int64_t slots = (int64_t)mcfr::sm_count() * (kG2Pair<OP, P, NC, ONC> && (OP == kScale || OP == kGrow) ? 1 : tma::kCtasPerSm);
+    const int64_t slots = (int64_t)mcfr::sm_count() * (kG2Pair<OP, P, NC, ONC> && (OP == kScale || OP == kGrow) ? 1
+                                                        : kW2<OP, P, NC, ONC>                                  ? MCF_W2_CTAS
+                                                                                                               : tma::kCtasPerSm);
     const int grid = (int)(tiles < slots ? tiles : slots);
     kt<<<grid, tma::kConsumerWarps * 32 + 32, G::kSmem, a.stream>>>(x, y, v, vmode, out, tiles);
     mcfr::note_launch();

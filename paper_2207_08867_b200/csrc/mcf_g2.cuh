@@ -358,42 +358,6 @@ struct QF32x2 {
   __device__ __forceinline__ static T ulpb(T w) { return __fmul2_rn(abs(w), c(0x1p-24)); }
 };
 
-// fl_exp<B32>(x1) = RN32(exp(x1)) for a small second component (|x1| <= 2^-12):
-// exp(x1) - 1 from a degree-4 polynomial in binary64 (truncation <= 2^-67,
-// evaluation ~2^-64 absolute), then RN32, accepted only when 1 + p is farther
-// than 2^-50 from a binary32 midpoint (the double rounding through binary64
-// and the approximation then cannot change the result).
-__device__ __forceinline__ bool exp_small_b32(float x1, float& f) {
-  const double d = (double)x1;
-  double p = __fma_rn(d, 1.0 / 24.0, 1.0 / 6.0);
-  p = __fma_rn(d, p, 0.5);
-  p = __fma_rn(__dmul_rn(d, d), p, d);
-  const double s = __dadd_rn(1.0, p);
-  f = __double2float_rn(s);
-  const double h = s >= 1.0 ? 0x1p-24 : 0x1p-25;  // half the binary32 spacing at f
-  return (fabsf(x1) <= 0x1p-12f) & (fabs(__dsub_rn(s, (double)f)) < h - 0x1p-50);
-}
-
-// mc_ops.hpp:303-313 Exp-MCN, nc = 2: expansion_of_double(exp(x0)) (exact
-// greedy split of the correctly rounded binary64 exp: the short evaluation
-// of mcf_exp.cuh, certified away from binary64 midpoints), then for
-// x1 != 0 scale_kernel(out, fl_exp(x1)) through the certified scale.
-// Branch-free: both outcomes are computed and selected (x1 == 0 skips the
-// scaling in the reference; a declined element, e.g. near a binary64
-// midpoint of exp(x0), takes the register path with the correctly rounded exp).
-__device__ __forceinline__ bool exp_b32(float x0, float x1, float& o0, float& o1) {
-  double E;
-  const bool oke = rn_exp_fast((double)x0, E);
-  const float e0 = __double2float_rn(E);
-  const float e1 = __double2float_rn(__dsub_rn(E, (double)e0));
-  float f, s0, s1;
-  const bool okf = exp_small_b32(x1, f);
-  const bool oks = scale<QF32>(e0, e1, f, s0, s1);
-  const bool z = x1 == 0.0f;
-  o0 = z ? e0 : s0;
-  o1 = z ? e1 : s1;
-  return oke & (z ? (bool)isfinite(e0) : okf & oks);
-}
 #endif
 
 }  // namespace g2

@@ -46,8 +46,8 @@
 //
 // Policy V: N (component type), W (wide type), wide(N), narrow(W) (exact on
 // P-bit values), add/sub/mul/fma/neg/abs on W, rcp_seed(W) (any approximation
-// of 1/y good to ~2^-16), rnp(W), away(W, m) (|L - mid| > m), tie(W) (L ==
-// mid), span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
+// of 1/y good to ~2^-16), rnpm(W, m, ok) (rnp, and ok &= |L - mid| > m),
+// span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
 // rnpe (nearest-even), in_window / below_window on N, kP.
 #pragma once
 
@@ -84,8 +84,8 @@ template <class V, bool PAIR>
 G2_HD bool digit(W_<V>& r, W_<V>& r0, W_<V> Y, W_<V> Y1, W_<V> rY, W_<V>& q) {
   using W = W_<V>;
   const W qt = V::mul(r0, rY);
-  q = V::rnp(qt);
-  bool ok = V::away(qt, 16);
+  bool ok = true;
+  q = V::rnpm(qt, 16, ok);
   W ph, pl;
   if constexpr (PAIR) {
     const W p0 = V::mul(q, Y), p1 = V::mul(q, Y1);  // exact (P x P bits)
@@ -95,11 +95,9 @@ G2_HD bool digit(W_<V>& r, W_<V>& r0, W_<V> Y, W_<V> Y1, W_<V> rY, W_<V>& q) {
     ph = V::mul(q, Y);
     pl = V::fma(q, Y, V::neg(ph));                 // q Y = ph + pl exactly
   }
-  const W s0 = V::rnp(ph);
-  ok &= V::away(ph, 64);                      // (M), |pl| <= half a unit
+  const W s0 = V::rnpm(ph, 64, ok);           // (M), |pl| <= half a unit
   const W t = V::add(V::sub(ph, s0), pl);     // q (y0 + y1) - s0 (exact unless PAIR: then to half a unit)
-  const W s1 = V::rnp(t);
-  ok &= V::away(t, 64);                       // (M) below s0 (a tie is declined)
+  const W s1 = V::rnpm(t, 64, ok);            // (M) below s0 (a tie is declined)
   const W u = V::sub(r, s0);                  // exact (Sterbenz); |u| <= 2^-(P-2) |r0| (1 + 2^-(P-3))
   const W v = V::sub(u, s1);
   // v is exact when s1's last place is within W bits of v's first:
@@ -121,8 +119,7 @@ G2_HD bool div_core(W_<V> X, W_<V> X0, W_<V> Y, W_<V> Y1, W_<V> Yl, W_<V> rY, W_
   bool ok = digit<V, PAIR>(r, r0, Y, Y1, rY, q0);
   ok &= digit<V, PAIR>(r, r0, Y, Y1, rY, q1);
   const W qt = V::mul(r0, rY);
-  const W q2 = V::rnp(qt);
-  ok &= V::away(qt, 16);
+  const W q2 = V::rnpm(qt, 16, ok);
   // out = first two components of S = q0 + q1 + q2.  u = fl(q1 + q2) and
   // Q = fl(q0 + u) are within 0.51 units of Q's last place of S; with
   // a = q0 - o0 (exact: zero or a step or two of q0's grid), a + q1 is exact
@@ -131,11 +128,9 @@ G2_HD bool div_core(W_<V> X, W_<V> X0, W_<V> Y, W_<V> Y1, W_<V> Yl, W_<V> rY, W_
   // is within half a unit of S - o0.
   ok &= V::ge(V::abs(q1), V::abs(q2));
   const W Q = V::add(q0, V::add(q1, q2));
-  o0 = V::rnp(Q);
-  ok &= V::away(Q, 64);
+  o0 = V::rnpm(Q, 64, ok);
   const W w = V::add(V::add(V::sub(q0, o0), q1), q2);
-  o1 = V::rnp(w);
-  ok &= V::away(w, 64);
+  o1 = V::rnpm(w, 64, ok);
   // range guards (the reference's arithmetic has a bounded exponent; the
   // callers keep |y0| and |x0| inside 2^+-40): every product q_d y_j must have
   // an exact low part and every digit must be normal.  The smallest product is
@@ -201,6 +196,43 @@ G2_HD bool mul(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& 
   return ok;
 }
 
+// First two components of the compressed expansion of X F (X = x0 + x1 exact in
+// the wide format, F a P-bit value): scale_raw + renorm_kernel of
+// mc_ops.hpp:143-169 for nc = 2 -> 2.  The product is ph + pl exactly, its
+// remainder below o0 spans at most W bits (exact), (M) twice.
+template <class V>
+G2_HD bool scale_core(W_<V> X, W_<V> F, W_<V>& o0, W_<V>& o1) {
+  using W = W_<V>;
+  bool ok = true;
+  const W ph = V::mul(X, F);
+  const W pl = V::fma(X, F, V::neg(ph));
+  o0 = V::rnpm(ph, 64, ok);
+  const W t = V::add(V::sub(ph, o0), pl);
+  o1 = V::rnpm(t, 64, ok);
+  return ok;
+}
+
+// ScalingN nc = 2 -> 2 on component operands (cx = x compressed); products
+// must have exact low parts: the smaller one, |x1 v| (or |x0 v| when x1 = 0),
+// at least 2^-100, or zero because a factor is; the lead below 2^100
+template <class V>
+G2_HD bool scale(N_<V> x0, N_<V> x1, N_<V> v, bool cx, N_<V>& o0, N_<V>& o1) {
+  using W = W_<V>;
+  const W zero = V::c(0.0);
+  const W X0 = V::wide(x0), X1 = V::wide(x1), F = V::wide(v);
+  const W X = V::add(X0, X1);
+  bool ok = cx & V::eq(V::sub(X, X0), X1);
+  const W xs = V::eq(X1, zero) ? X0 : X1;
+  const W sm = V::abs(V::mul(xs, F));
+  ok &= V::ge(sm, V::two(-100)) | V::eq(sm, zero);
+  ok &= V::le(V::abs(V::mul(X0, F)), V::two(100));
+  W w0, w1;
+  ok &= scale_core<V>(X, F, w0, w1);
+  o0 = V::canon(V::narrow(w0));
+  o1 = V::canon(V::narrow(w1));
+  return ok;
+}
+
 #if defined(__CUDACC__)
 // binary32 components in binary64 on sm_100a
 struct VD {
@@ -234,21 +266,60 @@ struct VD {
   // the magnitude, clear the 29 low bits; a carry runs into the exponent as
   // it should).  rnp: ties away from zero (every use declines near-ties);
   // rnpe: ties to even.
-  __device__ __forceinline__ static W rnp(W t) {
-    return __longlong_as_double((__double_as_longlong(t) + 0x10000000LL) & ~0x1fffffffLL);
+  // round to 24 bits AND test the margin m with one 64-bit add: b' = b + half
+  // + m; (b' & ~low29) is t rounded to nearest whenever t is not within m
+  // units of a midpoint (L in [mid - m, mid) would round the wrong way -- and is
+  // declined), and t is within m units of a midpoint exactly when the low 29
+  // bits of b' are <= 2 m.
+  __device__ __forceinline__ static W rnpm(W t, int m, bool& ok) {
+    const long long b = __double_as_longlong(t) + (0x10000000LL + m);
+    ok &= ((unsigned)b << 3) > ((unsigned)(2 * m) << 3);
+    return __longlong_as_double(b & ~0x1fffffffLL);
   }
+  // ties to even: (t + M) - M with M = 1.5 2^(e + 29), e = t's exponent; the
+  // sum lies in M's binade, whose spacing 2^(e - 23) is t's 24-bit grid.  M0 =
+  // 1.5 2^e is one mask-or of t's high word; the 2^29 rides on two fmas.
   __device__ __forceinline__ static W rnpe(W t) {
-    const long long b = __double_as_longlong(t);
-    return __longlong_as_double((b + 0x0fffffffLL + ((b >> 29) & 1LL)) & ~0x1fffffffLL);
-  }
-  // low 29 significand bits against the midpoint 2^28: (L - (2^28 - m)) > 2 m
-  // on the low word shifted up by 3 (which drops the three bits above L)
-  __device__ __forceinline__ static bool away(W t, int m) {
-    const unsigned l8 = (unsigned)__double2loint(t) << 3;
-    return l8 - ((0x10000000u - (unsigned)m) << 3) > (2u * (unsigned)m << 3);
+    const double M0 = __hiloint2double((__double2hiint(t) & 0x7ff00000) | 0x00080000, 0);
+    const double s = __fma_rn(M0, 0x1p29, t);
+    return __fma_rn(M0, -0x1p29, s);
   }
   __device__ __forceinline__ static bool span2p(W t) { return ((unsigned)__double2loint(t) & 0x1fu) == 0u; }
 };
+
+// the correctly rounded exp out of line: taken by the few lanes whose short
+// evaluation cannot decide the binary64 rounding
+static __device__ __noinline__ double cr_exp_call(double x) { return cr_exp(x); }
+
+// mc_ops.hpp:303-313 Exp-MCN, nc = 2, in the wide format: the greedy split of
+// the correctly rounded binary64 exp(x0) (expansion_of_double: two
+// nearest-even roundings, no renormalization in the reference either), then
+// for x1 != 0 the scaling by f = fl_exp(x1) = RN32(exp(x1)) through
+// scale_core.  f comes from a degree-4 polynomial in binary64 (|x1| <= 2^-12:
+// truncation <= 2^-67, evaluation ~2^-64 absolute) rounded with 16 units
+// (>= 2^-50) of margin, which the double rounding through binary64 and the
+// approximation cannot cross.  Branch-free: both outcomes computed, selected.
+__device__ __forceinline__ bool exp_b32(float x0, float x1, float& o0, float& o1) {
+  using V = VD;
+  double E;
+  if (!rn_exp_fast((double)x0, E)) E = cr_exp_call((double)x0);  // near a binary64 midpoint (2^-8 of arguments)
+  bool ok = (E >= 0x1p-60) & (E <= 0x1p100);   // every component and product normal, finite
+  const double e0 = V::rnpe(E);
+  const double e1 = V::rnpe(__dsub_rn(E, e0));
+  const double d = (double)x1;
+  double p = __fma_rn(d, 1.0 / 24.0, 1.0 / 6.0);
+  p = __fma_rn(d, p, 0.5);
+  p = __fma_rn(__dmul_rn(d, d), p, d);
+  bool oks = fabsf(x1) <= 0x1p-12f;
+  const double f = V::rnpm(__dadd_rn(1.0, p), 16, oks);
+  double s0, s1;
+  oks &= scale_core<V>(__dadd_rn(e0, e1), f, s0, s1);
+  oks &= (fabs(__dmul_rn(e1, f)) >= 0x1p-100) | (e1 == 0.0);
+  const bool z = x1 == 0.0f;
+  o0 = V::canon(V::narrow(z ? e0 : s0));
+  o1 = V::canon(V::narrow(z ? e1 : s1));
+  return ok & (z | oks);
+}
 #endif
 
 }  // namespace w2

@@ -41,7 +41,7 @@ def _run(exe, *args):
         if m:
             rows[m.group(2)] = dict(cases=int(m.group(3)), acc=float(m.group(4)), bad=int(m.group(5)),
                                     cap=int(m.group(6)))
-    assert set(rows) == {"scale", "square", "div", "mul", "add", "grow", "w2div", "w2mul"}, r.stdout + r.stderr
+    assert set(rows) == {"scale", "square", "div", "mul", "add", "grow", "w2div", "w2mul", "w2scale"}, r.stdout + r.stderr
     return rows, r.returncode
 
 

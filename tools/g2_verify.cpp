@@ -114,6 +114,10 @@ struct VE {
     const double m = std::frexp(std::fabs(t), &e);
     return std::copysign(std::ldexp(std::floor(std::ldexp(m, P) + 0.5), e - P), t);
   }
+  static W rnpm(W t, int m, bool& ok) {
+    ok &= away(t, m);
+    return rnp(t);
+  }
   static bool away(W t, int m) {
     const int64_t L = (int64_t)(wmant(t) & ((1ull << (WB() - P)) - 1)), mid = 1ll << (WB() - P - 1);
     return std::llabs(L - mid) > m;
@@ -321,7 +325,7 @@ int main(int argc, char** argv) {
     auto X = pairs(K, 1);
     const int M = 1 << (P - 1);
     printf("p=%d: %zu compressed pairs\n", P, X.size());
-    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"};
+    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"};
 #pragma omp parallel for schedule(dynamic, 16)
     for (long long i = 0; i < (long long)X.size(); ++i) {
       const double x[2] = {X[i].first, X[i].second};
@@ -339,6 +343,8 @@ int main(int argc, char** argv) {
           const double v = s * std::ldexp(M + a, -(P - 1));
           check(ss, [&](double* o) { ref_scale(x, v, o); },
                 [&](double* o) { return g2::scale<QE>(x[0], x[1], v, o[0], o[1]); }, "sc");
+          check(ws, [&](double* o) { ref_scale(x, v, o); },
+                [&](double* o) { return w2::scale<VE>(x[0], x[1], v, true, o[0], o[1]); }, "sc");
           for (int sh = -(P + 3); sh <= 2; ++sh) {  // grow by values around every component
             const double vg = std::ldexp(v, sh);
             check(sg, [&](double* o) { ref_grow(x, vg, o); },
@@ -364,14 +370,14 @@ int main(int argc, char** argv) {
         }
       }
     }
-    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm);
-    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws);
+    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | ss.cap | sq.cap | sd.cap | sm.cap |
             sa.cap | sg.cap) ? 1 : 0;
   }
   // sampled, config-0 style operands: v = U(-1,1) 2^U(-8,8) split greedily into p-bit comps
   P = argc > 2 ? atoi(argv[2]) : 24;
   const long long N = argc > 3 ? atoll(argv[3]) : 2000000;
-  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"};
+  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"};
 #pragma omp parallel
   {
     std::mt19937_64 g(1234 + 7919 * (unsigned long long)omp_get_thread_num());
@@ -389,6 +395,8 @@ int main(int argc, char** argv) {
       const double v = v2[0];
       check(ss, [&](double* o) { ref_scale(x, v, o); },
             [&](double* o) { return g2::scale<QE>(x[0], x[1], v, o[0], o[1]); }, "sc");
+      check(ws, [&](double* o) { ref_scale(x, v, o); },
+            [&](double* o) { return w2::scale<VE>(x[0], x[1], v, true, o[0], o[1]); }, "sc");
       check(sq, [&](double* o) { ref_square(x, o); },
             [&](double* o) { return g2::square<QE>(x[0], x[1], o[0], o[1]); }, "sq");
       check(sd, [&](double* o) { ref_div(x, y, o); },
@@ -413,7 +421,7 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::add<QE>(x[0], x[1], yn[0], yn[1], o[0], o[1]); }, "add");
     }
   }
-  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm);
-  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws);
+  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | ss.cap | sq.cap | sd.cap | sm.cap |
           sa.cap | sg.cap) ? 1 : 0;
 }
