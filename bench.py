@@ -47,10 +47,19 @@ WORKLOAD = "config2: MC(4096x4096, nc=2, fp32) x T(4096x4096, fp32)"
 L2_NOTE = "256 MiB buffer written between timed steps"
 
 
+def grid_for(world):
+    """Output-block grid (row blocks, column blocks) of the ranks; MCF_BENCH_GRID=rows keeps plain row shards."""
+    from paper_2207_08867_b200.dist import block_grid
+
+    return (world, 1) if os.environ.get("MCF_BENCH_GRID") == "rows" else block_grid(world)
+
+
 def config_dict(world):
     """The workload description, identical in both arms."""
-    return {"workload": WORKLOAD, "M": M, "K": K, "N": N, "nc": 2,
-            "parallelism": f"output rows / {world} GPUs" if world > 1 else "1 GPU", "l2": L2_NOTE}
+    gr, gc = grid_for(world)
+    par = "1 GPU" if world == 1 else (f"output rows / {world} GPUs" if gc == 1 else
+                                      f"output blocks, {gr} row blocks x {gc} column blocks / {world} GPUs")
+    return {"workload": WORKLOAD, "M": M, "K": K, "N": N, "nc": 2, "parallelism": par, "l2": L2_NOTE}
 
 
 def peaks():
@@ -443,7 +452,7 @@ def other_configs(torch, mcf, hbm_gbs, rank, world):
     return res
 
 
-def run_ours(args):
+def run_ours(args, N_ALL=N):
     import ctypes as C
 
     import numpy as np
@@ -452,7 +461,7 @@ def run_ours(args):
 
     import paper_2207_08867_b200 as mcf
     from paper_2207_08867_b200 import data
-    from paper_2207_08867_b200.dist import max_over_ranks, row_range
+    from paper_2207_08867_b200.dist import block_range, max_over_ranks
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -462,9 +471,13 @@ def run_ours(args):
     hbm = float(pk.get("hbm_gbs", 6446.6))
 
     # inputs: generated on the host from the reference's Rng mappings, resident in HBM
-    a_h, b_h = data.config2(M, K, N)
-    r0, r1 = row_range(M, rank, world)
+    # the rank's output block: its rows of A and its columns of B (N below is
+    # the block's width; the whole-job flops use M_ALL x N_ALL)
+    a_h, b_full = data.config2(M, K, N_ALL)
+    r0, r1, c0, c1 = block_range(M, N_ALL, rank, world, grid_for(world))
     rows = r1 - r0
+    N = c1 - c0  # noqa: N806 -- the block's width shadows the module constant inside this function
+    b_h = np.ascontiguousarray(b_full[:, c0:c1])
     a = torch.from_numpy(a_h[r0:r1]).cuda()
     b = torch.from_numpy(b_h).cuda()
     out = torch.empty((rows, N, 2), dtype=torch.float32, device="cuda")
@@ -500,7 +513,7 @@ def run_ours(args):
     launches = mcf.launch_count()
     times = [e0.elapsed_time(e1) for e0, e1 in ev]
     ms = max_over_ranks(sum(times) / len(times), device="cuda")
-    value = 2.0 * M * N * K / (ms * 1e-3) / 1e9
+    value = 2.0 * M * N_ALL * K / (ms * 1e-3) / 1e9
 
     # ---- roofline: the dominant kernel is the residue GEMM (one launch per
     # product, batched over the moduli).  Algorithmic int8 ops per launch:
@@ -560,7 +573,7 @@ def run_ours(args):
     f32 = C.c_double(0.0)
     lib.mcf_probe_pipe_rates(C.byref(f64), C.byref(f32))
     ops64 = lib.mcf_fast_ops_per_mad(0, mcf.B32, 2)
-    fp64_path = {"ms_per_step": round(ms64, 3), "GFLOP/s_eff": round(2.0 * M * N * K / ms64 / 1e6, 1),
+    fp64_path = {"ms_per_step": round(ms64, 3), "GFLOP/s_eff": round(2.0 * M * N_ALL * K / ms64 / 1e6, 1),
                  "fp64_ops_per_mad": ops64, "fp64_pipe_TFLOPs": round(ops64 * rows * N * K / ms64 / 1e9, 3),
                  "fp64_pipe_peak_measured": round(f64.value / 1e12, 3)}
     step()  # leave `out` holding the headline path's result (for the parity stamp)
@@ -586,7 +599,7 @@ def run_ours(args):
     for _ in range(e2e_steps):
         e2e_step()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, device="cuda")
-    e2e_val = 2.0 * M * N * K / e2e_s / 1e9
+    e2e_val = 2.0 * M * N_ALL * K / e2e_s / 1e9
     h2d_bytes = int(a_pin.numel() * 4 + b_pin.numel() * 4)
     d2h_bytes = int(o_pin.numel() * 4)
 

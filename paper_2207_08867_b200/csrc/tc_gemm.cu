@@ -45,6 +45,7 @@ constexpr int kMaxBatch = 32;
 constexpr float kMagic = 12582912.0f;  // 1.5 2^23
 
 struct Params {
+  int stages;  // pair kernel: depth of the shared-memory ring (<= kStages2)
   int m, n, kp, batch, tiles_m, tiles_n;
   int64_t ldo;           // output row stride (elements)
   int mode;              // 0: int32 C, 1: int8 residues C mod m_b
@@ -349,11 +350,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_tc_gemm_s8_pair(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nst = p.stages;  // ring depth: 7 fills the SM's shared memory, fewer leave room for co-resident kernels
   uint8_t* sa = smem;
-  uint8_t* sb = smem + kStages2 * kHalfBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2);
-  uint64_t* empty = full + kStages2;
-  uint64_t* tfull = empty + kStages2;
+  uint8_t* sb = smem + nst * kHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * kStage2);
+  uint64_t* empty = full + nst;
+  uint64_t* tfull = empty + nst;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -363,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
-    for (int s = 0; s < kStages2; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
@@ -403,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) mbar_expect_tx(full + stage, 2 * kStage2);
           tma_load_3d_pair(sa + stage * kHalfBytes, &ta, ka0 + kb * BK, mb * 256 + (int)rank * 128, zb, full + stage);
           tma_load_3d_pair(sb + stage * kHalfBytes, &tb, kb0 + kb * BK, nb * 256 + (int)rank * 128, zb, full + stage);
-          if (++stage == kStages2) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -427,7 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 32; ++kk)
             umma_i8_pair(d, smem_desc(a0 + kk * 32), smem_desc(b0 + kk * 32), (kb | kk) != 0);
           umma_commit_pair(empty + stage);
-          if (++stage == kStages2) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -527,6 +529,20 @@ bool make_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t kp, in
 
 namespace mcfr {
 
+// ring depth of the pair kernel (MCF_TC_STAGES, 5..7; default 7).  Measured
+// on B200 (r02, config 2): 5, 6 and 7 stages all give 1.33 ms per product, and
+// the shallower rings (which leave shared memory for the residue /
+// reconstruction kernels of other row blocks to share the SMs, MCF_OZ_PIPE)
+// do not make the pipelined product faster (2 blocks 1.34 ms, 4 blocks 1.37).
+static int pair_stages() {
+  static const int n = [] {
+    const char* e = getenv("MCF_TC_STAGES");
+    const int v = e ? atoi(e) : mcfg::tc::kStages2;
+    return v < 5 ? 5 : (v > mcfg::tc::kStages2 ? mcfg::tc::kStages2 : v);
+  }();
+  return n;
+}
+
 // C_b = A_b . B_b^T (b < batch) on the hand-written tcgen05 kernel.
 // a: [batch][m][kp], b: [batch][b_rows][kp] int8 (the first n rows used) (kp % 16 == 0, 16-byte aligned
 // bases); out: [batch][m][ldo] int32 (moduli == nullptr) or int8 residues
@@ -575,9 +591,11 @@ mcf_status tc_gemm_s8(const int8_t* a, const int8_t* b, void* out, int64_t m, in
   if (pair) {
     CUtensorMap tb2;
     if (!make_map(&tb2, b, b_rows, kp, batch, 128)) return MCF_ERR_UNSUPPORTED;
-    const int smem = kStages2 * kStage2 + 1024 + 256;
+    p.stages = pair_stages();
+    const int smem = p.stages * kStage2 + 1024 + 256;
     per_device_once(kOnceTcGemm, [&] {
-      cudaFuncSetAttribute(k_tc_gemm_s8_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_tc_gemm_s8_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kStages2 * kStage2 + 1024 + 256);
     });
     const int64_t tiles = (int64_t)((m + 255) / 256) * p.tiles_n * batch;
     const int grid = 2 * (int)std::min<int64_t>(tiles, sm_count() / 2);
@@ -634,9 +652,11 @@ mcf_status tc_gemm_s8_seg(const int8_t* a, int64_t lda, const int8_t* b, int64_t
   }
   CUtensorMap ta2, tb2;
   if (!make_map(&ta2, a, m, lda, 1, 128) || !make_map(&tb2, b, b_rows, ldb, 1, 128)) return MCF_ERR_UNSUPPORTED;
-  const int smem = kStages2 * kStage2 + 1024 + 256;
+  p.stages = pair_stages();
+  const int smem = p.stages * kStage2 + 1024 + 256;
   per_device_once(kOnceTcGemm, [&] {
-    cudaFuncSetAttribute(k_tc_gemm_s8_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_tc_gemm_s8_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kStages2 * kStage2 + 1024 + 256);
   });
   const int64_t tiles = (int64_t)((m + 255) / 256) * p.tiles_n * nseg;
   const int grid = 2 * (int)std::min<int64_t>(tiles, sm_count() / 2);

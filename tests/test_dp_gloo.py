@@ -139,3 +139,47 @@ def test_row_sharded_product_with_broadcast_b(tmp_path, world, mcmc):
     full, want = np.load(tmp_path / "full.npy"), np.load(tmp_path / "want.npy")
     assert np.array_equal(full.view(np.uint32), want.view(np.uint32))
     assert float(np.load(tmp_path / "t.npy")[0]) == world
+
+
+def _mm_block_worker(rank, world, port, outdir):
+    """Config 2's output-block grid: each rank computes its rows x columns block
+    from its rows of A and its columns of B (oracle compute), blocks assembled."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2207_08867_b200 import dist as pdist
+    from mcgen import split
+
+    port_ = oracle.Oracle("port")
+    m, k, n = 11, 24, 9
+    a = split(np.random.default_rng(3).uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    b = np.random.default_rng(4).uniform(-1, 1, (k, n)).astype(np.float32)
+    r0, r1, c0, c1 = pdist.block_range(m, n, rank, world)
+    local = port_.mm_mcn(np.ascontiguousarray(a[r0:r1]), np.ascontiguousarray(b[:, c0:c1]))
+    full = pdist.gather_blocks(torch.from_numpy(np.ascontiguousarray(local)), m, n)
+    if rank == 0:
+        np.save(os.path.join(outdir, "full.npy"), full.numpy())
+        np.save(os.path.join(outdir, "want.npy"), port_.mm_mcn(a, b))
+    dist.destroy_process_group()
+
+
+def test_block_grid_shapes():
+    from paper_2207_08867_b200.dist import block_grid, block_range
+
+    assert [block_grid(w) for w in (1, 2, 3, 4, 6, 8)] == [(1, 1), (1, 2), (1, 3), (2, 2), (2, 3), (2, 4)]
+    for world in (1, 2, 4, 6, 8):
+        cover = np.zeros((13, 10), dtype=int)
+        for r in range(world):
+            r0, r1, c0, c1 = block_range(13, 10, r, world)
+            cover[r0:r1, c0:c1] += 1
+        assert (cover == 1).all()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_block_sharded_product_assembles_bitwise(tmp_path, world):
+    mp.spawn(_mm_block_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    full, want = np.load(tmp_path / "full.npy"), np.load(tmp_path / "want.npy")
+    assert np.array_equal(full.view(np.uint32), want.view(np.uint32))

@@ -1,5 +1,6 @@
-"""Device time of one rank's share of the config-2 product under row sharding
-(rows = 4096 / G for G = 1, 2, 4, 8): the per-rank step of bench.py --gpus G."""
+"""Device time of one rank's share of the config-2 product: the per-rank step of
+bench.py --gpus G under a Gr x Gc grid of output blocks (rows / Gr of A, columns
+/ Gc of B; Gc = 1 is plain row sharding)."""
 import os
 import sys
 
@@ -11,17 +12,17 @@ from paper_2207_08867_b200 import data  # noqa: E402
 
 M = K = N = 4096
 a_h, b_h = data.config2(M, K, N)
-b = torch.from_numpy(b_h).cuda()
 lib = mcf.lib()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 base = None
-for g in (1, 2, 4, 8):
-    rows = M // g
+for gr, gc in ((1, 1), (2, 1), (1, 2), (4, 1), (2, 2), (1, 4), (8, 1), (4, 2), (2, 4), (1, 8)):
+    rows, cols = M // gr, N // gc
     a = torch.from_numpy(a_h[:rows]).cuda()
-    out = torch.empty((rows, N, 2), dtype=torch.float32, device="cuda")
+    b = torch.from_numpy(b_h[:, :cols].copy()).cuda()
+    out = torch.empty((rows, cols, 2), dtype=torch.float32, device="cuda")
 
     def step():
-        rc = lib.mcf_bmm_mcn(mcf.B32, a.data_ptr(), 2, b.data_ptr(), 1, rows, K, N, 0, out.data_ptr(), mcf.FAST, 1,
+        rc = lib.mcf_bmm_mcn(mcf.B32, a.data_ptr(), 2, b.data_ptr(), 1, rows, K, cols, 0, out.data_ptr(), mcf.FAST, 1,
                              torch.cuda.current_stream().cuda_stream)
         assert rc == 0, lib.mcf_last_error()
 
@@ -39,4 +40,6 @@ for g in (1, 2, 4, 8):
     ts.sort()
     ms = ts[len(ts) // 2]
     base = base or ms
-    print(f"G={g}: rows {rows}: {ms:.3f} ms per rank step, strong-scaling efficiency {base / (g * ms):.2f}")
+    g = gr * gc
+    print(f"G={g} ({gr} x {gc}): block {rows} x {cols}: {ms:.3f} ms per rank step, "
+          f"strong-scaling efficiency {base / (g * ms):.2f}", flush=True)
