@@ -26,6 +26,7 @@
 //       |L - 2^(W-P-1)| > 2^(W-2P+1) = 64 units (a value just below a power of
 //       two lies in the lower binade, whose finer grid makes the test
 //       conservative); one more unit covers a wide S known to half a unit.
+//       (The device declines L - mid in [-m, 3 m): one mask test.)
 //   (U) uniqueness: if S fits 2 P bits (the low W - 2P bits of its wide
 //       significand are zero) then (rnp(S), S - rnp(S)) is its ONLY compressed
 //       expansion: another one needs c_0 = the other neighbour, |c_1| = h and
@@ -46,7 +47,7 @@
 //
 // Policy V: N (component type), W (wide type), wide(N), narrow(W) (exact on
 // P-bit values), add/sub/mul/fma/neg/abs on W, rcp_seed(W) (any approximation
-// of 1/y good to ~2^-16), rnpm(W, m, ok) (rnp, and ok &= |L - mid| > m),
+// of 1/y good to ~2^-16), rnpm(W, m, ok) (rnp, and ok &= L - mid outside [-m, 3 m)),
 // span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
 // rnpe (nearest-even), in_window / below_window on N, kP.
 #pragma once
@@ -266,14 +267,14 @@ struct VD {
   // the magnitude, clear the 29 low bits; a carry runs into the exponent as
   // it should).  rnp: ties away from zero (every use declines near-ties);
   // rnpe: ties to even.
-  // round to 24 bits AND test the margin m with one 64-bit add: b' = b + half
-  // + m; (b' & ~low29) is t rounded to nearest whenever t is not within m
-  // units of a midpoint (L in [mid - m, mid) would round the wrong way -- and is
-  // declined), and t is within m units of a midpoint exactly when the low 29
-  // bits of b' are <= 2 m.
+  // round to 24 bits AND test the margin m (a power of two) with one 64-bit
+  // add: b' = b + half + m; (b' & ~low29) is t rounded to nearest whenever t
+  // is not within m units of a midpoint (L in [mid - m, mid) would round the
+  // wrong way -- and is declined); the low 29 bits of b' are below 4 m exactly
+  // when L is in [mid - m, mid + 3 m): one LOP3 with a predicate result.
   __device__ __forceinline__ static W rnpm(W t, int m, bool& ok) {
     const long long b = __double_as_longlong(t) + (0x10000000LL + m);
-    ok &= ((unsigned)b << 3) > ((unsigned)(2 * m) << 3);
+    ok &= ((unsigned)b & (0x1fffffffu & ~(4u * (unsigned)m - 1u))) != 0u;
     return __longlong_as_double(b & ~0x1fffffffLL);
   }
   // ties to even: (t + M) - M with M = 1.5 2^(e + 29), e = t's exponent; the

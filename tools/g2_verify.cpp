@@ -114,6 +114,8 @@ struct VE {
     const double m = std::frexp(std::fabs(t), &e);
     return std::copysign(std::ldexp(std::floor(std::ldexp(m, P) + 0.5), e - P), t);
   }
+  // the device declines L - mid in [-m, 3 m) (one mask test): a superset of
+  // this symmetric margin, which keeps more accepted cases to check here
   static W rnpm(W t, int m, bool& ok) {
     ok &= away(t, m);
     return rnp(t);
