@@ -18,8 +18,14 @@
  *    count dividing numel for a trailing-suffix broadcast, read as
  *    v[e % vn] (mc_ops.hpp:14-15, 317-329, 391).
  *  - Pointers without the mcf_h_ prefix are DEVICE pointers; the call is
- *    asynchronous on `stream` (NULL = legacy default stream), allocates
- *    nothing, and is safe from several host threads on distinct streams.
+ *    asynchronous on `stream` (NULL = legacy default stream) and safe from
+ *    several host threads on distinct streams.  The elementwise operators and
+ *    the reference-order contractions allocate nothing.  The MCF_FAST
+ *    contractions keep a workspace per (device, stream) -- residue planes, or
+ *    widened binary64 operands -- that grows on first use or when a larger
+ *    shape arrives (cudaMalloc; regrowing synchronizes that stream).  Call
+ *    mcf_fast_mm_reserve first where a call must not allocate (stream
+ *    capture, latency-critical loops).
  *    mcf_h_* entry points take HOST pointers, stage through the library's
  *    device workspace and return when the result is in host memory.
  *  - Results are bit-identical to the reference for every elementwise
@@ -168,6 +174,10 @@ int mcf_fast_tc_plan(int64_t k, int b_components, int* moduli, int* bits_a, int*
  * modulus product M), q_scale = RN32(2^(L-11) / M), m_bits = L; returns S
  * (0 for n outside 1..22).  Null pointers are skipped. */
 int mcf_fast_tc_crt_table(int n, int* moduli, float* w_slices, float* m_slices, float* q_scale, int* m_bits);
+/* Grows `stream`'s tensor-core workspace (and uploads the CRT tables) for an
+ * m x k x n binary32 nc=2 product with a b_components-component B, so that the
+ * product itself allocates nothing.  MCF_ERR_UNSUPPORTED outside the scheme. */
+mcf_status mcf_fast_mm_reserve(int64_t m, int64_t k, int64_t n, int b_components, mcf_stream stream);
 /* Instrumentation: one MC(nc=2, binary32) x T product on the tensor-core
  * path with per-phase device times (phase_ms[4]: B residues, A residues, int8
  * GEMMs, reconstruction + fallback) and the number of outputs recomputed by

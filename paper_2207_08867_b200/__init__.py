@@ -70,6 +70,7 @@ _SIGS = {
     "mcf_fast_tc_digits": [],
     "mcf_fast_tc_gemm_equivalents": [_int, _i64],
     "mcf_fast_mm_phases": [_p, _p, _i64, _i64, _i64, _p, _p, _p, _p],
+    "mcf_fast_mm_reserve": [_i64, _i64, _i64, C.c_int, _p],
     "mcf_fast_tc_plan": [_i64, _int, _p, _p, _p],
     "mcf_fast_tc_crt_table": [_int, _p, _p, _p, _p, _p],
     "mcf_tc_gemm_s8": [_p, _p, _p, _i64, _i64, _i64, _int, _i64, _p, _p],

@@ -589,6 +589,11 @@ int mcf_fast_tc_crt_table(int n, int* moduli, float* w_slices, float* m_slices, 
   return mcfr::ozaki_crt_table(n, moduli, w_slices, m_slices, q_scale, m_bits);
 }
 
+mcf_status mcf_fast_mm_reserve(int64_t m, int64_t k, int64_t n, int b_components, mcf_stream stream) {
+  if (mcfr::ensure_device_tables() != MCF_OK) return MCF_ERR_CUDA;
+  return mcfr::ozaki_reserve(m, k, n, b_components, stream);
+}
+
 mcf_status mcf_fast_mm_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out,
                               double* phase_ms, int64_t* fallback_outputs, mcf_stream stream) {
   if (!x || !w || !out || !phase_ms || !fallback_outputs)

@@ -1783,8 +1783,9 @@ bool ozaki_supported(int64_t m, int64_t k, int64_t n) {
 // multiples of 256 (the CTA-pair tile); products under 1024 rows run as one
 // block.  Results are those of the unpipelined product bit for bit (every
 // output depends on its own row and column only).
-static mcf_status pipelined(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n,
-                            float* out, int64_t ldo, const mcfg::oz::Epilogue& ep0, cudaStream_t s) {
+// row blocks of the one-call product: count nb, rows per block rb, and the
+// workspace bytes (B's planes + nb row-block workspaces)
+static std::size_t pipe_geometry(int64_t m, int64_t k, int64_t n, int ncb, int& nb, int64_t& rb) {
   using namespace mcfg::oz;
   static const int blocks_env = [] {
     // row blocks (1: no pipelining, the default).  Measured on B200 (r02,
@@ -1795,13 +1796,22 @@ static mcf_status pipelined(const float* x, int nca, const float* w, int ncb, in
     const char* e = getenv("MCF_OZ_PIPE");
     return e ? std::max(1, std::min(6, atoi(e))) : 1;
   }();
-  int nb = m >= 1024 ? blocks_env : 1;
-  int64_t rb = (m + nb - 1) / nb;
+  nb = m >= 1024 ? blocks_env : 1;
+  rb = (m + nb - 1) / nb;
   rb = (rb + 255) / 256 * 256;
   nb = (int)((m + rb - 1) / rb);
+  return al(b_bytes(k, n, ncb)) + nb * al(rows_bytes(rb, k, n, ncb));
+}
+
+static mcf_status pipelined(const float* x, int nca, const float* w, int ncb, int64_t m, int64_t k, int64_t n,
+                            float* out, int64_t ldo, const mcfg::oz::Epilogue& ep0, cudaStream_t s) {
+  using namespace mcfg::oz;
+  int nb;
+  int64_t rb;
+  const std::size_t total = pipe_geometry(m, k, n, ncb, nb, rb);
   const CrtPlan pl = crt_plan(k, ncb);
   const std::size_t bb = al(b_bytes(k, n, ncb)), rbytes = al(rows_bytes(rb, k, n, ncb));
-  char* ws = oz_workspace(bb + nb * rbytes, s);
+  char* ws = oz_workspace(total, s);
   if (!ws) return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
   cudaStream_t as = side_stream(12), cs = side_stream(13);
   cudaEvent_t fork = tl_event(0), bdone = tl_event(1);
@@ -1905,6 +1915,19 @@ int ozaki_gemm_equivalents(int ncb, int64_t k) { return mcfg::oz::crt_plan(k, nc
 
 // one product with phase timing: ms[0] B residues, ms[1] A residues, ms[2] the
 // int8 GEMMs, ms[3] reconstruction + fallback; *fallback = listed outputs
+// grows the stream's residue-plane workspace to what an m x k x n product
+// with an ncb-component B needs (so that the product itself allocates nothing)
+mcf_status ozaki_reserve(int64_t m, int64_t k, int64_t n, int ncb, cudaStream_t s) {
+  using namespace mcfg::oz;
+  if (!ozaki_supported(m, k, n) || (ncb != 1 && ncb != 2))
+    return fail(MCF_ERR_UNSUPPORTED, "mm_fast: shape outside the tensor-core path");
+  int nb;
+  int64_t rb;
+  if (!oz_workspace(pipe_geometry(m, k, n, ncb, nb, rb), s))
+    return fail(MCF_ERR_CUDA, "mm_fast: cannot allocate the residue-plane workspace");
+  return upload_crt_tables();
+}
+
 mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, double* ms,
                         int64_t* fallback, cudaStream_t s) {
   using namespace mcfg::oz;

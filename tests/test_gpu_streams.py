@@ -69,3 +69,33 @@ def test_errors_are_per_thread_and_reference_worded():
     bad = torch.zeros((4, 9), dtype=torch.float32, device="cuda")
     with pytest.raises(ValueError, match="1 <= nc <= 8"):
         mcf.square_mcn(bad)
+
+
+def test_reserved_product_runs_under_stream_capture():
+    """mcf_fast_mm_reserve grows the stream's workspace ahead of time, so the
+    FAST product allocates nothing and can be captured into a CUDA graph on a
+    stream that has never run it; the replay gives the bits of a direct call."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    lib = mcf.lib()
+    rng = np.random.default_rng(91)
+    m, k, n = 512, 1024, 384
+    x = torch.from_numpy(split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)).cuda()
+    w = torch.from_numpy(rng.uniform(-1, 1, (k, n)).astype(np.float32)).cuda()
+    want = mcf.mm_mcn(x, w, plan=mcf.FAST).cpu().numpy()
+    out = torch.zeros((m, n, 2), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    assert lib.mcf_fast_mm_reserve(m, k, n, 1, s.cuda_stream) == 0, lib.mcf_last_error()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            rc = lib.mcf_bmm_mcn(mcf.B32, x.data_ptr(), 2, w.data_ptr(), 1, m, k, n, 0, out.data_ptr(), mcf.FAST, 1,
+                                 torch.cuda.current_stream().cuda_stream)
+            assert rc == 0, lib.mcf_last_error()
+        g.replay()
+        s.synchronize()
+    assert_bits(out.cpu().numpy(), want, "captured FAST product")
+    assert lib.mcf_fast_mm_reserve(8, 1 << 20, 8, 1, 0) == 2  # MCF_ERR_UNSUPPORTED: outside the scheme
