@@ -332,3 +332,27 @@ def test_config3_fast_tracks_reference_within_spread():
     print("reference losses", ref, "\nreversed-order spread", spread, "\nFAST diff", diff)
     assert np.all(diff <= bound), (diff, bound)
     assert ref[-1] < ref[0]  # it trains
+
+
+@pytest.mark.parametrize("plan_name", ["SEQUENTIAL", "FAST"])
+def test_captured_step_replays_the_bits_of_direct_steps(plan_name):
+    """MCMLP.capture: the step as a CUDA graph (three streams, no allocation
+    inside) gives the losses and parameters of direct step() calls bit for bit;
+    the reference-order plan's graph still reproduces the reference's
+    trajectory."""
+    import paper_2207_08867_b200 as mcf
+
+    plan = getattr(mcf, plan_name)
+    direct, xt, y, dims, L, _ = _setup(plan)
+    graphed, xt2, y2, *_ = _setup(plan)
+    n = xt.shape[1]
+    steps = len(G["losses"])
+    want = [direct.loss_value(direct.step(xt, y, n), n) for _ in range(steps)]
+    replay = graphed.capture(xt2, y2, n)  # two real steps happen inside
+    got = [graphed.loss_value(replay(), n) for _ in range(steps - 2)]
+    assert np.array_equal(np.array(got, np.float32).view(np.uint32), np.array(want[2:], np.float32).view(np.uint32))
+    for l, ((w, b), (w2, b2)) in enumerate(zip(direct.params_numpy(), graphed.params_numpy())):
+        assert_bits(w2, w, f"W{l}")
+        assert_bits(b2, b, f"b{l}")
+    if plan_name == "SEQUENTIAL":
+        assert np.array_equal(np.array(got, np.float32).view(np.uint32), G["losses"][2:].view(np.uint32))
