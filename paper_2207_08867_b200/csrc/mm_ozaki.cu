@@ -1792,7 +1792,11 @@ static std::size_t pipe_geometry(int64_t m, int64_t k, int64_t n, int ncb, int& 
     // config 2): 1 block 1.308 ms, 2 blocks 1.329, 4 blocks 1.355, 6 blocks
     // 1.388 -- the residue and reconstruction kernels do not hide under the
     // GEMM (both are FMA-pipe / issue heavy and the GEMM's epilogue needs the
-    // same pipes), and the shorter GEMMs lose their last-wave tails.
+    // same pipes), and the shorter GEMMs lose their last-wave tails.  Retried
+    // with room for co-residency (a 5- or 6-stage GEMM ring, residue grids of
+    // 2-4 CTAs per SM): 2 blocks 1.33, 4 blocks 1.36, 6 blocks 1.40 against
+    // 1.31 -- the GEMM already runs at the power-capped clock (1.55 GHz), so
+    // work added beside it slows it by as much as it hides.
     const char* e = getenv("MCF_OZ_PIPE");
     return e ? std::max(1, std::min(6, atoi(e))) : 1;
   }();
