@@ -475,18 +475,31 @@ __global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, i
   for (int t = 0; t < NMOD; ++t) dg[t][tx][ty] = wd[t];
   __syncthreads();
   // residue rows: thread (jj = tid / 8, part = tid % 8) writes 4 bytes of
-  // column j0 + jj's 32-k run in every plane
+  // column j0 + jj's 32-k run in every plane (the planes a 32-bit word offset
+  // apart: one address add per store) and the same four k of the transposed
+  // binary32 copy (one 16-byte store when the run is whole and aligned)
   const int jj = threadIdx.x >> 3, part = threadIdx.x & 7;
   const int64_t gj = j0 + jj;
-  if (gj < n) {
-    int8_t* dst = out + gj * kp + k0 + part * 4;
+  if (gj >= n) return;
+  unsigned* dst = reinterpret_cast<unsigned*>(out + gj * kp + k0 + part * 4);
+  if ((uint64_t)NMOD * (uint64_t)np * (uint64_t)kp < (uint64_t(1) << 33)) {
+    const unsigned pw = (unsigned)((np * kp) >> 2);  // plane stride in words
 #pragma unroll
-    for (int t = 0; t < NMOD; ++t) *reinterpret_cast<unsigned*>(dst + t * np * kp) = dg[t][jj][part];
+    for (int t = 0; t < NMOD; ++t) dst[(unsigned)t * pw] = dg[t][jj][part];
+  } else {
+#pragma unroll
+    for (int t = 0; t < NMOD; ++t) dst[(int64_t)t * ((np * kp) >> 2)] = dg[t][jj][part];
   }
-  for (int w = threadIdx.x; w < kSlab * kSlab * NC; w += blockDim.x) {
-    const int wj = w / (kSlab * NC), rest = w - wj * (kSlab * NC);
-    const int64_t gj2 = j0 + wj, gk = k0 + rest / NC;
-    if (gj2 < n && gk < k) bt[(gj2 * k + gk) * NC + rest % NC] = tv[wj][rest];
+  const int64_t gk = k0 + part * 4;
+  float* bo = bt + (gj * k + gk) * NC;
+  const float* tr = &tv[jj][part * 4 * NC];
+  if (gk + 4 <= k && (reinterpret_cast<uintptr_t>(bo) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      reinterpret_cast<float4*>(bo)[q] = make_float4(tr[4 * q], tr[4 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
+  } else {
+    for (int u = 0; u < 4 * NC; ++u)
+      if (gk + u / NC < k) bo[u] = tr[u];
   }
 }
 
