@@ -418,9 +418,15 @@ __global__ void __launch_bounds__(256) k_res_rows(const float* __restrict__ a, i
     const int l0i[4] = {limb_int(l01[0].x), limb_int(l01[0].y), limb_int(l23[0].x), limb_int(l23[0].y)};
     unsigned wd[NMOD];
     residue_words<NMOD>(l01, l23, l0i, wd);
-    int8_t* o = out + i * kp + k0;
+    unsigned* o = reinterpret_cast<unsigned*>(out + i * kp + k0);
+    if ((uint64_t)NMOD * (uint64_t)plane < (uint64_t(1) << 33)) {  // word offsets of the planes fit 32 bits
+      const unsigned pw = (unsigned)(plane >> 2);
 #pragma unroll
-    for (int t = 0; t < NMOD; ++t) *reinterpret_cast<unsigned*>(o + t * plane) = wd[t];
+      for (int t = 0; t < NMOD; ++t) o[(unsigned)t * pw] = wd[t];
+    } else {
+#pragma unroll
+      for (int t = 0; t < NMOD; ++t) o[(int64_t)t * (plane >> 2)] = wd[t];
+    }
   }
 }
 
@@ -734,8 +740,15 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
   if (j0 >= n) return;
   const int64_t plane = m * ldr, off = i * ldr + j0;
   unsigned wv[NMOD];
+  const unsigned* rw = reinterpret_cast<const unsigned*>(rq + off);
+  if ((uint64_t)NMOD * (uint64_t)plane < (uint64_t(1) << 33)) {  // word offsets of the planes fit 32 bits
+    const unsigned pw = (unsigned)(plane >> 2);
 #pragma unroll
-  for (int t = 0; t < NMOD; ++t) wv[t] = __ldcs(reinterpret_cast<const unsigned*>(rq + t * plane + off));
+    for (int t = 0; t < NMOD; ++t) wv[t] = __ldcs(rw + (unsigned)t * pw);
+  } else {
+#pragma unroll
+    for (int t = 0; t < NMOD; ++t) wv[t] = __ldcs(rw + (int64_t)t * (plane >> 2));
+  }
   float2 T[2][kSlices];  // [column pair][slice] = (column 2p, column 2p + 1)
 #pragma unroll
   for (int h = 0; h < 2; ++h)
