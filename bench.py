@@ -416,7 +416,7 @@ def other_configs(torch, mcf, hbm_gbs, rank, world):
     xt = torch.from_numpy(np.ascontiguousarray(xb[s0:s1].T)).cuda()
     yt = torch.from_numpy(np.ascontiguousarray(yb[s0:s1])).cuda()
     first = model.loss_value(model.step(xt, yt, nglob), nglob)
-    # one process: the step replayed as a CUDA graph (58 launches over three
+    # one process: the step replayed as a CUDA graph (~50 launches over three
     # streams; same bits as direct calls); several ranks: direct calls
     run_step = model.capture(xt, yt, nglob) if world == 1 else (lambda: model.step(xt, yt, nglob))
     ms = _dev_time(torch, run_step, 10, world=world)

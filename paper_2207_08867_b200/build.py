@@ -34,7 +34,7 @@ CXXFLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-I" + os.path.jo
             "-I" + os.path.join(ROOT, "include")]
 
 CU_SOURCES = ["elementwise.cu", "linalg.cu", "mm_fast.cu", "mm_ozaki.cu", "stream_fast.cu", "mlp.cu", "mlp_fast.cu", "mc_nn.cu",
-              "hostapi.cu", "tc_gemm.cu"]
+              "hostapi.cu", "tc_gemm.cu", "mm_skinny.cu"]
 CXX_SOURCES = ["runtime.cpp"]
 
 

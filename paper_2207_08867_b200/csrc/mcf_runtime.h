@@ -94,6 +94,8 @@ mcf_status mm_ozaki_bias_act(const float* w, const float* a, int64_t m, int64_t 
 int ozaki_gemm_equivalents(int ncb, int64_t k);
 int ozaki_crt_info(int64_t k, int ncb, int* n, int* pa, int* pb);
 int ozaki_crt_table(int n, int* moduli, float* w, float* mh, float* cq, int* bits);
+// MC(nc=2, binary32) x T for m <= 16 rows in one FP64-pipe kernel (mm_skinny.cu)
+mcf_status mm_skinny_mct(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, cudaStream_t s);
 mcf_status ozaki_reserve(int64_t m, int64_t k, int64_t n, int ncb, cudaStream_t s);
 mcf_status ozaki_phases(const float* x, const float* w, int64_t m, int64_t k, int64_t n, float* out, double* ms,
                         int64_t* fallback, cudaStream_t s);

@@ -494,6 +494,26 @@ mcf_status mm_fast_mct(mcf_prec p, const void* x, int nc, const void* w, int64_t
       if (b + 1 == batch) return MCF_OK;
     }
   }
+  // short A (an MLP's class layer): one kernel, no binary64 workspace (mm_skinny.cu)
+  static const bool skinny_on = [] {
+    const char* e = getenv("MCF_MM_SKINNY");
+    return !(e && e[0] == '0');
+  }();
+  if (skinny_on && p == MCF_B32 && nc == 2 && m <= 16) {
+    const float* xf = static_cast<const float*>(x);
+    const float* wf = static_cast<const float*>(w);
+    float* of = static_cast<float*>(out);
+    for (int64_t b = 0; b < batch; ++b) {
+      const mcf_status st = mm_skinny_mct(xf + b * m * k * 2, wf + (w_batched ? b * k * n : 0), m, k, n,
+                                          of + b * m * n * 2, s);
+      if (st == MCF_ERR_UNSUPPORTED) {
+        if (b == 0) break;  // alignment / shape outside the kernel: the general path below
+        return fail(MCF_ERR_CUDA, "mm_fast: the short-A kernel refused a later batch entry");
+      }
+      if (st != MCF_OK) return st;
+      if (b + 1 == batch) return MCF_OK;
+    }
+  }
   if (p != MCF_B32 || (nc != 2 && nc != 3) || n % 2 != 0 || (k * nc) % 2 != 0)
     return MCF_ERR_UNSUPPORTED;
   const int64_t xa = batch * m * k * nc, wb = (w_batched ? batch : 1) * k * n;

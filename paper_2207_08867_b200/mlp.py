@@ -236,8 +236,8 @@ class MCMLP:
         """The step on (xt, labels) as a CUDA graph: returns replay(), which runs
         one training step on the CURRENT contents of xt / labels (refill them in
         place for a new batch) and returns the loss-terms tensor like step().
-        The graph holds the step's 58 launches over three streams, so the
-        launch overhead is paid once (config 3: 1.53 -> 1.44 ms per step);
+        The graph holds the step's ~50 launches over three streams, so the
+        launch overhead is paid once (config 3: 1.45 -> 1.36 ms per step);
         results are the bits of step().  Single process only: the gradient
         all-reduce of a multi-rank job is left to direct step() calls.  capture()
         itself performs two real training steps (warm-up on the capture stream)."""
