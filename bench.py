@@ -469,9 +469,18 @@ def run_ours(args, N_ALL=N):
     from paper_2207_08867_b200.dist import block_range, max_over_ranks
 
     rank, world, local = env_rank()
+    # MCF_BENCH_SHARE_GPU=1 MCF_BENCH_BACKEND=gloo: a plumbing rehearsal of the
+    # multi-rank flow on ONE GPU (all ranks on cuda:0, gloo collectives) --
+    # exercises the sharding, barriers and gathers, never used for numbers
+    if os.environ.get("MCF_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MCF_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6446.6))
 
