@@ -88,6 +88,58 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__
   c[i * ldc + j] = v;
 }
 
+// C (m x n) = op(A) B for a SHORT K (k <= 16, B's rows contiguous: the
+// 10-class layer's dA = approx(W)^T G, K = 10 classes): memory-bound (one
+// mask load and one store per output), so a thread keeps its four columns of
+// B (k x 4 values) in registers and walks a strip of rows with op(A)'s strip
+// in shared memory; 16-byte mask loads and stores.  The arithmetic is the
+// ordered kernel's (fl_mul then fl_add, k increasing, mask applied as 0 + c):
+// bit-identical to mcf_gemm_f32_ordered.
+constexpr int kSmallK = 16;
+constexpr int kSmallRows = 32;  // rows per CTA
+template <bool TA>
+__global__ void __launch_bounds__(256) k_gemm_smallk(const float* __restrict__ a, int64_t lda,
+                                                     const float* __restrict__ b, int64_t ldb, float* __restrict__ c,
+                                                     int64_t ldc, int64_t m, int64_t n, int k,
+                                                     const float* __restrict__ mask) {
+  __shared__ float as[kSmallK][kSmallRows];
+  const int64_t i0 = (int64_t)blockIdx.y * kSmallRows;
+  for (int e = threadIdx.x; e < k * kSmallRows; e += blockDim.x) {
+    const int kk = e / kSmallRows, r = e - kk * kSmallRows;
+    const int64_t gi = i0 + r;
+    as[kk][r] = gi < m ? (TA ? a[kk * lda + gi] : a[gi * lda + kk]) : 0.0f;
+  }
+  __syncthreads();
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j >= n) return;
+  float4 bv[kSmallK];
+#pragma unroll
+  for (int kk = 0; kk < kSmallK; ++kk)
+    bv[kk] = kk < k ? __ldg(reinterpret_cast<const float4*>(b + kk * ldb + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int rows = (int)(m - i0 < kSmallRows ? m - i0 : kSmallRows);
+  for (int r = 0; r < rows; ++r) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int kk = 0; kk < kSmallK; ++kk)
+      if (kk < k) {
+        const float av = as[kk][r];
+        acc.x = __fadd_rn(acc.x, __fmul_rn(av, bv[kk].x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(av, bv[kk].y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(av, bv[kk].z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(av, bv[kk].w));
+      }
+    float* cr = c + (i0 + r) * ldc + j;
+    if (mask) {
+      const float4 mk = __ldcs(reinterpret_cast<const float4*>(mask + (i0 + r) * ldc + j));
+      acc.x = mk.x > 0.0f ? __fadd_rn(0.0f, acc.x) : 0.0f;
+      acc.y = mk.y > 0.0f ? __fadd_rn(0.0f, acc.y) : 0.0f;
+      acc.z = mk.z > 0.0f ? __fadd_rn(0.0f, acc.z) : 0.0f;
+      acc.w = mk.w > 0.0f ? __fadd_rn(0.0f, acc.w) : 0.0f;
+    }
+    *reinterpret_cast<float4*>(cr) = acc;
+  }
+}
+
 // out[r] = sum_j g[r, j]: a CTA per row, tree reduction
 __global__ void __launch_bounds__(256) k_rowsum_tree(const float* __restrict__ g, int64_t n, float* __restrict__ out) {
   __shared__ float part[8];
@@ -147,8 +199,18 @@ mcf_status mcf_gemm_f32_fast(int trans_a, int trans_b, const float* a, int64_t l
     mcfr::note_launch();
     return mcfr::check_launch("gemm_f32 split-K kernels");
   }
-  // the other shapes outside the int8 path (a dimension below 64 with a short
-  // K, e.g. the 10-class layer's dA, K = 10): the ordered FFMA GEMM
+  // a short K with B's rows contiguous (the 10-class layer's dA, K = 10):
+  // the register-resident small-K kernel (bit-identical to the ordered GEMM)
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!trans_b && k >= 1 && k <= kSmallK && n % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && al16(b) && al16(c) &&
+      (!relu_mask || al16(relu_mask))) {
+    const dim3 grid((unsigned)((n / 4 + 255) / 256), (unsigned)((m + kSmallRows - 1) / kSmallRows));
+    if (trans_a) k_gemm_smallk<true><<<grid, 256, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, (int)k, relu_mask);
+    else k_gemm_smallk<false><<<grid, 256, 0, s>>>(a, lda, b, ldb, c, ldc, m, n, (int)k, relu_mask);
+    mcfr::note_launch();
+    return mcfr::check_launch("gemm_f32 small-K kernel");
+  }
+  // the other shapes outside the int8 path (a dimension below 64): the ordered FFMA GEMM
   return mcf_gemm_f32_ordered(trans_a, trans_b, a, lda, b, ldb, c, ldc, m, n, k, relu_mask, s);
 }
 

@@ -356,3 +356,31 @@ def test_captured_step_replays_the_bits_of_direct_steps(plan_name):
         assert_bits(b2, b, f"b{l}")
     if plan_name == "SEQUENTIAL":
         assert np.array_equal(np.array(got, np.float32).view(np.uint32), G["losses"][2:].view(np.uint32))
+
+
+@pytest.mark.parametrize("ta,k,m,n,masked", [(1, 10, 1024, 512, True), (0, 10, 70, 260, True), (1, 16, 33, 128, False),
+                                             (0, 1, 5, 4, True), (1, 7, 1000, 1028, True)])
+def test_fast_gemm_short_k_is_bitwise_the_ordered_gemm(ta, k, m, n, masked):
+    """Plan FAST's small-K kernel (the class layer's dA = approx(W)^T G, K = 10
+    classes; csrc/mlp_fast.cu k_gemm_smallk) computes fl_mul then fl_add in k
+    order like the reference's matmul2d: every output equals
+    mcf_gemm_f32_ordered bit for bit, with and without the ReLU mask."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(500 + k + m)
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    mask = rng.standard_normal((m, n)).astype(np.float32)
+    a_st = np.ascontiguousarray(A.T if ta else A)
+    da, db, dm = (torch.from_numpy(v).cuda() for v in (a_st, B, mask))
+    lib = mcf.lib()
+    outs = []
+    for fn in (lib.mcf_gemm_f32_fast, lib.mcf_gemm_f32_ordered):
+        dc = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+        assert fn(ta, 0, da.data_ptr(), a_st.shape[1], db.data_ptr(), n, dc.data_ptr(), n, m, n, k,
+                  dm.data_ptr() if masked else None, None) == 0, lib.mcf_last_error()
+        torch.cuda.synchronize()
+        outs.append(dc.cpu().numpy())
+    assert_bits(outs[0], outs[1], "small-K gemm vs ordered gemm")
