@@ -14,3 +14,8 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --log-file gpurun_out/mlp_step_launches.csv python tools/probes/mlp_steps.py > /dev/null 2>&1
 python tools/step_shares.py gpurun_out/mlp_step_launches.csv > gpurun_out/mlp_step_shares.md 2>&1
 head -14 gpurun_out/step_shares.md
+# launch list of the bench command itself (short, headline + config 0 only)
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-extras > gpurun_out/bench_under_ncu.log 2>&1
+python tools/ncu_summary.py gpurun_out/bench_launches.csv > gpurun_out/bench_launches.md 2>&1
+head -30 gpurun_out/bench_launches.md
