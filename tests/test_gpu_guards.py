@@ -117,3 +117,50 @@ def test_elementwise_certified_ops_write_stay_inside(numel):
         got = buf.cpu().numpy()
         assert np.all(got[2 * numel:] == SENTINEL), f"{name}: written past the output"
         assert np.all(np.isfinite(got[: 2 * numel])), f"{name}: interior not fully written"
+
+
+@pytest.mark.parametrize("m,k,n", [(10, 77, 68), (3, 513, 4), (16, 40, 132)])
+def test_short_a_kernel_writes_stay_inside(m, k, n):
+    """mm_skinny.cu (MC x T for m <= 16): ragged column tiles, K tails of the
+    ring stage and the chunk; the words after the m x n x 2 outputs stay."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(31 + m)
+    x = split(rng.uniform(-1, 1, m * k), 2, np.float32).reshape(m, k, 2)
+    w = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    dx, dw = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    total = m * n * 2
+    buf = torch.full((total + 4096,), float(SENTINEL), dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_bmm_mcn(mcf.B32, dx.data_ptr(), 2, dw.data_ptr(), 1, m, k, n, 0, buf.data_ptr(), mcf.FAST, 1,
+                           None) == 0, lib.mcf_last_error()
+    got = buf.cpu().numpy()
+    assert np.all(got[total:] == SENTINEL), "written past the output"
+    want = x.astype(np.float64).sum(-1) @ w.astype(np.float64)
+    res = got[:total].reshape(m, n, 2).astype(np.float64).sum(-1)
+    assert np.allclose(res, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+
+
+def test_small_k_gemm_writes_stay_inside():
+    """k_gemm_smallk (mlp_fast.cu): a padded C (ldc > n) and rows past m keep the sentinel."""
+    import torch
+
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng(41)
+    m, n, k = 70, 260, 10
+    ldc = n + 12
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    da, db = torch.from_numpy(np.ascontiguousarray(A.T)).cuda(), torch.from_numpy(B).cuda()
+    mask = torch.ones((m + 3, ldc), dtype=torch.float32, device="cuda")
+    buf = torch.full((m + 3, ldc), float(SENTINEL), dtype=torch.float32, device="cuda")
+    lib = mcf.lib()
+    assert lib.mcf_gemm_f32_fast(1, 0, da.data_ptr(), m, db.data_ptr(), n, buf.data_ptr(), ldc, m, n, k,
+                                 mask.data_ptr(), None) == 0, lib.mcf_last_error()
+    got = buf.cpu().numpy()
+    assert np.all(got[:m, n:] == SENTINEL) and np.all(got[m:] == SENTINEL)
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.allclose(got[:m, :n], want, rtol=1e-5, atol=1e-5)
