@@ -46,6 +46,7 @@ constexpr float kMagic = 12582912.0f;  // 1.5 2^23
 
 struct Params {
   int stages;  // pair kernel: depth of the shared-memory ring (<= kStages2)
+  int raster;  // row blocks per raster group (tile_coords)
   int m, n, kp, batch, tiles_m, tiles_n;
   int64_t ldo;           // output row stride (elements)
   int mode;              // 0: int32 C, 1: int8 residues C mod m_b
@@ -61,6 +62,20 @@ struct Params {
   int nseg;
   int seg_ka[kMaxBatch], seg_kb[kMaxBatch], seg_kblk[kMaxBatch];
 };
+
+// Tile order inside one batch entry (modulus / segment): row blocks in groups
+// of kRaster, and within a group the column block outermost -- the ~74 tiles
+// in flight then cover kRaster row blocks x ~9 column blocks instead of one
+// row block x every column block, so a wave re-reads a few operand panels
+// from L2 instead of streaming the whole B plane from HBM (16384^3: 14.7 GB
+// per modulus down to 2.3 GB).  r in [0, tiles_m * tiles_n).
+__device__ __forceinline__ void tile_coords(int r, int tiles_m, int tiles_n, int raster, int& mb, int& nb) {
+  const int per_group = raster * tiles_n;
+  const int g = r / per_group, q = r - g * per_group;
+  const int rows = tiles_m - g * raster < raster ? tiles_m - g * raster : raster;  // the last group may be short
+  nb = q / rows;
+  mb = g * raster + (q - nb * rows);
+}
 
 // ---- PTX helpers ----
 
@@ -194,7 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+        const int b = tile / per_b, r = tile - b * per_b;
+        int mb, nb;
+        tile_coords(r, p.tiles_m, p.tiles_n, p.raster, mb, nb);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           mbar_expect_tx(full + stage, kStageBytes);
@@ -242,7 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+      const int b = tile / per_b, r = tile - b * per_b;
+      int mb, nb;
+      tile_coords(r, p.tiles_m, p.tiles_n, p.raster, mb, nb);
       mbar_wait(tfull + acc, aphase);
       fence_after();
       const int row = mb * BM + row_in_tile;
@@ -397,7 +416,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < total; tile += npairs) {
-        const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+        const int b = tile / per_b, r = tile - b * per_b;
+        int mb, nb;
+        tile_coords(r, tiles_m2, p.tiles_n, p.raster, mb, nb);
         const int kbl = p.nseg ? p.seg_kblk[b] : kblocks, ka0 = p.nseg ? p.seg_ka[b] : 0,
                   kb0 = p.nseg ? p.seg_kb[b] : 0, zb = p.nseg ? 0 : b;
         for (int kb = 0; kb < kbl; ++kb) {
@@ -447,7 +468,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = pair; tile < total; tile += npairs) {
-      const int b = tile / per_b, r = tile - b * per_b, mb = r / p.tiles_n, nb = r - mb * p.tiles_n;
+      const int b = tile / per_b, r = tile - b * per_b;
+      int mb, nb;
+      tile_coords(r, tiles_m2, p.tiles_n, p.raster, mb, nb);
       mbar_wait(tfull + acc, aphase);
       fence_after();
       const int row = mb * 256 + row_in_tile;
@@ -529,6 +552,21 @@ bool make_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t kp, in
 
 namespace mcfr {
 
+// row blocks per raster group (MCF_TC_RASTER; default 8).  Measured on B200
+// (r02, 16384^3 x 20 moduli): DRAM reads per modulus 10.1 GB at 8 and 8.3 GB at
+// 16 against ~14 GB unrastered (ncu), the product 99.9 -> 87-91 ms; at that
+// size the GEMM is limited by the sustained power cap (a 4-modulus run of the
+// same shape reaches 3.1 POPS, the 20-modulus run 2.3 POPS at 1.16 GHz), which
+// the DRAM traffic shares.  Config 2 (everything L2-resident) is unchanged.
+static int raster_rows() {
+  static const int n = [] {
+    const char* e = getenv("MCF_TC_RASTER");
+    const int v = e ? atoi(e) : 8;
+    return v < 1 ? 1 : (v > 64 ? 64 : v);
+  }();
+  return n;
+}
+
 // ring depth of the pair kernel (MCF_TC_STAGES, 5..7; default 7).  Measured
 // on B200 (r02, config 2): 5, 6 and 7 stages all give 1.33 ms per product, and
 // the shallower rings (which leave shared memory for the residue /
@@ -573,6 +611,7 @@ mcf_status tc_gemm_s8(const int8_t* a, const int8_t* b, void* out, int64_t m, in
   p.mode = moduli ? 1 : 0;
   p.out = out;
   p.big = kp > 16384;
+  p.raster = raster_rows();
   if (moduli)
     for (int i = 0; i < batch; ++i) {
       const int mm = moduli[i];
@@ -642,6 +681,7 @@ mcf_status tc_gemm_s8_seg(const int8_t* a, int64_t lda, const int8_t* b, int64_t
   p.mode = 0;
   p.out = out;
   p.nseg = nseg;
+  p.raster = raster_rows();
   for (int d = 0; d < nseg; ++d) {
     if (ka[d] % BK || kb[d] % BK || kd[d] % BK || kd[d] <= 0 || ka[d] + kd[d] > lda || kb[d] + kd[d] > ldb ||
         kd[d] >= (1 << 17))
