@@ -133,23 +133,31 @@ __device__ __forceinline__ g2::M2 run_g2_pair(const float (&x)[4], const float (
   return ok;
 }
 
-template <int OP, class P, int NC, int ONC, bool TRY_G2 = true>
+// the wide tier alone (binary32 nc = 2 Div-MCN / DivN / Mul-MCN), branch-free:
+// the TMA kernel runs it for all of a thread's elements before it looks at any
+// verdict, so their independent chains interleave
+template <int OP>
+__device__ __forceinline__ bool run_w2(const float (&x)[2], const float (&y)[2], float v, float (&o)[2]) {
+  using V = w2::VD;
+  bool ok;
+  if constexpr (OP == kDivN) {  // x holds the divisor
+    ok = w2::div<V, true, true>(v, 0.0f, x[0], x[1], true, __fadd_rn(x[0], x[1]) == x[0], o[0], o[1]);
+  } else {
+    const bool cx = __fadd_rn(x[0], x[1]) == x[0], cy = __fadd_rn(y[0], y[1]) == y[0];
+    if constexpr (OP == kDiv) ok = w2::div<V, false, true>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
+    else {
+      ok = w2::mul<V, true>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
+      if (__fadd_rn(y[1], y[0]) == 0.0f || __fadd_rn(x[1], x[0]) == 0.0f) o[0] = o[1] = 0.0f, ok = true;
+    }
+  }
+  return ok;
+}
+
+template <int OP, class P, int NC, int ONC, bool TRY_G2 = true, bool TRY_W2 = true>
 __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[NC], RT<P> v,
                                          RT<P> (&o)[ONC]) {
-  if constexpr (TRY_G2 && kW2<OP, P, NC, ONC>) {
-    using V = w2::VD;
-    bool ok;
-    if constexpr (OP == kDivN) {  // x holds the divisor
-      ok = w2::div<V, true>(v, 0.0f, x[0], x[1], true, __fadd_rn(x[0], x[1]) == x[0], o[0], o[1]);
-    } else {
-      const bool cx = __fadd_rn(x[0], x[1]) == x[0], cy = __fadd_rn(y[0], y[1]) == y[0];
-      if constexpr (OP == kDiv) ok = w2::div<V, false>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
-      else {
-        ok = w2::mul<V>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
-        if (__fadd_rn(y[1], y[0]) == 0.0f || __fadd_rn(x[1], x[0]) == 0.0f) o[0] = o[1] = 0.0f, ok = true;
-      }
-    }
-    if (__builtin_expect(ok, 1)) return true;
+  if constexpr (TRY_G2 && TRY_W2 && kW2<OP, P, NC, ONC>) {
+    if (__builtin_expect(run_w2<OP>(x, y, v, o), 1)) return true;
   }
   if constexpr (TRY_G2 && kG2<OP, P, NC, ONC>) {
     using Q = g2::QF32;
@@ -509,6 +517,38 @@ __global__ void __launch_bounds__(tma::kConsumerWarps * 32 + 32, (kTmaCtas<OP, P
             }
             const RT<P> ve = i == 0 ? v0 : v1;
             if (!run_fast<OP, P, NC, ONC, false>(xa, ya, ve, oa)) bail |= 1u << i;
+#pragma unroll
+            for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
+          }
+      } else if constexpr (kW2<OP, P, NC, ONC>) {
+        // the wide tier for every element first (no branch between them), then
+        // the lower tiers for the declined ones
+        bool acc[EPT];
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          float xa[2], ya[2], oa[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            xa[c] = xs[i * 2 + c];
+            ya[c] = G::kY ? ys[i * 2 + c] : 0.0f;
+          }
+          float ve = 0.0f;
+          if constexpr (G::kV) ve = vmode == 0 ? vv[i] : vscalar;
+          acc[i] = run_w2<OP>(xa, ya, ve, oa);
+          os[i * 2] = oa[0], os[i * 2 + 1] = oa[1];
+        }
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+          if (__builtin_expect(!acc[i], 0)) {
+            RT<P> xa[NC], ya[NC], oa[ONC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              xa[c] = P::ld(xs[i * NC + c]);
+              ya[c] = G::kY ? P::ld(ys[i * NC + c]) : RT<P>(0);
+            }
+            RT<P> ve = RT<P>(0);
+            if constexpr (G::kV) ve = vmode == 0 ? P::ld(vv[i]) : vscalar;
+            if (!run_fast<OP, P, NC, ONC, true, false>(xa, ya, ve, oa)) bail |= 1u << i;
 #pragma unroll
             for (int c = 0; c < ONC; ++c) os[i * ONC + c] = P::sv(oa[c]);
           }

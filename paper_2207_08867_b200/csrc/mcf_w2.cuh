@@ -48,7 +48,7 @@
 // Policy V: N (component type), W (wide type), wide(N), narrow(W) (exact on
 // P-bit values), add/sub/mul/fma/neg/abs on W, rcp_seed(W) (any approximation
 // of 1/y good to ~2^-16), rnpm(W, m, ok) (rnp, and ok &= L - mid outside [-m, 3 m)),
-// span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
+// rnpv(W, ref, lg, ok) (rnp with the absolute margin |ref| 2^(lg - (W-1))), span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
 // rnpe (nearest-even), in_window / below_window on N, kP.
 #pragma once
 
@@ -145,9 +145,47 @@ G2_HD bool div_core(W_<V> X, W_<V> X0, W_<V> Y, W_<V> Y1, W_<V> Yl, W_<V> rY, W_
 }
 
 
+// The same division with ONE explicit digit.  After digit 0 the reference holds
+// r = X - trunc2(q0 (y0 + y1)) exactly (digit() checks it), and what it adds to
+// q0 is q1 + q2 with q1 = fl(r_0 / y_0), r' = trunc2(r - trunc2(q1 Y)), q2 =
+// fl(r'_0 / y_0).  With u = 2^-P (every rounding to P bits and every lead of a
+// compressed pair is within u, relative; a two-component truncation within
+// u^2 (1 + u)):  q1 = (r / Y)(1 + t1), |t1| <= 3 u;  r' = (r - q1 Y (1 + e1))(1 + e2);
+// q2 = (r' / Y)(1 + t2), so
+//   |q1 + q2 - r / Y| <= |r / Y| (|t1| (|e2| + |t2|) + |e1|) (1 + O(u)) <= 10 u^2 |r / Y| (1 + O(u)).
+// R = r rY (1 - y1 rY) is r / Y to u^2 (the dropped (y1 / y0)^2) + 2^-(W-3) (rY)
+// + three wide roundings, so S = q0 + q1 + q2 = q0 + R to within 11.3 u^2 |R|:
+// at most 11.3 x 2 x 2^(W-1-2P) = 362 units of R's last wide place.  The two
+// components of S then follow from (M) as in div_core, the second with an
+// absolute margin of |R| 2^(10 - (W-1)) >= 2^10 units of R's last place: 362, plus
+// the 64 units of (M) and the rounding of w = (q0 - o0) + R in w's own last
+// place, which is at most twice R's (|w| <= half a step of o0 <= |R| (1 + 2^-20)
+// whenever q0 != o0) -- and usually far below it: rnpv measures the margin
+// against w's own P-bit grid.
+// No q1, q2, second product or second remainder: ~2/3 of the instructions.
+// Guards: |R| >= 2^-60 keeps q1 normal and makes a subnormal q2's rounding
+// (<= 2^-150) invisible at w's resolution; |R Yl| >= 2^-85 is the exact-low-part
+// guard for both digits' products (|q1| <= |q0|; R = q1 (1 + 2^-21)).
+template <class V, bool PAIR>
+G2_HD bool div_core1(W_<V> X, W_<V> X0, W_<V> Y, W_<V> Y1, W_<V> Yl, W_<V> rY, W_<V>& o0, W_<V>& o1) {
+  using W = W_<V>;
+  W r = X, r0 = X0, q0;
+  bool ok = digit<V, PAIR>(r, r0, Y, Y1, rY, q0);
+  const W c = V::mul(Y1, rY);
+  const W R0 = V::mul(r, rY);
+  const W R = V::fma(V::neg(R0), c, R0);
+  const W Q = V::add(q0, R);
+  o0 = V::rnpm(Q, 64, ok);
+  const W w = V::add(V::sub(q0, o0), R);
+  o1 = V::rnpv(w, R, V::lg1(), ok);
+  ok &= V::ge(V::abs(R), V::two(-60));
+  ok &= V::ge(V::abs(V::mul(R, Yl)), V::two(-85));
+  return ok;
+}
+
 // mc_ops.hpp:188-207 div_kernel, nc = 2; cx / cy = the reference's compressed
 // predicate fl(c0 + c1) == c0 evaluated by the caller in the component format
-template <class V, bool X1ZERO>
+template <class V, bool X1ZERO, bool ONE = false>
 G2_HD bool div(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& o0, N_<V>& o1) {
   using W = W_<V>;
   const W zero = V::c(0.0);
@@ -166,7 +204,8 @@ G2_HD bool div(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& 
   ok &= recip<V>(Y0, V::rcp_seed(Y0), rY);
   const W Yl = V::eq(Y1, zero) ? Y0 : Y1;
   W w0, w1;
-  ok &= div_core<V, false>(X, X0, Y, Y1, Yl, rY, w0, w1);
+  if constexpr (ONE) ok &= div_core1<V, false>(X, X0, Y, Y1, Yl, rY, w0, w1);
+  else ok &= div_core<V, false>(X, X0, Y, Y1, Yl, rY, w0, w1);
   o0 = V::canon(V::narrow(w0));
   o1 = V::canon(V::narrow(w1));
   return ok;
@@ -174,7 +213,7 @@ G2_HD bool div(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& 
 
 // mc_ops.hpp:216-230 Mul-MCN (fast): x / (1 / y), zero fast path decided by
 // the caller (zx / zy: approx(x) == 0, approx(y) == 0)
-template <class V>
+template <class V, bool ONE = false>
 G2_HD bool mul(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& o0, N_<V>& o1) {
   using W = W_<V>;
   const W zero = V::c(0.0), one = V::c(1.0);
@@ -186,12 +225,14 @@ G2_HD bool mul(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& 
   ok &= recip<V>(Y0, V::rcp_seed(Y0), rY);
   const W Yl = V::eq(Y1, zero) ? Y0 : Y1;
   W c0, c1;
-  ok &= div_core<V, false>(one, one, Y, Y1, Yl, rY, c0, c1);  // recip = 1 / y (compressed by construction)
+  if constexpr (ONE) ok &= div_core1<V, false>(one, one, Y, Y1, Yl, rY, c0, c1);
+  else ok &= div_core<V, false>(one, one, Y, Y1, Yl, rY, c0, c1);  // recip = 1 / y (compressed by construction)
   W rC;
   ok &= recip<V>(c0, Y0, rC);                           // 1 / c0 ~ y0 (to 2^-(P-1)): seed y0
   const W Cl = V::eq(c1, zero) ? c0 : c1;
   W w0, w1;
-  ok &= div_core<V, true>(X, X0, c0, c1, Cl, rC, w0, w1);
+  if constexpr (ONE) ok &= div_core1<V, true>(X, X0, c0, c1, Cl, rC, w0, w1);
+  else ok &= div_core<V, true>(X, X0, c0, c1, Cl, rC, w0, w1);
   o0 = V::canon(V::narrow(w0));
   o1 = V::canon(V::narrow(w1));
   return ok;
@@ -261,6 +302,7 @@ struct VD {
     return r;
   }
   static constexpr int kP = 24;
+  __device__ __forceinline__ static int lg1() { return 10; }  // div_core1's margin: 2^10 units of R's last place
   __device__ __forceinline__ static bool in_window(N a) { return (fabsf(a) >= 0x1p-40f) & (fabsf(a) <= 0x1p40f); }
   __device__ __forceinline__ static bool below_window(N a) { return fabsf(a) <= 0x1p40f; }
   // round to 24 bits on the bit pattern (sign-magnitude: add half a step to
@@ -276,6 +318,20 @@ struct VD {
     const long long b = __double_as_longlong(t) + (0x10000000LL + m);
     ok &= ((unsigned)b & (0x1fffffffu & ~(4u * (unsigned)m - 1u))) != 0u;
     return __longlong_as_double(b & ~0x1fffffffLL);
+  }
+  // rnp(t), accepted when t is farther than |ref| 2^(lg - 52) (>= 2^lg units of
+  // ref's last place) from the nearest midpoint of ITS P-bit grid: the residual
+  // e = t - rnp(t) is exact, half = 2^(e(t) - 24) is half a step of that grid
+  // (one mask-and-subtract on the high word; a zero or tiny t gives a negative
+  // or NaN half and declines), so the distance is half - |e| -- on the FP64
+  // pipe, which has more room than the ALU pipe a variable shift would use
+  __device__ __forceinline__ static W rnpv(W t, W ref, int lg, bool& ok) {
+    const long long b = __double_as_longlong(t) + 0x10000000LL;
+    const double o = __longlong_as_double(b & ~0x1fffffffLL);
+    const double e = __dsub_rn(t, o);
+    const double half = __hiloint2double((__double2hiint(t) & 0x7ff00000) - (24 << 20), 0);
+    ok &= __dsub_rn(half, fabs(e)) > __dmul_rn(fabs(ref), __hiloint2double((1023 + lg - 52) << 20, 0));
+    return o;
   }
   // ties to even: (t + M) - M with M = 1.5 2^(e + 29), e = t's exponent; the
   // sum lies in M's binade, whose spacing 2^(e - 23) is t's 24-bit grid.  M0 =

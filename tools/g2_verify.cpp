@@ -83,6 +83,8 @@ static uint64_t wmant(double t) {  // the W-bit significand of a wide value as a
   int e;
   return (uint64_t)std::ldexp(std::frexp(std::fabs(t), &e), WB());
 }
+static int g_lg1 = 10;    // div_core1's margin (log2 units); G2_LG1 lowers it to probe the bound's slack
+static bool g_only1 = false;  // G2_ONLY1: only the one-digit rows
 struct VE {
   using N = double;
   using W = double;
@@ -102,6 +104,7 @@ struct VE {
   static bool ge(W a, W b) { return a >= b; }
   static bool le(W a, W b) { return a <= b; }
   static W rcp_seed(W y) { return rnw((1.0 / y) * (1.0 + std::ldexp(1.0, -16))); }
+  static int lg1() { return g_lg1; }
   static constexpr int kP_dummy = 0;
   struct KP { operator int() const { return P; } };
   static constexpr KP kP{};
@@ -119,6 +122,13 @@ struct VE {
   static W rnpm(W t, int m, bool& ok) {
     ok &= away(t, m);
     return rnp(t);
+  }
+  static W rnpv(W t, W ref, int lg, bool& ok) {  // as the device: distance to the nearest midpoint of t's grid
+    const W o = rnp(t);
+    if (t == 0 || !std::isfinite(t)) { ok = false; return o; }
+    const double half = std::ldexp(1.0, std::ilogb(t) - P);
+    ok &= sub(half, std::fabs(sub(t, o))) > mul(std::fabs(ref), std::ldexp(1.0, lg - (WB() - 1)));
+    return o;
   }
   static bool away(W t, int m) {
     const int64_t L = (int64_t)(wmant(t) & ((1ull << (WB() - P)) - 1)), mid = 1ll << (WB() - P - 1);
@@ -267,6 +277,7 @@ static bool same(double a, double b) { return std::memcmp(&a, &b, 8) == 0; }
 
 template <class F, class G>
 static void check(Stat& st, F ref, G fast, const char* what) {
+  if (g_only1 && st.name[1] != '1') return;
   double ro[2], fo[2];
   g_cap = false;
   ref(ro);
@@ -319,6 +330,8 @@ static std::vector<std::pair<double, double>> pairs(int K, int mstep) {
 
 int main(int argc, char** argv) {
   const char* mode = argc > 1 ? argv[1] : "small";
+  if (getenv("G2_LG1")) g_lg1 = atoi(getenv("G2_LG1"));
+  g_only1 = getenv("G2_ONLY1") != nullptr;
   using namespace mcfg;
   if (!strcmp(mode, "small")) {
     const int p = argc > 2 ? atoi(argv[2]) : 5;
@@ -327,7 +340,7 @@ int main(int argc, char** argv) {
     auto X = pairs(K, 1);
     const int M = 1 << (P - 1);
     printf("p=%d: %zu compressed pairs\n", P, X.size());
-    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"};
+    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"}, od{"w1div"}, om{"w1mul"};
 #pragma omp parallel for schedule(dynamic, 16)
     for (long long i = 0; i < (long long)X.size(); ++i) {
       const double x[2] = {X[i].first, X[i].second};
@@ -339,6 +352,8 @@ int main(int argc, char** argv) {
               [&](double* o) { return g2::div<QE, true>(vn[0], vn[1], x[0], x[1], o[0], o[1]); }, "divn");
         check(wd, [&](double* o) { ref_div(vn, x, o); },
               [&](double* o) { return w2::div<VE, true>(vn[0], vn[1], x[0], x[1], true, true, o[0], o[1]); }, "divn");
+        check(od, [&](double* o) { ref_div(vn, x, o); },
+              [&](double* o) { return w2::div<VE, true, true>(vn[0], vn[1], x[0], x[1], true, true, o[0], o[1]); }, "divn");
       }
       for (int s = -1; s <= 1; s += 2)
         for (int a = 0; a < M; ++a) {
@@ -359,6 +374,8 @@ int main(int argc, char** argv) {
               [&](double* o) { return g2::div<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "div");
         check(wd, [&](double* o) { ref_div(x, y, o); },
               [&](double* o) { return w2::div<VE, false>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
+        check(od, [&](double* o) { ref_div(x, y, o); },
+              [&](double* o) { return w2::div<VE, false, true>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
         for (int sh = -3; sh <= 3; sh += 3) {  // relative exponent of y
           const double ys[2] = {std::ldexp(y[0], sh), std::ldexp(y[1], sh)};
           check(sa, [&](double* o) { ref_add(x, ys, o); },
@@ -369,17 +386,19 @@ int main(int argc, char** argv) {
                 [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
           check(wm, [&](double* o) { ref_mul(x, y, o); },
                 [&](double* o) { return w2::mul<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
+          check(om, [&](double* o) { ref_mul(x, y, o); },
+                [&](double* o) { return w2::mul<VE, true>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
         }
       }
     }
-    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws);
-    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws), report(od), report(om);
+    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | od.bad | om.bad | ss.cap | sq.cap | sd.cap | sm.cap |
             sa.cap | sg.cap) ? 1 : 0;
   }
   // sampled, config-0 style operands: v = U(-1,1) 2^U(-8,8) split greedily into p-bit comps
   P = argc > 2 ? atoi(argv[2]) : 24;
   const long long N = argc > 3 ? atoll(argv[3]) : 2000000;
-  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"};
+  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"}, od{"w1div"}, om{"w1mul"};
 #pragma omp parallel
   {
     std::mt19937_64 g(1234 + 7919 * (unsigned long long)omp_get_thread_num());
@@ -410,10 +429,16 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::mul<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "mul");
       check(wd, [&](double* o) { ref_div(x, y, o); },
             [&](double* o) { return w2::div<VE, false>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
+      check(od, [&](double* o) { ref_div(x, y, o); },
+            [&](double* o) { return w2::div<VE, false, true>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
       check(wd, [&](double* o) { ref_div(vv, y, o); },
             [&](double* o) { return w2::div<VE, true>(vv[0], vv[1], y[0], y[1], true, true, o[0], o[1]); }, "divn");
+      check(od, [&](double* o) { ref_div(vv, y, o); },
+            [&](double* o) { return w2::div<VE, true, true>(vv[0], vv[1], y[0], y[1], true, true, o[0], o[1]); }, "divn");
       check(wm, [&](double* o) { ref_mul(x, y, o); },
             [&](double* o) { return w2::mul<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
+      check(om, [&](double* o) { ref_mul(x, y, o); },
+            [&](double* o) { return w2::mul<VE, true>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
       check(sa, [&](double* o) { ref_add(x, y, o); },
             [&](double* o) { return g2::add<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "add");
       check(sg, [&](double* o) { ref_grow(x, v, o); },
@@ -423,7 +448,7 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::add<QE>(x[0], x[1], yn[0], yn[1], o[0], o[1]); }, "add");
     }
   }
-  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws);
-  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws), report(od), report(om);
+  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | od.bad | om.bad | ss.cap | sq.cap | sd.cap | sm.cap |
           sa.cap | sg.cap) ? 1 : 0;
 }
