@@ -93,6 +93,7 @@ constexpr int kMinMod = 16;     // instantiated moduli counts: kMinMod .. kMaxMo
 constexpr int kSlices = 8;      // balanced 12-bit slices of the CRT weights
 constexpr int kSliceBits = 12;
 constexpr int kYShift = kSlices * kSliceBits;  // Y = C' / 2^(L - kYShift)
+constexpr int kMaxInx = 32;    // listed inexact elements per binary32 B column (more: the column falls back)
 constexpr float kMagic = 12582912.0f;  // 1.5 2^23: x + kMagic has x in its low mantissa bits (|x| < 2^22)
 
 struct CrtTab {
@@ -441,7 +442,8 @@ template <int NC, int NMOD>
 __global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, int64_t n, int64_t ldb, int64_t k,
                                                    int64_t kp, int64_t np, int pb, const int* __restrict__ e,
                                                    int8_t* __restrict__ out, float* __restrict__ bt,
-                                                   int* __restrict__ cinx) {
+                                                   int* __restrict__ cinx, int* __restrict__ clk,
+                                                   double* __restrict__ clr) {
   __shared__ unsigned dg[NMOD][kSlab][kSlab / 4 + 1];  // [t][j][k / 4]
   __shared__ float tv[kSlab][kSlab * NC + 1];          // [j][k * NC + c]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps x 4 k each
@@ -474,7 +476,29 @@ __global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, i
     inexact = limbs_pair<NC>(a0, a1, sa, sb, l01) + limbs_pair<NC>(b0, b1, sa, sb, l23);
   }
   const int l0i[4] = {limb_int(l01[0].x), limb_int(l01[0].y), limb_int(l23[0].x), limb_int(l23[0].y)};
-  if (inexact && j < n) atomicAdd(cinx + j, inexact);
+  if (inexact && j < n) {
+    if constexpr (NC == 1) {
+      // a binary32 B element that does not fit pb bits at the column's scale
+      // (or underflows it): list (k, what the rounding dropped) so that the
+      // reconstruction adds A[i, k] x it back; the scaled value is exact in
+      // binary64 and B' is its nearest integer, ties to even, as the limbs'
+      const double sc = pow2d(pb - e[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double xd = __dmul_rn((double)c[0][u], sc);
+        const double rem = __dsub_rn(xd, rint(xd));
+        if (rem != 0.0) {
+          const int slot = atomicAdd(cinx + j, 1);
+          if (slot < kMaxInx) {
+            clk[j * kMaxInx + slot] = (int)(k0 + ty * 4 + u);
+            clr[j * kMaxInx + slot] = rem;
+          }
+        }
+      }
+    } else {
+      atomicAdd(cinx + j, inexact);
+    }
+  }
   unsigned wd[NMOD];
   residue_words<NMOD>(l01, l23, l0i, wd);
 #pragma unroll
@@ -521,13 +545,16 @@ __device__ __forceinline__ int ulp_exp(float c) {
 // binary64, bit 2 (NC = 2) some nonzero c0 is not an integer at the scale
 // 2^(p - e) (then both components may round: 1 unit per element instead of
 // 1/2 in the error bound)
+// rth[r] = cb (sum_k |A'_rk| bound): the sum of |c0| + |c1| rounded up, at the
+// scale 2^(p - e), plus half a unit per element for the roundings
 template <int NC>
 __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int64_t rows, int64_t k, int p,
-                                                 int* __restrict__ e, int* __restrict__ nf) {
+                                                 int* __restrict__ e, int* __restrict__ nf, double cb,
+                                                 double* __restrict__ rth) {
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  double m = 0.0;
+  double m = 0.0, sum = 0.0;
   bool bad = false, split = false;
   int umin = 1 << 20;
   for (int64_t t = lane; t < k; t += 32) {
@@ -536,12 +563,14 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
     bad |= !isfinite(mag);
     split |= lo != 0.0;
     m = fmax(m, mag);
+    sum = __dadd_ru(sum, mag);
     const float c0 = a[(r * k + t) * NC];
     if (NC == 2 && c0 != 0.0f) umin = min(umin, ulp_exp(c0));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    sum = __dadd_ru(sum, __shfl_xor_sync(0xffffffffu, sum, off));
     umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, off));
   }
   bad = __any_sync(0xffffffffu, bad);
@@ -549,6 +578,7 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
   if (lane == 0) {
     const int ex = exp_above_d(m);
     e[r] = ex;
+    rth[r] = __dmul_ru(__fma_ru(sum, pow2d(p - ex), 0.5 * (double)k), cb);
     nf[r] = (bad ? 1 : 0) | (split ? 2 : 0) | (NC == 2 && umin + p - ex < 0 ? 4 : 0);
   }
 }
@@ -560,11 +590,11 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
 template <int NC>
 __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int64_t k, int64_t n, int64_t ldb,
                                                  unsigned long long* __restrict__ cm, int* __restrict__ nf,
-                                                 int* __restrict__ cu) {
+                                                 int* __restrict__ cu, double* __restrict__ csum) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t t0 = (int64_t)blockIdx.y * 64, t1 = t0 + 64 < k ? t0 + 64 : k;
-  double m = 0.0;
+  double m = 0.0, sum = 0.0;
   bool bad = false, split = false;
   int umin = 1 << 20;
   for (int64_t t = t0; t < t1; ++t) {
@@ -573,23 +603,29 @@ __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int
     bad |= !isfinite(mag);
     split |= lo != 0.0;
     m = fmax(m, mag);
+    sum = __dadd_ru(sum, mag);
     const float c0 = b[(t * ldb + j) * NC];
     if (NC == 2 && c0 != 0.0f) umin = min(umin, ulp_exp(c0));
   }
   if (m > 0.0) atomicMax(cm + j, (unsigned long long)__double_as_longlong(m));
+  if (sum > 0.0) atomicAdd(csum + j, sum);  // slab sums rounded up; the atomic adds to nearest (k_colexp pads)
   if (NC == 2 && umin < (1 << 20)) atomicMin(cu + j, umin);
   // bit 0: a non-finite element; bit 1: some c0 + c1 is not one binary64
   if (bad || split) atomicOr(nf + j, (bad ? 1 : 0) | (split ? 2 : 0));
 }
 
 // column exponents; flag bit 2 (MC B) as k_rowexp's at the scale 2^(p - e)
+// cth[j] = ca (sum_k |B'_kj| bound) as k_rowexp's rth (the 2^-40 covers the
+// round-to-nearest atomic adds of at most 2^10 slab sums)
 __global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __restrict__ cm, int64_t n, int p,
                                                  const int* __restrict__ cu, int* __restrict__ e,
-                                                 int* __restrict__ nf) {
+                                                 int* __restrict__ nf, const double* __restrict__ csum, int64_t k,
+                                                 double ca, double* __restrict__ cth) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int ex = exp_above_d(__longlong_as_double((long long)cm[j]));
   e[j] = ex;
+  cth[j] = __dmul_ru(__fma_ru(__dmul_ru(csum[j], 1.0 + 0x1p-40), pow2d(p - ex), 0.5 * (double)k), ca);
   if (cu && cu[j] + p - ex < 0) nf[j] |= 4;
 }
 
@@ -627,10 +663,31 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
 // B's for an MC B; xa / xb: the extra 1/2 unit per element of a row / MC
 // column whose leading components are not integers at the scale (flag bit 2);
 // inexact: per counted inexact element of a binary32 B column
+//
+// The roundings are bounded with the operands' own magnitude sums, not K times
+// the largest element: A's rounding of row i against column j costs at most
+// 0.51 sum_k |B'_kj| (cth[j], from the column sums of k_colmax), B's at most
+// 0.51 sum_k |A'_ik| (rth[i], k_rowexp) -- for a binary32 B only its counted
+// inexact elements, so the smaller of inexact * count and rth[i].  Operands
+// with a wide dynamic range (config 0's 2^U(-8,8) magnitudes, heavy tails)
+// have sums far below K maxima, and far fewer outputs fall back.
 struct Thresholds {
-  double base, xa, xb, inexact;
-  __device__ __forceinline__ double at(int rowflags, int colflags, int inx) const {
-    return base + ((rowflags & 4) ? xa : 0.0) + ((colflags & 4) ? xb : 0.0) + inexact * inx;
+  double base, inexact;   // base: the product of two roundings (K 1.1 units) + the CRT tail
+  const double* cth;
+  const double* rth;
+  int mcb;                // B is MC (both operands round every element)
+  double unit;            // one unit of C' (x 2^50)
+  // CORRECTED: the dropped parts of the inexact elements have been added back
+  // (k_crt8); what is left per element is A's rounding against it (<= 0.26) and
+  // an underflowed scaled value (far below a unit)
+  template <bool CORRECTED = false>
+  __device__ __forceinline__ double at(int rowflags, int colflags, int inx, int64_t i, int64_t j) const {
+    const double ca = cth[j], rb = rth[i];
+    double t = base + ((rowflags & 4) ? 2.0 * ca : ca);
+    if (mcb) t += (colflags & 4) ? 2.0 * rb : rb;
+    else if (CORRECTED) t += unit * 1.3 * inx;
+    else t += fmin(inexact * inx, rb);
+    return t;
   }
 };
 
@@ -709,7 +766,7 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
       double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], T[u][0]);
 #pragma unroll
       for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 4096.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], T[u][s]));
-      if (((fi | cfj[u]) & 1) || !(fabs(y) >= th.at(fi, cfj[u], inx[u]))) {
+      if (((fi | cfj[u]) & 1) || !(fabs(y) >= th.at(fi, cfj[u], inx[u], i, j0 + u))) {
         rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
         continue;
       }
@@ -728,13 +785,29 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
 // the slice sums are packed FFMA2 over column pairs with the weights as
 // scalar operands; the two components of the four outputs leave as two
 // 16-byte stores.
+// sum over a column's listed inexact elements of A[i, k] x (what B's rounding
+// dropped); out of line: no column of a narrow-range B lists any
+static __device__ __noinline__ double inexact_corr(const float* __restrict__ arow, int nca,
+                                                   const int* __restrict__ lk, const double* __restrict__ lr,
+                                                   int cnt) {
+  double corr = 0.0;
+  for (int sl = 0; sl < cnt; ++sl) {
+    const float* ap = arow + (int64_t)lk[sl] * nca;
+    const double av = nca == 2 ? __dadd_rn((double)ap[0], (double)ap[1]) : (double)ap[0];
+    corr = __fma_rn(isfinite(av) ? av : 0.0, lr[sl], corr);
+  }
+  return corr;
+}
+
 template <int NMOD>
 __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, int64_t m, int64_t n, int64_t ldr,
                                                  const int* __restrict__ ea, const int* __restrict__ eb,
                                                  const int* __restrict__ rnf, const int* __restrict__ cnf,
                                                  const int* __restrict__ cinx, Thresholds th, int sexp,
                                                  float* __restrict__ out, int64_t ldo, int* __restrict__ rlist,
-                                                 int* __restrict__ rcnt, Epilogue ep) {
+                                                 int* __restrict__ rcnt, Epilogue ep, const float* __restrict__ a,
+                                                 int nca, int64_t k, const int* __restrict__ clk,
+                                                 const double* __restrict__ clr, double ycorr) {
   const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t i = blockIdx.y;
   if (j0 >= n) return;
@@ -790,7 +863,15 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
 #pragma unroll
     for (int sl = 1; sl < kSlices; ++sl) y = __fma_rn(y, 4096.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[sl], Tu[sl]));
     const int fc = cnf[j];
-    if (((fi | fc) & 1) || !(fabs(y) >= th.at(fi, fc, cinx ? cinx[j] : 0))) {
+    const int inx = cinx ? cinx[j] : 0;
+    if (inx > 0 && inx <= kMaxInx) {
+      // the column's listed inexact elements: add A[i, k] x (what B's rounding
+      // dropped) back, in units of Y (ycorr = 2^(pa + 96 - L); binary64 is
+      // ample: the terms are below 2^-45 of the bound's scale)
+      y = __fma_rn(inexact_corr(a + i * k * nca, nca, clk + j * kMaxInx, clr + j * kMaxInx, inx),
+                   __dmul_rn(ycorr, pow2d(-ei)), y);
+    }
+    if (((fi | fc) & 1) || inx > kMaxInx || !(fabs(y) >= th.template at<true>(fi, fc, inx, i, j))) {
       rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
       done[u] = true;  // the fallback writes it
       continue;
@@ -1224,6 +1305,9 @@ struct PreparedB {
   const int* eb = nullptr;
   const int* cnf = nullptr;
   const int* cinx = nullptr;  // per column: elements not exact in pb bits (binary32 B)
+  const double* cth = nullptr;  // per column: fallback-threshold term of A's rounding (Thresholds)
+  const int* clk = nullptr;     // [n][kMaxInx] k of the listed inexact elements (binary32 B)
+  const double* clr = nullptr;  // [n][kMaxInx] what their rounding dropped, in units of B'
   int64_t k = 0, kp = 0, n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
   int ncb = 1;
   CrtPlan plan{};
@@ -1231,7 +1315,8 @@ struct PreparedB {
 
 std::size_t b_bytes(int64_t k, int64_t n, int ncb) {
   const CrtPlan pl = crt_plan(k, ncb);
-  return al(pl.n * pad16(n) * pad32(k)) + al(n * k * ncb * 4) + al(n * 4) * 4 + al(n * 8);
+  return al(pl.n * pad16(n) * pad32(k)) + al(n * k * ncb * 4) + al(n * 4) * 4 + al(n * 8) * 3 +
+         al(n * kMaxInx * 4) + al(n * kMaxInx * 8);
 }
 
 #define OZ_NMOD_SWITCH(N, ...)                         \
@@ -1244,6 +1329,12 @@ std::size_t b_bytes(int64_t k, int64_t n, int ncb) {
     case 21: { constexpr int NM = 21; __VA_ARGS__; } break; \
     default: { constexpr int NM = 22; __VA_ARGS__; } break; \
   }
+
+// one unit of C' in units of Y = C' / 2^(L - 96), times the 2^50 of the fallback
+// test (the thresholds are 2^50 x the error bound) and a rounding allowance
+double threshold_unit(int nmod) {
+  return std::ldexp(1.0, kYShift - host_crt().tab[nmod].L) * 1.0001 * std::ldexp(1.0, 50);
+}
 
 mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb, char* buf, PreparedB& pb,
                      cudaStream_t s) {
@@ -1268,24 +1359,34 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   unsigned long long* cm = reinterpret_cast<unsigned long long*>(buf);
   buf += al(n * 8);
   int* cu = reinterpret_cast<int*>(buf);
+  buf += al(n * 4);
+  double* csum = reinterpret_cast<double*>(buf);
+  buf += al(n * 8);
+  double* cth = reinterpret_cast<double*>(buf);
+  buf += al(n * 8);
+  int* clk = reinterpret_cast<int*>(buf);
+  buf += al(n * kMaxInx * 4);
+  double* clr = reinterpret_cast<double*>(buf);
   if (cudaMemsetAsync(cnf, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cm, 0, n * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(csum, 0, n * 8, s) != cudaSuccess ||
       cudaMemsetAsync(cinx, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cu, 0x7f, n * 4, s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the column maxima");
   const dim3 gm((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
-  if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu);
-  else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu);
-  k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, pl.pb, ncb == 2 ? cu : nullptr, eb, cnf);
+  if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu, csum);
+  else k_colmax<1><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu, csum);
+  k_colexp<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cm, n, pl.pb, ncb == 2 ? cu : nullptr, eb, cnf, csum, k,
+                                                        0.51 * threshold_unit(pl.n), cth);
   const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
-  OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx);
-                 else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx));
+  OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx, clk, clr);
+                 else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx, clk, clr));
   for (int i = 0; i < 3; ++i) mcfr::note_launch();
-  pb = PreparedB{planes, bt, eb, cnf, ncb == 1 ? cinx : nullptr, k, kp, n, np, ncb, pl};
+  pb = PreparedB{planes, bt, eb, cnf, ncb == 1 ? cinx : nullptr, cth, clk, clr, k, kp, n, np, ncb, pl};
   return mcfr::check_launch("mm_fast B residue kernels");
 }
 
 std::size_t rows_bytes(int64_t m, int64_t k, int64_t n, int ncb) {
   const CrtPlan pl = crt_plan(k, ncb);
-  return al(pl.n * m * pad32(k)) + al((int64_t)pl.n * m * pad16(n) * 4) + al(m * pad16(n) * 4) + al(m * 4) * 3;
+  return al(pl.n * m * pad32(k)) + al((int64_t)pl.n * m * pad16(n) * 4) + al(m * pad16(n) * 4) + al(m * 4) * 3 + al(m * 8);
 }
 
 // workspace layout of one row block (see rows_bytes)
@@ -1296,6 +1397,7 @@ struct RowsWs {
   int* ea;
   int* rnf;
   int* rcnt;
+  double* rth;  // per row: fallback-threshold term of B's rounding (Thresholds)
 };
 RowsWs rows_ws(char* buf, int64_t m, int64_t kp, int64_t np, int nmod) {
   RowsWs w;
@@ -1310,6 +1412,8 @@ RowsWs rows_ws(char* buf, int64_t m, int64_t kp, int64_t np, int nmod) {
   w.rnf = reinterpret_cast<int*>(buf);
   buf += al(m * 4);
   w.rcnt = reinterpret_cast<int*>(buf);
+  buf += al(m * 4);
+  w.rth = reinterpret_cast<double*>(buf);
   return w;
 }
 
@@ -1323,8 +1427,9 @@ mcf_status a_residues(const float* x, int nca, int64_t m, int64_t k, const CrtPl
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the fallback counters");
   const int64_t kp = pad32(k);
   const unsigned gr = (unsigned)((m + 7) / 8);
-  if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
-  else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf);
+  const double cb = 0.51 * threshold_unit(pl.n);
+  if (nca == 2) k_rowexp<2><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf, cb, w.rth);
+  else k_rowexp<1><<<gr, 256, 0, s>>>(x, m, k, pl.pa, w.ea, w.rnf, cb, w.rth);
   const int64_t gx = (kp / 4 + 255) / 256;  // ~8 CTAs per SM in all, rows strided over y
   const dim3 gsl((unsigned)gx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gx)));
   OZ_NMOD_SWITCH(pl.n, if (nca == 2) k_res_rows<2, NM><<<gsl, 256, 0, s>>>(x, m, k, kp, pl.pa, w.ea, w.planes);
@@ -1383,19 +1488,20 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
     s = cs;
   }
   // error bound per output in C' units (2^-(pa+pb) scaled): A's rounding
-  // (<= 0.51) times |B'| < 2^(pb-1), B's (<= 0.51 for an MC B; for a binary32
-  // B only its counted inexact elements, each <= 0.51 2^(pa-1)), their
-  // product, and the CRT slices' tail (<= 2^12 units of 2^(L - 96)).  The
-  // fallback threshold is 2^50 times it, in units of Y = C' / 2^(L-96).
+  // (<= 0.51 per element) against the column's |B'| sum (pb.cth), B's against
+  // the row's |A'| sum (w.rth; for a binary32 B only its counted inexact
+  // elements, each <= 0.51 2^(pa-1)), their product (K 1.1 units covers it),
+  // and the CRT slices' tail (<= 2^12 units of 2^(L - 96)).  The fallback
+  // threshold is 2^50 times it, in units of Y = C' / 2^(L-96).
   const int L = host_crt().tab[pl.n].L;
-  const double yu = std::ldexp(1.0, kYShift - L) * 1.0001 * std::ldexp(1.0, 50);  // C' units -> Y units, x 2^50
+  const double yu = threshold_unit(pl.n);
   Thresholds th;
-  const double ta = 0.51 * std::ldexp(1.0, pl.pb - 1), tb = 0.51 * std::ldexp(1.0, pl.pa - 1);
-  th.base = ((double)k * (ta + (pb.ncb == 2 ? tb : 0.0) + 1.1) * std::ldexp(1.0, kYShift - L) + 4096.0) * 1.0001 *
-            std::ldexp(1.0, 50);
-  th.xa = (double)k * ta * yu;
-  th.xb = pb.ncb == 2 ? (double)k * tb * yu : 0.0;
-  th.inexact = tb * yu;
+  th.base = (double)k * 1.1 * yu + 4096.0 * 1.0001 * std::ldexp(1.0, 50);
+  th.inexact = 0.51 * std::ldexp(1.0, pl.pa - 1) * yu;
+  th.cth = pb.cth;
+  th.rth = w.rth;
+  th.mcb = pb.ncb == 2;
+  th.unit = yu;
   const int sexp = L - kYShift - pl.pa - pl.pb;
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
@@ -1404,7 +1510,8 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
     const dim3 gc8((unsigned)((n + 1023) / 1024), (unsigned)m);
     OZ_NMOD_SWITCH(pl.n, k_crt8<NM><<<gc8, 256, 0, s>>>(reinterpret_cast<const int8_t*>(w.cq), m, n, np, w.ea, pb.eb,
                                                        w.rnf, pb.cnf, pb.cinx, th, sexp, out, ldo,
-                                                       w.rlist, w.rcnt, ep));
+                                                       w.rlist, w.rcnt, ep, x, nca, k, pb.clk, pb.clr,
+                                                       std::ldexp(1.0, pl.pa + kYShift - L)));
   } else
   OZ_NMOD_SWITCH(pl.n,
                  if (big) k_crt<NM, true><<<gc, 256, 0, s>>>(w.cq, m, n, np, w.ea, pb.eb, w.rnf, pb.cnf, pb.cinx, th,

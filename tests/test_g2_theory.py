@@ -66,13 +66,30 @@ def test_exhaustive_small_precision(g2v, p, k):
 
 def test_one_digit_core_exhaustive_p6(g2v):
     """Every compressed pair at p = 6 (second components up to one binade below
-    the first's last place) through the one-digit division core: accepted
-    cases bit-identical to the reference's three-digit div_kernel / Mul-MCN."""
-    rows, rc = _run(g2v, "small", 6, 0, env={"G2_ONLY1": "1"})
+    the first's last place) through the one-digit division core, with the
+    margin set FOUR TIMES BELOW the certified one (2^8 units; at 2^10 the
+    margin covers the whole rounding interval of this small format): every
+    accepted case -- a superset of what the certified margin would accept --
+    is bit-identical to the reference's three-digit div_kernel / Mul-MCN.
+    (The same run over second components six binades down, 826.7 M divisions
+    and 275.3 M multiplications, has zero mismatches: DESIGN 4.3c.)"""
+    rows, rc = _run(g2v, "small", 6, 0, env={"G2_ONLY1": "1", "G2_LG1": "8"})
     for op in ONE_DIGIT:
         r = rows[op]
         assert r["bad"] == 0 and r["cap"] == 0, (op, r)
-        assert r["cases"] > 10_000_000 and r["acc"] > 3.0, (op, r)
+        assert r["cases"] > 5_000_000 and r["acc"] > 10.0, (op, r)
+    assert rc == 0
+
+
+@pytest.mark.parametrize("p", [8, 10, 12])
+def test_one_digit_core_sampled_mid_precisions(g2v, p):
+    """The certified margin itself at precisions where it leaves room: sampled
+    config-0 operands, accepted cases bit-identical."""
+    rows, rc = _run(g2v, "sample", p, 1000000, env={"G2_ONLY1": "1"})
+    for op in ONE_DIGIT:
+        r = rows[op]
+        assert r["bad"] == 0 and r["cap"] == 0, (op, r)
+        assert r["acc"] > 15.0, (op, r)
     assert rc == 0
 
 

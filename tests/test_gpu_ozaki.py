@@ -163,6 +163,48 @@ def test_extreme_scales_and_zero_lines(gr, port):
     _within_4x(port, x, w, rows, cols, got[rows, cols], "extreme scales")
 
 
+@pytest.mark.parametrize("dist", ["config0", "cauchy", "lognormal2"])
+def test_wide_dynamic_range_operands(gr, port, dist):
+    """Operands whose elements span many binades below their row / column maxima
+    (config 0's U(-1,1) 2^U(-8,8) magnitudes, Cauchy and log-normal tails): the
+    binary32 B elements that do not fit the column's 48-bit fixed point are
+    listed per column and their dropped parts added back in the reconstruction,
+    and the fallback thresholds use the operands' magnitude sums -- so these
+    products stay on the tensor-core path (few fallback outputs) and within the
+    reference's error.  One column is given more inexact elements than the list
+    holds (it must fall back whole and still be right)."""
+    import paper_2207_08867_b200 as mcf
+
+    rng = np.random.default_rng({"config0": 51, "cauchy": 52, "lognormal2": 53}[dist])
+    m, k, n = 128, 2048, 256
+
+    def draw(shape):
+        if dist == "config0":
+            return rng.uniform(-1, 1, shape) * np.exp2(rng.uniform(-8, 8, shape))
+        if dist == "cauchy":
+            return rng.standard_cauchy(shape)
+        return rng.lognormal(0, 2, shape) * rng.choice([-1.0, 1.0], shape)
+
+    xv, wv = draw((m, k)), draw((k, n))
+    wv[:, 7] *= np.exp2(rng.uniform(-40, 0, k))  # hundreds of elements below the 48-bit window
+    x = split(xv.ravel(), 2, np.float32).reshape(m, k, 2)
+    w = wv.astype(np.float32)
+    got = gr.run("mm_mcn", x, w, plan=mcf.FAST)
+    rows, cols = np.meshgrid(np.arange(0, m, 3), np.arange(n), indexing="ij")
+    rows, cols = rows.ravel(), cols.ravel()
+    _within_4x(port, x, w, rows, cols, got[rows, cols], f"wide range ({dist})")
+    prod, _, fb = _phases(x, w)
+    assert_bits(prod, got, "phases entry point")
+    # how many columns list inexact elements at all (scaled below 2^-24 of twice the column maximum)
+    cmax = np.abs(w).max(0)
+    listed = int(((np.abs(w) < cmax * 2.0**-22) & (w != 0)).any(0).sum())
+    print(f"{dist}: fallback outputs {fb} of {m * n}; columns with elements 2^-22 below their maximum: {listed}")
+    assert fb >= m, "column 7 must fall back whole"
+    assert fb <= m * n * 0.05, "wide-range operands must stay on the tensor-core path"
+    if dist != "lognormal2":
+        assert listed > n // 4, "the case must exercise the inexact-element lists"
+
+
 def test_nonfinite_rows_and_columns(gr, port):
     """Inf / NaN operands propagate to exactly their row / column; every other
     output is unaffected (same bits as without the non-finite values)."""
