@@ -93,7 +93,7 @@ constexpr int kMinMod = 16;     // instantiated moduli counts: kMinMod .. kMaxMo
 constexpr int kSlices = 8;      // balanced 12-bit slices of the CRT weights
 constexpr int kSliceBits = 12;
 constexpr int kYShift = kSlices * kSliceBits;  // Y = C' / 2^(L - kYShift)
-constexpr int kMaxInx = 32;    // listed inexact elements per binary32 B column (more: the column falls back)
+constexpr int kMaxInx = 128;   // listed inexact elements per binary32 B column (more: the column falls back)
 constexpr float kMagic = 12582912.0f;  // 1.5 2^23: x + kMagic has x in its low mantissa bits (|x| < 2^22)
 
 struct CrtTab {
@@ -438,8 +438,31 @@ __global__ void __launch_bounds__(256) k_res_rows(const float* __restrict__ a, i
 // 32 k x 32 j: lane = column (coalesced loads along n), each thread four
 // consecutive k packed into one 32-bit word per modulus; shared rows padded to
 // 9 words so the lanes' stores hit distinct banks.
+// binary32 B elements that do not fit pb bits at the column's scale 2^sh (or
+// underflow it): list (k, what the rounding dropped) so that the
+// reconstruction adds A[i, k] x it back.  The scaled value is exact in
+// binary64 and B' is its nearest integer, ties to even, as the limbs'.  Out of
+// line: a narrow-range B never gets here.
+static __device__ __noinline__ void list_inexact(float c0, float c1, float c2, float c3, int sh, int kbase,
+                                                 int* __restrict__ cnt, int* __restrict__ lk,
+                                                 double* __restrict__ lr) {
+  const float c[4] = {c0, c1, c2, c3};
+  const double sc = pow2d(sh);
+  for (int u = 0; u < 4; ++u) {
+    const double xd = __dmul_rn((double)c[u], sc);
+    const double rem = __dsub_rn(xd, rint(xd));
+    if (rem != 0.0) {
+      const int slot = atomicAdd(cnt, 1);
+      if (slot < kMaxInx) {
+        lk[slot] = kbase + u;
+        lr[slot] = rem;
+      }
+    }
+  }
+}
+
 template <int NC, int NMOD>
-__global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, int64_t n, int64_t ldb, int64_t k,
+__global__ void __launch_bounds__(256, 4) k_res_cols(const float* __restrict__ b, int64_t n, int64_t ldb, int64_t k,
                                                    int64_t kp, int64_t np, int pb, const int* __restrict__ e,
                                                    int8_t* __restrict__ out, float* __restrict__ bt,
                                                    int* __restrict__ cinx, int* __restrict__ clk,
@@ -478,23 +501,8 @@ __global__ void __launch_bounds__(256) k_res_cols(const float* __restrict__ b, i
   const int l0i[4] = {limb_int(l01[0].x), limb_int(l01[0].y), limb_int(l23[0].x), limb_int(l23[0].y)};
   if (inexact && j < n) {
     if constexpr (NC == 1) {
-      // a binary32 B element that does not fit pb bits at the column's scale
-      // (or underflows it): list (k, what the rounding dropped) so that the
-      // reconstruction adds A[i, k] x it back; the scaled value is exact in
-      // binary64 and B' is its nearest integer, ties to even, as the limbs'
-      const double sc = pow2d(pb - e[j]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double xd = __dmul_rn((double)c[0][u], sc);
-        const double rem = __dsub_rn(xd, rint(xd));
-        if (rem != 0.0) {
-          const int slot = atomicAdd(cinx + j, 1);
-          if (slot < kMaxInx) {
-            clk[j * kMaxInx + slot] = (int)(k0 + ty * 4 + u);
-            clr[j * kMaxInx + slot] = rem;
-          }
-        }
-      }
+      list_inexact(c[0][0], c[0][1], c[0][2], c[0][3], pb - e[j], (int)(k0 + ty * 4), cinx + j, clk + j * kMaxInx,
+                   clr + j * kMaxInx);
     } else {
       atomicAdd(cinx + j, inexact);
     }
@@ -550,11 +558,12 @@ __device__ __forceinline__ int ulp_exp(float c) {
 template <int NC>
 __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int64_t rows, int64_t k, int p,
                                                  int* __restrict__ e, int* __restrict__ nf, double cb,
-                                                 double* __restrict__ rth) {
+                                                 float* __restrict__ rth) {
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  double m = 0.0, sum = 0.0;
+  double m = 0.0;
+  float sum = 0.0f;  // binary32, every add rounded up (the FMA pipe is idle here): an upper bound
   bool bad = false, split = false;
   int umin = 1 << 20;
   for (int64_t t = lane; t < k; t += 32) {
@@ -563,14 +572,14 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
     bad |= !isfinite(mag);
     split |= lo != 0.0;
     m = fmax(m, mag);
-    sum = __dadd_ru(sum, mag);
     const float c0 = a[(r * k + t) * NC];
+    sum = __fadd_ru(sum, NC == 2 ? __fadd_ru(fabsf(c0), fabsf(a[(r * k + t) * NC + NC - 1])) : fabsf(c0));
     if (NC == 2 && c0 != 0.0f) umin = min(umin, ulp_exp(c0));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    sum = __dadd_ru(sum, __shfl_xor_sync(0xffffffffu, sum, off));
+    sum = __fadd_ru(sum, __shfl_xor_sync(0xffffffffu, sum, off));
     umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, off));
   }
   bad = __any_sync(0xffffffffu, bad);
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
   if (lane == 0) {
     const int ex = exp_above_d(m);
     e[r] = ex;
-    rth[r] = __dmul_ru(__fma_ru(sum, pow2d(p - ex), 0.5 * (double)k), cb);
+    rth[r] = __double2float_ru(__dmul_ru(__fma_ru((double)sum, pow2d(p - ex), 0.5 * (double)k), cb));
     nf[r] = (bad ? 1 : 0) | (split ? 2 : 0) | (NC == 2 && umin + p - ex < 0 ? 4 : 0);
   }
 }
@@ -590,11 +599,12 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
 template <int NC>
 __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int64_t k, int64_t n, int64_t ldb,
                                                  unsigned long long* __restrict__ cm, int* __restrict__ nf,
-                                                 int* __restrict__ cu, double* __restrict__ csum) {
+                                                 int* __restrict__ cu, float* __restrict__ csum) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int64_t t0 = (int64_t)blockIdx.y * 64, t1 = t0 + 64 < k ? t0 + 64 : k;
-  double m = 0.0, sum = 0.0;
+  double m = 0.0;
+  float sum = 0.0f;  // as k_rowexp's
   bool bad = false, split = false;
   int umin = 1 << 20;
   for (int64_t t = t0; t < t1; ++t) {
@@ -603,30 +613,44 @@ __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int
     bad |= !isfinite(mag);
     split |= lo != 0.0;
     m = fmax(m, mag);
-    sum = __dadd_ru(sum, mag);
     const float c0 = b[(t * ldb + j) * NC];
+    sum = __fadd_ru(sum, NC == 2 ? __fadd_ru(fabsf(c0), fabsf(b[(t * ldb + j) * NC + NC - 1])) : fabsf(c0));
     if (NC == 2 && c0 != 0.0f) umin = min(umin, ulp_exp(c0));
   }
   if (m > 0.0) atomicMax(cm + j, (unsigned long long)__double_as_longlong(m));
-  if (sum > 0.0) atomicAdd(csum + j, sum);  // slab sums rounded up; the atomic adds to nearest (k_colexp pads)
+  if (sum > 0.0f) atomicAdd(csum + j, sum);  // slab sums rounded up; the atomic adds to nearest (k_colexp pads)
   if (NC == 2 && umin < (1 << 20)) atomicMin(cu + j, umin);
   // bit 0: a non-finite element; bit 1: some c0 + c1 is not one binary64
   if (bad || split) atomicOr(nf + j, (bad ? 1 : 0) | (split ? 2 : 0));
 }
 
 // column exponents; flag bit 2 (MC B) as k_rowexp's at the scale 2^(p - e)
-// cth[j] = ca (sum_k |B'_kj| bound) as k_rowexp's rth (the 2^-40 covers the
-// round-to-nearest atomic adds of at most 2^10 slab sums)
+// cth[j] = ca (sum_k |B'_kj| bound) as k_rowexp's rth (the 2^-13 covers the
+// round-to-nearest binary32 atomic adds of at most 2^10 slab sums)
 __global__ void __launch_bounds__(256) k_colexp(const unsigned long long* __restrict__ cm, int64_t n, int p,
                                                  const int* __restrict__ cu, int* __restrict__ e,
-                                                 int* __restrict__ nf, const double* __restrict__ csum, int64_t k,
-                                                 double ca, double* __restrict__ cth) {
+                                                 int* __restrict__ nf, const float* __restrict__ csum, int64_t k,
+                                                 double ca, float* __restrict__ cth) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int ex = exp_above_d(__longlong_as_double((long long)cm[j]));
   e[j] = ex;
-  cth[j] = __dmul_ru(__fma_ru(__dmul_ru(csum[j], 1.0 + 0x1p-40), pow2d(p - ex), 0.5 * (double)k), ca);
+  cth[j] = __double2float_ru(__dmul_ru(__fma_ru(__dmul_ru((double)csum[j], 1.0 + 0x1p-13), pow2d(p - ex), 0.5 * (double)k), ca));
   if (cu && cu[j] + p - ex < 0) nf[j] |= 4;
+}
+
+// binary32 B, after the residues have counted each column's inexact elements:
+// a listed column (1 .. kMaxInx of them) gets 1.3 units per element (A's
+// rounding against the part added back, an underflowed scaled value) and a
+// negative sign, which tells k_crt8 to apply its list; a column with more
+// than the list holds gets an infinite threshold (all of it falls back)
+__global__ void __launch_bounds__(256) k_colfin(const int* __restrict__ cinx, int64_t n, float unit,
+                                                 float* __restrict__ cth) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int c = cinx[j];
+  if (c > kMaxInx) cth[j] = INFINITY;
+  else if (c > 0) cth[j] = -__fadd_ru(cth[j], __fmul_ru(unit, (float)c));
 }
 
 // Optional fused epilogue of an MC-MLP layer (mc_linear_op, autodiff.hpp:265-
@@ -672,21 +696,19 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
 // with a wide dynamic range (config 0's 2^U(-8,8) magnitudes, heavy tails)
 // have sums far below K maxima, and far fewer outputs fall back.
 struct Thresholds {
-  double base, inexact;   // base: the product of two roundings (K 1.1 units) + the CRT tail
-  const double* cth;
-  const double* rth;
+  float base, inexact;    // base: the product of two roundings (K 1.1 units) + the CRT tail
+  const float* cth;
+  const float* rth;
   int mcb;                // B is MC (both operands round every element)
-  double unit;            // one unit of C' (x 2^50)
+  // binary32, every operation rounded up; the caller compares with |Y| rounded down.
   // CORRECTED: the dropped parts of the inexact elements have been added back
-  // (k_crt8); what is left per element is A's rounding against it (<= 0.26) and
-  // an underflowed scaled value (far below a unit)
+  // (k_crt8); what is left per element -- A's rounding against it (<= 0.26) and an
+  // underflowed scaled value (far below a unit) -- is already in ca (k_colfin)
   template <bool CORRECTED = false>
-  __device__ __forceinline__ double at(int rowflags, int colflags, int inx, int64_t i, int64_t j) const {
-    const double ca = cth[j], rb = rth[i];
-    double t = base + ((rowflags & 4) ? 2.0 * ca : ca);
-    if (mcb) t += (colflags & 4) ? 2.0 * rb : rb;
-    else if (CORRECTED) t += unit * 1.3 * inx;
-    else t += fmin(inexact * inx, rb);
+  __device__ __forceinline__ float at(int rowflags, int colflags, int inx, float ca, float rb) const {
+    float t = __fadd_ru(base, (rowflags & 4) ? __fadd_ru(ca, ca) : ca);
+    if (mcb) t = __fadd_ru(t, (colflags & 4) ? __fadd_ru(rb, rb) : rb);
+    else if (!CORRECTED && inx) t = __fadd_ru(t, fminf(__fmul_ru(inexact, (float)inx), rb));
     return t;
   }
 };
@@ -766,7 +788,7 @@ __global__ void __launch_bounds__(256) k_crt(const int* __restrict__ cq, int64_t
       double y = (double)__fmaf_rn(-q, c_crt[NMOD].mh[0], T[u][0]);
 #pragma unroll
       for (int s = 1; s < kSlices; ++s) y = __fma_rn(y, 4096.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[s], T[u][s]));
-      if (((fi | cfj[u]) & 1) || !(fabs(y) >= th.at(fi, cfj[u], inx[u], i, j0 + u))) {
+      if (((fi | cfj[u]) & 1) || !(__double2float_rd(fabs(y)) >= th.at(fi, cfj[u], inx[u], fabsf(th.cth[j0 + u]), th.rth[i]))) {
         rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
         continue;
       }
@@ -799,8 +821,11 @@ static __device__ __noinline__ double inexact_corr(const float* __restrict__ aro
   return corr;
 }
 
+#ifndef MCF_CRT8_CTAS
+#define MCF_CRT8_CTAS 4
+#endif
 template <int NMOD>
-__global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, int64_t m, int64_t n, int64_t ldr,
+__global__ void __launch_bounds__(256, MCF_CRT8_CTAS) k_crt8(const int8_t* __restrict__ rq, int64_t m, int64_t n, int64_t ldr,
                                                  const int* __restrict__ ea, const int* __restrict__ eb,
                                                  const int* __restrict__ rnf, const int* __restrict__ cnf,
                                                  const int* __restrict__ cinx, Thresholds th, int sexp,
@@ -846,6 +871,7 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
     }
   }
   const int ei = ea[i], fi = rnf[i];
+  const float rthi = th.rth[i];
   float res[4][2];
   bool done[4];
 #pragma unroll
@@ -863,15 +889,17 @@ __global__ void __launch_bounds__(256, 4) k_crt8(const int8_t* __restrict__ rq, 
 #pragma unroll
     for (int sl = 1; sl < kSlices; ++sl) y = __fma_rn(y, 4096.0, (double)__fmaf_rn(-q, c_crt[NMOD].mh[sl], Tu[sl]));
     const int fc = cnf[j];
-    const int inx = cinx ? cinx[j] : 0;
-    if (inx > 0 && inx <= kMaxInx) {
-      // the column's listed inexact elements: add A[i, k] x (what B's rounding
-      // dropped) back, in units of Y (ycorr = 2^(pa + 96 - L); binary64 is
-      // ample: the terms are below 2^-45 of the bound's scale)
-      y = __fma_rn(inexact_corr(a + i * k * nca, nca, clk + j * kMaxInx, clr + j * kMaxInx, inx),
+    float tc = th.cth[j];
+    if (tc < 0.0f) {
+      // the column lists inexact elements (k_colfin marks it by the sign): add
+      // A[i, k] x (what B's rounding dropped) back, in units of Y (ycorr =
+      // 2^(pa + 96 - L); binary64 is ample: the terms are below 2^-45 of the
+      // bound's scale)
+      y = __fma_rn(inexact_corr(a + i * k * nca, nca, clk + j * kMaxInx, clr + j * kMaxInx, cinx[j]),
                    __dmul_rn(ycorr, pow2d(-ei)), y);
+      tc = -tc;
     }
-    if (((fi | fc) & 1) || inx > kMaxInx || !(fabs(y) >= th.template at<true>(fi, fc, inx, i, j))) {
+    if (((fi | fc) & 1) || !(__double2float_rd(fabs(y)) >= th.template at<true>(fi, fc, 0, tc, rthi))) {
       rlist[i * n + atomicAdd(rcnt + i, 1)] = (int)j;
       done[u] = true;  // the fallback writes it
       continue;
@@ -1305,7 +1333,7 @@ struct PreparedB {
   const int* eb = nullptr;
   const int* cnf = nullptr;
   const int* cinx = nullptr;  // per column: elements not exact in pb bits (binary32 B)
-  const double* cth = nullptr;  // per column: fallback-threshold term of A's rounding (Thresholds)
+  const float* cth = nullptr;   // per column: fallback-threshold term of A's rounding (Thresholds)
   const int* clk = nullptr;     // [n][kMaxInx] k of the listed inexact elements (binary32 B)
   const double* clr = nullptr;  // [n][kMaxInx] what their rounding dropped, in units of B'
   int64_t k = 0, kp = 0, n = 0, np = 0;  // np: n padded to 16 (int8 GEMM alignment)
@@ -1352,24 +1380,25 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   buf += al(n * k * ncb * 4);
   int* eb = reinterpret_cast<int*>(buf);
   buf += al(n * 4);
+  int* cu = reinterpret_cast<int*>(buf);
+  buf += al(n * 4);
+  // zero-initialised arrays, contiguous: one memset
+  char* z0 = buf;
   int* cnf = reinterpret_cast<int*>(buf);
   buf += al(n * 4);
   int* cinx = reinterpret_cast<int*>(buf);
   buf += al(n * 4);
   unsigned long long* cm = reinterpret_cast<unsigned long long*>(buf);
   buf += al(n * 8);
-  int* cu = reinterpret_cast<int*>(buf);
-  buf += al(n * 4);
-  double* csum = reinterpret_cast<double*>(buf);
+  float* csum = reinterpret_cast<float*>(buf);
   buf += al(n * 8);
-  double* cth = reinterpret_cast<double*>(buf);
+  float* cth = reinterpret_cast<float*>(buf);  // read four columns at a time: n * 8 bytes hold the padded n
   buf += al(n * 8);
+  const std::size_t zbytes = (std::size_t)(buf - z0);
   int* clk = reinterpret_cast<int*>(buf);
   buf += al(n * kMaxInx * 4);
   double* clr = reinterpret_cast<double*>(buf);
-  if (cudaMemsetAsync(cnf, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cm, 0, n * 8, s) != cudaSuccess ||
-      cudaMemsetAsync(csum, 0, n * 8, s) != cudaSuccess ||
-      cudaMemsetAsync(cinx, 0, n * 4, s) != cudaSuccess || cudaMemsetAsync(cu, 0x7f, n * 4, s) != cudaSuccess)
+  if (cudaMemsetAsync(z0, 0, zbytes, s) != cudaSuccess || cudaMemsetAsync(cu, 0x7f, n * 4, s) != cudaSuccess)
     return mcfr::fail(MCF_ERR_CUDA, "mm_fast: cannot clear the column maxima");
   const dim3 gm((unsigned)((n + 255) / 256), (unsigned)((k + 63) / 64));
   if (ncb == 2) k_colmax<2><<<gm, 256, 0, s>>>(w, k, n, ldb, cm, cnf, cu, csum);
@@ -1379,6 +1408,10 @@ mcf_status prepare_b(const float* w, int ncb, int64_t k, int64_t n, int64_t ldb,
   const dim3 gs((unsigned)((n + kSlab - 1) / kSlab), (unsigned)(kp / kSlab));
   OZ_NMOD_SWITCH(pl.n, if (ncb == 2) k_res_cols<2, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx, clk, clr);
                  else k_res_cols<1, NM><<<gs, 256, 0, s>>>(w, n, ldb, k, kp, np, pl.pb, eb, planes, bt, cinx, clk, clr));
+  if (ncb == 1) {
+    k_colfin<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cinx, n, std::nextafterf((float)(1.3 * threshold_unit(pl.n)), INFINITY), cth);
+    mcfr::note_launch();
+  }
   for (int i = 0; i < 3; ++i) mcfr::note_launch();
   pb = PreparedB{planes, bt, eb, cnf, ncb == 1 ? cinx : nullptr, cth, clk, clr, k, kp, n, np, ncb, pl};
   return mcfr::check_launch("mm_fast B residue kernels");
@@ -1397,7 +1430,7 @@ struct RowsWs {
   int* ea;
   int* rnf;
   int* rcnt;
-  double* rth;  // per row: fallback-threshold term of B's rounding (Thresholds)
+  float* rth;  // per row: fallback-threshold term of B's rounding (Thresholds)
 };
 RowsWs rows_ws(char* buf, int64_t m, int64_t kp, int64_t np, int nmod) {
   RowsWs w;
@@ -1413,7 +1446,7 @@ RowsWs rows_ws(char* buf, int64_t m, int64_t kp, int64_t np, int nmod) {
   buf += al(m * 4);
   w.rcnt = reinterpret_cast<int*>(buf);
   buf += al(m * 4);
-  w.rth = reinterpret_cast<double*>(buf);
+  w.rth = reinterpret_cast<float*>(buf);
   return w;
 }
 
@@ -1496,12 +1529,12 @@ mcf_status rows_products(const float* x, int nca, int64_t m, const PreparedB& pb
   const int L = host_crt().tab[pl.n].L;
   const double yu = threshold_unit(pl.n);
   Thresholds th;
-  th.base = (double)k * 1.1 * yu + 4096.0 * 1.0001 * std::ldexp(1.0, 50);
-  th.inexact = 0.51 * std::ldexp(1.0, pl.pa - 1) * yu;
+  const auto up = [](double v) { return std::nextafterf((float)v, INFINITY); };  // binary32, rounded up
+  th.base = up((double)k * 1.1 * yu + 4096.0 * 1.0001 * std::ldexp(1.0, 50));
+  th.inexact = up(0.51 * std::ldexp(1.0, pl.pa - 1) * yu);
   th.cth = pb.cth;
   th.rth = w.rth;
   th.mcb = pb.ncb == 2;
-  th.unit = yu;
   const int sexp = L - kYShift - pl.pa - pl.pb;
   const int64_t gcx = (n + 1023) / 1024;
   const dim3 gc((unsigned)gcx, (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, mcfr::sm_count() * 8 / gcx)));
