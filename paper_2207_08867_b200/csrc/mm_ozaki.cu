@@ -296,12 +296,15 @@ __device__ __forceinline__ float pow2f(int v) { return __int_as_float((127 + v) 
 // fraction (error <= 1/2); rem is what is left (nonzero: inexact), scaled the
 // input as scaled (zero with x nonzero: underflow, also inexact).  |t_j| <=
 // 2^11 for j < 5, |t_5| <= 2^12.
+// NL limbs hold |x 2^s| < 2^(12 NL - 1) (4 for a binary32 B's 48 bits; the
+// limbs above stay untouched and unused).
+template <int NL = 6>
 __device__ __forceinline__ void limbs2(float2 x, float sa, float sb, float2 (&l)[6], float2& rem, float2& xs) {
   float2 r = __fmul2_rn(__fmul2_rn(x, make_float2(sa, sa)), make_float2(sb, sb));
   xs = r;
   const float2 mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
 #pragma unroll
-  for (int j = 5; j >= 0; --j) {
+  for (int j = NL - 1; j >= 0; --j) {
     const float dn = pow2f(-12 * j), up = -pow2f(12 * j);
     const float2 t = __fadd2_rn(__ffma2_rn(r, make_float2(dn, dn), mg), nmg);
     r = __ffma2_rn(t, make_float2(up, up), r);
@@ -312,17 +315,17 @@ __device__ __forceinline__ void limbs2(float2 x, float sa, float sb, float2 (&l)
 
 // the limbs of X = round(c0 2^s) + round(c1 2^s) (each rounding <= 1/2; c1 = 0
 // for NC = 1) for two elements; returns the number of inexact elements
-template <int NC>
+template <int NC, int NL = 6>
 __device__ __forceinline__ int limbs_pair(const float (&c0)[2], const float (&c1)[2], float sa, float sb,
                                           float2 (&l)[6]) {
   float2 rem, xs;
-  limbs2(make_float2(c0[0], c0[1]), sa, sb, l, rem, xs);
+  limbs2<NL>(make_float2(c0[0], c0[1]), sa, sb, l, rem, xs);
   int inexact = (rem.x != 0.0f || (xs.x == 0.0f && c0[0] != 0.0f)) + (rem.y != 0.0f || (xs.y == 0.0f && c0[1] != 0.0f));
   if constexpr (NC == 2) {
     float2 l1[6], rem1, xs1;
-    limbs2(make_float2(c1[0], c1[1]), sa, sb, l1, rem1, xs1);
+    limbs2<NL>(make_float2(c1[0], c1[1]), sa, sb, l1, rem1, xs1);
 #pragma unroll
-    for (int j = 0; j < 6; ++j) l[j] = __fadd2_rn(l[j], l1[j]);  // |sum| <= 2^12 (2^13 for j = 5): exact
+    for (int j = 0; j < NL; ++j) l[j] = __fadd2_rn(l[j], l1[j]);  // |sum| <= 2^12 (2^13 for j = 5): exact
     inexact += (rem1.x != 0.0f || (xs1.x == 0.0f && c1[0] != 0.0f)) + (rem1.y != 0.0f || (xs1.y == 0.0f && c1[1] != 0.0f));
   }
   return inexact;
@@ -355,12 +358,12 @@ __device__ __forceinline__ unsigned res_bits(const float (&l)[6]) {
 // res_bits for two elements at once: packed FFMA2 / FADD2 with the weights
 // as scalar (broadcast) operands, the same roundings per lane -- half the
 // issue slots of the scalar form (the residue kernels are issue-bound)
-template <int T>
+template <int T, int NL = 6>
 __device__ __forceinline__ float2 res_bits2(const float2 (&l)[6]) {
   const float2 mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
   float2 s = __ffma2_rn(l[0], make_float2(c_pw[T][0], c_pw[T][0]), mg);
 #pragma unroll
-  for (int j = 1; j < 6; ++j) s = __ffma2_rn(l[j], make_float2(c_pw[T][j], c_pw[T][j]), s);
+  for (int j = 1; j < NL; ++j) s = __ffma2_rn(l[j], make_float2(c_pw[T][j], c_pw[T][j]), s);
   const float2 q = __fadd2_rn(__ffma2_rn(__fadd2_rn(s, nmg), make_float2(c_inv[T], c_inv[T]), mg), nmg);
   return __ffma2_rn(q, make_float2(-c_mod[T], -c_mod[T]), s);
 }
@@ -370,17 +373,17 @@ __device__ __forceinline__ unsigned pack4(unsigned w0, unsigned w1, unsigned w2,
   return __byte_perm(__byte_perm(w0, w1, 0x0040), __byte_perm(w2, w3, 0x0040), 0x5410);
 }
 
-template <int NMOD, int T = 0>
+template <int NMOD, int T = 0, int NL = 6>
 __device__ __forceinline__ void residue_words(const float2 (&l01)[6], const float2 (&l23)[6], const int (&l0i)[4],
                                               unsigned (&wd)[NMOD]) {
   if constexpr (T < NMOD) {
     if constexpr (T == 0) {  // m = 256: X mod 256 is the lowest limb's low byte
       wd[0] = pack4((unsigned)l0i[0], (unsigned)l0i[1], (unsigned)l0i[2], (unsigned)l0i[3]);
     } else {
-      const float2 a = res_bits2<T>(l01), b = res_bits2<T>(l23);
+      const float2 a = res_bits2<T, NL>(l01), b = res_bits2<T, NL>(l23);
       wd[T] = pack4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(b.x), __float_as_uint(b.y));
     }
-    residue_words<NMOD, T + 1>(l01, l23, l0i, wd);
+    residue_words<NMOD, T + 1, NL>(l01, l23, l0i, wd);
   }
 }
 
@@ -491,12 +494,14 @@ __global__ void __launch_bounds__(256, 4) k_res_cols(const float* __restrict__ b
 #pragma unroll
       for (int q = 0; q < NC; ++q) c[q][u] = 0.0f;
   }
+  // a binary32 B keeps pb = 48 bits (crt_plan): four 12-bit limbs; an MC B up to 73: six
+  constexpr int NL = NC == 1 ? 4 : 6;
   float2 l01[6], l23[6];
   int inexact;
   {
     const float a0[2] = {c[0][0], c[0][1]}, a1[2] = {c[NC - 1][0], c[NC - 1][1]};
     const float b0[2] = {c[0][2], c[0][3]}, b1[2] = {c[NC - 1][2], c[NC - 1][3]};
-    inexact = limbs_pair<NC>(a0, a1, sa, sb, l01) + limbs_pair<NC>(b0, b1, sa, sb, l23);
+    inexact = limbs_pair<NC, NL>(a0, a1, sa, sb, l01) + limbs_pair<NC, NL>(b0, b1, sa, sb, l23);
   }
   const int l0i[4] = {limb_int(l01[0].x), limb_int(l01[0].y), limb_int(l23[0].x), limb_int(l23[0].y)};
   if (inexact && j < n) {
@@ -508,7 +513,7 @@ __global__ void __launch_bounds__(256, 4) k_res_cols(const float* __restrict__ b
     }
   }
   unsigned wd[NMOD];
-  residue_words<NMOD>(l01, l23, l0i, wd);
+  residue_words<NMOD, 0, NL>(l01, l23, l0i, wd);
 #pragma unroll
   for (int t = 0; t < NMOD; ++t) dg[t][tx][ty] = wd[t];
   __syncthreads();
