@@ -25,17 +25,23 @@
 //     whose partial sums are exact while they matter (|C'| <= M/4);
 //   * C = C' 2^(ea+eb-pa-pb), split greedily into the binary32 components.
 //
-// Error per output (scaled units) <= K 2^-(pa+1) (+ the counted inexact B
-// elements): 2^-62 at config 2, ~30x tighter than the nine-digit splitting
-// this replaces, with 17 int8 GEMMs instead of 39 GEMM-equivalents.  Outputs
-// whose magnitude is not at least 2^50 times their bound (cancellation) and
-// rows / columns holding Inf or NaN are listed per row and recomputed by the
+// Error per output: A's rounding against the column's sum of |B'| and (MC B) B's
+// against the row's sum of |A'| -- the operands' own magnitude sums, taken in
+// the exponent pre-passes -- at most K 2^-(pa+1) scaled: 2^-62 at config 2, ~30x
+// tighter than the nine-digit splitting this replaced, with 17 int8 GEMMs
+// instead of 39 GEMM-equivalents.  Binary32 B elements that do not fit the
+// column's 48-bit fixed point are listed per column and the part their
+// rounding dropped is added back in the reconstruction.  Outputs whose
+// magnitude is not at least 2^50 times their bound (cancellation) and rows /
+// columns holding Inf or NaN are listed per row and recomputed by the
 // fallback kernel in double-double from the binary32 operands, so every
 // output has relative error <= 2^-50 before the final split -- the resolution
 // of the reference's own nc=2 result (its measured max is 2^-49.1).
 //
-// The int8 GEMMs are plain library GEMMs (cuBLASLt IMMA, TN, s8 x s8 -> s32,
-// one strided-batched call over the moduli); the scaling, residue extraction,
+// The int8 GEMMs run on the hand-written tcgen05 kernel of tc_gemm.cu (one
+// launch over the moduli, int8 residues out of the epilogue); a strided-batched
+// cuBLASLt IMMA GEMM (int32 sums, reduced here) is kept behind
+// MCF_OZ_GEMM=cublaslt for A/B measurement.  The scaling, residue extraction,
 // transposes, CRT reconstruction + split and the cancellation fallback are
 // this file's kernels.
 #include <cublasLt.h>
@@ -571,7 +577,8 @@ __global__ void __launch_bounds__(256) k_rowexp(const float* __restrict__ a, int
   float sum = 0.0f;  // binary32, every add rounded up (the FMA pipe is idle here): an upper bound
   bool bad = false, split = false;
   int umin = 1 << 20;
-  for (int64_t t = lane; t < k; t += 32) {
+#pragma unroll 8
+  for (int64_t t = lane; t < k; t += 32) {  // unrolled: eight loads in flight per lane (the pass is HBM-bound)
     double hi, lo, mag;
     load_pair<NC>(a + (r * k + t) * NC, hi, lo, mag);
     bad |= !isfinite(mag);
@@ -612,6 +619,7 @@ __global__ void __launch_bounds__(256) k_colmax(const float* __restrict__ b, int
   float sum = 0.0f;  // as k_rowexp's
   bool bad = false, split = false;
   int umin = 1 << 20;
+#pragma unroll 8
   for (int64_t t = t0; t < t1; ++t) {
     double hi, lo, mag;
     load_pair<NC>(b + (t * ldb + j) * NC, hi, lo, mag);
@@ -688,16 +696,15 @@ __device__ __forceinline__ void emit(const double (&v)[2], int64_t i, int64_t j,
 }
 
 // fallback thresholds in units of Y = C' / 2^(L-96): 2^50 x the per-output
-// error bound.  base: A's rounding (1/2 unit per element) times |B'| plus
-// B's for an MC B; xa / xb: the extra 1/2 unit per element of a row / MC
-// column whose leading components are not integers at the scale (flag bit 2);
-// inexact: per counted inexact element of a binary32 B column
-//
-// The roundings are bounded with the operands' own magnitude sums, not K times
-// the largest element: A's rounding of row i against column j costs at most
-// 0.51 sum_k |B'_kj| (cth[j], from the column sums of k_colmax), B's at most
-// 0.51 sum_k |A'_ik| (rth[i], k_rowexp) -- for a binary32 B only its counted
-// inexact elements, so the smaller of inexact * count and rth[i].  Operands
+// error bound.  The roundings are bounded with the operands' own magnitude
+// sums, not K times the largest element: A's rounding of row i against column
+// j costs at most 0.51 sum_k |B'_kj| (cth[j], from the column sums of
+// k_colmax), B's at most 0.51 sum_k |A'_ik| (rth[i], k_rowexp); each doubles
+// for a row / MC column whose leading components are not integers at the
+// scale (flag bit 2: both components round).  A binary32 B rounds only its
+// counted inexact elements: k_crt8 adds their dropped parts back (CORRECTED;
+// the 1.3 units left per element are already in cth, k_colfin), the int32-plane
+// kernel k_crt charges the smaller of inexact * count and rth[i].  Operands
 // with a wide dynamic range (config 0's 2^U(-8,8) magnitudes, heavy tails)
 // have sums far below K maxima, and far fewer outputs fall back.
 struct Thresholds {
