@@ -74,3 +74,47 @@ def test_g2_ops_bitwise_on_margins(gr, port, seed):
     assert_bits(gr.run("div_mcn", xy, y), port.div_mcn(xy, y), "div_mcn exact quotients")
     one = np.ones(y.shape[0], np.float32)
     assert_bits(gr.run("div_n", one, y), port.div_n(one, y), "div_n reciprocals")
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_one_digit_division_core_near_exact_quotients(gr, port, seed):
+    """The wide tier's one-digit core (mcf_w2.cuh div_core1) replaces the second
+    and third quotient digits by the remainder's quotient R and certifies the
+    second component against an absolute margin of |R| 2^-42.  Inputs built to
+    stress exactly that: x = q y (1 + eps) with q of at most 24 or 48 bits and eps
+    from 2^-26 down to 2^-80 and zero (R tiny or zero against q0; the second
+    component many binades below it), quotients whose first digit is corrected by
+    R (x1 and y1 of opposite effect, |R| about half a step of q0), and divisors
+    of Mul-MCN whose reciprocal is nearly a power of two.  Bit-identical to the
+    oracle whichever tier ends up taking the element."""
+    rng = np.random.default_rng(7700 + seed)
+    n = 1 << 16
+    y64 = config_values(rng, n, -6, 6)
+    y64 += np.sign(y64) * 0.5
+    y = split(y64, 2, np.float32)
+    yv = y[:, 0].astype(np.float64) + y[:, 1].astype(np.float64)
+    bits = rng.choice([6, 12, 24, 30, 48], n)
+    q = np.ldexp(rng.integers(1, 1 << 52, n).astype(np.float64), -52) + 1.0
+    q = np.ldexp(np.floor(np.ldexp(q, bits - 1)), -(bits - 1)) * rng.choice([-1.0, 1.0], n)
+    eps = np.where(rng.uniform(0, 1, n) < 0.2, 0.0, rng.choice([-1.0, 1.0], n) * np.exp2(-rng.uniform(26, 80, n)))
+    xl = q.astype(np.longdouble) * yv.astype(np.longdouble) * (1 + eps.astype(np.longdouble))
+    x0 = xl.astype(np.float32)
+    x1 = (xl - x0.astype(np.longdouble)).astype(np.float32)
+    x = np.stack([x0, x1], -1)
+    keep = np.isfinite(x).all(-1) & (x0.astype(np.float32) + x1 == x0)
+    x, y = x[keep], y[keep]
+    assert x.shape[0] > n // 2
+    assert_bits(gr.run("div_mcn", x, y), port.div_mcn(x, y), "div_mcn near-exact")
+    v = x[:, 0].copy()
+    assert_bits(gr.run("div_n", v, y), port.div_n(v, y), "div_n near-exact")
+    # first digit corrected by the remainder: y1 at its largest, x1 of the sign that moves the quotient across a step
+    y2 = y.copy()
+    y2[:, 1] = (np.spacing(np.abs(y2[:, 0])) * rng.choice([-0.5, 0.5, -0.49, 0.49], y2.shape[0])).astype(np.float32)
+    y2 = y2[(y2[:, 0] + y2[:, 1]) == y2[:, 0]]
+    x2 = x[: y2.shape[0]]
+    assert_bits(gr.run("div_mcn", x2, y2), port.div_mcn(x2, y2), "div_mcn half-ulp y1")
+    # Mul-MCN: divisors whose reciprocal sits next to a power of two
+    p2 = np.exp2(rng.integers(-6, 7, x.shape[0]).astype(np.float64)) * rng.choice([-1.0, 1.0], x.shape[0])
+    yn = split(p2 * (1 + rng.choice([-1.0, 1.0], x.shape[0]) * np.exp2(-rng.uniform(20, 60, x.shape[0]))), 2, np.float32)
+    assert_bits(gr.run("mul_mcn", x, yn), port.mul_mcn(x, yn), "mul_mcn reciprocal near a power of two")
+    assert_bits(gr.run("mul_mcn", x, y), port.mul_mcn(x, y), "mul_mcn near-exact operands")
