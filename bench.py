@@ -255,7 +255,7 @@ def cpu_baselines_other(a2, b2):
     xe = ref_split(np.clip(u(1003, n0), -10.0, 10.0), 2, np.float32)
     ops = {"grow_expn": (dict(x=x, v=v), 20), "scaling_n": (dict(x=x, v=v), 20), "div_n": (dict(y=yd, v=v), 20),
            "add_mcn": (dict(x=x, y=y), 24), "mul_mcn": (dict(x=x, y=yd), 24), "div_mcn": (dict(x=x, y=yd), 24),
-           "exp_mcn": (dict(x=xe), 16), "square_mcn": (dict(x=x), 16)}
+           "exp_mcn": (dict(x=xe), 16), "square_mcn": (dict(x=x), 16), "mul_mcn_slow": (dict(x=x, y=y), 24)}
     c0 = {}
     for op, (kw, bpe) in ops.items():
         t, _ = ref.time_elementwise(op, threads=thr, **kw)
@@ -346,6 +346,7 @@ def elementwise_suite(torch, mcf, hbm_gbs, rank=0, world=1):
         "div_n": (lambda: mcf.div_n(v, yd), 20), "add_mcn": (lambda: mcf.add_mcn(x, y), 24),
         "mul_mcn": (lambda: mcf.mul_mcn(x, yd), 24), "div_mcn": (lambda: mcf.div_mcn(x, yd), 24),
         "exp_mcn": (lambda: mcf.exp_mcn(xe), 16), "square_mcn": (lambda: mcf.square_mcn(x), 16),
+        "mul_mcn_slow": (lambda: mcf.mul_mcn_slow(x, y), 24),
     }
     res = {}
     for name, (f, bpe) in ops.items():

@@ -95,18 +95,21 @@ struct OpTraits {
 // it declines runs the register path below, then the literal one
 template <int OP, class P, int NC, int ONC>
 constexpr bool kG2 = std::is_same<P, PB32>::value && NC == 2 && ONC == 2 &&
-                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kExp || OP == kAdd ||
-                      OP == kGrow);
+                     (OP == kScale || OP == kSquare || OP == kDiv || OP == kDivN || OP == kMul || OP == kMulSlow ||
+                      OP == kExp || OP == kAdd || OP == kGrow);
 
 // the ops whose certified shortcut runs two elements at once (FADD2 / FMUL2 /
 // FFMA2); exp keeps a per-element binary64 exp and runs one at a time
 // (measured on B200, 2^24 config-0 elements: Mul-MCN's chained divisions
 // need 79 registers packed, one ring per SM, 294 us against 275 us scalar at
 // two rings, so it stays scalar)
-// the division-based ones first try the wide tier (mcf_w2.cuh: the long
-// division carried in binary64, one element at a time)
+// the division-based ones and the direct product first try the wide tier
+// (mcf_w2.cuh: binary64 carries every exact intermediate, one element at a
+// time).  Square-MCN stays on the packed binary32 shortcut: its wide form
+// (w2::square) measured the same 54 us -- the operator is bound by its 8 B in /
+// 8 B out stream, not by instructions
 template <int OP, class P, int NC, int ONC>
-constexpr bool kW2 = kG2<OP, P, NC, ONC> && (OP == kDiv || OP == kDivN || OP == kMul);
+constexpr bool kW2 = kG2<OP, P, NC, ONC> && (OP == kDiv || OP == kDivN || OP == kMul || OP == kMulSlow);
 
 template <int OP, class P, int NC, int ONC>
 constexpr bool kG2Pair = kG2<OP, P, NC, ONC> && OP != kExp && !kW2<OP, P, NC, ONC>;
@@ -133,7 +136,7 @@ __device__ __forceinline__ g2::M2 run_g2_pair(const float (&x)[4], const float (
   return ok;
 }
 
-// the wide tier alone (binary32 nc = 2 Div-MCN / DivN / Mul-MCN), branch-free:
+// the wide tier alone (binary32 nc = 2 Div-MCN / DivN / Mul-MCN fast and slow), branch-free:
 // the TMA kernel runs it for all of a thread's elements before it looks at any
 // verdict, so their independent chains interleave
 template <int OP>
@@ -145,6 +148,7 @@ __device__ __forceinline__ bool run_w2(const float (&x)[2], const float (&y)[2],
   } else {
     const bool cx = __fadd_rn(x[0], x[1]) == x[0], cy = __fadd_rn(y[0], y[1]) == y[0];
     if constexpr (OP == kDiv) ok = w2::div<V, false, true>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
+    else if constexpr (OP == kMulSlow) ok = w2::mul_slow<V>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
     else {
       ok = w2::mul<V, true>(x[0], x[1], y[0], y[1], cx, cy, o[0], o[1]);
       if (__fadd_rn(y[1], y[0]) == 0.0f || __fadd_rn(x[1], x[0]) == 0.0f) o[0] = o[1] = 0.0f, ok = true;
@@ -169,6 +173,7 @@ __device__ __forceinline__ bool run_fast(const RT<P> (&x)[NC], const RT<P> (&y)[
     else if constexpr (OP == kMul) ok = g2::mul<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kAdd) ok = g2::add<Q>(x[0], x[1], y[0], y[1], o[0], o[1]);
     else if constexpr (OP == kGrow) ok = g2::grow<Q>(x[0], x[1], v, o[0], o[1]);
+    else if constexpr (OP == kMulSlow) ok = false;  // no binary32 shortcut: the register path is next
     else ok = w2::exp_b32(x[0], x[1], o[0], o[1]);
     if (__builtin_expect(ok, 1)) return true;
   }

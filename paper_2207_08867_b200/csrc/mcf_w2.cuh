@@ -49,7 +49,7 @@
 // P-bit values), add/sub/mul/fma/neg/abs on W, rcp_seed(W) (any approximation
 // of 1/y good to ~2^-16), rnpm(W, m, ok) (rnp, and ok &= L - mid outside [-m, 3 m)),
 // rnpv(W, ref, lg, ok) (rnp with the absolute margin |ref| 2^(lg - (W-1))), span2p(W) (fits 2 P bits), eq/ge/le on W, c(double), two(k) = 2^k,
-// rnpe (nearest-even), in_window / below_window on N, kP.
+// rnpe (nearest-even), in_window / below_window / lead_window / tail_window on N, kP.
 #pragma once
 
 #include "mcf_g2.cuh"
@@ -275,6 +275,45 @@ G2_HD bool scale(N_<V> x0, N_<V> x1, N_<V> v, bool cx, N_<V>& o0, N_<V>& o1) {
   return ok;
 }
 
+// mc_ops.hpp:234-251 mul_slow_kernel, nc = 2 (Mul-MCN, the direct product): the
+// seven terms two_prod(x0, y0), two_prod(x0, y1), two_prod(x1, y0) and the guard
+// product fl(x1 y1) sum EXACTLY to S = X Y - x1 y1 + fl(x1 y1), and the result is
+// the first two components of S's compressed expansion (renorm_kernel; (M)).
+// Wide: X Y = ph + pl exactly (one multiply, one fma); x1 y1 is exact in the wide
+// format (P x P bits), so c = rnpe(x1 y1) - x1 y1 is; pl + c rounds far below a
+// unit of what is tested (|pl + c| <= 2^-(W-1) |ph| (1 + 2^-(P-4))), and t = (ph -
+// o0) + (pl + c) is known to half a unit: 65 units of margin, as digit<PAIR>.
+// Guards (cx / cy: compressed operands, by the caller): X and Y single wide
+// values; every product with an exact low part and the guard product normal --
+// leads inside 2^[-30, 40], second components zero or at least 2^-60.
+template <class V>
+G2_HD bool mul_slow(N_<V> x0, N_<V> x1, N_<V> y0, N_<V> y1, bool cx, bool cy, N_<V>& o0, N_<V>& o1) {
+  using W = W_<V>;
+  const W X0 = V::wide(x0), X1 = V::wide(x1), Y0 = V::wide(y0), Y1 = V::wide(y1);
+  const W X = V::add(X0, X1), Y = V::add(Y0, Y1);
+  bool ok = cx & cy & V::eq(V::sub(X, X0), X1) & V::eq(V::sub(Y, Y0), Y1);
+  ok &= V::lead_window(x0) & V::lead_window(y0) & V::tail_window(x1) & V::tail_window(y1);
+  const W ph = V::mul(X, Y);
+  const W pl = V::fma(X, Y, V::neg(ph));
+  const W g = V::mul(X1, Y1);                       // exact
+  const W pc = V::add(pl, V::sub(V::rnpe(g), g));   // pl + (fl(x1 y1) - x1 y1)
+  const W w0 = V::rnpm(ph, 64, ok);
+  const W t = V::add(V::sub(ph, w0), pc);
+  const W w1 = V::rnpm(t, 64, ok);
+  o0 = V::canon(V::narrow(w0));
+  o1 = V::canon(V::narrow(w1));
+  return ok;
+}
+
+// mc_ops.hpp:256-282 square_kernel, nc = 2: two_prod(x0, x0), the doubled
+// two_prod(x0, x1) and fl(x1 x1) sum exactly to S = X^2 - x1^2 + fl(x1^2) -- the
+// direct product with y = x (five terms instead of seven; the same value, so
+// the same first two components)
+template <class V>
+G2_HD bool square(N_<V> x0, N_<V> x1, bool cx, N_<V>& o0, N_<V>& o1) {
+  return mul_slow<V>(x0, x1, x0, x1, cx, cx, o0, o1);
+}
+
 #if defined(__CUDACC__)
 // binary32 components in binary64 on sm_100a
 struct VD {
@@ -305,6 +344,8 @@ struct VD {
   __device__ __forceinline__ static int lg1() { return 10; }  // div_core1's margin: 2^10 units of R's last place
   __device__ __forceinline__ static bool in_window(N a) { return (fabsf(a) >= 0x1p-40f) & (fabsf(a) <= 0x1p40f); }
   __device__ __forceinline__ static bool below_window(N a) { return fabsf(a) <= 0x1p40f; }
+  __device__ __forceinline__ static bool lead_window(N a) { return (fabsf(a) >= 0x1p-30f) & (fabsf(a) <= 0x1p40f); }
+  __device__ __forceinline__ static bool tail_window(N a) { return (a == 0.0f) | (fabsf(a) >= 0x1p-60f); }
   // round to 24 bits on the bit pattern (sign-magnitude: add half a step to
   // the magnitude, clear the 29 low bits; a carry runs into the exponent as
   // it should).  rnp: ties away from zero (every use declines near-ties);

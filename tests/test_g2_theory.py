@@ -1,7 +1,7 @@
 """CPU check of the certified binary32 nc=2 tiers (csrc/mcf_g2.cuh, and the wide
 long-division tier csrc/mcf_w2.cuh: rows w2div / w2mul for the three-digit
-core, w1div / w1mul for the one-digit core the kernels use, emulated with a
-wide format of 2 p + 5 bits).
+core, w1div / w1mul for the one-digit core the kernels use, w2mslow / w2msq for
+the direct product and its square, emulated with a wide format of 2 p + 5 bits).
 
 tools/g2_verify.cpp runs the SAME header on an emulated binary format with p
 significand bits and compares it with the reference's algorithms restated in
@@ -34,7 +34,7 @@ def g2v(tmp_path_factory):
     return exe
 
 
-ROWS = {"scale", "square", "div", "mul", "add", "grow", "w2div", "w2mul", "w2scale", "w1div", "w1mul"}
+ROWS = {"scale", "square", "div", "mul", "add", "grow", "w2div", "w2mul", "w2scale", "w1div", "w1mul", "w2mslow", "w2msq"}
 # the one-digit core's margin (2^10 units of the remainder quotient's last
 # place) is wider than the whole rounding interval of the emulated format
 # below p = 6: it accepts nothing there and is checked at p = 6 instead

@@ -110,6 +110,8 @@ struct VE {
   static constexpr KP kP{};
   static bool in_window(N a) { return std::fabs(a) >= std::ldexp(1.0, -40) && std::fabs(a) <= std::ldexp(1.0, 40); }
   static bool below_window(N a) { return std::fabs(a) <= std::ldexp(1.0, 40); }
+  static bool lead_window(N a) { return std::fabs(a) >= std::ldexp(1.0, -30) && std::fabs(a) <= std::ldexp(1.0, 40); }
+  static bool tail_window(N a) { return a == 0.0 || std::fabs(a) >= std::ldexp(1.0, -60); }
   static W rnpe(W t) { return rn(t); }
   static W rnp(W t) {  // ties away from zero, as the device's pattern rounding
     if (t == 0 || !std::isfinite(t)) return t;
@@ -255,6 +257,18 @@ static void ref_mul(const double* x, const double* y, double* out) {  // :216-23
   ref_div(one, y, rec);
   ref_div(x, rec, out);
 }
+static void ref_mul_slow(const double* x, const double* y, double* out) {  // :234-251, nc = 2
+  double h[8];
+  int m = 0;
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; i + j < 2; ++j) {
+      const TS t = two_prod(x[i], y[j]);
+      h[m++] = t.s;
+      h[m++] = t.e;
+    }
+  h[m++] = rn(x[1] * y[1]);
+  renorm(h, m, out, 2);
+}
 static void ref_square(const double* x, double* out) {  // :256-282
   double h[8];
   int m = 0;
@@ -277,7 +291,7 @@ static bool same(double a, double b) { return std::memcmp(&a, &b, 8) == 0; }
 
 template <class F, class G>
 static void check(Stat& st, F ref, G fast, const char* what) {
-  if (g_only1 && st.name[1] != '1') return;
+  if (g_only1 && st.name[1] != '1' && st.name[2] != 'm') return;
   double ro[2], fo[2];
   g_cap = false;
   ref(ro);
@@ -340,12 +354,14 @@ int main(int argc, char** argv) {
     auto X = pairs(K, 1);
     const int M = 1 << (P - 1);
     printf("p=%d: %zu compressed pairs\n", P, X.size());
-    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"}, od{"w1div"}, om{"w1mul"};
+    Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"}, od{"w1div"}, om{"w1mul"}, wl{"w2mslow"}, wq{"w2msq"};
 #pragma omp parallel for schedule(dynamic, 16)
     for (long long i = 0; i < (long long)X.size(); ++i) {
       const double x[2] = {X[i].first, X[i].second};
       check(sq, [&](double* o) { ref_square(x, o); },
             [&](double* o) { return g2::square<QE>(x[0], x[1], o[0], o[1]); }, "sq");
+      check(wq, [&](double* o) { ref_square(x, o); },
+            [&](double* o) { return w2::square<VE>(x[0], x[1], true, o[0], o[1]); }, "sq");
       for (int a = 0; a < M; ++a) {  // div_n: a single-component numerator over x as divisor
         const double vn[2] = {std::ldexp(M + a, -(P - 1)), 0.0};
         check(sd, [&](double* o) { ref_div(vn, x, o); },
@@ -376,6 +392,8 @@ int main(int argc, char** argv) {
               [&](double* o) { return w2::div<VE, false>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
         check(od, [&](double* o) { ref_div(x, y, o); },
               [&](double* o) { return w2::div<VE, false, true>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "div");
+        check(wl, [&](double* o) { ref_mul_slow(x, y, o); },
+              [&](double* o) { return w2::mul_slow<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mslow");
         for (int sh = -3; sh <= 3; sh += 3) {  // relative exponent of y
           const double ys[2] = {std::ldexp(y[0], sh), std::ldexp(y[1], sh)};
           check(sa, [&](double* o) { ref_add(x, ys, o); },
@@ -391,14 +409,14 @@ int main(int argc, char** argv) {
         }
       }
     }
-    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws), report(od), report(om);
-    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | od.bad | om.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+    report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws), report(od), report(om), report(wl), report(wq);
+    return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | od.bad | om.bad | wl.bad | wq.bad | ss.cap | sq.cap | sd.cap | sm.cap |
             sa.cap | sg.cap) ? 1 : 0;
   }
   // sampled, config-0 style operands: v = U(-1,1) 2^U(-8,8) split greedily into p-bit comps
   P = argc > 2 ? atoi(argv[2]) : 24;
   const long long N = argc > 3 ? atoll(argv[3]) : 2000000;
-  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"}, od{"w1div"}, om{"w1mul"};
+  Stat ss{"scale"}, sq{"square"}, sd{"div"}, sm{"mul"}, sa{"add"}, sg{"grow"}, wd{"w2div"}, wm{"w2mul"}, ws{"w2scale"}, od{"w1div"}, om{"w1mul"}, wl{"w2mslow"}, wq{"w2msq"};
 #pragma omp parallel
   {
     std::mt19937_64 g(1234 + 7919 * (unsigned long long)omp_get_thread_num());
@@ -420,6 +438,8 @@ int main(int argc, char** argv) {
             [&](double* o) { return w2::scale<VE>(x[0], x[1], v, true, o[0], o[1]); }, "sc");
       check(sq, [&](double* o) { ref_square(x, o); },
             [&](double* o) { return g2::square<QE>(x[0], x[1], o[0], o[1]); }, "sq");
+      check(wq, [&](double* o) { ref_square(x, o); },
+            [&](double* o) { return w2::square<VE>(x[0], x[1], true, o[0], o[1]); }, "sq");
       check(sd, [&](double* o) { ref_div(x, y, o); },
             [&](double* o) { return g2::div<QE>(x[0], x[1], y[0], y[1], o[0], o[1]); }, "div");
       const double vv[2] = {v2[0], 0.0};
@@ -435,6 +455,8 @@ int main(int argc, char** argv) {
             [&](double* o) { return w2::div<VE, true>(vv[0], vv[1], y[0], y[1], true, true, o[0], o[1]); }, "divn");
       check(od, [&](double* o) { ref_div(vv, y, o); },
             [&](double* o) { return w2::div<VE, true, true>(vv[0], vv[1], y[0], y[1], true, true, o[0], o[1]); }, "divn");
+      check(wl, [&](double* o) { ref_mul_slow(x, y, o); },
+            [&](double* o) { return w2::mul_slow<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mslow");
       check(wm, [&](double* o) { ref_mul(x, y, o); },
             [&](double* o) { return w2::mul<VE>(x[0], x[1], y[0], y[1], true, true, o[0], o[1]); }, "mul");
       check(om, [&](double* o) { ref_mul(x, y, o); },
@@ -448,7 +470,7 @@ int main(int argc, char** argv) {
             [&](double* o) { return g2::add<QE>(x[0], x[1], yn[0], yn[1], o[0], o[1]); }, "add");
     }
   }
-  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws), report(od), report(om);
-  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | od.bad | om.bad | ss.cap | sq.cap | sd.cap | sm.cap |
+  report(ss), report(sq), report(sd), report(sm), report(sa), report(sg), report(wd), report(wm), report(ws), report(od), report(om), report(wl), report(wq);
+  return (ss.bad | sq.bad | sd.bad | sm.bad | sa.bad | sg.bad | wd.bad | wm.bad | ws.bad | od.bad | om.bad | wl.bad | wq.bad | ss.cap | sq.cap | sd.cap | sm.cap |
           sa.cap | sg.cap) ? 1 : 0;
 }
